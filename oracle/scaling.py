@@ -17,7 +17,7 @@ k = 0..n_l-1 in that order. Fill is discovered as the elimination proceeds:
 the blocks present in row k when k is eliminated are exactly struct(k).
 
 D_k^{-1}: LU with partial pivoting (LAPACK getrf) followed by inversion
-(R5). Singular if a pivot |u_ii| < 1e-14 ||Z~_kk||_F (R5).
+(R5). Singular if a pivot |u_ii| <= 1e-14 ||Z~_kk||_F (R5).
 """
 from __future__ import annotations
 
@@ -60,7 +60,7 @@ def inverse_lu(A: np.ndarray, pos: int = -1, leaf: int = -1) -> np.ndarray:
     """Explicit inverse via LU with partial pivoting (getrf) + solve with I."""
     lu, piv = sla.lu_factor(A, check_finite=True)
     fro = np.linalg.norm(A)
-    if np.min(np.abs(np.diag(lu))) < 1e-14 * fro:
+    if not np.min(np.abs(np.diag(lu))) > 1e-14 * fro:
         raise SingularBlock(pos, leaf)
     return sla.lu_solve((lu, piv), np.eye(A.shape[0], dtype=A.dtype))
 
