@@ -1,0 +1,313 @@
+#!/usr/bin/env python
+"""bench.py — ps_solve throughput (N*nrhs/s, complex128) of libps on B200.
+
+One "step" = one ps_solve of the configured right-hand-side block: the whole
+two-term hot path of SURVEY.md §8(a) rows a4-a8 (forward sweep R^T + D^-1,
+backward sweep R, far field Z_F, forward sweep + D^-1, combine + norms,
+backward sweep), device-resident B and X. The O(N) setup (rows a1-a3) is run
+once before the timed region and reported separately as `setup_ms`.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+Multi-GPU (torchrun, one process per GPU): RHS columns are independent, so
+every rank solves its own block of the monostatic sweep against a replicated
+operator — no data-path collective; `scaling: weak`. Time = max over ranks.
+
+--impl reference runs the CPU oracle (oracle/, numpy complex128) on the host
+cores as the reference arm (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+import warnings
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ps_solve N·nrhs/sec (complex128)"
+UNIT = "N·nrhs/s"
+SM_COUNT = 148
+DFMA_PER_SM_PER_CLK = 64          # FP64 FMA lanes per SM (B200); 2 flop each
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    d = {}
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+    return d
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_oracle_arm(meta, B, seconds=12.0, max_cols=16):
+    """The oracle (as it stands) on a bounded sample: first `max_cols` RHS columns,
+    repeated solves until ~`seconds` of CPU work. Returns (N*nrhs/s, details)."""
+    from oracle import compute_scaling, read_hm, solve
+    H = read_hm(meta["hm"])
+    t0 = time.perf_counter()
+    S = compute_scaling(H)
+    t_setup = time.perf_counter() - t0
+    cols = B[:, :max_cols]
+    n_done = 0
+    t0 = time.perf_counter()
+    while True:
+        solve(H, S, cols)
+        n_done += cols.shape[1]
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([d.get("num_threads", 1) for d in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    v = H.N * n_done / el
+    return v, dict(cores=int(cores), t_setup_s=t_setup, solved_cols=n_done, seconds=el,
+                   sample=f"{cols.shape[1]} RHS columns of the same block, solved repeatedly for "
+                          f"{el:.1f} s (oracle setup {t_setup:.1f} s excluded)")
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from hmgen.build import load_or_generate, read_rhs
+    meta = load_or_generate(args.config)
+    B, _ = read_rhs(meta["rhs"])
+    nrhs = args.nrhs or B.shape[1]
+    B = np.asfortranarray(B[:, :nrhs])
+    vals = []
+    det = None
+    for s in range(args.warmup + args.steps):
+        v, det = cpu_oracle_arm(meta, B, seconds=max(2.0, min(20.0, 60.0 / max(1, args.steps))),
+                                max_cols=min(nrhs, 16))
+        if s >= args.warmup:
+            vals.append(v)
+    v = float(np.median(vals))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * meta["N"] * nrhs / v, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            "config": _config(args, meta, nrhs, args.gpus),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": det["cores"], "kind": "oracle",
+                             "sample": det["sample"]},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def _config(args, meta, nrhs, world):
+    return {"workload": f"{args.config}: {meta['desc']}", "N": meta["N"], "nrhs_per_gpu": nrhs,
+            "global_nrhs": nrhs * world, "n_leaves": meta["n_leaves"],
+            "parallelism": f"rhs-columns x{world} (replicated operator)",
+            "l2": "operator (alpha panels + D^-1 + far factors) exceeds the 126 MB L2; no flush"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--nrhs", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=2)
+    args = ap.parse_args()
+    warnings.simplefilter("ignore", RuntimeWarning)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    from hmgen.build import load_or_generate, read_rhs
+    from paper_2109_04129_b200 import PsHandle
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if rank == 0:
+        meta = load_or_generate(args.config)
+    if world > 1:
+        dist.barrier()
+        if rank != 0:
+            meta = load_or_generate(args.config)
+    Bfull, _ = read_rhs(meta["rhs"])
+    nrhs = args.nrhs or Bfull.shape[1]
+    B = np.asfortranarray(Bfull[:, :nrhs])
+    N = meta["N"]
+
+    h = PsHandle(meta["hm"], device=local, rank=rank, nranks=world)
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    h.setup()
+    setup_ms = 1e3 * (time.perf_counter() - t0)
+    info = h.info()
+
+    def dev(A):
+        return torch.from_numpy(np.ascontiguousarray(A.T)).cuda().T
+
+    Bd = dev(B)
+    Xd = torch.empty_like(Bd)
+    for _ in range(args.warmup):
+        _, rep = h.solve(Bd, Xd, stream=st)
+    with ClockSampler(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(st)
+        for _ in range(args.steps):
+            _, rep = h.solve(Bd, Xd, stream=st, want_norms=False)
+        e1.record(st)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    launches = int(rep["launches"])
+    _, rep = h.solve(Bd, Xd, stream=st)
+    ratio = rep["ratio"]
+
+    # ---- end to end: host (pinned) buffers through the C ABI, copies inside ----
+    Bh = torch.from_numpy(np.ascontiguousarray(B.T)).pin_memory().T
+    Xh = torch.empty((nrhs, N), dtype=torch.complex128).pin_memory().T
+    for _ in range(max(1, args.warmup)):
+        h.solve(Bh, Xh, stream=st, want_norms=False)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(args.steps):
+        h.solve(Bh, Xh, stream=st, want_norms=False)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms_e2e = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms_e2e], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+
+    # ---- roofline of the dominant kernel (gather-GEMM), per-launch events ----
+    h.profile(True)
+    for _ in range(args.profile_steps):
+        h.solve(Bd, Xd, stream=st, want_norms=False)
+    prof = h.profile_read()
+    h.profile(False)
+    g_ms = sum(prof[c]["ms"] for c in prof if c != "aux")
+    g_fl = sum(prof[c]["flops"] for c in prof if c != "aux")
+    g_by = sum(prof[c]["bytes"] for c in prof if c != "aux")
+    tot_ms = g_ms + prof["aux"]["ms"]
+    peaks = _peaks()
+    clocks = clk.summary()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    fp64_peak = SM_COUNT * DFMA_PER_SM_PER_CLK * 2 * sm_max * 1e6 / 1e12   # TFLOP/s
+    achieved = g_fl / (g_ms * 1e-3) / 1e12 if g_ms > 0 else 0.0
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    roof = {"bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+            "frac": achieved / fp64_peak, "traffic": None,
+            "kernel": "gemm_kernel (gather-GEMM, all sweep/D^-1/far launches)",
+            "kernel_share_of_step": g_ms / tot_ms if tot_ms > 0 else None,
+            "peak_source": f"derived: {SM_COUNT} SM x {DFMA_PER_SM_PER_CLK} DFMA/clk x 2 flop x "
+                           f"{sm_max:.0f} MHz (FP64 has no tcgen05 kind; DESIGN.md §Roofline)",
+            "hbm_view": {"operator_bytes_per_step": g_by / max(1, args.profile_steps),
+                         "achieved_GBs": g_by / (g_ms * 1e-3) / 1e9 if g_ms > 0 else 0.0,
+                         "peak_GBs": hbm_peak},
+            "per_class": {c: {"ms_per_step": prof[c]["ms"] / args.profile_steps,
+                              "launches_per_step": prof[c]["launches"] / args.profile_steps,
+                              "gflop_per_step": prof[c]["flops"] / args.profile_steps / 1e9}
+                          for c in prof}}
+
+    value = world * N * nrhs / (ms * 1e-3)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic (seeded EFIE H-matrix from hmgen; plane-wave RHS)",
+            "config": _config(args, meta, nrhs, world),
+            "setup_ms": setup_ms,
+            "structure": {k: info[k] for k in ("n_leaves", "alpha_blocks", "nR", "nD", "nF", "height", "depth")},
+            "series": {"ratio_min": float(ratio.min()), "ratio_max": float(ratio.max()),
+                       "n_diverged": int(rep["n_diverged"]),
+                       "note": "ratio >= 0.1 flags divergence (Eq. 45); BASELINE configs use 0.25-lambda "
+                               "leaves, below the paper's 0.5-lambda accuracy threshold (DESIGN.md R14)"},
+            "roofline": roof,
+            "e2e": {"value": world * N * nrhs / (ms_e2e * 1e-3), "unit": UNIT,
+                    "h2d_bytes_per_step": 16 * N * nrhs, "d2h_bytes_per_step": 16 * N * nrhs,
+                    "ms_per_step": ms_e2e},
+            "gpu_launches": launches * args.steps,
+            "clocks": clocks}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, det = cpu_oracle_arm(meta, B)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": det["cores"], "kind": "oracle",
+                                "sample": det["sample"]}
+    if rank == 0:
+        print(json.dumps(line))
+    h.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

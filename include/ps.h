@@ -1,0 +1,200 @@
+/* ps.h — C ABI of libps: the B200-native solve phase (and its O(N) setup) of the
+ * two-term power-series method of Negi, Balakrishnan & Rao, "Fast Power Series
+ * Solution of Large 3-D Electrodynamic Integral Equation for PEC Scatterers",
+ * arXiv 2109.04129 (PAPER.md in the reference tree; line numbers "P:n").
+ *
+ * Problem statement (Eq. 9): [Z] x = b, Z dense N x N, here given as
+ * the H-matrix Z = Z_N + Z_F (Eq. 13): dense symmetric near-field leaf
+ * blocks Z_ij (Eq. 14; symmetric storage P:105) and ACA far
+ * blocks Z_sub ~ U V^T (Eq. 11). Extended to a block of nrhs columns.
+ *
+ * Conventions (all entry points):
+ *   - complex = interleaved complex128 (re, im) = C99 `double _Complex`;
+ *   - matrices column-major with an explicit leading dimension; 0-based;
+ *   - sizes are int64_t; B and X use the ORIGINAL RWG basis order of the
+ *     generator (edges sorted by node pair); every internal permutation
+ *     (octree/Morton order, nested-dissection elimination order) is private;
+ *   - no exception crosses the ABI; every call returns a ps_status and, on
+ *     failure, ps_last_error() holds a one-line message;
+ *   - calls on one handle must not run concurrently (a handle owns streams,
+ *     workspaces and cached solve plans).
+ *
+ * ---------------------------------------------------------------------------
+ * H-matrix file (".hm", written by hmgen/build.py:write_hm), little-endian:
+ *   header (128 B): "HMPS", u32 version=1, i64 N, i64 n_leaves, i64 n_near,
+ *     i64 n_far, i64 flags (bit0 = symmetric), f64 lambda, f64 k, f64 leaf_edge,
+ *     i64 L, f64 origin[3], f64 root_edge, i64 near_arena_len, i64 far_arena_len
+ *   then u64 checksum(header) and, for each section, its bytes padded to 8 B
+ *   followed by u64 checksum(section bytes):
+ *     perm[N] i64        Morton position -> RWG index
+ *     leaf_off[n_leaves+1] i64   leaf (Morton id) -> first Morton position
+ *     leaf_ijk[n_leaves][3] i32  octree box index of the leaf
+ *     elim_order[n_leaves] i32   elimination order (nested dissection)
+ *     near_list[n_near][3] i64   (i, j, offset), i <= j; Z_ij column-major
+ *                                n_i x n_j at near_arena[offset]; Z_ji = Z_ij^T
+ *     near_arena[near_arena_len] complex128
+ *     far_list[n_far][7] i64     (row0, m, col0, n, level, r, offset): block
+ *                                rows [row0,row0+m) x cols [col0,col0+n) in
+ *                                Morton positions ~ U V^T, U (m x r) at offset,
+ *                                V (n x r) at offset + m r; the mirrored block
+ *                                (cols x rows) = V U^T is implied, not stored
+ *     far_arena[far_arena_len] complex128
+ *   checksum64(bytes) = (sum_i w_i (2i+1) mod 2^64) XOR nbytes over the
+ *   little-endian u64 words w_i of the zero-padded bytes.
+ */
+#ifndef PS_H_
+#define PS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ps_handle ps_handle;
+
+typedef enum {
+  PS_OK = 0,
+  PS_EINVAL = 1,     /* bad argument: NULL pointer, ldb < N, nrhs < 1, X aliases B, ... */
+  PS_EIO = 2,        /* file cannot be opened / read */
+  PS_EFORMAT = 3,    /* bad magic, version, size or checksum */
+  PS_ENOMEM = 4,     /* host or device allocation failed */
+  PS_ECUDA = 5,      /* CUDA runtime error (message carries cudaGetErrorString) */
+  PS_ENCCL = 6,      /* reserved: collective failure (multi-GPU row partition) */
+  PS_ESINGULAR = 7,  /* a scaled diagonal block Z~_kk had a pivot |u_ii| <= 1e-14 ||Z~_kk||_F;
+                        the message names the leaf (Morton id) and its elimination position */
+  PS_EDIVERGED = 8,  /* >= 1 RHS column had ||it_1|| / ||it_0|| >= ratio_threshold
+                        (Eq. 45); X IS STILL FULLY WRITTEN */
+  PS_ESTATE = 9      /* call order violated (ps_solve before ps_setup, ...) */
+} ps_status;
+
+/* Process placement. nranks > 1 selects replicated-operator mode: every rank
+ * loads the whole operator and solves the RHS columns it is given (the data-
+ * parallel split of RHS columns is done by the caller).
+ * nccl_unique_id is reserved for the row-partitioned mode and must be NULL. */
+typedef struct {
+  int rank, nranks, device;
+  const void* nccl_unique_id;
+} ps_dist;
+
+typedef struct {
+  int deterministic;        /* 1 (default): fixed summation order, bitwise repeatable (always true in v1) */
+  int ordering;             /* 0 (default): elimination order from the file (nested dissection) */
+  int amalgamate_separators;/* reserved, must be 0 */
+  double ratio_threshold;   /* divergence threshold of Eq. 45 / P:245; default 0.1; ratio >= thr => diverged */
+} ps_setup_opts;
+
+typedef struct {
+  int64_t nrhs;             /* in: capacity of it0_norm / it1_norm (ignored if both NULL) */
+  double* it0_norm;         /* out [nrhs] or NULL: ||it_0|| = ||b_o||_2 per column (Eq. 44) */
+  double* it1_norm;         /* out [nrhs] or NULL: ||it_1|| = ||U b_o||_2 per column */
+  int n_diverged;           /* out: columns with it1/it0 >= threshold */
+  double t_solve_ms;        /* out: device time of the solve (CUDA events on the solve stream) */
+  double bytes_moved;       /* out: algorithmic operator + vector bytes of this solve */
+  double flops;             /* out: algorithmic flops of this solve */
+  int64_t kernel_launches;  /* out: libps kernels launched by this call */
+} ps_report;
+
+/* hm_load — read and verify an ".hm" file (layout above), copy the near and far
+ * arenas to the device of `dist->device` (or the current device when dist is
+ * NULL) and run the symbolic analysis (struct(k) with fill, elimination tree,
+ * schedules; Eqs. 14-23 structure).
+ *   path : NUL-terminated file name.            dist: NULL = single GPU.
+ *   out  : receives the new handle (caller frees with ps_free); *out = NULL on error.
+ * Errors: PS_EINVAL (NULL args), PS_EIO, PS_EFORMAT, PS_ENOMEM, PS_ECUDA. */
+ps_status hm_load(const char* path, const ps_dist* dist, ps_handle** out);
+
+/* ps_setup — the O(N) setup of P:105-171 (Eqs. 14-23) on the GPU: for every
+ * leaf k in elimination order (level-parallel over the elimination tree):
+ *   Z~_kk, Z~_kj after all Schur updates Z~_ij += alpha_ki^T Z~_kj (Eq. 21, fill
+ *   included), D_k^{-1} = Z~_kk^{-1} (LU-type elimination with partial pivoting,
+ *   explicit inverse), alpha_kj = -D_k^{-1} Z~_kj (Eq. 16).
+ * opts: NULL = defaults. Frees the near-field input arena when done.
+ * Errors: PS_EINVAL, PS_ESTATE (already set up), PS_ESINGULAR (message names
+ * the leaf), PS_ENOMEM, PS_ECUDA. */
+ps_status ps_setup(ps_handle* h, const ps_setup_opts* opts);
+
+/* ps_solve — the two-term power-series solve (Eqs. 24, 26, 30-36):
+ *   b~ = R^T b (Eq. 24), b_o = D^{-1} b~ (Eq. 32), u = U b_o = D^{-1} R^T Z_F R b_o
+ *   (Eq. 31), x~ = b_o - u (Eq. 36, two terms), x = R x~ (Eq. 26),
+ * with R = alpha_1 alpha_2 ... alpha_{n-1} applied as a block back-substitution
+ * and R^T as a forward substitution over the stored alpha panels.
+ *   nrhs      : number of columns, >= 1.
+ *   B, ldb    : N x nrhs input, column-major, ldb >= N; read only.
+ *   X, ldx    : N x nrhs output, column-major, ldx >= N; must not overlap B.
+ *   on_device : 0 = B and X are host pointers (any host memory; pinned is
+ *               faster); 1 = device pointers on this handle's GPU.
+ *   cuda_stream : cudaStream_t to order the work on, or NULL for the handle's
+ *               own stream. With on_device=1 the call returns once the work is
+ *               queued AND complete (it synchronises the stream).
+ *   rep       : optional report (see ps_report).
+ * Errors: PS_EINVAL, PS_ESTATE (no ps_setup yet), PS_ENOMEM, PS_ECUDA,
+ * PS_EDIVERGED (X fully written; see rep->n_diverged). */
+ps_status ps_solve(ps_handle* h, int64_t nrhs, const void* B, int64_t ldb, void* X, int64_t ldx,
+                   int on_device, void* cuda_stream, ps_report* rep);
+
+/* ps_n — number of unknowns N of the loaded H-matrix; -1 if h is NULL. */
+int64_t ps_n(const ps_handle* h);
+
+/* ps_last_error — message of the last failed call on h (or of the last failed
+ * hm_load on this thread when h is NULL). Never NULL; owned by the library. */
+const char* ps_last_error(const ps_handle* h);
+
+/* ps_free — release all host and device memory of h. NULL-safe; legal after
+ * hm_load without ps_setup. */
+void ps_free(ps_handle* h);
+
+/* ------------------------------------------------------------------------
+ * Diagnostic entry points (parity tests of individual hot-path steps).
+ * All vectors: N x nrhs column-major, ORIGINAL RWG order, DEVICE pointers on
+ * the handle's GPU; ld = N. The call synchronises before returning.
+ *   op = PS_OP_RT    : Y = R^T X            (forward sweep, Eq. 24)
+ *        PS_OP_DINV  : Y = D^{-1} X         (Eq. 32)
+ *        PS_OP_R     : Y = R X              (backward sweep, Eq. 26)
+ *        PS_OP_ZF    : Y = Z_F X            (far field, Eq. 13; both halves of each pair)
+ *        PS_OP_U     : Y = D^{-1} R^T Z_F R X (Eq. 31)
+ * Errors: PS_EINVAL (bad op / nrhs), PS_ESTATE (PS_OP_ZF is legal before setup,
+ * the others are not), PS_ECUDA. */
+enum { PS_OP_RT = 1, PS_OP_DINV = 2, PS_OP_R = 3, PS_OP_ZF = 4, PS_OP_U = 5 };
+ps_status ps_apply(ps_handle* h, int op, int64_t nrhs, const void* X, void* Y);
+
+/* ps_info — structural statistics into out[0..n): see PS_INFO_* indices.
+ * Returns the number of values written (<= n). */
+enum {
+  PS_INFO_N = 0, PS_INFO_NLEAVES, PS_INFO_NNEAR, PS_INFO_NFAR, PS_INFO_ALPHA_BLOCKS,
+  PS_INFO_NR, PS_INFO_ND, PS_INFO_NF, PS_INFO_HEIGHT, PS_INFO_DEPTH, PS_INFO_SETUP_MADDS,
+  PS_INFO_SETUP_DONE, PS_INFO_COUNT
+};
+int ps_info(const ps_handle* h, double* out, int n);
+
+/* ps_analyze — host-only: read + verify the file and run the symbolic analysis
+ * (no GPU needed); writes the ps_info statistics of the would-be handle.
+ * Returns the number of values written, or -ps_status on error (message in
+ * ps_last_error(NULL)). */
+int ps_analyze(const char* path, double* out, int n);
+
+/* ps_profile — enable (1) / disable (0) per-launch CUDA-event timing inside
+ * ps_solve / ps_apply (events on the launching stream around every kernel;
+ * adds a few microseconds per launch, so timed benchmarks run with it off).
+ * Resets the accumulators. */
+ps_status ps_profile(ps_handle* h, int enable);
+
+/* ps_profile_read — accumulated since ps_profile(h,1): for each kernel class
+ * c in {0 forward sweep, 1 backward sweep, 2 D^{-1}, 3 far stage 1,
+ * 4 far stage 2, 5 permutations/combine} four values out[4c..4c+3] =
+ * (device ms, launches, algorithmic flops, algorithmic operator bytes).
+ * Classes 0-4 are all the gather-GEMM kernel. Returns values written. */
+int ps_profile_read(const ps_handle* h, double* out, int n);
+
+/* ps_get_dinv — copy D_k^{-1} of the leaf at elimination position `pos`
+ * (n_k x n_k column-major, in the leaf's Morton-local unknown order) to host
+ * memory `out` (capacity n_k^2 complex). Returns n_k, or -1 on error. */
+int64_t ps_get_dinv(ps_handle* h, int64_t pos, void* out);
+
+/* ps_elim_leaf — Morton leaf id at elimination position pos; -1 if invalid. */
+int64_t ps_elim_leaf(const ps_handle* h, int64_t pos);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PS_H_ */

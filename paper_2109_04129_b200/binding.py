@@ -1,0 +1,221 @@
+"""ctypes binding of libps (include/ps.h). Marshalling only — no numerics here.
+
+Vectors are passed as column-major N x nrhs complex128 buffers in the caller's
+(RWG) order: torch CUDA tensors (device path, on_device=1) or numpy arrays /
+pinned torch CPU tensors (host path, on_device=0).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import warnings
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(HERE, "libps.so")
+
+PS_OK, PS_EINVAL, PS_EIO, PS_EFORMAT, PS_ENOMEM, PS_ECUDA, PS_ENCCL, PS_ESINGULAR, PS_EDIVERGED, \
+    PS_ESTATE = range(10)
+STATUS_NAMES = ["PS_OK", "PS_EINVAL", "PS_EIO", "PS_EFORMAT", "PS_ENOMEM", "PS_ECUDA", "PS_ENCCL",
+                "PS_ESINGULAR", "PS_EDIVERGED", "PS_ESTATE"]
+PS_OP_RT, PS_OP_DINV, PS_OP_R, PS_OP_ZF, PS_OP_U = 1, 2, 3, 4, 5
+INFO_KEYS = ["N", "n_leaves", "n_near", "n_far", "alpha_blocks", "nR", "nD", "nF", "height",
+             "depth", "setup_madds", "setup_done"]
+
+
+class PsError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES[status] if 0 <= status < 10 else status}: {msg}")
+        self.status = status
+
+
+class _Dist(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("device", ctypes.c_int),
+                ("nccl_unique_id", ctypes.c_void_p)]
+
+
+class _Opts(ctypes.Structure):
+    _fields_ = [("deterministic", ctypes.c_int), ("ordering", ctypes.c_int),
+                ("amalgamate_separators", ctypes.c_int), ("ratio_threshold", ctypes.c_double)]
+
+
+class _Report(ctypes.Structure):
+    _fields_ = [("nrhs", ctypes.c_int64), ("it0_norm", ctypes.c_void_p), ("it1_norm", ctypes.c_void_p),
+                ("n_diverged", ctypes.c_int), ("t_solve_ms", ctypes.c_double),
+                ("bytes_moved", ctypes.c_double), ("flops", ctypes.c_double),
+                ("kernel_launches", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def lib_path() -> str:
+    return _SO
+
+
+def load_library():
+    """Load libps.so (building it first if the sources are newer and nvcc exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_SO) or os.environ.get("PS_REBUILD"):
+        from .build import build
+        build()
+    if not os.path.exists(_SO):
+        raise ImportError(f"libps.so not found at {_SO}; run `python -m paper_2109_04129_b200.build`")
+    L = ctypes.CDLL(_SO)
+    P, I64, I, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
+    L.hm_load.restype = I
+    L.hm_load.argtypes = [ctypes.c_char_p, ctypes.POINTER(_Dist), ctypes.POINTER(ctypes.c_void_p)]
+    L.ps_setup.restype = I
+    L.ps_setup.argtypes = [P, ctypes.POINTER(_Opts)]
+    L.ps_solve.restype = I
+    L.ps_solve.argtypes = [P, I64, P, I64, P, I64, I, P, ctypes.POINTER(_Report)]
+    L.ps_apply.restype = I
+    L.ps_apply.argtypes = [P, I, I64, P, P]
+    L.ps_n.restype = I64
+    L.ps_n.argtypes = [P]
+    L.ps_last_error.restype = ctypes.c_char_p
+    L.ps_last_error.argtypes = [P]
+    L.ps_free.restype = None
+    L.ps_free.argtypes = [P]
+    L.ps_info.restype = I
+    L.ps_info.argtypes = [P, ctypes.POINTER(D), I]
+    L.ps_get_dinv.restype = I64
+    L.ps_get_dinv.argtypes = [P, I64, P]
+    L.ps_profile.restype = I
+    L.ps_profile.argtypes = [P, I]
+    L.ps_profile_read.restype = I
+    L.ps_profile_read.argtypes = [P, ctypes.POINTER(D), I]
+    L.ps_analyze.restype = I
+    L.ps_analyze.argtypes = [ctypes.c_char_p, ctypes.POINTER(D), I]
+    L.ps_elim_leaf.restype = I64
+    L.ps_elim_leaf.argtypes = [P, I64]
+    _lib = L
+    return L
+
+
+def _ptr_ld(X, N):
+    """(pointer, leading dimension, on_device) of a column-major N x nrhs complex128 buffer."""
+    try:
+        import torch
+        if isinstance(X, torch.Tensor):
+            if X.dtype != torch.complex128:
+                raise TypeError("expected complex128")
+            if X.dim() == 1:
+                X = X.unsqueeze(1)
+            if X.shape[0] != N or X.stride(0) != 1:
+                raise ValueError("expected a column-major (stride(0) == 1) N x nrhs tensor")
+            ld = X.stride(1) if X.shape[1] > 1 else N
+            return X.data_ptr(), ld, X.shape[1], (1 if X.is_cuda else 0)
+    except ImportError:
+        pass
+    X = np.asarray(X)
+    if X.dtype != np.complex128:
+        raise TypeError("expected complex128")
+    if X.ndim == 1:
+        X = X[:, None]
+    if X.shape[0] != N or not (X.flags.f_contiguous or X.shape[1] == 1):
+        raise ValueError("expected a Fortran-ordered N x nrhs array")
+    return X.ctypes.data, N, X.shape[1], 0
+
+
+class PsHandle:
+    """One loaded H-matrix on one GPU (hm_load / ps_setup / ps_solve)."""
+
+    def __init__(self, path: str, device: int | None = None, rank: int = 0, nranks: int = 1):
+        L = load_library()
+        h = ctypes.c_void_p()
+        dist = None
+        if device is not None or nranks > 1:
+            dist = _Dist(rank, nranks, 0 if device is None else device, None)
+        st = L.hm_load(path.encode(), ctypes.byref(dist) if dist is not None else None, ctypes.byref(h))
+        if st != PS_OK:
+            raise PsError(st, L.ps_last_error(None).decode())
+        self._h = h
+        self.N = int(L.ps_n(h))
+        self.last_report = None
+
+    def _check(self, st: int):
+        if st != PS_OK and st != PS_EDIVERGED:
+            raise PsError(st, load_library().ps_last_error(self._h).decode())
+        return st
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load_library().ps_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def setup(self, ratio_threshold: float = 0.1):
+        o = _Opts(1, 0, 0, float(ratio_threshold))
+        self._check(load_library().ps_setup(self._h, ctypes.byref(o)))
+
+    def solve(self, B, X, stream=None, want_norms: bool = True):
+        """X <- two-term solution for B (both column-major N x nrhs complex128).
+        Returns (status, report dict). PS_EDIVERGED becomes a warning."""
+        bp, ldb, nrhs, bdev = _ptr_ld(B, self.N)
+        xp, ldx, nrhs2, xdev = _ptr_ld(X, self.N)
+        if nrhs != nrhs2 or bdev != xdev:
+            raise ValueError("B and X must have the same shape and location")
+        it0 = np.zeros(nrhs) if want_norms else None
+        it1 = np.zeros(nrhs) if want_norms else None
+        rep = _Report(nrhs, it0.ctypes.data if want_norms else None, it1.ctypes.data if want_norms else None,
+                      0, 0.0, 0.0, 0.0, 0)
+        s = None
+        if stream is not None:
+            s = ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+        st = self._check(load_library().ps_solve(self._h, nrhs, bp, ldb, xp, ldx, bdev, s,
+                                                 ctypes.byref(rep)))
+        r = dict(it0=it0, it1=it1, n_diverged=rep.n_diverged, t_solve_ms=rep.t_solve_ms,
+                 bytes=rep.bytes_moved, flops=rep.flops, launches=rep.kernel_launches,
+                 status=STATUS_NAMES[st])
+        if want_norms:
+            r["ratio"] = it1 / np.where(it0 > 0, it0, 1.0)
+        if st == PS_EDIVERGED:
+            warnings.warn(load_library().ps_last_error(self._h).decode(), RuntimeWarning, stacklevel=2)
+        self.last_report = r
+        return st, r
+
+    def apply(self, op: int, X, Y):
+        """Y <- op X for DEVICE column-major tensors with ld = N (diagnostics)."""
+        xp, ldx, nrhs, xdev = _ptr_ld(X, self.N)
+        yp, ldy, nrhs2, ydev = _ptr_ld(Y, self.N)
+        if not (xdev and ydev) or ldx != self.N or ldy != self.N or nrhs != nrhs2:
+            raise ValueError("ps_apply takes device tensors with ld == N")
+        self._check(load_library().ps_apply(self._h, op, nrhs, xp, yp))
+
+    def info(self) -> dict:
+        out = (ctypes.c_double * len(INFO_KEYS))()
+        n = load_library().ps_info(self._h, out, len(INFO_KEYS))
+        return {k: out[i] for i, k in enumerate(INFO_KEYS[:n])}
+
+    def dinv(self, pos: int) -> np.ndarray:
+        info = self.info()
+        cap = int(self.N) ** 2 if info["N"] < 4096 else 400 * 400
+        buf = np.zeros(cap, dtype=np.complex128)
+        n = load_library().ps_get_dinv(self._h, pos, buf.ctypes.data)
+        if n < 0:
+            raise PsError(PS_EINVAL, "ps_get_dinv failed")
+        return buf[:n * n].reshape(n, n, order="F")
+
+    PROFILE_CLASSES = ["fwd_sweep", "bwd_sweep", "dinv", "far_stage1", "far_stage2", "aux"]
+
+    def profile(self, enable: bool = True):
+        self._check(load_library().ps_profile(self._h, 1 if enable else 0))
+
+    def profile_read(self) -> dict:
+        n = 4 * len(self.PROFILE_CLASSES)
+        out = (ctypes.c_double * n)()
+        load_library().ps_profile_read(self._h, out, n)
+        return {c: dict(ms=out[4 * i], launches=int(out[4 * i + 1]), flops=out[4 * i + 2],
+                        bytes=out[4 * i + 3]) for i, c in enumerate(self.PROFILE_CLASSES)}
+
+    def elim_leaf(self, pos: int) -> int:
+        return int(load_library().ps_elim_leaf(self._h, pos))

@@ -1,0 +1,1018 @@
+// ps_host.cpp — host side of libps: the C ABI of include/ps.h.
+//
+//   hm_load  : read + verify the .hm file, upload the near/far arenas, symbolic
+//              analysis of the scaling (Eqs. 14-23): struct(k) with
+//              fill-in, elimination tree, level schedules, arena layout.
+//   ps_setup : GPU, level by level over the elimination tree (left-looking):
+//              Z~_p* = Z_p* + sum_d alpha_dp^T Z~_d*     (Eq. 21)
+//              D_p^{-1} = (Z~_pp)^{-1}                  (Eqs. 23, 30)
+//              alpha_p* = -D_p^{-1} Z~_p*               (Eq. 16)
+//   ps_solve : GPU, two-term series (Eqs. 24, 26, 31, 32, 36, 44-45).
+//
+// Everything that runs per leaf/block is expressed as rows of the gather-GEMM
+// task tables consumed by ps_kernels.cu; this file only builds tables (once per
+// handle / per nrhs) and enqueues launches. No numerical work happens here.
+#include "../../include/ps.h"
+#include "ps_internal.h"
+
+#include <algorithm>
+#include <array>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+using namespace ps;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct PsError {
+  ps_status st;
+  std::string msg;
+};
+
+#define CK(x)                                                                                   \
+  do {                                                                                          \
+    cudaError_t e_ = (x);                                                                       \
+    if (e_ != cudaSuccess)                                                                      \
+      throw PsError{e_ == cudaErrorMemoryAllocation ? PS_ENOMEM : PS_ECUDA,                     \
+                    std::string(#x) + ": " + cudaGetErrorString(e_)};                           \
+  } while (0)
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  int64_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(int64_t count) {
+    release();
+    if (count <= 0) return;
+    CK(cudaMalloc(&p, sizeof(T) * (size_t)count));
+    n = count;
+  }
+  void upload(const std::vector<T>& v, cudaStream_t st) {
+    alloc((int64_t)v.size());
+    if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, st));
+  }
+};
+
+uint64_t checksum64(const uint8_t* b, size_t nbytes) {
+  uint64_t h = 0;
+  size_t nw = nbytes / 8;
+  for (size_t i = 0; i < nw; ++i) {
+    uint64_t w;
+    std::memcpy(&w, b + 8 * i, 8);
+    h += w * (2 * (uint64_t)i + 1);
+  }
+  if (nbytes % 8) {
+    uint64_t w = 0;
+    std::memcpy(&w, b + 8 * nw, nbytes % 8);
+    h += w * (2 * (uint64_t)nw + 1);
+  }
+  return h ^ (uint64_t)nbytes;
+}
+
+// Optional per-launch CUDA-event profiling (ps_profile): events are recorded on
+// the launching stream around every kernel; elapsed times are accumulated per
+// kernel class after the solve's final synchronisation.
+enum { PC_FWD = 0, PC_BWD, PC_DINV, PC_FAR1, PC_FAR2, PC_AUX, PC_COUNT };
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  std::vector<std::pair<int, size_t>> marks;
+  size_t used = 0;
+  double ms[PC_COUNT] = {0}, flops[PC_COUNT] = {0}, bytes[PC_COUNT] = {0};
+  int64_t n[PC_COUNT] = {0};
+  void begin(int cls, cudaStream_t s) {
+    if (!on) return;
+    if (used + 2 > pool.size()) {
+      size_t old = pool.size();
+      pool.resize(std::max<size_t>(64, 2 * pool.size()));
+      for (size_t i = old; i < pool.size(); ++i) CK(cudaEventCreate(&pool[i]));
+    }
+    marks.push_back({cls, used});
+    CK(cudaEventRecord(pool[used], s));
+    used += 2;
+  }
+  void end(cudaStream_t s) {
+    if (!on) return;
+    CK(cudaEventRecord(pool[marks.back().second + 1], s));
+  }
+  void collect() {  // after a stream sync
+    for (auto& m : marks) {
+      float t = 0;
+      CK(cudaEventElapsedTime(&t, pool[m.second], pool[m.second + 1]));
+      ms[m.first] += t;
+      n[m.first] += 1;
+    }
+    marks.clear();
+    used = 0;
+  }
+  void reset() {
+    for (int c = 0; c < PC_COUNT; ++c) ms[c] = flops[c] = bytes[c] = 0, n[c] = 0;
+  }
+  ~Prof() {
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+
+// A gather-GEMM table: tasks, terms, work items and batches (one launch each).
+struct Table {
+  std::vector<GTask> tasks;
+  std::vector<GTerm> terms;
+  std::vector<GWork> work;
+  std::vector<Batch> batches;
+  DevBuf<GTask> d_tasks;
+  DevBuf<GTerm> d_terms;
+  DevBuf<GWork> d_work;
+  int64_t cur_batch_start = 0;
+
+  int32_t add_task(int64_t oO, int64_t sOi, int64_t sOc, int64_t oI, int64_t sIi, int64_t sIc, int m,
+                   int n, int sign) {
+    GTask t;
+    t.oO = oO; t.sOi = sOi; t.sOc = sOc;
+    t.oI = oI; t.sIi = sIi; t.sIc = sIc;
+    t.m = m; t.n = n; t.sign = sign;
+    t.t0 = t.t1 = (int32_t)terms.size();
+    t.pad = 0;
+    tasks.push_back(t);
+    return (int32_t)tasks.size() - 1;
+  }
+  void add_term(int32_t task, int64_t oA, int64_t sAi, int64_t sAk, int64_t oB, int64_t sBk,
+                int64_t sBc, int K) {
+    GTerm g;
+    g.oA = oA; g.sAi = sAi; g.sAk = sAk;
+    g.oB = oB; g.sBk = sBk; g.sBc = sBc;
+    g.K = K; g.pad = 0;
+    terms.push_back(g);
+    tasks[task].t1 = (int32_t)terms.size();
+  }
+  void tile(int32_t task) {
+    const GTask& t = tasks[task];
+    int mt = (t.m + GM_MT - 1) / GM_MT, nt = (t.n + GM_NT - 1) / GM_NT;
+    for (int a = 0; a < mt; ++a)
+      for (int b = 0; b < nt; ++b) work.push_back({task, a, b});
+  }
+  void close_batch() {
+    int64_t n = (int64_t)work.size() - cur_batch_start;
+    batches.push_back({cur_batch_start, n});
+    cur_batch_start = (int64_t)work.size();
+  }
+  double alg_flops = 0, alg_bytes = 0;   // useful flops / operator (A) bytes of one full pass
+  void upload(cudaStream_t st) {
+    alg_flops = alg_bytes = 0;
+    for (const GTask& t : tasks)
+      for (int32_t k = t.t0; k < t.t1; ++k) {
+        alg_flops += 8.0 * t.m * (double)t.n * terms[k].K;
+        alg_bytes += 16.0 * t.m * (double)terms[k].K;
+      }
+    d_tasks.upload(tasks, st);
+    d_terms.upload(terms, st);
+    d_work.upload(work, st);
+  }
+  int64_t launch(int b, double2* O, const double2* I, const double2* A, const double2* B,
+                 cudaStream_t st, Prof* pf = nullptr, int cls = 0) const {
+    const Batch& bt = batches[b];
+    if (bt.nw <= 0) return 0;
+    if (pf) pf->begin(cls, st);
+    launch_gemm(d_work.p + bt.w0, bt.nw, d_tasks.p, d_terms.p, O, I, A, B, st);
+    if (pf) pf->end(st);
+    return 1;
+  }
+  int64_t launch_all(double2* O, const double2* I, const double2* A, const double2* B,
+                     cudaStream_t st, Prof* pf = nullptr, int cls = 0) const {
+    int64_t n = 0;
+    for (size_t b = 0; b < batches.size(); ++b) n += launch((int)b, O, I, A, B, st, pf, cls);
+    if (pf && pf->on) {
+      pf->flops[cls] += alg_flops;
+      pf->bytes[cls] += alg_bytes;
+    }
+    return n;
+  }
+};
+
+// Per-nrhs solve plan: tables + workspaces.
+struct SolvePlan {
+  int64_t nrhs = 0;
+  Table fwd, bwd, dinv, far1, far2;
+  DevBuf<double2> y, bo, w, u, xt, wm, tm, ftmp, part, norms, stage;
+  int64_t nchunks = 0, rpc = 64;
+  int64_t launches_per_solve = 0;
+};
+
+}  // namespace
+
+struct ps_handle {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  // ---- file ----
+  int64_t N = 0, nl = 0, nnear = 0, nfar = 0;
+  std::vector<int64_t> perm, leaf_off;
+  std::vector<int32_t> leaf_ijk, elim;
+  std::vector<int64_t> near_list;   // 3 per block
+  std::vector<int64_t> far_list;    // 7 per block
+  int64_t near_len = 0, far_len = 0;
+  // ---- symbolic (positions p = elimination order) ----
+  std::vector<int32_t> pos_of, leaf_at, nsz, parent, height, depth;
+  std::vector<int64_t> eoff;                          // first unknown of p (E order)
+  std::vector<std::vector<int32_t>> st;               // struct(p), sorted
+  std::vector<std::vector<int64_t>> pcol;             // column offset of st[p][i] inside P_p
+  std::vector<int64_t> S;                             // sum of sizes in struct(p)
+  std::vector<std::vector<std::pair<int32_t, int32_t>>> gath;  // q -> (d, idx of q in st[d])
+  std::vector<int64_t> Woff, Poff, Doff;
+  int64_t Wlen = 0, Plen = 0, Dlen = 0;
+  int max_height = 0, max_depth = 0;
+  std::vector<int64_t> e2rwg, e2mort, m2e;
+  double setup_madds = 0;
+  int64_t alpha_blocks = 0;
+  // near block lookup: (leaf a, leaf b) -> index into near_list
+  std::unordered_map<uint64_t, int64_t> near_idx;
+  // ---- device ----
+  DevBuf<double2> d_near, d_far, d_W, d_P, d_D;
+  DevBuf<int64_t> d_e2rwg, d_e2mort, d_m2e;
+  bool setup_done = false;
+  double ratio_threshold = 0.1;
+  std::unique_ptr<SolvePlan> plan;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  Prof prof;
+};
+
+namespace {
+
+ps_status fail(ps_handle* h, ps_status s, const std::string& msg) {
+  if (h) h->err = msg;
+  g_err = msg;
+  return s;
+}
+
+// ------------------------------------------------------------------ file
+void read_file(ps_handle* h, const char* path, std::vector<double2>& near_arena,
+               std::vector<double2>& far_arena) {
+  FILE* f = std::fopen(path, "rb");
+  if (!f) throw PsError{PS_EIO, std::string("cannot open ") + path};
+  std::unique_ptr<FILE, int (*)(FILE*)> guard(f, std::fclose);
+  auto rd = [&](void* dst, size_t n) {
+    if (n && std::fread(dst, 1, n, f) != n) throw PsError{PS_EFORMAT, "truncated file"};
+  };
+  uint8_t hdr[128];
+  rd(hdr, 128);
+  if (std::memcmp(hdr, "HMPS", 4) != 0) throw PsError{PS_EFORMAT, "bad magic (not an .hm file)"};
+  uint32_t ver;
+  std::memcpy(&ver, hdr + 4, 4);
+  if (ver != 1) throw PsError{PS_EFORMAT, "unsupported .hm version " + std::to_string(ver)};
+  int64_t v5[5];
+  std::memcpy(v5, hdr + 8, 40);
+  h->N = v5[0]; h->nl = v5[1]; h->nnear = v5[2]; h->nfar = v5[3];
+  if (!(v5[4] & 1)) throw PsError{PS_EFORMAT, "only symmetric H-matrices are supported"};
+  std::memcpy(&h->near_len, hdr + 112, 8);
+  std::memcpy(&h->far_len, hdr + 120, 8);
+  if (h->N <= 0 || h->nl <= 0 || h->nl > h->N || h->nnear < h->nl || h->nfar < 0 ||
+      h->near_len < 0 || h->far_len < 0)
+    throw PsError{PS_EFORMAT, "inconsistent header sizes"};
+  uint64_t ck;
+  rd(&ck, 8);
+  if (ck != checksum64(hdr, 128)) throw PsError{PS_EFORMAT, "header checksum mismatch"};
+  auto section = [&](void* dst, size_t nbytes, const char* name) {
+    rd(dst, nbytes);
+    size_t pad = (8 - nbytes % 8) % 8;
+    uint8_t z[8];
+    rd(z, pad);
+    uint64_t c;
+    rd(&c, 8);
+    if (c != checksum64((const uint8_t*)dst, nbytes))
+      throw PsError{PS_EFORMAT, std::string("checksum mismatch in section ") + name};
+  };
+  h->perm.resize(h->N);
+  section(h->perm.data(), 8 * h->N, "perm");
+  h->leaf_off.resize(h->nl + 1);
+  section(h->leaf_off.data(), 8 * (h->nl + 1), "leaf_off");
+  h->leaf_ijk.resize(3 * h->nl);
+  section(h->leaf_ijk.data(), 12 * h->nl, "leaf_ijk");
+  h->elim.resize(h->nl);
+  section(h->elim.data(), 4 * h->nl, "elim_order");
+  h->near_list.resize(3 * h->nnear);
+  section(h->near_list.data(), 24 * h->nnear, "near_list");
+  near_arena.resize(h->near_len);
+  section(near_arena.data(), 16 * h->near_len, "near_arena");
+  h->far_list.resize(7 * h->nfar);
+  section(h->far_list.data(), 56 * h->nfar, "far_list");
+  far_arena.resize(h->far_len);
+  section(far_arena.data(), 16 * h->far_len, "far_arena");
+  // validation of indices
+  if (h->leaf_off[0] != 0 || h->leaf_off[h->nl] != h->N) throw PsError{PS_EFORMAT, "bad leaf_off"};
+  for (int64_t l = 0; l < h->nl; ++l)
+    if (h->leaf_off[l + 1] <= h->leaf_off[l]) throw PsError{PS_EFORMAT, "empty leaf"};
+  std::vector<char> seen(h->N, 0);
+  for (int64_t p : h->perm) {
+    if (p < 0 || p >= h->N || seen[p]) throw PsError{PS_EFORMAT, "perm is not a permutation"};
+    seen[p] = 1;
+  }
+  std::vector<char> seenl(h->nl, 0);
+  for (int32_t l : h->elim) {
+    if (l < 0 || l >= h->nl || seenl[l]) throw PsError{PS_EFORMAT, "elim_order is not a permutation"};
+    seenl[l] = 1;
+  }
+  for (int64_t b = 0; b < h->nnear; ++b) {
+    int64_t i = h->near_list[3 * b], j = h->near_list[3 * b + 1], o = h->near_list[3 * b + 2];
+    if (i < 0 || j < i || j >= h->nl) throw PsError{PS_EFORMAT, "bad near pair"};
+    int64_t ni = h->leaf_off[i + 1] - h->leaf_off[i], nj = h->leaf_off[j + 1] - h->leaf_off[j];
+    if (o < 0 || o + ni * nj > h->near_len) throw PsError{PS_EFORMAT, "near block out of arena"};
+  }
+  for (int64_t b = 0; b < h->nfar; ++b) {
+    const int64_t* F = &h->far_list[7 * b];
+    if (F[0] < 0 || F[1] <= 0 || F[0] + F[1] > h->N || F[2] < 0 || F[3] <= 0 || F[2] + F[3] > h->N ||
+        F[5] < 0 || F[6] < 0 || F[6] + F[5] * (F[1] + F[3]) > h->far_len)
+      throw PsError{PS_EFORMAT, "bad far block"};
+  }
+}
+
+// ------------------------------------------------------------------ symbolic
+void symbolic(ps_handle* h) {
+  const int64_t nl = h->nl;
+  h->pos_of.assign(nl, 0);
+  h->leaf_at.assign(nl, 0);
+  for (int64_t p = 0; p < nl; ++p) {
+    h->leaf_at[p] = h->elim[p];
+    h->pos_of[h->elim[p]] = (int32_t)p;
+  }
+  h->nsz.resize(nl);
+  h->eoff.assign(nl + 1, 0);
+  for (int64_t p = 0; p < nl; ++p) {
+    int32_t l = h->leaf_at[p];
+    h->nsz[p] = (int32_t)(h->leaf_off[l + 1] - h->leaf_off[l]);
+    h->eoff[p + 1] = h->eoff[p] + h->nsz[p];
+  }
+  // adjacency (upper, by position) from the near list
+  std::vector<std::vector<int32_t>> up(nl);
+  bool has_diag_missing = false;
+  std::vector<char> diag(nl, 0);
+  for (int64_t b = 0; b < h->nnear; ++b) {
+    int64_t i = h->near_list[3 * b], j = h->near_list[3 * b + 1];
+    h->near_idx[(uint64_t)i * (uint64_t)nl + (uint64_t)j] = b;
+    int32_t p = h->pos_of[i], q = h->pos_of[j];
+    if (p == q) { diag[p] = 1; continue; }
+    if (p > q) std::swap(p, q);
+    up[p].push_back(q);
+  }
+  for (int64_t p = 0; p < nl; ++p) has_diag_missing |= !diag[p];
+  if (has_diag_missing) throw PsError{PS_EFORMAT, "near list lacks a diagonal block"};
+  // struct(p) = up(p) U (U_children struct(c) \ {p}); parent = min struct(p)
+  h->st.assign(nl, {});
+  h->parent.assign(nl, -1);
+  std::vector<std::vector<int32_t>> children(nl);
+  for (int64_t p = 0; p < nl; ++p) {
+    std::vector<int32_t> s = up[p];
+    for (int32_t c : children[p])
+      for (int32_t x : h->st[c])
+        if (x != p) s.push_back(x);
+    std::sort(s.begin(), s.end());
+    s.erase(std::unique(s.begin(), s.end()), s.end());
+    h->st[p] = std::move(s);
+    if (!h->st[p].empty()) {
+      h->parent[p] = h->st[p][0];
+      children[h->st[p][0]].push_back((int32_t)p);
+    }
+  }
+  // levels: height (forward sweep / setup), depth (backward sweep)
+  h->height.assign(nl, 0);
+  for (int64_t p = 0; p < nl; ++p)
+    if (h->parent[p] >= 0) h->height[h->parent[p]] = std::max(h->height[h->parent[p]], h->height[p] + 1);
+  h->depth.assign(nl, 0);
+  for (int64_t p = nl - 1; p >= 0; --p)
+    if (h->parent[p] >= 0) h->depth[p] = h->depth[h->parent[p]] + 1;
+  h->max_height = 0;
+  h->max_depth = 0;
+  for (int64_t p = 0; p < nl; ++p) {
+    h->max_height = std::max(h->max_height, h->height[p]);
+    h->max_depth = std::max(h->max_depth, h->depth[p]);
+  }
+  // panel column offsets, arena layout, gather lists, setup cost
+  h->pcol.assign(nl, {});
+  h->S.assign(nl, 0);
+  h->gath.assign(nl, {});
+  h->Woff.assign(nl, 0);
+  h->Poff.assign(nl, 0);
+  h->Doff.assign(nl, 0);
+  int64_t W = 0, P = 0, D = 0;
+  h->setup_madds = 0;
+  h->alpha_blocks = 0;
+  for (int64_t p = 0; p < nl; ++p) {
+    int64_t c = 0;
+    h->pcol[p].resize(h->st[p].size());
+    for (size_t i = 0; i < h->st[p].size(); ++i) {
+      h->pcol[p][i] = c;
+      c += h->nsz[h->st[p][i]];
+      h->gath[h->st[p][i]].push_back({(int32_t)p, (int32_t)i});
+    }
+    h->S[p] = c;
+    h->alpha_blocks += (int64_t)h->st[p].size();
+    const int64_t n = h->nsz[p];
+    h->Woff[p] = W;
+    W += n * (n + c);
+    h->Poff[p] = P;
+    P += n * c;
+    h->Doff[p] = D;
+    D += n * n;
+    h->setup_madds += (double)n * n * n + (double)n * n * c + 0.5 * (double)n * c * (c + n);
+  }
+  h->Wlen = W;
+  h->Plen = P;
+  h->Dlen = D;
+  // unknown maps
+  h->e2mort.resize(h->N);
+  h->e2rwg.resize(h->N);
+  h->m2e.resize(h->N);
+  for (int64_t p = 0; p < nl; ++p) {
+    int32_t l = h->leaf_at[p];
+    for (int64_t t = 0; t < h->nsz[p]; ++t) {
+      int64_t e = h->eoff[p] + t, m = h->leaf_off[l] + t;
+      h->e2mort[e] = m;
+      h->e2rwg[e] = h->perm[m];
+      h->m2e[m] = e;
+    }
+  }
+}
+
+int64_t wcol(const ps_handle* h, int32_t p, int32_t j) {
+  // column offset of block j inside W_p = [Z~_pp | Z~_p,struct(p)]
+  if (j == p) return 0;
+  const auto& s = h->st[p];
+  auto it = std::lower_bound(s.begin(), s.end(), j);
+  if (it == s.end() || *it != j) throw PsError{PS_ECUDA, "internal: struct lookup failed"};
+  return h->nsz[p] + h->pcol[p][it - s.begin()];
+}
+
+// ------------------------------------------------------------------ setup
+struct SetupPlan {
+  Table asmb, panel;
+  std::vector<std::vector<int32_t>> level_leaves;
+  std::vector<DevBuf<int32_t>> d_ids, d_sz;
+  std::vector<DevBuf<int64_t>> d_src, d_ld, d_dst;
+  std::vector<int> level_maxn;
+};
+
+void build_setup_plan(ps_handle* h, SetupPlan& sp) {
+  const int64_t nl = h->nl;
+  sp.level_leaves.assign(h->max_height + 1, {});
+  for (int64_t p = 0; p < nl; ++p) sp.level_leaves[h->height[p]].push_back((int32_t)p);
+  for (int lev = 0; lev <= h->max_height; ++lev) {
+    for (int32_t p : sp.level_leaves[lev]) {
+      const int64_t np_ = h->nsz[p];
+      const int32_t lp = h->leaf_at[p];
+      // targets j in {p} U struct(p): W_pj = Z_pj + sum_d alpha_dp^T W_dj
+      std::vector<int32_t> targets;
+      targets.push_back(p);
+      for (int32_t j : h->st[p]) targets.push_back(j);
+      std::map<int32_t, int32_t> task_of;
+      for (int32_t j : targets) {
+        const int64_t nj = h->nsz[j];
+        const int32_t lj = h->leaf_at[j];
+        // near block init (file stores i <= j by leaf id; Z_ji = Z_ij^T)
+        int64_t oI = -1, sIi = 0, sIc = 0;
+        uint64_t key_a = (uint64_t)std::min(lp, lj) * (uint64_t)nl + (uint64_t)std::max(lp, lj);
+        auto it = h->near_idx.find(key_a);
+        if (it != h->near_idx.end()) {
+          const int64_t* nb = &h->near_list[3 * it->second];
+          const int64_t n_first = h->leaf_off[nb[0] + 1] - h->leaf_off[nb[0]];
+          oI = nb[2];
+          if (lp == nb[0]) { sIi = 1; sIc = n_first; }   // Z_{lp,lj} as stored
+          else { sIi = n_first; sIc = 1; }               // transpose view
+        }
+        const int64_t oO = h->Woff[p] + wcol(h, p, j) * np_;
+        int32_t t = sp.asmb.add_task(oO, 1, np_, oI, sIi, sIc, (int)np_, (int)nj, +1);
+        task_of[j] = t;
+      }
+      // updates from descendants d with p in struct(d), in increasing d
+      for (auto [d, idx] : h->gath[p]) {
+        const int64_t nd = h->nsz[d];
+        const auto& sd = h->st[d];
+        const int64_t oA = h->Poff[d] + h->pcol[d][idx] * nd;   // alpha_dp (nd x np), transposed view
+        for (size_t jj = idx; jj < sd.size(); ++jj) {
+          const int32_t j = sd[jj];
+          const int64_t oB = h->Woff[d] + (nd + h->pcol[d][jj]) * nd;  // W_dj (nd x nj)
+          sp.asmb.add_term(task_of.at(j), oA, nd, 1, oB, 1, nd, (int)nd);
+        }
+      }
+      for (int32_t j : targets) sp.asmb.tile(task_of.at(j));
+    }
+    sp.asmb.close_batch();
+    // panel: P_p = -Dinv_p W_p[:, n_p:]
+    for (int32_t p : sp.level_leaves[lev]) {
+      const int64_t np_ = h->nsz[p];
+      if (h->S[p] == 0) continue;
+      int32_t t = sp.panel.add_task(h->Poff[p], 1, np_, -1, 0, 0, (int)np_, (int)h->S[p], -1);
+      sp.panel.add_term(t, h->Doff[p], 1, np_, h->Woff[p] + np_ * np_, 1, np_, (int)np_);
+      sp.panel.tile(t);
+    }
+    sp.panel.close_batch();
+  }
+  sp.asmb.upload(h->stream);
+  sp.panel.upload(h->stream);
+  const int L = h->max_height + 1;
+  sp.d_ids.resize(L);
+  sp.d_sz.resize(L);
+  sp.d_src.resize(L);
+  sp.d_ld.resize(L);
+  sp.d_dst.resize(L);
+  sp.level_maxn.assign(L, 0);
+  for (int lev = 0; lev < L; ++lev) {
+    std::vector<int32_t> ids, sz;
+    std::vector<int64_t> src, ld, dst;
+    for (int32_t p : sp.level_leaves[lev]) {
+      ids.push_back(p);
+      sz.push_back(h->nsz[p]);
+      src.push_back(h->Woff[p]);
+      ld.push_back(h->nsz[p]);
+      dst.push_back(h->Doff[p]);
+      sp.level_maxn[lev] = std::max(sp.level_maxn[lev], h->nsz[p]);
+    }
+    sp.d_ids[lev].upload(ids, h->stream);
+    sp.d_sz[lev].upload(sz, h->stream);
+    sp.d_src[lev].upload(src, h->stream);
+    sp.d_ld[lev].upload(ld, h->stream);
+    sp.d_dst[lev].upload(dst, h->stream);
+  }
+}
+
+// ------------------------------------------------------------------ solve plan
+void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
+  const int64_t nl = h->nl;
+  const int64_t R = nrhs;
+  sp.nrhs = nrhs;
+  // forward sweep (gather form of Eq. 24), batches by height:
+  //   y_q = y_q + sum_{d: q in struct(d)} alpha_dq^T y_d
+  std::vector<std::vector<int32_t>> byh(h->max_height + 1), byd(h->max_depth + 1);
+  for (int64_t p = 0; p < nl; ++p) {
+    byh[h->height[p]].push_back((int32_t)p);
+    byd[h->depth[p]].push_back((int32_t)p);
+  }
+  for (int lev = 0; lev <= h->max_height; ++lev) {
+    for (int32_t q : byh[lev]) {
+      if (h->gath[q].empty()) continue;
+      const int64_t nq = h->nsz[q];
+      int32_t t = sp.fwd.add_task(h->eoff[q] * R, R, 1, h->eoff[q] * R, R, 1, (int)nq, (int)R, +1);
+      for (auto [d, idx] : h->gath[q]) {
+        const int64_t nd = h->nsz[d];
+        sp.fwd.add_term(t, h->Poff[d] + h->pcol[d][idx] * nd, nd, 1, h->eoff[d] * R, R, 1, (int)nd);
+      }
+      sp.fwd.tile(t);
+    }
+    sp.fwd.close_batch();
+  }
+  // backward sweep (Eq. 26), batches by depth: w_p = v_p + sum_j alpha_pj w_j
+  for (int lev = 0; lev <= h->max_depth; ++lev) {
+    for (int32_t p : byd[lev]) {
+      const int64_t np_ = h->nsz[p];
+      int32_t t = sp.bwd.add_task(h->eoff[p] * R, R, 1, h->eoff[p] * R, R, 1, (int)np_, (int)R, +1);
+      for (size_t i = 0; i < h->st[p].size(); ++i) {
+        const int32_t j = h->st[p][i];
+        sp.bwd.add_term(t, h->Poff[p] + h->pcol[p][i] * np_, 1, np_, h->eoff[j] * R, R, 1,
+                        (int)h->nsz[j]);
+      }
+      sp.bwd.tile(t);
+    }
+    sp.bwd.close_batch();
+  }
+  // D^{-1} (Eq. 32), one batch
+  for (int64_t p = 0; p < nl; ++p) {
+    const int64_t np_ = h->nsz[p];
+    int32_t t = sp.dinv.add_task(h->eoff[p] * R, R, 1, -1, 0, 0, (int)np_, (int)R, +1);
+    sp.dinv.add_term(t, h->Doff[p], 1, np_, h->eoff[p] * R, R, 1, (int)np_);
+    sp.dinv.tile(t);
+  }
+  sp.dinv.close_batch();
+  // far field, Morton order. stage 1: tmp_b = V^T w[s], tmp'_b = U^T w[t]
+  std::vector<int64_t> toff(h->nfar);
+  int64_t T = 0;
+  for (int64_t b = 0; b < h->nfar; ++b) {
+    const int64_t* F = &h->far_list[7 * b];
+    const int64_t r0 = F[0], m = F[1], c0 = F[2], n = F[3], r = F[5], off = F[6];
+    toff[b] = T;
+    T += 2 * r * R;
+    if (r == 0) continue;
+    int32_t t1 = sp.far1.add_task(toff[b], R, 1, -1, 0, 0, (int)r, (int)R, +1);
+    sp.far1.add_term(t1, off + m * r, n, 1, c0 * R, R, 1, (int)n);      // V^T (r x n)
+    sp.far1.tile(t1);
+    int32_t t2 = sp.far1.add_task(toff[b] + r * R, R, 1, -1, 0, 0, (int)r, (int)R, +1);
+    sp.far1.add_term(t2, off, m, 1, r0 * R, R, 1, (int)m);              // U^T (r x m)
+    sp.far1.tile(t2);
+  }
+  sp.far1.close_batch();
+  // stage 2 per Morton leaf: t_l = sum U_b[rows of l] tmp_b + sum V_b[rows of l] tmp'_b
+  std::vector<std::vector<std::array<int64_t, 4>>> contrib(nl);  // (oA, lda, oB, K)
+  auto leaf_of_pos = [&](int64_t m) {
+    return (int64_t)(std::upper_bound(h->leaf_off.begin(), h->leaf_off.end(), m) - h->leaf_off.begin()) - 1;
+  };
+  for (int64_t b = 0; b < h->nfar; ++b) {
+    const int64_t* F = &h->far_list[7 * b];
+    const int64_t r0 = F[0], m = F[1], c0 = F[2], n = F[3], r = F[5], off = F[6];
+    if (r == 0) continue;
+    for (int64_t l = leaf_of_pos(r0); l < nl && h->leaf_off[l] < r0 + m; ++l)
+      contrib[l].push_back({off + (h->leaf_off[l] - r0), m, toff[b], r});
+    for (int64_t l = leaf_of_pos(c0); l < nl && h->leaf_off[l] < c0 + n; ++l)
+      contrib[l].push_back({off + m * r + (h->leaf_off[l] - c0), n, toff[b] + r * R, r});
+  }
+  for (int64_t l = 0; l < nl; ++l) {
+    const int64_t nlf = h->leaf_off[l + 1] - h->leaf_off[l];
+    int32_t t = sp.far2.add_task(h->leaf_off[l] * R, R, 1, -1, 0, 0, (int)nlf, (int)R, +1);
+    for (auto& c : contrib[l]) sp.far2.add_term(t, c[0], 1, c[1], c[2], R, 1, (int)c[3]);
+    sp.far2.tile(t);
+  }
+  sp.far2.close_batch();
+  for (Table* tb : {&sp.fwd, &sp.bwd, &sp.dinv, &sp.far1, &sp.far2}) tb->upload(h->stream);
+  const int64_t NR = h->N * R;
+  sp.y.alloc(NR); sp.bo.alloc(NR); sp.w.alloc(NR); sp.u.alloc(NR); sp.xt.alloc(NR);
+  sp.wm.alloc(NR); sp.tm.alloc(NR); sp.stage.alloc(NR);
+  sp.ftmp.alloc(std::max<int64_t>(T, 1));
+  sp.nchunks = (h->N + sp.rpc - 1) / sp.rpc;
+  sp.part.alloc(sp.nchunks * R);
+  sp.norms.alloc(R);
+  CK(cudaStreamSynchronize(h->stream));
+}
+
+SolvePlan& get_plan(ps_handle* h, int64_t nrhs) {
+  if (!h->plan || h->plan->nrhs != nrhs) {
+    h->plan.reset();
+    auto sp = std::make_unique<SolvePlan>();
+    build_solve_plan(h, *sp, nrhs);
+    h->plan = std::move(sp);
+  }
+  return *h->plan;
+}
+
+// individual operators on internal (E-order, row-major) vectors --------------
+int64_t op_Rt(ps_handle* h, SolvePlan& sp, double2* v, cudaStream_t s) {   // in place
+  return sp.fwd.launch_all(v, v, h->d_P.p, v, s, &h->prof, PC_FWD);
+}
+int64_t op_R(ps_handle* h, SolvePlan& sp, const double2* in, double2* out, cudaStream_t s) {
+  return sp.bwd.launch_all(out, in, h->d_P.p, out, s, &h->prof, PC_BWD);
+}
+int64_t op_Dinv(ps_handle* h, SolvePlan& sp, const double2* in, double2* out, cudaStream_t s) {
+  return sp.dinv.launch_all(out, nullptr, h->d_D.p, in, s, &h->prof, PC_DINV);
+}
+template <class F>
+int64_t aux(ps_handle* h, cudaStream_t s, F f) {
+  h->prof.begin(PC_AUX, s);
+  f();
+  h->prof.end(s);
+  return 1;
+}
+int64_t op_ZF(ps_handle* h, SolvePlan& sp, const double2* in, double2* out, cudaStream_t s) {
+  const int64_t N = h->N, R = sp.nrhs;
+  int64_t n = 0;
+  n += aux(h, s, [&] { launch_permute_rows(N, R, h->d_m2e.p, in, sp.wm.p, s); });      // E -> Morton
+  n += sp.far1.launch_all(sp.ftmp.p, nullptr, h->d_far.p, sp.wm.p, s, &h->prof, PC_FAR1);
+  n += sp.far2.launch_all(sp.tm.p, nullptr, h->d_far.p, sp.ftmp.p, s, &h->prof, PC_FAR2);
+  n += aux(h, s, [&] { launch_permute_rows(N, R, h->d_e2mort.p, sp.tm.p, out, s); });  // Morton -> E
+  return n;
+}
+
+double solve_bytes(const ps_handle* h, int64_t nrhs) {
+  double nR = 0, nD = 0, nF = 0;
+  for (int64_t p = 0; p < h->nl; ++p) {
+    nR += (double)h->nsz[p] * h->S[p];
+    nD += (double)h->nsz[p] * h->nsz[p];
+  }
+  for (int64_t b = 0; b < h->nfar; ++b) nF += (double)h->far_list[7 * b + 5] * (h->far_list[7 * b + 1] + h->far_list[7 * b + 3]);
+  // operator: 4 alpha sweeps, 2 D^{-1}, far factors once;
+  // vectors: each of ~12 N x nrhs passes (read or write)
+  return 16.0 * (4 * nR + 2 * nD + nF) + 16.0 * 12.0 * (double)h->N * nrhs;
+}
+double solve_flops(const ps_handle* h, int64_t nrhs) {
+  double nR = 0, nD = 0, nF = 0;
+  for (int64_t p = 0; p < h->nl; ++p) {
+    nR += (double)h->nsz[p] * h->S[p];
+    nD += (double)h->nsz[p] * h->nsz[p];
+  }
+  for (int64_t b = 0; b < h->nfar; ++b) nF += (double)h->far_list[7 * b + 5] * (h->far_list[7 * b + 1] + h->far_list[7 * b + 3]);
+  return 8.0 * nrhs * (4 * nR + 2 * nD + 2 * nF);
+}
+
+}  // namespace
+
+// ======================================================================= C ABI
+extern "C" {
+
+ps_status hm_load(const char* path, const ps_dist* dist, ps_handle** out) {
+  if (!out) return fail(nullptr, PS_EINVAL, "hm_load: out is NULL");
+  *out = nullptr;
+  if (!path) return fail(nullptr, PS_EINVAL, "hm_load: path is NULL");
+  if (dist && (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks || dist->nccl_unique_id))
+    return fail(nullptr, PS_EINVAL, "hm_load: bad ps_dist (nccl_unique_id must be NULL in this version)");
+  std::unique_ptr<ps_handle> h(new ps_handle());
+  try {
+    std::vector<double2> near_arena, far_arena;
+    read_file(h.get(), path, near_arena, far_arena);
+    symbolic(h.get());
+    if (dist) {
+      h->device = dist->device;
+      CK(cudaSetDevice(h->device));
+    } else {
+      CK(cudaGetDevice(&h->device));
+    }
+    CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&h->ev0));
+    CK(cudaEventCreate(&h->ev1));
+    h->d_near.upload(near_arena, h->stream);
+    h->d_far.upload(far_arena, h->stream);
+    h->d_e2rwg.upload(h->e2rwg, h->stream);
+    h->d_e2mort.upload(h->e2mort, h->stream);
+    h->d_m2e.upload(h->m2e, h->stream);
+    CK(cudaStreamSynchronize(h->stream));
+  } catch (const PsError& e) {
+    return fail(nullptr, e.st, "hm_load: " + e.msg);
+  } catch (const std::bad_alloc&) {
+    return fail(nullptr, PS_ENOMEM, "hm_load: host allocation failed");
+  }
+  *out = h.release();
+  return PS_OK;
+}
+
+ps_status ps_setup(ps_handle* h, const ps_setup_opts* opts) {
+  if (!h) return fail(nullptr, PS_EINVAL, "ps_setup: handle is NULL");
+  if (h->setup_done) return fail(h, PS_ESTATE, "ps_setup: already set up");
+  if (opts) {
+    if (opts->ordering != 0 || opts->amalgamate_separators != 0)
+      return fail(h, PS_EINVAL, "ps_setup: only ordering=0 and amalgamate_separators=0 are supported");
+    if (!(opts->ratio_threshold > 0.0)) return fail(h, PS_EINVAL, "ps_setup: ratio_threshold must be > 0");
+    h->ratio_threshold = opts->ratio_threshold;
+  }
+  try {
+    CK(cudaSetDevice(h->device));
+    cudaStream_t s = h->stream;
+    h->d_W.alloc(std::max<int64_t>(h->Wlen, 1));
+    h->d_P.alloc(std::max<int64_t>(h->Plen, 1));
+    h->d_D.alloc(std::max<int64_t>(h->Dlen, 1));
+    SetupPlan sp;
+    build_setup_plan(h, sp);
+    DevBuf<int32_t> d_status;
+    d_status.alloc(h->nl);
+    CK(cudaMemsetAsync(d_status.p, 0, sizeof(int32_t) * h->nl, s));
+    std::vector<int32_t> status(h->nl, 0);
+    for (int lev = 0; lev <= h->max_height; ++lev) {
+      // Eq. 21 (left-looking): assemble W_p = [Z~_pp | Z~_p,struct(p)]
+      sp.asmb.launch(lev, h->d_W.p, h->d_near.p, h->d_P.p, h->d_W.p, s);
+      // Eqs. 23/30: D_p^{-1}
+      const int64_t nlev = (int64_t)sp.level_leaves[lev].size();
+      launch_inverse(nlev, sp.d_ids[lev].p, sp.d_sz[lev].p, sp.d_src[lev].p, sp.d_ld[lev].p,
+                     sp.d_dst[lev].p, h->d_W.p, h->d_D.p, d_status.p, sp.level_maxn[lev], s);
+      // per-level status slot: leaves of this level write status[0..nlev)
+      CK(cudaMemcpyAsync(status.data(), d_status.p, sizeof(int32_t) * nlev, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      for (int64_t i = 0; i < nlev; ++i)
+        if (status[i]) {
+          int32_t p = sp.level_leaves[lev][i];
+          h->d_W.release();
+          h->d_P.release();
+          h->d_D.release();
+          return fail(h, PS_ESINGULAR,
+                      "ps_setup: singular scaled diagonal block at elimination position " +
+                          std::to_string(p) + " (leaf " + std::to_string(h->leaf_at[p]) + ")");
+        }
+      // Eq. 16: alpha_p* = -D_p^{-1} Z~_p*
+      sp.panel.launch(lev, h->d_P.p, nullptr, h->d_D.p, h->d_W.p, s);
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+    h->d_W.release();
+    h->d_near.release();
+    h->setup_done = true;
+  } catch (const PsError& e) {
+    return fail(h, e.st, "ps_setup: " + e.msg);
+  } catch (const std::bad_alloc&) {
+    return fail(h, PS_ENOMEM, "ps_setup: host allocation failed");
+  }
+  return PS_OK;
+}
+
+ps_status ps_solve(ps_handle* h, int64_t nrhs, const void* B, int64_t ldb, void* X, int64_t ldx,
+                   int on_device, void* cuda_stream, ps_report* rep) {
+  if (!h) return fail(nullptr, PS_EINVAL, "ps_solve: handle is NULL");
+  if (!h->setup_done) return fail(h, PS_ESTATE, "ps_solve: ps_setup has not run");
+  if (nrhs < 1 || !B || !X || ldb < h->N || ldx < h->N)
+    return fail(h, PS_EINVAL, "ps_solve: bad arguments (nrhs >= 1, B/X non-NULL, ldb/ldx >= N)");
+  {
+    const char* b0 = (const char*)B;
+    const char* b1 = b0 + 16 * (ldb * (nrhs - 1) + h->N);
+    const char* x0 = (const char*)X;
+    const char* x1 = x0 + 16 * (ldx * (nrhs - 1) + h->N);
+    if (b0 < x1 && x0 < b1) return fail(h, PS_EINVAL, "ps_solve: X overlaps B");
+  }
+  try {
+    CK(cudaSetDevice(h->device));
+    cudaStream_t s = cuda_stream ? (cudaStream_t)cuda_stream : h->stream;
+    SolvePlan& sp = get_plan(h, nrhs);
+    const int64_t N = h->N, R = nrhs;
+    int64_t launches = 0;
+    const double2* Bd = (const double2*)B;
+    int64_t ldb_d = ldb;
+    if (!on_device) {
+      CK(cudaMemcpy2DAsync(sp.stage.p, 16 * N, B, 16 * ldb, 16 * N, nrhs, cudaMemcpyHostToDevice, s));
+      Bd = sp.stage.p;
+      ldb_d = N;
+    }
+    CK(cudaEventRecord(h->ev0, s));
+    launches += aux(h, s, [&] { launch_permute_in(N, R, h->d_e2rwg.p, Bd, ldb_d, sp.y.p, s); });  // RWG -> E
+    launches += op_Rt(h, sp, sp.y.p, s);                                // b~ = R^T b     (Eq. 24)
+    launches += op_Dinv(h, sp, sp.y.p, sp.bo.p, s);                     // b_o = D^-1 b~  (Eq. 32)
+    launches += op_R(h, sp, sp.bo.p, sp.w.p, s);                        // w = R b_o
+    launches += op_ZF(h, sp, sp.w.p, sp.y.p, s);                        // t = Z_F w
+    launches += op_Rt(h, sp, sp.y.p, s);                                // z = R^T t
+    launches += op_Dinv(h, sp, sp.y.p, sp.u.p, s);                      // u = D^-1 z = U b_o (Eq. 31)
+    launches += aux(h, s, [&] {                                         // x~ = b_o - u (Eq. 36), norms
+      launch_combine_norms(N, R, sp.bo.p, sp.u.p, sp.xt.p, sp.part.p, sp.rpc, s);
+      launch_finalize_norms(sp.nchunks, R, sp.part.p, sp.norms.p, s);
+    }) + 1;
+    launches += op_R(h, sp, sp.xt.p, sp.xt.p, s);                       // x = R x~       (Eq. 26)
+    double2* Xd = on_device ? (double2*)X : sp.stage.p;
+    launches += aux(h, s, [&] { launch_permute_out(N, R, h->d_e2rwg.p, sp.xt.p, Xd, on_device ? ldx : N, s); });
+    CK(cudaEventRecord(h->ev1, s));
+    CK(cudaGetLastError());
+    if (!on_device)
+      CK(cudaMemcpy2DAsync(X, 16 * ldx, sp.stage.p, 16 * N, 16 * N, nrhs, cudaMemcpyDeviceToHost, s));
+    std::vector<double2> norms(R);
+    CK(cudaMemcpyAsync(norms.data(), sp.norms.p, 16 * R, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (h->prof.on) h->prof.collect();
+    int ndiv = 0;
+    for (int64_t c = 0; c < R; ++c) {
+      const double r = norms[c].x > 0 ? norms[c].y / norms[c].x : 0.0;
+      if (!(r < h->ratio_threshold)) ++ndiv;
+    }
+    sp.launches_per_solve = launches;
+    if (rep) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+      rep->t_solve_ms = ms;
+      rep->n_diverged = ndiv;
+      rep->bytes_moved = solve_bytes(h, nrhs);
+      rep->flops = solve_flops(h, nrhs);
+      rep->kernel_launches = launches;
+      const int64_t cap = std::min<int64_t>(rep->nrhs, R);
+      for (int64_t c = 0; c < cap; ++c) {
+        if (rep->it0_norm) rep->it0_norm[c] = norms[c].x;
+        if (rep->it1_norm) rep->it1_norm[c] = norms[c].y;
+      }
+    }
+    if (ndiv > 0)
+      return fail(h, PS_EDIVERGED, "ps_solve: " + std::to_string(ndiv) + " of " + std::to_string(R) +
+                                       " columns have ||it_1||/||it_0|| >= " + std::to_string(h->ratio_threshold));
+  } catch (const PsError& e) {
+    return fail(h, e.st, "ps_solve: " + e.msg);
+  } catch (const std::bad_alloc&) {
+    return fail(h, PS_ENOMEM, "ps_solve: host allocation failed");
+  }
+  return PS_OK;
+}
+
+ps_status ps_apply(ps_handle* h, int op, int64_t nrhs, const void* Xin, void* Yout) {
+  if (!h) return fail(nullptr, PS_EINVAL, "ps_apply: handle is NULL");
+  if (op < PS_OP_RT || op > PS_OP_U || nrhs < 1 || !Xin || !Yout)
+    return fail(h, PS_EINVAL, "ps_apply: bad arguments");
+  if (op != PS_OP_ZF && !h->setup_done) return fail(h, PS_ESTATE, "ps_apply: ps_setup has not run");
+  try {
+    CK(cudaSetDevice(h->device));
+    cudaStream_t s = h->stream;
+    SolvePlan& sp = get_plan(h, nrhs);
+    const int64_t N = h->N, R = nrhs;
+    launch_permute_in(N, R, h->d_e2rwg.p, (const double2*)Xin, N, sp.y.p, s);
+    double2* res = sp.y.p;
+    switch (op) {
+      case PS_OP_RT: op_Rt(h, sp, sp.y.p, s); break;
+      case PS_OP_DINV: op_Dinv(h, sp, sp.y.p, sp.bo.p, s); res = sp.bo.p; break;
+      case PS_OP_R: op_R(h, sp, sp.y.p, sp.w.p, s); res = sp.w.p; break;
+      case PS_OP_ZF: op_ZF(h, sp, sp.y.p, sp.w.p, s); res = sp.w.p; break;
+      case PS_OP_U:
+        op_R(h, sp, sp.y.p, sp.w.p, s);
+        op_ZF(h, sp, sp.w.p, sp.bo.p, s);
+        op_Rt(h, sp, sp.bo.p, s);
+        op_Dinv(h, sp, sp.bo.p, sp.u.p, s);
+        res = sp.u.p;
+        break;
+    }
+    launch_permute_out(N, R, h->d_e2rwg.p, res, (double2*)Yout, N, s);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+    if (h->prof.on) h->prof.collect();
+  } catch (const PsError& e) {
+    return fail(h, e.st, "ps_apply: " + e.msg);
+  }
+  return PS_OK;
+}
+
+int ps_analyze(const char* path, double* out, int n) {
+  if (!path || !out || n <= 0) return -PS_EINVAL;
+  ps_handle h;
+  try {
+    std::vector<double2> near_arena, far_arena;
+    read_file(&h, path, near_arena, far_arena);
+    symbolic(&h);
+  } catch (const PsError& e) {
+    g_err = "ps_analyze: " + e.msg;
+    return -(int)e.st;
+  } catch (const std::bad_alloc&) {
+    g_err = "ps_analyze: host allocation failed";
+    return -PS_ENOMEM;
+  }
+  return ps_info(&h, out, n);
+}
+
+ps_status ps_profile(ps_handle* h, int enable) {
+  if (!h) return fail(nullptr, PS_EINVAL, "ps_profile: handle is NULL");
+  h->prof.on = enable != 0;
+  h->prof.reset();
+  return PS_OK;
+}
+
+int ps_profile_read(const ps_handle* h, double* out, int n) {
+  if (!h || !out) return 0;
+  int k = 0;
+  for (int c = 0; c < PC_COUNT && k + 4 <= n; ++c) {
+    out[k++] = h->prof.ms[c];
+    out[k++] = (double)h->prof.n[c];
+    out[k++] = h->prof.flops[c];
+    out[k++] = h->prof.bytes[c];
+  }
+  return k;
+}
+
+int64_t ps_n(const ps_handle* h) { return h ? h->N : -1; }
+
+const char* ps_last_error(const ps_handle* h) {
+  if (h) return h->err.c_str();
+  return g_err.c_str();
+}
+
+void ps_free(ps_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  h->plan.reset();
+  if (h->ev0) cudaEventDestroy(h->ev0);
+  if (h->ev1) cudaEventDestroy(h->ev1);
+  cudaStream_t s = h->stream;
+  delete h;
+  if (s) cudaStreamDestroy(s);
+}
+
+int ps_info(const ps_handle* h, double* out, int n) {
+  if (!h || !out || n <= 0) return 0;
+  double v[PS_INFO_COUNT];
+  double nR = 0, nD = 0, nF = 0;
+  for (int64_t p = 0; p < h->nl; ++p) {
+    nR += (double)h->nsz[p] * h->S[p];
+    nD += (double)h->nsz[p] * h->nsz[p];
+  }
+  for (int64_t b = 0; b < h->nfar; ++b) nF += (double)h->far_list[7 * b + 5] * (h->far_list[7 * b + 1] + h->far_list[7 * b + 3]);
+  v[PS_INFO_N] = (double)h->N;
+  v[PS_INFO_NLEAVES] = (double)h->nl;
+  v[PS_INFO_NNEAR] = (double)h->nnear;
+  v[PS_INFO_NFAR] = (double)h->nfar;
+  v[PS_INFO_ALPHA_BLOCKS] = (double)h->alpha_blocks;
+  v[PS_INFO_NR] = nR;
+  v[PS_INFO_ND] = nD;
+  v[PS_INFO_NF] = nF;
+  v[PS_INFO_HEIGHT] = h->max_height + 1;
+  v[PS_INFO_DEPTH] = h->max_depth + 1;
+  v[PS_INFO_SETUP_MADDS] = h->setup_madds;
+  v[PS_INFO_SETUP_DONE] = h->setup_done ? 1 : 0;
+  int m = std::min(n, (int)PS_INFO_COUNT);
+  std::memcpy(out, v, sizeof(double) * m);
+  return m;
+}
+
+int64_t ps_get_dinv(ps_handle* h, int64_t pos, void* out) {
+  if (!h || !out || pos < 0 || pos >= h->nl || !h->setup_done) return -1;
+  const int64_t n = h->nsz[pos];
+  if (cudaMemcpy(out, h->d_D.p + h->Doff[pos], 16 * n * n, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  return n;
+}
+
+int64_t ps_elim_leaf(const ps_handle* h, int64_t pos) {
+  if (!h || pos < 0 || pos >= h->nl) return -1;
+  return h->leaf_at[pos];
+}
+
+}  // extern "C"

@@ -1,0 +1,73 @@
+// ps_internal.h — structures shared by the host side (ps_host.cpp) and the
+// sm_100a kernels (ps_kernels.cu) of libps. Not part of the public ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ps {
+
+// One output block of the gathered batched complex GEMM ("gather-GEMM"):
+//   O(i,c) = [I(i,c)] + sign * sum_{t in [t0,t1)} sum_k A_t(i,k) B_t(k,c),
+// i < m, c < n. Every operand is addressed by (base pointer passed at launch)
+// + element offset + two element strides, so the same table serves several
+// buffers (e.g. both forward sweeps) and transposed views cost nothing.
+struct GTask {
+  int64_t oO, oI;          // element offsets into the O / I bases (oI < 0: no init)
+  int64_t sOi, sOc, sIi, sIc;
+  int32_t m, n;
+  int32_t t0, t1;
+  int32_t sign;
+  int32_t pad;
+};
+
+struct GTerm {
+  int64_t oA, oB;
+  int64_t sAi, sAk, sBk, sBc;
+  int32_t K;
+  int32_t pad;
+};
+
+struct GWork {             // one CTA: (task, row tile, column tile)
+  int32_t task, mt, nt;
+};
+
+// A batch = a contiguous range of work items launched as one kernel.
+struct Batch {
+  int64_t w0, nw;
+};
+
+// Tile geometry of the gather-GEMM kernel (ps_kernels.cu).
+constexpr int GM_MT = 32;
+constexpr int GM_NT = 32;
+
+// ---- kernel launchers (ps_kernels.cu) ----
+void launch_gemm(const GWork* work, int64_t nw, const GTask* tasks, const GTerm* terms,
+                 double2* Obase, const double2* Ibase, const double2* Abase,
+                 const double2* Bbase, cudaStream_t st);
+
+// Batched in-place Gauss-Jordan inversion with partial pivoting:
+// for each leaf l in [0,nl): src = Wbase + src_off[l] (n x n, ld = src_ld[l]),
+// dst = Dbase + dst_off[l] (n x n, ld n). status[l] = 1 if singular.
+void launch_inverse(int64_t nl, const int32_t* leaf_ids, const int32_t* sizes,
+                    const int64_t* src_off, const int64_t* src_ld, const int64_t* dst_off,
+                    const double2* Wbase, double2* Dbase, int32_t* status, int max_n,
+                    cudaStream_t st);
+
+// y[e*nrhs + c] = B[map[e] + c*ldb]   (gather rows of a column-major block)
+void launch_permute_in(int64_t N, int64_t nrhs, const int64_t* map, const double2* B, int64_t ldb,
+                       double2* y, cudaStream_t st);
+// X[map[e] + c*ldx] = y[e*nrhs + c]
+void launch_permute_out(int64_t N, int64_t nrhs, const int64_t* map, const double2* y, double2* X,
+                        int64_t ldx, cudaStream_t st);
+// dst[e*nrhs + c] = src[map[e]*nrhs + c]  (row permutation, row-major blocks)
+void launch_permute_rows(int64_t N, int64_t nrhs, const int64_t* map, const double2* src,
+                         double2* dst, cudaStream_t st);
+// xt = bo - u; part[chunk*nrhs + c] = (sum |bo|^2, sum |u|^2) over the chunk's rows
+void launch_combine_norms(int64_t N, int64_t nrhs, const double2* bo, const double2* u, double2* xt,
+                          double2* part, int64_t rows_per_chunk, cudaStream_t st);
+// norms[c] = (sqrt sum_chunks part.x, sqrt sum part.y)
+void launch_finalize_norms(int64_t nchunks, int64_t nrhs, const double2* part, double2* norms,
+                           cudaStream_t st);
+void launch_zero(double2* p, int64_t n, cudaStream_t st);
+
+}  // namespace ps

@@ -1,0 +1,354 @@
+// ps_kernels.cu — sm_100a kernels of libps (complex128 throughout).
+//
+// Every hot-path step of PAPER.md §III reduces to small dense complex block
+// products over leaf-cluster lists:
+//   * forward sweep  b~_j = b_j + sum_k alpha_kj^T b~_k      (Eq. 24, gather form)
+//   * D^{-1} apply   b_o = Z~_N^{-1} b~                     (Eq. 32)
+//   * backward sweep w_k = v_k + sum_j alpha_kj w_j          (Eq. 26)
+//   * far field      t = U (V^T w), two stages               (Eqs. 11, 13, 31)
+//   * setup          Z~_pj = Z_pj + sum_d alpha_dp^T Z~_dj   (Eq. 21, left-looking)
+//                    alpha_pj = -D_p^{-1} Z~_pj              (Eq. 16)
+// They all run through ONE gather-GEMM kernel driven by task/term tables built
+// on the host (ps_host.cpp); D_p^{-1} comes from a batched Gauss-Jordan kernel.
+// There are no float atomics: every output tile is owned by one CTA and its
+// terms are summed in a fixed order, so results are bitwise repeatable.
+//
+// FP64 note: tcgen05 has no f64 kind; complex128 products run on the DFMA pipe
+// (4 DFMA per complex multiply-add). DESIGN.md §Roofline derives the peak.
+#include "ps_internal.h"
+
+#include <cstdio>
+
+namespace ps {
+
+__device__ __forceinline__ void cfma(double2& acc, double2 a, double2 b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+}
+
+// ---------------------------------------------------------------------------
+// Gather-GEMM. CTA = 256 threads owns an MT x NT = 32 x 32 complex output tile;
+// each thread a 2 x 2 register tile (rows ty, ty+16; cols tx, tx+16). Operand
+// tiles (32 x KC and KC x 32) are staged in shared memory, loaded along the
+// operand's unit-stride dimension so global reads coalesce.
+constexpr int KC = 16;
+
+__global__ void __launch_bounds__(256)
+gemm_kernel(const GWork* __restrict__ work, const GTask* __restrict__ tasks,
+            const GTerm* __restrict__ terms, double2* __restrict__ Ob,
+            const double2* __restrict__ Ib, const double2* __restrict__ Ab,
+            const double2* __restrict__ Bb) {
+  __shared__ double2 As[KC][GM_MT + 1];
+  __shared__ double2 Bs[KC][GM_NT + 1];
+  const GWork w = work[blockIdx.x];
+  const GTask T = tasks[w.task];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int i0 = w.mt * GM_MT, c0 = w.nt * GM_NT;
+  const int mm = min(GM_MT, T.m - i0), nn = min(GM_NT, T.n - c0);
+  double2 acc[2][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) acc[a][b] = make_double2(0.0, 0.0);
+
+  for (int t = T.t0; t < T.t1; ++t) {
+    const GTerm tm = terms[t];
+    const double2* A = Ab + tm.oA + (int64_t)i0 * tm.sAi;
+    const double2* B = Bb + tm.oB + (int64_t)c0 * tm.sBc;
+    const bool a_unit_i = (tm.sAi == 1);
+    const bool b_unit_c = (tm.sBc == 1);
+    for (int k0 = 0; k0 < tm.K; k0 += KC) {
+      const int kk = min(KC, tm.K - k0);
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int e = tid + r * 256;
+        int i, k;
+        if (a_unit_i) { i = e & 31; k = e >> 5; } else { k = e & 15; i = e >> 4; }
+        double2 v = make_double2(0.0, 0.0);
+        if (i < mm && k < kk) v = __ldg(A + (int64_t)i * tm.sAi + (int64_t)(k0 + k) * tm.sAk);
+        As[k][i] = v;
+        int c;
+        if (b_unit_c) { c = e & 31; k = e >> 5; } else { k = e & 15; c = e >> 4; }
+        double2 u = make_double2(0.0, 0.0);
+        if (c < nn && k < kk) u = __ldg(B + (int64_t)(k0 + k) * tm.sBk + (int64_t)c * tm.sBc);
+        Bs[k][c] = u;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < KC; ++k) {
+        const double2 a0 = As[k][ty], a1 = As[k][ty + 16];
+        const double2 b0 = Bs[k][tx], b1 = Bs[k][tx + 16];
+        cfma(acc[0][0], a0, b0);
+        cfma(acc[0][1], a0, b1);
+        cfma(acc[1][0], a1, b0);
+        cfma(acc[1][1], a1, b1);
+      }
+      __syncthreads();
+    }
+  }
+  const double sg = (double)T.sign;
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const int i = ty + 16 * a, c = tx + 16 * b;
+      if (i < mm && c < nn) {
+        double2 v = make_double2(sg * acc[a][b].x, sg * acc[a][b].y);
+        if (T.oI >= 0) {
+          const double2 z = Ib[T.oI + (int64_t)(i0 + i) * T.sIi + (int64_t)(c0 + c) * T.sIc];
+          v.x += z.x;
+          v.y += z.y;
+        }
+        Ob[T.oO + (int64_t)(i0 + i) * T.sOi + (int64_t)(c0 + c) * T.sOc] = v;
+      }
+    }
+}
+
+void launch_gemm(const GWork* work, int64_t nw, const GTask* tasks, const GTerm* terms,
+                 double2* Obase, const double2* Ibase, const double2* Abase, const double2* Bbase,
+                 cudaStream_t st) {
+  if (nw <= 0) return;
+  gemm_kernel<<<(unsigned)nw, 256, 0, st>>>(work, tasks, terms, Obase, Ibase, Abase, Bbase);
+}
+
+// ---------------------------------------------------------------------------
+// Batched explicit inverse of the scaled diagonal blocks (Eqs. 23, 30):
+// in-place Gauss-Jordan with partial pivoting (max |z|^2, lowest row on ties),
+// one CTA per leaf. Blocks up to SMEM_N fit shared memory; larger ones are
+// eliminated in place in the destination buffer (L2-resident).
+constexpr int SMEM_N = 80;
+
+__global__ void __launch_bounds__(512)
+inverse_kernel(const int32_t* __restrict__ leaf_ids, const int32_t* __restrict__ sizes,
+               const int64_t* __restrict__ src_off, const int64_t* __restrict__ src_ld,
+               const int64_t* __restrict__ dst_off, const double2* __restrict__ Wb,
+               double2* __restrict__ Db, int32_t* __restrict__ status, int use_smem) {
+  extern __shared__ double2 sm[];
+  __shared__ double red_v[512];
+  __shared__ int red_i[512];
+  __shared__ double s_fro;
+  __shared__ int s_piv;
+  __shared__ int s_sing;
+  const int l = blockIdx.x;
+  const int n = sizes[l];
+  const int64_t ld_src = src_ld[l];
+  const double2* src = Wb + src_off[l];
+  double2* dst = Db + dst_off[l];
+  const bool in_smem = use_smem != 0;
+  double2* a = in_smem ? sm : dst;       // working matrix, column-major, ld n
+  double2* colk = in_smem ? sm + n * n : sm;  // column k factors (n)
+  int* piv = (int*)(colk + n);
+  const int tid = threadIdx.x, nt = blockDim.x;
+  double fro = 0.0;
+  for (int e = tid; e < n * n; e += nt) {
+    const int i = e % n, j = e / n;
+    const double2 v = src[i + (int64_t)j * ld_src];
+    a[e] = v;
+    fro += v.x * v.x + v.y * v.y;
+  }
+  red_v[tid] = fro;
+  __syncthreads();
+  for (int s = nt / 2; s > 0; s >>= 1) {
+    if (tid < s) red_v[tid] += red_v[tid + s];
+    __syncthreads();
+  }
+  if (tid == 0) { s_fro = sqrt(red_v[0]); s_sing = 0; }
+  __syncthreads();
+  const double tol2 = (1e-14 * s_fro) * (1e-14 * s_fro);
+  for (int k = 0; k < n; ++k) {
+    // pivot search in column k, rows k..n-1
+    double best = -1.0;
+    int bi = n;
+    for (int i = k + tid; i < n; i += nt) {
+      const double2 v = a[i + k * n];
+      const double m2 = v.x * v.x + v.y * v.y;
+      if (m2 > best) { best = m2; bi = i; }
+    }
+    red_v[tid] = best;
+    red_i[tid] = bi;
+    __syncthreads();
+    for (int s = nt / 2; s > 0; s >>= 1) {
+      if (tid < s) {
+        const double vo = red_v[tid + s];
+        const int io = red_i[tid + s];
+        if (vo > red_v[tid] || (vo == red_v[tid] && io < red_i[tid])) { red_v[tid] = vo; red_i[tid] = io; }
+      }
+      __syncthreads();
+    }
+    if (tid == 0) {
+      s_piv = red_i[0];
+      piv[k] = red_i[0];
+      if (!(red_v[0] > tol2)) s_sing = 1;
+    }
+    __syncthreads();
+    if (s_sing) break;
+    const int r = s_piv;
+    if (r != k)
+      for (int j = tid; j < n; j += nt) {
+        const double2 t = a[k + j * n];
+        a[k + j * n] = a[r + j * n];
+        a[r + j * n] = t;
+      }
+    __syncthreads();
+    const double2 p = a[k + k * n];
+    const double pm = p.x * p.x + p.y * p.y;
+    const double2 inv = make_double2(p.x / pm, -p.y / pm);
+    // column k factors (before the update), then scale row k
+    for (int i = tid; i < n; i += nt) colk[i] = a[i + k * n];
+    __syncthreads();
+    for (int j = tid; j < n; j += nt) {
+      double2 v = (j == k) ? make_double2(1.0, 0.0) : a[k + j * n];
+      a[k + j * n] = make_double2(v.x * inv.x - v.y * inv.y, v.x * inv.y + v.y * inv.x);
+    }
+    __syncthreads();
+    for (int e = tid; e < n * n; e += nt) {
+      const int i = e % n, j = e / n;
+      if (i == k) continue;
+      const double2 f = colk[i];
+      double2 base = (j == k) ? make_double2(0.0, 0.0) : a[e];
+      const double2 rk = a[k + j * n];
+      base.x -= f.x * rk.x - f.y * rk.y;
+      base.y -= f.x * rk.y + f.y * rk.x;
+      a[e] = base;
+    }
+    __syncthreads();
+  }
+  if (s_sing) {
+    if (tid == 0) status[l] = 1;
+    return;
+  }
+  // undo the row interchanges as column interchanges, in reverse order
+  for (int k = n - 1; k >= 0; --k) {
+    const int r = piv[k];
+    if (r != k)
+      for (int i = tid; i < n; i += nt) {
+        const double2 t = a[i + k * n];
+        a[i + k * n] = a[i + r * n];
+        a[i + r * n] = t;
+      }
+    __syncthreads();
+  }
+  if (in_smem)
+    for (int e = tid; e < n * n; e += nt) dst[e] = a[e];
+  if (tid == 0) status[l] = 0;
+}
+
+void launch_inverse(int64_t nl, const int32_t* leaf_ids, const int32_t* sizes, const int64_t* src_off,
+                    const int64_t* src_ld, const int64_t* dst_off, const double2* Wbase,
+                    double2* Dbase, int32_t* status, int max_n, cudaStream_t st) {
+  if (nl <= 0) return;
+  const int nn = max_n <= SMEM_N ? max_n : 0;
+  size_t smem = (size_t)nn * nn * sizeof(double2) + (size_t)max_n * sizeof(double2) +
+                (size_t)max_n * sizeof(int) + 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  inverse_kernel<<<(unsigned)nl, 512, smem, st>>>(leaf_ids, sizes, src_off, src_ld, dst_off, Wbase,
+                                                  Dbase, status, nn > 0 ? 1 : 0);
+}
+
+// ---------------------------------------------------------------------------
+// Permutations between the caller's RWG order (column-major N x nrhs) and the
+// internal leaf-row-major layout (row = unknown, nrhs contiguous complex).
+__global__ void permute_in_kernel(int64_t N, int64_t nrhs, const int64_t* __restrict__ map,
+                                  const double2* __restrict__ B, int64_t ldb, double2* __restrict__ y) {
+  const int64_t tot = N * nrhs;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / nrhs, c = e - r * nrhs;
+    y[e] = B[map[r] + c * ldb];
+  }
+}
+__global__ void permute_out_kernel(int64_t N, int64_t nrhs, const int64_t* __restrict__ map,
+                                   const double2* __restrict__ y, double2* __restrict__ X, int64_t ldx) {
+  const int64_t tot = N * nrhs;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / nrhs, c = e - r * nrhs;
+    X[map[r] + c * ldx] = y[e];
+  }
+}
+__global__ void permute_rows_kernel(int64_t N, int64_t nrhs, const int64_t* __restrict__ map,
+                                    const double2* __restrict__ src, double2* __restrict__ dst) {
+  const int64_t tot = N * nrhs;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / nrhs, c = e - r * nrhs;
+    dst[e] = src[map[r] * nrhs + c];
+  }
+}
+
+static unsigned grid_for(int64_t tot) {
+  int64_t g = (tot + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  return (unsigned)(g < 1 ? 1 : g);
+}
+
+void launch_permute_in(int64_t N, int64_t nrhs, const int64_t* map, const double2* B, int64_t ldb,
+                       double2* y, cudaStream_t st) {
+  permute_in_kernel<<<grid_for(N * nrhs), 256, 0, st>>>(N, nrhs, map, B, ldb, y);
+}
+void launch_permute_out(int64_t N, int64_t nrhs, const int64_t* map, const double2* y, double2* X,
+                        int64_t ldx, cudaStream_t st) {
+  permute_out_kernel<<<grid_for(N * nrhs), 256, 0, st>>>(N, nrhs, map, y, X, ldx);
+}
+void launch_permute_rows(int64_t N, int64_t nrhs, const int64_t* map, const double2* src,
+                         double2* dst, cudaStream_t st) {
+  permute_rows_kernel<<<grid_for(N * nrhs), 256, 0, st>>>(N, nrhs, map, src, dst);
+}
+
+// ---------------------------------------------------------------------------
+// x~ = b_o - u (Eq. 36) fused with the per-column squared norms of it_0 = b_o
+// and it_1 = u (Eq. 44). Deterministic two-stage reduction (fixed chunking).
+__global__ void combine_norms_kernel(int64_t N, int64_t nrhs, const double2* __restrict__ bo,
+                                     const double2* __restrict__ u, double2* __restrict__ xt,
+                                     double2* __restrict__ part, int64_t rpc) {
+  const int64_t c = blockIdx.y * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= nrhs) return;
+  const int64_t r0 = blockIdx.x * rpc, r1 = min(N, r0 + rpc);
+  double s0 = 0.0, s1 = 0.0;
+  for (int64_t r = r0; r < r1; ++r) {
+    const int64_t e = r * nrhs + c;
+    const double2 a = bo[e], b = u[e];
+    s0 += a.x * a.x + a.y * a.y;
+    s1 += b.x * b.x + b.y * b.y;
+    xt[e] = make_double2(a.x - b.x, a.y - b.y);
+  }
+  part[blockIdx.x * nrhs + c] = make_double2(s0, s1);
+}
+__global__ void finalize_norms_kernel(int64_t nch, int64_t nrhs, const double2* __restrict__ part,
+                                      double2* __restrict__ norms) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= nrhs) return;
+  double s0 = 0.0, s1 = 0.0;
+  for (int64_t k = 0; k < nch; ++k) {
+    const double2 p = part[k * nrhs + c];
+    s0 += p.x;
+    s1 += p.y;
+  }
+  norms[c] = make_double2(sqrt(s0), sqrt(s1));
+}
+void launch_combine_norms(int64_t N, int64_t nrhs, const double2* bo, const double2* u, double2* xt,
+                          double2* part, int64_t rpc, cudaStream_t st) {
+  dim3 g((unsigned)((N + rpc - 1) / rpc), (unsigned)((nrhs + 127) / 128));
+  combine_norms_kernel<<<g, 128, 0, st>>>(N, nrhs, bo, u, xt, part, rpc);
+}
+void launch_finalize_norms(int64_t nch, int64_t nrhs, const double2* part, double2* norms,
+                           cudaStream_t st) {
+  finalize_norms_kernel<<<(unsigned)((nrhs + 127) / 128), 128, 0, st>>>(nch, nrhs, part, norms);
+}
+
+__global__ void zero_kernel(double2* p, int64_t n) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    p[e] = make_double2(0.0, 0.0);
+}
+void launch_zero(double2* p, int64_t n, cudaStream_t st) {
+  if (n > 0) zero_kernel<<<grid_for(n), 256, 0, st>>>(p, n);
+}
+
+}  // namespace ps
