@@ -161,6 +161,8 @@ struct Table {
   }
   void add_term(int32_t task, int64_t oA, int64_t sAi, int64_t sAk, int64_t oB, int64_t sBk,
                 int64_t sBc, int K) {
+    if (task != (int32_t)tasks.size() - 1)
+      throw PsError{PS_ECUDA, "internal: terms must be added to the newest task"};
     GTerm g;
     g.oA = oA; g.sAi = sAi; g.sAk = sAk;
     g.oB = oB; g.sBk = sBk; g.sBc = sBc;
@@ -485,7 +487,17 @@ void build_setup_plan(ps_handle* h, SetupPlan& sp) {
       std::vector<int32_t> targets;
       targets.push_back(p);
       for (int32_t j : h->st[p]) targets.push_back(j);
-      std::map<int32_t, int32_t> task_of;
+      // terms of each target, from descendants d with p in struct(d), in increasing d
+      std::map<int32_t, std::vector<std::array<int64_t, 3>>> terms_of;  // j -> (oA, oB, nd)
+      for (auto [d, idx] : h->gath[p]) {
+        const int64_t nd = h->nsz[d];
+        const auto& sd = h->st[d];
+        const int64_t oA = h->Poff[d] + h->pcol[d][idx] * nd;   // alpha_dp (nd x np), transposed view
+        for (size_t jj = idx; jj < sd.size(); ++jj) {
+          const int64_t oB = h->Woff[d] + (nd + h->pcol[d][jj]) * nd;  // W_dj (nd x nj)
+          terms_of[sd[jj]].push_back({oA, oB, nd});
+        }
+      }
       for (int32_t j : targets) {
         const int64_t nj = h->nsz[j];
         const int32_t lj = h->leaf_at[j];
@@ -502,20 +514,11 @@ void build_setup_plan(ps_handle* h, SetupPlan& sp) {
         }
         const int64_t oO = h->Woff[p] + wcol(h, p, j) * np_;
         int32_t t = sp.asmb.add_task(oO, 1, np_, oI, sIi, sIc, (int)np_, (int)nj, +1);
-        task_of[j] = t;
+        auto tj = terms_of.find(j);
+        if (tj != terms_of.end())
+          for (auto& c : tj->second) sp.asmb.add_term(t, c[0], c[2], 1, c[1], 1, c[2], (int)c[2]);
+        sp.asmb.tile(t);
       }
-      // updates from descendants d with p in struct(d), in increasing d
-      for (auto [d, idx] : h->gath[p]) {
-        const int64_t nd = h->nsz[d];
-        const auto& sd = h->st[d];
-        const int64_t oA = h->Poff[d] + h->pcol[d][idx] * nd;   // alpha_dp (nd x np), transposed view
-        for (size_t jj = idx; jj < sd.size(); ++jj) {
-          const int32_t j = sd[jj];
-          const int64_t oB = h->Woff[d] + (nd + h->pcol[d][jj]) * nd;  // W_dj (nd x nj)
-          sp.asmb.add_term(task_of.at(j), oA, nd, 1, oB, 1, nd, (int)nd);
-        }
-      }
-      for (int32_t j : targets) sp.asmb.tile(task_of.at(j));
     }
     sp.asmb.close_batch();
     // panel: P_p = -Dinv_p W_p[:, n_p:]
