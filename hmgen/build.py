@@ -622,7 +622,7 @@ def write_hm(path: str, hd: HData) -> None:
         f.write(hdr)
         f.write(struct.pack("<Q", checksum64(hdr)))
         for s in sections:
-            mv = memoryview(s).cast("B")
+            mv = memoryview(s.reshape(-1).view(np.uint8)) if s.size else memoryview(b"")
             f.write(mv)
             pad = (-len(mv)) % 8
             if pad:

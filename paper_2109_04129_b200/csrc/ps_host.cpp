@@ -138,6 +138,9 @@ struct Prof {
 };
 
 // A gather-GEMM table: tasks, terms, work items and batches (one launch each).
+constexpr int KMAX = 128;          // longer terms are split (keeps split-K chunks balanced)
+constexpr int CHUNK_STEPS = 24;    // target k-steps (of GM_KC) per split-K work item
+
 struct Table {
   std::vector<GTask> tasks;
   std::vector<GTerm> terms;
@@ -146,7 +149,12 @@ struct Table {
   DevBuf<GTask> d_tasks;
   DevBuf<GTerm> d_terms;
   DevBuf<GWork> d_work;
+  DevBuf<int32_t> d_counters;
+  DevBuf<double2> d_partial;
   int64_t cur_batch_start = 0;
+  int32_t n_units = 0, n_tiles = 0;
+  int64_t n_slots = 0;
+  int chunk_steps = CHUNK_STEPS;
 
   int32_t add_task(int64_t oO, int64_t sOi, int64_t sOc, int64_t oI, int64_t sIi, int64_t sIc, int m,
                    int n, int sign) {
@@ -155,26 +163,49 @@ struct Table {
     t.oI = oI; t.sIi = sIi; t.sIc = sIc;
     t.m = m; t.n = n; t.sign = sign;
     t.t0 = t.t1 = (int32_t)terms.size();
-    t.pad = 0;
+    t.unit0 = 0; t.n_mt = (m + GM_MT - 1) / GM_MT; t.pad = 0;
     tasks.push_back(t);
     return (int32_t)tasks.size() - 1;
   }
   void add_term(int32_t task, int64_t oA, int64_t sAi, int64_t sAk, int64_t oB, int64_t sBk,
-                int64_t sBc, int K) {
+                int64_t sBc, int K, int32_t dep = -1) {
     if (task != (int32_t)tasks.size() - 1)
       throw PsError{PS_ECUDA, "internal: terms must be added to the newest task"};
-    GTerm g;
-    g.oA = oA; g.sAi = sAi; g.sAk = sAk;
-    g.oB = oB; g.sBk = sBk; g.sBc = sBc;
-    g.K = K; g.pad = 0;
-    terms.push_back(g);
+    for (int k0 = 0; k0 < K; k0 += KMAX) {
+      GTerm g;
+      g.oA = oA + (int64_t)k0 * sAk; g.sAi = sAi; g.sAk = sAk;
+      g.oB = oB + (int64_t)k0 * sBk; g.sBk = sBk; g.sBc = sBc;
+      g.K = std::min(KMAX, K - k0); g.dep = dep;
+      terms.push_back(g);
+    }
     tasks[task].t1 = (int32_t)terms.size();
   }
+  // work items of a task: every (mt, nt) tile, its terms split into chunks of
+  // ~chunk_steps k-steps (split-K); also assigns the task's completion units.
   void tile(int32_t task) {
-    const GTask& t = tasks[task];
-    int mt = (t.m + GM_MT - 1) / GM_MT, nt = (t.n + GM_NT - 1) / GM_NT;
-    for (int a = 0; a < mt; ++a)
-      for (int b = 0; b < nt; ++b) work.push_back({task, a, b});
+    GTask& t = tasks[task];
+    const int nmt = t.n_mt, nnt = (t.n + GM_NT - 1) / GM_NT;
+    t.unit0 = n_units;
+    n_units += nnt;
+    std::vector<int32_t> cut{t.t0};
+    int steps = 0;
+    for (int32_t k = t.t0; k < t.t1; ++k) {
+      steps += (terms[k].K + GM_KC - 1) / GM_KC;
+      if (steps >= chunk_steps && k + 1 < t.t1) {
+        cut.push_back(k + 1);
+        steps = 0;
+      }
+    }
+    cut.push_back(t.t1);
+    const int nch = (int)cut.size() - 1;
+    for (int a = 0; a < nmt; ++a)
+      for (int b = 0; b < nnt; ++b) {
+        const int32_t tile_id = n_tiles++;
+        const int64_t slot = nch > 1 ? n_slots : 0;
+        if (nch > 1) n_slots += nch;
+        for (int c = 0; c < nch; ++c)
+          work.push_back({task, a, b, cut[c], cut[c + 1], c, nch, tile_id, slot});
+      }
   }
   void close_batch() {
     int64_t n = (int64_t)work.size() - cur_batch_start;
@@ -192,13 +223,26 @@ struct Table {
     d_tasks.upload(tasks, st);
     d_terms.upload(terms, st);
     d_work.upload(work, st);
+    d_counters.alloc(1 + (int64_t)n_units + n_tiles);
+    d_partial.alloc(std::max<int64_t>(n_slots, 1) * GM_MT * GM_NT);
   }
   int64_t launch(int b, double2* O, const double2* I, const double2* A, const double2* B,
                  cudaStream_t st, Prof* pf = nullptr, int cls = 0) const {
     const Batch& bt = batches[b];
     if (bt.nw <= 0) return 0;
     if (pf) pf->begin(cls, st);
-    launch_gemm(d_work.p + bt.w0, bt.nw, d_tasks.p, d_terms.p, O, I, A, B, st);
+    CK(cudaMemsetAsync(d_counters.p, 0, sizeof(int32_t) * d_counters.n, st));
+    FlowArgs fa;
+    fa.work = d_work.p + bt.w0;
+    fa.nwork = bt.nw;
+    fa.tasks = d_tasks.p;
+    fa.terms = d_terms.p;
+    fa.O = O; fa.I = I; fa.A = A; fa.B = B;
+    fa.counters = d_counters.p;
+    fa.n_units = n_units;
+    fa.pad = 0;
+    fa.partial = d_partial.p;
+    launch_flow(fa, 0, st);
     if (pf) pf->end(st);
     return 1;
   }
@@ -571,6 +615,7 @@ void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
     byh[h->height[p]].push_back((int32_t)p);
     byd[h->depth[p]].push_back((int32_t)p);
   }
+  std::vector<int32_t> ftask(nl, -1), btask(nl, -1);
   for (int lev = 0; lev <= h->max_height; ++lev) {
     for (int32_t q : byh[lev]) {
       if (h->gath[q].empty()) continue;
@@ -578,13 +623,15 @@ void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
       int32_t t = sp.fwd.add_task(h->eoff[q] * R, R, 1, h->eoff[q] * R, R, 1, (int)nq, (int)R, +1);
       for (auto [d, idx] : h->gath[q]) {
         const int64_t nd = h->nsz[d];
-        sp.fwd.add_term(t, h->Poff[d] + h->pcol[d][idx] * nd, nd, 1, h->eoff[d] * R, R, 1, (int)nd);
+        sp.fwd.add_term(t, h->Poff[d] + h->pcol[d][idx] * nd, nd, 1, h->eoff[d] * R, R, 1, (int)nd,
+                        ftask[d]);
       }
       sp.fwd.tile(t);
+      ftask[q] = t;
     }
-    sp.fwd.close_batch();
   }
-  // backward sweep (Eq. 26), batches by depth: w_p = v_p + sum_j alpha_pj w_j
+  sp.fwd.close_batch();
+  // backward sweep (Eq. 26), ordered by depth: w_p = v_p + sum_j alpha_pj w_j
   for (int lev = 0; lev <= h->max_depth; ++lev) {
     for (int32_t p : byd[lev]) {
       const int64_t np_ = h->nsz[p];
@@ -592,12 +639,13 @@ void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
       for (size_t i = 0; i < h->st[p].size(); ++i) {
         const int32_t j = h->st[p][i];
         sp.bwd.add_term(t, h->Poff[p] + h->pcol[p][i] * np_, 1, np_, h->eoff[j] * R, R, 1,
-                        (int)h->nsz[j]);
+                        (int)h->nsz[j], btask[j]);
       }
       sp.bwd.tile(t);
+      btask[p] = t;
     }
-    sp.bwd.close_batch();
   }
+  sp.bwd.close_batch();
   // D^{-1} (Eq. 32), one batch
   for (int64_t p = 0; p < nl; ++p) {
     const int64_t np_ = h->nsz[p];

@@ -17,33 +17,54 @@ struct GTask {
   int32_t m, n;
   int32_t t0, t1;
   int32_t sign;
-  int32_t pad;
+  int32_t unit0;           // first completion counter of this task (one per column tile)
+  int32_t n_mt;            // row tiles: the task's column tile nt is complete when
+  int32_t pad;             //   done[unit0 + nt] == n_mt
 };
 
 struct GTerm {
   int64_t oA, oB;
   int64_t sAi, sAk, sBk, sBc;
   int32_t K;
+  int32_t dep;             // task (same launch) producing this term's B rows; -1: none
+};
+
+// One CTA-sized piece of work: output tile (mt, nt) of `task`, terms [ta, tb).
+// A tile whose terms are split into nchunks > 1 pieces (split-K) writes its
+// partial sums to slots [slot, slot + nchunks); the last piece to arrive
+// (counter arrive[tile]) adds them up in chunk order — deterministic.
+struct GWork {
+  int32_t task, mt, nt, ta, tb, chunk, nchunks, tile;
+  int64_t slot;
+};
+
+// Arguments of one persistent dataflow launch over work[0..nwork): items are
+// in topological order and fetched through a global ticket; an item waits
+// (acquire) until the tasks producing its B operands have completed its column tile.
+struct FlowArgs {
+  const GWork* work;
+  int64_t nwork;
+  const GTask* tasks;
+  const GTerm* terms;
+  double2* O;
+  const double2* I;
+  const double2* A;
+  const double2* B;
+  int32_t* counters;       // [0] ticket, [1 .. 1+n_units) done, then arrive[n_tiles]
+  int32_t n_units;
   int32_t pad;
-};
-
-struct GWork {             // one CTA: (task, row tile, column tile)
-  int32_t task, mt, nt;
-};
-
-// A batch = a contiguous range of work items launched as one kernel.
-struct Batch {
-  int64_t w0, nw;
+  double2* partial;        // split-K partial tiles, GM_MT * GM_NT each
 };
 
 // Tile geometry of the gather-GEMM kernel (ps_kernels.cu).
 constexpr int GM_MT = 32;
 constexpr int GM_NT = 32;
+constexpr int GM_KC = 16;
 
 // ---- kernel launchers (ps_kernels.cu) ----
-void launch_gemm(const GWork* work, int64_t nw, const GTask* tasks, const GTerm* terms,
-                 double2* Obase, const double2* Ibase, const double2* Abase,
-                 const double2* Bbase, cudaStream_t st);
+// grid <= 0: one persistent CTA per resident slot (148 SMs x occupancy).
+void launch_flow(const FlowArgs& a, int grid, cudaStream_t st);
+int flow_resident_ctas();
 
 // Batched in-place Gauss-Jordan inversion with partial pivoting:
 // for each leaf l in [0,nl): src = Wbase + src_off[l] (n x n, ld = src_ld[l]),

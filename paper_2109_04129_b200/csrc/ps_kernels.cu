@@ -29,89 +29,219 @@ __device__ __forceinline__ void cfma(double2& acc, double2 a, double2 b) {
 }
 
 // ---------------------------------------------------------------------------
-// Gather-GEMM. CTA = 256 threads owns an MT x NT = 32 x 32 complex output tile;
-// each thread a 2 x 2 register tile (rows ty, ty+16; cols tx, tx+16). Operand
-// tiles (32 x KC and KC x 32) are staged in shared memory, loaded along the
-// operand's unit-stride dimension so global reads coalesce.
-constexpr int KC = 16;
+// Gather-GEMM, persistent dataflow form.
+//
+// CTA = 256 threads; output tile MT x NT = 32 x 32 complex; each thread owns a
+// 2 x 2 register tile (rows ty, ty+16; cols tx, tx+16). Operand tiles (32 x KC
+// of A, KC x 32 of B) go through two shared-memory buffers: the global loads of
+// k-step s+1 are issued into registers before the FMAs of step s, so load
+// latency overlaps compute. Loads follow the operand's unit-stride dimension
+// (coalesced). A operands (operator panels) use the read-only path; B operands
+// and inits are produced inside the same launch by other CTAs, so they are read
+// with ld.global.cg (L2, never a stale L1 line).
+//
+// Scheduling: a CTA takes the next item from a global ticket (items are in
+// topological order), waits with ld.acquire until every task producing its B
+// rows has completed this column tile, computes, and publishes its tile with a
+// release (threadfence + atomic). Deadlock-free: an item only waits on items
+// with smaller tickets, which resident CTAs already hold.
+constexpr int KC = GM_KC;
 
-__global__ void __launch_bounds__(256)
-gemm_kernel(const GWork* __restrict__ work, const GTask* __restrict__ tasks,
-            const GTerm* __restrict__ terms, double2* __restrict__ Ob,
-            const double2* __restrict__ Ib, const double2* __restrict__ Ab,
-            const double2* __restrict__ Bb) {
-  __shared__ double2 As[KC][GM_MT + 1];
-  __shared__ double2 Bs[KC][GM_NT + 1];
-  const GWork w = work[blockIdx.x];
-  const GTask T = tasks[w.task];
-  const int tid = threadIdx.x;
-  const int tx = tid & 15, ty = tid >> 4;
-  const int i0 = w.mt * GM_MT, c0 = w.nt * GM_NT;
-  const int mm = min(GM_MT, T.m - i0), nn = min(GM_NT, T.n - c0);
-  double2 acc[2][2];
-#pragma unroll
-  for (int a = 0; a < 2; ++a)
-#pragma unroll
-    for (int b = 0; b < 2; ++b) acc[a][b] = make_double2(0.0, 0.0);
-
-  for (int t = T.t0; t < T.t1; ++t) {
-    const GTerm tm = terms[t];
-    const double2* A = Ab + tm.oA + (int64_t)i0 * tm.sAi;
-    const double2* B = Bb + tm.oB + (int64_t)c0 * tm.sBc;
-    const bool a_unit_i = (tm.sAi == 1);
-    const bool b_unit_c = (tm.sBc == 1);
-    for (int k0 = 0; k0 < tm.K; k0 += KC) {
-      const int kk = min(KC, tm.K - k0);
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const int e = tid + r * 256;
-        int i, k;
-        if (a_unit_i) { i = e & 31; k = e >> 5; } else { k = e & 15; i = e >> 4; }
-        double2 v = make_double2(0.0, 0.0);
-        if (i < mm && k < kk) v = __ldg(A + (int64_t)i * tm.sAi + (int64_t)(k0 + k) * tm.sAk);
-        As[k][i] = v;
-        int c;
-        if (b_unit_c) { c = e & 31; k = e >> 5; } else { k = e & 15; c = e >> 4; }
-        double2 u = make_double2(0.0, 0.0);
-        if (c < nn && k < kk) u = __ldg(B + (int64_t)(k0 + k) * tm.sBk + (int64_t)c * tm.sBc);
-        Bs[k][c] = u;
-      }
-      __syncthreads();
-#pragma unroll
-      for (int k = 0; k < KC; ++k) {
-        const double2 a0 = As[k][ty], a1 = As[k][ty + 16];
-        const double2 b0 = Bs[k][tx], b1 = Bs[k][tx + 16];
-        cfma(acc[0][0], a0, b0);
-        cfma(acc[0][1], a0, b1);
-        cfma(acc[1][0], a1, b0);
-        cfma(acc[1][1], a1, b1);
-      }
-      __syncthreads();
-    }
-  }
-  const double sg = (double)T.sign;
-#pragma unroll
-  for (int a = 0; a < 2; ++a)
-#pragma unroll
-    for (int b = 0; b < 2; ++b) {
-      const int i = ty + 16 * a, c = tx + 16 * b;
-      if (i < mm && c < nn) {
-        double2 v = make_double2(sg * acc[a][b].x, sg * acc[a][b].y);
-        if (T.oI >= 0) {
-          const double2 z = Ib[T.oI + (int64_t)(i0 + i) * T.sIi + (int64_t)(c0 + c) * T.sIc];
-          v.x += z.x;
-          v.y += z.y;
-        }
-        Ob[T.oO + (int64_t)(i0 + i) * T.sOi + (int64_t)(c0 + c) * T.sOc] = v;
-      }
-    }
+__device__ __forceinline__ int ld_acquire(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 
-void launch_gemm(const GWork* work, int64_t nw, const GTask* tasks, const GTerm* terms,
-                 double2* Obase, const double2* Ibase, const double2* Abase, const double2* Bbase,
-                 cudaStream_t st) {
-  if (nw <= 0) return;
-  gemm_kernel<<<(unsigned)nw, 256, 0, st>>>(work, tasks, terms, Obase, Ibase, Abase, Bbase);
+struct StepRegs {
+  double2 a[2], b[2];
+};
+
+__device__ __forceinline__ void fetch_step(const GTerm& tm, int k0, int i0, int c0, int mm, int nn,
+                                           const double2* __restrict__ Ab,
+                                           const double2* __restrict__ Bb, int tid, StepRegs& r) {
+  const int kk = min(KC, tm.K - k0);
+  const double2* A = Ab + tm.oA + (int64_t)i0 * tm.sAi + (int64_t)k0 * tm.sAk;
+  const double2* B = Bb + tm.oB + (int64_t)c0 * tm.sBc + (int64_t)k0 * tm.sBk;
+  const bool a_unit_i = (tm.sAi == 1);
+  const bool b_unit_c = (tm.sBc == 1);
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int e = tid + q * 256;
+    int i, k;
+    if (a_unit_i) { i = e & 31; k = e >> 5; } else { k = e & 15; i = e >> 4; }
+    r.a[q] = (i < mm && k < kk) ? __ldg(A + (int64_t)i * tm.sAi + (int64_t)k * tm.sAk)
+                                : make_double2(0.0, 0.0);
+    int c;
+    if (b_unit_c) { c = e & 31; k = e >> 5; } else { k = e & 15; c = e >> 4; }
+    r.b[q] = (c < nn && k < kk) ? __ldcg(B + (int64_t)k * tm.sBk + (int64_t)c * tm.sBc)
+                                : make_double2(0.0, 0.0);
+  }
+}
+
+__device__ __forceinline__ void store_step(const GTerm& tm, int tid, const StepRegs& r,
+                                           double2 (*As)[GM_MT + 1], double2 (*Bs)[GM_NT + 1]) {
+  const bool a_unit_i = (tm.sAi == 1);
+  const bool b_unit_c = (tm.sBc == 1);
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int e = tid + q * 256;
+    int i, k;
+    if (a_unit_i) { i = e & 31; k = e >> 5; } else { k = e & 15; i = e >> 4; }
+    As[k][i] = r.a[q];
+    int c;
+    if (b_unit_c) { c = e & 31; k = e >> 5; } else { k = e & 15; c = e >> 4; }
+    Bs[k][c] = r.b[q];
+  }
+}
+
+__global__ void __launch_bounds__(256)
+flow_kernel(const FlowArgs a) {
+  __shared__ double2 As[2][KC][GM_MT + 1];
+  __shared__ double2 Bs[2][KC][GM_NT + 1];
+  __shared__ int s_item, s_last;
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  int32_t* ticket = a.counters;
+  int32_t* done = a.counters + 1;
+  int32_t* arrive = a.counters + 1 + a.n_units;
+  for (;;) {
+    if (tid == 0) s_item = atomicAdd(ticket, 1);
+    __syncthreads();
+    const int64_t item = s_item;
+    if (item >= a.nwork) return;
+    const GWork w = a.work[item];
+    const GTask T = a.tasks[w.task];
+    const int i0 = w.mt * GM_MT, c0 = w.nt * GM_NT;
+    const int mm = min(GM_MT, T.m - i0), nn = min(GM_NT, T.n - c0);
+    // ---- wait for producers (warp 0, one term per lane) ----
+    if (tid < 32) {
+      for (int t = w.ta + tid; t < w.tb; t += 32) {
+        const int dep = a.terms[t].dep;
+        if (dep >= 0) {
+          const int32_t need = a.tasks[dep].n_mt;
+          const int32_t* flag = done + a.tasks[dep].unit0 + w.nt;
+          while (ld_acquire(flag) < need) __nanosleep(64);
+        }
+      }
+      __threadfence();
+    }
+    __syncthreads();
+    // ---- pipelined K loop over terms [ta, tb) ----
+    double2 acc[2][2];
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) acc[p][q] = make_double2(0.0, 0.0);
+    int t = w.ta, k0 = 0;
+    if (t < w.tb) {
+      GTerm tm = a.terms[t];
+      StepRegs r;
+      fetch_step(tm, 0, i0, c0, mm, nn, a.A, a.B, tid, r);
+      store_step(tm, tid, r, As[0], Bs[0]);
+      __syncthreads();
+      int cur = 0;
+      while (t < w.tb) {
+        int t2 = t, k2 = k0 + KC;
+        GTerm tm2 = tm;
+        if (k2 >= tm.K) {
+          t2 = t + 1;
+          k2 = 0;
+          if (t2 < w.tb) tm2 = a.terms[t2];
+        }
+        const bool nxt = t2 < w.tb;
+        if (nxt) fetch_step(tm2, k2, i0, c0, mm, nn, a.A, a.B, tid, r);
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+          const double2 a0 = As[cur][k][ty], a1 = As[cur][k][ty + 16];
+          const double2 b0 = Bs[cur][k][tx], b1 = Bs[cur][k][tx + 16];
+          cfma(acc[0][0], a0, b0);
+          cfma(acc[0][1], a0, b1);
+          cfma(acc[1][0], a1, b0);
+          cfma(acc[1][1], a1, b1);
+        }
+        if (nxt) store_step(tm2, tid, r, As[cur ^ 1], Bs[cur ^ 1]);
+        __syncthreads();
+        cur ^= 1;
+        t = t2;
+        k0 = k2;
+        tm = tm2;
+      }
+    }
+    // ---- split-K: publish the partial; the last chunk reduces in chunk order ----
+    bool finalize = true;
+    if (w.nchunks > 1) {
+      double2* P = a.partial + (w.slot + w.chunk) * (int64_t)(GM_MT * GM_NT);
+#pragma unroll
+      for (int p = 0; p < 2; ++p)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) P[(ty + 16 * p) * GM_NT + tx + 16 * q] = acc[p][q];
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) s_last = (atomicAdd(arrive + w.tile, 1) == w.nchunks - 1);
+      __syncthreads();
+      finalize = s_last;
+      if (finalize) {
+        __threadfence();
+#pragma unroll
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) acc[p][q] = make_double2(0.0, 0.0);
+        for (int c = 0; c < w.nchunks; ++c) {
+          const double2* Q = a.partial + (w.slot + c) * (int64_t)(GM_MT * GM_NT);
+#pragma unroll
+          for (int p = 0; p < 2; ++p)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const double2 v = __ldcg(Q + (ty + 16 * p) * GM_NT + tx + 16 * q);
+              acc[p][q].x += v.x;
+              acc[p][q].y += v.y;
+            }
+        }
+      }
+    }
+    if (finalize) {
+      const double sg = (double)T.sign;
+#pragma unroll
+      for (int p = 0; p < 2; ++p)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int i = ty + 16 * p, c = tx + 16 * q;
+          if (i < mm && c < nn) {
+            double2 v = make_double2(sg * acc[p][q].x, sg * acc[p][q].y);
+            if (T.oI >= 0) {
+              const double2 z = __ldcg(a.I + T.oI + (int64_t)(i0 + i) * T.sIi + (int64_t)(c0 + c) * T.sIc);
+              v.x += z.x;
+              v.y += z.y;
+            }
+            a.O[T.oO + (int64_t)(i0 + i) * T.sOi + (int64_t)(c0 + c) * T.sOc] = v;
+          }
+        }
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) atomicAdd(done + T.unit0 + w.nt, 1);
+    }
+    __syncthreads();
+  }
+}
+
+int flow_resident_ctas() {
+  static int n = 0;
+  if (n == 0) {
+    int per_sm = 0, dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, flow_kernel, 256, 0);
+    n = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  return n;
+}
+
+void launch_flow(const FlowArgs& a, int grid, cudaStream_t st) {
+  if (a.nwork <= 0) return;
+  int g = grid > 0 ? grid : flow_resident_ctas();
+  if (g > a.nwork) g = (int)a.nwork;
+  flow_kernel<<<g, 256, 0, st>>>(a);
 }
 
 // ---------------------------------------------------------------------------
