@@ -59,9 +59,9 @@ def load_library():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(_SO) or os.environ.get("PS_REBUILD"):
-        from .build import build
-        build()
+    from .build import build, nvcc_available
+    if nvcc_available():
+        build(force=bool(os.environ.get("PS_REBUILD")))     # no-op unless sources are newer
     if not os.path.exists(_SO):
         raise ImportError(f"libps.so not found at {_SO}; run `python -m paper_2109_04129_b200.build`")
     L = ctypes.CDLL(_SO)

@@ -15,6 +15,10 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", 
               "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--shared"]
 
 
+def nvcc_available() -> bool:
+    return os.path.exists(os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc"))
+
+
 def _stale() -> bool:
     if not os.path.exists(SO):
         return True

@@ -38,6 +38,11 @@ struct GWork {
   int64_t slot;
 };
 
+// A batch = a contiguous range of work items launched as one kernel.
+struct Batch {
+  int64_t w0, nw;
+};
+
 // Arguments of one persistent dataflow launch over work[0..nwork): items are
 // in topological order and fetched through a global ticket; an item waits
 // (acquire) until the tasks producing its B operands have completed its column tile.
