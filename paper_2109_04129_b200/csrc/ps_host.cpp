@@ -137,8 +137,7 @@ struct Prof {
   }
 };
 
-// A gather-GEMM table: tasks, terms, work items and batches (one launch each).
-constexpr int KMAX = 128;          // longer terms are split (keeps split-K chunks balanced)
+// A gather-GEMM table: tasks, segments, work items and batches (one launch each).
 constexpr int CHUNK_STEPS = 24;    // target k-steps (of GM_KC) per split-K work item
 
 struct Table {
@@ -163,48 +162,68 @@ struct Table {
     t.oI = oI; t.sIi = sIi; t.sIc = sIc;
     t.m = m; t.n = n; t.sign = sign;
     t.t0 = t.t1 = (int32_t)terms.size();
-    t.unit0 = 0; t.n_mt = (m + GM_MT - 1) / GM_MT; t.pad = 0;
+    t.K = 0;
+    t.unit0 = 0; t.n_mt = (m + GM_MT - 1) / GM_MT;
+    t.a_kmajor = 0; t.b_kmajor = 0; t.pad = 0;
     tasks.push_back(t);
     return (int32_t)tasks.size() - 1;
   }
+  // append a K-segment: A(i,k) = A[oA + k sAk + i sAi], B(k,c) = B[oB + k sBk + c sBc]
   void add_term(int32_t task, int64_t oA, int64_t sAi, int64_t sAk, int64_t oB, int64_t sBk,
                 int64_t sBc, int K, int32_t dep = -1) {
     if (task != (int32_t)tasks.size() - 1)
       throw PsError{PS_ECUDA, "internal: terms must be added to the newest task"};
-    for (int k0 = 0; k0 < K; k0 += KMAX) {
-      GTerm g;
-      g.oA = oA + (int64_t)k0 * sAk; g.sAi = sAi; g.sAk = sAk;
-      g.oB = oB + (int64_t)k0 * sBk; g.sBk = sBk; g.sBc = sBc;
-      g.K = std::min(KMAX, K - k0); g.dep = dep;
-      terms.push_back(g);
+    if (K <= 0) return;
+    GTask& t = tasks[task];
+    if (t.t1 == t.t0) {
+      t.a_kmajor = (sAi != 1) ? 1 : 0;
+      t.b_kmajor = (sBc != 1) ? 1 : 0;
     }
-    tasks[task].t1 = (int32_t)terms.size();
+    GTerm g;
+    g.oA = oA; g.sAi = sAi; g.sAk = sAk;
+    g.oB = oB; g.sBk = sBk; g.sBc = sBc;
+    g.kstart = t.K; g.K = K; g.dep = dep; g.pad = 0;
+    terms.push_back(g);
+    t.K += K;
+    t.t1 = (int32_t)terms.size();
   }
-  // work items of a task: every (mt, nt) tile, its terms split into chunks of
-  // ~chunk_steps k-steps (split-K); also assigns the task's completion units.
+  // work items of a task: every (mt, nt) tile, its virtual K split into chunks
+  // of ~chunk_steps k-steps (split-K); also assigns the task's completion units.
   void tile(int32_t task) {
     GTask& t = tasks[task];
     const int nmt = t.n_mt, nnt = (t.n + GM_NT - 1) / GM_NT;
     t.unit0 = n_units;
     n_units += nnt;
-    std::vector<int32_t> cut{t.t0};
-    int steps = 0;
-    for (int32_t k = t.t0; k < t.t1; ++k) {
-      steps += (terms[k].K + GM_KC - 1) / GM_KC;
-      if (steps >= chunk_steps && k + 1 < t.t1) {
-        cut.push_back(k + 1);
-        steps = 0;
+    // chunk boundaries in virtual k (multiples of GM_KC), <= GM_CHUNK_K k's and <= GM_MAXSEG segments
+    std::vector<std::array<int32_t, 4>> ch;   // (ka, kb, ta, tb)
+    const int target = std::min(chunk_steps * GM_KC, GM_CHUNK_K);
+    int32_t ka = 0, ta = t.t0;
+    while (ka < t.K || ch.empty()) {
+      int32_t kb = std::min(t.K, ka + target);
+      // segments overlapping [ka, kb)
+      int32_t tb = ta;
+      while (tb < t.t1 && terms[tb].kstart < kb) ++tb;
+      if (tb - ta > GM_MAXSEG) {          // too many tiny segments: stop earlier
+        tb = ta + GM_MAXSEG;
+        kb = terms[tb - 1].kstart + terms[tb - 1].K;
+        kb = ka + std::max<int32_t>(GM_KC, ((kb - ka) / GM_KC) * GM_KC);
+        kb = std::min(kb, t.K);
+        tb = ta;
+        while (tb < t.t1 && terms[tb].kstart < kb) ++tb;
       }
+      ch.push_back({ka, kb, ta, tb});
+      if (kb >= t.K) break;
+      ka = kb;
+      while (ta < t.t1 && terms[ta].kstart + terms[ta].K <= ka) ++ta;
     }
-    cut.push_back(t.t1);
-    const int nch = (int)cut.size() - 1;
+    const int nch = (int)ch.size();
     for (int a = 0; a < nmt; ++a)
       for (int b = 0; b < nnt; ++b) {
         const int32_t tile_id = n_tiles++;
         const int64_t slot = nch > 1 ? n_slots : 0;
         if (nch > 1) n_slots += nch;
         for (int c = 0; c < nch; ++c)
-          work.push_back({task, a, b, cut[c], cut[c + 1], c, nch, tile_id, slot});
+          work.push_back({task, a, b, ch[c][2], ch[c][3], ch[c][0], ch[c][1], c, nch, tile_id, slot});
       }
   }
   void close_batch() {

@@ -15,26 +15,34 @@ struct GTask {
   int64_t oO, oI;          // element offsets into the O / I bases (oI < 0: no init)
   int64_t sOi, sOc, sIi, sIc;
   int32_t m, n;
-  int32_t t0, t1;
+  int32_t t0, t1;          // segment range
+  int32_t K;               // total (virtual) K = sum of segment lengths
   int32_t sign;
   int32_t unit0;           // first completion counter of this task (one per column tile)
-  int32_t n_mt;            // row tiles: the task's column tile nt is complete when
-  int32_t pad;             //   done[unit0 + nt] == n_mt
+  int32_t n_mt;            // row tiles: column tile nt is complete when done[unit0+nt] == n_mt
+  int32_t a_kmajor;        // 1: A's unit stride is along k (transposed views), 0: along i
+  int32_t b_kmajor;        // 1: B's unit stride is along k, 0: along c
+  int32_t pad;
 };
 
+// A segment of a task's K dimension: K_s consecutive k's starting at virtual
+// position kstart; A(i, k) = A[oA + (k - kstart) sAk + i sAi],
+// B(k, c) = B[oB + (k - kstart) sBk + c sBc].
 struct GTerm {
   int64_t oA, oB;
   int64_t sAi, sAk, sBk, sBc;
-  int32_t K;
-  int32_t dep;             // task (same launch) producing this term's B rows; -1: none
+  int32_t kstart, K;
+  int32_t dep;             // task (same launch) producing this segment's B rows; -1: none
+  int32_t pad;
 };
 
-// One CTA-sized piece of work: output tile (mt, nt) of `task`, terms [ta, tb).
-// A tile whose terms are split into nchunks > 1 pieces (split-K) writes its
-// partial sums to slots [slot, slot + nchunks); the last piece to arrive
-// (counter arrive[tile]) adds them up in chunk order — deterministic.
+// One CTA-sized piece of work: output tile (mt, nt) of `task`, virtual k in
+// [ka, kb) touching segments [ta, tb). A tile whose K is split into
+// nchunks > 1 pieces (split-K) writes partial sums to slots
+// [slot, slot + nchunks); the last piece to arrive (counter arrive[tile]) adds
+// them up in chunk order — deterministic.
 struct GWork {
-  int32_t task, mt, nt, ta, tb, chunk, nchunks, tile;
+  int32_t task, mt, nt, ta, tb, ka, kb, chunk, nchunks, tile;
   int64_t slot;
 };
 
@@ -65,6 +73,8 @@ struct FlowArgs {
 constexpr int GM_MT = 32;
 constexpr int GM_NT = 32;
 constexpr int GM_KC = 16;
+constexpr int GM_CHUNK_K = 512;   // max virtual k per work item (shared-memory k tables)
+constexpr int GM_MAXSEG = 96;     // max segments per work item
 
 // ---- kernel launchers (ps_kernels.cu) ----
 // grid <= 0: one persistent CTA per resident slot (148 SMs x occupancy).

@@ -57,48 +57,55 @@ struct StepRegs {
   double2 a[2], b[2];
 };
 
-__device__ __forceinline__ void fetch_step(const GTerm& tm, int k0, int i0, int c0, int mm, int nn,
+// Shared per-item k tables: for the item's virtual k range [ka, kb) the A
+// column base, A row stride and B row base of every k (built from the
+// segment list at item start), so k-steps run densely across segments.
+struct KTab {
+  int64_t kA[GM_CHUNK_K];
+  int64_t kB[GM_CHUNK_K];
+  int32_t kSi[GM_CHUNK_K];
+  int32_t kSc[GM_CHUNK_K];
+};
+
+__device__ __forceinline__ void fetch_step(const KTab& kt, int k0, int klen, int i0, int c0, int mm,
+                                           int nn, bool a_km, bool b_km,
                                            const double2* __restrict__ Ab,
                                            const double2* __restrict__ Bb, int tid, StepRegs& r) {
-  const int kk = min(KC, tm.K - k0);
-  const double2* A = Ab + tm.oA + (int64_t)i0 * tm.sAi + (int64_t)k0 * tm.sAk;
-  const double2* B = Bb + tm.oB + (int64_t)c0 * tm.sBc + (int64_t)k0 * tm.sBk;
-  const bool a_unit_i = (tm.sAi == 1);
-  const bool b_unit_c = (tm.sBc == 1);
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
     const int e = tid + q * 256;
     int i, k;
-    if (a_unit_i) { i = e & 31; k = e >> 5; } else { k = e & 15; i = e >> 4; }
-    r.a[q] = (i < mm && k < kk) ? __ldg(A + (int64_t)i * tm.sAi + (int64_t)k * tm.sAk)
-                                : make_double2(0.0, 0.0);
+    if (a_km) { k = e & 15; i = e >> 4; } else { i = e & 31; k = e >> 5; }
+    const int kk = k0 + k;
+    r.a[q] = (i < mm && kk < klen) ? __ldg(Ab + kt.kA[kk] + (int64_t)(i0 + i) * kt.kSi[kk])
+                                   : make_double2(0.0, 0.0);
     int c;
-    if (b_unit_c) { c = e & 31; k = e >> 5; } else { k = e & 15; c = e >> 4; }
-    r.b[q] = (c < nn && k < kk) ? __ldcg(B + (int64_t)k * tm.sBk + (int64_t)c * tm.sBc)
-                                : make_double2(0.0, 0.0);
+    if (b_km) { k = e & 15; c = e >> 4; } else { c = e & 31; k = e >> 5; }
+    const int kb = k0 + k;
+    r.b[q] = (c < nn && kb < klen) ? __ldcg(Bb + kt.kB[kb] + (int64_t)(c0 + c) * kt.kSc[kb])
+                                   : make_double2(0.0, 0.0);
   }
 }
 
-__device__ __forceinline__ void store_step(const GTerm& tm, int tid, const StepRegs& r,
+__device__ __forceinline__ void store_step(bool a_km, bool b_km, int tid, const StepRegs& r,
                                            double2 (*As)[GM_MT + 1], double2 (*Bs)[GM_NT + 1]) {
-  const bool a_unit_i = (tm.sAi == 1);
-  const bool b_unit_c = (tm.sBc == 1);
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
     const int e = tid + q * 256;
     int i, k;
-    if (a_unit_i) { i = e & 31; k = e >> 5; } else { k = e & 15; i = e >> 4; }
+    if (a_km) { k = e & 15; i = e >> 4; } else { i = e & 31; k = e >> 5; }
     As[k][i] = r.a[q];
     int c;
-    if (b_unit_c) { c = e & 31; k = e >> 5; } else { k = e & 15; c = e >> 4; }
+    if (b_km) { k = e & 15; c = e >> 4; } else { c = e & 31; k = e >> 5; }
     Bs[k][c] = r.b[q];
   }
 }
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)
 flow_kernel(const FlowArgs a) {
   __shared__ double2 As[2][KC][GM_MT + 1];
   __shared__ double2 Bs[2][KC][GM_NT + 1];
+  __shared__ KTab kt;
   __shared__ int s_item, s_last;
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
@@ -114,7 +121,20 @@ flow_kernel(const FlowArgs a) {
     const GTask T = a.tasks[w.task];
     const int i0 = w.mt * GM_MT, c0 = w.nt * GM_NT;
     const int mm = min(GM_MT, T.m - i0), nn = min(GM_NT, T.n - c0);
-    // ---- wait for producers (warp 0, one term per lane) ----
+    const int klen = w.kb - w.ka;
+    // ---- k tables of this item (segments [ta, tb) clipped to [ka, kb)) ----
+    for (int t = w.ta + tid; t < w.tb; t += 256) {
+      const GTerm g = a.terms[t];
+      const int lo = max(g.kstart, w.ka), hi = min(g.kstart + g.K, w.kb);
+      for (int k = lo; k < hi; ++k) {
+        const int64_t d = k - g.kstart;
+        kt.kA[k - w.ka] = g.oA + d * g.sAk;
+        kt.kB[k - w.ka] = g.oB + d * g.sBk;
+        kt.kSi[k - w.ka] = (int32_t)g.sAi;
+        kt.kSc[k - w.ka] = (int32_t)g.sBc;
+      }
+    }
+    // ---- wait for producers (warp 0, one segment per lane) ----
     if (tid < 32) {
       for (int t = w.ta + tid; t < w.tb; t += 32) {
         const int dep = a.terms[t].dep;
@@ -127,30 +147,22 @@ flow_kernel(const FlowArgs a) {
       __threadfence();
     }
     __syncthreads();
-    // ---- pipelined K loop over terms [ta, tb) ----
+    // ---- pipelined, dense k-steps ----
     double2 acc[2][2];
 #pragma unroll
     for (int p = 0; p < 2; ++p)
 #pragma unroll
       for (int q = 0; q < 2; ++q) acc[p][q] = make_double2(0.0, 0.0);
-    int t = w.ta, k0 = 0;
-    if (t < w.tb) {
-      GTerm tm = a.terms[t];
+    const bool a_km = T.a_kmajor != 0, b_km = T.b_kmajor != 0;
+    if (klen > 0) {
       StepRegs r;
-      fetch_step(tm, 0, i0, c0, mm, nn, a.A, a.B, tid, r);
-      store_step(tm, tid, r, As[0], Bs[0]);
+      fetch_step(kt, 0, klen, i0, c0, mm, nn, a_km, b_km, a.A, a.B, tid, r);
+      store_step(a_km, b_km, tid, r, As[0], Bs[0]);
       __syncthreads();
       int cur = 0;
-      while (t < w.tb) {
-        int t2 = t, k2 = k0 + KC;
-        GTerm tm2 = tm;
-        if (k2 >= tm.K) {
-          t2 = t + 1;
-          k2 = 0;
-          if (t2 < w.tb) tm2 = a.terms[t2];
-        }
-        const bool nxt = t2 < w.tb;
-        if (nxt) fetch_step(tm2, k2, i0, c0, mm, nn, a.A, a.B, tid, r);
+      for (int k0 = 0; k0 < klen; k0 += KC) {
+        const bool nxt = k0 + KC < klen;
+        if (nxt) fetch_step(kt, k0 + KC, klen, i0, c0, mm, nn, a_km, b_km, a.A, a.B, tid, r);
 #pragma unroll
         for (int k = 0; k < KC; ++k) {
           const double2 a0 = As[cur][k][ty], a1 = As[cur][k][ty + 16];
@@ -160,12 +172,9 @@ flow_kernel(const FlowArgs a) {
           cfma(acc[1][0], a1, b0);
           cfma(acc[1][1], a1, b1);
         }
-        if (nxt) store_step(tm2, tid, r, As[cur ^ 1], Bs[cur ^ 1]);
+        if (nxt) store_step(a_km, b_km, tid, r, As[cur ^ 1], Bs[cur ^ 1]);
         __syncthreads();
         cur ^= 1;
-        t = t2;
-        k0 = k2;
-        tm = tm2;
       }
     }
     // ---- split-K: publish the partial; the last chunk reduces in chunk order ----
