@@ -138,7 +138,7 @@ struct Prof {
 };
 
 // A gather-GEMM table: tasks, segments, work items and batches (one launch each).
-constexpr int CHUNK_STEPS = 24;    // target k-steps (of GM_KC) per split-K work item
+constexpr int CHUNK_STEPS = 16;    // target k-steps (of GM_KC) per split-K work item
 
 struct Table {
   std::vector<GTask> tasks;
@@ -189,33 +189,53 @@ struct Table {
   }
   // work items of a task: every (mt, nt) tile, its virtual K split into chunks
   // of ~chunk_steps k-steps (split-K); also assigns the task's completion units.
-  void tile(int32_t task) {
-    GTask& t = tasks[task];
-    const int nmt = t.n_mt, nnt = (t.n + GM_NT - 1) / GM_NT;
-    t.unit0 = n_units;
-    n_units += nnt;
-    // chunk boundaries in virtual k (multiples of GM_KC), <= GM_CHUNK_K k's and <= GM_MAXSEG segments
-    std::vector<std::array<int32_t, 4>> ch;   // (ka, kb, ta, tb)
+  // chunks (ka, kb, ta, tb) covering virtual k in [k_lo, k_hi) = segments [s0, s1)
+  void chunk_range(int32_t s0, int32_t s1, std::vector<std::array<int32_t, 4>>& ch) const {
+    if (s0 >= s1) return;
+    const int32_t k_lo = terms[s0].kstart, k_hi = terms[s1 - 1].kstart + terms[s1 - 1].K;
     const int target = std::min(chunk_steps * GM_KC, GM_CHUNK_K);
-    int32_t ka = 0, ta = t.t0;
-    while (ka < t.K || ch.empty()) {
-      int32_t kb = std::min(t.K, ka + target);
-      // segments overlapping [ka, kb)
+    int32_t ka = k_lo, ta = s0;
+    while (ka < k_hi) {
+      int32_t kb = std::min(k_hi, ka + target);
       int32_t tb = ta;
-      while (tb < t.t1 && terms[tb].kstart < kb) ++tb;
+      while (tb < s1 && terms[tb].kstart < kb) ++tb;
       if (tb - ta > GM_MAXSEG) {          // too many tiny segments: stop earlier
         tb = ta + GM_MAXSEG;
         kb = terms[tb - 1].kstart + terms[tb - 1].K;
         kb = ka + std::max<int32_t>(GM_KC, ((kb - ka) / GM_KC) * GM_KC);
-        kb = std::min(kb, t.K);
+        kb = std::min(kb, k_hi);
         tb = ta;
-        while (tb < t.t1 && terms[tb].kstart < kb) ++tb;
+        while (tb < s1 && terms[tb].kstart < kb) ++tb;
       }
       ch.push_back({ka, kb, ta, tb});
-      if (kb >= t.K) break;
       ka = kb;
-      while (ta < t.t1 && terms[ta].kstart + terms[ta].K <= ka) ++ta;
+      while (ta < s1 && terms[ta].kstart + terms[ta].K <= ka) ++ta;
     }
+  }
+  // Work items of a task: every (mt, nt) tile, its virtual K split into chunks
+  // of ~chunk_steps k-steps (split-K); also assigns the task's completion units.
+  // isolate = +1 / -1 puts the first / last segment (the dependency expected to
+  // complete last: the parent in the backward sweep, the last child in the
+  // forward sweep) in a chunk of its own, so a chain hop waits on a short chunk.
+  void tile(int32_t task, int isolate = 0) {
+    GTask& t = tasks[task];
+    const int nmt = t.n_mt, nnt = (t.n + GM_NT - 1) / GM_NT;
+    t.unit0 = n_units;
+    n_units += nnt;
+    std::vector<std::array<int32_t, 4>> ch;   // (ka, kb, ta, tb)
+    const int nseg = t.t1 - t.t0;
+    if (isolate != 0 && nseg >= 2) {
+      if (isolate > 0) {
+        chunk_range(t.t0, t.t0 + 1, ch);
+        chunk_range(t.t0 + 1, t.t1, ch);
+      } else {
+        chunk_range(t.t0, t.t1 - 1, ch);
+        chunk_range(t.t1 - 1, t.t1, ch);
+      }
+    } else {
+      chunk_range(t.t0, t.t1, ch);
+    }
+    if (ch.empty()) ch.push_back({0, 0, t.t0, t.t0});
     const int nch = (int)ch.size();
     for (int a = 0; a < nmt; ++a)
       for (int b = 0; b < nnt; ++b) {
@@ -310,6 +330,11 @@ struct ps_handle {
   int64_t Wlen = 0, Plen = 0, Dlen = 0;
   int max_height = 0, max_depth = 0;
   std::vector<int64_t> e2rwg, e2mort, m2e;
+  // far field restacked per cluster (Morton range): S_c = [factor^T of every
+  // block side whose rows are cluster c] (sum_r x len, column-major)
+  std::vector<int64_t> cl_start, cl_len, cl_sr, cl_soff;
+  std::vector<int64_t> fb_ct, fb_cs, fb_rbt, fb_rbs;   // per block: clusters, row offsets in stacks
+  int64_t stack_len = 0;
   double setup_madds = 0;
   int64_t alpha_blocks = 0;
   // near block lookup: (leaf a, leaf b) -> index into near_list
@@ -520,6 +545,57 @@ void symbolic(ps_handle* h) {
   }
 }
 
+// Restack the far factors per cluster (DESIGN.md §Far field): block b ~ U V^T
+// with rows t = [r0, r0+m), cols s = [c0, c0+n) contributes U^T (r x m) to the
+// stack of t and V^T (r x n) to the stack of s. Stage 1 is then one GEMM per
+// cluster, S_c w_c, and stage 2 reads U/V rows from the same stacks.
+void far_layout(ps_handle* h, const std::vector<double2>& far_arena, std::vector<double2>& stacked) {
+  std::map<std::pair<int64_t, int64_t>, int64_t> cid;
+  auto get = [&](int64_t a, int64_t l) {
+    auto it = cid.find({a, l});
+    if (it != cid.end()) return it->second;
+    int64_t id = (int64_t)h->cl_start.size();
+    cid[{a, l}] = id;
+    h->cl_start.push_back(a);
+    h->cl_len.push_back(l);
+    h->cl_sr.push_back(0);
+    return id;
+  };
+  const int64_t nf = h->nfar;
+  h->fb_ct.assign(nf, 0); h->fb_cs.assign(nf, 0); h->fb_rbt.assign(nf, 0); h->fb_rbs.assign(nf, 0);
+  for (int64_t b = 0; b < nf; ++b) {
+    const int64_t* F = &h->far_list[7 * b];
+    const int64_t t = get(F[0], F[1]), c = get(F[2], F[3]), r = F[5];
+    h->fb_ct[b] = t;
+    h->fb_cs[b] = c;
+    h->fb_rbt[b] = h->cl_sr[t];
+    h->cl_sr[t] += r;
+    h->fb_rbs[b] = h->cl_sr[c];
+    h->cl_sr[c] += r;
+  }
+  const int64_t nc = (int64_t)h->cl_start.size();
+  h->cl_soff.assign(nc, 0);
+  int64_t off = 0;
+  for (int64_t c = 0; c < nc; ++c) {
+    h->cl_soff[c] = off;
+    off += h->cl_sr[c] * h->cl_len[c];
+  }
+  h->stack_len = off;
+  stacked.assign(std::max<int64_t>(off, 1), double2{0.0, 0.0});
+  for (int64_t b = 0; b < nf; ++b) {
+    const int64_t* F = &h->far_list[7 * b];
+    const int64_t m = F[1], n = F[3], r = F[5], fo = F[6];
+    const int64_t t = h->fb_ct[b], c = h->fb_cs[b];
+    const int64_t srt = h->cl_sr[t], src = h->cl_sr[c];
+    for (int64_t j = 0; j < r; ++j) {
+      for (int64_t k = 0; k < m; ++k)   // U(k, j) -> S_t(rb_t + j, k)
+        stacked[h->cl_soff[t] + (h->fb_rbt[b] + j) + k * srt] = far_arena[fo + k + j * m];
+      for (int64_t k = 0; k < n; ++k)   // V(k, j) -> S_s(rb_s + j, k)
+        stacked[h->cl_soff[c] + (h->fb_rbs[b] + j) + k * src] = far_arena[fo + m * r + k + j * n];
+    }
+  }
+}
+
 int64_t wcol(const ps_handle* h, int32_t p, int32_t j) {
   // column offset of block j inside W_p = [Z~_pp | Z~_p,struct(p)]
   if (j == p) return 0;
@@ -645,7 +721,7 @@ void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
         sp.fwd.add_term(t, h->Poff[d] + h->pcol[d][idx] * nd, nd, 1, h->eoff[d] * R, R, 1, (int)nd,
                         ftask[d]);
       }
-      sp.fwd.tile(t);
+      sp.fwd.tile(t, -1);
       ftask[q] = t;
     }
   }
@@ -660,7 +736,7 @@ void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
         sp.bwd.add_term(t, h->Poff[p] + h->pcol[p][i] * np_, 1, np_, h->eoff[j] * R, R, 1,
                         (int)h->nsz[j], btask[j]);
       }
-      sp.bwd.tile(t);
+      sp.bwd.tile(t, +1);
       btask[p] = t;
     }
   }
@@ -673,41 +749,41 @@ void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
     sp.dinv.tile(t);
   }
   sp.dinv.close_batch();
-  // far field, Morton order. stage 1: tmp_b = V^T w[s], tmp'_b = U^T w[t]
-  std::vector<int64_t> toff(h->nfar);
+  // far field, Morton order (DESIGN.md §Far field).
+  // stage 1, one task per cluster c: tmp_c (sum_r x R) = S_c w[c]
+  const int64_t ncl = (int64_t)h->cl_start.size();
+  std::vector<int64_t> toff(ncl);
   int64_t T = 0;
-  for (int64_t b = 0; b < h->nfar; ++b) {
-    const int64_t* F = &h->far_list[7 * b];
-    const int64_t r0 = F[0], m = F[1], c0 = F[2], n = F[3], r = F[5], off = F[6];
-    toff[b] = T;
-    T += 2 * r * R;
-    if (r == 0) continue;
-    int32_t t1 = sp.far1.add_task(toff[b], R, 1, -1, 0, 0, (int)r, (int)R, +1);
-    sp.far1.add_term(t1, off + m * r, n, 1, c0 * R, R, 1, (int)n);      // V^T (r x n)
+  for (int64_t c = 0; c < ncl; ++c) {
+    toff[c] = T;
+    T += h->cl_sr[c] * R;
+    if (h->cl_sr[c] == 0) continue;
+    int32_t t1 = sp.far1.add_task(toff[c], R, 1, -1, 0, 0, (int)h->cl_sr[c], (int)R, +1);
+    sp.far1.add_term(t1, h->cl_soff[c], 1, h->cl_sr[c], h->cl_start[c] * R, R, 1, (int)h->cl_len[c]);
     sp.far1.tile(t1);
-    int32_t t2 = sp.far1.add_task(toff[b] + r * R, R, 1, -1, 0, 0, (int)r, (int)R, +1);
-    sp.far1.add_term(t2, off, m, 1, r0 * R, R, 1, (int)m);              // U^T (r x m)
-    sp.far1.tile(t2);
   }
   sp.far1.close_batch();
-  // stage 2 per Morton leaf: t_l = sum U_b[rows of l] tmp_b + sum V_b[rows of l] tmp'_b
-  std::vector<std::vector<std::array<int64_t, 4>>> contrib(nl);  // (oA, lda, oB, K)
+  // stage 2 per Morton leaf l: t_l = sum_b U_b[rows of l] (V_b^T w_s) + sum_b V_b[rows of l] (U_b^T w_t)
+  std::vector<std::vector<std::array<int64_t, 4>>> contrib(nl);  // (oA, sAi, oB, K)
   auto leaf_of_pos = [&](int64_t m) {
     return (int64_t)(std::upper_bound(h->leaf_off.begin(), h->leaf_off.end(), m) - h->leaf_off.begin()) - 1;
   };
   for (int64_t b = 0; b < h->nfar; ++b) {
     const int64_t* F = &h->far_list[7 * b];
-    const int64_t r0 = F[0], m = F[1], c0 = F[2], n = F[3], r = F[5], off = F[6];
+    const int64_t r0 = F[0], m = F[1], c0 = F[2], n = F[3], r = F[5];
     if (r == 0) continue;
+    const int64_t ct = h->fb_ct[b], cs = h->fb_cs[b];
     for (int64_t l = leaf_of_pos(r0); l < nl && h->leaf_off[l] < r0 + m; ++l)
-      contrib[l].push_back({off + (h->leaf_off[l] - r0), m, toff[b], r});
+      contrib[l].push_back({h->cl_soff[ct] + h->fb_rbt[b] + (h->leaf_off[l] - r0) * h->cl_sr[ct],
+                            h->cl_sr[ct], toff[cs] + h->fb_rbs[b] * R, r});
     for (int64_t l = leaf_of_pos(c0); l < nl && h->leaf_off[l] < c0 + n; ++l)
-      contrib[l].push_back({off + m * r + (h->leaf_off[l] - c0), n, toff[b] + r * R, r});
+      contrib[l].push_back({h->cl_soff[cs] + h->fb_rbs[b] + (h->leaf_off[l] - c0) * h->cl_sr[cs],
+                            h->cl_sr[cs], toff[ct] + h->fb_rbt[b] * R, r});
   }
   for (int64_t l = 0; l < nl; ++l) {
     const int64_t nlf = h->leaf_off[l + 1] - h->leaf_off[l];
     int32_t t = sp.far2.add_task(h->leaf_off[l] * R, R, 1, -1, 0, 0, (int)nlf, (int)R, +1);
-    for (auto& c : contrib[l]) sp.far2.add_term(t, c[0], 1, c[1], c[2], R, 1, (int)c[3]);
+    for (auto& c : contrib[l]) sp.far2.add_term(t, c[0], c[1], 1, c[2], R, 1, (int)c[3]);
     sp.far2.tile(t);
   }
   sp.far2.close_batch();
@@ -806,7 +882,13 @@ ps_status hm_load(const char* path, const ps_dist* dist, ps_handle** out) {
     CK(cudaEventCreate(&h->ev0));
     CK(cudaEventCreate(&h->ev1));
     h->d_near.upload(near_arena, h->stream);
-    h->d_far.upload(far_arena, h->stream);
+    {
+      std::vector<double2> stacked;
+      far_layout(h.get(), far_arena, stacked);
+      far_arena.clear();
+      far_arena.shrink_to_fit();
+      h->d_far.upload(stacked, h->stream);
+    }
     h->d_e2rwg.upload(h->e2rwg, h->stream);
     h->d_e2mort.upload(h->e2mort, h->stream);
     h->d_m2e.upload(h->m2e, h->stream);
