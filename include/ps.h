@@ -186,6 +186,15 @@ ps_status ps_profile(ps_handle* h, int enable);
  * Classes 0-4 are all the gather-GEMM kernel. Returns values written. */
 int ps_profile_read(const ps_handle* h, double* out, int n);
 
+/* ps_trace / ps_trace_read — debug instrumentation of the persistent dataflow
+ * kernel: ps_trace(h, c) records, for the next launches of kernel class c
+ * (as in ps_profile_read; -1 disables), per work item: item, SM id, and the
+ * globaltimer (ns) at fetch, dependencies satisfied, compute done, published.
+ * ps_trace_read copies the last traced launch, 12 int64 per item (those 6 plus
+ * task, row tile, column tile, chunk, n_chunks, k-length); returns the item count. */
+ps_status ps_trace(ps_handle* h, int cls);
+int64_t ps_trace_read(ps_handle* h, int64_t* out, int64_t cap_items);
+
 /* ps_get_dinv — copy D_k^{-1} of the leaf at elimination position `pos`
  * (n_k x n_k column-major, in the leaf's Morton-local unknown order) to host
  * memory `out` (capacity n_k^2 complex). Returns n_k, or -1 on error. */

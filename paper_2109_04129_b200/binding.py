@@ -90,6 +90,10 @@ def load_library():
     L.ps_profile_read.argtypes = [P, ctypes.POINTER(D), I]
     L.ps_analyze.restype = I
     L.ps_analyze.argtypes = [ctypes.c_char_p, ctypes.POINTER(D), I]
+    L.ps_trace.restype = I
+    L.ps_trace.argtypes = [P, I]
+    L.ps_trace_read.restype = I64
+    L.ps_trace_read.argtypes = [P, ctypes.POINTER(I64), I64]
     L.ps_elim_leaf.restype = I64
     L.ps_elim_leaf.argtypes = [P, I64]
     _lib = L
@@ -216,6 +220,14 @@ class PsHandle:
         load_library().ps_profile_read(self._h, out, n)
         return {c: dict(ms=out[4 * i], launches=int(out[4 * i + 1]), flops=out[4 * i + 2],
                         bytes=out[4 * i + 3]) for i, c in enumerate(self.PROFILE_CLASSES)}
+
+    def trace(self, cls: int):
+        self._check(load_library().ps_trace(self._h, cls))
+
+    def trace_read(self, cap: int = 2_000_000) -> np.ndarray:
+        buf = np.zeros(12 * cap, dtype=np.int64)
+        n = load_library().ps_trace_read(self._h, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), cap)
+        return buf[:12 * n].reshape(n, 12)
 
     def elim_leaf(self, pos: int) -> int:
         return int(load_library().ps_elim_leaf(self._h, pos))

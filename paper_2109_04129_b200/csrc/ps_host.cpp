@@ -99,6 +99,13 @@ uint64_t checksum64(const uint8_t* b, size_t nbytes) {
 enum { PC_FWD = 0, PC_BWD, PC_DINV, PC_FAR1, PC_FAR2, PC_AUX, PC_COUNT };
 struct Prof {
   bool on = false;
+  // debug trace of the LAST profiled flow launch of class trace_cls
+  bool trace_on = false;
+  int trace_cls = 0;
+  DevBuf<int64_t> trace_buf;
+  const std::vector<GWork>* trace_work = nullptr;
+  const std::vector<GTask>* trace_tasks = nullptr;
+  int64_t trace_w0 = 0, trace_nw = 0;
   std::vector<cudaEvent_t> pool;
   std::vector<std::pair<int, size_t>> marks;
   size_t used = 0;
@@ -281,6 +288,15 @@ struct Table {
     fa.n_units = n_units;
     fa.pad = 0;
     fa.partial = d_partial.p;
+    fa.trace = nullptr;
+    if (pf && pf->trace_on && cls == pf->trace_cls) {
+      pf->trace_buf.alloc(6 * bt.nw);
+      fa.trace = pf->trace_buf.p;
+      pf->trace_work = &work;
+      pf->trace_tasks = &tasks;
+      pf->trace_w0 = bt.w0;
+      pf->trace_nw = bt.nw;
+    }
     launch_flow(fa, 0, st);
     if (pf) pf->end(st);
     return 1;
@@ -1108,6 +1124,36 @@ int ps_profile_read(const ps_handle* h, double* out, int n) {
     out[k++] = h->prof.bytes[c];
   }
   return k;
+}
+
+// Debug: trace every work item of the next flow launches of kernel class
+// `cls` (0..4; -1 disables). ps_trace_read copies the last one: 12 int64 per
+// item (item, smid, t_fetch, t_ready, t_computed, t_done [ns, globaltimer],
+// task, mt, nt, chunk, nchunks, klen). Returns the number of items.
+ps_status ps_trace(ps_handle* h, int cls) {
+  if (!h) return fail(nullptr, PS_EINVAL, "ps_trace: handle is NULL");
+  h->prof.trace_on = cls >= 0;
+  h->prof.trace_cls = cls;
+  return PS_OK;
+}
+
+int64_t ps_trace_read(ps_handle* h, int64_t* out, int64_t cap_items) {
+  if (!h || !out || !h->prof.trace_work || h->prof.trace_buf.n == 0) return 0;
+  const int64_t n = std::min(cap_items, h->prof.trace_nw);
+  std::vector<int64_t> raw(6 * h->prof.trace_nw);
+  if (cudaMemcpy(raw.data(), h->prof.trace_buf.p, 8 * raw.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return 0;
+  for (int64_t i = 0; i < n; ++i) {
+    for (int k = 0; k < 6; ++k) out[12 * i + k] = raw[6 * i + k];
+    const GWork& w = (*h->prof.trace_work)[h->prof.trace_w0 + i];
+    out[12 * i + 6] = w.task;
+    out[12 * i + 7] = w.mt;
+    out[12 * i + 8] = w.nt;
+    out[12 * i + 9] = w.chunk;
+    out[12 * i + 10] = w.nchunks;
+    out[12 * i + 11] = w.kb - w.ka;
+  }
+  return n;
 }
 
 int64_t ps_n(const ps_handle* h) { return h ? h->N : -1; }

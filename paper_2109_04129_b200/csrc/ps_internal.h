@@ -67,6 +67,7 @@ struct FlowArgs {
   int32_t n_units;
   int32_t pad;
   double2* partial;        // split-K partial tiles, GM_MT * GM_NT each
+  int64_t* trace;          // optional: 6 x int64 per item (item, smid, t_fetch, t_ready, t_computed, t_done), ns
 };
 
 // Tile geometry of the gather-GEMM kernel (ps_kernels.cu).

@@ -47,6 +47,17 @@ __device__ __forceinline__ void cfma(double2& acc, double2 a, double2 b) {
 // with smaller tickets, which resident CTAs already hold.
 constexpr int KC = GM_KC;
 
+__device__ __forceinline__ int64_t gtimer() {
+  int64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ int smid() {
+  int s;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+  return s;
+}
+
 __device__ __forceinline__ int ld_acquire(const int32_t* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -117,6 +128,8 @@ flow_kernel(const FlowArgs a) {
     __syncthreads();
     const int64_t item = s_item;
     if (item >= a.nwork) return;
+    int64_t* tr = (a.trace != nullptr && tid == 0) ? a.trace + 6 * item : nullptr;
+    if (tr) { tr[0] = item; tr[1] = smid(); tr[2] = gtimer(); }
     const GWork w = a.work[item];
     const GTask T = a.tasks[w.task];
     const int i0 = w.mt * GM_MT, c0 = w.nt * GM_NT;
@@ -147,6 +160,7 @@ flow_kernel(const FlowArgs a) {
       __threadfence();
     }
     __syncthreads();
+    if (tr) tr[3] = gtimer();
     // ---- pipelined, dense k-steps ----
     double2 acc[2][2];
 #pragma unroll
@@ -177,6 +191,7 @@ flow_kernel(const FlowArgs a) {
         cur ^= 1;
       }
     }
+    if (tr) tr[4] = gtimer();
     // ---- split-K: publish the partial; the last chunk reduces in chunk order ----
     bool finalize = true;
     if (w.nchunks > 1) {
@@ -230,6 +245,7 @@ flow_kernel(const FlowArgs a) {
       __syncthreads();
       if (tid == 0) atomicAdd(done + T.unit0 + w.nt, 1);
     }
+    if (tr) tr[5] = gtimer();
     __syncthreads();
   }
 }
