@@ -64,12 +64,8 @@ __device__ __forceinline__ int ld_acquire(const int32_t* p) {
   return v;
 }
 
-struct StepRegs {
-  double2 a[2], b[2];
-};
-
-// Shared per-item k tables: for the item's virtual k range [ka, kb) the A
-// column base, A row stride and B row base of every k (built from the
+// Per-item k tables: for the item's virtual k range [ka, kb) the A column
+// base, A row stride, B row base and B column stride of every k (built from the
 // segment list at item start), so k-steps run densely across segments.
 struct KTab {
   int64_t kA[GM_CHUNK_K];
@@ -78,48 +74,76 @@ struct KTab {
   int32_t kSc[GM_CHUNK_K];
 };
 
+constexpr int A_PER_T = GM_MT * KC / 256;   // 3 A elements per thread per k-step
+constexpr int B_PER_T = GM_NT * KC / 256;   // 4 B elements per thread per k-step
+constexpr int AS_LD = GM_MT;                // As[k][i]
+constexpr int BS_LD = GM_NT;                // Bs[k][c]
+
+struct StepRegs {
+  double2 a[A_PER_T], b[B_PER_T];
+};
+
+__device__ __forceinline__ void a_map(bool a_km, int e, int& i, int& k) {
+  if (a_km) { k = e & (KC - 1); i = e / KC; } else { i = e % GM_MT; k = e / GM_MT; }
+}
+__device__ __forceinline__ void b_map(bool b_km, int e, int& c, int& k) {
+  if (b_km) { k = e & (KC - 1); c = e / KC; } else { c = e & (GM_NT - 1); k = e / GM_NT; }
+}
+
 __device__ __forceinline__ void fetch_step(const KTab& kt, int k0, int klen, int i0, int c0, int mm,
                                            int nn, bool a_km, bool b_km,
                                            const double2* __restrict__ Ab,
                                            const double2* __restrict__ Bb, int tid, StepRegs& r) {
 #pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    const int e = tid + q * 256;
+  for (int q = 0; q < A_PER_T; ++q) {
     int i, k;
-    if (a_km) { k = e & 15; i = e >> 4; } else { i = e & 31; k = e >> 5; }
+    a_map(a_km, tid + q * 256, i, k);
     const int kk = k0 + k;
     r.a[q] = (i < mm && kk < klen) ? __ldg(Ab + kt.kA[kk] + (int64_t)(i0 + i) * kt.kSi[kk])
                                    : make_double2(0.0, 0.0);
-    int c;
-    if (b_km) { k = e & 15; c = e >> 4; } else { c = e & 31; k = e >> 5; }
-    const int kb = k0 + k;
-    r.b[q] = (c < nn && kb < klen) ? __ldcg(Bb + kt.kB[kb] + (int64_t)(c0 + c) * kt.kSc[kb])
+  }
+#pragma unroll
+  for (int q = 0; q < B_PER_T; ++q) {
+    int c, k;
+    b_map(b_km, tid + q * 256, c, k);
+    const int kk = k0 + k;
+    r.b[q] = (c < nn && kk < klen) ? __ldcg(Bb + kt.kB[kk] + (int64_t)(c0 + c) * kt.kSc[kk])
                                    : make_double2(0.0, 0.0);
   }
 }
 
 __device__ __forceinline__ void store_step(bool a_km, bool b_km, int tid, const StepRegs& r,
-                                           double2 (*As)[GM_MT + 1], double2 (*Bs)[GM_NT + 1]) {
+                                           double2* As, double2* Bs) {
 #pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    const int e = tid + q * 256;
+  for (int q = 0; q < A_PER_T; ++q) {
     int i, k;
-    if (a_km) { k = e & 15; i = e >> 4; } else { i = e & 31; k = e >> 5; }
-    As[k][i] = r.a[q];
-    int c;
-    if (b_km) { k = e & 15; c = e >> 4; } else { c = e & 31; k = e >> 5; }
-    Bs[k][c] = r.b[q];
+    a_map(a_km, tid + q * 256, i, k);
+    As[k * AS_LD + i] = r.a[q];
+  }
+#pragma unroll
+  for (int q = 0; q < B_PER_T; ++q) {
+    int c, k;
+    b_map(b_km, tid + q * 256, c, k);
+    Bs[k * BS_LD + c] = r.b[q];
   }
 }
 
-__global__ void __launch_bounds__(256, 3)
+constexpr size_t FLOW_SMEM = 2 * (size_t)KC * (AS_LD + BS_LD) * sizeof(double2) + sizeof(KTab);
+
+// Output tile: warp w = (wm, wn) = (w % 4, w / 4) owns rows
+// [wm*RM, min(mm, (wm+1)*RM)) with RM = ceil(mm / 4) <= 12 (so the tile is
+// only as tall as the task) and column wn*32 + lane. A values are broadcast
+// shared loads, one B load feeds RM complex FMAs.
+__global__ void __launch_bounds__(256, 2)
 flow_kernel(const FlowArgs a) {
-  __shared__ double2 As[2][KC][GM_MT + 1];
-  __shared__ double2 Bs[2][KC][GM_NT + 1];
-  __shared__ KTab kt;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* As0 = reinterpret_cast<double2*>(smem_raw);
+  double2* Bs0 = As0 + 2 * KC * AS_LD;
+  KTab& kt = *reinterpret_cast<KTab*>(Bs0 + 2 * KC * BS_LD);
   __shared__ int s_item, s_last;
   const int tid = threadIdx.x;
-  const int tx = tid & 15, ty = tid >> 4;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wm = warp % GM_WM, wn = warp / GM_WM;
   int32_t* ticket = a.counters;
   int32_t* done = a.counters + 1;
   int32_t* arrive = a.counters + 1 + a.n_units;
@@ -135,6 +159,9 @@ flow_kernel(const FlowArgs a) {
     const int i0 = w.mt * GM_MT, c0 = w.nt * GM_NT;
     const int mm = min(GM_MT, T.m - i0), nn = min(GM_NT, T.n - c0);
     const int klen = w.kb - w.ka;
+    const int RM = (mm + GM_WM - 1) / GM_WM;
+    const int rbase = wm * RM;
+    const int col = wn * 32 + lane;
     // ---- k tables of this item (segments [ta, tb) clipped to [ka, kb)) ----
     for (int t = w.ta + tid; t < w.tb; t += 256) {
       const GTerm g = a.terms[t];
@@ -162,31 +189,30 @@ flow_kernel(const FlowArgs a) {
     __syncthreads();
     if (tr) tr[3] = gtimer();
     // ---- pipelined, dense k-steps ----
-    double2 acc[2][2];
+    double2 acc[GM_RMAX];
 #pragma unroll
-    for (int p = 0; p < 2; ++p)
-#pragma unroll
-      for (int q = 0; q < 2; ++q) acc[p][q] = make_double2(0.0, 0.0);
+    for (int r = 0; r < GM_RMAX; ++r) acc[r] = make_double2(0.0, 0.0);
     const bool a_km = T.a_kmajor != 0, b_km = T.b_kmajor != 0;
     if (klen > 0) {
-      StepRegs r;
-      fetch_step(kt, 0, klen, i0, c0, mm, nn, a_km, b_km, a.A, a.B, tid, r);
-      store_step(a_km, b_km, tid, r, As[0], Bs[0]);
+      StepRegs rg;
+      fetch_step(kt, 0, klen, i0, c0, mm, nn, a_km, b_km, a.A, a.B, tid, rg);
+      store_step(a_km, b_km, tid, rg, As0, Bs0);
       __syncthreads();
       int cur = 0;
       for (int k0 = 0; k0 < klen; k0 += KC) {
         const bool nxt = k0 + KC < klen;
-        if (nxt) fetch_step(kt, k0 + KC, klen, i0, c0, mm, nn, a_km, b_km, a.A, a.B, tid, r);
-#pragma unroll
+        if (nxt) fetch_step(kt, k0 + KC, klen, i0, c0, mm, nn, a_km, b_km, a.A, a.B, tid, rg);
+        const double2* As = As0 + cur * KC * AS_LD;
+        const double2* Bs = Bs0 + cur * KC * BS_LD;
+#pragma unroll 4
         for (int k = 0; k < KC; ++k) {
-          const double2 a0 = As[cur][k][ty], a1 = As[cur][k][ty + 16];
-          const double2 b0 = Bs[cur][k][tx], b1 = Bs[cur][k][tx + 16];
-          cfma(acc[0][0], a0, b0);
-          cfma(acc[0][1], a0, b1);
-          cfma(acc[1][0], a1, b0);
-          cfma(acc[1][1], a1, b1);
+          const double2 b = Bs[k * BS_LD + col];
+          const double2* ak = As + k * AS_LD + rbase;
+#pragma unroll
+          for (int r = 0; r < GM_RMAX; ++r)
+            if (r < RM) cfma(acc[r], ak[r], b);
         }
-        if (nxt) store_step(a_km, b_km, tid, r, As[cur ^ 1], Bs[cur ^ 1]);
+        if (nxt) store_step(a_km, b_km, tid, rg, As0 + (cur ^ 1) * KC * AS_LD, Bs0 + (cur ^ 1) * KC * BS_LD);
         __syncthreads();
         cur ^= 1;
       }
@@ -197,9 +223,8 @@ flow_kernel(const FlowArgs a) {
     if (w.nchunks > 1) {
       double2* P = a.partial + (w.slot + w.chunk) * (int64_t)(GM_MT * GM_NT);
 #pragma unroll
-      for (int p = 0; p < 2; ++p)
-#pragma unroll
-        for (int q = 0; q < 2; ++q) P[(ty + 16 * p) * GM_NT + tx + 16 * q] = acc[p][q];
+      for (int r = 0; r < GM_RMAX; ++r)
+        if (r < RM) P[(rbase + r) * GM_NT + col] = acc[r];
       __threadfence();
       __syncthreads();
       if (tid == 0) s_last = (atomicAdd(arrive + w.tile, 1) == w.nchunks - 1);
@@ -208,39 +233,36 @@ flow_kernel(const FlowArgs a) {
       if (finalize) {
         __threadfence();
 #pragma unroll
-        for (int p = 0; p < 2; ++p)
-#pragma unroll
-          for (int q = 0; q < 2; ++q) acc[p][q] = make_double2(0.0, 0.0);
+        for (int r = 0; r < GM_RMAX; ++r) acc[r] = make_double2(0.0, 0.0);
         for (int c = 0; c < w.nchunks; ++c) {
           const double2* Q = a.partial + (w.slot + c) * (int64_t)(GM_MT * GM_NT);
 #pragma unroll
-          for (int p = 0; p < 2; ++p)
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-              const double2 v = __ldcg(Q + (ty + 16 * p) * GM_NT + tx + 16 * q);
-              acc[p][q].x += v.x;
-              acc[p][q].y += v.y;
+          for (int r = 0; r < GM_RMAX; ++r)
+            if (r < RM) {
+              const double2 v = __ldcg(Q + (rbase + r) * GM_NT + col);
+              acc[r].x += v.x;
+              acc[r].y += v.y;
             }
         }
       }
     }
     if (finalize) {
       const double sg = (double)T.sign;
+      if (col < nn) {
 #pragma unroll
-      for (int p = 0; p < 2; ++p)
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int i = ty + 16 * p, c = tx + 16 * q;
-          if (i < mm && c < nn) {
-            double2 v = make_double2(sg * acc[p][q].x, sg * acc[p][q].y);
+        for (int r = 0; r < GM_RMAX; ++r) {
+          const int i = rbase + r;
+          if (r < RM && i < mm) {
+            double2 v = make_double2(sg * acc[r].x, sg * acc[r].y);
             if (T.oI >= 0) {
-              const double2 z = __ldcg(a.I + T.oI + (int64_t)(i0 + i) * T.sIi + (int64_t)(c0 + c) * T.sIc);
+              const double2 z = __ldcg(a.I + T.oI + (int64_t)(i0 + i) * T.sIi + (int64_t)(c0 + col) * T.sIc);
               v.x += z.x;
               v.y += z.y;
             }
-            a.O[T.oO + (int64_t)(i0 + i) * T.sOi + (int64_t)(c0 + c) * T.sOc] = v;
+            a.O[T.oO + (int64_t)(i0 + i) * T.sOi + (int64_t)(c0 + col) * T.sOc] = v;
           }
         }
+      }
       __threadfence();
       __syncthreads();
       if (tid == 0) atomicAdd(done + T.unit0 + w.nt, 1);
@@ -256,7 +278,8 @@ int flow_resident_ctas() {
     int per_sm = 0, dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, flow_kernel, 256, 0);
+    cudaFuncSetAttribute(flow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FLOW_SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, flow_kernel, 256, FLOW_SMEM);
     n = sms * (per_sm > 0 ? per_sm : 1);
   }
   return n;
@@ -266,7 +289,7 @@ void launch_flow(const FlowArgs& a, int grid, cudaStream_t st) {
   if (a.nwork <= 0) return;
   int g = grid > 0 ? grid : flow_resident_ctas();
   if (g > a.nwork) g = (int)a.nwork;
-  flow_kernel<<<g, 256, 0, st>>>(a);
+  flow_kernel<<<g, 256, FLOW_SMEM, st>>>(a);
 }
 
 // ---------------------------------------------------------------------------
