@@ -71,9 +71,9 @@ struct FlowArgs {
 };
 
 // Tile geometry of the gather-GEMM kernel (ps_kernels.cu).
-constexpr int GM_RMAX = 12;                 // rows per warp (register accumulators per thread)
+constexpr int GM_RMAX = 8;                  // rows per warp (register accumulators per thread)
 constexpr int GM_WM = 4, GM_WN = 2;         // warp grid: 4 row groups x 2 column groups
-constexpr int GM_MT = GM_WM * GM_RMAX;      // 48 rows per tile (max)
+constexpr int GM_MT = GM_WM * GM_RMAX;      // 32 rows per tile (max)
 constexpr int GM_NT = GM_WN * 32;           // 64 columns per tile (one per lane)
 constexpr int GM_KC = 16;
 constexpr int GM_CHUNK_K = 512;   // max virtual k per work item (shared-memory k tables)

@@ -130,8 +130,97 @@ __device__ __forceinline__ void store_step(bool a_km, bool b_km, int tid, const 
 
 constexpr size_t FLOW_SMEM = 2 * (size_t)KC * (AS_LD + BS_LD) * sizeof(double2) + sizeof(KTab);
 
+// Everything of one work item after its producers are complete, for a
+// compile-time rows-per-warp RM (so the FMA stream is branch-free).
+template <int RM>
+__device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, const GTask& T,
+                                          const KTab& kt, double2* As0, double2* Bs0, int tid,
+                                          int lane, int wm, int wn, int* s_last, int64_t* tr) {
+  const int i0 = w.mt * GM_MT, c0 = w.nt * GM_NT;
+  const int mm = min(GM_MT, T.m - i0), nn = min(GM_NT, T.n - c0);
+  const int klen = w.kb - w.ka;
+  const int rbase = wm * RM;
+  const int col = wn * 32 + lane;
+  int32_t* done = a.counters + 1;
+  int32_t* arrive = a.counters + 1 + a.n_units;
+  double2 acc[RM];
+#pragma unroll
+  for (int r = 0; r < RM; ++r) acc[r] = make_double2(0.0, 0.0);
+  const bool a_km = T.a_kmajor != 0, b_km = T.b_kmajor != 0;
+  if (klen > 0) {
+    StepRegs rg;
+    fetch_step(kt, 0, klen, i0, c0, mm, nn, a_km, b_km, a.A, a.B, tid, rg);
+    store_step(a_km, b_km, tid, rg, As0, Bs0);
+    __syncthreads();
+    int cur = 0;
+    for (int k0 = 0; k0 < klen; k0 += KC) {
+      const bool nxt = k0 + KC < klen;
+      if (nxt) fetch_step(kt, k0 + KC, klen, i0, c0, mm, nn, a_km, b_km, a.A, a.B, tid, rg);
+      const double2* As = As0 + cur * KC * AS_LD + rbase;
+      const double2* Bs = Bs0 + cur * KC * BS_LD + col;
+#pragma unroll
+      for (int k = 0; k < KC; ++k) {
+        const double2 b = Bs[k * BS_LD];
+#pragma unroll
+        for (int r = 0; r < RM; ++r) cfma(acc[r], As[k * AS_LD + r], b);
+      }
+      if (nxt) store_step(a_km, b_km, tid, rg, As0 + (cur ^ 1) * KC * AS_LD, Bs0 + (cur ^ 1) * KC * BS_LD);
+      __syncthreads();
+      cur ^= 1;
+    }
+  }
+  if (tr) tr[4] = gtimer();
+  // ---- split-K: publish the partial; the last chunk reduces in chunk order ----
+  bool finalize = true;
+  if (w.nchunks > 1) {
+    double2* P = a.partial + (w.slot + w.chunk) * (int64_t)(GM_MT * GM_NT);
+#pragma unroll
+    for (int r = 0; r < RM; ++r) P[(rbase + r) * GM_NT + col] = acc[r];
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) *s_last = (atomicAdd(arrive + w.tile, 1) == w.nchunks - 1);
+    __syncthreads();
+    finalize = *s_last;
+    if (finalize) {
+      __threadfence();
+#pragma unroll
+      for (int r = 0; r < RM; ++r) acc[r] = make_double2(0.0, 0.0);
+      for (int c = 0; c < w.nchunks; ++c) {
+        const double2* Q = a.partial + (w.slot + c) * (int64_t)(GM_MT * GM_NT);
+#pragma unroll
+        for (int r = 0; r < RM; ++r) {
+          const double2 v = __ldcg(Q + (rbase + r) * GM_NT + col);
+          acc[r].x += v.x;
+          acc[r].y += v.y;
+        }
+      }
+    }
+  }
+  if (finalize) {
+    const double sg = (double)T.sign;
+    if (col < nn) {
+#pragma unroll
+      for (int r = 0; r < RM; ++r) {
+        const int i = rbase + r;
+        if (i < mm) {
+          double2 v = make_double2(sg * acc[r].x, sg * acc[r].y);
+          if (T.oI >= 0) {
+            const double2 z = __ldcg(a.I + T.oI + (int64_t)(i0 + i) * T.sIi + (int64_t)(c0 + col) * T.sIc);
+            v.x += z.x;
+            v.y += z.y;
+          }
+          a.O[T.oO + (int64_t)(i0 + i) * T.sOi + (int64_t)(c0 + col) * T.sOc] = v;
+        }
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) atomicAdd(done + T.unit0 + w.nt, 1);
+  }
+}
+
 // Output tile: warp w = (wm, wn) = (w % 4, w / 4) owns rows
-// [wm*RM, min(mm, (wm+1)*RM)) with RM = ceil(mm / 4) <= 12 (so the tile is
+// [wm*RM, min(mm, (wm+1)*RM)) with RM = ceil(mm / 4) <= 8 (so the tile is
 // only as tall as the task) and column wn*32 + lane. A values are broadcast
 // shared loads, one B load feeds RM complex FMAs.
 __global__ void __launch_bounds__(256, 2)
@@ -146,7 +235,6 @@ flow_kernel(const FlowArgs a) {
   const int wm = warp % GM_WM, wn = warp / GM_WM;
   int32_t* ticket = a.counters;
   int32_t* done = a.counters + 1;
-  int32_t* arrive = a.counters + 1 + a.n_units;
   for (;;) {
     if (tid == 0) s_item = atomicAdd(ticket, 1);
     __syncthreads();
@@ -156,12 +244,8 @@ flow_kernel(const FlowArgs a) {
     if (tr) { tr[0] = item; tr[1] = smid(); tr[2] = gtimer(); }
     const GWork w = a.work[item];
     const GTask T = a.tasks[w.task];
-    const int i0 = w.mt * GM_MT, c0 = w.nt * GM_NT;
-    const int mm = min(GM_MT, T.m - i0), nn = min(GM_NT, T.n - c0);
-    const int klen = w.kb - w.ka;
+    const int mm = min(GM_MT, T.m - w.mt * GM_MT);
     const int RM = (mm + GM_WM - 1) / GM_WM;
-    const int rbase = wm * RM;
-    const int col = wn * 32 + lane;
     // ---- k tables of this item (segments [ta, tb) clipped to [ka, kb)) ----
     for (int t = w.ta + tid; t < w.tb; t += 256) {
       const GTerm g = a.terms[t];
@@ -188,84 +272,13 @@ flow_kernel(const FlowArgs a) {
     }
     __syncthreads();
     if (tr) tr[3] = gtimer();
-    // ---- pipelined, dense k-steps ----
-    double2 acc[GM_RMAX];
-#pragma unroll
-    for (int r = 0; r < GM_RMAX; ++r) acc[r] = make_double2(0.0, 0.0);
-    const bool a_km = T.a_kmajor != 0, b_km = T.b_kmajor != 0;
-    if (klen > 0) {
-      StepRegs rg;
-      fetch_step(kt, 0, klen, i0, c0, mm, nn, a_km, b_km, a.A, a.B, tid, rg);
-      store_step(a_km, b_km, tid, rg, As0, Bs0);
-      __syncthreads();
-      int cur = 0;
-      for (int k0 = 0; k0 < klen; k0 += KC) {
-        const bool nxt = k0 + KC < klen;
-        if (nxt) fetch_step(kt, k0 + KC, klen, i0, c0, mm, nn, a_km, b_km, a.A, a.B, tid, rg);
-        const double2* As = As0 + cur * KC * AS_LD;
-        const double2* Bs = Bs0 + cur * KC * BS_LD;
-#pragma unroll 4
-        for (int k = 0; k < KC; ++k) {
-          const double2 b = Bs[k * BS_LD + col];
-          const double2* ak = As + k * AS_LD + rbase;
-#pragma unroll
-          for (int r = 0; r < GM_RMAX; ++r)
-            if (r < RM) cfma(acc[r], ak[r], b);
-        }
-        if (nxt) store_step(a_km, b_km, tid, rg, As0 + (cur ^ 1) * KC * AS_LD, Bs0 + (cur ^ 1) * KC * BS_LD);
-        __syncthreads();
-        cur ^= 1;
-      }
-    }
-    if (tr) tr[4] = gtimer();
-    // ---- split-K: publish the partial; the last chunk reduces in chunk order ----
-    bool finalize = true;
-    if (w.nchunks > 1) {
-      double2* P = a.partial + (w.slot + w.chunk) * (int64_t)(GM_MT * GM_NT);
-#pragma unroll
-      for (int r = 0; r < GM_RMAX; ++r)
-        if (r < RM) P[(rbase + r) * GM_NT + col] = acc[r];
-      __threadfence();
-      __syncthreads();
-      if (tid == 0) s_last = (atomicAdd(arrive + w.tile, 1) == w.nchunks - 1);
-      __syncthreads();
-      finalize = s_last;
-      if (finalize) {
-        __threadfence();
-#pragma unroll
-        for (int r = 0; r < GM_RMAX; ++r) acc[r] = make_double2(0.0, 0.0);
-        for (int c = 0; c < w.nchunks; ++c) {
-          const double2* Q = a.partial + (w.slot + c) * (int64_t)(GM_MT * GM_NT);
-#pragma unroll
-          for (int r = 0; r < GM_RMAX; ++r)
-            if (r < RM) {
-              const double2 v = __ldcg(Q + (rbase + r) * GM_NT + col);
-              acc[r].x += v.x;
-              acc[r].y += v.y;
-            }
-        }
-      }
-    }
-    if (finalize) {
-      const double sg = (double)T.sign;
-      if (col < nn) {
-#pragma unroll
-        for (int r = 0; r < GM_RMAX; ++r) {
-          const int i = rbase + r;
-          if (r < RM && i < mm) {
-            double2 v = make_double2(sg * acc[r].x, sg * acc[r].y);
-            if (T.oI >= 0) {
-              const double2 z = __ldcg(a.I + T.oI + (int64_t)(i0 + i) * T.sIi + (int64_t)(c0 + col) * T.sIc);
-              v.x += z.x;
-              v.y += z.y;
-            }
-            a.O[T.oO + (int64_t)(i0 + i) * T.sOi + (int64_t)(c0 + col) * T.sOc] = v;
-          }
-        }
-      }
-      __threadfence();
-      __syncthreads();
-      if (tid == 0) atomicAdd(done + T.unit0 + w.nt, 1);
+    switch (RM) {
+#define PS_RM_CASE(R) \
+      case R: item_body<R>(a, w, T, kt, As0, Bs0, tid, lane, wm, wn, &s_last, tr); break;
+      PS_RM_CASE(1) PS_RM_CASE(2) PS_RM_CASE(3) PS_RM_CASE(4) PS_RM_CASE(5) PS_RM_CASE(6)
+      PS_RM_CASE(7) PS_RM_CASE(8)
+#undef PS_RM_CASE
+      default: break;
     }
     if (tr) tr[5] = gtimer();
     __syncthreads();
