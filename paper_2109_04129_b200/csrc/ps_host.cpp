@@ -161,6 +161,7 @@ struct Table {
   int32_t n_units = 0, n_tiles = 0;
   int64_t n_slots = 0;
   int chunk_steps = CHUNK_STEPS;
+  int acc_dir = 0;        // see FlowArgs::acc_dir; items of a tile are queued in accumulation order
 
   int32_t add_task(int64_t oO, int64_t sOi, int64_t sOc, int64_t oI, int64_t sIi, int64_t sIc, int m,
                    int n, int sign) {
@@ -197,10 +198,10 @@ struct Table {
   // work items of a task: every (mt, nt) tile, its virtual K split into chunks
   // of ~chunk_steps k-steps (split-K); also assigns the task's completion units.
   // chunks (ka, kb, ta, tb) covering virtual k in [k_lo, k_hi) = segments [s0, s1)
-  void chunk_range(int32_t s0, int32_t s1, std::vector<std::array<int32_t, 4>>& ch) const {
+  void chunk_range(int32_t s0, int32_t s1, std::vector<std::array<int32_t, 4>>& ch, int steps) const {
     if (s0 >= s1) return;
     const int32_t k_lo = terms[s0].kstart, k_hi = terms[s1 - 1].kstart + terms[s1 - 1].K;
-    const int target = std::min(chunk_steps * GM_KC, GM_CHUNK_K);
+    const int target = std::min(steps * GM_KC, GM_CHUNK_K);
     int32_t ka = k_lo, ta = s0;
     while (ka < k_hi) {
       int32_t kb = std::min(k_hi, ka + target);
@@ -224,7 +225,8 @@ struct Table {
   // isolate = +1 / -1 puts the first / last segment (the dependency expected to
   // complete last: the parent in the backward sweep, the last child in the
   // forward sweep) in a chunk of its own, so a chain hop waits on a short chunk.
-  void tile(int32_t task, int isolate = 0) {
+  void tile(int32_t task, int isolate = 0, int steps = 0) {
+    if (steps <= 0) steps = chunk_steps;
     GTask& t = tasks[task];
     const int nmt = t.n_mt, nnt = (t.n + GM_NT - 1) / GM_NT;
     t.unit0 = n_units;
@@ -233,14 +235,14 @@ struct Table {
     const int nseg = t.t1 - t.t0;
     if (isolate != 0 && nseg >= 2) {
       if (isolate > 0) {
-        chunk_range(t.t0, t.t0 + 1, ch);
-        chunk_range(t.t0 + 1, t.t1, ch);
+        chunk_range(t.t0, t.t0 + 1, ch, steps);
+        chunk_range(t.t0 + 1, t.t1, ch, steps);
       } else {
-        chunk_range(t.t0, t.t1 - 1, ch);
-        chunk_range(t.t1 - 1, t.t1, ch);
+        chunk_range(t.t0, t.t1 - 1, ch, steps);
+        chunk_range(t.t1 - 1, t.t1, ch, steps);
       }
     } else {
-      chunk_range(t.t0, t.t1, ch);
+      chunk_range(t.t0, t.t1, ch, steps);
     }
     if (ch.empty()) ch.push_back({0, 0, t.t0, t.t0});
     const int nch = (int)ch.size();
@@ -249,8 +251,10 @@ struct Table {
         const int32_t tile_id = n_tiles++;
         const int64_t slot = nch > 1 ? n_slots : 0;
         if (nch > 1) n_slots += nch;
-        for (int c = 0; c < nch; ++c)
+        for (int q = 0; q < nch; ++q) {
+          const int c = (acc_dir < 0) ? nch - 1 - q : q;   // queue in accumulation order
           work.push_back({task, a, b, ch[c][2], ch[c][3], ch[c][0], ch[c][1], c, nch, tile_id, slot});
+        }
       }
   }
   void close_batch() {
@@ -289,6 +293,8 @@ struct Table {
     fa.pad = 0;
     fa.partial = d_partial.p;
     fa.trace = nullptr;
+    fa.acc_dir = acc_dir;
+    fa.pad2 = 0;
     if (pf && pf->trace_on && cls == pf->trace_cls) {
       pf->trace_buf.alloc(6 * bt.nw);
       fa.trace = pf->trace_buf.p;
@@ -727,7 +733,13 @@ void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
     byd[h->depth[p]].push_back((int32_t)p);
   }
   std::vector<int32_t> ftask(nl, -1), btask(nl, -1);
+  sp.fwd.acc_dir = +1;
+  sp.bwd.acc_dir = -1;
+  // narrow levels (the separator chains) get small split-K chunks so each hop
+  // waits on ~1-4 k-steps; wide levels keep large chunks (less overhead)
+  auto steps_for = [](size_t width) { return width <= 4 ? 4 : (width <= 16 ? 8 : 16); };
   for (int lev = 0; lev <= h->max_height; ++lev) {
+    const int stp = steps_for(byh[lev].size());
     for (int32_t q : byh[lev]) {
       if (h->gath[q].empty()) continue;
       const int64_t nq = h->nsz[q];
@@ -737,13 +749,14 @@ void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
         sp.fwd.add_term(t, h->Poff[d] + h->pcol[d][idx] * nd, nd, 1, h->eoff[d] * R, R, 1, (int)nd,
                         ftask[d]);
       }
-      sp.fwd.tile(t, -1);
+      sp.fwd.tile(t, -1, stp);
       ftask[q] = t;
     }
   }
   sp.fwd.close_batch();
   // backward sweep (Eq. 26), ordered by depth: w_p = v_p + sum_j alpha_pj w_j
   for (int lev = 0; lev <= h->max_depth; ++lev) {
+    const int stp = steps_for(byd[lev].size());
     for (int32_t p : byd[lev]) {
       const int64_t np_ = h->nsz[p];
       int32_t t = sp.bwd.add_task(h->eoff[p] * R, R, 1, h->eoff[p] * R, R, 1, (int)np_, (int)R, +1);
@@ -752,7 +765,7 @@ void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
         sp.bwd.add_term(t, h->Poff[p] + h->pcol[p][i] * np_, 1, np_, h->eoff[j] * R, R, 1,
                         (int)h->nsz[j], btask[j]);
       }
-      sp.bwd.tile(t, +1);
+      sp.bwd.tile(t, +1, stp);
       btask[p] = t;
     }
   }

@@ -68,6 +68,10 @@ struct FlowArgs {
   int32_t pad;
   double2* partial;        // split-K partial tiles, GM_MT * GM_NT each
   int64_t* trace;          // optional: 6 x int64 per item (item, smid, t_fetch, t_ready, t_computed, t_done), ns
+  int32_t acc_dir;         // split-K combine: 0 = last arriver sums all partials in chunk order;
+                           // -1 = chained suffix S_k = p_k + S_{k+1}, chunk 0 finalises;
+                           // +1 = chained prefix S_k = S_{k-1} + p_k, chunk n-1 finalises
+  int32_t pad2;
 };
 
 // Tile geometry of the gather-GEMM kernel (ps_kernels.cu).
