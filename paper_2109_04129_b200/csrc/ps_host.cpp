@@ -744,7 +744,14 @@ void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
       if (h->gath[q].empty()) continue;
       const int64_t nq = h->nsz[q];
       int32_t t = sp.fwd.add_task(h->eoff[q] * R, R, 1, h->eoff[q] * R, R, 1, (int)nq, (int)R, +1);
-      for (auto [d, idx] : h->gath[q]) {
+      // segments in producer completion order (height), so the chained prefix
+      // accumulation follows readiness; the last one (the chain child) is isolated
+      auto gl = h->gath[q];
+      std::stable_sort(gl.begin(), gl.end(), [&](const std::pair<int32_t, int32_t>& x,
+                                                 const std::pair<int32_t, int32_t>& y) {
+        return h->height[x.first] < h->height[y.first];
+      });
+      for (auto [d, idx] : gl) {
         const int64_t nd = h->nsz[d];
         sp.fwd.add_term(t, h->Poff[d] + h->pcol[d][idx] * nd, nd, 1, h->eoff[d] * R, R, 1, (int)nd,
                         ftask[d]);
