@@ -161,7 +161,6 @@ struct Table {
   int32_t n_units = 0, n_tiles = 0;
   int64_t n_slots = 0;
   int chunk_steps = CHUNK_STEPS;
-  int acc_dir = 0;        // see FlowArgs::acc_dir; items of a tile are queued in accumulation order
 
   int32_t add_task(int64_t oO, int64_t sOi, int64_t sOc, int64_t oI, int64_t sIi, int64_t sIc, int m,
                    int n, int sign) {
@@ -246,15 +245,20 @@ struct Table {
     }
     if (ch.empty()) ch.push_back({0, 0, t.t0, t.t0});
     const int nch = (int)ch.size();
+    // critical chunk = the isolated one (queued last); -1: plain last-arriver combine
+    int32_t crit = -1;
+    if (isolate != 0 && nseg >= 2 && nch >= 2) crit = isolate > 0 ? 0 : nch - 1;
     for (int a = 0; a < nmt; ++a)
       for (int b = 0; b < nnt; ++b) {
         const int32_t tile_id = n_tiles++;
         const int64_t slot = nch > 1 ? n_slots : 0;
         if (nch > 1) n_slots += nch;
-        for (int q = 0; q < nch; ++q) {
-          const int c = (acc_dir < 0) ? nch - 1 - q : q;   // queue in accumulation order
-          work.push_back({task, a, b, ch[c][2], ch[c][3], ch[c][0], ch[c][1], c, nch, tile_id, slot});
-        }
+        for (int c = 0; c < nch; ++c)
+          if (c != crit)
+            work.push_back({task, a, b, ch[c][2], ch[c][3], ch[c][0], ch[c][1], c, nch, tile_id, crit, 0, slot});
+        if (crit >= 0)
+          work.push_back({task, a, b, ch[crit][2], ch[crit][3], ch[crit][0], ch[crit][1], crit, nch, tile_id,
+                          crit, 0, slot});
       }
   }
   void close_batch() {
@@ -293,8 +297,8 @@ struct Table {
     fa.pad = 0;
     fa.partial = d_partial.p;
     fa.trace = nullptr;
-    fa.acc_dir = acc_dir;
     fa.pad2 = 0;
+    fa.pad3 = 0;
     if (pf && pf->trace_on && cls == pf->trace_cls) {
       pf->trace_buf.alloc(6 * bt.nw);
       fa.trace = pf->trace_buf.p;
@@ -733,8 +737,6 @@ void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
     byd[h->depth[p]].push_back((int32_t)p);
   }
   std::vector<int32_t> ftask(nl, -1), btask(nl, -1);
-  sp.fwd.acc_dir = +1;
-  sp.bwd.acc_dir = -1;
   // narrow levels (the separator chains) get small split-K chunks so each hop
   // waits on ~1-4 k-steps; wide levels keep large chunks (less overhead)
   auto steps_for = [](size_t width) { return width <= 4 ? 4 : (width <= 16 ? 8 : 16); };

@@ -43,6 +43,11 @@ struct GTerm {
 // them up in chunk order — deterministic.
 struct GWork {
   int32_t task, mt, nt, ta, tb, ka, kb, chunk, nchunks, tile;
+  int32_t crit;            // split-K combine: -1 = last arriver sums all partials in chunk
+                           // order; else the chunk that carries the latest dependency: the
+                           // other chunks' last arriver sums them (chunk order) into slot
+                           // `crit`, and chunk `crit` (queued last) adds that one sum
+  int32_t pad;
   int64_t slot;
 };
 
@@ -68,10 +73,7 @@ struct FlowArgs {
   int32_t pad;
   double2* partial;        // split-K partial tiles, GM_MT * GM_NT each
   int64_t* trace;          // optional: 6 x int64 per item (item, smid, t_fetch, t_ready, t_computed, t_done), ns
-  int32_t acc_dir;         // split-K combine: 0 = last arriver sums all partials in chunk order;
-                           // -1 = chained suffix S_k = p_k + S_{k+1}, chunk 0 finalises;
-                           // +1 = chained prefix S_k = S_{k-1} + p_k, chunk n-1 finalises
-  int32_t pad2;
+  int32_t pad2, pad3;
 };
 
 // Tile geometry of the gather-GEMM kernel (ps_kernels.cu).

@@ -170,60 +170,57 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
     }
   }
   if (tr) tr[4] = gtimer();
-  // ---- split-K combine ----
+  // ---- split-K combine (fixed summation order => deterministic) ----
   bool finalize = true;
-  if (w.nchunks > 1 && a.acc_dir != 0) {
-    // chained: chunk k folds in the running sum of its predecessor in the
-    // accumulation order (published in slot pred), publishes its own, and the
-    // last chunk in that order finalises. Fixed order => deterministic.
-    const bool first = (a.acc_dir < 0) ? (w.chunk == w.nchunks - 1) : (w.chunk == 0);
-    const bool last = (a.acc_dir < 0) ? (w.chunk == 0) : (w.chunk == w.nchunks - 1);
-    const int32_t pos = (a.acc_dir < 0) ? (w.nchunks - 1 - w.chunk) : w.chunk;   // place in order
-    if (!first) {
-      const int pred = w.chunk - a.acc_dir;   // dir -1: k+1, dir +1: k-1
+  if (w.nchunks > 1) {
+    const int64_t TS = (int64_t)(GM_MT * GM_NT);
+    const bool crit_mode = w.crit >= 0;
+    if (crit_mode && w.chunk == w.crit) {
+      // the other chunks' sum arrives in slot `crit` once arrive[tile] == nchunks
       if (tid == 0) {
-        while (ld_acquire(arrive + w.tile) < pos) __nanosleep(32);
+        while (ld_acquire(arrive + w.tile) < w.nchunks) __nanosleep(32);
         __threadfence();
       }
       __syncthreads();
-      const double2* Q = a.partial + (w.slot + pred) * (int64_t)(GM_MT * GM_NT);
+      const double2* G = a.partial + (w.slot + w.crit) * TS;
 #pragma unroll
       for (int r = 0; r < RM; ++r) {
-        const double2 v = __ldcg(Q + (rbase + r) * GM_NT + col);
-        if (a.acc_dir < 0) { acc[r].x += v.x; acc[r].y += v.y; }          // p_k + S_{k+1}
-        else { acc[r].x = v.x + acc[r].x; acc[r].y = v.y + acc[r].y; }    // S_{k-1} + p_k
+        const double2 v = __ldcg(G + (rbase + r) * GM_NT + col);
+        if (w.crit == 0) { acc[r].x = acc[r].x + v.x; acc[r].y = acc[r].y + v.y; }  // p_0 + G
+        else { acc[r].x = v.x + acc[r].x; acc[r].y = v.y + acc[r].y; }              // G + p_last
       }
-    }
-    if (!last) {
-      double2* P = a.partial + (w.slot + w.chunk) * (int64_t)(GM_MT * GM_NT);
+    } else {
+      double2* P = a.partial + (w.slot + w.chunk) * TS;
 #pragma unroll
       for (int r = 0; r < RM; ++r) P[(rbase + r) * GM_NT + col] = acc[r];
       __threadfence();
       __syncthreads();
-      if (tid == 0) atomicAdd(arrive + w.tile, 1);
-      finalize = false;
-    }
-  } else if (w.nchunks > 1) {
-    // last arriver sums all partials in chunk order
-    double2* P = a.partial + (w.slot + w.chunk) * (int64_t)(GM_MT * GM_NT);
+      const int group = crit_mode ? w.nchunks - 1 : w.nchunks;
+      if (tid == 0) *s_last = (atomicAdd(arrive + w.tile, 1) == group - 1);
+      __syncthreads();
+      finalize = *s_last;
+      if (finalize) {
+        __threadfence();
 #pragma unroll
-    for (int r = 0; r < RM; ++r) P[(rbase + r) * GM_NT + col] = acc[r];
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) *s_last = (atomicAdd(arrive + w.tile, 1) == w.nchunks - 1);
-    __syncthreads();
-    finalize = *s_last;
-    if (finalize) {
-      __threadfence();
+        for (int r = 0; r < RM; ++r) acc[r] = make_double2(0.0, 0.0);
+        for (int c = 0; c < w.nchunks; ++c) {
+          if (c == w.crit) continue;
+          const double2* Q = a.partial + (w.slot + c) * TS;
 #pragma unroll
-      for (int r = 0; r < RM; ++r) acc[r] = make_double2(0.0, 0.0);
-      for (int c = 0; c < w.nchunks; ++c) {
-        const double2* Q = a.partial + (w.slot + c) * (int64_t)(GM_MT * GM_NT);
+          for (int r = 0; r < RM; ++r) {
+            const double2 v = __ldcg(Q + (rbase + r) * GM_NT + col);
+            acc[r].x += v.x;
+            acc[r].y += v.y;
+          }
+        }
+        if (crit_mode) {        // publish the group sum for the critical chunk
+          double2* G = a.partial + (w.slot + w.crit) * TS;
 #pragma unroll
-        for (int r = 0; r < RM; ++r) {
-          const double2 v = __ldcg(Q + (rbase + r) * GM_NT + col);
-          acc[r].x += v.x;
-          acc[r].y += v.y;
+          for (int r = 0; r < RM; ++r) G[(rbase + r) * GM_NT + col] = acc[r];
+          __threadfence();
+          __syncthreads();
+          if (tid == 0) atomicAdd(arrive + w.tile, 1);
+          finalize = false;
         }
       }
     }
