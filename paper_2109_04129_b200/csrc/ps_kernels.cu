@@ -74,14 +74,12 @@ struct KTab {
   int32_t kSc[GM_CHUNK_K];
 };
 
-constexpr int A_PER_T = GM_MT * KC / 256;   // 3 A elements per thread per k-step
+constexpr int A_PER_T = GM_MT * KC / 256;   // 2 A elements per thread per k-step
 constexpr int B_PER_T = GM_NT * KC / 256;   // 4 B elements per thread per k-step
 constexpr int AS_LD = GM_MT;                // As[k][i]
 constexpr int BS_LD = GM_NT;                // Bs[k][c]
-
-struct StepRegs {
-  double2 a[A_PER_T], b[B_PER_T];
-};
+constexpr int NSTAGE = 3;                   // cp.async pipeline depth
+constexpr int STAGE_A = KC * AS_LD, STAGE_B = KC * BS_LD;
 
 __device__ __forceinline__ void a_map(bool a_km, int e, int& i, int& k) {
   if (a_km) { k = e & (KC - 1); i = e / KC; } else { i = e % GM_MT; k = e / GM_MT; }
@@ -90,48 +88,57 @@ __device__ __forceinline__ void b_map(bool b_km, int e, int& c, int& k) {
   if (b_km) { k = e & (KC - 1); c = e / KC; } else { c = e & (GM_NT - 1); k = e / GM_NT; }
 }
 
-__device__ __forceinline__ void fetch_step(const KTab& kt, int k0, int klen, int i0, int c0, int mm,
-                                           int nn, bool a_km, bool b_km,
-                                           const double2* __restrict__ Ab,
-                                           const double2* __restrict__ Bb, int tid, StepRegs& r) {
+// 16-byte global -> shared async copy (L2 only, .cg); zero-fills when !valid.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  const int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ void issue_a(const KTab& kt, int k0, int klen, int i0, int mm, bool a_km,
+                                        const double2* __restrict__ Ab, int tid, double2* As) {
 #pragma unroll
   for (int q = 0; q < A_PER_T; ++q) {
     int i, k;
     a_map(a_km, tid + q * 256, i, k);
     const int kk = k0 + k;
-    r.a[q] = (i < mm && kk < klen) ? __ldg(Ab + kt.kA[kk] + (int64_t)(i0 + i) * kt.kSi[kk])
-                                   : make_double2(0.0, 0.0);
+    const bool v = (i < mm && kk < klen);
+    const double2* src = v ? Ab + kt.kA[kk] + (int64_t)(i0 + i) * kt.kSi[kk] : Ab;
+    cp_async16(As + k * AS_LD + i, src, v);
   }
+}
+__device__ __forceinline__ void issue_b(const KTab& kt, int k0, int klen, int c0, int nn, bool b_km,
+                                        const double2* __restrict__ Bb, int tid, double2* Bs) {
 #pragma unroll
   for (int q = 0; q < B_PER_T; ++q) {
     int c, k;
     b_map(b_km, tid + q * 256, c, k);
     const int kk = k0 + k;
-    r.b[q] = (c < nn && kk < klen) ? __ldcg(Bb + kt.kB[kk] + (int64_t)(c0 + c) * kt.kSc[kk])
-                                   : make_double2(0.0, 0.0);
+    const bool v = (c < nn && kk < klen);
+    const double2* src = v ? Bb + kt.kB[kk] + (int64_t)(c0 + c) * kt.kSc[kk] : Bb;
+    cp_async16(Bs + k * BS_LD + c, src, v);
   }
 }
 
-__device__ __forceinline__ void store_step(bool a_km, bool b_km, int tid, const StepRegs& r,
-                                           double2* As, double2* Bs) {
-#pragma unroll
-  for (int q = 0; q < A_PER_T; ++q) {
-    int i, k;
-    a_map(a_km, tid + q * 256, i, k);
-    As[k * AS_LD + i] = r.a[q];
-  }
-#pragma unroll
-  for (int q = 0; q < B_PER_T; ++q) {
-    int c, k;
-    b_map(b_km, tid + q * 256, c, k);
-    Bs[k * BS_LD + c] = r.b[q];
-  }
+// release / acquire flag operations (one thread, after / before a CTA barrier)
+__device__ __forceinline__ void red_release(int32_t* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int atom_acq_rel(int32_t* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
 }
 
-constexpr size_t FLOW_SMEM = 2 * (size_t)KC * (AS_LD + BS_LD) * sizeof(double2) + sizeof(KTab);
+constexpr size_t FLOW_SMEM = (size_t)NSTAGE * (STAGE_A + STAGE_B) * sizeof(double2) + sizeof(KTab);
 
-// Everything of one work item after its producers are complete, for a
-// compile-time rows-per-warp RM (so the FMA stream is branch-free).
+// Everything of one work item, for a compile-time rows-per-warp RM (so the
+// FMA stream is branch-free). A operands (operator panels: immutable in the
+// launch) of the first stages are requested before waiting for the producers
+// of the B operands.
 template <int RM>
 __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, const GTask& T,
                                           const KTab& kt, double2* As0, double2* Bs0, int tid,
@@ -143,32 +150,58 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
   const int col = wn * 32 + lane;
   int32_t* done = a.counters + 1;
   int32_t* arrive = a.counters + 1 + a.n_units;
+  const bool a_km = T.a_kmajor != 0, b_km = T.b_kmajor != 0;
+  const int nsteps = (klen + KC - 1) / KC;
+  // ---- prologue part 1: A of stages 0..NSTAGE-2 (one group) ----
+#pragma unroll
+  for (int s = 0; s < NSTAGE - 1; ++s)
+    if (s < nsteps) issue_a(kt, s * KC, klen, i0, mm, a_km, a.A, tid, As0 + s * STAGE_A);
+  cp_commit();
+  // ---- wait for the producers of B (warp 0, one segment per lane) ----
+  if (tid < 32) {
+    for (int t = w.ta + tid; t < w.tb; t += 32) {
+      const int dep = a.terms[t].dep;
+      if (dep >= 0) {
+        const int32_t need = a.tasks[dep].n_mt;
+        const int32_t* flag = done + a.tasks[dep].unit0 + w.nt;
+        while (ld_acquire(flag) < need) __nanosleep(32);
+      }
+    }
+  }
+  __syncthreads();
+  if (tr) tr[3] = gtimer();
+  // ---- prologue part 2: B of stages 0..NSTAGE-2 (one group each) ----
+#pragma unroll
+  for (int s = 0; s < NSTAGE - 1; ++s) {
+    if (s < nsteps) issue_b(kt, s * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + s * STAGE_B);
+    cp_commit();
+  }
   double2 acc[RM];
 #pragma unroll
   for (int r = 0; r < RM; ++r) acc[r] = make_double2(0.0, 0.0);
-  const bool a_km = T.a_kmajor != 0, b_km = T.b_kmajor != 0;
-  if (klen > 0) {
-    StepRegs rg;
-    fetch_step(kt, 0, klen, i0, c0, mm, nn, a_km, b_km, a.A, a.B, tid, rg);
-    store_step(a_km, b_km, tid, rg, As0, Bs0);
+  for (int s = 0; s < nsteps; ++s) {
+    cp_wait<NSTAGE - 2>();
     __syncthreads();
-    int cur = 0;
-    for (int k0 = 0; k0 < klen; k0 += KC) {
-      const bool nxt = k0 + KC < klen;
-      if (nxt) fetch_step(kt, k0 + KC, klen, i0, c0, mm, nn, a_km, b_km, a.A, a.B, tid, rg);
-      const double2* As = As0 + cur * KC * AS_LD + rbase;
-      const double2* Bs = Bs0 + cur * KC * BS_LD + col;
+    const int st = s % NSTAGE;
+    const double2* As = As0 + st * STAGE_A + rbase;
+    const double2* Bs = Bs0 + st * STAGE_B + col;
 #pragma unroll
-      for (int k = 0; k < KC; ++k) {
-        const double2 b = Bs[k * BS_LD];
+    for (int k = 0; k < KC; ++k) {
+      const double2 b = Bs[k * BS_LD];
 #pragma unroll
-        for (int r = 0; r < RM; ++r) cfma(acc[r], As[k * AS_LD + r], b);
-      }
-      if (nxt) store_step(a_km, b_km, tid, rg, As0 + (cur ^ 1) * KC * AS_LD, Bs0 + (cur ^ 1) * KC * BS_LD);
-      __syncthreads();
-      cur ^= 1;
+      for (int r = 0; r < RM; ++r) cfma(acc[r], As[k * AS_LD + r], b);
     }
+    // refill the stage consumed one iteration ago (all threads are past the barrier above)
+    const int sn = s + NSTAGE - 1;
+    if (sn < nsteps) {
+      const int stn = sn % NSTAGE;
+      issue_a(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * STAGE_A);
+      issue_b(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * STAGE_B);
+    }
+    cp_commit();
   }
+  cp_wait<0>();
+  __syncthreads();          // all warps done with the stage buffers before the next item
   if (tr) tr[4] = gtimer();
   // ---- split-K combine (fixed summation order => deterministic) ----
   bool finalize = true;
@@ -177,10 +210,8 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
     const bool crit_mode = w.crit >= 0;
     if (crit_mode && w.chunk == w.crit) {
       // the other chunks' sum arrives in slot `crit` once arrive[tile] == nchunks
-      if (tid == 0) {
+      if (tid == 0)
         while (ld_acquire(arrive + w.tile) < w.nchunks) __nanosleep(32);
-        __threadfence();
-      }
       __syncthreads();
       const double2* G = a.partial + (w.slot + w.crit) * TS;
 #pragma unroll
@@ -192,15 +223,13 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
     } else {
       double2* P = a.partial + (w.slot + w.chunk) * TS;
 #pragma unroll
-      for (int r = 0; r < RM; ++r) P[(rbase + r) * GM_NT + col] = acc[r];
-      __threadfence();
+      for (int r = 0; r < RM; ++r) __stcg(P + (rbase + r) * GM_NT + col, acc[r]);
       __syncthreads();
       const int group = crit_mode ? w.nchunks - 1 : w.nchunks;
-      if (tid == 0) *s_last = (atomicAdd(arrive + w.tile, 1) == group - 1);
+      if (tid == 0) *s_last = (atom_acq_rel(arrive + w.tile, 1) == group - 1);
       __syncthreads();
       finalize = *s_last;
       if (finalize) {
-        __threadfence();
 #pragma unroll
         for (int r = 0; r < RM; ++r) acc[r] = make_double2(0.0, 0.0);
         for (int c = 0; c < w.nchunks; ++c) {
@@ -216,10 +245,9 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
         if (crit_mode) {        // publish the group sum for the critical chunk
           double2* G = a.partial + (w.slot + w.crit) * TS;
 #pragma unroll
-          for (int r = 0; r < RM; ++r) G[(rbase + r) * GM_NT + col] = acc[r];
-          __threadfence();
+          for (int r = 0; r < RM; ++r) __stcg(G + (rbase + r) * GM_NT + col, acc[r]);
           __syncthreads();
-          if (tid == 0) atomicAdd(arrive + w.tile, 1);
+          if (tid == 0) red_release(arrive + w.tile, 1);
           finalize = false;
         }
       }
@@ -238,13 +266,12 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
             v.x += z.x;
             v.y += z.y;
           }
-          a.O[T.oO + (int64_t)(i0 + i) * T.sOi + (int64_t)(c0 + col) * T.sOc] = v;
+          __stcg(a.O + T.oO + (int64_t)(i0 + i) * T.sOi + (int64_t)(c0 + col) * T.sOc, v);
         }
       }
     }
-    __threadfence();
     __syncthreads();
-    if (tid == 0) atomicAdd(done + T.unit0 + w.nt, 1);
+    if (tid == 0) red_release(done + T.unit0 + w.nt, 1);
   }
 }
 
@@ -256,14 +283,13 @@ __global__ void __launch_bounds__(256, 2)
 flow_kernel(const FlowArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* As0 = reinterpret_cast<double2*>(smem_raw);
-  double2* Bs0 = As0 + 2 * KC * AS_LD;
-  KTab& kt = *reinterpret_cast<KTab*>(Bs0 + 2 * KC * BS_LD);
+  double2* Bs0 = As0 + NSTAGE * STAGE_A;
+  KTab& kt = *reinterpret_cast<KTab*>(Bs0 + NSTAGE * STAGE_B);
   __shared__ int s_item, s_last;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int wm = warp % GM_WM, wn = warp / GM_WM;
   int32_t* ticket = a.counters;
-  int32_t* done = a.counters + 1;
   for (;;) {
     if (tid == 0) s_item = atomicAdd(ticket, 1);
     __syncthreads();
@@ -287,20 +313,7 @@ flow_kernel(const FlowArgs a) {
         kt.kSc[k - w.ka] = (int32_t)g.sBc;
       }
     }
-    // ---- wait for producers (warp 0, one segment per lane) ----
-    if (tid < 32) {
-      for (int t = w.ta + tid; t < w.tb; t += 32) {
-        const int dep = a.terms[t].dep;
-        if (dep >= 0) {
-          const int32_t need = a.tasks[dep].n_mt;
-          const int32_t* flag = done + a.tasks[dep].unit0 + w.nt;
-          while (ld_acquire(flag) < need) __nanosleep(64);
-        }
-      }
-      __threadfence();
-    }
     __syncthreads();
-    if (tr) tr[3] = gtimer();
     switch (RM) {
 #define PS_RM_CASE(R) \
       case R: item_body<R>(a, w, T, kt, As0, Bs0, tid, lane, wm, wn, &s_last, tr); break;
