@@ -250,6 +250,7 @@ def main():
         ms_e2e = float(t.item())
 
     # ---- roofline of the dominant kernel (gather-GEMM), per-launch events ----
+    args.profile_steps = max(1, args.profile_steps)
     h.profile(True)
     for _ in range(args.profile_steps):
         h.solve(Bd, Xd, stream=st, want_norms=False)
