@@ -64,9 +64,9 @@ __device__ __forceinline__ int ld_acquire(const int32_t* p) {
   return v;
 }
 
-// Per-item k tables: for the item's virtual k range [ka, kb) the A column
-// base, A row stride, B row base and B column stride of every k (built from the
-// segment list at item start), so k-steps run densely across segments.
+// Per-item k tables (producer-private): for the item's virtual k range
+// [ka, kb) the A column base, A row stride, B row base and B column stride of
+// every k, built from the segment list, so k-steps run densely across segments.
 struct KTab {
   int64_t kA[GM_CHUNK_K];
   int64_t kB[GM_CHUNK_K];
@@ -74,56 +74,58 @@ struct KTab {
   int32_t kSc[GM_CHUNK_K];
 };
 
-constexpr int A_PER_T = GM_MT * KC / 256;   // 2 A elements per thread per k-step
-constexpr int B_PER_T = GM_NT * KC / 256;   // 4 B elements per thread per k-step
-constexpr int AS_LD = GM_MT;                // As[k][i]
-constexpr int BS_LD = GM_NT;                // Bs[k][c]
-constexpr int NSTAGE = 3;                   // cp.async pipeline depth
+constexpr int NCW = 8;                      // consumer (MMA) warps
+constexpr int NTHREADS = (NCW + 1) * 32;    // + 1 producer warp
+constexpr int AS_LD = GM_MT;                // stage A tile: As[k][i]
+constexpr int BS_LD = GM_NT;                // stage B tile: Bs[k][c]
+constexpr int NSTAGE = 4;                   // operand ring depth
 constexpr int STAGE_A = KC * AS_LD, STAGE_B = KC * BS_LD;
 
-__device__ __forceinline__ void a_map(bool a_km, int e, int& i, int& k) {
-  if (a_km) { k = e & (KC - 1); i = e / KC; } else { i = e % GM_MT; k = e / GM_MT; }
-}
-__device__ __forceinline__ void b_map(bool b_km, int e, int& c, int& k) {
-  if (b_km) { k = e & (KC - 1); c = e / KC; } else { c = e & (GM_NT - 1); k = e / GM_NT; }
-}
+struct ItemDesc {
+  GWork w;
+  GTask T;
+  int64_t item;
+  int32_t nsteps, end;
+};
 
+struct FlowSmem {
+  double2 A[NSTAGE][STAGE_A];
+  double2 B[NSTAGE][STAGE_B];
+  KTab kt;
+  ItemDesc desc[2];
+  unsigned long long full[NSTAGE], empty[NSTAGE], ifull[2], iempty[2];
+  int s_last;
+};
+constexpr size_t FLOW_SMEM = sizeof(FlowSmem);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, int parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT%=;\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+// arrive on b once every cp.async this thread issued so far has landed
+__device__ __forceinline__ void cp_arrive(unsigned long long* b) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
+}
 // 16-byte global -> shared async copy (L2 only, .cg); zero-fills when !valid.
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
-  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
   const int n = valid ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(n) : "memory");
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem), "r"(n)
+               : "memory");
 }
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
-__device__ __forceinline__ void issue_a(const KTab& kt, int k0, int klen, int i0, int mm, bool a_km,
-                                        const double2* __restrict__ Ab, int tid, double2* As) {
-#pragma unroll
-  for (int q = 0; q < A_PER_T; ++q) {
-    int i, k;
-    a_map(a_km, tid + q * 256, i, k);
-    const int kk = k0 + k;
-    const bool v = (i < mm && kk < klen);
-    const double2* src = v ? Ab + kt.kA[kk] + (int64_t)(i0 + i) * kt.kSi[kk] : Ab;
-    cp_async16(As + k * AS_LD + i, src, v);
-  }
-}
-__device__ __forceinline__ void issue_b(const KTab& kt, int k0, int klen, int c0, int nn, bool b_km,
-                                        const double2* __restrict__ Bb, int tid, double2* Bs) {
-#pragma unroll
-  for (int q = 0; q < B_PER_T; ++q) {
-    int c, k;
-    b_map(b_km, tid + q * 256, c, k);
-    const int kk = k0 + k;
-    const bool v = (c < nn && kk < klen);
-    const double2* src = v ? Bb + kt.kB[kk] + (int64_t)(c0 + c) * kt.kSc[kk] : Bb;
-    cp_async16(Bs + k * BS_LD + c, src, v);
-  }
-}
-
-// release / acquire flag operations (one thread, after / before a CTA barrier)
+// release / acquire flag operations (one thread, after / before a barrier)
 __device__ __forceinline__ void red_release(int32_t* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -133,33 +135,94 @@ __device__ __forceinline__ int atom_acq_rel(int32_t* p, int v) {
   return old;
 }
 
-constexpr size_t FLOW_SMEM = (size_t)NSTAGE * (STAGE_A + STAGE_B) * sizeof(double2) + sizeof(KTab);
+// producer: one k-step's A (GM_MT x KC) / B (KC x GM_NT) tile, 16 / 32 copies per lane
+__device__ __forceinline__ void issue_a(const KTab& kt, int k0, int klen, int i0, int mm, bool a_km,
+                                        const double2* __restrict__ Ab, int lane, double2* As) {
+#pragma unroll 4
+  for (int q = 0; q < GM_MT * KC / 32; ++q) {
+    const int e = lane + 32 * q;
+    int i, k;
+    if (a_km) { k = e & (KC - 1); i = e / KC; } else { i = e % GM_MT; k = e / GM_MT; }
+    const int kk = k0 + k;
+    const bool v = (i < mm && kk < klen);
+    const double2* src = v ? Ab + kt.kA[kk] + (int64_t)(i0 + i) * kt.kSi[kk] : Ab;
+    cp_async16(As + k * AS_LD + i, src, v);
+  }
+}
+__device__ __forceinline__ void issue_b(const KTab& kt, int k0, int klen, int c0, int nn, bool b_km,
+                                        const double2* __restrict__ Bb, int lane, double2* Bs) {
+#pragma unroll 4
+  for (int q = 0; q < GM_NT * KC / 32; ++q) {
+    const int e = lane + 32 * q;
+    int c, k;
+    if (b_km) { k = e & (KC - 1); c = e / KC; } else { c = e & (GM_NT - 1); k = e / GM_NT; }
+    const int kk = k0 + k;
+    const bool v = (c < nn && kk < klen);
+    const double2* src = v ? Bb + kt.kB[kk] + (int64_t)(c0 + c) * kt.kSc[kk] : Bb;
+    cp_async16(Bs + k * BS_LD + c, src, v);
+  }
+}
 
-// Everything of one work item, for a compile-time rows-per-warp RM (so the
-// FMA stream is branch-free). A operands (operator panels: immutable in the
-// launch) of the first stages are requested before waiting for the producers
-// of the B operands.
-template <int RM>
-__device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, const GTask& T,
-                                          const KTab& kt, double2* As0, double2* Bs0, int tid,
-                                          int lane, int wm, int wn, int* s_last, int64_t* tr) {
-  const int i0 = w.mt * GM_MT, c0 = w.nt * GM_NT;
-  const int mm = min(GM_MT, T.m - i0), nn = min(GM_NT, T.n - c0);
-  const int klen = w.kb - w.ka;
-  const int rbase = wm * RM;
-  const int col = wn * 32 + lane;
+// ---- producer warp: tickets, k tables, dependency waits, operand stream ----
+__device__ void producer_loop(const FlowArgs& a, FlowSmem& sm, int lane) {
+  int32_t* ticket = a.counters;
   int32_t* done = a.counters + 1;
-  int32_t* arrive = a.counters + 1 + a.n_units;
-  const bool a_km = T.a_kmajor != 0, b_km = T.b_kmajor != 0;
-  const int nsteps = (klen + KC - 1) / KC;
-  // ---- prologue part 1: A of stages 0..NSTAGE-2 (one group) ----
-#pragma unroll
-  for (int s = 0; s < NSTAGE - 1; ++s)
-    if (s < nsteps) issue_a(kt, s * KC, klen, i0, mm, a_km, a.A, tid, As0 + s * STAGE_A);
-  cp_commit();
-  // ---- wait for the producers of B (warp 0, one segment per lane) ----
-  if (tid < 32) {
-    for (int t = w.ta + tid; t < w.tb; t += 32) {
+  int64_t g = 0;      // stage sequence number (shared convention with the consumers)
+  int j = 0;          // item sequence number of this CTA
+  for (;; ++j) {
+    int item = 0;
+    if (lane == 0) item = atomicAdd(ticket, 1);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    const int slot = j & 1, ir = j >> 1;
+    if (ir > 0) mbar_wait(&sm.iempty[slot], (ir - 1) & 1);
+    ItemDesc& D = sm.desc[slot];
+    if (item >= a.nwork) {
+      if (lane == 0) {
+        D.end = 1;
+        mbar_arrive(&sm.ifull[slot]);
+      }
+      return;
+    }
+    int64_t* tr = (a.trace != nullptr && lane == 0) ? a.trace + 6 * (int64_t)item : nullptr;
+    if (tr) { tr[0] = item; tr[1] = smid(); tr[2] = gtimer(); }
+    const GWork w = a.work[item];
+    const GTask T = a.tasks[w.task];
+    const int klen = w.kb - w.ka;
+    const int nsteps = (klen + KC - 1) / KC;
+    // k table (lanes over segments)
+    for (int t = w.ta + lane; t < w.tb; t += 32) {
+      const GTerm gt = a.terms[t];
+      const int lo = max(gt.kstart, w.ka), hi = min(gt.kstart + gt.K, w.kb);
+      for (int k = lo; k < hi; ++k) {
+        const int64_t d = k - gt.kstart;
+        sm.kt.kA[k - w.ka] = gt.oA + d * gt.sAk;
+        sm.kt.kB[k - w.ka] = gt.oB + d * gt.sBk;
+        sm.kt.kSi[k - w.ka] = (int32_t)gt.sAi;
+        sm.kt.kSc[k - w.ka] = (int32_t)gt.sBc;
+      }
+    }
+    if (lane == 0) {
+      D.w = w;
+      D.T = T;
+      D.item = item;
+      D.nsteps = nsteps;
+      D.end = 0;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.ifull[slot]);
+    const int i0 = w.mt * GM_MT, c0 = w.nt * GM_NT;
+    const int mm = min(GM_MT, T.m - i0), nn = min(GM_NT, T.n - c0);
+    const bool a_km = T.a_kmajor != 0, b_km = T.b_kmajor != 0;
+    // A (immutable operator) of the first stages before waiting for B's producers
+    const int npre = min(NSTAGE, nsteps);
+    for (int s = 0; s < npre; ++s) {
+      const int64_t gs = g + s;
+      const int st = (int)(gs % NSTAGE);
+      const int64_t r = gs / NSTAGE;
+      if (r > 0) mbar_wait(&sm.empty[st], (int)((r - 1) & 1));
+      issue_a(sm.kt, s * KC, klen, i0, mm, a_km, a.A, lane, sm.A[st]);
+    }
+    for (int t = w.ta + lane; t < w.tb; t += 32) {
       const int dep = a.terms[t].dep;
       if (dep >= 0) {
         const int32_t need = a.tasks[dep].n_mt;
@@ -167,41 +230,53 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
         while (ld_acquire(flag) < need) __nanosleep(32);
       }
     }
+    __syncwarp();
+    if (tr) tr[3] = gtimer();
+    for (int s = 0; s < nsteps; ++s) {
+      const int64_t gs = g + s;
+      const int st = (int)(gs % NSTAGE);
+      if (s >= npre) {
+        const int64_t r = gs / NSTAGE;
+        if (r > 0) mbar_wait(&sm.empty[st], (int)((r - 1) & 1));
+        issue_a(sm.kt, s * KC, klen, i0, mm, a_km, a.A, lane, sm.A[st]);
+      }
+      issue_b(sm.kt, s * KC, klen, c0, nn, b_km, a.B, lane, sm.B[st]);
+      cp_arrive(&sm.full[st]);
+    }
+    g += nsteps;
   }
-  __syncthreads();
-  if (tr) tr[3] = gtimer();
-  // ---- prologue part 2: B of stages 0..NSTAGE-2 (one group each) ----
-#pragma unroll
-  for (int s = 0; s < NSTAGE - 1; ++s) {
-    if (s < nsteps) issue_b(kt, s * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + s * STAGE_B);
-    cp_commit();
-  }
+}
+
+// ---- consumer warps: FMA stream for a compile-time rows-per-warp RM, then
+// the split-K combine / finalize / publish of the item ----
+template <int RM>
+__device__ __forceinline__ void consume_item(const FlowArgs& a, FlowSmem& sm, const GWork& w,
+                                             const GTask& T, int nsteps, int64_t g, int ctid,
+                                             int lane, int wm, int wn, int64_t* tr) {
+  const int i0 = w.mt * GM_MT, c0 = w.nt * GM_NT;
+  const int mm = min(GM_MT, T.m - i0), nn = min(GM_NT, T.n - c0);
+  const int rbase = wm * RM;
+  const int col = wn * 32 + lane;
+  int32_t* done = a.counters + 1;
+  int32_t* arrive = a.counters + 1 + a.n_units;
   double2 acc[RM];
 #pragma unroll
   for (int r = 0; r < RM; ++r) acc[r] = make_double2(0.0, 0.0);
   for (int s = 0; s < nsteps; ++s) {
-    cp_wait<NSTAGE - 2>();
-    __syncthreads();
-    const int st = s % NSTAGE;
-    const double2* As = As0 + st * STAGE_A + rbase;
-    const double2* Bs = Bs0 + st * STAGE_B + col;
+    const int64_t gs = g + s;
+    const int st = (int)(gs % NSTAGE);
+    mbar_wait(&sm.full[st], (int)((gs / NSTAGE) & 1));
+    const double2* As = sm.A[st] + rbase;
+    const double2* Bs = sm.B[st] + col;
 #pragma unroll
     for (int k = 0; k < KC; ++k) {
       const double2 b = Bs[k * BS_LD];
 #pragma unroll
       for (int r = 0; r < RM; ++r) cfma(acc[r], As[k * AS_LD + r], b);
     }
-    // refill the stage consumed one iteration ago (all threads are past the barrier above)
-    const int sn = s + NSTAGE - 1;
-    if (sn < nsteps) {
-      const int stn = sn % NSTAGE;
-      issue_a(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * STAGE_A);
-      issue_b(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * STAGE_B);
-    }
-    cp_commit();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[st]);
   }
-  cp_wait<0>();
-  __syncthreads();          // all warps done with the stage buffers before the next item
   if (tr) tr[4] = gtimer();
   // ---- split-K combine (fixed summation order => deterministic) ----
   bool finalize = true;
@@ -210,9 +285,9 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
     const bool crit_mode = w.crit >= 0;
     if (crit_mode && w.chunk == w.crit) {
       // the other chunks' sum arrives in slot `crit` once arrive[tile] == nchunks
-      if (tid == 0)
+      if (ctid == 0)
         while (ld_acquire(arrive + w.tile) < w.nchunks) __nanosleep(32);
-      __syncthreads();
+      consumers_sync();
       const double2* G = a.partial + (w.slot + w.crit) * TS;
 #pragma unroll
       for (int r = 0; r < RM; ++r) {
@@ -224,11 +299,11 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
       double2* P = a.partial + (w.slot + w.chunk) * TS;
 #pragma unroll
       for (int r = 0; r < RM; ++r) __stcg(P + (rbase + r) * GM_NT + col, acc[r]);
-      __syncthreads();
+      consumers_sync();
       const int group = crit_mode ? w.nchunks - 1 : w.nchunks;
-      if (tid == 0) *s_last = (atom_acq_rel(arrive + w.tile, 1) == group - 1);
-      __syncthreads();
-      finalize = *s_last;
+      if (ctid == 0) sm.s_last = (atom_acq_rel(arrive + w.tile, 1) == group - 1);
+      consumers_sync();
+      finalize = sm.s_last;
       if (finalize) {
 #pragma unroll
         for (int r = 0; r < RM; ++r) acc[r] = make_double2(0.0, 0.0);
@@ -246,8 +321,8 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
           double2* G = a.partial + (w.slot + w.crit) * TS;
 #pragma unroll
           for (int r = 0; r < RM; ++r) __stcg(G + (rbase + r) * GM_NT + col, acc[r]);
-          __syncthreads();
-          if (tid == 0) red_release(arrive + w.tile, 1);
+          consumers_sync();
+          if (ctid == 0) red_release(arrive + w.tile, 1);
           finalize = false;
         }
       }
@@ -270,60 +345,64 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
         }
       }
     }
-    __syncthreads();
-    if (tid == 0) red_release(done + T.unit0 + w.nt, 1);
+    consumers_sync();
+    if (ctid == 0) red_release(done + T.unit0 + w.nt, 1);
   }
+  if (tr) tr[5] = gtimer();
 }
 
-// Output tile: warp w = (wm, wn) = (w % 4, w / 4) owns rows
-// [wm*RM, min(mm, (wm+1)*RM)) with RM = ceil(mm / 4) <= 8 (so the tile is
-// only as tall as the task) and column wn*32 + lane. A values are broadcast
-// shared loads, one B load feeds RM complex FMAs.
-__global__ void __launch_bounds__(256, 2)
+// Persistent dataflow gather-GEMM. Warps 0-7 consume: output
+// tile 32 x 64, warp (wm, wn) = (w % 4, w / 4) owns RM = ceil(rows / 4) <= 8
+// rows and column wn*32 + lane. Warp 8 produces: it takes tickets (topological
+// order), builds the k table, waits for the producers of B, and streams A/B
+// k-step tiles into a 4-deep cp.async + mbarrier ring, running ahead into the
+// next item while the consumers finish and publish the current one.
+__global__ void __launch_bounds__(NTHREADS, 2)
 flow_kernel(const FlowArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* As0 = reinterpret_cast<double2*>(smem_raw);
-  double2* Bs0 = As0 + NSTAGE * STAGE_A;
-  KTab& kt = *reinterpret_cast<KTab*>(Bs0 + NSTAGE * STAGE_B);
-  __shared__ int s_item, s_last;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  FlowSmem& sm = *reinterpret_cast<FlowSmem*>(smem_raw);
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < NSTAGE; ++s) {
+      mbar_init(&sm.full[s], 32);      // one cp.async arrive per producer lane
+      mbar_init(&sm.empty[s], NCW);    // one arrive per consumer warp
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&sm.ifull[s], 1);
+      mbar_init(&sm.iempty[s], NCW);
+    }
+  }
+  __syncthreads();
+  if (warp == NCW) {
+    producer_loop(a, sm, lane);
+    return;
+  }
   const int wm = warp % GM_WM, wn = warp / GM_WM;
-  int32_t* ticket = a.counters;
-  for (;;) {
-    if (tid == 0) s_item = atomicAdd(ticket, 1);
-    __syncthreads();
-    const int64_t item = s_item;
-    if (item >= a.nwork) return;
+  int64_t g = 0;
+  for (int j = 0;; ++j) {
+    const int slot = j & 1;
+    mbar_wait(&sm.ifull[slot], (j >> 1) & 1);
+    const ItemDesc& D = sm.desc[slot];
+    if (D.end) return;
+    const GWork w = D.w;
+    const GTask T = D.T;
+    const int nsteps = D.nsteps;
+    const int64_t item = D.item;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.iempty[slot]);     // descriptor copied: slot reusable
     int64_t* tr = (a.trace != nullptr && tid == 0) ? a.trace + 6 * item : nullptr;
-    if (tr) { tr[0] = item; tr[1] = smid(); tr[2] = gtimer(); }
-    const GWork w = a.work[item];
-    const GTask T = a.tasks[w.task];
     const int mm = min(GM_MT, T.m - w.mt * GM_MT);
     const int RM = (mm + GM_WM - 1) / GM_WM;
-    // ---- k tables of this item (segments [ta, tb) clipped to [ka, kb)) ----
-    for (int t = w.ta + tid; t < w.tb; t += 256) {
-      const GTerm g = a.terms[t];
-      const int lo = max(g.kstart, w.ka), hi = min(g.kstart + g.K, w.kb);
-      for (int k = lo; k < hi; ++k) {
-        const int64_t d = k - g.kstart;
-        kt.kA[k - w.ka] = g.oA + d * g.sAk;
-        kt.kB[k - w.ka] = g.oB + d * g.sBk;
-        kt.kSi[k - w.ka] = (int32_t)g.sAi;
-        kt.kSc[k - w.ka] = (int32_t)g.sBc;
-      }
-    }
-    __syncthreads();
     switch (RM) {
 #define PS_RM_CASE(R) \
-      case R: item_body<R>(a, w, T, kt, As0, Bs0, tid, lane, wm, wn, &s_last, tr); break;
+      case R: consume_item<R>(a, sm, w, T, nsteps, g, tid, lane, wm, wn, tr); break;
       PS_RM_CASE(1) PS_RM_CASE(2) PS_RM_CASE(3) PS_RM_CASE(4) PS_RM_CASE(5) PS_RM_CASE(6)
       PS_RM_CASE(7) PS_RM_CASE(8)
 #undef PS_RM_CASE
       default: break;
     }
-    if (tr) tr[5] = gtimer();
-    __syncthreads();
+    g += nsteps;
   }
 }
 
@@ -334,7 +413,7 @@ int flow_resident_ctas() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(flow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FLOW_SMEM);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, flow_kernel, 256, FLOW_SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, flow_kernel, NTHREADS, FLOW_SMEM);
     n = sms * (per_sm > 0 ? per_sm : 1);
   }
   return n;
@@ -344,7 +423,7 @@ void launch_flow(const FlowArgs& a, int grid, cudaStream_t st) {
   if (a.nwork <= 0) return;
   int g = grid > 0 ? grid : flow_resident_ctas();
   if (g > a.nwork) g = (int)a.nwork;
-  flow_kernel<<<g, 256, FLOW_SMEM, st>>>(a);
+  flow_kernel<<<g, NTHREADS, FLOW_SMEM, st>>>(a);
 }
 
 // ---------------------------------------------------------------------------
