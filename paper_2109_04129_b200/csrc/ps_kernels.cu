@@ -64,7 +64,7 @@ __device__ __forceinline__ int ld_acquire(const int32_t* p) {
   return v;
 }
 
-// Per-item k tables (producer-private): for the item's virtual k range
+// Per-item k tables (built by the scheduler warp, double buffered): for the item's virtual k range
 // [ka, kb) the A column base, A row stride, B row base and B column stride of
 // every k, built from the segment list, so k-steps run densely across segments.
 struct KTab {
@@ -74,12 +74,14 @@ struct KTab {
   int32_t kSc[GM_CHUNK_K];
 };
 
-constexpr int NCW = 8;                      // consumer (MMA) warps
-constexpr int NTHREADS = (NCW + 1) * 32;    // + 1 producer warp
+constexpr int NCW = 8;                      // compute warps
+constexpr int NTHREADS = (NCW + 1) * 32;    // + 1 scheduler warp
 constexpr int AS_LD = GM_MT;                // stage A tile: As[k][i]
 constexpr int BS_LD = GM_NT;                // stage B tile: Bs[k][c]
-constexpr int NSTAGE = 4;                   // operand ring depth
+constexpr int NSTAGE = 3;                   // cp.async pipeline depth
 constexpr int STAGE_A = KC * AS_LD, STAGE_B = KC * BS_LD;
+constexpr int A_PER_T = GM_MT * KC / 256;   // 2 A copies per compute thread per k-step
+constexpr int B_PER_T = GM_NT * KC / 256;   // 4 B copies per compute thread per k-step
 
 struct ItemDesc {
   GWork w;
@@ -91,9 +93,9 @@ struct ItemDesc {
 struct FlowSmem {
   double2 A[NSTAGE][STAGE_A];
   double2 B[NSTAGE][STAGE_B];
-  KTab kt;
+  KTab kt[2];
   ItemDesc desc[2];
-  unsigned long long full[NSTAGE], empty[NSTAGE], ifull[2], iempty[2];
+  unsigned long long ifull[2], ideps[2], iempty[2];
   int s_last;
 };
 constexpr size_t FLOW_SMEM = sizeof(FlowSmem);
@@ -113,17 +115,16 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, int parity) {
       "r"(parity)
       : "memory");
 }
-// arrive on b once every cp.async this thread issued so far has landed
-__device__ __forceinline__ void cp_arrive(unsigned long long* b) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
-}
 // 16-byte global -> shared async copy (L2 only, .cg); zero-fills when !valid.
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
   const int n = valid ? 16 : 0;
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem), "r"(n)
                : "memory");
 }
-__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void compute_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 // release / acquire flag operations (one thread, after / before a barrier)
 __device__ __forceinline__ void red_release(int32_t* p, int v) {
@@ -135,12 +136,11 @@ __device__ __forceinline__ int atom_acq_rel(int32_t* p, int v) {
   return old;
 }
 
-// producer: one k-step's A (GM_MT x KC) / B (KC x GM_NT) tile, 16 / 32 copies per lane
 __device__ __forceinline__ void issue_a(const KTab& kt, int k0, int klen, int i0, int mm, bool a_km,
-                                        const double2* __restrict__ Ab, int lane, double2* As) {
-#pragma unroll 4
-  for (int q = 0; q < GM_MT * KC / 32; ++q) {
-    const int e = lane + 32 * q;
+                                        const double2* __restrict__ Ab, int tid, double2* As) {
+#pragma unroll
+  for (int q = 0; q < A_PER_T; ++q) {
+    const int e = tid + 256 * q;
     int i, k;
     if (a_km) { k = e & (KC - 1); i = e / KC; } else { i = e % GM_MT; k = e / GM_MT; }
     const int kk = k0 + k;
@@ -150,10 +150,10 @@ __device__ __forceinline__ void issue_a(const KTab& kt, int k0, int klen, int i0
   }
 }
 __device__ __forceinline__ void issue_b(const KTab& kt, int k0, int klen, int c0, int nn, bool b_km,
-                                        const double2* __restrict__ Bb, int lane, double2* Bs) {
-#pragma unroll 4
-  for (int q = 0; q < GM_NT * KC / 32; ++q) {
-    const int e = lane + 32 * q;
+                                        const double2* __restrict__ Bb, int tid, double2* Bs) {
+#pragma unroll
+  for (int q = 0; q < B_PER_T; ++q) {
+    const int e = tid + 256 * q;
     int c, k;
     if (b_km) { k = e & (KC - 1); c = e / KC; } else { c = e & (GM_NT - 1); k = e / GM_NT; }
     const int kk = k0 + k;
@@ -163,13 +163,11 @@ __device__ __forceinline__ void issue_b(const KTab& kt, int k0, int klen, int c0
   }
 }
 
-// ---- producer warp: tickets, k tables, dependency waits, operand stream ----
-__device__ void producer_loop(const FlowArgs& a, FlowSmem& sm, int lane) {
+// ---- scheduler warp: next item's ticket, descriptor, k table, dependency wait ----
+__device__ void scheduler_loop(const FlowArgs& a, FlowSmem& sm, int lane) {
   int32_t* ticket = a.counters;
   int32_t* done = a.counters + 1;
-  int64_t g = 0;      // stage sequence number (shared convention with the consumers)
-  int j = 0;          // item sequence number of this CTA
-  for (;; ++j) {
+  for (int j = 0;; ++j) {
     int item = 0;
     if (lane == 0) item = atomicAdd(ticket, 1);
     item = __shfl_sync(0xffffffffu, item, 0);
@@ -186,42 +184,27 @@ __device__ void producer_loop(const FlowArgs& a, FlowSmem& sm, int lane) {
     int64_t* tr = (a.trace != nullptr && lane == 0) ? a.trace + 6 * (int64_t)item : nullptr;
     if (tr) { tr[0] = item; tr[1] = smid(); tr[2] = gtimer(); }
     const GWork w = a.work[item];
-    const GTask T = a.tasks[w.task];
-    const int klen = w.kb - w.ka;
-    const int nsteps = (klen + KC - 1) / KC;
-    // k table (lanes over segments)
+    KTab& kt = sm.kt[slot];
     for (int t = w.ta + lane; t < w.tb; t += 32) {
       const GTerm gt = a.terms[t];
       const int lo = max(gt.kstart, w.ka), hi = min(gt.kstart + gt.K, w.kb);
       for (int k = lo; k < hi; ++k) {
         const int64_t d = k - gt.kstart;
-        sm.kt.kA[k - w.ka] = gt.oA + d * gt.sAk;
-        sm.kt.kB[k - w.ka] = gt.oB + d * gt.sBk;
-        sm.kt.kSi[k - w.ka] = (int32_t)gt.sAi;
-        sm.kt.kSc[k - w.ka] = (int32_t)gt.sBc;
+        kt.kA[k - w.ka] = gt.oA + d * gt.sAk;
+        kt.kB[k - w.ka] = gt.oB + d * gt.sBk;
+        kt.kSi[k - w.ka] = (int32_t)gt.sAi;
+        kt.kSc[k - w.ka] = (int32_t)gt.sBc;
       }
     }
     if (lane == 0) {
       D.w = w;
-      D.T = T;
+      D.T = a.tasks[w.task];
       D.item = item;
-      D.nsteps = nsteps;
+      D.nsteps = (w.kb - w.ka + KC - 1) / KC;
       D.end = 0;
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.ifull[slot]);
-    const int i0 = w.mt * GM_MT, c0 = w.nt * GM_NT;
-    const int mm = min(GM_MT, T.m - i0), nn = min(GM_NT, T.n - c0);
-    const bool a_km = T.a_kmajor != 0, b_km = T.b_kmajor != 0;
-    // A (immutable operator) of the first stages before waiting for B's producers
-    const int npre = min(NSTAGE, nsteps);
-    for (int s = 0; s < npre; ++s) {
-      const int64_t gs = g + s;
-      const int st = (int)(gs % NSTAGE);
-      const int64_t r = gs / NSTAGE;
-      if (r > 0) mbar_wait(&sm.empty[st], (int)((r - 1) & 1));
-      issue_a(sm.kt, s * KC, klen, i0, mm, a_km, a.A, lane, sm.A[st]);
-    }
+    if (lane == 0) mbar_arrive(&sm.ifull[slot]);       // descriptor + k table ready
     for (int t = w.ta + lane; t < w.tb; t += 32) {
       const int dep = a.terms[t].dep;
       if (dep >= 0) {
@@ -232,40 +215,43 @@ __device__ void producer_loop(const FlowArgs& a, FlowSmem& sm, int lane) {
     }
     __syncwarp();
     if (tr) tr[3] = gtimer();
-    for (int s = 0; s < nsteps; ++s) {
-      const int64_t gs = g + s;
-      const int st = (int)(gs % NSTAGE);
-      if (s >= npre) {
-        const int64_t r = gs / NSTAGE;
-        if (r > 0) mbar_wait(&sm.empty[st], (int)((r - 1) & 1));
-        issue_a(sm.kt, s * KC, klen, i0, mm, a_km, a.A, lane, sm.A[st]);
-      }
-      issue_b(sm.kt, s * KC, klen, c0, nn, b_km, a.B, lane, sm.B[st]);
-      cp_arrive(&sm.full[st]);
-    }
-    g += nsteps;
+    if (lane == 0) mbar_arrive(&sm.ideps[slot]);       // B operands are final
   }
 }
 
-// ---- consumer warps: FMA stream for a compile-time rows-per-warp RM, then
-// the split-K combine / finalize / publish of the item ----
+// ---- compute warps: cp.async pipeline + FMA stream for a compile-time
+// rows-per-warp RM, then split-K combine / finalize / publish ----
 template <int RM>
-__device__ __forceinline__ void consume_item(const FlowArgs& a, FlowSmem& sm, const GWork& w,
-                                             const GTask& T, int nsteps, int64_t g, int ctid,
-                                             int lane, int wm, int wn, int64_t* tr) {
+__device__ __forceinline__ void compute_item(const FlowArgs& a, FlowSmem& sm, const GWork& w,
+                                             const GTask& T, const KTab& kt, unsigned long long* ideps,
+                                             int dpar, int nsteps, int tid, int lane, int wm, int wn,
+                                             int64_t* tr) {
   const int i0 = w.mt * GM_MT, c0 = w.nt * GM_NT;
   const int mm = min(GM_MT, T.m - i0), nn = min(GM_NT, T.n - c0);
+  const int klen = w.kb - w.ka;
   const int rbase = wm * RM;
   const int col = wn * 32 + lane;
   int32_t* done = a.counters + 1;
   int32_t* arrive = a.counters + 1 + a.n_units;
+  const bool a_km = T.a_kmajor != 0, b_km = T.b_kmajor != 0;
+  // A (immutable operator) of the first stages before the producers of B are done
+#pragma unroll
+  for (int s = 0; s < NSTAGE - 1; ++s)
+    if (s < nsteps) issue_a(kt, s * KC, klen, i0, mm, a_km, a.A, tid, sm.A[s]);
+  cp_commit();
+  mbar_wait(ideps, dpar);
+#pragma unroll
+  for (int s = 0; s < NSTAGE - 1; ++s) {
+    if (s < nsteps) issue_b(kt, s * KC, klen, c0, nn, b_km, a.B, tid, sm.B[s]);
+    cp_commit();
+  }
   double2 acc[RM];
 #pragma unroll
   for (int r = 0; r < RM; ++r) acc[r] = make_double2(0.0, 0.0);
   for (int s = 0; s < nsteps; ++s) {
-    const int64_t gs = g + s;
-    const int st = (int)(gs % NSTAGE);
-    mbar_wait(&sm.full[st], (int)((gs / NSTAGE) & 1));
+    cp_wait<NSTAGE - 2>();
+    compute_sync();
+    const int st = s % NSTAGE;
     const double2* As = sm.A[st] + rbase;
     const double2* Bs = sm.B[st] + col;
 #pragma unroll
@@ -274,9 +260,16 @@ __device__ __forceinline__ void consume_item(const FlowArgs& a, FlowSmem& sm, co
 #pragma unroll
       for (int r = 0; r < RM; ++r) cfma(acc[r], As[k * AS_LD + r], b);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty[st]);
+    const int sn = s + NSTAGE - 1;
+    if (sn < nsteps) {
+      const int stn = sn % NSTAGE;
+      issue_a(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, sm.A[stn]);
+      issue_b(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, sm.B[stn]);
+    }
+    cp_commit();
   }
+  cp_wait<0>();
+  compute_sync();          // stage buffers and this item's k table are free
   if (tr) tr[4] = gtimer();
   // ---- split-K combine (fixed summation order => deterministic) ----
   bool finalize = true;
@@ -285,9 +278,9 @@ __device__ __forceinline__ void consume_item(const FlowArgs& a, FlowSmem& sm, co
     const bool crit_mode = w.crit >= 0;
     if (crit_mode && w.chunk == w.crit) {
       // the other chunks' sum arrives in slot `crit` once arrive[tile] == nchunks
-      if (ctid == 0)
+      if (tid == 0)
         while (ld_acquire(arrive + w.tile) < w.nchunks) __nanosleep(32);
-      consumers_sync();
+      compute_sync();
       const double2* G = a.partial + (w.slot + w.crit) * TS;
 #pragma unroll
       for (int r = 0; r < RM; ++r) {
@@ -299,10 +292,10 @@ __device__ __forceinline__ void consume_item(const FlowArgs& a, FlowSmem& sm, co
       double2* P = a.partial + (w.slot + w.chunk) * TS;
 #pragma unroll
       for (int r = 0; r < RM; ++r) __stcg(P + (rbase + r) * GM_NT + col, acc[r]);
-      consumers_sync();
+      compute_sync();
       const int group = crit_mode ? w.nchunks - 1 : w.nchunks;
-      if (ctid == 0) sm.s_last = (atom_acq_rel(arrive + w.tile, 1) == group - 1);
-      consumers_sync();
+      if (tid == 0) sm.s_last = (atom_acq_rel(arrive + w.tile, 1) == group - 1);
+      compute_sync();
       finalize = sm.s_last;
       if (finalize) {
 #pragma unroll
@@ -321,8 +314,8 @@ __device__ __forceinline__ void consume_item(const FlowArgs& a, FlowSmem& sm, co
           double2* G = a.partial + (w.slot + w.crit) * TS;
 #pragma unroll
           for (int r = 0; r < RM; ++r) __stcg(G + (rbase + r) * GM_NT + col, acc[r]);
-          consumers_sync();
-          if (ctid == 0) red_release(arrive + w.tile, 1);
+          compute_sync();
+          if (tid == 0) red_release(arrive + w.tile, 1);
           finalize = false;
         }
       }
@@ -345,18 +338,20 @@ __device__ __forceinline__ void consume_item(const FlowArgs& a, FlowSmem& sm, co
         }
       }
     }
-    consumers_sync();
-    if (ctid == 0) red_release(done + T.unit0 + w.nt, 1);
+    compute_sync();
+    if (tid == 0) red_release(done + T.unit0 + w.nt, 1);
   }
   if (tr) tr[5] = gtimer();
 }
 
-// Persistent dataflow gather-GEMM. Warps 0-7 consume: output
+// Persistent dataflow gather-GEMM. Warps 0-7 compute: output
 // tile 32 x 64, warp (wm, wn) = (w % 4, w / 4) owns RM = ceil(rows / 4) <= 8
-// rows and column wn*32 + lane. Warp 8 produces: it takes tickets (topological
-// order), builds the k table, waits for the producers of B, and streams A/B
-// k-step tiles into a 4-deep cp.async + mbarrier ring, running ahead into the
-// next item while the consumers finish and publish the current one.
+// rows and column wn*32 + lane; they stream their own operands through a
+// 3-stage cp.async pipeline. Warp 8 schedules: it takes the next ticket
+// (topological order), builds that item's k table (double buffered) and waits
+// for the producers of its B operands while the compute warps are still busy
+// with the current item; readiness is signalled in two mbarrier phases (k table
+// ready -> A may be fetched; dependencies done -> B may be fetched).
 __global__ void __launch_bounds__(NTHREADS, 2)
 flow_kernel(const FlowArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -364,45 +359,40 @@ flow_kernel(const FlowArgs a) {
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
-    for (int s = 0; s < NSTAGE; ++s) {
-      mbar_init(&sm.full[s], 32);      // one cp.async arrive per producer lane
-      mbar_init(&sm.empty[s], NCW);    // one arrive per consumer warp
-    }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&sm.ifull[s], 1);
-      mbar_init(&sm.iempty[s], NCW);
+      mbar_init(&sm.ideps[s], 1);
+      mbar_init(&sm.iempty[s], 1);
     }
   }
   __syncthreads();
   if (warp == NCW) {
-    producer_loop(a, sm, lane);
+    scheduler_loop(a, sm, lane);
     return;
   }
   const int wm = warp % GM_WM, wn = warp / GM_WM;
-  int64_t g = 0;
   for (int j = 0;; ++j) {
-    const int slot = j & 1;
-    mbar_wait(&sm.ifull[slot], (j >> 1) & 1);
+    const int slot = j & 1, par = (j >> 1) & 1;
+    mbar_wait(&sm.ifull[slot], par);
     const ItemDesc& D = sm.desc[slot];
     if (D.end) return;
     const GWork w = D.w;
     const GTask T = D.T;
     const int nsteps = D.nsteps;
     const int64_t item = D.item;
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.iempty[slot]);     // descriptor copied: slot reusable
     int64_t* tr = (a.trace != nullptr && tid == 0) ? a.trace + 6 * item : nullptr;
     const int mm = min(GM_MT, T.m - w.mt * GM_MT);
     const int RM = (mm + GM_WM - 1) / GM_WM;
     switch (RM) {
 #define PS_RM_CASE(R) \
-      case R: consume_item<R>(a, sm, w, T, nsteps, g, tid, lane, wm, wn, tr); break;
+      case R: compute_item<R>(a, sm, w, T, sm.kt[slot], &sm.ideps[slot], par, nsteps, tid, lane, wm, wn, tr); break;
       PS_RM_CASE(1) PS_RM_CASE(2) PS_RM_CASE(3) PS_RM_CASE(4) PS_RM_CASE(5) PS_RM_CASE(6)
       PS_RM_CASE(7) PS_RM_CASE(8)
 #undef PS_RM_CASE
       default: break;
     }
-    g += nsteps;
+    // compute_item ended with a compute-warp barrier: slot (descriptor + k table) reusable
+    if (tid == 0) mbar_arrive(&sm.iempty[slot]);
   }
 }
 
