@@ -167,6 +167,8 @@ def main():
     ap.add_argument("--nrhs", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=2)
+    ap.add_argument("--rhs-split", default="weak", choices=["weak", "strong"],
+                    help="weak: every rank solves the config's full RHS block; strong: the block is split")
     args = ap.parse_args()
     warnings.simplefilter("ignore", RuntimeWarning)
     if args.impl == "reference":
@@ -176,6 +178,7 @@ def main():
     import torch.distributed as dist
     from hmgen.build import load_or_generate, read_rhs
     from paper_2109_04129_b200 import PsHandle
+    from paper_2109_04129_b200.dist import column_slice, max_over_ranks
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -190,8 +193,9 @@ def main():
         if rank != 0:
             meta = load_or_generate(args.config)
     Bfull, _ = read_rhs(meta["rhs"])
-    nrhs = args.nrhs or Bfull.shape[1]
-    B = np.asfortranarray(Bfull[:, :nrhs])
+    nrhs_global = args.nrhs or Bfull.shape[1]
+    B = np.asfortranarray(Bfull[:, :nrhs_global][:, column_slice(nrhs_global, world, rank, args.rhs_split)])
+    nrhs = B.shape[1]
     N = meta["N"]
 
     h = PsHandle(meta["hm"], device=local, rank=rank, nranks=world)
@@ -204,7 +208,7 @@ def main():
     info = h.info()
 
     def dev(A):
-        return torch.from_numpy(np.ascontiguousarray(A.T)).cuda().T
+        return torch.from_numpy(np.array(A.T, order="C")).cuda().T
 
     Bd = dev(B)
     Xd = torch.empty_like(Bd)
@@ -221,11 +225,7 @@ def main():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-    ms = e0.elapsed_time(e1) / args.steps
-    if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, dist, "cuda")
     launches = int(rep["launches"])
     _, rep = h.solve(Bd, Xd, stream=st)
     ratio = rep["ratio"]
@@ -243,11 +243,7 @@ def main():
         h.solve(Bh, Xh, stream=st, want_norms=False)
     e1.record(st)
     torch.cuda.synchronize()
-    ms_e2e = e0.elapsed_time(e1) / args.steps
-    if world > 1:
-        t = torch.tensor([ms_e2e], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_e2e = float(t.item())
+    ms_e2e = max_over_ranks(e0.elapsed_time(e1) / args.steps, dist, "cuda")
 
     # ---- roofline of the dominant kernel (gather-GEMM), per-launch events ----
     args.profile_steps = max(1, args.profile_steps)
@@ -280,9 +276,11 @@ def main():
                               "gflop_per_step": prof[c]["flops"] / args.profile_steps / 1e9}
                           for c in prof}}
 
-    value = world * N * nrhs / (ms * 1e-3)
+    total_cols = nrhs * world if args.rhs_split == "weak" else nrhs_global
+    value = N * total_cols / (ms * 1e-3)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": args.rhs_split,
             "vs_baseline": None, "dtype": "c128",
             "data": "synthetic (seeded EFIE H-matrix from hmgen; plane-wave RHS)",
             "config": _config(args, meta, nrhs, world),
@@ -293,7 +291,7 @@ def main():
                        "note": "ratio >= 0.1 flags divergence (Eq. 45); BASELINE configs use 0.25-lambda "
                                "leaves, below the paper's 0.5-lambda accuracy threshold (DESIGN.md R14)"},
             "roofline": roof,
-            "e2e": {"value": world * N * nrhs / (ms_e2e * 1e-3), "unit": UNIT,
+            "e2e": {"value": N * total_cols / (ms_e2e * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": 16 * N * nrhs, "d2h_bytes_per_step": 16 * N * nrhs,
                     "ms_per_step": ms_e2e},
             "gpu_launches": launches * args.steps,

@@ -327,7 +327,7 @@ struct Table {
 struct SolvePlan {
   int64_t nrhs = 0;
   Table fwd, bwd, dinv, far1, far2;
-  DevBuf<double2> y, bo, w, u, xt, wm, tm, ftmp, part, norms, stage;
+  DevBuf<double2> y, bo, w, u, xt, wm, tm, part, norms, stage;
   int64_t nchunks = 0, rpc = 64;
   int64_t launches_per_solve = 0;
 };
@@ -360,6 +360,7 @@ struct ps_handle {
   // block side whose rows are cluster c] (sum_r x len, column-major)
   std::vector<int64_t> cl_start, cl_len, cl_sr, cl_soff;
   std::vector<int64_t> fb_ct, fb_cs, fb_rbt, fb_rbs;   // per block: clusters, row offsets in stacks
+  std::vector<int64_t> fb_dense;                       // per block: offset of dense D (m x n) or -1
   int64_t stack_len = 0;
   double setup_madds = 0;
   int64_t alpha_blocks = 0;
@@ -575,6 +576,15 @@ void symbolic(ps_handle* h) {
 // with rows t = [r0, r0+m), cols s = [c0, c0+n) contributes U^T (r x m) to the
 // stack of t and V^T (r x n) to the stack of s. Stage 1 is then one GEMM per
 // cluster, S_c w_c, and stage 2 reads U/V rows from the same stacks.
+static bool is_identity(const double2* M, int64_t n) {
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t i = 0; i < n; ++i) {
+      const double2 v = M[i + j * n];
+      if (v.y != 0.0 || v.x != (i == j ? 1.0 : 0.0)) return false;
+    }
+  return true;
+}
+
 void far_layout(ps_handle* h, const std::vector<double2>& far_arena, std::vector<double2>& stacked) {
   std::map<std::pair<int64_t, int64_t>, int64_t> cid;
   auto get = [&](int64_t a, int64_t l) {
@@ -589,11 +599,28 @@ void far_layout(ps_handle* h, const std::vector<double2>& far_arena, std::vector
   };
   const int64_t nf = h->nfar;
   h->fb_ct.assign(nf, 0); h->fb_cs.assign(nf, 0); h->fb_rbt.assign(nf, 0); h->fb_rbs.assign(nf, 0);
+  h->fb_dense.assign(nf, -1);
+  // Blocks stored exactly as dense x I (ACA rank cap, R18) are applied as the
+  // dense block D (m x n) itself: multiplying by an exact identity is exact, so
+  // this only removes work. D lives after the stacks in the same arena.
+  std::vector<int64_t> dense_src(nf, -1);   // 0: D = U, 1: D = V^T
+  int64_t dense_len = 0;
+  for (int64_t b = 0; b < nf; ++b) {
+    const int64_t* F = &h->far_list[7 * b];
+    const int64_t m = F[1], n = F[3], r = F[5], fo = F[6];
+    if (r == n && is_identity(&far_arena[fo + m * r], n)) dense_src[b] = 0;
+    else if (r == m && is_identity(&far_arena[fo], m)) dense_src[b] = 1;
+    if (dense_src[b] >= 0) {
+      h->fb_dense[b] = dense_len;
+      dense_len += m * n;
+    }
+  }
   for (int64_t b = 0; b < nf; ++b) {
     const int64_t* F = &h->far_list[7 * b];
     const int64_t t = get(F[0], F[1]), c = get(F[2], F[3]), r = F[5];
     h->fb_ct[b] = t;
     h->fb_cs[b] = c;
+    if (dense_src[b] >= 0) continue;
     h->fb_rbt[b] = h->cl_sr[t];
     h->cl_sr[t] += r;
     h->fb_rbs[b] = h->cl_sr[c];
@@ -607,10 +634,21 @@ void far_layout(ps_handle* h, const std::vector<double2>& far_arena, std::vector
     off += h->cl_sr[c] * h->cl_len[c];
   }
   h->stack_len = off;
-  stacked.assign(std::max<int64_t>(off, 1), double2{0.0, 0.0});
+  for (int64_t b = 0; b < nf; ++b)
+    if (h->fb_dense[b] >= 0) h->fb_dense[b] += off;
+  stacked.assign(std::max<int64_t>(off + dense_len, 1), double2{0.0, 0.0});
   for (int64_t b = 0; b < nf; ++b) {
     const int64_t* F = &h->far_list[7 * b];
     const int64_t m = F[1], n = F[3], r = F[5], fo = F[6];
+    if (dense_src[b] == 0) {          // D = U (m x n)
+      std::copy(&far_arena[fo], &far_arena[fo] + m * n, &stacked[h->fb_dense[b]]);
+      continue;
+    }
+    if (dense_src[b] == 1) {          // D = V^T: D(i, k) = V(k, i), V n x m
+      for (int64_t k = 0; k < n; ++k)
+        for (int64_t i = 0; i < m; ++i) stacked[h->fb_dense[b] + i + k * m] = far_arena[fo + m * r + k + i * n];
+      continue;
+    }
     const int64_t t = h->fb_ct[b], c = h->fb_cs[b];
     const int64_t srt = h->cl_sr[t], src = h->cl_sr[c];
     for (int64_t j = 0; j < r; ++j) {
@@ -787,13 +825,16 @@ void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
     sp.dinv.tile(t);
   }
   sp.dinv.close_batch();
-  // far field, Morton order (DESIGN.md §Far field).
+  // far field, Morton order (DESIGN.md §Far field). Workspace `wm` holds the
+  // Morton-ordered w (N x R) followed by the stage-1 products (one buffer, so
+  // stage 2 reads both through one base).
+  const int64_t NRw = h->N * R;
   // stage 1, one task per cluster c: tmp_c (sum_r x R) = S_c w[c]
   const int64_t ncl = (int64_t)h->cl_start.size();
   std::vector<int64_t> toff(ncl);
   int64_t T = 0;
   for (int64_t c = 0; c < ncl; ++c) {
-    toff[c] = T;
+    toff[c] = NRw + T;
     T += h->cl_sr[c] * R;
     if (h->cl_sr[c] == 0) continue;
     int32_t t1 = sp.far1.add_task(toff[c], R, 1, -1, 0, 0, (int)h->cl_sr[c], (int)R, +1);
@@ -802,7 +843,8 @@ void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
   }
   sp.far1.close_batch();
   // stage 2 per Morton leaf l: t_l = sum_b U_b[rows of l] (V_b^T w_s) + sum_b V_b[rows of l] (U_b^T w_t)
-  std::vector<std::vector<std::array<int64_t, 4>>> contrib(nl);  // (oA, sAi, oB, K)
+  //                                 + dense blocks D w_s / D^T w_t
+  std::vector<std::vector<std::array<int64_t, 6>>> contrib(nl);  // (oA, sAi, sAk, oB, K, -)
   auto leaf_of_pos = [&](int64_t m) {
     return (int64_t)(std::upper_bound(h->leaf_off.begin(), h->leaf_off.end(), m) - h->leaf_off.begin()) - 1;
   };
@@ -811,25 +853,32 @@ void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
     const int64_t r0 = F[0], m = F[1], c0 = F[2], n = F[3], r = F[5];
     if (r == 0) continue;
     const int64_t ct = h->fb_ct[b], cs = h->fb_cs[b];
+    if (h->fb_dense[b] >= 0) {
+      const int64_t D = h->fb_dense[b];
+      for (int64_t l = leaf_of_pos(r0); l < nl && h->leaf_off[l] < r0 + m; ++l)   // D w_s
+        contrib[l].push_back({D + (h->leaf_off[l] - r0), 1, m, c0 * R, n, 0});
+      for (int64_t l = leaf_of_pos(c0); l < nl && h->leaf_off[l] < c0 + n; ++l)   // D^T w_t
+        contrib[l].push_back({D + (h->leaf_off[l] - c0) * m, m, 1, r0 * R, m, 0});
+      continue;
+    }
     for (int64_t l = leaf_of_pos(r0); l < nl && h->leaf_off[l] < r0 + m; ++l)
       contrib[l].push_back({h->cl_soff[ct] + h->fb_rbt[b] + (h->leaf_off[l] - r0) * h->cl_sr[ct],
-                            h->cl_sr[ct], toff[cs] + h->fb_rbs[b] * R, r});
+                            h->cl_sr[ct], 1, toff[cs] + h->fb_rbs[b] * R, r, 0});
     for (int64_t l = leaf_of_pos(c0); l < nl && h->leaf_off[l] < c0 + n; ++l)
       contrib[l].push_back({h->cl_soff[cs] + h->fb_rbs[b] + (h->leaf_off[l] - c0) * h->cl_sr[cs],
-                            h->cl_sr[cs], toff[ct] + h->fb_rbt[b] * R, r});
+                            h->cl_sr[cs], 1, toff[ct] + h->fb_rbt[b] * R, r, 0});
   }
   for (int64_t l = 0; l < nl; ++l) {
     const int64_t nlf = h->leaf_off[l + 1] - h->leaf_off[l];
     int32_t t = sp.far2.add_task(h->leaf_off[l] * R, R, 1, -1, 0, 0, (int)nlf, (int)R, +1);
-    for (auto& c : contrib[l]) sp.far2.add_term(t, c[0], c[1], 1, c[2], R, 1, (int)c[3]);
+    for (auto& c : contrib[l]) sp.far2.add_term(t, c[0], c[1], c[2], c[3], R, 1, (int)c[4]);
     sp.far2.tile(t);
   }
   sp.far2.close_batch();
   for (Table* tb : {&sp.fwd, &sp.bwd, &sp.dinv, &sp.far1, &sp.far2}) tb->upload(h->stream);
   const int64_t NR = h->N * R;
   sp.y.alloc(NR); sp.bo.alloc(NR); sp.w.alloc(NR); sp.u.alloc(NR); sp.xt.alloc(NR);
-  sp.wm.alloc(NR); sp.tm.alloc(NR); sp.stage.alloc(NR);
-  sp.ftmp.alloc(std::max<int64_t>(T, 1));
+  sp.wm.alloc(NR + std::max<int64_t>(T, 1)); sp.tm.alloc(NR); sp.stage.alloc(NR);
   sp.nchunks = (h->N + sp.rpc - 1) / sp.rpc;
   sp.part.alloc(sp.nchunks * R);
   sp.norms.alloc(R);
@@ -867,8 +916,8 @@ int64_t op_ZF(ps_handle* h, SolvePlan& sp, const double2* in, double2* out, cuda
   const int64_t N = h->N, R = sp.nrhs;
   int64_t n = 0;
   n += aux(h, s, [&] { launch_permute_rows(N, R, h->d_m2e.p, in, sp.wm.p, s); });      // E -> Morton
-  n += sp.far1.launch_all(sp.ftmp.p, nullptr, h->d_far.p, sp.wm.p, s, &h->prof, PC_FAR1);
-  n += sp.far2.launch_all(sp.tm.p, nullptr, h->d_far.p, sp.ftmp.p, s, &h->prof, PC_FAR2);
+  n += sp.far1.launch_all(sp.wm.p, nullptr, h->d_far.p, sp.wm.p, s, &h->prof, PC_FAR1);
+  n += sp.far2.launch_all(sp.tm.p, nullptr, h->d_far.p, sp.wm.p, s, &h->prof, PC_FAR2);
   n += aux(h, s, [&] { launch_permute_rows(N, R, h->d_e2mort.p, sp.tm.p, out, s); });  // Morton -> E
   return n;
 }

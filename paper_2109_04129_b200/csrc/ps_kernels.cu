@@ -64,9 +64,9 @@ __device__ __forceinline__ int ld_acquire(const int32_t* p) {
   return v;
 }
 
-// Per-item k tables (built by the scheduler warp, double buffered): for the item's virtual k range
-// [ka, kb) the A column base, A row stride, B row base and B column stride of
-// every k, built from the segment list, so k-steps run densely across segments.
+// Per-item k tables: for the item's virtual k range [ka, kb) the A column
+// base, A row stride, B row base and B column stride of every k (built from the
+// segment list at item start), so k-steps run densely across segments.
 struct KTab {
   int64_t kA[GM_CHUNK_K];
   int64_t kB[GM_CHUNK_K];
@@ -74,75 +74,36 @@ struct KTab {
   int32_t kSc[GM_CHUNK_K];
 };
 
-constexpr int NCW = 8;                      // compute warps
-constexpr int NTHREADS = (NCW + 1) * 32;    // + 1 scheduler warp
-constexpr int AS_LD = GM_MT;                // stage A tile: As[k][i]
-constexpr int BS_LD = GM_NT;                // stage B tile: Bs[k][c]
+constexpr int A_PER_T = GM_MT * KC / 256;   // 2 A elements per thread per k-step
+constexpr int B_PER_T = GM_NT * KC / 256;   // 4 B elements per thread per k-step
+constexpr int AS_LD = GM_MT;                // As[k][i]
+constexpr int BS_LD = GM_NT;                // Bs[k][c]
 constexpr int NSTAGE = 3;                   // cp.async pipeline depth
 constexpr int STAGE_A = KC * AS_LD, STAGE_B = KC * BS_LD;
-constexpr int A_PER_T = GM_MT * KC / 256;   // 2 A copies per compute thread per k-step
-constexpr int B_PER_T = GM_NT * KC / 256;   // 4 B copies per compute thread per k-step
 
-struct ItemDesc {
-  GWork w;
-  GTask T;
-  int64_t item;
-  int32_t nsteps, end;
-};
+__device__ __forceinline__ void a_map(bool a_km, int e, int& i, int& k) {
+  if (a_km) { k = e & (KC - 1); i = e / KC; } else { i = e % GM_MT; k = e / GM_MT; }
+}
+__device__ __forceinline__ void b_map(bool b_km, int e, int& c, int& k) {
+  if (b_km) { k = e & (KC - 1); c = e / KC; } else { c = e & (GM_NT - 1); k = e / GM_NT; }
+}
 
-struct FlowSmem {
-  double2 A[NSTAGE][STAGE_A];
-  double2 B[NSTAGE][STAGE_B];
-  KTab kt[2];
-  ItemDesc desc[2];
-  unsigned long long ifull[2], ideps[2], iempty[2];
-  int s_last;
-};
-constexpr size_t FLOW_SMEM = sizeof(FlowSmem);
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(unsigned long long* b, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* b, int parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT%=;\n}\n" ::"r"(smem_u32(b)),
-      "r"(parity)
-      : "memory");
-}
 // 16-byte global -> shared async copy (L2 only, .cg); zero-fills when !valid.
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
   const int n = valid ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem), "r"(n)
-               : "memory");
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(n) : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-__device__ __forceinline__ void compute_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
-
-// release / acquire flag operations (one thread, after / before a barrier)
-__device__ __forceinline__ void red_release(int32_t* p, int v) {
-  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ int atom_acq_rel(int32_t* p, int v) {
-  int old;
-  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-  return old;
-}
 
 __device__ __forceinline__ void issue_a(const KTab& kt, int k0, int klen, int i0, int mm, bool a_km,
                                         const double2* __restrict__ Ab, int tid, double2* As) {
 #pragma unroll
   for (int q = 0; q < A_PER_T; ++q) {
-    const int e = tid + 256 * q;
     int i, k;
-    if (a_km) { k = e & (KC - 1); i = e / KC; } else { i = e % GM_MT; k = e / GM_MT; }
+    a_map(a_km, tid + q * 256, i, k);
     const int kk = k0 + k;
     const bool v = (i < mm && kk < klen);
     const double2* src = v ? Ab + kt.kA[kk] + (int64_t)(i0 + i) * kt.kSi[kk] : Ab;
@@ -153,9 +114,8 @@ __device__ __forceinline__ void issue_b(const KTab& kt, int k0, int klen, int c0
                                         const double2* __restrict__ Bb, int tid, double2* Bs) {
 #pragma unroll
   for (int q = 0; q < B_PER_T; ++q) {
-    const int e = tid + 256 * q;
     int c, k;
-    if (b_km) { k = e & (KC - 1); c = e / KC; } else { c = e & (GM_NT - 1); k = e / GM_NT; }
+    b_map(b_km, tid + q * 256, c, k);
     const int kk = k0 + k;
     const bool v = (c < nn && kk < klen);
     const double2* src = v ? Bb + kt.kB[kk] + (int64_t)(c0 + c) * kt.kSc[kk] : Bb;
@@ -163,69 +123,26 @@ __device__ __forceinline__ void issue_b(const KTab& kt, int k0, int klen, int c0
   }
 }
 
-// ---- scheduler warp: next item's ticket, descriptor, k table, dependency wait ----
-__device__ void scheduler_loop(const FlowArgs& a, FlowSmem& sm, int lane) {
-  int32_t* ticket = a.counters;
-  int32_t* done = a.counters + 1;
-  for (int j = 0;; ++j) {
-    int item = 0;
-    if (lane == 0) item = atomicAdd(ticket, 1);
-    item = __shfl_sync(0xffffffffu, item, 0);
-    const int slot = j & 1, ir = j >> 1;
-    if (ir > 0) mbar_wait(&sm.iempty[slot], (ir - 1) & 1);
-    ItemDesc& D = sm.desc[slot];
-    if (item >= a.nwork) {
-      if (lane == 0) {
-        D.end = 1;
-        mbar_arrive(&sm.ifull[slot]);
-      }
-      return;
-    }
-    int64_t* tr = (a.trace != nullptr && lane == 0) ? a.trace + 6 * (int64_t)item : nullptr;
-    if (tr) { tr[0] = item; tr[1] = smid(); tr[2] = gtimer(); }
-    const GWork w = a.work[item];
-    KTab& kt = sm.kt[slot];
-    for (int t = w.ta + lane; t < w.tb; t += 32) {
-      const GTerm gt = a.terms[t];
-      const int lo = max(gt.kstart, w.ka), hi = min(gt.kstart + gt.K, w.kb);
-      for (int k = lo; k < hi; ++k) {
-        const int64_t d = k - gt.kstart;
-        kt.kA[k - w.ka] = gt.oA + d * gt.sAk;
-        kt.kB[k - w.ka] = gt.oB + d * gt.sBk;
-        kt.kSi[k - w.ka] = (int32_t)gt.sAi;
-        kt.kSc[k - w.ka] = (int32_t)gt.sBc;
-      }
-    }
-    if (lane == 0) {
-      D.w = w;
-      D.T = a.tasks[w.task];
-      D.item = item;
-      D.nsteps = (w.kb - w.ka + KC - 1) / KC;
-      D.end = 0;
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.ifull[slot]);       // descriptor + k table ready
-    for (int t = w.ta + lane; t < w.tb; t += 32) {
-      const int dep = a.terms[t].dep;
-      if (dep >= 0) {
-        const int32_t need = a.tasks[dep].n_mt;
-        const int32_t* flag = done + a.tasks[dep].unit0 + w.nt;
-        while (ld_acquire(flag) < need) __nanosleep(32);
-      }
-    }
-    __syncwarp();
-    if (tr) tr[3] = gtimer();
-    if (lane == 0) mbar_arrive(&sm.ideps[slot]);       // B operands are final
-  }
+// release / acquire flag operations (one thread, after / before a CTA barrier)
+__device__ __forceinline__ void red_release(int32_t* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int atom_acq_rel(int32_t* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
 }
 
-// ---- compute warps: cp.async pipeline + FMA stream for a compile-time
-// rows-per-warp RM, then split-K combine / finalize / publish ----
+constexpr size_t FLOW_SMEM = (size_t)NSTAGE * (STAGE_A + STAGE_B) * sizeof(double2) + sizeof(KTab);
+
+// Everything of one work item, for a compile-time rows-per-warp RM (so the
+// FMA stream is branch-free). A operands (operator panels: immutable in the
+// launch) of the first stages are requested before waiting for the producers
+// of the B operands.
 template <int RM>
-__device__ __forceinline__ void compute_item(const FlowArgs& a, FlowSmem& sm, const GWork& w,
-                                             const GTask& T, const KTab& kt, unsigned long long* ideps,
-                                             int dpar, int nsteps, int tid, int lane, int wm, int wn,
-                                             int64_t* tr) {
+__device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, const GTask& T,
+                                          const KTab& kt, double2* As0, double2* Bs0, int tid,
+                                          int lane, int wm, int wn, int* s_last, int64_t* tr) {
   const int i0 = w.mt * GM_MT, c0 = w.nt * GM_NT;
   const int mm = min(GM_MT, T.m - i0), nn = min(GM_NT, T.n - c0);
   const int klen = w.kb - w.ka;
@@ -234,15 +151,29 @@ __device__ __forceinline__ void compute_item(const FlowArgs& a, FlowSmem& sm, co
   int32_t* done = a.counters + 1;
   int32_t* arrive = a.counters + 1 + a.n_units;
   const bool a_km = T.a_kmajor != 0, b_km = T.b_kmajor != 0;
-  // A (immutable operator) of the first stages before the producers of B are done
+  const int nsteps = (klen + KC - 1) / KC;
+  // ---- prologue part 1: A of stages 0..NSTAGE-2 (one group) ----
 #pragma unroll
   for (int s = 0; s < NSTAGE - 1; ++s)
-    if (s < nsteps) issue_a(kt, s * KC, klen, i0, mm, a_km, a.A, tid, sm.A[s]);
+    if (s < nsteps) issue_a(kt, s * KC, klen, i0, mm, a_km, a.A, tid, As0 + s * STAGE_A);
   cp_commit();
-  mbar_wait(ideps, dpar);
+  // ---- wait for the producers of B (warp 0, one segment per lane) ----
+  if (tid < 32) {
+    for (int t = w.ta + tid; t < w.tb; t += 32) {
+      const int dep = a.terms[t].dep;
+      if (dep >= 0) {
+        const int32_t need = a.tasks[dep].n_mt;
+        const int32_t* flag = done + a.tasks[dep].unit0 + w.nt;
+        while (ld_acquire(flag) < need) __nanosleep(32);
+      }
+    }
+  }
+  __syncthreads();
+  if (tr) tr[3] = gtimer();
+  // ---- prologue part 2: B of stages 0..NSTAGE-2 (one group each) ----
 #pragma unroll
   for (int s = 0; s < NSTAGE - 1; ++s) {
-    if (s < nsteps) issue_b(kt, s * KC, klen, c0, nn, b_km, a.B, tid, sm.B[s]);
+    if (s < nsteps) issue_b(kt, s * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + s * STAGE_B);
     cp_commit();
   }
   double2 acc[RM];
@@ -250,26 +181,27 @@ __device__ __forceinline__ void compute_item(const FlowArgs& a, FlowSmem& sm, co
   for (int r = 0; r < RM; ++r) acc[r] = make_double2(0.0, 0.0);
   for (int s = 0; s < nsteps; ++s) {
     cp_wait<NSTAGE - 2>();
-    compute_sync();
+    __syncthreads();
     const int st = s % NSTAGE;
-    const double2* As = sm.A[st] + rbase;
-    const double2* Bs = sm.B[st] + col;
+    const double2* As = As0 + st * STAGE_A + rbase;
+    const double2* Bs = Bs0 + st * STAGE_B + col;
 #pragma unroll
     for (int k = 0; k < KC; ++k) {
       const double2 b = Bs[k * BS_LD];
 #pragma unroll
       for (int r = 0; r < RM; ++r) cfma(acc[r], As[k * AS_LD + r], b);
     }
+    // refill the stage consumed one iteration ago (all threads are past the barrier above)
     const int sn = s + NSTAGE - 1;
     if (sn < nsteps) {
       const int stn = sn % NSTAGE;
-      issue_a(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, sm.A[stn]);
-      issue_b(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, sm.B[stn]);
+      issue_a(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * STAGE_A);
+      issue_b(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * STAGE_B);
     }
     cp_commit();
   }
   cp_wait<0>();
-  compute_sync();          // stage buffers and this item's k table are free
+  __syncthreads();          // all warps done with the stage buffers before the next item
   if (tr) tr[4] = gtimer();
   // ---- split-K combine (fixed summation order => deterministic) ----
   bool finalize = true;
@@ -280,7 +212,7 @@ __device__ __forceinline__ void compute_item(const FlowArgs& a, FlowSmem& sm, co
       // the other chunks' sum arrives in slot `crit` once arrive[tile] == nchunks
       if (tid == 0)
         while (ld_acquire(arrive + w.tile) < w.nchunks) __nanosleep(32);
-      compute_sync();
+      __syncthreads();
       const double2* G = a.partial + (w.slot + w.crit) * TS;
 #pragma unroll
       for (int r = 0; r < RM; ++r) {
@@ -292,11 +224,11 @@ __device__ __forceinline__ void compute_item(const FlowArgs& a, FlowSmem& sm, co
       double2* P = a.partial + (w.slot + w.chunk) * TS;
 #pragma unroll
       for (int r = 0; r < RM; ++r) __stcg(P + (rbase + r) * GM_NT + col, acc[r]);
-      compute_sync();
+      __syncthreads();
       const int group = crit_mode ? w.nchunks - 1 : w.nchunks;
-      if (tid == 0) sm.s_last = (atom_acq_rel(arrive + w.tile, 1) == group - 1);
-      compute_sync();
-      finalize = sm.s_last;
+      if (tid == 0) *s_last = (atom_acq_rel(arrive + w.tile, 1) == group - 1);
+      __syncthreads();
+      finalize = *s_last;
       if (finalize) {
 #pragma unroll
         for (int r = 0; r < RM; ++r) acc[r] = make_double2(0.0, 0.0);
@@ -314,7 +246,7 @@ __device__ __forceinline__ void compute_item(const FlowArgs& a, FlowSmem& sm, co
           double2* G = a.partial + (w.slot + w.crit) * TS;
 #pragma unroll
           for (int r = 0; r < RM; ++r) __stcg(G + (rbase + r) * GM_NT + col, acc[r]);
-          compute_sync();
+          __syncthreads();
           if (tid == 0) red_release(arrive + w.tile, 1);
           finalize = false;
         }
@@ -338,61 +270,60 @@ __device__ __forceinline__ void compute_item(const FlowArgs& a, FlowSmem& sm, co
         }
       }
     }
-    compute_sync();
+    __syncthreads();
     if (tid == 0) red_release(done + T.unit0 + w.nt, 1);
   }
-  if (tr) tr[5] = gtimer();
 }
 
-// Persistent dataflow gather-GEMM. Warps 0-7 compute: output
-// tile 32 x 64, warp (wm, wn) = (w % 4, w / 4) owns RM = ceil(rows / 4) <= 8
-// rows and column wn*32 + lane; they stream their own operands through a
-// 3-stage cp.async pipeline. Warp 8 schedules: it takes the next ticket
-// (topological order), builds that item's k table (double buffered) and waits
-// for the producers of its B operands while the compute warps are still busy
-// with the current item; readiness is signalled in two mbarrier phases (k table
-// ready -> A may be fetched; dependencies done -> B may be fetched).
-__global__ void __launch_bounds__(NTHREADS, 2)
+// Output tile: warp w = (wm, wn) = (w % 4, w / 4) owns rows
+// [wm*RM, min(mm, (wm+1)*RM)) with RM = ceil(mm / 4) <= 8 (so the tile is
+// only as tall as the task) and column wn*32 + lane. A values are broadcast
+// shared loads, one B load feeds RM complex FMAs.
+__global__ void __launch_bounds__(256, 2)
 flow_kernel(const FlowArgs a) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  FlowSmem& sm = *reinterpret_cast<FlowSmem*>(smem_raw);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* As0 = reinterpret_cast<double2*>(smem_raw);
+  double2* Bs0 = As0 + NSTAGE * STAGE_A;
+  KTab& kt = *reinterpret_cast<KTab*>(Bs0 + NSTAGE * STAGE_B);
+  __shared__ int s_item, s_last;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) {
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&sm.ifull[s], 1);
-      mbar_init(&sm.ideps[s], 1);
-      mbar_init(&sm.iempty[s], 1);
-    }
-  }
-  __syncthreads();
-  if (warp == NCW) {
-    scheduler_loop(a, sm, lane);
-    return;
-  }
   const int wm = warp % GM_WM, wn = warp / GM_WM;
-  for (int j = 0;; ++j) {
-    const int slot = j & 1, par = (j >> 1) & 1;
-    mbar_wait(&sm.ifull[slot], par);
-    const ItemDesc& D = sm.desc[slot];
-    if (D.end) return;
-    const GWork w = D.w;
-    const GTask T = D.T;
-    const int nsteps = D.nsteps;
-    const int64_t item = D.item;
+  int32_t* ticket = a.counters;
+  for (;;) {
+    if (tid == 0) s_item = atomicAdd(ticket, 1);
+    __syncthreads();
+    const int64_t item = s_item;
+    if (item >= a.nwork) return;
     int64_t* tr = (a.trace != nullptr && tid == 0) ? a.trace + 6 * item : nullptr;
+    if (tr) { tr[0] = item; tr[1] = smid(); tr[2] = gtimer(); }
+    const GWork w = a.work[item];
+    const GTask T = a.tasks[w.task];
     const int mm = min(GM_MT, T.m - w.mt * GM_MT);
     const int RM = (mm + GM_WM - 1) / GM_WM;
+    // ---- k tables of this item (segments [ta, tb) clipped to [ka, kb)) ----
+    for (int t = w.ta + tid; t < w.tb; t += 256) {
+      const GTerm g = a.terms[t];
+      const int lo = max(g.kstart, w.ka), hi = min(g.kstart + g.K, w.kb);
+      for (int k = lo; k < hi; ++k) {
+        const int64_t d = k - g.kstart;
+        kt.kA[k - w.ka] = g.oA + d * g.sAk;
+        kt.kB[k - w.ka] = g.oB + d * g.sBk;
+        kt.kSi[k - w.ka] = (int32_t)g.sAi;
+        kt.kSc[k - w.ka] = (int32_t)g.sBc;
+      }
+    }
+    __syncthreads();
     switch (RM) {
 #define PS_RM_CASE(R) \
-      case R: compute_item<R>(a, sm, w, T, sm.kt[slot], &sm.ideps[slot], par, nsteps, tid, lane, wm, wn, tr); break;
+      case R: item_body<R>(a, w, T, kt, As0, Bs0, tid, lane, wm, wn, &s_last, tr); break;
       PS_RM_CASE(1) PS_RM_CASE(2) PS_RM_CASE(3) PS_RM_CASE(4) PS_RM_CASE(5) PS_RM_CASE(6)
       PS_RM_CASE(7) PS_RM_CASE(8)
 #undef PS_RM_CASE
       default: break;
     }
-    // compute_item ended with a compute-warp barrier: slot (descriptor + k table) reusable
-    if (tid == 0) mbar_arrive(&sm.iempty[slot]);
+    if (tr) tr[5] = gtimer();
+    __syncthreads();
   }
 }
 
@@ -403,7 +334,7 @@ int flow_resident_ctas() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(flow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FLOW_SMEM);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, flow_kernel, NTHREADS, FLOW_SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, flow_kernel, 256, FLOW_SMEM);
     n = sms * (per_sm > 0 ? per_sm : 1);
   }
   return n;
@@ -413,7 +344,7 @@ void launch_flow(const FlowArgs& a, int grid, cudaStream_t st) {
   if (a.nwork <= 0) return;
   int g = grid > 0 ? grid : flow_resident_ctas();
   if (g > a.nwork) g = (int)a.nwork;
-  flow_kernel<<<g, NTHREADS, FLOW_SMEM, st>>>(a);
+  flow_kernel<<<g, 256, FLOW_SMEM, st>>>(a);
 }
 
 // ---------------------------------------------------------------------------
