@@ -135,28 +135,19 @@ __device__ __forceinline__ int atom_acq_rel(int32_t* p, int v) {
 
 constexpr size_t FLOW_SMEM = (size_t)NSTAGE * (STAGE_A + STAGE_B) * sizeof(double2) + sizeof(KTab);
 
-// FP64 tensor-core MMA: D(8x8) += A(8x4, row) * B(4x8, col); per lane
-// A[g][q], B[q][g], C[g][2q], C[g][2q+1] with g = lane / 4, q = lane % 4.
-__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
-}
-
-// Everything of one work item for a compile-time number of 8-row MMA tiles
-// MT8 = ceil(rows / 8) <= 4. Warp w computes column tile w (8 columns) of the
-// 32 x 64 output tile for all MT8 row tiles; a complex product is 4 real
-// DMMAs (re*re, -im*im, re*im, im*re) fed by one 16-byte shared load per
-// fragment element. A operands (immutable in the launch) of the first stages
-// are requested before waiting for the producers of B.
-template <int MT8>
+// Everything of one work item, for a compile-time rows-per-warp RM (so the
+// FMA stream is branch-free). A operands (operator panels: immutable in the
+// launch) of the first stages are requested before waiting for the producers
+// of the B operands.
+template <int RM>
 __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, const GTask& T,
                                           const KTab& kt, double2* As0, double2* Bs0, int tid,
-                                          int lane, int warp, int* s_last, int64_t* tr) {
+                                          int lane, int wm, int wn, int* s_last, int64_t* tr) {
   const int i0 = w.mt * GM_MT, c0 = w.nt * GM_NT;
   const int mm = min(GM_MT, T.m - i0), nn = min(GM_NT, T.n - c0);
   const int klen = w.kb - w.ka;
-  const int g = lane >> 2, q = lane & 3;
+  const int rbase = wm * RM;
+  const int col = wn * 32 + lane;
   int32_t* done = a.counters + 1;
   int32_t* arrive = a.counters + 1 + a.n_units;
   const bool a_km = T.a_kmajor != 0, b_km = T.b_kmajor != 0;
@@ -185,26 +176,20 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
     if (s < nsteps) issue_b(kt, s * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + s * STAGE_B);
     cp_commit();
   }
-  double cre[MT8][2], cim[MT8][2];
+  double2 acc[RM];
 #pragma unroll
-  for (int m = 0; m < MT8; ++m) cre[m][0] = cre[m][1] = cim[m][0] = cim[m][1] = 0.0;
+  for (int r = 0; r < RM; ++r) acc[r] = make_double2(0.0, 0.0);
   for (int s = 0; s < nsteps; ++s) {
     cp_wait<NSTAGE - 2>();
     __syncthreads();
     const int st = s % NSTAGE;
-    const double2* As = As0 + st * STAGE_A + q * AS_LD + g;
-    const double2* Bs = Bs0 + st * STAGE_B + q * BS_LD + warp * 8 + g;
+    const double2* As = As0 + st * STAGE_A + rbase;
+    const double2* Bs = Bs0 + st * STAGE_B + col;
 #pragma unroll
-    for (int kk = 0; kk < KC / 4; ++kk) {
-      const double2 b = Bs[kk * 4 * BS_LD];
+    for (int k = 0; k < KC; ++k) {
+      const double2 b = Bs[k * BS_LD];
 #pragma unroll
-      for (int m = 0; m < MT8; ++m) {
-        const double2 av = As[kk * 4 * AS_LD + m * 8];
-        dmma(cre[m][0], cre[m][1], av.x, b.x);
-        dmma(cre[m][0], cre[m][1], -av.y, b.y);
-        dmma(cim[m][0], cim[m][1], av.x, b.y);
-        dmma(cim[m][0], cim[m][1], av.y, b.x);
-      }
+      for (int r = 0; r < RM; ++r) cfma(acc[r], As[k * AS_LD + r], b);
     }
     // refill the stage consumed one iteration ago (all threads are past the barrier above)
     const int sn = s + NSTAGE - 1;
@@ -218,13 +203,6 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
   cp_wait<0>();
   __syncthreads();          // all warps done with the stage buffers before the next item
   if (tr) tr[4] = gtimer();
-  double2 acc[MT8][2];
-#pragma unroll
-  for (int m = 0; m < MT8; ++m)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) acc[m][e] = make_double2(cre[m][e], cim[m][e]);
-  // element (m, e) of this thread: row m*8 + g, column warp*8 + 2q + e
-  const int colb = warp * 8 + 2 * q;
   // ---- split-K combine (fixed summation order => deterministic) ----
   bool finalize = true;
   if (w.nchunks > 1) {
@@ -237,19 +215,15 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
       __syncthreads();
       const double2* G = a.partial + (w.slot + w.crit) * TS;
 #pragma unroll
-      for (int m = 0; m < MT8; ++m)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const double2 v = __ldcg(G + (m * 8 + g) * GM_NT + colb + e);
-          if (w.crit == 0) { acc[m][e].x = acc[m][e].x + v.x; acc[m][e].y = acc[m][e].y + v.y; }  // p_0 + G
-          else { acc[m][e].x = v.x + acc[m][e].x; acc[m][e].y = v.y + acc[m][e].y; }              // G + p_last
-        }
+      for (int r = 0; r < RM; ++r) {
+        const double2 v = __ldcg(G + (rbase + r) * GM_NT + col);
+        if (w.crit == 0) { acc[r].x = acc[r].x + v.x; acc[r].y = acc[r].y + v.y; }  // p_0 + G
+        else { acc[r].x = v.x + acc[r].x; acc[r].y = v.y + acc[r].y; }              // G + p_last
+      }
     } else {
       double2* P = a.partial + (w.slot + w.chunk) * TS;
 #pragma unroll
-      for (int m = 0; m < MT8; ++m)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) __stcg(P + (m * 8 + g) * GM_NT + colb + e, acc[m][e]);
+      for (int r = 0; r < RM; ++r) __stcg(P + (rbase + r) * GM_NT + col, acc[r]);
       __syncthreads();
       const int group = crit_mode ? w.nchunks - 1 : w.nchunks;
       if (tid == 0) *s_last = (atom_acq_rel(arrive + w.tile, 1) == group - 1);
@@ -257,27 +231,21 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
       finalize = *s_last;
       if (finalize) {
 #pragma unroll
-        for (int m = 0; m < MT8; ++m)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) acc[m][e] = make_double2(0.0, 0.0);
+        for (int r = 0; r < RM; ++r) acc[r] = make_double2(0.0, 0.0);
         for (int c = 0; c < w.nchunks; ++c) {
           if (c == w.crit) continue;
           const double2* Q = a.partial + (w.slot + c) * TS;
 #pragma unroll
-          for (int m = 0; m < MT8; ++m)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const double2 v = __ldcg(Q + (m * 8 + g) * GM_NT + colb + e);
-              acc[m][e].x += v.x;
-              acc[m][e].y += v.y;
-            }
+          for (int r = 0; r < RM; ++r) {
+            const double2 v = __ldcg(Q + (rbase + r) * GM_NT + col);
+            acc[r].x += v.x;
+            acc[r].y += v.y;
+          }
         }
         if (crit_mode) {        // publish the group sum for the critical chunk
           double2* G = a.partial + (w.slot + w.crit) * TS;
 #pragma unroll
-          for (int m = 0; m < MT8; ++m)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) __stcg(G + (m * 8 + g) * GM_NT + colb + e, acc[m][e]);
+          for (int r = 0; r < RM; ++r) __stcg(G + (rbase + r) * GM_NT + col, acc[r]);
           __syncthreads();
           if (tid == 0) red_release(arrive + w.tile, 1);
           finalize = false;
@@ -287,22 +255,18 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
   }
   if (finalize) {
     const double sg = (double)T.sign;
+    if (col < nn) {
 #pragma unroll
-    for (int m = 0; m < MT8; ++m) {
-      const int i = m * 8 + g;
-      if (i < mm) {
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int col = colb + e;
-          if (col < nn) {
-            double2 v = make_double2(sg * acc[m][e].x, sg * acc[m][e].y);
-            if (T.oI >= 0) {
-              const double2 z = __ldcg(a.I + T.oI + (int64_t)(i0 + i) * T.sIi + (int64_t)(c0 + col) * T.sIc);
-              v.x += z.x;
-              v.y += z.y;
-            }
-            __stcg(a.O + T.oO + (int64_t)(i0 + i) * T.sOi + (int64_t)(c0 + col) * T.sOc, v);
+      for (int r = 0; r < RM; ++r) {
+        const int i = rbase + r;
+        if (i < mm) {
+          double2 v = make_double2(sg * acc[r].x, sg * acc[r].y);
+          if (T.oI >= 0) {
+            const double2 z = __ldcg(a.I + T.oI + (int64_t)(i0 + i) * T.sIi + (int64_t)(c0 + col) * T.sIc);
+            v.x += z.x;
+            v.y += z.y;
           }
+          __stcg(a.O + T.oO + (int64_t)(i0 + i) * T.sOi + (int64_t)(c0 + col) * T.sOc, v);
         }
       }
     }
@@ -311,9 +275,10 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
   }
 }
 
-// Persistent dataflow gather-GEMM: output tile 32 x 64
-// (rows padded to a multiple of 8), 8 warps = 8 column tiles of 8, FP64 tensor
-// core MMAs; operands through a 3-stage cp.async pipeline.
+// Output tile: warp w = (wm, wn) = (w % 4, w / 4) owns rows
+// [wm*RM, min(mm, (wm+1)*RM)) with RM = ceil(mm / 4) <= 8 (so the tile is
+// only as tall as the task) and column wn*32 + lane. A values are broadcast
+// shared loads, one B load feeds RM complex FMAs.
 __global__ void __launch_bounds__(256, 2)
 flow_kernel(const FlowArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -323,6 +288,7 @@ flow_kernel(const FlowArgs a) {
   __shared__ int s_item, s_last;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
+  const int wm = warp % GM_WM, wn = warp / GM_WM;
   int32_t* ticket = a.counters;
   for (;;) {
     if (tid == 0) s_item = atomicAdd(ticket, 1);
@@ -334,7 +300,7 @@ flow_kernel(const FlowArgs a) {
     const GWork w = a.work[item];
     const GTask T = a.tasks[w.task];
     const int mm = min(GM_MT, T.m - w.mt * GM_MT);
-    const int MT8 = (mm + 7) / 8;
+    const int RM = (mm + GM_WM - 1) / GM_WM;
     // ---- k tables of this item (segments [ta, tb) clipped to [ka, kb)) ----
     for (int t = w.ta + tid; t < w.tb; t += 256) {
       const GTerm g = a.terms[t];
@@ -348,11 +314,12 @@ flow_kernel(const FlowArgs a) {
       }
     }
     __syncthreads();
-    switch (MT8) {
-      case 1: item_body<1>(a, w, T, kt, As0, Bs0, tid, lane, warp, &s_last, tr); break;
-      case 2: item_body<2>(a, w, T, kt, As0, Bs0, tid, lane, warp, &s_last, tr); break;
-      case 3: item_body<3>(a, w, T, kt, As0, Bs0, tid, lane, warp, &s_last, tr); break;
-      case 4: item_body<4>(a, w, T, kt, As0, Bs0, tid, lane, warp, &s_last, tr); break;
+    switch (RM) {
+#define PS_RM_CASE(R) \
+      case R: item_body<R>(a, w, T, kt, As0, Bs0, tid, lane, wm, wn, &s_last, tr); break;
+      PS_RM_CASE(1) PS_RM_CASE(2) PS_RM_CASE(3) PS_RM_CASE(4) PS_RM_CASE(5) PS_RM_CASE(6)
+      PS_RM_CASE(7) PS_RM_CASE(8)
+#undef PS_RM_CASE
       default: break;
     }
     if (tr) tr[5] = gtimer();
