@@ -231,7 +231,7 @@ def main():
     ratio = rep["ratio"]
 
     # ---- end to end: host (pinned) buffers through the C ABI, copies inside ----
-    Bh = torch.from_numpy(np.ascontiguousarray(B.T)).pin_memory().T
+    Bh = torch.from_numpy(np.array(B.T, order="C")).pin_memory().T
     Xh = torch.empty((nrhs, N), dtype=torch.complex128).pin_memory().T
     for _ in range(max(1, args.warmup)):
         h.solve(Bh, Xh, stream=st, want_norms=False)
@@ -259,15 +259,19 @@ def main():
     peaks = _peaks()
     clocks = clk.summary()
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    fp64_peak = SM_COUNT * DFMA_PER_SM_PER_CLK * 2 * sm_max * 1e6 / 1e12   # TFLOP/s
+    # measured FP64 ceiling on this pool's B200 (scripts/fp64_peak.cu, profiles/r1/fp64_peak_b200.json):
+    # mma.sync f64 37.0 TF, DFMA loop 34.0 TF; derived 148 SM x 64 FMA/clk x 2 x 1965 MHz = 37.2 TF
+    fp64_peak = 37.02
     achieved = g_fl / (g_ms * 1e-3) / 1e12 if g_ms > 0 else 0.0
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     roof = {"bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
             "frac": achieved / fp64_peak, "traffic": None,
-            "kernel": "gemm_kernel (gather-GEMM, all sweep/D^-1/far launches)",
+            "kernel": "flow_kernel (persistent gather-GEMM: all sweep / D^-1 / far-field launches)",
             "kernel_share_of_step": g_ms / tot_ms if tot_ms > 0 else None,
-            "peak_source": f"derived: {SM_COUNT} SM x {DFMA_PER_SM_PER_CLK} DFMA/clk x 2 flop x "
-                           f"{sm_max:.0f} MHz (FP64 has no tcgen05 kind; DESIGN.md §Roofline)",
+            "peak_source": "measured FP64 ceiling on this pool's B200 (mma.sync f64 37.0 TF, DFMA loop "
+                           "34.0 TF; profiles/r1/fp64_peak_b200.json) = derived 148 SM x 64 FMA/clk x 2 x "
+                           "1.965 GHz; FP64 has no tcgen05 kind",
+            "kernel_name_in_ncu": "ps::flow_kernel",
             "hbm_view": {"operator_bytes_per_step": g_by / max(1, args.profile_steps),
                          "achieved_GBs": g_by / (g_ms * 1e-3) / 1e9 if g_ms > 0 else 0.0,
                          "peak_GBs": hbm_peak},
