@@ -193,3 +193,17 @@ def test_singular_leaf_is_named(tmp_path):
         h.setup()
     assert e.value.status == PS_ESINGULAR
     assert "(leaf 0)" in str(e.value)
+
+
+@pytest.mark.slow
+def test_ops_c3(cfgdata):
+    """BASELINE config 2 (sphere N=30720, 113-unknown leaves: row tiles 32+32+32+17)."""
+    _ops_check(cfgdata("C3")["hm"], nrhs=2)
+
+
+@pytest.mark.slow
+def test_solve_c3_plane_waves(cfgdata):
+    meta = cfgdata("C3")
+    B, _ = read_rhs(meta["rhs"])
+    _solve_check(meta["hm"], np.asfortranarray(B[:, :181]), check_host=False)
+    _solve_check(meta["hm"], np.asfortranarray(B[:, :1]), check_host=True)     # the 1-RHS run
