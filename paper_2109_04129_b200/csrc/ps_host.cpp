@@ -161,6 +161,9 @@ struct Table {
   int32_t n_units = 0, n_tiles = 0;
   int64_t n_slots = 0;
   int chunk_steps = CHUNK_STEPS;
+  int narrow = 0;          // 1: 64 x 8 tiles (small nrhs)
+  int MT() const { return narrow ? GN_MT : GM_MT; }
+  int NT() const { return narrow ? GN_NT : GM_NT; }
 
   int32_t add_task(int64_t oO, int64_t sOi, int64_t sOc, int64_t oI, int64_t sIi, int64_t sIc, int m,
                    int n, int sign) {
@@ -227,7 +230,8 @@ struct Table {
   void tile(int32_t task, int isolate = 0, int steps = 0) {
     if (steps <= 0) steps = chunk_steps;
     GTask& t = tasks[task];
-    const int nmt = t.n_mt, nnt = (t.n + GM_NT - 1) / GM_NT;
+    t.n_mt = (t.m + MT() - 1) / MT();
+    const int nmt = t.n_mt, nnt = (t.n + NT() - 1) / NT();
     t.unit0 = n_units;
     n_units += nnt;
     std::vector<std::array<int32_t, 4>> ch;   // (ka, kb, ta, tb)
@@ -297,7 +301,7 @@ struct Table {
     fa.pad = 0;
     fa.partial = d_partial.p;
     fa.trace = nullptr;
-    fa.pad2 = 0;
+    fa.narrow = narrow;
     fa.pad3 = 0;
     if (pf && pf->trace_on && cls == pf->trace_cls) {
       pf->trace_buf.alloc(6 * bt.nw);
@@ -774,6 +778,8 @@ void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
     byh[h->height[p]].push_back((int32_t)p);
     byd[h->depth[p]].push_back((int32_t)p);
   }
+  const int narrow = (R <= 8) ? 1 : 0;
+  for (Table* tb : {&sp.fwd, &sp.bwd, &sp.dinv, &sp.far1, &sp.far2}) tb->narrow = narrow;
   std::vector<int32_t> ftask(nl, -1), btask(nl, -1);
   // narrow levels (the separator chains) get small split-K chunks so each hop
   // waits on ~1-4 k-steps; wide levels keep large chunks (less overhead)

@@ -73,7 +73,8 @@ struct FlowArgs {
   int32_t pad;
   double2* partial;        // split-K partial tiles, GM_MT * GM_NT each
   int64_t* trace;          // optional: 6 x int64 per item (item, smid, t_fetch, t_ready, t_computed, t_done), ns
-  int32_t pad2, pad3;
+  int32_t narrow;          // 1: narrow 64 x 8 tiles (small nrhs), 0: 32 x 64 tiles
+  int32_t pad3;
 };
 
 // Tile geometry of the gather-GEMM kernel (ps_kernels.cu).
@@ -82,6 +83,9 @@ constexpr int GM_WM = 4, GM_WN = 2;         // warp grid: 4 row groups x 2 colum
 constexpr int GM_MT = GM_WM * GM_RMAX;      // 32 rows per tile (max)
 constexpr int GM_NT = GM_WN * 32;           // 64 columns per tile (one per lane)
 constexpr int GM_KC = 16;
+// narrow tile (small nrhs: GEMV-like, operator-streaming): 64 rows x 8 columns
+constexpr int GN_MT = 64;
+constexpr int GN_NT = 8;
 constexpr int GM_CHUNK_K = 512;   // max virtual k per work item (shared-memory k tables)
 constexpr int GM_MAXSEG = 96;     // max segments per work item
 

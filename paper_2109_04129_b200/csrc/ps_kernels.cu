@@ -79,7 +79,8 @@ constexpr int B_PER_T = GM_NT * KC / 256;   // 4 B elements per thread per k-ste
 constexpr int AS_LD = GM_MT;                // As[k][i]
 constexpr int BS_LD = GM_NT;                // Bs[k][c]
 constexpr int NSTAGE = 3;                   // cp.async pipeline depth
-constexpr int STAGE_A = KC * AS_LD, STAGE_B = KC * BS_LD;
+constexpr int STAGE_A = KC * (GM_MT > GN_MT ? GM_MT : GN_MT);   // both tile geometries fit a stage
+constexpr int STAGE_B = KC * (GM_NT > GN_NT ? GM_NT : GN_NT);
 
 __device__ __forceinline__ void a_map(bool a_km, int e, int& i, int& k) {
   if (a_km) { k = e & (KC - 1); i = e / KC; } else { i = e % GM_MT; k = e / GM_MT; }
@@ -98,28 +99,34 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+template <int MT, int NT>
 __device__ __forceinline__ void issue_a(const KTab& kt, int k0, int klen, int i0, int mm, bool a_km,
                                         const double2* __restrict__ Ab, int tid, double2* As) {
 #pragma unroll
-  for (int q = 0; q < A_PER_T; ++q) {
+  for (int q = 0; q < MT * KC / 256; ++q) {
+    const int e = tid + q * 256;
     int i, k;
-    a_map(a_km, tid + q * 256, i, k);
+    if (a_km) { k = e & (KC - 1); i = e / KC; } else { i = e % MT; k = e / MT; }
     const int kk = k0 + k;
     const bool v = (i < mm && kk < klen);
     const double2* src = v ? Ab + kt.kA[kk] + (int64_t)(i0 + i) * kt.kSi[kk] : Ab;
-    cp_async16(As + k * AS_LD + i, src, v);
+    cp_async16(As + k * MT + i, src, v);
   }
 }
+template <int MT, int NT>
 __device__ __forceinline__ void issue_b(const KTab& kt, int k0, int klen, int c0, int nn, bool b_km,
                                         const double2* __restrict__ Bb, int tid, double2* Bs) {
+  constexpr int NB = NT * KC;
 #pragma unroll
-  for (int q = 0; q < B_PER_T; ++q) {
+  for (int q = 0; q < (NB + 255) / 256; ++q) {
+    const int e = tid + q * 256;
+    if (NB % 256 != 0 && e >= NB) break;
     int c, k;
-    b_map(b_km, tid + q * 256, c, k);
+    if (b_km) { k = e & (KC - 1); c = e / KC; } else { c = e % NT; k = e / NT; }
     const int kk = k0 + k;
     const bool v = (c < nn && kk < klen);
     const double2* src = v ? Bb + kt.kB[kk] + (int64_t)(c0 + c) * kt.kSc[kk] : Bb;
-    cp_async16(Bs + k * BS_LD + c, src, v);
+    cp_async16(Bs + k * NT + c, src, v);
   }
 }
 
@@ -155,7 +162,7 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
   // ---- prologue part 1: A of stages 0..NSTAGE-2 (one group) ----
 #pragma unroll
   for (int s = 0; s < NSTAGE - 1; ++s)
-    if (s < nsteps) issue_a(kt, s * KC, klen, i0, mm, a_km, a.A, tid, As0 + s * STAGE_A);
+    if (s < nsteps) issue_a<GM_MT, GM_NT>(kt, s * KC, klen, i0, mm, a_km, a.A, tid, As0 + s * STAGE_A);
   cp_commit();
   // ---- wait for the producers of B (warp 0, one segment per lane) ----
   if (tid < 32) {
@@ -173,7 +180,7 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
   // ---- prologue part 2: B of stages 0..NSTAGE-2 (one group each) ----
 #pragma unroll
   for (int s = 0; s < NSTAGE - 1; ++s) {
-    if (s < nsteps) issue_b(kt, s * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + s * STAGE_B);
+    if (s < nsteps) issue_b<GM_MT, GM_NT>(kt, s * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + s * STAGE_B);
     cp_commit();
   }
   double2 acc[RM];
@@ -195,8 +202,8 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
     const int sn = s + NSTAGE - 1;
     if (sn < nsteps) {
       const int stn = sn % NSTAGE;
-      issue_a(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * STAGE_A);
-      issue_b(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * STAGE_B);
+      issue_a<GM_MT, GM_NT>(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * STAGE_A);
+      issue_b<GM_MT, GM_NT>(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * STAGE_B);
     }
     cp_commit();
   }
@@ -275,6 +282,137 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
   }
 }
 
+// Narrow tile (small nrhs): 64 rows x 8 columns; thread t owns row t % 64 and
+// columns 2 (t / 64) + {0, 1}. The operator panel is streamed through the same
+// cp.async ring (HBM-bound regime), B values are warp broadcasts.
+__device__ __forceinline__ void item_body_narrow(const FlowArgs& a, const GWork& w, const GTask& T,
+                                                 const KTab& kt, double2* As0, double2* Bs0, int tid,
+                                                 int* s_last, int64_t* tr) {
+  const int i0 = w.mt * GN_MT, c0 = w.nt * GN_NT;
+  const int mm = min(GN_MT, T.m - i0), nn = min(GN_NT, T.n - c0);
+  const int klen = w.kb - w.ka;
+  const int row = tid & (GN_MT - 1), cb = 2 * (tid / GN_MT);
+  int32_t* done = a.counters + 1;
+  int32_t* arrive = a.counters + 1 + a.n_units;
+  const bool a_km = T.a_kmajor != 0, b_km = T.b_kmajor != 0;
+  const int nsteps = (klen + KC - 1) / KC;
+#pragma unroll
+  for (int s = 0; s < NSTAGE - 1; ++s)
+    if (s < nsteps) issue_a<GN_MT, GN_NT>(kt, s * KC, klen, i0, mm, a_km, a.A, tid, As0 + s * STAGE_A);
+  cp_commit();
+  if (tid < 32) {
+    for (int t = w.ta + tid; t < w.tb; t += 32) {
+      const int dep = a.terms[t].dep;
+      if (dep >= 0) {
+        const int32_t need = a.tasks[dep].n_mt;
+        const int32_t* flag = done + a.tasks[dep].unit0 + w.nt;
+        while (ld_acquire(flag) < need) __nanosleep(32);
+      }
+    }
+  }
+  __syncthreads();
+  if (tr) tr[3] = gtimer();
+#pragma unroll
+  for (int s = 0; s < NSTAGE - 1; ++s) {
+    if (s < nsteps) issue_b<GN_MT, GN_NT>(kt, s * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + s * STAGE_B);
+    cp_commit();
+  }
+  double2 acc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+  const bool live = (row < mm) && (cb < nn);
+  for (int s = 0; s < nsteps; ++s) {
+    cp_wait<NSTAGE - 2>();
+    __syncthreads();
+    const int st = s % NSTAGE;
+    if (live) {
+      const double2* As = As0 + st * STAGE_A + row;
+      const double2* Bs = Bs0 + st * STAGE_B + cb;
+#pragma unroll
+      for (int k = 0; k < KC; ++k) {
+        const double2 av = As[k * GN_MT];
+        cfma(acc[0], av, Bs[k * GN_NT]);
+        cfma(acc[1], av, Bs[k * GN_NT + 1]);
+      }
+    }
+    const int sn = s + NSTAGE - 1;
+    if (sn < nsteps) {
+      const int stn = sn % NSTAGE;
+      issue_a<GN_MT, GN_NT>(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * STAGE_A);
+      issue_b<GN_MT, GN_NT>(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * STAGE_B);
+    }
+    cp_commit();
+  }
+  cp_wait<0>();
+  __syncthreads();
+  if (tr) tr[4] = gtimer();
+  bool finalize = true;
+  if (w.nchunks > 1) {
+    const int64_t TS = (int64_t)(GM_MT * GM_NT);
+    const bool crit_mode = w.crit >= 0;
+    if (crit_mode && w.chunk == w.crit) {
+      if (tid == 0)
+        while (ld_acquire(arrive + w.tile) < w.nchunks) __nanosleep(32);
+      __syncthreads();
+      const double2* G = a.partial + (w.slot + w.crit) * TS;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double2 v = __ldcg(G + row * GN_NT + cb + e);
+        if (w.crit == 0) { acc[e].x = acc[e].x + v.x; acc[e].y = acc[e].y + v.y; }
+        else { acc[e].x = v.x + acc[e].x; acc[e].y = v.y + acc[e].y; }
+      }
+    } else {
+      double2* P = a.partial + (w.slot + w.chunk) * TS;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) __stcg(P + row * GN_NT + cb + e, acc[e]);
+      __syncthreads();
+      const int group = crit_mode ? w.nchunks - 1 : w.nchunks;
+      if (tid == 0) *s_last = (atom_acq_rel(arrive + w.tile, 1) == group - 1);
+      __syncthreads();
+      finalize = *s_last;
+      if (finalize) {
+        acc[0] = acc[1] = make_double2(0.0, 0.0);
+        for (int c = 0; c < w.nchunks; ++c) {
+          if (c == w.crit) continue;
+          const double2* Q = a.partial + (w.slot + c) * TS;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const double2 v = __ldcg(Q + row * GN_NT + cb + e);
+            acc[e].x += v.x;
+            acc[e].y += v.y;
+          }
+        }
+        if (crit_mode) {
+          double2* G = a.partial + (w.slot + w.crit) * TS;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) __stcg(G + row * GN_NT + cb + e, acc[e]);
+          __syncthreads();
+          if (tid == 0) red_release(arrive + w.tile, 1);
+          finalize = false;
+        }
+      }
+    }
+  }
+  if (finalize) {
+    const double sg = (double)T.sign;
+    if (row < mm) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = cb + e;
+        if (col < nn) {
+          double2 v = make_double2(sg * acc[e].x, sg * acc[e].y);
+          if (T.oI >= 0) {
+            const double2 z = __ldcg(a.I + T.oI + (int64_t)(i0 + row) * T.sIi + (int64_t)(c0 + col) * T.sIc);
+            v.x += z.x;
+            v.y += z.y;
+          }
+          __stcg(a.O + T.oO + (int64_t)(i0 + row) * T.sOi + (int64_t)(c0 + col) * T.sOc, v);
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) red_release(done + T.unit0 + w.nt, 1);
+  }
+}
+
 // Output tile: warp w = (wm, wn) = (w % 4, w / 4) owns rows
 // [wm*RM, min(mm, (wm+1)*RM)) with RM = ceil(mm / 4) <= 8 (so the tile is
 // only as tall as the task) and column wn*32 + lane. A values are broadcast
@@ -300,7 +438,7 @@ flow_kernel(const FlowArgs a) {
     const GWork w = a.work[item];
     const GTask T = a.tasks[w.task];
     const int mm = min(GM_MT, T.m - w.mt * GM_MT);
-    const int RM = (mm + GM_WM - 1) / GM_WM;
+    const int RM = a.narrow ? 0 : (mm + GM_WM - 1) / GM_WM;
     // ---- k tables of this item (segments [ta, tb) clipped to [ka, kb)) ----
     for (int t = w.ta + tid; t < w.tb; t += 256) {
       const GTerm g = a.terms[t];
@@ -315,6 +453,7 @@ flow_kernel(const FlowArgs a) {
     }
     __syncthreads();
     switch (RM) {
+      case 0: item_body_narrow(a, w, T, kt, As0, Bs0, tid, &s_last, tr); break;
 #define PS_RM_CASE(R) \
       case R: item_body<R>(a, w, T, kt, As0, Bs0, tid, lane, wm, wn, &s_last, tr); break;
       PS_RM_CASE(1) PS_RM_CASE(2) PS_RM_CASE(3) PS_RM_CASE(4) PS_RM_CASE(5) PS_RM_CASE(6)
