@@ -779,11 +779,18 @@ void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
     byd[h->depth[p]].push_back((int32_t)p);
   }
   const int narrow = (R <= 8) ? 1 : 0;
-  for (Table* tb : {&sp.fwd, &sp.bwd, &sp.dinv, &sp.far1, &sp.far2}) tb->narrow = narrow;
+  for (Table* tb : {&sp.fwd, &sp.bwd, &sp.dinv, &sp.far1, &sp.far2}) {
+    tb->narrow = narrow;
+    if (narrow) tb->chunk_steps = 4;
+  }
   std::vector<int32_t> ftask(nl, -1), btask(nl, -1);
   // narrow levels (the separator chains) get small split-K chunks so each hop
   // waits on ~1-4 k-steps; wide levels keep large chunks (less overhead)
-  auto steps_for = [](size_t width) { return width <= 4 ? 4 : (width <= 16 ? 8 : 16); };
+  // (narrow tiles stream the operator: always small chunks for parallel streams)
+  auto steps_for = [narrow](size_t width) {
+    if (narrow) return 4;
+    return width <= 4 ? 4 : (width <= 16 ? 8 : 16);
+  };
   for (int lev = 0; lev <= h->max_height; ++lev) {
     const int stp = steps_for(byh[lev].size());
     for (int32_t q : byh[lev]) {
