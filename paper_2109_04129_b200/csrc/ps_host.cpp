@@ -254,9 +254,13 @@ struct Table {
     if (isolate != 0 && nseg >= 2 && nch >= 2) crit = isolate > 0 ? 0 : nch - 1;
     for (int a = 0; a < nmt; ++a)
       for (int b = 0; b < nnt; ++b) {
-        const int32_t tile_id = n_tiles++;
+        // split-K tiles: counters [top, subgroups...], slots [chunks..., subgroup sums...]
+        const int G = (crit >= 0) ? nch - 1 : nch;
+        const int nsub = (G + 15) / 16;       // SUBG in ps_kernels.cu
+        const int32_t tile_id = n_tiles;
+        if (nch > 1) n_tiles += 1 + nsub;
         const int64_t slot = nch > 1 ? n_slots : 0;
-        if (nch > 1) n_slots += nch;
+        if (nch > 1) n_slots += nch + nsub;
         for (int c = 0; c < nch; ++c)
           if (c != crit)
             work.push_back({task, a, b, ch[c][2], ch[c][3], ch[c][0], ch[c][1], c, nch, tile_id, crit, 0, slot});

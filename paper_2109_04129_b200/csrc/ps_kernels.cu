@@ -74,8 +74,6 @@ struct KTab {
   int32_t kSc[GM_CHUNK_K];
 };
 
-constexpr int A_PER_T = GM_MT * KC / 256;   // 2 A elements per thread per k-step
-constexpr int B_PER_T = GM_NT * KC / 256;   // 4 B elements per thread per k-step
 constexpr int AS_LD = GM_MT;                // As[k][i]
 constexpr int BS_LD = GM_NT;                // Bs[k][c]
 constexpr int NSTAGE = 3;                   // cp.async pipeline depth
@@ -142,6 +140,103 @@ __device__ __forceinline__ int atom_acq_rel(int32_t* p, int v) {
 
 constexpr size_t FLOW_SMEM = (size_t)NSTAGE * (STAGE_A + STAGE_B) * sizeof(double2) + sizeof(KTab);
 
+// ---------------------------------------------------------------------------
+// Split-K combine of one output tile, fixed summation order (deterministic).
+// Each thread owns E tile elements at tile offsets off[e] with partial sums
+// acc[e]. Non-critical chunks (all chunks except `crit`) are summed by a fixed
+// two-level tree: subgroups of SUBG consecutive chunks (by rank), the last
+// arriver of a subgroup sums its members in rank order, the last subgroup sums
+// the subgroup sums in order. Counters of the tile: arrive[tile] (top) and
+// arrive[tile + 1 + sg]. Slots: [slot, slot + nchunks) chunk partials,
+// [slot + nchunks, ...) subgroup sums; the group sum goes to slot `crit`.
+// crit >= 0: the critical chunk (queued last) waits for top == nsub + 1 and
+// adds the group sum (p_0 + G, or G + p_last); crit < 0: the tree root finalises.
+// Returns true when the caller must finalise with acc.
+constexpr int SUBG = 16;
+
+template <int E>
+__device__ __forceinline__ bool splitk_combine(const FlowArgs& a, const GWork& w, double2 (&acc)[E],
+                                               const int (&off)[E], const bool (&own)[E], int tid,
+                                               int* s_flag) {
+  if (w.nchunks <= 1) return true;
+  const int64_t TS = (int64_t)(GM_MT * GM_NT);
+  int32_t* ctr = a.counters + 1 + a.n_units + w.tile;
+  const bool crit_mode = w.crit >= 0;
+  const int G = crit_mode ? w.nchunks - 1 : w.nchunks;       // non-critical chunks
+  const int nsub = (G + SUBG - 1) / SUBG;
+  if (crit_mode && w.chunk == w.crit) {
+    if (tid == 0)
+      while (ld_acquire(ctr) < nsub + 1) __nanosleep(32);
+    __syncthreads();
+    const double2* Gs = a.partial + (w.slot + w.crit) * TS;
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      if (own[e]) {
+        const double2 v = __ldcg(Gs + off[e]);
+        if (w.crit == 0) { acc[e].x = acc[e].x + v.x; acc[e].y = acc[e].y + v.y; }  // p_0 + G
+        else { acc[e].x = v.x + acc[e].x; acc[e].y = v.y + acc[e].y; }              // G + p_last
+      }
+    return true;
+  }
+  auto chunk_of_rank = [&](int r) { return (crit_mode && r >= w.crit) ? r + 1 : r; };
+  const int rank = (crit_mode && w.chunk > w.crit) ? w.chunk - 1 : w.chunk;
+  const int sg = rank / SUBG;
+  const int r0 = sg * SUBG, r1 = min(G, r0 + SUBG);
+  double2* P = a.partial + (w.slot + w.chunk) * TS;
+#pragma unroll
+  for (int e = 0; e < E; ++e)
+    if (own[e]) __stcg(P + off[e], acc[e]);
+  __syncthreads();
+  if (tid == 0) *s_flag = (atom_acq_rel(ctr + 1 + sg, 1) == (r1 - r0) - 1);
+  __syncthreads();
+  if (!*s_flag) return false;
+  // last of its subgroup: sum the members in rank order (loads batched)
+#pragma unroll
+  for (int e = 0; e < E; ++e) acc[e] = make_double2(0.0, 0.0);
+  for (int r = r0; r < r1; ++r) {
+    const double2* Q = a.partial + (w.slot + chunk_of_rank(r)) * TS;
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      if (own[e]) {
+        const double2 v = __ldcg(Q + off[e]);
+        acc[e].x += v.x;
+        acc[e].y += v.y;
+      }
+  }
+  if (nsub > 1) {
+    double2* S = a.partial + (w.slot + w.nchunks + sg) * TS;
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      if (own[e]) __stcg(S + off[e], acc[e]);
+    __syncthreads();
+    if (tid == 0) *s_flag = (atom_acq_rel(ctr, 1) == nsub - 1);
+    __syncthreads();
+    if (!*s_flag) return false;
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[e] = make_double2(0.0, 0.0);
+    for (int q = 0; q < nsub; ++q) {
+      const double2* Q = a.partial + (w.slot + w.nchunks + q) * TS;
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (own[e]) {
+          const double2 v = __ldcg(Q + off[e]);
+          acc[e].x += v.x;
+          acc[e].y += v.y;
+        }
+    }
+  } else if (crit_mode) {
+    if (tid == 0) red_release(ctr, 1);       // top counts the (single) subgroup
+  }
+  if (!crit_mode) return true;                // the tree root finalises
+  double2* Gs = a.partial + (w.slot + w.crit) * TS;
+#pragma unroll
+  for (int e = 0; e < E; ++e)
+    if (own[e]) __stcg(Gs + off[e], acc[e]);
+  __syncthreads();
+  if (tid == 0) red_release(ctr, 1);          // top reaches nsub + 1: group sum published
+  return false;
+}
+
 // Everything of one work item, for a compile-time rows-per-warp RM (so the
 // FMA stream is branch-free). A operands (operator panels: immutable in the
 // launch) of the first stages are requested before waiting for the producers
@@ -156,7 +251,6 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
   const int rbase = wm * RM;
   const int col = wn * 32 + lane;
   int32_t* done = a.counters + 1;
-  int32_t* arrive = a.counters + 1 + a.n_units;
   const bool a_km = T.a_kmajor != 0, b_km = T.b_kmajor != 0;
   const int nsteps = (klen + KC - 1) / KC;
   // ---- prologue part 1: A of stages 0..NSTAGE-2 (one group) ----
@@ -211,55 +305,14 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
   __syncthreads();          // all warps done with the stage buffers before the next item
   if (tr) tr[4] = gtimer();
   // ---- split-K combine (fixed summation order => deterministic) ----
-  bool finalize = true;
-  if (w.nchunks > 1) {
-    const int64_t TS = (int64_t)(GM_MT * GM_NT);
-    const bool crit_mode = w.crit >= 0;
-    if (crit_mode && w.chunk == w.crit) {
-      // the other chunks' sum arrives in slot `crit` once arrive[tile] == nchunks
-      if (tid == 0)
-        while (ld_acquire(arrive + w.tile) < w.nchunks) __nanosleep(32);
-      __syncthreads();
-      const double2* G = a.partial + (w.slot + w.crit) * TS;
+  int off[RM];
+  bool own[RM];
 #pragma unroll
-      for (int r = 0; r < RM; ++r) {
-        const double2 v = __ldcg(G + (rbase + r) * GM_NT + col);
-        if (w.crit == 0) { acc[r].x = acc[r].x + v.x; acc[r].y = acc[r].y + v.y; }  // p_0 + G
-        else { acc[r].x = v.x + acc[r].x; acc[r].y = v.y + acc[r].y; }              // G + p_last
-      }
-    } else {
-      double2* P = a.partial + (w.slot + w.chunk) * TS;
-#pragma unroll
-      for (int r = 0; r < RM; ++r) __stcg(P + (rbase + r) * GM_NT + col, acc[r]);
-      __syncthreads();
-      const int group = crit_mode ? w.nchunks - 1 : w.nchunks;
-      if (tid == 0) *s_last = (atom_acq_rel(arrive + w.tile, 1) == group - 1);
-      __syncthreads();
-      finalize = *s_last;
-      if (finalize) {
-#pragma unroll
-        for (int r = 0; r < RM; ++r) acc[r] = make_double2(0.0, 0.0);
-        for (int c = 0; c < w.nchunks; ++c) {
-          if (c == w.crit) continue;
-          const double2* Q = a.partial + (w.slot + c) * TS;
-#pragma unroll
-          for (int r = 0; r < RM; ++r) {
-            const double2 v = __ldcg(Q + (rbase + r) * GM_NT + col);
-            acc[r].x += v.x;
-            acc[r].y += v.y;
-          }
-        }
-        if (crit_mode) {        // publish the group sum for the critical chunk
-          double2* G = a.partial + (w.slot + w.crit) * TS;
-#pragma unroll
-          for (int r = 0; r < RM; ++r) __stcg(G + (rbase + r) * GM_NT + col, acc[r]);
-          __syncthreads();
-          if (tid == 0) red_release(arrive + w.tile, 1);
-          finalize = false;
-        }
-      }
-    }
+  for (int r = 0; r < RM; ++r) {
+    off[r] = (rbase + r) * GM_NT + col;
+    own[r] = true;
   }
+  const bool finalize = splitk_combine<RM>(a, w, acc, off, own, tid, s_last);
   if (finalize) {
     const double sg = (double)T.sign;
     if (col < nn) {
@@ -293,7 +346,6 @@ __device__ __forceinline__ void item_body_narrow(const FlowArgs& a, const GWork&
   const int klen = w.kb - w.ka;
   const int row = tid & (GN_MT - 1), cb = 2 * (tid / GN_MT);
   int32_t* done = a.counters + 1;
-  int32_t* arrive = a.counters + 1 + a.n_units;
   const bool a_km = T.a_kmajor != 0, b_km = T.b_kmajor != 0;
   const int nsteps = (klen + KC - 1) / KC;
 #pragma unroll
@@ -344,53 +396,9 @@ __device__ __forceinline__ void item_body_narrow(const FlowArgs& a, const GWork&
   cp_wait<0>();
   __syncthreads();
   if (tr) tr[4] = gtimer();
-  bool finalize = true;
-  if (w.nchunks > 1) {
-    const int64_t TS = (int64_t)(GM_MT * GM_NT);
-    const bool crit_mode = w.crit >= 0;
-    if (crit_mode && w.chunk == w.crit) {
-      if (tid == 0)
-        while (ld_acquire(arrive + w.tile) < w.nchunks) __nanosleep(32);
-      __syncthreads();
-      const double2* G = a.partial + (w.slot + w.crit) * TS;
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const double2 v = __ldcg(G + row * GN_NT + cb + e);
-        if (w.crit == 0) { acc[e].x = acc[e].x + v.x; acc[e].y = acc[e].y + v.y; }
-        else { acc[e].x = v.x + acc[e].x; acc[e].y = v.y + acc[e].y; }
-      }
-    } else {
-      double2* P = a.partial + (w.slot + w.chunk) * TS;
-#pragma unroll
-      for (int e = 0; e < 2; ++e) __stcg(P + row * GN_NT + cb + e, acc[e]);
-      __syncthreads();
-      const int group = crit_mode ? w.nchunks - 1 : w.nchunks;
-      if (tid == 0) *s_last = (atom_acq_rel(arrive + w.tile, 1) == group - 1);
-      __syncthreads();
-      finalize = *s_last;
-      if (finalize) {
-        acc[0] = acc[1] = make_double2(0.0, 0.0);
-        for (int c = 0; c < w.nchunks; ++c) {
-          if (c == w.crit) continue;
-          const double2* Q = a.partial + (w.slot + c) * TS;
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const double2 v = __ldcg(Q + row * GN_NT + cb + e);
-            acc[e].x += v.x;
-            acc[e].y += v.y;
-          }
-        }
-        if (crit_mode) {
-          double2* G = a.partial + (w.slot + w.crit) * TS;
-#pragma unroll
-          for (int e = 0; e < 2; ++e) __stcg(G + row * GN_NT + cb + e, acc[e]);
-          __syncthreads();
-          if (tid == 0) red_release(arrive + w.tile, 1);
-          finalize = false;
-        }
-      }
-    }
-  }
+  int off[2] = {row * GN_NT + cb, row * GN_NT + cb + 1};
+  bool own[2] = {true, true};
+  const bool finalize = splitk_combine<2>(a, w, acc, off, own, tid, s_last);
   if (finalize) {
     const double sg = (double)T.sign;
     if (row < mm) {
