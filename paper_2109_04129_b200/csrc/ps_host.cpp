@@ -20,6 +20,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -306,7 +307,11 @@ struct Table {
     fa.partial = d_partial.p;
     fa.trace = nullptr;
     fa.narrow = narrow;
-    fa.pad3 = 0;
+    static const int mma_env = [] {
+      const char* e = std::getenv("PS_MMA");
+      return (e && std::string(e) == "dmma") ? 1 : 0;
+    }();
+    fa.mma = mma_env;
     if (pf && pf->trace_on && cls == pf->trace_cls) {
       pf->trace_buf.alloc(6 * bt.nw);
       fa.trace = pf->trace_buf.p;

@@ -74,7 +74,7 @@ struct FlowArgs {
   double2* partial;        // split-K partial tiles, GM_MT * GM_NT each
   int64_t* trace;          // optional: 6 x int64 per item (item, smid, t_fetch, t_ready, t_computed, t_done), ns
   int32_t narrow;          // 1: narrow 64 x 8 tiles (small nrhs), 0: 32 x 64 tiles
-  int32_t pad3;
+  int32_t mma;             // wide tiles: 0 = DFMA consumer, 1 = FP64 tensor-core (DMMA) consumer
 };
 
 // Tile geometry of the gather-GEMM kernel (ps_kernels.cu).

@@ -335,6 +335,120 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
   }
 }
 
+// FP64 tensor-core MMA: D(8x8) += A(8x4, row) * B(4x8, col); per lane
+// A[g][q], B[q][g], C[g][2q], C[g][2q+1] with g = lane / 4, q = lane % 4.
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// Wide tile on FP64 tensor cores: MT8 = ceil(rows / 8) <= 4 row tiles of 8;
+// warp w computes column tile w (8 columns) for all row tiles; a complex
+// product is 4 real DMMAs fed by one 16-byte shared load per fragment element.
+template <int MT8>
+__device__ __forceinline__ void item_body_dmma(const FlowArgs& a, const GWork& w, const GTask& T,
+                                               const KTab& kt, double2* As0, double2* Bs0, int tid,
+                                               int lane, int warp, int* s_last, int64_t* tr) {
+  const int i0 = w.mt * GM_MT, c0 = w.nt * GM_NT;
+  const int mm = min(GM_MT, T.m - i0), nn = min(GM_NT, T.n - c0);
+  const int klen = w.kb - w.ka;
+  const int g = lane >> 2, q = lane & 3;
+  int32_t* done = a.counters + 1;
+  const bool a_km = T.a_kmajor != 0, b_km = T.b_kmajor != 0;
+  const int nsteps = (klen + KC - 1) / KC;
+#pragma unroll
+  for (int s = 0; s < NSTAGE - 1; ++s)
+    if (s < nsteps) issue_a<GM_MT, GM_NT>(kt, s * KC, klen, i0, mm, a_km, a.A, tid, As0 + s * STAGE_A);
+  cp_commit();
+  if (tid < 32) {
+    for (int t = w.ta + tid; t < w.tb; t += 32) {
+      const int dep = a.terms[t].dep;
+      if (dep >= 0) {
+        const int32_t need = a.tasks[dep].n_mt;
+        const int32_t* flag = done + a.tasks[dep].unit0 + w.nt;
+        while (ld_acquire(flag) < need) __nanosleep(32);
+      }
+    }
+  }
+  __syncthreads();
+  if (tr) tr[3] = gtimer();
+#pragma unroll
+  for (int s = 0; s < NSTAGE - 1; ++s) {
+    if (s < nsteps) issue_b<GM_MT, GM_NT>(kt, s * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + s * STAGE_B);
+    cp_commit();
+  }
+  double cre[MT8][2], cim[MT8][2];
+#pragma unroll
+  for (int m = 0; m < MT8; ++m) cre[m][0] = cre[m][1] = cim[m][0] = cim[m][1] = 0.0;
+  for (int s = 0; s < nsteps; ++s) {
+    cp_wait<NSTAGE - 2>();
+    __syncthreads();
+    const int st = s % NSTAGE;
+    const double2* As = As0 + st * STAGE_A + q * GM_MT + g;
+    const double2* Bs = Bs0 + st * STAGE_B + q * GM_NT + warp * 8 + g;
+#pragma unroll
+    for (int kk = 0; kk < KC / 4; ++kk) {
+      const double2 b = Bs[kk * 4 * GM_NT];
+#pragma unroll
+      for (int m = 0; m < MT8; ++m) {
+        const double2 av = As[kk * 4 * GM_MT + m * 8];
+        dmma(cre[m][0], cre[m][1], av.x, b.x);
+        dmma(cre[m][0], cre[m][1], -av.y, b.y);
+        dmma(cim[m][0], cim[m][1], av.x, b.y);
+        dmma(cim[m][0], cim[m][1], av.y, b.x);
+      }
+    }
+    const int sn = s + NSTAGE - 1;
+    if (sn < nsteps) {
+      const int stn = sn % NSTAGE;
+      issue_a<GM_MT, GM_NT>(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * STAGE_A);
+      issue_b<GM_MT, GM_NT>(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * STAGE_B);
+    }
+    cp_commit();
+  }
+  cp_wait<0>();
+  __syncthreads();
+  if (tr) tr[4] = gtimer();
+  double2 acc[2 * MT8];
+  int off[2 * MT8];
+  bool own[2 * MT8];
+  const int colb = warp * 8 + 2 * q;
+#pragma unroll
+  for (int m = 0; m < MT8; ++m)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      acc[2 * m + e] = make_double2(cre[m][e], cim[m][e]);
+      off[2 * m + e] = (m * 8 + g) * GM_NT + colb + e;
+      own[2 * m + e] = true;
+    }
+  const bool finalize = splitk_combine<2 * MT8>(a, w, acc, off, own, tid, s_last);
+  if (finalize) {
+    const double sg = (double)T.sign;
+#pragma unroll
+    for (int m = 0; m < MT8; ++m) {
+      const int i = m * 8 + g;
+      if (i < mm) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = colb + e;
+          if (col < nn) {
+            double2 v = make_double2(sg * acc[2 * m + e].x, sg * acc[2 * m + e].y);
+            if (T.oI >= 0) {
+              const double2 z = __ldcg(a.I + T.oI + (int64_t)(i0 + i) * T.sIi + (int64_t)(c0 + col) * T.sIc);
+              v.x += z.x;
+              v.y += z.y;
+            }
+            __stcg(a.O + T.oO + (int64_t)(i0 + i) * T.sOi + (int64_t)(c0 + col) * T.sOc, v);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) red_release(done + T.unit0 + w.nt, 1);
+  }
+}
+
 // Narrow tile (small nrhs): 64 rows x 8 columns; thread t owns row t % 64 and
 // columns 2 (t / 64) + {0, 1}. The operator panel is streamed through the same
 // cp.async ring (HBM-bound regime), B values are warp broadcasts.
@@ -460,6 +574,14 @@ flow_kernel(const FlowArgs a) {
       }
     }
     __syncthreads();
+    if (!a.narrow && a.mma) {
+      switch ((mm + 7) / 8) {
+        case 1: item_body_dmma<1>(a, w, T, kt, As0, Bs0, tid, lane, warp, &s_last, tr); break;
+        case 2: item_body_dmma<2>(a, w, T, kt, As0, Bs0, tid, lane, warp, &s_last, tr); break;
+        case 3: item_body_dmma<3>(a, w, T, kt, As0, Bs0, tid, lane, warp, &s_last, tr); break;
+        default: item_body_dmma<4>(a, w, T, kt, As0, Bs0, tid, lane, warp, &s_last, tr); break;
+      }
+    } else
     switch (RM) {
       case 0: item_body_narrow(a, w, T, kt, As0, Bs0, tid, &s_last, tr); break;
 #define PS_RM_CASE(R) \
