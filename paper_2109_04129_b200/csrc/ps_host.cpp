@@ -795,13 +795,26 @@ void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
   std::vector<int32_t> ftask(nl, -1), btask(nl, -1);
   // narrow levels (the separator chains) get small split-K chunks so each hop
   // waits on ~1-4 k-steps; wide levels keep large chunks (less overhead)
-  // (narrow tiles stream the operator: always small chunks for parallel streams)
-  auto steps_for = [narrow](size_t width) {
+  // split-K chunk size per elimination level: aim at ~2 work items per
+  // resident CTA for the level's total k-steps (clamped to [4, 32] steps), so
+  // thin chain levels get short chunks (short hops) and heavy levels long ones
+  // (less per-item overhead). Narrow tiles stream the operator: short chunks.
+  const int resident = flow_resident_ctas();
+  auto steps_for = [&](const std::vector<int32_t>& lev_nodes, bool fwd) {
     if (narrow) return 4;
-    return width <= 4 ? 4 : (width <= 16 ? 8 : 16);
+    double ks = 0;
+    const int MTw = GM_MT, NTw = GM_NT;
+    for (int32_t p : lev_nodes) {
+      double K = 0;
+      if (fwd) { for (auto [d, idx] : h->gath[p]) K += h->nsz[d]; }
+      else K = (double)h->S[p];
+      ks += std::ceil((double)h->nsz[p] / MTw) * std::ceil((double)R / NTw) * std::ceil(K / GM_KC);
+    }
+    const int st = (int)std::ceil(ks / (2.0 * resident));
+    return std::max(4, std::min(32, st));
   };
   for (int lev = 0; lev <= h->max_height; ++lev) {
-    const int stp = steps_for(byh[lev].size());
+    const int stp = steps_for(byh[lev], true);
     for (int32_t q : byh[lev]) {
       if (h->gath[q].empty()) continue;
       const int64_t nq = h->nsz[q];
@@ -825,7 +838,7 @@ void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
   sp.fwd.close_batch();
   // backward sweep (Eq. 26), ordered by depth: w_p = v_p + sum_j alpha_pj w_j
   for (int lev = 0; lev <= h->max_depth; ++lev) {
-    const int stp = steps_for(byd[lev].size());
+    const int stp = steps_for(byd[lev], false);
     for (int32_t p : byd[lev]) {
       const int64_t np_ = h->nsz[p];
       int32_t t = sp.bwd.add_task(h->eoff[p] * R, R, 1, h->eoff[p] * R, R, 1, (int)np_, (int)R, +1);
