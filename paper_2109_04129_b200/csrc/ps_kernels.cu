@@ -237,6 +237,18 @@ __device__ __forceinline__ bool splitk_combine(const FlowArgs& a, const GWork& w
   return false;
 }
 
+// Critical chunk: wait until the tile's non-critical group sum is published
+// (top counter == nsub + 1). Never waits on a later ticket.
+__device__ __forceinline__ void wait_group_sum(const FlowArgs& a, const GWork& w, int tid) {
+  const int G = w.nchunks - 1;
+  const int nsub = (G + SUBG - 1) / SUBG;
+  const int32_t* ctr = a.counters + 1 + a.n_units + w.tile;
+  if (tid == 0)
+    while (ld_acquire(ctr) < nsub + 1) __nanosleep(32);
+  __syncthreads();
+}
+
+
 // Everything of one work item, for a compile-time rows-per-warp RM (so the
 // FMA stream is branch-free). A operands (operator panels: immutable in the
 // launch) of the first stages are requested before waiting for the producers
@@ -258,6 +270,31 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
   for (int s = 0; s < NSTAGE - 1; ++s)
     if (s < nsteps) issue_a<GM_MT, GM_NT>(kt, s * KC, klen, i0, mm, a_km, a.A, tid, As0 + s * STAGE_A);
   cp_commit();
+  // ---- accumulator start values that do not depend on the producers of B,
+  // fetched before the wait: the chunk owning the init rows starts from
+  // sign * I (rows no other task of the launch writes), and the critical chunk
+  // adds the published group sum G of the other chunks (never a later ticket)
+  const double sgn = (double)T.sign;
+  const bool crit_fin = (w.nchunks > 1 && w.crit >= 0 && w.chunk == w.crit);
+  const bool owns_init = (w.nchunks == 1) || (w.crit >= 0 ? w.chunk == w.crit : w.chunk == 0);
+  double2 acc[RM];
+#pragma unroll
+  for (int r = 0; r < RM; ++r) acc[r] = make_double2(0.0, 0.0);
+  if (crit_fin) {
+    wait_group_sum(a, w, tid);
+    const double2* Gs = a.partial + (w.slot + w.crit) * (int64_t)(GM_MT * GM_NT);
+#pragma unroll
+    for (int r = 0; r < RM; ++r) acc[r] = __ldcg(Gs + (rbase + r) * GM_NT + col);
+  }
+  if (owns_init && T.oI >= 0 && col < nn) {
+#pragma unroll
+    for (int r = 0; r < RM; ++r)
+      if (rbase + r < mm) {
+        const double2 z = __ldcg(a.I + T.oI + (int64_t)(i0 + rbase + r) * T.sIi + (int64_t)(c0 + col) * T.sIc);
+        acc[r].x += sgn * z.x;
+        acc[r].y += sgn * z.y;
+      }
+  }
   // ---- wait for the producers of B (warp 0, one segment per lane) ----
   if (tid < 32) {
     for (int t = w.ta + tid; t < w.tb; t += 32) {
@@ -277,9 +314,7 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
     if (s < nsteps) issue_b<GM_MT, GM_NT>(kt, s * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + s * STAGE_B);
     cp_commit();
   }
-  double2 acc[RM];
-#pragma unroll
-  for (int r = 0; r < RM; ++r) acc[r] = make_double2(0.0, 0.0);
+
   for (int s = 0; s < nsteps; ++s) {
     cp_wait<NSTAGE - 2>();
     __syncthreads();
@@ -312,20 +347,14 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
     off[r] = (rbase + r) * GM_NT + col;
     own[r] = true;
   }
-  const bool finalize = splitk_combine<RM>(a, w, acc, off, own, tid, s_last);
+  const bool finalize = crit_fin ? true : splitk_combine<RM>(a, w, acc, off, own, tid, s_last);
   if (finalize) {
-    const double sg = (double)T.sign;
     if (col < nn) {
 #pragma unroll
       for (int r = 0; r < RM; ++r) {
         const int i = rbase + r;
         if (i < mm) {
-          double2 v = make_double2(sg * acc[r].x, sg * acc[r].y);
-          if (T.oI >= 0) {
-            const double2 z = __ldcg(a.I + T.oI + (int64_t)(i0 + i) * T.sIi + (int64_t)(c0 + col) * T.sIc);
-            v.x += z.x;
-            v.y += z.y;
-          }
+          const double2 v = make_double2(sgn * acc[r].x, sgn * acc[r].y);   // O = I + sign * sum
           __stcg(a.O + T.oO + (int64_t)(i0 + i) * T.sOi + (int64_t)(c0 + col) * T.sOc, v);
         }
       }
@@ -334,6 +363,7 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
     if (tid == 0) red_release(done + T.unit0 + w.nt, 1);
   }
 }
+
 
 // FP64 tensor-core MMA: D(8x8) += A(8x4, row) * B(4x8, col); per lane
 // A[g][q], B[q][g], C[g][2q], C[g][2q+1] with g = lane / 4, q = lane % 4.
@@ -466,6 +496,25 @@ __device__ __forceinline__ void item_body_narrow(const FlowArgs& a, const GWork&
   for (int s = 0; s < NSTAGE - 1; ++s)
     if (s < nsteps) issue_a<GN_MT, GN_NT>(kt, s * KC, klen, i0, mm, a_km, a.A, tid, As0 + s * STAGE_A);
   cp_commit();
+  const double sgn = (double)T.sign;
+  const bool crit_fin = (w.nchunks > 1 && w.crit >= 0 && w.chunk == w.crit);
+  const bool owns_init = (w.nchunks == 1) || (w.crit >= 0 ? w.chunk == w.crit : w.chunk == 0);
+  double2 acc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+  if (crit_fin) {
+    wait_group_sum(a, w, tid);
+    const double2* Gs = a.partial + (w.slot + w.crit) * (int64_t)(GM_MT * GM_NT);
+    acc[0] = __ldcg(Gs + row * GN_NT + cb);
+    acc[1] = __ldcg(Gs + row * GN_NT + cb + 1);
+  }
+  if (owns_init && T.oI >= 0 && row < mm) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+      if (cb + e < nn) {
+        const double2 z = __ldcg(a.I + T.oI + (int64_t)(i0 + row) * T.sIi + (int64_t)(c0 + cb + e) * T.sIc);
+        acc[e].x += sgn * z.x;
+        acc[e].y += sgn * z.y;
+      }
+  }
   if (tid < 32) {
     for (int t = w.ta + tid; t < w.tb; t += 32) {
       const int dep = a.terms[t].dep;
@@ -483,7 +532,6 @@ __device__ __forceinline__ void item_body_narrow(const FlowArgs& a, const GWork&
     if (s < nsteps) issue_b<GN_MT, GN_NT>(kt, s * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + s * STAGE_B);
     cp_commit();
   }
-  double2 acc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
   const bool live = (row < mm) && (cb < nn);
   for (int s = 0; s < nsteps; ++s) {
     cp_wait<NSTAGE - 2>();
@@ -512,20 +560,14 @@ __device__ __forceinline__ void item_body_narrow(const FlowArgs& a, const GWork&
   if (tr) tr[4] = gtimer();
   int off[2] = {row * GN_NT + cb, row * GN_NT + cb + 1};
   bool own[2] = {true, true};
-  const bool finalize = splitk_combine<2>(a, w, acc, off, own, tid, s_last);
+  const bool finalize = crit_fin ? true : splitk_combine<2>(a, w, acc, off, own, tid, s_last);
   if (finalize) {
-    const double sg = (double)T.sign;
     if (row < mm) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int col = cb + e;
         if (col < nn) {
-          double2 v = make_double2(sg * acc[e].x, sg * acc[e].y);
-          if (T.oI >= 0) {
-            const double2 z = __ldcg(a.I + T.oI + (int64_t)(i0 + row) * T.sIi + (int64_t)(c0 + col) * T.sIc);
-            v.x += z.x;
-            v.y += z.y;
-          }
+          const double2 v = make_double2(sgn * acc[e].x, sgn * acc[e].y);   // O = I + sign * sum
           __stcg(a.O + T.oO + (int64_t)(i0 + row) * T.sOi + (int64_t)(c0 + col) * T.sOc, v);
         }
       }
