@@ -207,3 +207,14 @@ def test_solve_c3_plane_waves(cfgdata):
     B, _ = read_rhs(meta["rhs"])
     _solve_check(meta["hm"], np.asfortranarray(B[:, :181]), check_host=False)
     _solve_check(meta["hm"], np.asfortranarray(B[:, :1]), check_host=True)     # the 1-RHS run
+
+
+@pytest.mark.slow
+def test_solve_c4_plane_waves(cfgdata):
+    """BASELINE config 3 (closed cylinder, N=83160, 5106 leaves, elimination
+    tree height 277): both polarisations, a few monostatic angles, plus R^T/R/Z_F."""
+    meta = cfgdata("C4")
+    B, _ = read_rhs(meta["rhs"])
+    cols = [0, 90, 180, 270]                 # theta-pol and phi-pol incidences
+    _solve_check(meta["hm"], np.asfortranarray(B[:, cols]), check_host=False)
+    _ops_check(meta["hm"], nrhs=2)
