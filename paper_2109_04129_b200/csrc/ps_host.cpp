@@ -228,6 +228,15 @@ struct Table {
   // isolate = +1 / -1 puts the first / last segment (the dependency expected to
   // complete last: the parent in the backward sweep, the last child in the
   // forward sweep) in a chunk of its own, so a chain hop waits on a short chunk.
+  // Work items of a task: every (mt, nt) tile, its virtual K split into chunks
+  // of ~steps k-steps (split-K); also assigns the task's completion units.
+  // isolate = +1 / -1: the first / last segment (the dependency expected to
+  // complete last: the parent in the backward sweep, the last child in the
+  // forward sweep) becomes the critical chunk (queued last, adds the sum of
+  // the others); the NEAR - 1 segments next to it (the next-latest
+  // dependencies) become single-segment chunks in subgroups of their own, the
+  // bulk is chunked normally and combined in subgroups of SUBG.
+  static constexpr int NEAR = 4, SUBG = 16;
   void tile(int32_t task, int isolate = 0, int steps = 0) {
     if (steps <= 0) steps = chunk_steps;
     GTask& t = tasks[task];
@@ -236,38 +245,68 @@ struct Table {
     t.unit0 = n_units;
     n_units += nnt;
     std::vector<std::array<int32_t, 4>> ch;   // (ka, kb, ta, tb)
+    std::vector<char> single;                 // chunk forms its own subgroup
+    auto add = [&](int32_t s0, int32_t s1, bool one) {
+      const size_t before = ch.size();
+      chunk_range(s0, s1, ch, steps);
+      single.resize(ch.size(), one ? 1 : 0);
+      (void)before;
+    };
     const int nseg = t.t1 - t.t0;
+    int32_t crit = -1;
     if (isolate != 0 && nseg >= 2) {
+      const int nnear = std::min(NEAR - 1, nseg - 1);
       if (isolate > 0) {
-        chunk_range(t.t0, t.t0 + 1, ch, steps);
-        chunk_range(t.t0 + 1, t.t1, ch, steps);
+        add(t.t0, t.t0 + 1, true);                                   // critical
+        for (int q = 1; q <= nnear; ++q) add(t.t0 + q, t.t0 + q + 1, true);
+        add(t.t0 + 1 + nnear, t.t1, false);
+        crit = 0;
       } else {
-        chunk_range(t.t0, t.t1 - 1, ch, steps);
-        chunk_range(t.t1 - 1, t.t1, ch, steps);
+        add(t.t0, t.t1 - 1 - nnear, false);
+        for (int q = nnear; q >= 1; --q) add(t.t1 - 1 - q, t.t1 - q, true);
+        add(t.t1 - 1, t.t1, true);                                   // critical
+        crit = (int32_t)ch.size() - 1;
       }
     } else {
-      chunk_range(t.t0, t.t1, ch, steps);
+      add(t.t0, t.t1, false);
     }
-    if (ch.empty()) ch.push_back({0, 0, t.t0, t.t0});
+    if (ch.empty()) {
+      ch.push_back({0, 0, t.t0, t.t0});
+      single.push_back(0);
+    }
     const int nch = (int)ch.size();
-    // critical chunk = the isolated one (queued last); -1: plain last-arriver combine
-    int32_t crit = -1;
-    if (isolate != 0 && nseg >= 2 && nch >= 2) crit = isolate > 0 ? 0 : nch - 1;
+    if (nch < 2) crit = -1;
+    // subgroups over the non-critical chunks in rank order
+    std::vector<int32_t> rank_chunk;
+    for (int c = 0; c < nch; ++c)
+      if (c != crit) rank_chunk.push_back(c);
+    const int G = (int)rank_chunk.size();
+    std::vector<int32_t> sub_of(nch, -1), sub_r0, sub_r1;
+    for (int r = 0; r < G;) {
+      int r1 = r + 1;
+      if (!single[rank_chunk[r]])
+        while (r1 < G && r1 - r < SUBG && !single[rank_chunk[r1]]) ++r1;
+      for (int q = r; q < r1; ++q) sub_of[rank_chunk[q]] = (int32_t)sub_r0.size();
+      sub_r0.push_back(r);
+      sub_r1.push_back(r1);
+      r = r1;
+    }
+    const int nsub = (int)sub_r0.size();
     for (int a = 0; a < nmt; ++a)
       for (int b = 0; b < nnt; ++b) {
         // split-K tiles: counters [top, subgroups...], slots [chunks..., subgroup sums...]
-        const int G = (crit >= 0) ? nch - 1 : nch;
-        const int nsub = (G + 15) / 16;       // SUBG in ps_kernels.cu
         const int32_t tile_id = n_tiles;
         if (nch > 1) n_tiles += 1 + nsub;
         const int64_t slot = nch > 1 ? n_slots : 0;
         if (nch > 1) n_slots += nch + nsub;
+        auto push = [&](int c) {
+          const int sg = sub_of[c];
+          work.push_back({task, a, b, ch[c][2], ch[c][3], ch[c][0], ch[c][1], c, nch, tile_id, crit,
+                          sg, sg >= 0 ? sub_r0[sg] : 0, sg >= 0 ? sub_r1[sg] : 0, nsub, 0, slot});
+        };
         for (int c = 0; c < nch; ++c)
-          if (c != crit)
-            work.push_back({task, a, b, ch[c][2], ch[c][3], ch[c][0], ch[c][1], c, nch, tile_id, crit, 0, slot});
-        if (crit >= 0)
-          work.push_back({task, a, b, ch[crit][2], ch[crit][3], ch[crit][0], ch[crit][1], crit, nch, tile_id,
-                          crit, 0, slot});
+          if (c != crit) push(c);
+        if (crit >= 0) push(crit);
       }
   }
   void close_batch() {

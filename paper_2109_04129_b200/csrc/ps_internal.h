@@ -43,10 +43,12 @@ struct GTerm {
 // them up in chunk order — deterministic.
 struct GWork {
   int32_t task, mt, nt, ta, tb, ka, kb, chunk, nchunks, tile;
-  int32_t crit;            // split-K combine: -1 = last arriver sums all partials in chunk
-                           // order; else the chunk that carries the latest dependency: the
-                           // other chunks' last arriver sums them (chunk order) into slot
-                           // `crit`, and chunk `crit` (queued last) adds that one sum
+  int32_t crit;            // split-K combine: -1 = the tree root finalises; else the chunk that
+                           // carries the latest dependency (queued last): it adds the published
+                           // sum of all other chunks
+  int32_t sub;             // combine subgroup of this chunk: members are the non-critical chunks
+  int32_t sub_r0, sub_r1;  // of rank [sub_r0, sub_r1) (rank = chunk index skipping crit)
+  int32_t nsub;            // number of subgroups of the tile
   int32_t pad;
   int64_t slot;
 };

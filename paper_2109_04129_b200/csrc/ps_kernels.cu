@@ -144,7 +144,7 @@ constexpr size_t FLOW_SMEM = (size_t)NSTAGE * (STAGE_A + STAGE_B) * sizeof(doubl
 // Split-K combine of one output tile, fixed summation order (deterministic).
 // Each thread owns E tile elements at tile offsets off[e] with partial sums
 // acc[e]. Non-critical chunks (all chunks except `crit`) are summed by a fixed
-// two-level tree: subgroups of SUBG consecutive chunks (by rank), the last
+// two-level tree: subgroups of consecutive chunks (by rank; host-chosen), the last
 // arriver of a subgroup sums its members in rank order, the last subgroup sums
 // the subgroup sums in order. Counters of the tile: arrive[tile] (top) and
 // arrive[tile + 1 + sg]. Slots: [slot, slot + nchunks) chunk partials,
@@ -152,7 +152,7 @@ constexpr size_t FLOW_SMEM = (size_t)NSTAGE * (STAGE_A + STAGE_B) * sizeof(doubl
 // crit >= 0: the critical chunk (queued last) waits for top == nsub + 1 and
 // adds the group sum (p_0 + G, or G + p_last); crit < 0: the tree root finalises.
 // Returns true when the caller must finalise with acc.
-constexpr int SUBG = 16;
+
 
 template <int E>
 __device__ __forceinline__ bool splitk_combine(const FlowArgs& a, const GWork& w, double2 (&acc)[E],
@@ -162,8 +162,7 @@ __device__ __forceinline__ bool splitk_combine(const FlowArgs& a, const GWork& w
   const int64_t TS = (int64_t)(GM_MT * GM_NT);
   int32_t* ctr = a.counters + 1 + a.n_units + w.tile;
   const bool crit_mode = w.crit >= 0;
-  const int G = crit_mode ? w.nchunks - 1 : w.nchunks;       // non-critical chunks
-  const int nsub = (G + SUBG - 1) / SUBG;
+  const int nsub = w.nsub;
   if (crit_mode && w.chunk == w.crit) {
     if (tid == 0)
       while (ld_acquire(ctr) < nsub + 1) __nanosleep(32);
@@ -179,9 +178,8 @@ __device__ __forceinline__ bool splitk_combine(const FlowArgs& a, const GWork& w
     return true;
   }
   auto chunk_of_rank = [&](int r) { return (crit_mode && r >= w.crit) ? r + 1 : r; };
-  const int rank = (crit_mode && w.chunk > w.crit) ? w.chunk - 1 : w.chunk;
-  const int sg = rank / SUBG;
-  const int r0 = sg * SUBG, r1 = min(G, r0 + SUBG);
+  const int sg = w.sub;
+  const int r0 = w.sub_r0, r1 = w.sub_r1;
   double2* P = a.partial + (w.slot + w.chunk) * TS;
 #pragma unroll
   for (int e = 0; e < E; ++e)
@@ -240,8 +238,7 @@ __device__ __forceinline__ bool splitk_combine(const FlowArgs& a, const GWork& w
 // Critical chunk: wait until the tile's non-critical group sum is published
 // (top counter == nsub + 1). Never waits on a later ticket.
 __device__ __forceinline__ void wait_group_sum(const FlowArgs& a, const GWork& w, int tid) {
-  const int G = w.nchunks - 1;
-  const int nsub = (G + SUBG - 1) / SUBG;
+  const int nsub = w.nsub;
   const int32_t* ctr = a.counters + 1 + a.n_units + w.tile;
   if (tid == 0)
     while (ld_acquire(ctr) < nsub + 1) __nanosleep(32);
