@@ -585,19 +585,28 @@ flow_kernel(const FlowArgs a) {
   double2* Bs0 = As0 + NSTAGE * STAGE_A;
   KTab& kt = *reinterpret_cast<KTab*>(Bs0 + NSTAGE * STAGE_B);
   __shared__ int s_item, s_last;
+  __shared__ GWork s_w;
+  __shared__ GTask s_T;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int wm = warp % GM_WM, wn = warp / GM_WM;
   int32_t* ticket = a.counters;
   for (;;) {
-    if (tid == 0) s_item = atomicAdd(ticket, 1);
+    if (tid == 0) {
+      const int it = atomicAdd(ticket, 1);
+      s_item = it;
+      if (it < a.nwork) {
+        s_w = a.work[it];
+        s_T = a.tasks[s_w.task];
+      }
+    }
     __syncthreads();
     const int64_t item = s_item;
     if (item >= a.nwork) return;
     int64_t* tr = (a.trace != nullptr && tid == 0) ? a.trace + 6 * item : nullptr;
     if (tr) { tr[0] = item; tr[1] = smid(); tr[2] = gtimer(); }
-    const GWork w = a.work[item];
-    const GTask T = a.tasks[w.task];
+    const GWork& w = s_w;       // shared: one copy per CTA, not per-thread registers
+    const GTask& T = s_T;
     const int mm = min(GM_MT, T.m - w.mt * GM_MT);
     const int RM = a.narrow ? 0 : (mm + GM_WM - 1) / GM_WM;
     // ---- k tables of this item (segments [ta, tb) clipped to [ka, kb)) ----
