@@ -181,9 +181,10 @@ ps_status ps_profile(ps_handle* h, int enable);
 
 /* ps_profile_read — accumulated since ps_profile(h,1): for each kernel class
  * c in {0 forward sweep, 1 backward sweep, 2 D^{-1}, 3 far stage 1,
- * 4 far stage 2, 5 permutations/combine} four values out[4c..4c+3] =
+ * 4 far stage 2, 5 permutations/combine/norms, 6 the whole-solve dataflow
+ * program (default ps_solve path)} four values out[4c..4c+3] =
  * (device ms, launches, algorithmic flops, algorithmic operator bytes).
- * Classes 0-4 are all the gather-GEMM kernel. Returns values written. */
+ * Classes 0-4 and 6 are all the gather-GEMM kernel. Returns values written. */
 int ps_profile_read(const ps_handle* h, double* out, int n);
 
 /* ps_trace / ps_trace_read — debug instrumentation of the persistent dataflow

@@ -209,7 +209,7 @@ class PsHandle:
             raise PsError(PS_EINVAL, "ps_get_dinv failed")
         return buf[:n * n].reshape(n, n, order="F")
 
-    PROFILE_CLASSES = ["fwd_sweep", "bwd_sweep", "dinv", "far_stage1", "far_stage2", "aux"]
+    PROFILE_CLASSES = ["fwd_sweep", "bwd_sweep", "dinv", "far_stage1", "far_stage2", "aux", "solve_program"]
 
     def profile(self, enable: bool = True):
         self._check(load_library().ps_profile(self._h, 1 if enable else 0))

@@ -97,7 +97,7 @@ uint64_t checksum64(const uint8_t* b, size_t nbytes) {
 // Optional per-launch CUDA-event profiling (ps_profile): events are recorded on
 // the launching stream around every kernel; elapsed times are accumulated per
 // kernel class after the solve's final synchronisation.
-enum { PC_FWD = 0, PC_BWD, PC_DINV, PC_FAR1, PC_FAR2, PC_AUX, PC_COUNT };
+enum { PC_FWD = 0, PC_BWD, PC_DINV, PC_FAR1, PC_FAR2, PC_AUX, PC_PROG, PC_COUNT };
 struct Prof {
   bool on = false;
   // debug trace of the LAST profiled flow launch of class trace_cls
@@ -163,6 +163,19 @@ struct Table {
   int64_t n_slots = 0;
   int chunk_steps = CHUNK_STEPS;
   int narrow = 0;          // 1: 64 x 8 tiles (small nrhs)
+  // optional global ordering of work items (ticket order): key = key_base + nt * key_stagger,
+  // stable-sorted by sort_by_key() (valid when every dependency has a smaller key)
+  double key_base = 0, key_stagger = 0;
+  std::vector<double> keys;
+  void sort_by_key() {
+    std::vector<int64_t> idx(work.size());
+    std::iota(idx.begin(), idx.end(), 0);
+    std::stable_sort(idx.begin(), idx.end(), [&](int64_t x, int64_t y) { return keys[x] < keys[y]; });
+    std::vector<GWork> w2(work.size());
+    for (size_t i = 0; i < idx.size(); ++i) w2[i] = work[idx[i]];
+    work.swap(w2);
+    keys.clear();
+  }
   int MT() const { return narrow ? GN_MT : GM_MT; }
   int NT() const { return narrow ? GN_NT : GM_NT; }
 
@@ -175,7 +188,7 @@ struct Table {
     t.t0 = t.t1 = (int32_t)terms.size();
     t.K = 0;
     t.unit0 = 0; t.n_mt = (m + GM_MT - 1) / GM_MT;
-    t.a_kmajor = 0; t.b_kmajor = 0; t.pad = 0;
+    t.a_kmajor = 0; t.b_kmajor = 0; t.idep = -1;
     tasks.push_back(t);
     return (int32_t)tasks.size() - 1;
   }
@@ -303,6 +316,7 @@ struct Table {
           const int sg = sub_of[c];
           work.push_back({task, a, b, ch[c][2], ch[c][3], ch[c][0], ch[c][1], c, nch, tile_id, crit,
                           sg, sg >= 0 ? sub_r0[sg] : 0, sg >= 0 ? sub_r1[sg] : 0, nsub, 0, slot});
+          keys.push_back(key_base + b * key_stagger);
         };
         for (int c = 0; c < nch; ++c)
           if (c != crit) push(c);
@@ -378,7 +392,10 @@ struct Table {
 // Per-nrhs solve plan: tables + workspaces.
 struct SolvePlan {
   int64_t nrhs = 0;
-  Table fwd, bwd, dinv, far1, far2;
+  Table fwd, bwd, dinv, far1, far2;        // per-operator tables (ps_apply, PS_SOLVE=stages)
+  Table prog;                              // the whole two-term solve as one dataflow program
+  DevBuf<double2> ws;                      // program workspace: Y BO W Z XT X TMP (offsets below)
+  int64_t oY = 0, oBO = 0, oW = 0, oZ = 0, oXT = 0, oX = 0, oTMP = 0;
   DevBuf<double2> y, bo, w, u, xt, wm, tm, part, norms, stage;
   int64_t nchunks = 0, rpc = 64;
   int64_t launches_per_solve = 0;
@@ -419,7 +436,10 @@ struct ps_handle {
   // near block lookup: (leaf a, leaf b) -> index into near_list
   std::unordered_map<uint64_t, int64_t> near_idx;
   // ---- device ----
-  DevBuf<double2> d_near, d_far, d_W, d_P, d_D;
+  // operator arena: [ alpha panels P (Plen) | D^-1 (Dlen) | far stacks + dense far blocks ]
+  DevBuf<double2> d_near, d_W, d_op;
+  struct RawBuf { double2* p = nullptr; } d_P, d_D, d_far;   // views into d_op
+  int64_t Pbase = 0, Dbase = 0, Fbase = 0;
   DevBuf<int64_t> d_e2rwg, d_e2mort, d_m2e;
   bool setup_done = false;
   double ratio_threshold = 0.1;
@@ -959,11 +979,196 @@ void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
   CK(cudaStreamSynchronize(h->stream));
 }
 
+
+// ------------------------------------------------------------------ solve program
+// The whole two-term solve (Eqs. 24, 32, 26, 31, 36, 26) as ONE task
+// table for one persistent launch. Stages and their dependencies (per column
+// tile nt; B = segment producers, I = init producer):
+//   S1 fwd    y_q  = y_q + sum_d a_dq^T y_d              B: S1(d)
+//   S2 dinv   bo_p = D_p^-1 y_p                          B: S1(p)
+//   S3 bwd    w_p  = bo_p + sum_j a_pj w_j               I: S2(p)  B: S3(j)
+//   S4 far1   tmp_c = S_c w[c]  (per cluster, rows gathered per leaf)   B: S3
+//   S5 far2   z_l  = sum U tmp + V tmp + dense D w       B: S4 / S3
+//   S6 fwd    z_q  = z_q + sum_d a_dq^T z_d              I: S5(q)  B: S6(d) or S5(d)
+//   S7 dinv   xt_p = bo_p - D_p^-1 z_p                   I: S2(p)  B: S6(p) or S5(p)
+//   S8 bwd    x_p  = xt_p + sum_j a_pj x_j               I: S7(p)  B: S8(j)
+// Work items are ordered by (stage, level) + nt * stagger: every dependency has
+// a smaller key (deadlock-free ticket order), and the column tiles enter the
+// pipeline staggered, so one tile's thin elimination-chain phase overlaps
+// another tile's bulk work. Vectors live in one workspace arena, operators in
+// one operator arena, so a single set of base pointers serves every task.
+void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
+  const int64_t nl = h->nl;
+  Table& P = sp.prog;
+  P.narrow = (R <= 8) ? 1 : 0;
+  if (P.narrow) P.chunk_steps = 4;
+  const int64_t NR = h->N * R;
+  sp.oY = 0; sp.oBO = NR; sp.oW = 2 * NR; sp.oZ = 3 * NR; sp.oXT = 4 * NR; sp.oX = 5 * NR; sp.oTMP = 6 * NR;
+  const int64_t ncl = (int64_t)h->cl_start.size();
+  std::vector<int64_t> toff(ncl);
+  int64_t Ttot = 0;
+  for (int64_t c = 0; c < ncl; ++c) { toff[c] = sp.oTMP + Ttot; Ttot += h->cl_sr[c] * R; }
+  std::vector<std::vector<int32_t>> byh(h->max_height + 1), byd(h->max_depth + 1);
+  for (int64_t p = 0; p < nl; ++p) {
+    byh[h->height[p]].push_back((int32_t)p);
+    byd[h->depth[p]].push_back((int32_t)p);
+  }
+  const int resident = flow_resident_ctas();
+  auto steps_for = [&](const std::vector<int32_t>& nodes, bool fwd) {
+    if (P.narrow) return 4;
+    double ks = 0;
+    for (int32_t p : nodes) {
+      double K = 0;
+      if (fwd) { for (auto [d, idx] : h->gath[p]) K += h->nsz[d]; }
+      else K = (double)h->S[p];
+      ks += std::ceil((double)h->nsz[p] / GM_MT) * std::ceil((double)R / GM_NT) * std::ceil(K / GM_KC);
+    }
+    return std::max(4, std::min(32, (int)std::ceil(ks / (2.0 * resident))));
+  };
+  const int nnt = (int)((R + P.NT() - 1) / P.NT());
+  const double Ltot = 2.0 * (h->max_height + 1) + 2.0 * (h->max_depth + 1) + 4.0;
+  P.key_stagger = nnt > 1 ? Ltot / nnt : 0.0;
+  double lev = 0;
+  const int64_t Fb = h->Fbase, Pb = h->Pbase, Db = h->Dbase;
+  auto leaf_of_pos = [&](int64_t m) {
+    return (int64_t)(std::upper_bound(h->leaf_off.begin(), h->leaf_off.end(), m) - h->leaf_off.begin()) - 1;
+  };
+  std::vector<int32_t> s1(nl, -1), s2(nl, -1), s3(nl, -1), s4(ncl, -1), s5(nl, -1), s6(nl, -1), s7(nl, -1),
+      s8(nl, -1);
+  // forward sweep over buffer `buf` (in place), producers of the init / of untouched rows given
+  auto fwd_stage = [&](int64_t buf, std::vector<int32_t>& out, const std::vector<int32_t>* init_dep) {
+    for (int L = 0; L <= h->max_height; ++L) {
+      P.key_base = lev++;
+      const int stp = steps_for(byh[L], true);
+      for (int32_t q : byh[L]) {
+        if (h->gath[q].empty()) continue;
+        const int64_t nq = h->nsz[q];
+        int32_t t = P.add_task(buf + h->eoff[q] * R, R, 1, buf + h->eoff[q] * R, R, 1, (int)nq, (int)R, +1);
+        if (init_dep) P.tasks[t].idep = (*init_dep)[q];
+        auto gl = h->gath[q];
+        std::stable_sort(gl.begin(), gl.end(), [&](const std::pair<int32_t, int32_t>& x,
+                                                   const std::pair<int32_t, int32_t>& y) {
+          return h->height[x.first] < h->height[y.first];
+        });
+        for (auto [d, idx] : gl) {
+          const int64_t nd = h->nsz[d];
+          const int32_t dep = out[d] >= 0 ? out[d] : (init_dep ? (*init_dep)[d] : -1);
+          P.add_term(t, Pb + h->Poff[d] + h->pcol[d][idx] * nd, nd, 1, buf + h->eoff[d] * R, R, 1, (int)nd, dep);
+        }
+        P.tile(t, -1, stp);
+        out[q] = t;
+      }
+    }
+  };
+  auto dinv_stage = [&](int64_t src, int64_t dst, int64_t init, int sign, std::vector<int32_t>& out,
+                        const std::vector<int32_t>& src_dep, const std::vector<int32_t>* init_dep) {
+    P.key_base = lev++;
+    for (int64_t p = 0; p < nl; ++p) {
+      const int64_t np_ = h->nsz[p];
+      int32_t t = P.add_task(dst + h->eoff[p] * R, R, 1, init >= 0 ? init + h->eoff[p] * R : -1, R, 1,
+                             (int)np_, (int)R, sign);
+      if (init_dep) P.tasks[t].idep = (*init_dep)[p];
+      P.add_term(t, Db + h->Doff[p], 1, np_, src + h->eoff[p] * R, R, 1, (int)np_, src_dep[p]);
+      P.tile(t);
+      out[p] = t;
+    }
+  };
+  auto bwd_stage = [&](int64_t init, int64_t out_buf, std::vector<int32_t>& out,
+                       const std::vector<int32_t>& init_dep) {
+    for (int L = 0; L <= h->max_depth; ++L) {
+      P.key_base = lev++;
+      const int stp = steps_for(byd[L], false);
+      for (int32_t p : byd[L]) {
+        const int64_t np_ = h->nsz[p];
+        int32_t t = P.add_task(out_buf + h->eoff[p] * R, R, 1, init + h->eoff[p] * R, R, 1, (int)np_, (int)R, +1);
+        P.tasks[t].idep = init_dep[p];
+        for (size_t i = 0; i < h->st[p].size(); ++i) {
+          const int32_t j = h->st[p][i];
+          P.add_term(t, Pb + h->Poff[p] + h->pcol[p][i] * np_, 1, np_, out_buf + h->eoff[j] * R, R, 1,
+                     (int)h->nsz[j], out[j]);
+        }
+        P.tile(t, +1, stp);
+        out[p] = t;
+      }
+    }
+  };
+  fwd_stage(sp.oY, s1, nullptr);                                         // S1
+  dinv_stage(sp.oY, sp.oBO, -1, +1, s2, s1, nullptr);                    // S2
+  bwd_stage(sp.oBO, sp.oW, s3, s2);                                      // S3
+  // S4 far stage 1: per cluster, rows gathered per leaf from W (elimination order)
+  P.key_base = lev++;
+  for (int64_t c = 0; c < ncl; ++c) {
+    if (h->cl_sr[c] == 0) continue;
+    const int64_t sr = h->cl_sr[c], a0 = h->cl_start[c], len = h->cl_len[c];
+    int32_t t = P.add_task(toff[c], R, 1, -1, 0, 0, (int)sr, (int)R, +1);
+    for (int64_t l = leaf_of_pos(a0); l < nl && h->leaf_off[l] < a0 + len; ++l) {
+      const int32_t pos = h->pos_of[l];
+      P.add_term(t, Fb + h->cl_soff[c] + (h->leaf_off[l] - a0) * sr, 1, sr, sp.oW + h->eoff[pos] * R, R, 1,
+                 (int)(h->leaf_off[l + 1] - h->leaf_off[l]), s3[pos]);
+    }
+    P.tile(t);
+    s4[c] = t;
+  }
+  // S5 far stage 2: per leaf, written in elimination order into Z
+  P.key_base = lev++;
+  {
+    struct Seg { int64_t oA, sAi, sAk, oB; int K; int32_t dep; };
+    std::vector<std::vector<Seg>> contrib(nl);
+    for (int64_t b = 0; b < h->nfar; ++b) {
+      const int64_t* F = &h->far_list[7 * b];
+      const int64_t r0 = F[0], m = F[1], c0 = F[2], n = F[3], r = F[5];
+      if (r == 0) continue;
+      const int64_t ct = h->fb_ct[b], cs = h->fb_cs[b];
+      if (h->fb_dense[b] >= 0) {
+        const int64_t D = Fb + h->fb_dense[b];
+        // t rows: D w_s, K over the source leaves;  s rows: D^T w_t, K over the target leaves
+        for (int64_t l = leaf_of_pos(r0); l < nl && h->leaf_off[l] < r0 + m; ++l)
+          for (int64_t g = leaf_of_pos(c0); g < nl && h->leaf_off[g] < c0 + n; ++g) {
+            const int32_t pg = h->pos_of[g];
+            contrib[l].push_back({D + (h->leaf_off[l] - r0) + (h->leaf_off[g] - c0) * m, 1, m,
+                                  sp.oW + h->eoff[pg] * R, (int)(h->leaf_off[g + 1] - h->leaf_off[g]), s3[pg]});
+          }
+        for (int64_t l = leaf_of_pos(c0); l < nl && h->leaf_off[l] < c0 + n; ++l)
+          for (int64_t g = leaf_of_pos(r0); g < nl && h->leaf_off[g] < r0 + m; ++g) {
+            const int32_t pg = h->pos_of[g];
+            contrib[l].push_back({D + (h->leaf_off[g] - r0) + (h->leaf_off[l] - c0) * m, m, 1,
+                                  sp.oW + h->eoff[pg] * R, (int)(h->leaf_off[g + 1] - h->leaf_off[g]), s3[pg]});
+          }
+        continue;
+      }
+      for (int64_t l = leaf_of_pos(r0); l < nl && h->leaf_off[l] < r0 + m; ++l)
+        contrib[l].push_back({Fb + h->cl_soff[ct] + h->fb_rbt[b] + (h->leaf_off[l] - r0) * h->cl_sr[ct],
+                              h->cl_sr[ct], 1, toff[cs] + h->fb_rbs[b] * R, (int)r, s4[cs]});
+      for (int64_t l = leaf_of_pos(c0); l < nl && h->leaf_off[l] < c0 + n; ++l)
+        contrib[l].push_back({Fb + h->cl_soff[cs] + h->fb_rbs[b] + (h->leaf_off[l] - c0) * h->cl_sr[cs],
+                              h->cl_sr[cs], 1, toff[ct] + h->fb_rbt[b] * R, (int)r, s4[ct]});
+    }
+    for (int64_t l = 0; l < nl; ++l) {
+      const int32_t pos = h->pos_of[l];
+      const int64_t nlf = h->leaf_off[l + 1] - h->leaf_off[l];
+      int32_t t = P.add_task(sp.oZ + h->eoff[pos] * R, R, 1, -1, 0, 0, (int)nlf, (int)R, +1);
+      for (auto& g : contrib[l]) P.add_term(t, g.oA, g.sAi, g.sAk, g.oB, R, 1, g.K, g.dep);
+      P.tile(t);
+      s5[pos] = t;
+    }
+  }
+  fwd_stage(sp.oZ, s6, &s5);                                             // S6
+  std::vector<int32_t> zfin(nl);
+  for (int64_t p = 0; p < nl; ++p) zfin[p] = s6[p] >= 0 ? s6[p] : s5[p];
+  dinv_stage(sp.oZ, sp.oXT, sp.oBO, -1, s7, zfin, &s2);                  // S7: xt = bo - D^-1 z
+  bwd_stage(sp.oXT, sp.oX, s8, s7);                                      // S8
+  P.sort_by_key();
+  P.close_batch();
+  P.upload(h->stream);
+  sp.ws.alloc(6 * NR + std::max<int64_t>(Ttot, 1));
+}
+
 SolvePlan& get_plan(ps_handle* h, int64_t nrhs) {
   if (!h->plan || h->plan->nrhs != nrhs) {
     h->plan.reset();
     auto sp = std::make_unique<SolvePlan>();
     build_solve_plan(h, *sp, nrhs);
+    build_program(h, *sp, nrhs);
     h->plan = std::move(sp);
   }
   return *h->plan;
@@ -1048,7 +1253,16 @@ ps_status hm_load(const char* path, const ps_dist* dist, ps_handle** out) {
       far_layout(h.get(), far_arena, stacked);
       far_arena.clear();
       far_arena.shrink_to_fit();
-      h->d_far.upload(stacked, h->stream);
+      h->Pbase = 0;
+      h->Dbase = h->Plen;
+      h->Fbase = h->Plen + h->Dlen;
+      h->d_op.alloc(h->Fbase + (int64_t)stacked.size());
+      h->d_P.p = h->d_op.p + h->Pbase;
+      h->d_D.p = h->d_op.p + h->Dbase;
+      h->d_far.p = h->d_op.p + h->Fbase;
+      CK(cudaMemcpyAsync(h->d_far.p, stacked.data(), sizeof(double2) * stacked.size(), cudaMemcpyHostToDevice,
+                         h->stream));
+      CK(cudaStreamSynchronize(h->stream));
     }
     h->d_e2rwg.upload(h->e2rwg, h->stream);
     h->d_e2mort.upload(h->e2mort, h->stream);
@@ -1076,8 +1290,6 @@ ps_status ps_setup(ps_handle* h, const ps_setup_opts* opts) {
     CK(cudaSetDevice(h->device));
     cudaStream_t s = h->stream;
     h->d_W.alloc(std::max<int64_t>(h->Wlen, 1));
-    h->d_P.alloc(std::max<int64_t>(h->Plen, 1));
-    h->d_D.alloc(std::max<int64_t>(h->Dlen, 1));
     SetupPlan sp;
     build_setup_plan(h, sp);
     DevBuf<int32_t> d_status;
@@ -1098,8 +1310,6 @@ ps_status ps_setup(ps_handle* h, const ps_setup_opts* opts) {
         if (status[i]) {
           int32_t p = sp.level_leaves[lev][i];
           h->d_W.release();
-          h->d_P.release();
-          h->d_D.release();
           return fail(h, PS_ESINGULAR,
                       "ps_setup: singular scaled diagonal block at elimination position " +
                           std::to_string(p) + " (leaf " + std::to_string(h->leaf_at[p]) + ")");
@@ -1147,6 +1357,22 @@ ps_status ps_solve(ps_handle* h, int64_t nrhs, const void* B, int64_t ldb, void*
       ldb_d = N;
     }
     CK(cudaEventRecord(h->ev0, s));
+    static const bool stages_env = [] {
+      const char* e = std::getenv("PS_SOLVE");
+      return e && std::string(e) == "stages";
+    }();
+    double2* xres = sp.xt.p;   // where x ends up (elimination order)
+    if (!stages_env) {
+      // the whole solve as one dataflow program (build_program)
+      double2* ws = sp.ws.p;
+      launches += aux(h, s, [&] { launch_permute_in(N, R, h->d_e2rwg.p, Bd, ldb_d, ws + sp.oY, s); });
+      launches += sp.prog.launch_all(ws, ws, h->d_op.p, ws, s, &h->prof, PC_PROG);
+      launches += aux(h, s, [&] {
+        launch_norms2(N, R, ws + sp.oBO, ws + sp.oXT, sp.part.p, sp.rpc, s);
+        launch_finalize_norms(sp.nchunks, R, sp.part.p, sp.norms.p, s);
+      }) + 1;
+      xres = ws + sp.oX;
+    } else {
     launches += aux(h, s, [&] { launch_permute_in(N, R, h->d_e2rwg.p, Bd, ldb_d, sp.y.p, s); });  // RWG -> E
     launches += op_Rt(h, sp, sp.y.p, s);                                // b~ = R^T b     (Eq. 24)
     launches += op_Dinv(h, sp, sp.y.p, sp.bo.p, s);                     // b_o = D^-1 b~  (Eq. 32)
@@ -1159,8 +1385,9 @@ ps_status ps_solve(ps_handle* h, int64_t nrhs, const void* B, int64_t ldb, void*
       launch_finalize_norms(sp.nchunks, R, sp.part.p, sp.norms.p, s);
     }) + 1;
     launches += op_R(h, sp, sp.xt.p, sp.xt.p, s);                       // x = R x~       (Eq. 26)
+    }
     double2* Xd = on_device ? (double2*)X : sp.stage.p;
-    launches += aux(h, s, [&] { launch_permute_out(N, R, h->d_e2rwg.p, sp.xt.p, Xd, on_device ? ldx : N, s); });
+    launches += aux(h, s, [&] { launch_permute_out(N, R, h->d_e2rwg.p, xres, Xd, on_device ? ldx : N, s); });
     CK(cudaEventRecord(h->ev1, s));
     CK(cudaGetLastError());
     if (!on_device)

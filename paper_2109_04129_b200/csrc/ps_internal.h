@@ -22,7 +22,7 @@ struct GTask {
   int32_t n_mt;            // row tiles: column tile nt is complete when done[unit0+nt] == n_mt
   int32_t a_kmajor;        // 1: A's unit stride is along k (transposed views), 0: along i
   int32_t b_kmajor;        // 1: B's unit stride is along k, 0: along c
-  int32_t pad;
+  int32_t idep;            // task (same launch) producing the init rows I; -1: none
 };
 
 // A segment of a task's K dimension: K_s consecutive k's starting at virtual
@@ -116,6 +116,9 @@ void launch_permute_rows(int64_t N, int64_t nrhs, const int64_t* map, const doub
 // xt = bo - u; part[chunk*nrhs + c] = (sum |bo|^2, sum |u|^2) over the chunk's rows
 void launch_combine_norms(int64_t N, int64_t nrhs, const double2* bo, const double2* u, double2* xt,
                           double2* part, int64_t rows_per_chunk, cudaStream_t st);
+// part[chunk*nrhs + c] = (sum |bo|^2, sum |bo - xt|^2) over the chunk's rows
+void launch_norms2(int64_t N, int64_t nrhs, const double2* bo, const double2* xt, double2* part,
+                   int64_t rows_per_chunk, cudaStream_t st);
 // norms[c] = (sqrt sum_chunks part.x, sqrt sum part.y)
 void launch_finalize_norms(int64_t nchunks, int64_t nrhs, const double2* part, double2* norms,
                            cudaStream_t st);

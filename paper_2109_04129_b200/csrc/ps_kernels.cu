@@ -294,6 +294,11 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
   }
   // ---- wait for the producers of B (warp 0, one segment per lane) ----
   if (tid < 32) {
+    if (tid == 0 && T.idep >= 0) {          // producer of the init rows
+      const int32_t need = a.tasks[T.idep].n_mt;
+      const int32_t* flag = done + a.tasks[T.idep].unit0 + w.nt;
+      while (ld_acquire(flag) < need) __nanosleep(32);
+    }
     for (int t = w.ta + tid; t < w.tb; t += 32) {
       const int dep = a.terms[t].dep;
       if (dep >= 0) {
@@ -389,6 +394,11 @@ __device__ __forceinline__ void item_body_dmma(const FlowArgs& a, const GWork& w
     if (s < nsteps) issue_a<GM_MT, GM_NT>(kt, s * KC, klen, i0, mm, a_km, a.A, tid, As0 + s * STAGE_A);
   cp_commit();
   if (tid < 32) {
+    if (tid == 0 && T.idep >= 0) {          // producer of the init rows
+      const int32_t need = a.tasks[T.idep].n_mt;
+      const int32_t* flag = done + a.tasks[T.idep].unit0 + w.nt;
+      while (ld_acquire(flag) < need) __nanosleep(32);
+    }
     for (int t = w.ta + tid; t < w.tb; t += 32) {
       const int dep = a.terms[t].dep;
       if (dep >= 0) {
@@ -513,6 +523,11 @@ __device__ __forceinline__ void item_body_narrow(const FlowArgs& a, const GWork&
       }
   }
   if (tid < 32) {
+    if (tid == 0 && T.idep >= 0) {          // producer of the init rows
+      const int32_t need = a.tasks[T.idep].n_mt;
+      const int32_t* flag = done + a.tasks[T.idep].unit0 + w.nt;
+      while (ld_acquire(flag) < need) __nanosleep(32);
+    }
     for (int t = w.ta + tid; t < w.tb; t += 32) {
       const int dep = a.terms[t].dep;
       if (dep >= 0) {
@@ -871,6 +886,28 @@ __global__ void combine_norms_kernel(int64_t N, int64_t nrhs, const double2* __r
   }
   part[blockIdx.x * nrhs + c] = make_double2(s0, s1);
 }
+// ||b_o||^2 and ||u||^2 = ||b_o - x~||^2 per column (Eq. 44), fixed chunking
+__global__ void norms2_kernel(int64_t N, int64_t nrhs, const double2* __restrict__ bo,
+                              const double2* __restrict__ xt, double2* __restrict__ part, int64_t rpc) {
+  const int64_t c = blockIdx.y * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= nrhs) return;
+  const int64_t r0 = blockIdx.x * rpc, r1 = min(N, r0 + rpc);
+  double s0 = 0.0, s1 = 0.0;
+  for (int64_t r = r0; r < r1; ++r) {
+    const int64_t e = r * nrhs + c;
+    const double2 a = bo[e], x = xt[e];
+    const double ux = a.x - x.x, uy = a.y - x.y;
+    s0 += a.x * a.x + a.y * a.y;
+    s1 += ux * ux + uy * uy;
+  }
+  part[blockIdx.x * nrhs + c] = make_double2(s0, s1);
+}
+void launch_norms2(int64_t N, int64_t nrhs, const double2* bo, const double2* xt, double2* part,
+                   int64_t rpc, cudaStream_t st) {
+  dim3 g((unsigned)((N + rpc - 1) / rpc), (unsigned)((nrhs + 127) / 128));
+  norms2_kernel<<<g, 128, 0, st>>>(N, nrhs, bo, xt, part, rpc);
+}
+
 __global__ void finalize_norms_kernel(int64_t nch, int64_t nrhs, const double2* __restrict__ part,
                                       double2* __restrict__ norms) {
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
