@@ -283,15 +283,20 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
 #pragma unroll
     for (int r = 0; r < RM; ++r) acc[r] = __ldcg(Gs + (rbase + r) * GM_NT + col);
   }
-  if (owns_init && T.oI >= 0 && col < nn) {
+  // init rows produced by an earlier task of this launch (idep >= 0) are read
+  // only after that producer has published them (below, after the wait)
+  auto load_init = [&]() {
+    if (owns_init && T.oI >= 0 && col < nn) {
 #pragma unroll
-    for (int r = 0; r < RM; ++r)
-      if (rbase + r < mm) {
-        const double2 z = __ldcg(a.I + T.oI + (int64_t)(i0 + rbase + r) * T.sIi + (int64_t)(c0 + col) * T.sIc);
-        acc[r].x += sgn * z.x;
-        acc[r].y += sgn * z.y;
-      }
-  }
+      for (int r = 0; r < RM; ++r)
+        if (rbase + r < mm) {
+          const double2 z = __ldcg(a.I + T.oI + (int64_t)(i0 + rbase + r) * T.sIi + (int64_t)(c0 + col) * T.sIc);
+          acc[r].x += sgn * z.x;
+          acc[r].y += sgn * z.y;
+        }
+    }
+  };
+  if (T.idep < 0) load_init();
   // ---- wait for the producers of B (warp 0, one segment per lane) ----
   if (tid < 32) {
     if (tid == 0 && T.idep >= 0) {          // producer of the init rows
@@ -309,6 +314,7 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
     }
   }
   __syncthreads();
+  if (T.idep >= 0) load_init();
   if (tr) tr[3] = gtimer();
   // ---- prologue part 2: B of stages 0..NSTAGE-2 (one group each) ----
 #pragma unroll
@@ -513,15 +519,18 @@ __device__ __forceinline__ void item_body_narrow(const FlowArgs& a, const GWork&
     acc[0] = __ldcg(Gs + row * GN_NT + cb);
     acc[1] = __ldcg(Gs + row * GN_NT + cb + 1);
   }
-  if (owns_init && T.oI >= 0 && row < mm) {
+  auto load_init = [&]() {    // after the producer's publication when idep >= 0
+    if (owns_init && T.oI >= 0 && row < mm) {
 #pragma unroll
-    for (int e = 0; e < 2; ++e)
-      if (cb + e < nn) {
-        const double2 z = __ldcg(a.I + T.oI + (int64_t)(i0 + row) * T.sIi + (int64_t)(c0 + cb + e) * T.sIc);
-        acc[e].x += sgn * z.x;
-        acc[e].y += sgn * z.y;
-      }
-  }
+      for (int e = 0; e < 2; ++e)
+        if (cb + e < nn) {
+          const double2 z = __ldcg(a.I + T.oI + (int64_t)(i0 + row) * T.sIi + (int64_t)(c0 + cb + e) * T.sIc);
+          acc[e].x += sgn * z.x;
+          acc[e].y += sgn * z.y;
+        }
+    }
+  };
+  if (T.idep < 0) load_init();
   if (tid < 32) {
     if (tid == 0 && T.idep >= 0) {          // producer of the init rows
       const int32_t need = a.tasks[T.idep].n_mt;
@@ -538,6 +547,7 @@ __device__ __forceinline__ void item_body_narrow(const FlowArgs& a, const GWork&
     }
   }
   __syncthreads();
+  if (T.idep >= 0) load_init();
   if (tr) tr[3] = gtimer();
 #pragma unroll
   for (int s = 0; s < NSTAGE - 1; ++s) {
