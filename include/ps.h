@@ -68,13 +68,30 @@ typedef enum {
   PS_ESTATE = 9      /* call order violated (ps_solve before ps_setup, ...) */
 } ps_status;
 
-/* Process placement. nranks > 1 selects replicated-operator mode: every rank
- * loads the whole operator and solves the RHS columns it is given (the data-
- * parallel split of RHS columns is done by the caller).
- * nccl_unique_id is reserved for the row-partitioned mode and must be NULL. */
+/* Process placement.
+ *   partition = 0 : replicated operator. Every rank loads the whole operator
+ *                   and solves the RHS columns it is given (the caller splits
+ *                   the columns); no collective. nccl_unique_id must be NULL.
+ *   partition = 1 : row partition over nranks. Whole subtrees of the
+ *                   elimination tree (leaf-cluster block rows: their alpha
+ *                   panels, D^-1 and the far-field rows they own) are assigned
+ *                   to ranks, the separator nodes above them are replicated.
+ *                   One solve = 4 phases separated by collectives (sum
+ *                   all-reduce of the separator rows after each interior forward
+ *                   sweep, all-gather of w = R b_o before the far field — the
+ *                   exchange between the two series terms — and of x at the end).
+ *                   nccl_unique_id != NULL: 128-byte ncclUniqueId from
+ *                   ps_nccl_unique_id() on rank 0, shared by the caller; hm_load
+ *                   then joins the NCCL communicator (collective: all ranks must
+ *                   call it) and ps_solve runs this rank's share (every rank
+ *                   passes the full B and receives the full X).
+ *                   nccl_unique_id == NULL: in-process group; the handles of all
+ *                   ranks live in one process and are solved with ps_solve_group.
+ *   device         : CUDA device of this rank. */
 typedef struct {
   int rank, nranks, device;
   const void* nccl_unique_id;
+  int partition;
 } ps_dist;
 
 typedef struct {
@@ -133,6 +150,31 @@ ps_status ps_setup(ps_handle* h, const ps_setup_opts* opts);
 ps_status ps_solve(ps_handle* h, int64_t nrhs, const void* B, int64_t ldb, void* X, int64_t ldx,
                    int on_device, void* cuda_stream, ps_report* rep);
 
+/* ps_solve_group — one two-term solve of a row-partitioned problem whose ranks
+ * are handles of THIS process (hm_load with partition = 1, nccl_unique_id =
+ * NULL, ranks 0..nranks-1 in hs[0..nranks-1], all on one device). The phases
+ * of every rank run in rank order on one stream and the collectives are
+ * device copies / fixed-order sums between the ranks' workspaces — the same
+ * per-rank work and exchange layout as the NCCL path, without concurrency.
+ *   B, X : device pointers (N x nrhs, column-major, RWG order); X written from
+ *          rank 0's gathered result. Other arguments as ps_solve.
+ * Errors: PS_EINVAL (handles not one consistent group), PS_ESTATE, PS_ECUDA,
+ * PS_EDIVERGED (X fully written). */
+ps_status ps_solve_group(ps_handle* const* hs, int nranks, int64_t nrhs, const void* B, int64_t ldb,
+                         void* X, int64_t ldx, void* cuda_stream, ps_report* rep);
+
+/* ps_nccl_unique_id — ncclGetUniqueId into out[0..128) (call on rank 0, share
+ * the bytes, pass them as ps_dist.nccl_unique_id on every rank). NCCL is
+ * loaded at run time (libnccl.so.2). Errors: PS_EINVAL (cap < 128), PS_ENCCL. */
+ps_status ps_nccl_unique_id(void* out, int64_t cap);
+
+/* ps_partition — host-only: the row partition hm_load would use for nranks
+ * ranks (no GPU needed). For every elimination position p (0..n_leaves-1):
+ * owner[p] = rank owning the interior node p, or -1 for a replicated separator
+ * node; far_owner[p] = rank computing the far-field rows of leaf p.
+ * cap = capacity of both arrays. Returns n_leaves, or -ps_status on error. */
+int64_t ps_partition(const char* path, int nranks, int32_t* owner, int32_t* far_owner, int64_t cap);
+
 /* ps_n — number of unknowns N of the loaded H-matrix; -1 if h is NULL. */
 int64_t ps_n(const ps_handle* h);
 
@@ -163,7 +205,11 @@ ps_status ps_apply(ps_handle* h, int op, int64_t nrhs, const void* X, void* Y);
 enum {
   PS_INFO_N = 0, PS_INFO_NLEAVES, PS_INFO_NNEAR, PS_INFO_NFAR, PS_INFO_ALPHA_BLOCKS,
   PS_INFO_NR, PS_INFO_ND, PS_INFO_NF, PS_INFO_HEIGHT, PS_INFO_DEPTH, PS_INFO_SETUP_MADDS,
-  PS_INFO_SETUP_DONE, PS_INFO_COUNT
+  PS_INFO_SETUP_DONE,
+  PS_INFO_NRANKS,            /* ranks of the row partition (1 otherwise) */
+  PS_INFO_OWN_ROWS,          /* unknowns in this rank's interior subtrees */
+  PS_INFO_SEP_ROWS,          /* unknowns in the replicated separator nodes */
+  PS_INFO_COUNT
 };
 int ps_info(const ps_handle* h, double* out, int n);
 

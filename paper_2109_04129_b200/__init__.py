@@ -6,4 +6,5 @@ There is no CPU fallback: if libps.so is missing or no CUDA device is present,
 the calls raise.
 """
 from .binding import (PsError, PsHandle, PS_OP_DINV, PS_OP_R, PS_OP_RT, PS_OP_U,  # noqa: F401
-                      PS_OP_ZF, load_library, lib_path, INFO_KEYS)
+                      PS_OP_ZF, load_library, lib_path, INFO_KEYS, solve_group, nccl_unique_id,
+                      partition)

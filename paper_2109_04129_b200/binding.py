@@ -21,7 +21,7 @@ STATUS_NAMES = ["PS_OK", "PS_EINVAL", "PS_EIO", "PS_EFORMAT", "PS_ENOMEM", "PS_E
                 "PS_ESINGULAR", "PS_EDIVERGED", "PS_ESTATE"]
 PS_OP_RT, PS_OP_DINV, PS_OP_R, PS_OP_ZF, PS_OP_U = 1, 2, 3, 4, 5
 INFO_KEYS = ["N", "n_leaves", "n_near", "n_far", "alpha_blocks", "nR", "nD", "nF", "height",
-             "depth", "setup_madds", "setup_done"]
+             "depth", "setup_madds", "setup_done", "nranks", "own_rows", "sep_rows"]
 
 
 class PsError(RuntimeError):
@@ -32,7 +32,7 @@ class PsError(RuntimeError):
 
 class _Dist(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("device", ctypes.c_int),
-                ("nccl_unique_id", ctypes.c_void_p)]
+                ("nccl_unique_id", ctypes.c_void_p), ("partition", ctypes.c_int)]
 
 
 class _Opts(ctypes.Structure):
@@ -96,6 +96,12 @@ def load_library():
     L.ps_trace_read.argtypes = [P, ctypes.POINTER(I64), I64]
     L.ps_elim_leaf.restype = I64
     L.ps_elim_leaf.argtypes = [P, I64]
+    L.ps_solve_group.restype = I
+    L.ps_solve_group.argtypes = [ctypes.POINTER(P), I, I64, P, I64, P, I64, P, ctypes.POINTER(_Report)]
+    L.ps_nccl_unique_id.restype = I
+    L.ps_nccl_unique_id.argtypes = [P, I64]
+    L.ps_partition.restype = I64
+    L.ps_partition.argtypes = [ctypes.c_char_p, I, P, P, I64]
     _lib = L
     return L
 
@@ -128,12 +134,23 @@ def _ptr_ld(X, N):
 class PsHandle:
     """One loaded H-matrix on one GPU (hm_load / ps_setup / ps_solve)."""
 
-    def __init__(self, path: str, device: int | None = None, rank: int = 0, nranks: int = 1):
+    def __init__(self, path: str, device: int | None = None, rank: int = 0, nranks: int = 1,
+                 partition: bool = False, nccl_id: bytes | None = None):
+        """partition=False: replicated operator (the caller splits RHS columns).
+        partition=True: row partition over nranks (include/ps.h ps_dist); with
+        nccl_id (ps_nccl_unique_id() bytes shared by rank 0) ps_solve runs this
+        rank's share with NCCL collectives, without it the handles of all ranks
+        belong to one process and are solved together by solve_group()."""
         L = load_library()
         h = ctypes.c_void_p()
         dist = None
+        self._idbuf = None
         if device is not None or nranks > 1:
-            dist = _Dist(rank, nranks, 0 if device is None else device, None)
+            idp = None
+            if nccl_id is not None:
+                self._idbuf = ctypes.create_string_buffer(bytes(nccl_id), len(nccl_id))
+                idp = ctypes.cast(self._idbuf, ctypes.c_void_p)
+            dist = _Dist(rank, nranks, 0 if device is None else device, idp, 1 if partition else 0)
         st = L.hm_load(path.encode(), ctypes.byref(dist) if dist is not None else None, ctypes.byref(h))
         if st != PS_OK:
             raise PsError(st, L.ps_last_error(None).decode())
@@ -231,3 +248,59 @@ class PsHandle:
 
     def elim_leaf(self, pos: int) -> int:
         return int(load_library().ps_elim_leaf(self._h, pos))
+
+
+def _report(nrhs, want_norms):
+    it0 = np.zeros(nrhs) if want_norms else None
+    it1 = np.zeros(nrhs) if want_norms else None
+    rep = _Report(nrhs, it0.ctypes.data if want_norms else None, it1.ctypes.data if want_norms else None,
+                  0, 0.0, 0.0, 0.0, 0)
+    return rep, it0, it1
+
+
+def solve_group(handles, B, X, stream=None, want_norms: bool = True):
+    """ps_solve_group: one solve of an in-process row partition (handles =
+    ranks 0..P-1, PsHandle(..., rank=g, nranks=P, partition=True)); B and X
+    are device column-major N x nrhs complex128 tensors. Returns (status, report)."""
+    L = load_library()
+    N = handles[0].N
+    bp, ldb, nrhs, bdev = _ptr_ld(B, N)
+    xp, ldx, nrhs2, xdev = _ptr_ld(X, N)
+    if nrhs != nrhs2 or not (bdev and xdev):
+        raise ValueError("solve_group takes device tensors of equal shape")
+    arr = (ctypes.c_void_p * len(handles))(*[h._h for h in handles])
+    rep, it0, it1 = _report(nrhs, want_norms)
+    s = None
+    if stream is not None:
+        s = ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+    st = L.ps_solve_group(arr, len(handles), nrhs, bp, ldb, xp, ldx, s, ctypes.byref(rep))
+    if st != PS_OK and st != PS_EDIVERGED:
+        raise PsError(st, L.ps_last_error(handles[0]._h).decode())
+    r = dict(it0=it0, it1=it1, n_diverged=rep.n_diverged, t_solve_ms=rep.t_solve_ms,
+             launches=rep.kernel_launches, status=STATUS_NAMES[st])
+    if want_norms:
+        r["ratio"] = it1 / np.where(it0 > 0, it0, 1.0)
+    return st, r
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId through libps (128 bytes; rank 0 creates, all ranks share)."""
+    L = load_library()
+    buf = ctypes.create_string_buffer(128)
+    st = L.ps_nccl_unique_id(buf, 128)
+    if st != PS_OK:
+        raise PsError(st, L.ps_last_error(None).decode())
+    return buf.raw
+
+
+def partition(path: str, nranks: int):
+    """Host-only: (owner, far_owner) per elimination position for nranks ranks
+    (owner -1 = replicated separator node); see include/ps.h ps_partition."""
+    L = load_library()
+    cap = 1 << 22
+    ow = np.zeros(cap, dtype=np.int32)
+    fo = np.zeros(cap, dtype=np.int32)
+    n = L.ps_partition(path.encode(), nranks, ow.ctypes.data, fo.ctypes.data, cap)
+    if n < 0:
+        raise PsError(-n, L.ps_last_error(None).decode())
+    return ow[:n].copy(), fo[:n].copy()

@@ -15,6 +15,9 @@
 #include "../../include/ps.h"
 #include "ps_internal.h"
 
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include <algorithm>
 #include <array>
 #include <chrono>
@@ -401,6 +404,17 @@ struct SolvePlan {
   int64_t launches_per_solve = 0;
 };
 
+// Per-nrhs plan of the row-partitioned solve: this rank's tables
+// over one workspace arena ws = [Y | BO | W | Z | XT | X | TMP] in the
+// partitioned row layout (doff), every table addressing it through offsets.
+struct DistPlan {
+  int64_t nrhs = 0;
+  Table fwdIA, fwdSA, dinvA, bwdA, far1, far2, fwdIC, fwdSC, dinvC, bwdC;
+  DevBuf<double2> ws, part, sums, scratch;
+  int64_t oY = 0, oBO = 0, oW = 0, oZ = 0, oXT = 0, oX = 0, oTMP = 0;
+  int64_t rpc = 64, nchI = 0, nchS = 0;
+};
+
 }  // namespace
 
 struct ps_handle {
@@ -446,6 +460,17 @@ struct ps_handle {
   std::unique_ptr<SolvePlan> plan;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   Prof prof;
+  // ---- row partition (ps_dist.partition = 1) ----
+  int rank = 0, nranks = 1, part_mode = 0;
+  std::vector<int32_t> owner, far_owner;   // per position: interior rank (-1 separator); far-row rank
+  std::vector<int64_t> doff;               // first row of position p in the partitioned layout:
+                                           // [rank 0 interior | ... | rank P-1 interior | separators],
+                                           // each interior block padded to maxI rows
+  int64_t own_rows = 0, maxI = 0, Nsep = 0, Npad = 0;
+  std::vector<int64_t> d2rwg;              // layout row -> RWG index (-1: padding)
+  DevBuf<int64_t> d_d2rwg;
+  void* nccl = nullptr;                    // ncclComm_t; nullptr: in-process group (ps_solve_group)
+  std::unique_ptr<DistPlan> dplan;
 };
 
 namespace {
@@ -641,6 +666,110 @@ void symbolic(ps_handle* h) {
       h->e2rwg[e] = h->perm[m];
       h->m2e[m] = e;
     }
+  }
+}
+
+// ------------------------------------------------------------------ row partition
+// Row partition of the solve over P ranks (SURVEY §8(e) option 1).
+// The elimination tree decouples disjoint subtrees: struct(p) only holds
+// ancestors of p, so the forward sweep of a subtree needs nothing from outside
+// it, and the backward sweep of a subtree needs only its ancestors. Whole
+// subtrees are assigned to ranks ("interior"); the nodes above them
+// ("separators") are replicated on every rank. Starting from the roots, the
+// heaviest subtree is split (its root becomes a separator) and the resulting
+// subtrees are bin-packed (largest first) onto the ranks; the split count that
+// minimises max-rank-load + replicated-separator load is kept.
+//   owner[p]     : rank owning interior position p, -1 for separators
+//   far_owner[p] : rank computing the far-field rows t_p (owner for interior
+//                  nodes; separators spread greedily by far-field work)
+void partition(const ps_handle* h, int P, std::vector<int32_t>& owner, std::vector<int32_t>& far_owner) {
+  const int64_t nl = h->nl;
+  owner.assign(nl, 0);
+  far_owner.assign(nl, 0);
+  if (P <= 1) return;
+  // per-position weights ~ operator entries touched per solve (4 sweeps, 2 D^-1; far 2 stages)
+  std::vector<double> wn(nl), wf(nl, 0.0);
+  for (int64_t p = 0; p < nl; ++p) wn[p] = 4.0 * h->nsz[p] * (double)h->S[p] + 2.0 * h->nsz[p] * (double)h->nsz[p];
+  auto leaf_of_m = [&](int64_t m) {
+    return (int64_t)(std::upper_bound(h->leaf_off.begin(), h->leaf_off.end(), m) - h->leaf_off.begin()) - 1;
+  };
+  for (int64_t b = 0; b < h->nfar; ++b) {
+    const int64_t* F = &h->far_list[7 * b];
+    const int64_t r0 = F[0], m = F[1], c0 = F[2], n = F[3], r = F[5];
+    for (int side = 0; side < 2; ++side) {
+      const int64_t a0 = side ? c0 : r0, len = side ? n : m, other = side ? m : n;
+      for (int64_t l = leaf_of_m(a0); l < nl && h->leaf_off[l] < a0 + len; ++l) {
+        const int64_t lo = std::max(a0, h->leaf_off[l]), hi = std::min(a0 + len, h->leaf_off[l + 1]);
+        wf[h->pos_of[l]] += (double)(hi - lo) * (double)std::min<int64_t>(2 * r, other);
+      }
+    }
+  }
+  std::vector<std::vector<int32_t>> children(nl);
+  std::vector<int32_t> roots;
+  for (int64_t p = 0; p < nl; ++p) {
+    if (h->parent[p] >= 0) children[h->parent[p]].push_back((int32_t)p);
+    else roots.push_back((int32_t)p);
+  }
+  std::vector<double> W(nl);   // subtree weight (children have smaller positions)
+  for (int64_t p = 0; p < nl; ++p) W[p] = wn[p] + wf[p];
+  for (int64_t p = 0; p < nl; ++p)
+    if (h->parent[p] >= 0) W[h->parent[p]] += W[p];
+  std::vector<int32_t> subs = roots, sep;
+  double sep_near = 0, sep_far = 0;
+  double best = 1e300;
+  std::vector<int32_t> best_subs, best_sep, best_bin;
+  const size_t max_subs = (size_t)(32 * P);
+  for (int it = 0; it < 64 * P + 64; ++it) {
+    // LPT bin packing of the current subtrees
+    std::vector<int32_t> ord = subs;
+    std::sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) { return W[x] > W[y] || (W[x] == W[y] && x < y); });
+    std::vector<double> load(P, 0.0);
+    std::vector<int32_t> bin(nl, -1);
+    for (int32_t s : ord) {
+      int g = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+      load[g] += W[s];
+      bin[s] = g;
+    }
+    const double cost = *std::max_element(load.begin(), load.end()) + sep_near + sep_far / P;
+    if (cost < best) {
+      best = cost;
+      best_subs = subs;
+      best_sep = sep;
+      best_bin = bin;
+    }
+    if (subs.size() >= max_subs) break;
+    // split the heaviest subtree that has children
+    int32_t hv = -1;
+    for (int32_t s : subs)
+      if (!children[s].empty() && (hv < 0 || W[s] > W[hv])) hv = s;
+    if (hv < 0) break;
+    subs.erase(std::find(subs.begin(), subs.end(), hv));
+    for (int32_t c : children[hv]) subs.push_back(c);
+    sep.push_back(hv);
+    sep_near += wn[hv];
+    sep_far += wf[hv];
+  }
+  // interior owners: every node of an assigned subtree (children have smaller
+  // positions, so a reverse sweep propagates the owner down from the subtree roots)
+  owner.assign(nl, -2);
+  for (int32_t s : best_sep) owner[s] = -1;
+  for (int32_t s : best_subs) owner[s] = best_bin[s];
+  for (int64_t p = nl - 1; p >= 0; --p)
+    if (owner[p] == -2) owner[p] = owner[h->parent[p]];
+  // far rows of the separators: greedy by far work onto the least-loaded rank
+  std::vector<double> load(P, 0.0);
+  for (int64_t p = 0; p < nl; ++p)
+    if (owner[p] >= 0) load[owner[p]] += wn[p] + wf[p];
+  std::vector<int32_t> sp_ord;
+  for (int64_t p = 0; p < nl; ++p) {
+    far_owner[p] = owner[p];
+    if (owner[p] < 0) sp_ord.push_back((int32_t)p);
+  }
+  std::sort(sp_ord.begin(), sp_ord.end(), [&](int32_t x, int32_t y) { return wf[x] > wf[y] || (wf[x] == wf[y] && x < y); });
+  for (int32_t p : sp_ord) {
+    int g = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+    far_owner[p] = g;
+    load[g] += wf[p];
   }
 }
 
@@ -1168,7 +1297,8 @@ SolvePlan& get_plan(ps_handle* h, int64_t nrhs) {
     h->plan.reset();
     auto sp = std::make_unique<SolvePlan>();
     build_solve_plan(h, *sp, nrhs);
-    build_program(h, *sp, nrhs);
+    const char* e = std::getenv("PS_SOLVE");
+    if (e && std::string(e) == "program") build_program(h, *sp, nrhs);
     h->plan = std::move(sp);
   }
   return *h->plan;
@@ -1222,6 +1352,483 @@ double solve_flops(const ps_handle* h, int64_t nrhs) {
   return 8.0 * nrhs * (4 * nR + 2 * nD + 2 * nF);
 }
 
+// ------------------------------------------------------------------ NCCL (run-time loaded)
+// libps does not link NCCL: it is opened on first use (the copy torch already
+// loaded when present, else the system one), so single-GPU users need none.
+struct NcclApi {
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*errStr)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl_api() {
+  static NcclApi api;
+  static bool tried = false;
+  static std::string why;
+  if (!tried) {
+    tried = true;
+    void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) {
+      why = std::string("cannot load libnccl.so.2: ") + dlerror();
+    } else {
+      api.getUniqueId = (decltype(api.getUniqueId))dlsym(lib, "ncclGetUniqueId");
+      api.commInitRank = (decltype(api.commInitRank))dlsym(lib, "ncclCommInitRank");
+      api.allReduce = (decltype(api.allReduce))dlsym(lib, "ncclAllReduce");
+      api.allGather = (decltype(api.allGather))dlsym(lib, "ncclAllGather");
+      api.commDestroy = (decltype(api.commDestroy))dlsym(lib, "ncclCommDestroy");
+      api.errStr = (decltype(api.errStr))dlsym(lib, "ncclGetErrorString");
+      if (!api.getUniqueId || !api.commInitRank || !api.allReduce || !api.allGather || !api.commDestroy)
+        why = "libnccl.so.2 lacks a required symbol";
+    }
+  }
+  if (!why.empty()) throw PsError{PS_ENCCL, why};
+  return api;
+}
+
+#define NCK(x)                                                                                  \
+  do {                                                                                          \
+    ncclResult_t r_ = (x);                                                                      \
+    if (r_ != ncclSuccess)                                                                      \
+      throw PsError{PS_ENCCL, std::string(#x) + ": " +                                          \
+                                  (nccl_api().errStr ? nccl_api().errStr(r_) : "nccl error")};  \
+  } while (0)
+
+// ------------------------------------------------------------------ row-partitioned solve
+// Vector layout of the partitioned mode: rank g's interior positions (in
+// elimination order) at rows [g maxI, g maxI + own_g), the separators (in
+// elimination order) at rows [P maxI, P maxI + Nsep). The separator block and
+// every rank block are contiguous, so the exchanges are plain all-reduce /
+// all-gather calls on sub-ranges of one buffer.
+void dist_layout(ps_handle* h) {
+  const int P = h->nranks;
+  partition(h, P, h->owner, h->far_owner);
+  std::vector<int64_t> cnt(P, 0);
+  h->Nsep = 0;
+  for (int64_t p = 0; p < h->nl; ++p) {
+    if (h->owner[p] >= 0) cnt[h->owner[p]] += h->nsz[p];
+    else h->Nsep += h->nsz[p];
+  }
+  h->maxI = *std::max_element(cnt.begin(), cnt.end());
+  h->own_rows = cnt[h->rank];
+  h->Npad = P * h->maxI + h->Nsep;
+  h->doff.assign(h->nl, 0);
+  std::vector<int64_t> next(P);
+  for (int g = 0; g < P; ++g) next[g] = g * h->maxI;
+  int64_t sn = P * h->maxI;
+  for (int64_t p = 0; p < h->nl; ++p) {
+    if (h->owner[p] >= 0) { h->doff[p] = next[h->owner[p]]; next[h->owner[p]] += h->nsz[p]; }
+    else { h->doff[p] = sn; sn += h->nsz[p]; }
+  }
+  h->d2rwg.assign(h->Npad, -1);
+  for (int64_t p = 0; p < h->nl; ++p) {
+    const int32_t l = h->leaf_at[p];
+    for (int64_t t = 0; t < h->nsz[p]; ++t) h->d2rwg[h->doff[p] + t] = h->perm[h->leaf_off[l] + t];
+  }
+}
+
+// This rank's tables. Phases and the exchange after each:
+//   0  y = B; y[S] = 0 on ranks != 0; forward sweep of the interior subtrees
+//      plus their contributions to the separator rows            -> all-reduce y[S]
+//   1  separator forward sweep; b_o = D^-1 y; w = R b_o (separators, then
+//      interior)                                                  -> all-gather w
+//   2  z = Z_F w on this rank's far rows (z[S] = 0 elsewhere); interior forward
+//      sweep of z + separator contributions                       -> all-reduce z[S]
+//   3  separator forward sweep of z; xt = b_o - D^-1 z; norms of this rank's
+//      rows; x = R xt                                             -> all-gather x, all-reduce norms
+//   4  X = x in RWG order
+void build_dist_plan(ps_handle* h, DistPlan& dp, int64_t R) {
+  const int64_t nl = h->nl;
+  const int g = h->rank;
+  dp.nrhs = R;
+  const int64_t NP = h->Npad * R;
+  dp.oY = 0; dp.oBO = NP; dp.oW = 2 * NP; dp.oZ = 3 * NP; dp.oXT = 4 * NP; dp.oX = 5 * NP; dp.oTMP = 6 * NP;
+  const int64_t ncl = (int64_t)h->cl_start.size();
+  std::vector<int64_t> toff(ncl);
+  int64_t Ttot = 0;
+  for (int64_t c = 0; c < ncl; ++c) { toff[c] = dp.oTMP + Ttot; Ttot += h->cl_sr[c] * R; }
+  const int narrow = (R <= 8) ? 1 : 0;
+  for (Table* tb : {&dp.fwdIA, &dp.fwdSA, &dp.dinvA, &dp.bwdA, &dp.far1, &dp.far2, &dp.fwdIC, &dp.fwdSC,
+                    &dp.dinvC, &dp.bwdC}) {
+    tb->narrow = narrow;
+    if (narrow) tb->chunk_steps = 4;
+  }
+  auto mine = [&](int64_t p) { return h->owner[p] == g; };
+  auto sep = [&](int64_t p) { return h->owner[p] < 0; };
+  std::vector<std::vector<int32_t>> byh(h->max_height + 1), byd(h->max_depth + 1);
+  for (int64_t p = 0; p < nl; ++p) {
+    byh[h->height[p]].push_back((int32_t)p);
+    byd[h->depth[p]].push_back((int32_t)p);
+  }
+  const int resident = flow_resident_ctas();
+  auto steps_for = [&](const std::vector<int32_t>& nodes, bool fwd) {
+    if (narrow) return 4;
+    double ks = 0;
+    for (int32_t p : nodes) {
+      if (!(mine(p) || sep(p))) continue;
+      double K = 0;
+      if (fwd) { for (auto [d, idx] : h->gath[p]) K += h->nsz[d]; }
+      else K = (double)h->S[p];
+      ks += std::ceil((double)h->nsz[p] / GM_MT) * std::ceil((double)R / GM_NT) * std::ceil(K / GM_KC);
+    }
+    return std::max(4, std::min(32, (int)std::ceil(ks / (2.0 * resident))));
+  };
+  const int64_t Pb = h->Pbase, Db = h->Dbase, Fb = h->Fbase;
+  // forward sweep (gather form of Eq. 24), in place on `buf`; interior = this
+  // rank's subtrees plus their partial sums into separator rows, else the
+  // separator nodes fed by separator descendants only
+  auto fwd = [&](Table& T, int64_t buf, bool interior) {
+    std::vector<int32_t> ft(nl, -1);
+    for (int L = 0; L <= h->max_height; ++L) {
+      const int stp = steps_for(byh[L], true);
+      for (int32_t q : byh[L]) {
+        if (interior ? !(mine(q) || sep(q)) : !sep(q)) continue;
+        std::vector<std::pair<int32_t, int32_t>> gl;
+        for (auto [d, idx] : h->gath[q])
+          if (interior ? mine(d) : sep(d)) gl.push_back({d, idx});
+        if (gl.empty()) continue;
+        std::stable_sort(gl.begin(), gl.end(), [&](const std::pair<int32_t, int32_t>& x,
+                                                   const std::pair<int32_t, int32_t>& y) {
+          return h->height[x.first] < h->height[y.first];
+        });
+        const int64_t nq = h->nsz[q];
+        int32_t t = T.add_task(buf + h->doff[q] * R, R, 1, buf + h->doff[q] * R, R, 1, (int)nq, (int)R, +1);
+        for (auto [d, idx] : gl) {
+          const int64_t nd = h->nsz[d];
+          T.add_term(t, Pb + h->Poff[d] + h->pcol[d][idx] * nd, nd, 1, buf + h->doff[d] * R, R, 1, (int)nd, ft[d]);
+        }
+        T.tile(t, -1, stp);
+        ft[q] = t;
+      }
+    }
+    T.close_batch();
+  };
+  // D^-1 on this rank's interior and the separators: dst = init + sign D^-1 src
+  auto dinv = [&](Table& T, int64_t src, int64_t dst, int64_t init, int sign) {
+    for (int64_t p = 0; p < nl; ++p) {
+      if (!(mine(p) || sep(p))) continue;
+      const int64_t np_ = h->nsz[p];
+      int32_t t = T.add_task(dst + h->doff[p] * R, R, 1, init >= 0 ? init + h->doff[p] * R : -1, R, 1, (int)np_,
+                             (int)R, sign);
+      T.add_term(t, Db + h->Doff[p], 1, np_, src + h->doff[p] * R, R, 1, (int)np_);
+      T.tile(t);
+    }
+    T.close_batch();
+  };
+  // backward sweep (Eq. 26): separators (depth order puts them first), then the
+  // interior subtrees, whose struct lies in the subtree or the separators
+  auto bwd = [&](Table& T, int64_t in, int64_t out) {
+    std::vector<int32_t> bt(nl, -1);
+    for (int L = 0; L <= h->max_depth; ++L) {
+      const int stp = steps_for(byd[L], false);
+      for (int32_t p : byd[L]) {
+        if (!(mine(p) || sep(p))) continue;
+        const int64_t np_ = h->nsz[p];
+        int32_t t = T.add_task(out + h->doff[p] * R, R, 1, in + h->doff[p] * R, R, 1, (int)np_, (int)R, +1);
+        for (size_t i = 0; i < h->st[p].size(); ++i) {
+          const int32_t j = h->st[p][i];
+          if (!(mine(j) || sep(j))) throw PsError{PS_ECUDA, "internal: struct leaves the rank's subtree"};
+          T.add_term(t, Pb + h->Poff[p] + h->pcol[p][i] * np_, 1, np_, out + h->doff[j] * R, R, 1,
+                     (int)h->nsz[j], bt[j]);
+        }
+        T.tile(t, +1, stp);
+        bt[p] = t;
+      }
+    }
+    T.close_batch();
+  };
+  fwd(dp.fwdIA, dp.oY, true);
+  fwd(dp.fwdSA, dp.oY, false);
+  dinv(dp.dinvA, dp.oY, dp.oBO, -1, +1);
+  bwd(dp.bwdA, dp.oBO, dp.oW);
+  fwd(dp.fwdIC, dp.oZ, true);
+  fwd(dp.fwdSC, dp.oZ, false);
+  dinv(dp.dinvC, dp.oZ, dp.oXT, dp.oBO, -1);
+  bwd(dp.bwdC, dp.oXT, dp.oX);
+  // far field z = Z_F w for the leaves whose far rows this rank computes: stage 2
+  // per leaf (as build_program's S5), stage 1 only for the stacked rows it reads
+  auto leaf_of_pos = [&](int64_t m) {
+    return (int64_t)(std::upper_bound(h->leaf_off.begin(), h->leaf_off.end(), m) - h->leaf_off.begin()) - 1;
+  };
+  struct Seg { int64_t oA, sAi, sAk, oB; int K; };
+  std::vector<std::vector<Seg>> contrib(nl);
+  std::vector<std::vector<std::pair<int64_t, int64_t>>> need(ncl);   // stage-1 rows [a, a + r) per cluster
+  auto target = [&](int64_t l) { return h->far_owner[h->pos_of[l]] == g; };
+  for (int64_t b = 0; b < h->nfar; ++b) {
+    const int64_t* F = &h->far_list[7 * b];
+    const int64_t r0 = F[0], m = F[1], c0 = F[2], n = F[3], r = F[5];
+    if (r == 0) continue;
+    const int64_t ct = h->fb_ct[b], cs = h->fb_cs[b];
+    if (h->fb_dense[b] >= 0) {
+      const int64_t D = Fb + h->fb_dense[b];
+      for (int64_t l = leaf_of_pos(r0); l < nl && h->leaf_off[l] < r0 + m; ++l) {
+        if (!target(l)) continue;
+        for (int64_t q = leaf_of_pos(c0); q < nl && h->leaf_off[q] < c0 + n; ++q)
+          contrib[l].push_back({D + (h->leaf_off[l] - r0) + (h->leaf_off[q] - c0) * m, 1, m,
+                                dp.oW + h->doff[h->pos_of[q]] * R, (int)(h->leaf_off[q + 1] - h->leaf_off[q])});
+      }
+      for (int64_t l = leaf_of_pos(c0); l < nl && h->leaf_off[l] < c0 + n; ++l) {
+        if (!target(l)) continue;
+        for (int64_t q = leaf_of_pos(r0); q < nl && h->leaf_off[q] < r0 + m; ++q)
+          contrib[l].push_back({D + (h->leaf_off[q] - r0) + (h->leaf_off[l] - c0) * m, m, 1,
+                                dp.oW + h->doff[h->pos_of[q]] * R, (int)(h->leaf_off[q + 1] - h->leaf_off[q])});
+      }
+      continue;
+    }
+    bool used_s = false, used_t = false;
+    for (int64_t l = leaf_of_pos(r0); l < nl && h->leaf_off[l] < r0 + m; ++l)
+      if (target(l)) {
+        contrib[l].push_back({Fb + h->cl_soff[ct] + h->fb_rbt[b] + (h->leaf_off[l] - r0) * h->cl_sr[ct],
+                              h->cl_sr[ct], 1, toff[cs] + h->fb_rbs[b] * R, (int)r});
+        used_s = true;
+      }
+    for (int64_t l = leaf_of_pos(c0); l < nl && h->leaf_off[l] < c0 + n; ++l)
+      if (target(l)) {
+        contrib[l].push_back({Fb + h->cl_soff[cs] + h->fb_rbs[b] + (h->leaf_off[l] - c0) * h->cl_sr[cs],
+                              h->cl_sr[cs], 1, toff[ct] + h->fb_rbt[b] * R, (int)r});
+        used_t = true;
+      }
+    if (used_s) need[cs].push_back({h->fb_rbs[b], r});    // V_b^T w_s
+    if (used_t) need[ct].push_back({h->fb_rbt[b], r});    // U_b^T w_t
+  }
+  for (int64_t c = 0; c < ncl; ++c) {
+    auto& v = need[c];
+    if (v.empty()) continue;
+    std::sort(v.begin(), v.end());
+    std::vector<std::pair<int64_t, int64_t>> merged;   // (a, end)
+    for (auto [a, r] : v) {
+      if (!merged.empty() && a <= merged.back().second) merged.back().second = std::max(merged.back().second, a + r);
+      else merged.push_back({a, a + r});
+    }
+    const int64_t sr = h->cl_sr[c], a0 = h->cl_start[c], len = h->cl_len[c];
+    for (auto [a, e] : merged) {
+      int32_t t = dp.far1.add_task(toff[c] + a * R, R, 1, -1, 0, 0, (int)(e - a), (int)R, +1);
+      for (int64_t l = leaf_of_pos(a0); l < nl && h->leaf_off[l] < a0 + len; ++l)
+        dp.far1.add_term(t, Fb + h->cl_soff[c] + a + (h->leaf_off[l] - a0) * sr, 1, sr,
+                         dp.oW + h->doff[h->pos_of[l]] * R, R, 1, (int)(h->leaf_off[l + 1] - h->leaf_off[l]));
+      dp.far1.tile(t);
+    }
+  }
+  dp.far1.close_batch();
+  for (int64_t l = 0; l < nl; ++l) {
+    if (!target(l)) continue;
+    const int32_t pos = h->pos_of[l];
+    int32_t t = dp.far2.add_task(dp.oZ + h->doff[pos] * R, R, 1, -1, 0, 0, (int)h->nsz[pos], (int)R, +1);
+    for (auto& q : contrib[l]) dp.far2.add_term(t, q.oA, q.sAi, q.sAk, q.oB, R, 1, q.K);
+    dp.far2.tile(t);
+  }
+  dp.far2.close_batch();
+  for (Table* tb : {&dp.fwdIA, &dp.fwdSA, &dp.dinvA, &dp.bwdA, &dp.far1, &dp.far2, &dp.fwdIC, &dp.fwdSC,
+                    &dp.dinvC, &dp.bwdC})
+    tb->upload(h->stream);
+  dp.ws.alloc(6 * NP + std::max<int64_t>(Ttot, 1));
+  CK(cudaMemsetAsync(dp.ws.p, 0, sizeof(double2) * dp.ws.n, h->stream));   // padding rows stay 0
+  dp.nchI = (h->own_rows + dp.rpc - 1) / dp.rpc;
+  dp.nchS = h->rank == 0 ? (h->Nsep + dp.rpc - 1) / dp.rpc : 0;
+  dp.part.alloc(std::max<int64_t>(dp.nchI + dp.nchS, 1) * R);
+  dp.sums.alloc(R);
+  dp.scratch.alloc(std::max<int64_t>(std::max(h->Nsep, h->maxI) * R, R));
+  CK(cudaStreamSynchronize(h->stream));
+}
+
+DistPlan& get_dist_plan(ps_handle* h, int64_t nrhs) {
+  if (!h->dplan || h->dplan->nrhs != nrhs) {
+    h->dplan.reset();
+    auto dp = std::make_unique<DistPlan>();
+    build_dist_plan(h, *dp, nrhs);
+    h->dplan = std::move(dp);
+  }
+  return *h->dplan;
+}
+
+// One phase of this rank's partitioned solve (see build_dist_plan).
+int64_t dist_phase(ps_handle* h, DistPlan& dp, int k, const double2* Bd, int64_t ldb, double2* Xd, int64_t ldx,
+                   cudaStream_t s) {
+  const int64_t R = dp.nrhs;
+  double2* ws = dp.ws.p;
+  const double2* A = h->d_op.p;
+  const int64_t sep0 = h->nranks * h->maxI;
+  Prof* pf = &h->prof;
+  int64_t n = 0;
+  switch (k) {
+    case 0:
+      n += aux(h, s, [&] { launch_permute_in(h->Npad, R, h->d_d2rwg.p, Bd, ldb, ws + dp.oY, s); });
+      if (h->rank != 0 && h->Nsep > 0)
+        CK(cudaMemsetAsync(ws + dp.oY + sep0 * R, 0, sizeof(double2) * h->Nsep * R, s));
+      n += dp.fwdIA.launch_all(ws, ws, A, ws, s, pf, PC_FWD);
+      break;
+    case 1:
+      n += dp.fwdSA.launch_all(ws, ws, A, ws, s, pf, PC_FWD);
+      n += dp.dinvA.launch_all(ws, ws, A, ws, s, pf, PC_DINV);
+      n += dp.bwdA.launch_all(ws, ws, A, ws, s, pf, PC_BWD);
+      break;
+    case 2:
+      if (h->Nsep > 0) CK(cudaMemsetAsync(ws + dp.oZ + sep0 * R, 0, sizeof(double2) * h->Nsep * R, s));
+      n += dp.far1.launch_all(ws, ws, A, ws, s, pf, PC_FAR1);
+      n += dp.far2.launch_all(ws, ws, A, ws, s, pf, PC_FAR2);
+      n += dp.fwdIC.launch_all(ws, ws, A, ws, s, pf, PC_FWD);
+      break;
+    case 3:
+      n += dp.fwdSC.launch_all(ws, ws, A, ws, s, pf, PC_FWD);
+      n += dp.dinvC.launch_all(ws, ws, A, ws, s, pf, PC_DINV);
+      n += aux(h, s, [&] {    // ||b_o||^2, ||u||^2 = ||b_o - xt||^2 over this rank's rows (Eq. 44)
+        const int64_t r0 = h->rank * h->maxI;
+        if (h->own_rows > 0)
+          launch_norms2(h->own_rows, R, ws + dp.oBO + r0 * R, ws + dp.oXT + r0 * R, dp.part.p, dp.rpc, s);
+        if (dp.nchS > 0)
+          launch_norms2(h->Nsep, R, ws + dp.oBO + sep0 * R, ws + dp.oXT + sep0 * R, dp.part.p + dp.nchI * R,
+                        dp.rpc, s);
+        if (dp.nchI + dp.nchS > 0) launch_finalize_norms(dp.nchI + dp.nchS, R, dp.part.p, dp.sums.p, s, 0);
+        else CK(cudaMemsetAsync(dp.sums.p, 0, sizeof(double2) * R, s));
+      }) + 2;
+      n += dp.bwdC.launch_all(ws, ws, A, ws, s, pf, PC_BWD);
+      break;
+    case 4:
+      n += aux(h, s, [&] { launch_permute_out(h->Npad, R, h->d_d2rwg.p, ws + dp.oX, Xd, ldx, s); });
+      break;
+  }
+  return n;
+}
+
+// The exchange after phase k, as (offset, count) sub-ranges of the workspace
+// (complex elements): kind 0 = sum all-reduce, 1 = all-gather of equal blocks
+// (rank g's block at off + g * count), 2 = sum all-reduce of the norm sums.
+struct Xchg { int kind; int64_t off, count; };
+std::vector<Xchg> dist_exchanges(const ps_handle* h, const DistPlan& dp, int k) {
+  const int64_t R = dp.nrhs, sep0 = h->nranks * h->maxI;
+  switch (k) {
+    case 0: return {{0, dp.oY + sep0 * R, h->Nsep * R}};
+    case 1: return {{1, dp.oW, h->maxI * R}};
+    case 2: return {{0, dp.oZ + sep0 * R, h->Nsep * R}};
+    case 3: return {{1, dp.oX, h->maxI * R}, {2, 0, R}};
+  }
+  return {};
+}
+
+void nccl_exchange(ps_handle* h, DistPlan& dp, int k, cudaStream_t s) {
+  NcclApi& api = nccl_api();
+  ncclComm_t comm = (ncclComm_t)h->nccl;
+  for (const Xchg& x : dist_exchanges(h, dp, k)) {
+    if (x.count <= 0) continue;
+    if (x.kind == 1) {
+      double2* base = dp.ws.p + x.off;
+      NCK(api.allGather(base + h->rank * x.count, base, 2 * x.count, ncclDouble, comm, s));
+    } else {
+      double2* p = x.kind == 2 ? dp.sums.p : dp.ws.p + x.off;
+      NCK(api.allReduce(p, p, 2 * x.count, ncclDouble, ncclSum, comm, s));
+    }
+  }
+}
+
+// The partitioned solve over `nh` handles: nh = 1 with an NCCL communicator
+// (this rank's share, collectives through NCCL), or nh = nranks handles of an
+// in-process group (phases in rank order, group_exchange between them).
+void group_exchange(ps_handle* const* hs, int P, int k, cudaStream_t s);
+void dist_solve(ps_handle* const* hs, int nh, int64_t nrhs, const void* B, int64_t ldb, void* X, int64_t ldx,
+                int on_device, cudaStream_t s, std::vector<double2>& norms, int64_t& launches, float& ms) {
+  ps_handle* h0 = hs[0];
+  const int64_t N = h0->N, R = nrhs;
+  for (int i = 0; i < nh; ++i) get_dist_plan(hs[i], nrhs);
+  DistPlan& d0 = *h0->dplan;
+  const double2* Bd = (const double2*)B;
+  double2* Xd = (double2*)X;
+  int64_t ldb_d = ldb, ldx_d = ldx;
+  if (!on_device) {          // stage through d0.ws's TMP tail is not safe; use a dedicated buffer
+    if (d0.scratch.n < 2 * N * R) d0.scratch.alloc(std::max<int64_t>(2 * N * R, d0.scratch.n));
+    CK(cudaMemcpy2DAsync(d0.scratch.p, 16 * N, B, 16 * ldb, 16 * N, nrhs, cudaMemcpyHostToDevice, s));
+    Bd = d0.scratch.p;
+    Xd = d0.scratch.p + N * R;
+    ldb_d = ldx_d = N;
+  }
+  CK(cudaEventRecord(h0->ev0, s));
+  launches = 0;
+  for (int k = 0; k < 5; ++k) {
+    for (int i = 0; i < nh; ++i)
+      if (k < 4 || i == 0) launches += dist_phase(hs[i], *hs[i]->dplan, k, Bd, ldb_d, Xd, ldx_d, s);
+    if (k < 4) {
+      if (nh == 1) nccl_exchange(h0, d0, k, s);
+      else group_exchange(hs, nh, k, s);
+    }
+  }
+  CK(cudaEventRecord(h0->ev1, s));
+  CK(cudaGetLastError());
+  if (!on_device)
+    CK(cudaMemcpy2DAsync(X, 16 * ldx, Xd, 16 * N, 16 * N, nrhs, cudaMemcpyDeviceToHost, s));
+  norms.assign(R, double2{0.0, 0.0});
+  CK(cudaMemcpyAsync(norms.data(), d0.sums.p, 16 * R, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (auto& v : norms) v = double2{std::sqrt(v.x), std::sqrt(v.y)};
+  CK(cudaEventElapsedTime(&ms, h0->ev0, h0->ev1));
+  for (int i = 0; i < nh; ++i)
+    if (hs[i]->prof.on) hs[i]->prof.collect();
+}
+
+// In-process group (ps_solve_group): the same exchanges between the ranks'
+// workspaces on one device, summing in rank order.
+void group_exchange(ps_handle* const* hs, int P, int k, cudaStream_t s) {
+  const std::vector<Xchg> xs = dist_exchanges(hs[0], *hs[0]->dplan, k);
+  for (const Xchg& x : xs) {
+    if (x.count <= 0) continue;
+    const size_t bytes = sizeof(double2) * x.count;
+    auto at = [&](int g) { DistPlan& d = *hs[g]->dplan; return x.kind == 2 ? d.sums.p : d.ws.p + x.off; };
+    if (x.kind == 1) {
+      for (int src = 0; src < P; ++src)
+        for (int dst = 0; dst < P; ++dst)
+          if (dst != src)
+            CK(cudaMemcpyAsync(at(dst) + src * x.count, at(src) + src * x.count, bytes, cudaMemcpyDeviceToDevice, s));
+    } else {
+      double2* acc = hs[0]->dplan->scratch.p;
+      CK(cudaMemcpyAsync(acc, at(0), bytes, cudaMemcpyDeviceToDevice, s));
+      for (int g = 1; g < P; ++g) launch_add((double*)acc, (const double*)at(g), 2 * x.count, s);
+      for (int g = 0; g < P; ++g) CK(cudaMemcpyAsync(at(g), acc, bytes, cudaMemcpyDeviceToDevice, s));
+    }
+  }
+}
+
+}  // namespace
+
+namespace {
+ps_status finish_dist(ps_handle* const* hs, int nh, int64_t nrhs, const void* B, int64_t ldb, void* X,
+                      int64_t ldx, int on_device, void* cuda_stream, ps_report* rep, const char* who) {
+  ps_handle* h = hs[0];
+  try {
+    CK(cudaSetDevice(h->device));
+    cudaStream_t s = cuda_stream ? (cudaStream_t)cuda_stream : h->stream;
+    std::vector<double2> norms;
+    int64_t launches = 0;
+    float ms = 0;
+    dist_solve(hs, nh, nrhs, B, ldb, X, ldx, on_device, s, norms, launches, ms);
+    int ndiv = 0;
+    for (int64_t c = 0; c < nrhs; ++c) {
+      const double r = norms[c].x > 0 ? norms[c].y / norms[c].x : 0.0;
+      if (!(r < h->ratio_threshold)) ++ndiv;
+    }
+    if (rep) {
+      rep->t_solve_ms = ms;
+      rep->n_diverged = ndiv;
+      rep->bytes_moved = solve_bytes(h, nrhs);
+      rep->flops = solve_flops(h, nrhs);
+      rep->kernel_launches = launches;
+      const int64_t cap = std::min<int64_t>(rep->nrhs, nrhs);
+      for (int64_t c = 0; c < cap; ++c) {
+        if (rep->it0_norm) rep->it0_norm[c] = norms[c].x;
+        if (rep->it1_norm) rep->it1_norm[c] = norms[c].y;
+      }
+    }
+    if (ndiv > 0)
+      return fail(h, PS_EDIVERGED, std::string(who) + ": " + std::to_string(ndiv) + " of " + std::to_string(nrhs) +
+                                       " columns have ||it_1||/||it_0|| >= " + std::to_string(h->ratio_threshold));
+  } catch (const PsError& e) {
+    return fail(h, e.st, std::string(who) + ": " + e.msg);
+  } catch (const std::bad_alloc&) {
+    return fail(h, PS_ENOMEM, std::string(who) + ": host allocation failed");
+  }
+  return PS_OK;
+}
 }  // namespace
 
 // ======================================================================= C ABI
@@ -1231,13 +1838,22 @@ ps_status hm_load(const char* path, const ps_dist* dist, ps_handle** out) {
   if (!out) return fail(nullptr, PS_EINVAL, "hm_load: out is NULL");
   *out = nullptr;
   if (!path) return fail(nullptr, PS_EINVAL, "hm_load: path is NULL");
-  if (dist && (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks || dist->nccl_unique_id))
-    return fail(nullptr, PS_EINVAL, "hm_load: bad ps_dist (nccl_unique_id must be NULL in this version)");
+  if (dist && (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks ||
+               (dist->nccl_unique_id && !dist->partition)))
+    return fail(nullptr, PS_EINVAL, "hm_load: bad ps_dist (rank/nranks, or nccl_unique_id without partition)");
   std::unique_ptr<ps_handle> h(new ps_handle());
   try {
     std::vector<double2> near_arena, far_arena;
     read_file(h.get(), path, near_arena, far_arena);
     symbolic(h.get());
+    if (dist) {
+      h->rank = dist->rank;
+      h->nranks = dist->nranks;
+      if (dist->partition && dist->nranks > 1) {
+        h->part_mode = 1;
+        dist_layout(h.get());
+      }
+    }
     if (dist) {
       h->device = dist->device;
       CK(cudaSetDevice(h->device));
@@ -1267,7 +1883,15 @@ ps_status hm_load(const char* path, const ps_dist* dist, ps_handle** out) {
     h->d_e2rwg.upload(h->e2rwg, h->stream);
     h->d_e2mort.upload(h->e2mort, h->stream);
     h->d_m2e.upload(h->m2e, h->stream);
+    if (h->part_mode) h->d_d2rwg.upload(h->d2rwg, h->stream);
     CK(cudaStreamSynchronize(h->stream));
+    if (h->part_mode && dist->nccl_unique_id) {      // collective: every rank joins
+      ncclUniqueId id;
+      std::memcpy(&id, dist->nccl_unique_id, sizeof(id));
+      ncclComm_t comm;
+      NCK(nccl_api().commInitRank(&comm, h->nranks, id, h->rank));
+      h->nccl = comm;
+    }
   } catch (const PsError& e) {
     return fail(nullptr, e.st, "hm_load: " + e.msg);
   } catch (const std::bad_alloc&) {
@@ -1343,6 +1967,12 @@ ps_status ps_solve(ps_handle* h, int64_t nrhs, const void* B, int64_t ldb, void*
     const char* x1 = x0 + 16 * (ldx * (nrhs - 1) + h->N);
     if (b0 < x1 && x0 < b1) return fail(h, PS_EINVAL, "ps_solve: X overlaps B");
   }
+  if (h->part_mode) {
+    if (!h->nccl)
+      return fail(h, PS_ESTATE, "ps_solve: in-process row-partition handle (no NCCL id): use ps_solve_group");
+    ps_handle* hs[1] = {h};
+    return finish_dist(hs, 1, nrhs, B, ldb, X, ldx, on_device, cuda_stream, rep, "ps_solve");
+  }
   try {
     CK(cudaSetDevice(h->device));
     cudaStream_t s = cuda_stream ? (cudaStream_t)cuda_stream : h->stream;
@@ -1357,9 +1987,11 @@ ps_status ps_solve(ps_handle* h, int64_t nrhs, const void* B, int64_t ldb, void*
       ldb_d = N;
     }
     CK(cudaEventRecord(h->ev0, s));
+    // default: one launch per stage (measured faster on C2 than the single-launch
+    // program); PS_SOLVE=program selects the whole-solve dataflow program
     static const bool stages_env = [] {
       const char* e = std::getenv("PS_SOLVE");
-      return e && std::string(e) == "stages";
+      return !(e && std::string(e) == "program");
     }();
     double2* xres = sp.xt.p;   // where x ends up (elimination order)
     if (!stages_env) {
@@ -1528,6 +2160,58 @@ int64_t ps_trace_read(ps_handle* h, int64_t* out, int64_t cap_items) {
   return n;
 }
 
+ps_status ps_solve_group(ps_handle* const* hs, int nranks, int64_t nrhs, const void* B, int64_t ldb, void* X,
+                         int64_t ldx, void* cuda_stream, ps_report* rep) {
+  if (!hs || nranks < 2 || !hs[0]) return fail(nullptr, PS_EINVAL, "ps_solve_group: need nranks >= 2 handles");
+  ps_handle* h = hs[0];
+  for (int g = 0; g < nranks; ++g) {
+    if (!hs[g] || !hs[g]->part_mode || hs[g]->nccl || hs[g]->rank != g || hs[g]->nranks != nranks ||
+        hs[g]->N != h->N || hs[g]->device != h->device)
+      return fail(h, PS_EINVAL, "ps_solve_group: handles must be ranks 0..nranks-1 of one in-process row partition");
+    if (!hs[g]->setup_done) return fail(h, PS_ESTATE, "ps_solve_group: ps_setup has not run on every rank");
+  }
+  if (nrhs < 1 || !B || !X || ldb < h->N || ldx < h->N)
+    return fail(h, PS_EINVAL, "ps_solve_group: bad arguments (nrhs >= 1, B/X non-NULL, ldb/ldx >= N)");
+  return finish_dist(hs, nranks, nrhs, B, ldb, X, ldx, 1, cuda_stream, rep, "ps_solve_group");
+}
+
+ps_status ps_nccl_unique_id(void* out, int64_t cap) {
+  if (!out || cap < (int64_t)sizeof(ncclUniqueId)) return fail(nullptr, PS_EINVAL, "ps_nccl_unique_id: cap < 128");
+  try {
+    ncclUniqueId id;
+    NCK(nccl_api().getUniqueId(&id));
+    std::memcpy(out, &id, sizeof(id));
+  } catch (const PsError& e) {
+    return fail(nullptr, e.st, "ps_nccl_unique_id: " + e.msg);
+  }
+  return PS_OK;
+}
+
+int64_t ps_partition(const char* path, int nranks, int32_t* owner, int32_t* far_owner, int64_t cap) {
+  if (!path || !owner || !far_owner || nranks < 1) return -PS_EINVAL;
+  ps_handle h;
+  try {
+    std::vector<double2> near_arena, far_arena;
+    read_file(&h, path, near_arena, far_arena);
+    symbolic(&h);
+    if (cap < h.nl) {
+      g_err = "ps_partition: cap < n_leaves";
+      return -PS_EINVAL;
+    }
+    std::vector<int32_t> ow, fo;
+    partition(&h, nranks, ow, fo);
+    std::copy(ow.begin(), ow.end(), owner);
+    std::copy(fo.begin(), fo.end(), far_owner);
+  } catch (const PsError& e) {
+    g_err = "ps_partition: " + e.msg;
+    return -(int64_t)e.st;
+  } catch (const std::bad_alloc&) {
+    g_err = "ps_partition: host allocation failed";
+    return -PS_ENOMEM;
+  }
+  return h.nl;
+}
+
 int64_t ps_n(const ps_handle* h) { return h ? h->N : -1; }
 
 const char* ps_last_error(const ps_handle* h) {
@@ -1540,6 +2224,11 @@ void ps_free(ps_handle* h) {
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   h->plan.reset();
+  h->dplan.reset();
+  if (h->nccl) {
+    try { nccl_api().commDestroy((ncclComm_t)h->nccl); } catch (const PsError&) {}
+    h->nccl = nullptr;
+  }
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
   cudaStream_t s = h->stream;
@@ -1568,6 +2257,9 @@ int ps_info(const ps_handle* h, double* out, int n) {
   v[PS_INFO_DEPTH] = h->max_depth + 1;
   v[PS_INFO_SETUP_MADDS] = h->setup_madds;
   v[PS_INFO_SETUP_DONE] = h->setup_done ? 1 : 0;
+  v[PS_INFO_NRANKS] = h->part_mode ? h->nranks : 1;
+  v[PS_INFO_OWN_ROWS] = h->part_mode ? (double)h->own_rows : (double)h->N;
+  v[PS_INFO_SEP_ROWS] = h->part_mode ? (double)h->Nsep : 0.0;
   int m = std::min(n, (int)PS_INFO_COUNT);
   std::memcpy(out, v, sizeof(double) * m);
   return m;

@@ -104,10 +104,10 @@ void launch_inverse(int64_t nl, const int32_t* leaf_ids, const int32_t* sizes,
                     const double2* Wbase, double2* Dbase, int32_t* status, int max_n,
                     cudaStream_t st);
 
-// y[e*nrhs + c] = B[map[e] + c*ldb]   (gather rows of a column-major block)
+// y[e*nrhs + c] = B[map[e] + c*ldb]   (gather rows of a column-major block; map[e] < 0: 0)
 void launch_permute_in(int64_t N, int64_t nrhs, const int64_t* map, const double2* B, int64_t ldb,
                        double2* y, cudaStream_t st);
-// X[map[e] + c*ldx] = y[e*nrhs + c]
+// X[map[e] + c*ldx] = y[e*nrhs + c]   (rows with map[e] < 0 are skipped)
 void launch_permute_out(int64_t N, int64_t nrhs, const int64_t* map, const double2* y, double2* X,
                         int64_t ldx, cudaStream_t st);
 // dst[e*nrhs + c] = src[map[e]*nrhs + c]  (row permutation, row-major blocks)
@@ -119,9 +119,11 @@ void launch_combine_norms(int64_t N, int64_t nrhs, const double2* bo, const doub
 // part[chunk*nrhs + c] = (sum |bo|^2, sum |bo - xt|^2) over the chunk's rows
 void launch_norms2(int64_t N, int64_t nrhs, const double2* bo, const double2* xt, double2* part,
                    int64_t rows_per_chunk, cudaStream_t st);
-// norms[c] = (sqrt sum_chunks part.x, sqrt sum part.y)
+// norms[c] = (sqrt sum_chunks part.x, sqrt sum part.y); do_sqrt = 0: the sums themselves
 void launch_finalize_norms(int64_t nchunks, int64_t nrhs, const double2* part, double2* norms,
-                           cudaStream_t st);
+                           cudaStream_t st, int do_sqrt = 1);
+// dst[i] += src[i] (i < n), the in-process stand-in of a sum all-reduce (rank order fixed)
+void launch_add(double* dst, const double* src, int64_t n, cudaStream_t st);
 void launch_zero(double2* p, int64_t n, cudaStream_t st);
 
 }  // namespace ps

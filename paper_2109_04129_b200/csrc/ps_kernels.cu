@@ -836,7 +836,8 @@ __global__ void permute_in_kernel(int64_t N, int64_t nrhs, const int64_t* __rest
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / nrhs, c = e - r * nrhs;
-    y[e] = B[map[r] + c * ldb];
+    const int64_t m = map[r];
+    y[e] = m >= 0 ? B[m + c * ldb] : make_double2(0.0, 0.0);
   }
 }
 __global__ void permute_out_kernel(int64_t N, int64_t nrhs, const int64_t* __restrict__ map,
@@ -845,7 +846,8 @@ __global__ void permute_out_kernel(int64_t N, int64_t nrhs, const int64_t* __res
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / nrhs, c = e - r * nrhs;
-    X[map[r] + c * ldx] = y[e];
+    const int64_t m = map[r];
+    if (m >= 0) X[m + c * ldx] = y[e];
   }
 }
 __global__ void permute_rows_kernel(int64_t N, int64_t nrhs, const int64_t* __restrict__ map,
@@ -919,7 +921,7 @@ void launch_norms2(int64_t N, int64_t nrhs, const double2* bo, const double2* xt
 }
 
 __global__ void finalize_norms_kernel(int64_t nch, int64_t nrhs, const double2* __restrict__ part,
-                                      double2* __restrict__ norms) {
+                                      double2* __restrict__ norms, int do_sqrt) {
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= nrhs) return;
   double s0 = 0.0, s1 = 0.0;
@@ -928,7 +930,7 @@ __global__ void finalize_norms_kernel(int64_t nch, int64_t nrhs, const double2* 
     s0 += p.x;
     s1 += p.y;
   }
-  norms[c] = make_double2(sqrt(s0), sqrt(s1));
+  norms[c] = do_sqrt ? make_double2(sqrt(s0), sqrt(s1)) : make_double2(s0, s1);
 }
 void launch_combine_norms(int64_t N, int64_t nrhs, const double2* bo, const double2* u, double2* xt,
                           double2* part, int64_t rpc, cudaStream_t st) {
@@ -936,8 +938,16 @@ void launch_combine_norms(int64_t N, int64_t nrhs, const double2* bo, const doub
   combine_norms_kernel<<<g, 128, 0, st>>>(N, nrhs, bo, u, xt, part, rpc);
 }
 void launch_finalize_norms(int64_t nch, int64_t nrhs, const double2* part, double2* norms,
-                           cudaStream_t st) {
-  finalize_norms_kernel<<<(unsigned)((nrhs + 127) / 128), 128, 0, st>>>(nch, nrhs, part, norms);
+                           cudaStream_t st, int do_sqrt) {
+  finalize_norms_kernel<<<(unsigned)((nrhs + 127) / 128), 128, 0, st>>>(nch, nrhs, part, norms, do_sqrt);
+}
+
+__global__ void add_kernel(double* __restrict__ dst, const double* __restrict__ src, int64_t n) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    dst[e] += src[e];
+}
+void launch_add(double* dst, const double* src, int64_t n, cudaStream_t st) {
+  if (n > 0) add_kernel<<<grid_for(n), 256, 0, st>>>(dst, src, n);
 }
 
 __global__ void zero_kernel(double2* p, int64_t n) {
