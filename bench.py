@@ -48,38 +48,65 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled during the timed region:
+    one nvidia-smi process in loop mode (a sample every 20 ms), each line
+    time-stamped on arrival; mark() / stop() bracket the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int = 0):
         self.index = index
         self.samples = []
-        self._stop = threading.Event()
+        self._all = []
+        self._p = None
         self._t = None
+        self.t0 = self.t1 = None
 
-    def _run(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+    def _read(self):
+        for line in self._p.stdout:
+            if line.strip():
+                self._all.append((time.perf_counter(), [x.strip() for x in line.split(",")]))
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                        "--format=csv,noheader,nounits", "-lms", "20"],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+            t = time.perf_counter()
+            while not self._all and time.perf_counter() - t < 3.0:   # sampler is live
+                time.sleep(0.01)
+        except Exception:
+            self._p = None
         return self
 
+    def mark(self):
+        self.t0 = time.perf_counter()
+
+    def stop(self):
+        self.t1 = time.perf_counter()
+
     def __exit__(self, *a):
-        self._stop.set()
+        if self._p is None:
+            return
+        if self.t1 is None:
+            self.t1 = time.perf_counter()
+        time.sleep(0.05)
+        self._p.terminate()
+        try:
+            self._p.wait(timeout=10)
+        except Exception:
+            self._p.kill()
         if self._t:
-            self._t.join(timeout=10)
+            self._t.join(timeout=5)
+        t0 = self.t0 if self.t0 is not None else 0.0
+        inside = [v for (t, v) in self._all if t0 <= t <= self.t1]
+        if not inside and self._all:      # region shorter than one sample period: nearest sample
+            inside = [min(self._all, key=lambda tv: abs(tv[0] - 0.5 * (t0 + self.t1)))[1]]
+        self.samples = inside
 
     def summary(self):
         if not self.samples:
@@ -151,16 +178,21 @@ def run_reference(args):
 
 
 def _config(args, meta, nrhs, world):
-    return {"workload": f"{args.config}: {meta['desc']}", "N": meta["N"], "nrhs_per_gpu": nrhs,
-            "global_nrhs": nrhs * world, "n_leaves": meta["n_leaves"],
-            "parallelism": f"rhs-columns x{world} (replicated operator)",
+    rows = getattr(args, "mode", "cols") == "rows" and world > 1
+    return {"workload": f"{args.config}: {meta['desc']}", "N": meta["N"],
+            "nrhs_per_gpu": nrhs, "global_nrhs": nrhs if rows else (
+                nrhs * world if args.rhs_split == "weak" else args.nrhs or nrhs * world),
+            "n_leaves": meta["n_leaves"],
+            "parallelism": (f"row partition x{world} (elimination-tree subtrees per rank, replicated "
+                            f"separators; NCCL all-reduce of separator rows, all-gather of w and x)"
+                            if rows else f"rhs-columns x{world} (replicated operator)"),
             "l2": "operator (alpha panels + D^-1 + far factors) exceeds the 126 MB L2; no flush"}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2")
@@ -168,7 +200,12 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=2)
     ap.add_argument("--rhs-split", default="weak", choices=["weak", "strong"],
-                    help="weak: every rank solves the config's full RHS block; strong: the block is split")
+                    help="cols mode: weak = every rank solves the config's full RHS block; strong = the "
+                         "block is split")
+    ap.add_argument("--partition", default="auto", choices=["auto", "cols", "rows"],
+                    help="N > 1: cols = replicated operator, RHS columns per rank (no collective); rows = "
+                         "row partition of the operator over the ranks (NCCL exchanges, every rank solves "
+                         "the whole block: strong scaling); auto = cols when nrhs >= 16 N, else rows")
     args = ap.parse_args()
     warnings.simplefilter("ignore", RuntimeWarning)
     if args.impl == "reference":
@@ -194,11 +231,27 @@ def main():
             meta = load_or_generate(args.config)
     Bfull, _ = read_rhs(meta["rhs"])
     nrhs_global = args.nrhs or Bfull.shape[1]
-    B = np.asfortranarray(Bfull[:, :nrhs_global][:, column_slice(nrhs_global, world, rank, args.rhs_split)])
+    if nrhs_global > Bfull.shape[1]:        # more columns than the config's table: repeat it
+        Bfull = np.tile(Bfull, (1, -(-nrhs_global // Bfull.shape[1])))
+    mode = args.partition
+    if mode == "auto":
+        mode = "cols" if (world == 1 or nrhs_global >= 16 * world) else "rows"
+    args.mode = mode
+    if mode == "rows":
+        args.rhs_split = "strong"
+        B = np.asfortranarray(Bfull[:, :nrhs_global])
+    else:
+        B = np.asfortranarray(Bfull[:, :nrhs_global][:, column_slice(nrhs_global, world, rank, args.rhs_split)])
     nrhs = B.shape[1]
     N = meta["N"]
 
-    h = PsHandle(meta["hm"], device=local, rank=rank, nranks=world)
+    if mode == "rows" and world > 1:
+        from paper_2109_04129_b200 import nccl_unique_id
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        h = PsHandle(meta["hm"], device=local, rank=rank, nranks=world, partition=True, nccl_id=obj[0])
+    else:
+        h = PsHandle(meta["hm"], device=local, rank=rank, nranks=world)
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
@@ -218,11 +271,13 @@ def main():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+        clk.mark()
         e0.record(st)
         for _ in range(args.steps):
             _, rep = h.solve(Bd, Xd, stream=st, want_norms=False)
         e1.record(st)
         torch.cuda.synchronize()
+        clk.stop()
         if world > 1:
             dist.barrier()
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, dist, "cuda")
@@ -280,7 +335,7 @@ def main():
                               "gflop_per_step": prof[c]["flops"] / args.profile_steps / 1e9}
                           for c in prof}}
 
-    total_cols = nrhs * world if args.rhs_split == "weak" else nrhs_global
+    total_cols = nrhs * world if (mode == "cols" and args.rhs_split == "weak") else nrhs_global
     value = N * total_cols / (ms * 1e-3)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,

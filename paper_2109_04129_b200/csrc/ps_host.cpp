@@ -148,6 +148,18 @@ struct Prof {
   }
 };
 
+// Tuning knobs (environment, read once; defaults are the measured choices).
+int env_int(const char* name, int def) {
+  const char* e = std::getenv(name);
+  return (e && *e) ? std::atoi(e) : def;
+}
+
+// split-K chunk (k-steps) of the narrow (small nrhs, operator-streaming) tiles
+int NARROW_STEPS() {
+  static const int v = env_int("PS_NARROW_STEPS", 16);
+  return v;
+}
+
 // A gather-GEMM table: tasks, segments, work items and batches (one launch each).
 constexpr int CHUNK_STEPS = 16;    // target k-steps (of GM_KC) per split-K work item
 
@@ -166,10 +178,17 @@ struct Table {
   int64_t n_slots = 0;
   int chunk_steps = CHUNK_STEPS;
   int narrow = 0;          // 1: 64 x 8 tiles (small nrhs)
+  double2* S = nullptr;    // scratch vector base of osel / bsel offsets (chain stages)
   // optional global ordering of work items (ticket order): key = key_base + nt * key_stagger,
   // stable-sorted by sort_by_key() (valid when every dependency has a smaller key)
   double key_base = 0, key_stagger = 0;
   std::vector<double> keys;
+  std::vector<double> task_key;      // key_base of every task at creation
+  // early_keys: a chunk is keyed just after the latest of its producers' tasks
+  // (not at its own task's key), so a gather's bulk chunks enter the ticket
+  // order as soon as their inputs can exist; the critical chunk (which adds the
+  // group sum) keeps the task's key. Every item still follows its producers.
+  bool early_keys = false;
   void sort_by_key() {
     std::vector<int64_t> idx(work.size());
     std::iota(idx.begin(), idx.end(), 0);
@@ -191,13 +210,14 @@ struct Table {
     t.t0 = t.t1 = (int32_t)terms.size();
     t.K = 0;
     t.unit0 = 0; t.n_mt = (m + GM_MT - 1) / GM_MT;
-    t.a_kmajor = 0; t.b_kmajor = 0; t.idep = -1;
+    t.a_kmajor = 0; t.b_kmajor = 0; t.idep = -1; t.osel = 0;
     tasks.push_back(t);
+    task_key.push_back(key_base);
     return (int32_t)tasks.size() - 1;
   }
   // append a K-segment: A(i,k) = A[oA + k sAk + i sAi], B(k,c) = B[oB + k sBk + c sBc]
   void add_term(int32_t task, int64_t oA, int64_t sAi, int64_t sAk, int64_t oB, int64_t sBk,
-                int64_t sBc, int K, int32_t dep = -1) {
+                int64_t sBc, int K, int32_t dep = -1, int32_t bsel = 0) {
     if (task != (int32_t)tasks.size() - 1)
       throw PsError{PS_ECUDA, "internal: terms must be added to the newest task"};
     if (K <= 0) return;
@@ -209,7 +229,7 @@ struct Table {
     GTerm g;
     g.oA = oA; g.sAi = sAi; g.sAk = sAk;
     g.oB = oB; g.sBk = sBk; g.sBc = sBc;
-    g.kstart = t.K; g.K = K; g.dep = dep; g.pad = 0;
+    g.kstart = t.K; g.K = K; g.dep = dep; g.bsel = bsel;
     terms.push_back(g);
     t.K += K;
     t.t1 = (int32_t)terms.size();
@@ -252,7 +272,11 @@ struct Table {
   // the others); the NEAR - 1 segments next to it (the next-latest
   // dependencies) become single-segment chunks in subgroups of their own, the
   // bulk is chunked normally and combined in subgroups of SUBG.
-  static constexpr int NEAR = 4, SUBG = 16;
+  static inline const int NEAR = env_int("PS_NEAR", 4), SUBG = env_int("PS_SUBG", 16);
+  // segments in the critical chunk: the chain predecessor AND the one before it,
+  // so the group sum the critical chunk adds never waits on a just-finished
+  // producer (its latest input is >= 2 hops old)
+  static inline const int CRITSEG = env_int("PS_CRITSEG", 2);
   void tile(int32_t task, int isolate = 0, int steps = 0) {
     if (steps <= 0) steps = chunk_steps;
     GTask& t = tasks[task];
@@ -271,16 +295,21 @@ struct Table {
     const int nseg = t.t1 - t.t0;
     int32_t crit = -1;
     if (isolate != 0 && nseg >= 2) {
-      const int nnear = std::min(NEAR - 1, nseg - 1);
+      const int cs = std::max(1, std::min(CRITSEG, nseg - 1));       // segments in the critical chunk
+      const int nnear = std::max(0, std::min(NEAR - 1, nseg - cs));
+      auto add_one = [&](int32_t s0, int32_t s1) {                    // one chunk, however long
+        chunk_range(s0, s1, ch, 1 << 20);
+        single.resize(ch.size(), 1);
+      };
       if (isolate > 0) {
-        add(t.t0, t.t0 + 1, true);                                   // critical
-        for (int q = 1; q <= nnear; ++q) add(t.t0 + q, t.t0 + q + 1, true);
-        add(t.t0 + 1 + nnear, t.t1, false);
+        add_one(t.t0, t.t0 + cs);                                    // critical
+        for (int q = 0; q < nnear; ++q) add(t.t0 + cs + q, t.t0 + cs + q + 1, true);
+        add(t.t0 + cs + nnear, t.t1, false);
         crit = 0;
       } else {
-        add(t.t0, t.t1 - 1 - nnear, false);
-        for (int q = nnear; q >= 1; --q) add(t.t1 - 1 - q, t.t1 - q, true);
-        add(t.t1 - 1, t.t1, true);                                   // critical
+        add(t.t0, t.t1 - cs - nnear, false);
+        for (int q = nnear - 1; q >= 0; --q) add(t.t1 - cs - 1 - q, t.t1 - cs - q, true);
+        add_one(t.t1 - cs, t.t1);                                    // critical
         crit = (int32_t)ch.size() - 1;
       }
     } else {
@@ -319,7 +348,15 @@ struct Table {
           const int sg = sub_of[c];
           work.push_back({task, a, b, ch[c][2], ch[c][3], ch[c][0], ch[c][1], c, nch, tile_id, crit,
                           sg, sg >= 0 ? sub_r0[sg] : 0, sg >= 0 ? sub_r1[sg] : 0, nsub, 0, slot});
-          keys.push_back(key_base + b * key_stagger);
+          double k = key_base;
+          if (early_keys && c != crit) {
+            double kp = -1.0;
+            for (int32_t q = ch[c][2]; q < ch[c][3]; ++q)
+              if (terms[q].dep >= 0) kp = std::max(kp, task_key[terms[q].dep]);
+            if (t.idep >= 0) kp = std::max(kp, task_key[t.idep]);
+            k = std::min(key_base, kp + 0.5);
+          }
+          keys.push_back(k + b * key_stagger);
         };
         for (int c = 0; c < nch; ++c)
           if (c != crit) push(c);
@@ -356,7 +393,7 @@ struct Table {
     fa.nwork = bt.nw;
     fa.tasks = d_tasks.p;
     fa.terms = d_terms.p;
-    fa.O = O; fa.I = I; fa.A = A; fa.B = B;
+    fa.O = O; fa.I = I; fa.A = A; fa.B = B; fa.S = S;
     fa.counters = d_counters.p;
     fa.n_units = n_units;
     fa.pad = 0;
@@ -399,7 +436,7 @@ struct SolvePlan {
   Table prog;                              // the whole two-term solve as one dataflow program
   DevBuf<double2> ws;                      // program workspace: Y BO W Z XT X TMP (offsets below)
   int64_t oY = 0, oBO = 0, oW = 0, oZ = 0, oXT = 0, oX = 0, oTMP = 0;
-  DevBuf<double2> y, bo, w, u, xt, wm, tm, part, norms, stage;
+  DevBuf<double2> y, bo, w, u, xt, wm, tm, part, norms, stage, sc;
   int64_t nchunks = 0, rpc = 64;
   int64_t launches_per_solve = 0;
 };
@@ -447,6 +484,20 @@ struct ps_handle {
   int64_t stack_len = 0;
   double setup_madds = 0;
   int64_t alpha_blocks = 0;
+  // ---- elimination-tree chains: maximal paths p_1 -> ... -> p_L
+  // (p_{i+1} = parent(p_i) with p_i its only child), cut into pieces of at most
+  // PS_TMAX unknowns. A piece with L >= 2 has T_c = (I - A_c^T)^{-1}, A_c the
+  // strictly upper block matrix of its internal alpha blocks (U_c x U_c,
+  // column-major, in the T region of the operator arena), so each sweep over
+  // the piece is one parallel block product instead of L dependent hops.
+  std::vector<int32_t> chain_of;                 // per position
+  std::vector<std::vector<int32_t>> chains;      // positions p_1..p_L, bottom to top
+  std::vector<int64_t> ch_U, ch_Toff;            // unknowns; offset of T_c (-1: L = 1)
+  std::vector<int64_t> cpos;                     // per position: first row inside its chain
+  std::vector<int32_t> ch_height, ch_depth;
+  int max_ch_height = 0, max_ch_depth = 0;
+  int64_t Tlen = 0, Tbase = 0;
+  bool use_chains = true;
   // near block lookup: (leaf a, leaf b) -> index into near_list
   std::unordered_map<uint64_t, int64_t> near_idx;
   // ---- device ----
@@ -654,6 +705,73 @@ void symbolic(ps_handle* h) {
   h->Wlen = W;
   h->Plen = P;
   h->Dlen = D;
+  // chains of the elimination tree (see ps_handle), bottom-up by position
+  {
+    const int64_t tmax = env_int("PS_TMAX", 2048);
+    h->use_chains = env_int("PS_CHAINS", 1) != 0;
+    std::vector<int32_t> nch(nl, 0);
+    for (int64_t p = 0; p < nl; ++p)
+      if (h->parent[p] >= 0) ++nch[h->parent[p]];
+    h->chain_of.assign(nl, -1);
+    h->cpos.assign(nl, 0);
+    h->chains.clear();
+    h->ch_U.clear();
+    for (int64_t p = 0; p < nl; ++p) {
+      if (h->chain_of[p] >= 0) continue;
+      std::vector<int32_t> c{(int32_t)p};
+      int64_t U = h->nsz[p];
+      int32_t q = (int32_t)p;
+      while (h->parent[q] >= 0 && nch[h->parent[q]] == 1 && h->chain_of[h->parent[q]] < 0 &&
+             U + h->nsz[h->parent[q]] <= tmax) {
+        q = h->parent[q];
+        h->cpos[q] = U;
+        U += h->nsz[q];
+        c.push_back(q);
+      }
+      static const int cmin = env_int("PS_CHAIN_MIN", 2);
+      if ((int)c.size() < cmin) {                   // too short to pay for a T_c: single nodes
+        for (int32_t x : c) {
+          h->chain_of[x] = (int32_t)h->chains.size();
+          h->cpos[x] = 0;
+          h->chains.push_back({x});
+          h->ch_U.push_back(h->nsz[x]);
+        }
+        continue;
+      }
+      const int32_t id = (int32_t)h->chains.size();
+      for (int32_t x : c) h->chain_of[x] = id;
+      h->chains.push_back(std::move(c));
+      h->ch_U.push_back(U);
+    }
+    const int64_t nc = (int64_t)h->chains.size();
+    h->ch_Toff.assign(nc, -1);
+    h->Tlen = 0;
+    for (int64_t c = 0; c < nc; ++c)
+      if (h->chains[c].size() >= 2) {
+        h->ch_Toff[c] = h->Tlen;
+        h->Tlen += h->ch_U[c] * h->ch_U[c];
+      }
+    // chain-graph levels: the parent of a piece's top is the first node of another piece
+    std::vector<int32_t> order(nc);
+    std::iota(order.begin(), order.end(), 0);
+    std::sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return h->chains[x].back() < h->chains[y].back(); });
+    h->ch_height.assign(nc, 0);
+    h->ch_depth.assign(nc, 0);
+    for (int32_t c : order) {
+      const int32_t up = h->parent[h->chains[c].back()];
+      if (up >= 0) h->ch_height[h->chain_of[up]] = std::max(h->ch_height[h->chain_of[up]], h->ch_height[c] + 1);
+    }
+    for (auto it = order.rbegin(); it != order.rend(); ++it) {
+      const int32_t up = h->parent[h->chains[*it].back()];
+      if (up >= 0) h->ch_depth[*it] = h->ch_depth[h->chain_of[up]] + 1;
+    }
+    h->max_ch_height = h->max_ch_depth = 0;
+    for (int64_t c = 0; c < nc; ++c) {
+      h->max_ch_height = std::max(h->max_ch_height, h->ch_height[c]);
+      h->max_ch_depth = std::max(h->max_ch_depth, h->ch_depth[c]);
+    }
+    if (!h->use_chains) h->Tlen = 0;
+  }
   // unknown maps
   h->e2mort.resize(h->N);
   h->e2rwg.resize(h->N);
@@ -963,6 +1081,201 @@ void build_setup_plan(ps_handle* h, SetupPlan& sp) {
   }
 }
 
+// T_c = (I - A_c^T)^{-1} of every chain piece with L >= 2 (see ps_handle): the
+// forward sweep (Eq. 24) restricted to the piece, applied to the identity:
+//   X_i = delta_i + sum_{k < i, p_i in struct(p_k)} alpha_{p_k p_i}^T X_k,
+// row block i of T_c = X_i (columns beyond the diagonal block stay 0). One
+// dataflow launch; pieces are independent, hops within a piece are ordered.
+void chain_setup(ps_handle* h, cudaStream_t s) {
+  if (h->Tlen == 0) return;
+  CK(cudaMemsetAsync(h->d_op.p + h->Tbase, 0, sizeof(double2) * h->Tlen, s));
+  std::vector<int64_t> ones;
+  Table Tt;
+  std::vector<int32_t> tk(h->nl, -1);
+  const int64_t Tb = h->Tbase, Pb = h->Pbase;
+  for (size_t c = 0; c < h->chains.size(); ++c) {
+    if (h->ch_Toff[c] < 0) continue;
+    const int64_t U = h->ch_U[c], To = Tb + h->ch_Toff[c];
+    for (int64_t i = 0; i < U; ++i) ones.push_back(To + i + i * U);
+    for (int32_t p : h->chains[c]) {
+      const int64_t np_ = h->nsz[p], cp = h->cpos[p];
+      int32_t t = Tt.add_task(To + cp, 1, U, To + cp, 1, U, (int)np_, (int)(cp + np_), +1);
+      for (auto [d, idx] : h->gath[p]) {
+        if (h->chain_of[d] != (int32_t)c) continue;
+        const int64_t nd = h->nsz[d];
+        Tt.add_term(t, Pb + h->Poff[d] + h->pcol[d][idx] * nd, nd, 1, To + h->cpos[d], 1, U, (int)nd, tk[d]);
+      }
+      Tt.tile(t, -1, 8);
+      tk[p] = t;
+    }
+  }
+  Tt.close_batch();
+  Tt.upload(s);
+  DevBuf<int64_t> d_ones;
+  d_ones.upload(ones, s);
+  launch_set_ones(h->d_op.p, d_ones.p, (int64_t)ones.size(), s);
+  Tt.launch_all(h->d_op.p, h->d_op.p, h->d_op.p, h->d_op.p, s);
+  CK(cudaStreamSynchronize(s));
+}
+
+// Chain-aware sweeps. Pieces are processed in chain-graph order
+// (forward: by chain height; backward: by chain depth). A single-node piece is
+// an ordinary gather task. A piece with L >= 2 is two stages:
+//   forward   E_i: e_{p_i} = y_{p_i} + sum_{d outside} alpha_{d p_i}^T y_d   (-> scratch)
+//             Y_i: y_{p_i} = sum_{j <= i} T_c[i, j] e_{p_j}
+//   backward  F_i: f_{p_i} = v_{p_i} + sum_{j outside} alpha_{p_i j} w_j      (-> scratch)
+//             W_i: w_{p_i} = sum_{j >= i} T_c[j, i]^T f_{p_j}
+// so a piece costs 2 dependent hops instead of L. Exact reformulation of
+// Eqs. 24 / 26: T_c is the piece's product of the elementary factors (Eq. 15).
+void build_chain_sweeps(ps_handle* h, SolvePlan& sp, int64_t R, int narrow, int resident) {
+  const int64_t nl = h->nl, nc = (int64_t)h->chains.size();
+  const int64_t Pb = h->Pbase, Tb = h->Tbase;
+  sp.fwd.S = sp.bwd.S = sp.sc.p;
+  sp.fwd.early_keys = sp.bwd.early_keys = env_int("PS_EARLY", 1) != 0;
+  // split-K chunk size per stage: ~ipc items per resident CTA, clamped to
+  // [2, maxs] k-steps (a stage lasts as long as its longest item)
+  static const int maxs = env_int("PS_SWEEP_MAXSTEPS", 16), ipc = env_int("PS_SWEEP_IPC", 2);
+  auto steps_of = [&](const std::vector<std::pair<int64_t, int64_t>>& mk) {   // (m, K) of a stage's tasks
+    if (narrow) return NARROW_STEPS();
+    double ks = 0;
+    for (auto [m, K] : mk) ks += std::ceil((double)m / GM_MT) * std::ceil((double)R / GM_NT) * std::ceil((double)K / GM_KC);
+    return std::max(2, std::min(maxs, (int)std::ceil(ks / ((double)ipc * resident))));
+  };
+  // ticket order: (stage + column tile * stagger), so the column tiles enter the
+  // stage sequence staggered and the window of fetched items holds ready work
+  static const int stag_pct = env_int("PS_STAGGER", 0);
+  const int nnt = (int)((R + (narrow ? GN_NT : GM_NT) - 1) / (narrow ? GN_NT : GM_NT));
+  const double nst_f = 2.0 * (h->max_ch_height + 1), nst_b = 2.0 * (h->max_ch_depth + 1);
+  sp.fwd.key_stagger = nnt > 1 ? 0.01 * stag_pct * nst_f / nnt : 0.0;
+  sp.bwd.key_stagger = nnt > 1 ? 0.01 * stag_pct * nst_b / nnt : 0.0;
+  double stage = 0;
+  auto by_height = [&](const std::vector<std::pair<int32_t, int32_t>>& gl) {
+    auto v = gl;
+    std::stable_sort(v.begin(), v.end(), [&](const std::pair<int32_t, int32_t>& x, const std::pair<int32_t, int32_t>& y) {
+      return h->height[x.first] < h->height[y.first];
+    });
+    return v;
+  };
+  std::vector<std::vector<int32_t>> lev_f(h->max_ch_height + 1), lev_b(h->max_ch_depth + 1);
+  for (int64_t c = 0; c < nc; ++c) {
+    lev_f[h->ch_height[c]].push_back((int32_t)c);
+    lev_b[h->ch_depth[c]].push_back((int32_t)c);
+  }
+  // ---- forward sweep (in place on v; e in scratch) ----
+  std::vector<int32_t> yt(nl, -1), et(nl, -1);
+  for (const auto& cl : lev_f) {
+    std::vector<std::pair<int64_t, int64_t>> mk;
+    for (int32_t c : cl)
+      for (int32_t p : h->chains[c]) {
+        int64_t K = 0;
+        for (auto [d, idx] : h->gath[p])
+          if (h->chain_of[d] != c) K += h->nsz[d];
+        mk.push_back({h->nsz[p], K});
+      }
+    const int stpE = steps_of(mk);
+    sp.fwd.key_base = stage++;
+    for (int32_t c : cl) {
+      const bool single = h->chains[c].size() == 1;
+      for (int32_t p : h->chains[c]) {
+        std::vector<std::pair<int32_t, int32_t>> gl;
+        for (auto [d, idx] : h->gath[p])
+          if (h->chain_of[d] != c) gl.push_back({d, idx});
+        if (single && gl.empty()) continue;          // y_p = b_p: nothing to do
+        const int64_t np_ = h->nsz[p];
+        int32_t t = sp.fwd.add_task(h->eoff[p] * R, R, 1, h->eoff[p] * R, R, 1, (int)np_, (int)R, +1);
+        if (!single) sp.fwd.tasks[t].osel = 1;        // e_p -> scratch
+        for (auto [d, idx] : by_height(gl)) {
+          const int64_t nd = h->nsz[d];
+          sp.fwd.add_term(t, Pb + h->Poff[d] + h->pcol[d][idx] * nd, nd, 1, h->eoff[d] * R, R, 1, (int)nd, yt[d]);
+        }
+        sp.fwd.tile(t, -1, stpE);
+        (single ? yt : et)[p] = t;
+      }
+    }
+    mk.clear();
+    for (int32_t c : cl)
+      if (h->chains[c].size() > 1)
+        for (int32_t p : h->chains[c]) mk.push_back({h->nsz[p], h->cpos[p]});
+    const int stpY = steps_of(mk);
+    sp.fwd.key_base = stage++;
+    for (int32_t c : cl) {
+      if (h->chains[c].size() == 1) continue;
+      const int64_t U = h->ch_U[c], To = Tb + h->ch_Toff[c];
+      for (size_t i = 0; i < h->chains[c].size(); ++i) {
+        const int32_t p = h->chains[c][i];
+        const int64_t np_ = h->nsz[p];
+        int32_t t = sp.fwd.add_task(h->eoff[p] * R, R, 1, h->eoff[p] * R, R, 1, (int)np_, (int)R, +1);
+        sp.fwd.tasks[t].osel = 2;                     // init e_p (T_c[i, i] = I) from scratch
+        sp.fwd.tasks[t].idep = et[p];
+        for (size_t j = 0; j < i; ++j) {
+          const int32_t q = h->chains[c][j];
+          sp.fwd.add_term(t, To + h->cpos[p] + h->cpos[q] * U, 1, U, h->eoff[q] * R, R, 1, (int)h->nsz[q], et[q], 1);
+        }
+        sp.fwd.tile(t, 0, stpY);
+        yt[p] = t;
+      }
+    }
+  }
+  sp.fwd.sort_by_key();
+  sp.fwd.close_batch();
+  stage = 0;
+  // ---- backward sweep (O = out, I = in, B = out; f in scratch) ----
+  std::vector<int32_t> wt(nl, -1), ft(nl, -1);
+  for (const auto& cl : lev_b) {
+    std::vector<std::pair<int64_t, int64_t>> mk;
+    for (int32_t c : cl)
+      for (int32_t p : h->chains[c]) {
+        int64_t K = 0;
+        for (int32_t j : h->st[p])
+          if (h->chain_of[j] != c) K += h->nsz[j];
+        mk.push_back({h->nsz[p], K});
+      }
+    const int stpF = steps_of(mk);
+    sp.bwd.key_base = stage++;
+    for (int32_t c : cl) {
+      const bool single = h->chains[c].size() == 1;
+      for (int32_t p : h->chains[c]) {
+        const int64_t np_ = h->nsz[p];
+        int32_t t = sp.bwd.add_task(h->eoff[p] * R, R, 1, h->eoff[p] * R, R, 1, (int)np_, (int)R, +1);
+        if (!single) sp.bwd.tasks[t].osel = 1;        // f_p -> scratch
+        for (size_t i = 0; i < h->st[p].size(); ++i) {
+          const int32_t j = h->st[p][i];
+          if (h->chain_of[j] == c) continue;
+          sp.bwd.add_term(t, Pb + h->Poff[p] + h->pcol[p][i] * np_, 1, np_, h->eoff[j] * R, R, 1, (int)h->nsz[j], wt[j]);
+        }
+        sp.bwd.tile(t, +1, stpF);
+        (single ? wt : ft)[p] = t;
+      }
+    }
+    mk.clear();
+    for (int32_t c : cl)
+      if (h->chains[c].size() > 1)
+        for (int32_t p : h->chains[c]) mk.push_back({h->nsz[p], h->ch_U[c] - h->cpos[p] - h->nsz[p]});
+    const int stpW = steps_of(mk);
+    sp.bwd.key_base = stage++;
+    for (int32_t c : cl) {
+      if (h->chains[c].size() == 1) continue;
+      const int64_t U = h->ch_U[c], To = Tb + h->ch_Toff[c];
+      const auto& ch = h->chains[c];
+      for (size_t i = 0; i < ch.size(); ++i) {
+        const int32_t p = ch[i];
+        const int64_t np_ = h->nsz[p];
+        int32_t t = sp.bwd.add_task(h->eoff[p] * R, R, 1, h->eoff[p] * R, R, 1, (int)np_, (int)R, +1);
+        sp.bwd.tasks[t].osel = 2;                     // init f_p (T_c[i, i] = I) from scratch
+        sp.bwd.tasks[t].idep = ft[p];
+        for (size_t j = i + 1; j < ch.size(); ++j) {  // T_c[j, i]^T: A(r, k) = T_c[cpos_j + k + (cpos_i + r) U]
+          const int32_t q = ch[j];
+          sp.bwd.add_term(t, To + h->cpos[q] + h->cpos[p] * U, U, 1, h->eoff[q] * R, R, 1, (int)h->nsz[q], ft[q], 1);
+        }
+        sp.bwd.tile(t, 0, stpW);
+        wt[p] = t;
+      }
+    }
+  }
+  sp.bwd.sort_by_key();
+  sp.bwd.close_batch();
+}
+
 // ------------------------------------------------------------------ solve plan
 void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
   const int64_t nl = h->nl;
@@ -976,10 +1289,12 @@ void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
     byd[h->depth[p]].push_back((int32_t)p);
   }
   const int narrow = (R <= 8) ? 1 : 0;
+  if (h->use_chains) sp.sc.alloc(h->N * R);        // chain-stage scratch (e / f)
   for (Table* tb : {&sp.fwd, &sp.bwd, &sp.dinv, &sp.far1, &sp.far2}) {
     tb->narrow = narrow;
-    if (narrow) tb->chunk_steps = 4;
+    if (narrow) tb->chunk_steps = NARROW_STEPS();
   }
+  if (!narrow) sp.far1.chunk_steps = sp.far2.chunk_steps = env_int("PS_FAR_STEPS", CHUNK_STEPS);
   std::vector<int32_t> ftask(nl, -1), btask(nl, -1);
   // narrow levels (the separator chains) get small split-K chunks so each hop
   // waits on ~1-4 k-steps; wide levels keep large chunks (less overhead)
@@ -989,7 +1304,7 @@ void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
   // (less per-item overhead). Narrow tiles stream the operator: short chunks.
   const int resident = flow_resident_ctas();
   auto steps_for = [&](const std::vector<int32_t>& lev_nodes, bool fwd) {
-    if (narrow) return 4;
+    if (narrow) return NARROW_STEPS();
     double ks = 0;
     const int MTw = GM_MT, NTw = GM_NT;
     for (int32_t p : lev_nodes) {
@@ -1001,45 +1316,60 @@ void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
     const int st = (int)std::ceil(ks / (2.0 * resident));
     return std::max(4, std::min(32, st));
   };
-  for (int lev = 0; lev <= h->max_height; ++lev) {
-    const int stp = steps_for(byh[lev], true);
-    for (int32_t q : byh[lev]) {
-      if (h->gath[q].empty()) continue;
-      const int64_t nq = h->nsz[q];
-      int32_t t = sp.fwd.add_task(h->eoff[q] * R, R, 1, h->eoff[q] * R, R, 1, (int)nq, (int)R, +1);
-      // segments in producer completion order (height), so the chained prefix
-      // accumulation follows readiness; the last one (the chain child) is isolated
-      auto gl = h->gath[q];
-      std::stable_sort(gl.begin(), gl.end(), [&](const std::pair<int32_t, int32_t>& x,
-                                                 const std::pair<int32_t, int32_t>& y) {
-        return h->height[x.first] < h->height[y.first];
-      });
-      for (auto [d, idx] : gl) {
-        const int64_t nd = h->nsz[d];
-        sp.fwd.add_term(t, h->Poff[d] + h->pcol[d][idx] * nd, nd, 1, h->eoff[d] * R, R, 1, (int)nd,
-                        ftask[d]);
+  // wide levels (enough tiles to fill the machine without split-K): no critical-chunk
+  // isolation and long chunks (PS_WIDE = tiles per resident CTA in percent, 0 = off)
+  const int wide_pct = env_int("PS_WIDE", 0), wide_steps = env_int("PS_WIDE_STEPS", 32);
+  auto is_wide = [&](const std::vector<int32_t>& nodes) {
+    if (wide_pct <= 0 || narrow) return false;
+    double tiles = 0;
+    for (int32_t p : nodes) tiles += std::ceil((double)h->nsz[p] / GM_MT) * std::ceil((double)R / GM_NT);
+    return tiles * 100.0 >= (double)wide_pct * resident;
+  };
+  if (h->use_chains) {
+    build_chain_sweeps(h, sp, R, narrow, resident);
+  } else {
+    for (int lev = 0; lev <= h->max_height; ++lev) {
+      const bool wide = is_wide(byh[lev]);
+      const int stp = wide ? wide_steps : steps_for(byh[lev], true);
+      for (int32_t q : byh[lev]) {
+        if (h->gath[q].empty()) continue;
+        const int64_t nq = h->nsz[q];
+        int32_t t = sp.fwd.add_task(h->eoff[q] * R, R, 1, h->eoff[q] * R, R, 1, (int)nq, (int)R, +1);
+        // segments in producer completion order (height), so the chained prefix
+        // accumulation follows readiness; the last one (the chain child) is isolated
+        auto gl = h->gath[q];
+        std::stable_sort(gl.begin(), gl.end(), [&](const std::pair<int32_t, int32_t>& x,
+                                                   const std::pair<int32_t, int32_t>& y) {
+          return h->height[x.first] < h->height[y.first];
+        });
+        for (auto [d, idx] : gl) {
+          const int64_t nd = h->nsz[d];
+          sp.fwd.add_term(t, h->Poff[d] + h->pcol[d][idx] * nd, nd, 1, h->eoff[d] * R, R, 1, (int)nd,
+                          ftask[d]);
+        }
+        sp.fwd.tile(t, wide ? 0 : -1, stp);
+        ftask[q] = t;
       }
-      sp.fwd.tile(t, -1, stp);
-      ftask[q] = t;
     }
-  }
-  sp.fwd.close_batch();
-  // backward sweep (Eq. 26), ordered by depth: w_p = v_p + sum_j alpha_pj w_j
-  for (int lev = 0; lev <= h->max_depth; ++lev) {
-    const int stp = steps_for(byd[lev], false);
-    for (int32_t p : byd[lev]) {
-      const int64_t np_ = h->nsz[p];
-      int32_t t = sp.bwd.add_task(h->eoff[p] * R, R, 1, h->eoff[p] * R, R, 1, (int)np_, (int)R, +1);
-      for (size_t i = 0; i < h->st[p].size(); ++i) {
-        const int32_t j = h->st[p][i];
-        sp.bwd.add_term(t, h->Poff[p] + h->pcol[p][i] * np_, 1, np_, h->eoff[j] * R, R, 1,
-                        (int)h->nsz[j], btask[j]);
+    sp.fwd.close_batch();
+    // backward sweep (Eq. 26), ordered by depth: w_p = v_p + sum_j alpha_pj w_j
+    for (int lev = 0; lev <= h->max_depth; ++lev) {
+      const bool wide = is_wide(byd[lev]);
+      const int stp = wide ? wide_steps : steps_for(byd[lev], false);
+      for (int32_t p : byd[lev]) {
+        const int64_t np_ = h->nsz[p];
+        int32_t t = sp.bwd.add_task(h->eoff[p] * R, R, 1, h->eoff[p] * R, R, 1, (int)np_, (int)R, +1);
+        for (size_t i = 0; i < h->st[p].size(); ++i) {
+          const int32_t j = h->st[p][i];
+          sp.bwd.add_term(t, h->Poff[p] + h->pcol[p][i] * np_, 1, np_, h->eoff[j] * R, R, 1,
+                          (int)h->nsz[j], btask[j]);
+        }
+        sp.bwd.tile(t, wide ? 0 : +1, stp);
+        btask[p] = t;
       }
-      sp.bwd.tile(t, +1, stp);
-      btask[p] = t;
     }
+    sp.bwd.close_batch();
   }
-  sp.bwd.close_batch();
   // D^{-1} (Eq. 32), one batch
   for (int64_t p = 0; p < nl; ++p) {
     const int64_t np_ = h->nsz[p];
@@ -1130,7 +1460,7 @@ void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
   const int64_t nl = h->nl;
   Table& P = sp.prog;
   P.narrow = (R <= 8) ? 1 : 0;
-  if (P.narrow) P.chunk_steps = 4;
+  if (P.narrow) P.chunk_steps = NARROW_STEPS();
   const int64_t NR = h->N * R;
   sp.oY = 0; sp.oBO = NR; sp.oW = 2 * NR; sp.oZ = 3 * NR; sp.oXT = 4 * NR; sp.oX = 5 * NR; sp.oTMP = 6 * NR;
   const int64_t ncl = (int64_t)h->cl_start.size();
@@ -1144,7 +1474,7 @@ void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
   }
   const int resident = flow_resident_ctas();
   auto steps_for = [&](const std::vector<int32_t>& nodes, bool fwd) {
-    if (P.narrow) return 4;
+    if (P.narrow) return NARROW_STEPS();
     double ks = 0;
     for (int32_t p : nodes) {
       double K = 0;
@@ -1455,7 +1785,7 @@ void build_dist_plan(ps_handle* h, DistPlan& dp, int64_t R) {
   for (Table* tb : {&dp.fwdIA, &dp.fwdSA, &dp.dinvA, &dp.bwdA, &dp.far1, &dp.far2, &dp.fwdIC, &dp.fwdSC,
                     &dp.dinvC, &dp.bwdC}) {
     tb->narrow = narrow;
-    if (narrow) tb->chunk_steps = 4;
+    if (narrow) tb->chunk_steps = NARROW_STEPS();
   }
   auto mine = [&](int64_t p) { return h->owner[p] == g; };
   auto sep = [&](int64_t p) { return h->owner[p] < 0; };
@@ -1466,7 +1796,7 @@ void build_dist_plan(ps_handle* h, DistPlan& dp, int64_t R) {
   }
   const int resident = flow_resident_ctas();
   auto steps_for = [&](const std::vector<int32_t>& nodes, bool fwd) {
-    if (narrow) return 4;
+    if (narrow) return NARROW_STEPS();
     double ks = 0;
     for (int32_t p : nodes) {
       if (!(mine(p) || sep(p))) continue;
@@ -1872,7 +2202,8 @@ ps_status hm_load(const char* path, const ps_dist* dist, ps_handle** out) {
       h->Pbase = 0;
       h->Dbase = h->Plen;
       h->Fbase = h->Plen + h->Dlen;
-      h->d_op.alloc(h->Fbase + (int64_t)stacked.size());
+      h->Tbase = h->Fbase + (int64_t)stacked.size();
+      h->d_op.alloc(h->Tbase + h->Tlen);
       h->d_P.p = h->d_op.p + h->Pbase;
       h->d_D.p = h->d_op.p + h->Dbase;
       h->d_far.p = h->d_op.p + h->Fbase;
@@ -1942,6 +2273,7 @@ ps_status ps_setup(ps_handle* h, const ps_setup_opts* opts) {
       sp.panel.launch(lev, h->d_P.p, nullptr, h->d_D.p, h->d_W.p, s);
     }
     CK(cudaGetLastError());
+    chain_setup(h, s);
     CK(cudaStreamSynchronize(s));
     h->d_W.release();
     h->d_near.release();

@@ -23,6 +23,8 @@ struct GTask {
   int32_t a_kmajor;        // 1: A's unit stride is along k (transposed views), 0: along i
   int32_t b_kmajor;        // 1: B's unit stride is along k, 0: along c
   int32_t idep;            // task (same launch) producing the init rows I; -1: none
+  int32_t osel;            // bit 0: O offsets address the scratch base S instead of O;
+                           // bit 1: I offsets address S instead of I
 };
 
 // A segment of a task's K dimension: K_s consecutive k's starting at virtual
@@ -33,7 +35,7 @@ struct GTerm {
   int64_t sAi, sAk, sBk, sBc;
   int32_t kstart, K;
   int32_t dep;             // task (same launch) producing this segment's B rows; -1: none
-  int32_t pad;
+  int32_t bsel;            // 1: oB addresses the scratch base S instead of B
 };
 
 // One CTA-sized piece of work: output tile (mt, nt) of `task`, virtual k in
@@ -70,6 +72,7 @@ struct FlowArgs {
   const double2* I;
   const double2* A;
   const double2* B;
+  double2* S;              // scratch vector base (chain stages of the sweeps)
   int32_t* counters;       // [0] ticket, [1 .. 1+n_units) done, then arrive[n_tiles]
   int32_t n_units;
   int32_t pad;
@@ -125,5 +128,7 @@ void launch_finalize_norms(int64_t nchunks, int64_t nrhs, const double2* part, d
 // dst[i] += src[i] (i < n), the in-process stand-in of a sum all-reduce (rank order fixed)
 void launch_add(double* dst, const double* src, int64_t n, cudaStream_t st);
 void launch_zero(double2* p, int64_t n, cudaStream_t st);
+// base[offs[e]] = 1 (e < n): identity diagonals of the chain matrices T_c
+void launch_set_ones(double2* base, const int64_t* offs, int64_t n, cudaStream_t st);
 
 }  // namespace ps

@@ -69,7 +69,7 @@ __device__ __forceinline__ int ld_acquire(const int32_t* p) {
 // segment list at item start), so k-steps run densely across segments.
 struct KTab {
   int64_t kA[GM_CHUNK_K];
-  int64_t kB[GM_CHUNK_K];
+  const double2* kB[GM_CHUNK_K];     // absolute row pointer of B (base B or scratch S)
   int32_t kSi[GM_CHUNK_K];
   int32_t kSc[GM_CHUNK_K];
 };
@@ -123,7 +123,7 @@ __device__ __forceinline__ void issue_b(const KTab& kt, int k0, int klen, int c0
     if (b_km) { k = e & (KC - 1); c = e / KC; } else { c = e % NT; k = e / NT; }
     const int kk = k0 + k;
     const bool v = (c < nn && kk < klen);
-    const double2* src = v ? Bb + kt.kB[kk] + (int64_t)(c0 + c) * kt.kSc[kk] : Bb;
+    const double2* src = v ? kt.kB[kk] + (int64_t)(c0 + c) * kt.kSc[kk] : Bb;
     cp_async16(Bs + k * NT + c, src, v);
   }
 }
@@ -235,6 +235,25 @@ __device__ __forceinline__ bool splitk_combine(const FlowArgs& a, const GWork& w
   return false;
 }
 
+// Wait (warp 0) until every producer task of this item's B rows (and of its
+// init rows) has completed column tile w.nt. A producer with fewer columns than
+// the consumer (chain setup: T row blocks widen up the chain) has no tile w.nt:
+// the consumer's extra columns read zeros nobody writes, so there is no wait.
+__device__ __forceinline__ void wait_dep_task(const FlowArgs& a, int dep, int nt) {
+  const GTask& P = a.tasks[dep];
+  const int NTw = a.narrow ? GN_NT : GM_NT;
+  if (nt * NTw >= P.n) return;
+  const int32_t* flag = a.counters + 1 + P.unit0 + nt;
+  while (ld_acquire(flag) < P.n_mt) __nanosleep(32);
+}
+__device__ __forceinline__ void wait_deps(const FlowArgs& a, const GWork& w, const GTask& T, int tid) {
+  if (tid == 0 && T.idep >= 0) wait_dep_task(a, T.idep, w.nt);
+  for (int t = w.ta + tid; t < w.tb; t += 32) {
+    const int dep = a.terms[t].dep;
+    if (dep >= 0) wait_dep_task(a, dep, w.nt);
+  }
+}
+
 // Critical chunk: wait until the tile's non-critical group sum is published
 // (top counter == nsub + 1). Never waits on a later ticket.
 __device__ __forceinline__ void wait_group_sum(const FlowArgs& a, const GWork& w, int tid) {
@@ -290,7 +309,7 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
 #pragma unroll
       for (int r = 0; r < RM; ++r)
         if (rbase + r < mm) {
-          const double2 z = __ldcg(a.I + T.oI + (int64_t)(i0 + rbase + r) * T.sIi + (int64_t)(c0 + col) * T.sIc);
+          const double2 z = __ldcg(((T.osel & 2) ? (const double2*)a.S : a.I) + T.oI + (int64_t)(i0 + rbase + r) * T.sIi + (int64_t)(c0 + col) * T.sIc);
           acc[r].x += sgn * z.x;
           acc[r].y += sgn * z.y;
         }
@@ -298,21 +317,7 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
   };
   if (T.idep < 0) load_init();
   // ---- wait for the producers of B (warp 0, one segment per lane) ----
-  if (tid < 32) {
-    if (tid == 0 && T.idep >= 0) {          // producer of the init rows
-      const int32_t need = a.tasks[T.idep].n_mt;
-      const int32_t* flag = done + a.tasks[T.idep].unit0 + w.nt;
-      while (ld_acquire(flag) < need) __nanosleep(32);
-    }
-    for (int t = w.ta + tid; t < w.tb; t += 32) {
-      const int dep = a.terms[t].dep;
-      if (dep >= 0) {
-        const int32_t need = a.tasks[dep].n_mt;
-        const int32_t* flag = done + a.tasks[dep].unit0 + w.nt;
-        while (ld_acquire(flag) < need) __nanosleep(32);
-      }
-    }
-  }
+  if (tid < 32) wait_deps(a, w, T, tid);
   __syncthreads();
   if (T.idep >= 0) load_init();
   if (tr) tr[3] = gtimer();
@@ -363,7 +368,7 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
         const int i = rbase + r;
         if (i < mm) {
           const double2 v = make_double2(sgn * acc[r].x, sgn * acc[r].y);   // O = I + sign * sum
-          __stcg(a.O + T.oO + (int64_t)(i0 + i) * T.sOi + (int64_t)(c0 + col) * T.sOc, v);
+          __stcg(((T.osel & 1) ? a.S : a.O) + T.oO + (int64_t)(i0 + i) * T.sOi + (int64_t)(c0 + col) * T.sOc, v);
         }
       }
     }
@@ -381,17 +386,28 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-// Wide tile on FP64 tensor cores: MT8 = ceil(rows / 8) <= 4 row tiles of 8;
-// warp w computes column tile w (8 columns) for all row tiles; a complex
-// product is 4 real DMMAs fed by one 16-byte shared load per fragment element.
-template <int MT8>
+// Wide tile on the FP64 tensor cores (mma.sync m8n8k4 f64; tcgen05 has no f64
+// kind). 8 warps = 2 k-halves x 4 column groups: warp (kh, wc) computes rows
+// [0, 8 MT) x columns [16 wc, 16 wc + 16) over k rows [8 kh, 8 kh + 8) of every
+// KC = 16 stage; the two k-halves are summed through shared memory at the end
+// (fixed order: kh 0 + kh 1). A complex k4-step is 4 real DMMAs per 8x8 block
+// (re += Ar Br, im += Ar Bi, then re += (-Ai) Bi, im += Ai Br: dependent
+// MMAs are MT*NT*2 instructions apart). One 16-byte shared load per lane per
+// fragment (A[g][q], B[q][g] as (re, im)); per k4 a warp loads MT + 2
+// fragments for 8 MT DMMAs, so the L1/shared pipe is no longer the bound it is
+// for the DFMA tile.
+__device__ __forceinline__ double dneg(double x) { return __longlong_as_double(__double_as_longlong(x) ^ (1ll << 63)); }
+
+template <int MT>
 __device__ __forceinline__ void item_body_dmma(const FlowArgs& a, const GWork& w, const GTask& T,
                                                const KTab& kt, double2* As0, double2* Bs0, int tid,
                                                int lane, int warp, int* s_last, int64_t* tr) {
+  constexpr int NT = 2;
   const int i0 = w.mt * GM_MT, c0 = w.nt * GM_NT;
   const int mm = min(GM_MT, T.m - i0), nn = min(GM_NT, T.n - c0);
   const int klen = w.kb - w.ka;
   const int g = lane >> 2, q = lane & 3;
+  const int kh = warp >> 2, wc = warp & 3;
   int32_t* done = a.counters + 1;
   const bool a_km = T.a_kmajor != 0, b_km = T.b_kmajor != 0;
   const int nsteps = (klen + KC - 1) / KC;
@@ -399,48 +415,85 @@ __device__ __forceinline__ void item_body_dmma(const FlowArgs& a, const GWork& w
   for (int s = 0; s < NSTAGE - 1; ++s)
     if (s < nsteps) issue_a<GM_MT, GM_NT>(kt, s * KC, klen, i0, mm, a_km, a.A, tid, As0 + s * STAGE_A);
   cp_commit();
-  if (tid < 32) {
-    if (tid == 0 && T.idep >= 0) {          // producer of the init rows
-      const int32_t need = a.tasks[T.idep].n_mt;
-      const int32_t* flag = done + a.tasks[T.idep].unit0 + w.nt;
-      while (ld_acquire(flag) < need) __nanosleep(32);
-    }
-    for (int t = w.ta + tid; t < w.tb; t += 32) {
-      const int dep = a.terms[t].dep;
-      if (dep >= 0) {
-        const int32_t need = a.tasks[dep].n_mt;
-        const int32_t* flag = done + a.tasks[dep].unit0 + w.nt;
-        while (ld_acquire(flag) < need) __nanosleep(32);
-      }
+  const double sgn = (double)T.sign;
+  const bool crit_fin = (w.nchunks > 1 && w.crit >= 0 && w.chunk == w.crit);
+  const bool owns_init = (w.nchunks == 1) || (w.crit >= 0 ? w.chunk == w.crit : w.chunk == 0);
+  // accumulators: block (m, n) rows m*8+g, columns 16 wc + 8 n + 2 q + {0, 1}
+  double cre[MT][NT][2], cim[MT][NT][2];
+#pragma unroll
+  for (int m = 0; m < MT; ++m)
+#pragma unroll
+    for (int n = 0; n < NT; ++n) cre[m][n][0] = cre[m][n][1] = cim[m][n][0] = cim[m][n][1] = 0.0;
+  auto tile_off = [&](int m, int n, int e) { return (m * 8 + g) * GM_NT + 16 * wc + 8 * n + 2 * q + e; };
+  if (crit_fin) {
+    wait_group_sum(a, w, tid);
+    if (kh == 0) {
+      const double2* Gs = a.partial + (w.slot + w.crit) * (int64_t)(GM_MT * GM_NT);
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int n = 0; n < NT; ++n)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const double2 v = __ldcg(Gs + tile_off(m, n, e));
+            cre[m][n][e] = v.x;
+            cim[m][n][e] = v.y;
+          }
     }
   }
+  auto load_init = [&]() {
+    if (!(owns_init && T.oI >= 0 && kh == 0)) return;
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+      for (int n = 0; n < NT; ++n)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int i = m * 8 + g, c = 16 * wc + 8 * n + 2 * q + e;
+          if (i < mm && c < nn) {
+            const double2 z = __ldcg(((T.osel & 2) ? (const double2*)a.S : a.I) + T.oI + (int64_t)(i0 + i) * T.sIi + (int64_t)(c0 + c) * T.sIc);
+            cre[m][n][e] += sgn * z.x;
+            cim[m][n][e] += sgn * z.y;
+          }
+        }
+  };
+  if (T.idep < 0) load_init();
+  if (tid < 32) wait_deps(a, w, T, tid);
   __syncthreads();
+  if (T.idep >= 0) load_init();
   if (tr) tr[3] = gtimer();
 #pragma unroll
   for (int s = 0; s < NSTAGE - 1; ++s) {
     if (s < nsteps) issue_b<GM_MT, GM_NT>(kt, s * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + s * STAGE_B);
     cp_commit();
   }
-  double cre[MT8][2], cim[MT8][2];
-#pragma unroll
-  for (int m = 0; m < MT8; ++m) cre[m][0] = cre[m][1] = cim[m][0] = cim[m][1] = 0.0;
   for (int s = 0; s < nsteps; ++s) {
     cp_wait<NSTAGE - 2>();
     __syncthreads();
     const int st = s % NSTAGE;
-    const double2* As = As0 + st * STAGE_A + q * GM_MT + g;
-    const double2* Bs = Bs0 + st * STAGE_B + q * GM_NT + warp * 8 + g;
+    const double2* As = As0 + st * STAGE_A + (8 * kh + q) * GM_MT + g;
+    const double2* Bs = Bs0 + st * STAGE_B + (8 * kh + q) * GM_NT + 16 * wc + g;
 #pragma unroll
-    for (int kk = 0; kk < KC / 4; ++kk) {
-      const double2 b = Bs[kk * 4 * GM_NT];
+    for (int kk = 0; kk < 2; ++kk) {
+      double2 av[MT], bv[NT];
 #pragma unroll
-      for (int m = 0; m < MT8; ++m) {
-        const double2 av = As[kk * 4 * GM_MT + m * 8];
-        dmma(cre[m][0], cre[m][1], av.x, b.x);
-        dmma(cre[m][0], cre[m][1], -av.y, b.y);
-        dmma(cim[m][0], cim[m][1], av.x, b.y);
-        dmma(cim[m][0], cim[m][1], av.y, b.x);
-      }
+      for (int m = 0; m < MT; ++m) av[m] = As[kk * 4 * GM_MT + m * 8];
+#pragma unroll
+      for (int n = 0; n < NT; ++n) bv[n] = Bs[kk * 4 * GM_NT + n * 8];
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          dmma(cre[m][n][0], cre[m][n][1], av[m].x, bv[n].x);
+          dmma(cim[m][n][0], cim[m][n][1], av[m].x, bv[n].y);
+        }
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          dmma(cre[m][n][0], cre[m][n][1], dneg(av[m].y), bv[n].y);
+          dmma(cim[m][n][0], cim[m][n][1], av[m].y, bv[n].x);
+        }
     }
     const int sn = s + NSTAGE - 1;
     if (sn < nsteps) {
@@ -453,39 +506,54 @@ __device__ __forceinline__ void item_body_dmma(const FlowArgs& a, const GWork& w
   cp_wait<0>();
   __syncthreads();
   if (tr) tr[4] = gtimer();
-  double2 acc[2 * MT8];
-  int off[2 * MT8];
-  bool own[2 * MT8];
-  const int colb = warp * 8 + 2 * q;
+  // k-half reduction through shared memory (stage buffers are free now)
+  double2* red = As0;      // 32 x 64 complex = 32 KB <= NSTAGE * (STAGE_A + STAGE_B)
+  if (kh == 1) {
 #pragma unroll
-  for (int m = 0; m < MT8; ++m)
+    for (int m = 0; m < MT; ++m)
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      acc[2 * m + e] = make_double2(cre[m][e], cim[m][e]);
-      off[2 * m + e] = (m * 8 + g) * GM_NT + colb + e;
-      own[2 * m + e] = true;
-    }
-  const bool finalize = splitk_combine<2 * MT8>(a, w, acc, off, own, tid, s_last);
-  if (finalize) {
-    const double sg = (double)T.sign;
+      for (int n = 0; n < NT; ++n)
 #pragma unroll
-    for (int m = 0; m < MT8; ++m) {
-      const int i = m * 8 + g;
-      if (i < mm) {
+        for (int e = 0; e < 2; ++e) red[tile_off(m, n, e)] = make_double2(cre[m][n][e], cim[m][n][e]);
+  }
+  __syncthreads();
+  constexpr int E = MT * NT * 2;
+  double2 acc[E];
+  int off[E];
+  bool own[E];
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int col = colb + e;
-          if (col < nn) {
-            double2 v = make_double2(sg * acc[2 * m + e].x, sg * acc[2 * m + e].y);
-            if (T.oI >= 0) {
-              const double2 z = __ldcg(a.I + T.oI + (int64_t)(i0 + i) * T.sIi + (int64_t)(c0 + col) * T.sIc);
-              v.x += z.x;
-              v.y += z.y;
-            }
-            __stcg(a.O + T.oO + (int64_t)(i0 + i) * T.sOi + (int64_t)(c0 + col) * T.sOc, v);
-          }
+  for (int m = 0; m < MT; ++m)
+#pragma unroll
+    for (int n = 0; n < NT; ++n)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int x = (m * NT + n) * 2 + e;
+        off[x] = tile_off(m, n, e);
+        own[x] = (kh == 0);
+        if (kh == 0) {
+          const double2 v = red[off[x]];
+          acc[x] = make_double2(cre[m][n][e] + v.x, cim[m][n][e] + v.y);
+        } else {
+          acc[x] = make_double2(0.0, 0.0);
         }
       }
+  __syncthreads();          // red (= stage buffers) free again before the next item / partial reads
+  const bool finalize = crit_fin ? true : splitk_combine<E>(a, w, acc, off, own, tid, s_last);
+  if (finalize) {
+    if (kh == 0) {
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int n = 0; n < NT; ++n)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int i = m * 8 + g, c = 16 * wc + 8 * n + 2 * q + e;
+            if (i < mm && c < nn) {
+              const double2 v = acc[(m * NT + n) * 2 + e];
+              __stcg(((T.osel & 1) ? a.S : a.O) + T.oO + (int64_t)(i0 + i) * T.sOi + (int64_t)(c0 + c) * T.sOc,
+                     make_double2(sgn * v.x, sgn * v.y));      // O = I + sign * sum
+            }
+          }
     }
     __syncthreads();
     if (tid == 0) red_release(done + T.unit0 + w.nt, 1);
@@ -524,28 +592,14 @@ __device__ __forceinline__ void item_body_narrow(const FlowArgs& a, const GWork&
 #pragma unroll
       for (int e = 0; e < 2; ++e)
         if (cb + e < nn) {
-          const double2 z = __ldcg(a.I + T.oI + (int64_t)(i0 + row) * T.sIi + (int64_t)(c0 + cb + e) * T.sIc);
+          const double2 z = __ldcg(((T.osel & 2) ? (const double2*)a.S : a.I) + T.oI + (int64_t)(i0 + row) * T.sIi + (int64_t)(c0 + cb + e) * T.sIc);
           acc[e].x += sgn * z.x;
           acc[e].y += sgn * z.y;
         }
     }
   };
   if (T.idep < 0) load_init();
-  if (tid < 32) {
-    if (tid == 0 && T.idep >= 0) {          // producer of the init rows
-      const int32_t need = a.tasks[T.idep].n_mt;
-      const int32_t* flag = done + a.tasks[T.idep].unit0 + w.nt;
-      while (ld_acquire(flag) < need) __nanosleep(32);
-    }
-    for (int t = w.ta + tid; t < w.tb; t += 32) {
-      const int dep = a.terms[t].dep;
-      if (dep >= 0) {
-        const int32_t need = a.tasks[dep].n_mt;
-        const int32_t* flag = done + a.tasks[dep].unit0 + w.nt;
-        while (ld_acquire(flag) < need) __nanosleep(32);
-      }
-    }
-  }
+  if (tid < 32) wait_deps(a, w, T, tid);
   __syncthreads();
   if (T.idep >= 0) load_init();
   if (tr) tr[3] = gtimer();
@@ -590,7 +644,7 @@ __device__ __forceinline__ void item_body_narrow(const FlowArgs& a, const GWork&
         const int col = cb + e;
         if (col < nn) {
           const double2 v = make_double2(sgn * acc[e].x, sgn * acc[e].y);   // O = I + sign * sum
-          __stcg(a.O + T.oO + (int64_t)(i0 + row) * T.sOi + (int64_t)(c0 + col) * T.sOc, v);
+          __stcg(((T.osel & 1) ? a.S : a.O) + T.oO + (int64_t)(i0 + row) * T.sOi + (int64_t)(c0 + col) * T.sOc, v);
         }
       }
     }
@@ -641,7 +695,7 @@ flow_kernel(const FlowArgs a) {
       for (int k = lo; k < hi; ++k) {
         const int64_t d = k - g.kstart;
         kt.kA[k - w.ka] = g.oA + d * g.sAk;
-        kt.kB[k - w.ka] = g.oB + d * g.sBk;
+        kt.kB[k - w.ka] = (g.bsel ? a.S : a.B) + g.oB + d * g.sBk;
         kt.kSi[k - w.ka] = (int32_t)g.sAi;
         kt.kSc[k - w.ka] = (int32_t)g.sBc;
       }
@@ -940,6 +994,14 @@ void launch_combine_norms(int64_t N, int64_t nrhs, const double2* bo, const doub
 void launch_finalize_norms(int64_t nch, int64_t nrhs, const double2* part, double2* norms,
                            cudaStream_t st, int do_sqrt) {
   finalize_norms_kernel<<<(unsigned)((nrhs + 127) / 128), 128, 0, st>>>(nch, nrhs, part, norms, do_sqrt);
+}
+
+__global__ void set_ones_kernel(double2* __restrict__ base, const int64_t* __restrict__ offs, int64_t n) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    base[offs[e]] = make_double2(1.0, 0.0);
+}
+void launch_set_ones(double2* base, const int64_t* offs, int64_t n, cudaStream_t st) {
+  if (n > 0) set_ones_kernel<<<grid_for(n), 256, 0, st>>>(base, offs, n);
 }
 
 __global__ void add_kernel(double* __restrict__ dst, const double* __restrict__ src, int64_t n) {
