@@ -62,9 +62,10 @@ def load_library():
     from .build import build, nvcc_available
     if nvcc_available():
         build(force=bool(os.environ.get("PS_REBUILD")))     # no-op unless sources are newer
-    if not os.path.exists(_SO):
-        raise ImportError(f"libps.so not found at {_SO}; run `python -m paper_2109_04129_b200.build`")
-    L = ctypes.CDLL(_SO)
+    so = os.environ.get("PS_LIB", _SO)         # A/B experiments with alternative builds
+    if not os.path.exists(so):
+        raise ImportError(f"libps.so not found at {so}; run `python -m paper_2109_04129_b200.build`")
+    L = ctypes.CDLL(so)
     P, I64, I, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
     L.hm_load.restype = I
     L.hm_load.argtypes = [ctypes.c_char_p, ctypes.POINTER(_Dist), ctypes.POINTER(ctypes.c_void_p)]
