@@ -179,6 +179,7 @@ struct Table {
   int chunk_steps = CHUNK_STEPS;
   int narrow = 0;          // 1: 64 x 8 tiles (small nrhs)
   double2* S = nullptr;    // scratch vector base of osel / bsel offsets (chain stages)
+  int mma = 0;             // wide-tile consumer: 0 DFMA, 1 FP64 mma.sync (DMMA)
   // optional global ordering of work items (ticket order): key = key_base + nt * key_stagger,
   // stable-sorted by sort_by_key() (valid when every dependency has a smaller key)
   double key_base = 0, key_stagger = 0;
@@ -400,11 +401,15 @@ struct Table {
     fa.partial = d_partial.p;
     fa.trace = nullptr;
     fa.narrow = narrow;
+    // consumer: PS_MMA=dmma / dfma forces one for every table, else the table's own
+    // choice (far-field tables: FP64 tensor cores; sweeps / D^-1 / setup: DFMA)
     static const int mma_env = [] {
       const char* e = std::getenv("PS_MMA");
-      return (e && std::string(e) == "dmma") ? 1 : 0;
+      if (e && std::string(e) == "dmma") return 1;
+      if (e && std::string(e) == "dfma") return 0;
+      return -1;
     }();
-    fa.mma = mma_env;
+    fa.mma = mma_env >= 0 ? mma_env : mma;
     if (pf && pf->trace_on && cls == pf->trace_cls) {
       pf->trace_buf.alloc(6 * bt.nw);
       fa.trace = pf->trace_buf.p;
@@ -1294,7 +1299,10 @@ void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
     tb->narrow = narrow;
     if (narrow) tb->chunk_steps = NARROW_STEPS();
   }
-  if (!narrow) sp.far1.chunk_steps = sp.far2.chunk_steps = env_int("PS_FAR_STEPS", CHUNK_STEPS);
+  if (!narrow) {
+    sp.far1.chunk_steps = sp.far2.chunk_steps = env_int("PS_FAR_STEPS", 32);
+    sp.far1.mma = sp.far2.mma = env_int("PS_FAR_MMA", 1);
+  }
   std::vector<int32_t> ftask(nl, -1), btask(nl, -1);
   // narrow levels (the separator chains) get small split-K chunks so each hop
   // waits on ~1-4 k-steps; wide levels keep large chunks (less overhead)
