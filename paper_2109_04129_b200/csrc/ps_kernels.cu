@@ -18,6 +18,7 @@
 #include "ps_internal.h"
 
 #include <cstdio>
+#include <cstdlib>
 
 namespace ps {
 
@@ -154,7 +155,15 @@ constexpr size_t FLOW_SMEM = (size_t)NSTAGE * (STAGE_A + STAGE_B) * sizeof(doubl
 // Returns true when the caller must finalise with acc.
 
 
-template <int E>
+// CTA barrier of the compute threads: the whole CTA, or (warp-specialised
+// kernel) the 8 compute warps only — the scheduler warp never joins it.
+template <bool WS>
+__device__ __forceinline__ void bsync() {
+  if constexpr (WS) asm volatile("bar.sync 5, 256;" ::: "memory");
+  else __syncthreads();
+}
+
+template <int E, bool WS = false>
 __device__ __forceinline__ bool splitk_combine(const FlowArgs& a, const GWork& w, double2 (&acc)[E],
                                                const int (&off)[E], const bool (&own)[E], int tid,
                                                int* s_flag) {
@@ -166,7 +175,7 @@ __device__ __forceinline__ bool splitk_combine(const FlowArgs& a, const GWork& w
   if (crit_mode && w.chunk == w.crit) {
     if (tid == 0)
       while (ld_acquire(ctr) < nsub + 1) __nanosleep(32);
-    __syncthreads();
+    bsync<WS>();
     const double2* Gs = a.partial + (w.slot + w.crit) * TS;
 #pragma unroll
     for (int e = 0; e < E; ++e)
@@ -184,9 +193,9 @@ __device__ __forceinline__ bool splitk_combine(const FlowArgs& a, const GWork& w
 #pragma unroll
   for (int e = 0; e < E; ++e)
     if (own[e]) __stcg(P + off[e], acc[e]);
-  __syncthreads();
+  bsync<WS>();
   if (tid == 0) *s_flag = (atom_acq_rel(ctr + 1 + sg, 1) == (r1 - r0) - 1);
-  __syncthreads();
+  bsync<WS>();
   if (!*s_flag) return false;
   // last of its subgroup: sum the members in rank order (loads batched)
 #pragma unroll
@@ -206,9 +215,9 @@ __device__ __forceinline__ bool splitk_combine(const FlowArgs& a, const GWork& w
 #pragma unroll
     for (int e = 0; e < E; ++e)
       if (own[e]) __stcg(S + off[e], acc[e]);
-    __syncthreads();
+    bsync<WS>();
     if (tid == 0) *s_flag = (atom_acq_rel(ctr, 1) == nsub - 1);
-    __syncthreads();
+    bsync<WS>();
     if (!*s_flag) return false;
 #pragma unroll
     for (int e = 0; e < E; ++e) acc[e] = make_double2(0.0, 0.0);
@@ -230,7 +239,7 @@ __device__ __forceinline__ bool splitk_combine(const FlowArgs& a, const GWork& w
 #pragma unroll
   for (int e = 0; e < E; ++e)
     if (own[e]) __stcg(Gs + off[e], acc[e]);
-  __syncthreads();
+  bsync<WS>();
   if (tid == 0) red_release(ctr, 1);          // top reaches nsub + 1: group sum published
   return false;
 }
@@ -563,9 +572,10 @@ __device__ __forceinline__ void item_body_dmma(const FlowArgs& a, const GWork& w
 // Narrow tile (small nrhs): 64 rows x 8 columns; thread t owns row t % 64 and
 // columns 2 (t / 64) + {0, 1}. The operator panel is streamed through the same
 // cp.async ring (HBM-bound regime), B values are warp broadcasts.
+template <bool WS>
 __device__ __forceinline__ void item_body_narrow(const FlowArgs& a, const GWork& w, const GTask& T,
                                                  const KTab& kt, double2* As0, double2* Bs0, int tid,
-                                                 int* s_last, int64_t* tr) {
+                                                 int* s_last, int64_t* tr, int sa, int sb) {
   const int i0 = w.mt * GN_MT, c0 = w.nt * GN_NT;
   const int mm = min(GN_MT, T.m - i0), nn = min(GN_NT, T.n - c0);
   const int klen = w.kb - w.ka;
@@ -575,14 +585,14 @@ __device__ __forceinline__ void item_body_narrow(const FlowArgs& a, const GWork&
   const int nsteps = (klen + KC - 1) / KC;
 #pragma unroll
   for (int s = 0; s < NSTAGE - 1; ++s)
-    if (s < nsteps) issue_a<GN_MT, GN_NT>(kt, s * KC, klen, i0, mm, a_km, a.A, tid, As0 + s * STAGE_A);
+    if (s < nsteps) issue_a<GN_MT, GN_NT>(kt, s * KC, klen, i0, mm, a_km, a.A, tid, As0 + s * sa);
   cp_commit();
   const double sgn = (double)T.sign;
   const bool crit_fin = (w.nchunks > 1 && w.crit >= 0 && w.chunk == w.crit);
   const bool owns_init = (w.nchunks == 1) || (w.crit >= 0 ? w.chunk == w.crit : w.chunk == 0);
   double2 acc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
   if (crit_fin) {
-    wait_group_sum(a, w, tid);
+    if constexpr (!WS) wait_group_sum(a, w, tid);
     const double2* Gs = a.partial + (w.slot + w.crit) * (int64_t)(GM_MT * GM_NT);
     acc[0] = __ldcg(Gs + row * GN_NT + cb);
     acc[1] = __ldcg(Gs + row * GN_NT + cb + 1);
@@ -599,23 +609,25 @@ __device__ __forceinline__ void item_body_narrow(const FlowArgs& a, const GWork&
     }
   };
   if (T.idep < 0) load_init();
-  if (tid < 32) wait_deps(a, w, T, tid);
-  __syncthreads();
+  if constexpr (!WS) {                     // the scheduler warp waited already
+    if (tid < 32) wait_deps(a, w, T, tid);
+    bsync<WS>();
+  }
   if (T.idep >= 0) load_init();
   if (tr) tr[3] = gtimer();
 #pragma unroll
   for (int s = 0; s < NSTAGE - 1; ++s) {
-    if (s < nsteps) issue_b<GN_MT, GN_NT>(kt, s * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + s * STAGE_B);
+    if (s < nsteps) issue_b<GN_MT, GN_NT>(kt, s * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + s * sb);
     cp_commit();
   }
   const bool live = (row < mm) && (cb < nn);
   for (int s = 0; s < nsteps; ++s) {
     cp_wait<NSTAGE - 2>();
-    __syncthreads();
+    bsync<WS>();
     const int st = s % NSTAGE;
     if (live) {
-      const double2* As = As0 + st * STAGE_A + row;
-      const double2* Bs = Bs0 + st * STAGE_B + cb;
+      const double2* As = As0 + st * sa + row;
+      const double2* Bs = Bs0 + st * sb + cb;
 #pragma unroll
       for (int k = 0; k < KC; ++k) {
         const double2 av = As[k * GN_MT];
@@ -626,17 +638,17 @@ __device__ __forceinline__ void item_body_narrow(const FlowArgs& a, const GWork&
     const int sn = s + NSTAGE - 1;
     if (sn < nsteps) {
       const int stn = sn % NSTAGE;
-      issue_a<GN_MT, GN_NT>(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * STAGE_A);
-      issue_b<GN_MT, GN_NT>(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * STAGE_B);
+      issue_a<GN_MT, GN_NT>(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * sa);
+      issue_b<GN_MT, GN_NT>(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * sb);
     }
     cp_commit();
   }
   cp_wait<0>();
-  __syncthreads();
+  bsync<WS>();
   if (tr) tr[4] = gtimer();
   int off[2] = {row * GN_NT + cb, row * GN_NT + cb + 1};
   bool own[2] = {true, true};
-  const bool finalize = crit_fin ? true : splitk_combine<2>(a, w, acc, off, own, tid, s_last);
+  const bool finalize = crit_fin ? true : splitk_combine<2, WS>(a, w, acc, off, own, tid, s_last);
   if (finalize) {
     if (row < mm) {
 #pragma unroll
@@ -648,7 +660,7 @@ __device__ __forceinline__ void item_body_narrow(const FlowArgs& a, const GWork&
         }
       }
     }
-    __syncthreads();
+    bsync<WS>();
     if (tid == 0) red_release(done + T.unit0 + w.nt, 1);
   }
 }
@@ -710,7 +722,7 @@ flow_kernel(const FlowArgs a) {
       }
     } else
     switch (RM) {
-      case 0: item_body_narrow(a, w, T, kt, As0, Bs0, tid, &s_last, tr); break;
+      case 0: item_body_narrow<false>(a, w, T, kt, As0, Bs0, tid, &s_last, tr, STAGE_A, STAGE_B); break;
 #define PS_RM_CASE(R) \
       case R: item_body<R>(a, w, T, kt, As0, Bs0, tid, lane, wm, wn, &s_last, tr); break;
       PS_RM_CASE(1) PS_RM_CASE(2) PS_RM_CASE(3) PS_RM_CASE(4) PS_RM_CASE(5) PS_RM_CASE(6)
@@ -721,6 +733,133 @@ flow_kernel(const FlowArgs a) {
     if (tr) tr[5] = gtimer();
     __syncthreads();
   }
+}
+
+// ---------------------------------------------------------------------------
+// Narrow tiles (nrhs <= 8, operator streaming): warp-specialised variant of the
+// dataflow kernel. Warps 0-7 compute; warp 8 schedules: it takes the next
+// ticket, copies the item's descriptors and segment list into a slot, builds
+// the k table there (lanes over the k's of each segment) and waits (acquire)
+// for the producers of the item's B / init rows and, for a critical chunk, for
+// the group sum — while the compute warps stream the previous item. Two slots
+// alternate; hand-over through named barriers FULL[s] = 1 + s / EMPTY[s] =
+// 3 + s (288 threads); compute warps synchronise on barrier 5 (256).
+// Deadlock-free: a handed-over item runs to completion without waiting, and the
+// scheduler only waits on smaller tickets (the smallest unfinished ticket is
+// always a running item or is handed over as soon as its CTA's item ends).
+// (For the wide tiles this costs the compute warps registers — 2 CTAs x 288
+// threads cap them at 112 — and measured slower.)
+struct SlotWS {
+  GWork w;
+  GTask T;
+  int64_t item;
+  GTerm seg[GM_MAXSEG];
+};
+constexpr int WS_SA = KC * GN_MT + KC * GN_NT;      // one narrow stage: A tile then B tile
+constexpr size_t FLOW_WS_SMEM = (size_t)NSTAGE * WS_SA * sizeof(double2) + 2 * sizeof(KTab) + 2 * sizeof(SlotWS);
+
+__device__ __forceinline__ void bar_sync_n(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void bar_arrive_n(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+__device__ void ws_scheduler(const FlowArgs& a, SlotWS* slots, KTab* kts, int lane) {
+  int32_t* ticket = a.counters;
+  for (int64_t j = 0;; ++j) {
+    const int s = (int)(j & 1);
+    if (j >= 2) bar_sync_n(3 + s, 288);               // compute warps released slot s
+    int it = 0;
+    if (lane == 0) it = atomicAdd(ticket, 1);
+    it = __shfl_sync(0xffffffffu, it, 0);
+    SlotWS& sl = slots[s];
+    if (it >= a.nwork) {
+      if (lane == 0) sl.item = -1;
+      __syncwarp();
+      bar_arrive_n(1 + s, 288);
+      return;
+    }
+    {
+      const int32_t* src = reinterpret_cast<const int32_t*>(a.work + it);
+      int32_t* dst = reinterpret_cast<int32_t*>(&sl.w);
+      if (lane < (int)(sizeof(GWork) / 4)) dst[lane] = src[lane];
+    }
+    __syncwarp();
+    const int ta = sl.w.ta, tb = sl.w.tb, ka = sl.w.ka, kb = sl.w.kb;
+    {
+      const int32_t* src = reinterpret_cast<const int32_t*>(a.tasks + sl.w.task);
+      int32_t* dst = reinterpret_cast<int32_t*>(&sl.T);
+      for (int q = lane; q < (int)(sizeof(GTask) / 4); q += 32) dst[q] = src[q];
+      // segment list (<= GM_MAXSEG), lanes in parallel
+      const int32_t* ts = reinterpret_cast<const int32_t*>(a.terms + ta);
+      int32_t* td = reinterpret_cast<int32_t*>(sl.seg);
+      const int n4 = (tb - ta) * (int)(sizeof(GTerm) / 4);
+      for (int q = lane; q < n4; q += 32) td[q] = ts[q];
+    }
+    if (lane == 0) sl.item = it;
+    __syncwarp();
+    KTab& kt = kts[s];
+    for (int t = 0; t < tb - ta; ++t) {
+      const GTerm& g = sl.seg[t];
+      const int lo = max(g.kstart, ka), hi = min(g.kstart + g.K, kb);
+      const double2* bb = (g.bsel ? a.S : a.B) + g.oB;
+      for (int k = lo + lane; k < hi; k += 32) {
+        const int64_t d = k - g.kstart;
+        kt.kA[k - ka] = g.oA + d * g.sAk;
+        kt.kB[k - ka] = bb + d * g.sBk;
+        kt.kSi[k - ka] = (int32_t)g.sAi;
+        kt.kSc[k - ka] = (int32_t)g.sBc;
+      }
+    }
+    // producers (lanes over segments), init producer, split-K group sum
+    const int nt = sl.w.nt;
+    if (lane == 0 && sl.T.idep >= 0) wait_dep_task(a, sl.T.idep, nt);
+    for (int t = lane; t < tb - ta; t += 32)
+      if (sl.seg[t].dep >= 0) wait_dep_task(a, sl.seg[t].dep, nt);
+    if (lane == 0 && sl.w.nchunks > 1 && sl.w.crit >= 0 && sl.w.chunk == sl.w.crit) {
+      const int32_t* ctr = a.counters + 1 + a.n_units + sl.w.tile;
+      while (ld_acquire(ctr) < sl.w.nsub + 1) __nanosleep(32);
+    }
+    __syncwarp();
+    bar_arrive_n(1 + s, 288);                         // slot s full
+  }
+}
+
+__global__ void __launch_bounds__(288, 2)
+flow_kernel_ws(const FlowArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* stages = reinterpret_cast<double2*>(smem_raw);
+  KTab* kts = reinterpret_cast<KTab*>(stages + NSTAGE * WS_SA);
+  SlotWS* slots = reinterpret_cast<SlotWS*>(kts + 2);
+  __shared__ int s_last;
+  const int tid = threadIdx.x;
+  if (tid >= 256) {
+    ws_scheduler(a, slots, kts, tid & 31);
+    return;
+  }
+  for (int64_t j = 0;; ++j) {
+    const int s = (int)(j & 1);
+    bar_sync_n(1 + s, 288);                           // slot s full
+    const SlotWS& sl = slots[s];
+    const int64_t item = sl.item;
+    if (item < 0) return;
+    int64_t* tr = (a.trace != nullptr && tid == 0) ? a.trace + 6 * item : nullptr;
+    if (tr) { tr[0] = item; tr[1] = smid(); tr[2] = gtimer(); }
+    item_body_narrow<true>(a, sl.w, sl.T, kts[s], stages, stages + KC * GN_MT, tid, &s_last, tr, WS_SA, WS_SA);
+    if (tr) tr[5] = gtimer();
+    bsync<true>();                                    // every compute warp is done with slot s
+    bar_arrive_n(3 + s, 288);                         // slot s empty
+  }
+}
+
+int flow_ws_resident_ctas() {
+  static int n = 0;
+  if (n == 0) {
+    int per_sm = 0, dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(flow_kernel_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FLOW_WS_SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, flow_kernel_ws, 288, FLOW_WS_SMEM);
+    n = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  return n;
 }
 
 int flow_resident_ctas() {
@@ -738,6 +877,16 @@ int flow_resident_ctas() {
 
 void launch_flow(const FlowArgs& a, int grid, cudaStream_t st) {
   if (a.nwork <= 0) return;
+  static const bool ws = [] {
+    const char* e = std::getenv("PS_NARROW_WS");
+    return !(e && e[0] == '0');
+  }();
+  if (a.narrow && ws) {
+    int g = grid > 0 ? grid : flow_ws_resident_ctas();
+    if (g > a.nwork) g = (int)a.nwork;
+    flow_kernel_ws<<<g, 288, FLOW_WS_SMEM, st>>>(a);
+    return;
+  }
   int g = grid > 0 ? grid : flow_resident_ctas();
   if (g > a.nwork) g = (int)a.nwork;
   flow_kernel<<<g, 256, FLOW_SMEM, st>>>(a);
