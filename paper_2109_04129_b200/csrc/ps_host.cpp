@@ -241,7 +241,7 @@ struct Table {
   void chunk_range(int32_t s0, int32_t s1, std::vector<std::array<int32_t, 4>>& ch, int steps) const {
     if (s0 >= s1) return;
     const int32_t k_lo = terms[s0].kstart, k_hi = terms[s1 - 1].kstart + terms[s1 - 1].K;
-    const int target = std::min(steps * GM_KC, GM_CHUNK_K);
+    const int target = std::min(steps * GM_KC, narrow ? GN_CHUNK_K : GM_CHUNK_K);
     int32_t ka = k_lo, ta = s0;
     while (ka < k_hi) {
       int32_t kb = std::min(k_hi, ka + target);

@@ -68,12 +68,15 @@ __device__ __forceinline__ int ld_acquire(const int32_t* p) {
 // Per-item k tables: for the item's virtual k range [ka, kb) the A column
 // base, A row stride, B row base and B column stride of every k (built from the
 // segment list at item start), so k-steps run densely across segments.
-struct KTab {
-  int64_t kA[GM_CHUNK_K];
-  const double2* kB[GM_CHUNK_K];     // absolute row pointer of B (base B or scratch S)
-  int32_t kSi[GM_CHUNK_K];
-  int32_t kSc[GM_CHUNK_K];
+template <int NK>
+struct KTabT {
+  int64_t kA[NK];
+  const double2* kB[NK];             // absolute row pointer of B (base B or scratch S)
+  int32_t kSi[NK];
+  int32_t kSc[NK];
 };
+using KTab = KTabT<GM_CHUNK_K>;
+using KTabN = KTabT<GN_CHUNK_K>;     // narrow (warp-specialised) items: <= GN_CHUNK_K k
 
 constexpr int AS_LD = GM_MT;                // As[k][i]
 constexpr int BS_LD = GM_NT;                // Bs[k][c]
@@ -98,8 +101,8 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int MT, int NT>
-__device__ __forceinline__ void issue_a(const KTab& kt, int k0, int klen, int i0, int mm, bool a_km,
+template <int MT, int NT, class KT>
+__device__ __forceinline__ void issue_a(const KT& kt, int k0, int klen, int i0, int mm, bool a_km,
                                         const double2* __restrict__ Ab, int tid, double2* As) {
 #pragma unroll
   for (int q = 0; q < MT * KC / 256; ++q) {
@@ -112,8 +115,8 @@ __device__ __forceinline__ void issue_a(const KTab& kt, int k0, int klen, int i0
     cp_async16(As + k * MT + i, src, v);
   }
 }
-template <int MT, int NT>
-__device__ __forceinline__ void issue_b(const KTab& kt, int k0, int klen, int c0, int nn, bool b_km,
+template <int MT, int NT, class KT>
+__device__ __forceinline__ void issue_b(const KT& kt, int k0, int klen, int c0, int nn, bool b_km,
                                         const double2* __restrict__ Bb, int tid, double2* Bs) {
   constexpr int NB = NT * KC;
 #pragma unroll
@@ -572,9 +575,9 @@ __device__ __forceinline__ void item_body_dmma(const FlowArgs& a, const GWork& w
 // Narrow tile (small nrhs): 64 rows x 8 columns; thread t owns row t % 64 and
 // columns 2 (t / 64) + {0, 1}. The operator panel is streamed through the same
 // cp.async ring (HBM-bound regime), B values are warp broadcasts.
-template <bool WS>
+template <bool WS, int NS, class KT>
 __device__ __forceinline__ void item_body_narrow(const FlowArgs& a, const GWork& w, const GTask& T,
-                                                 const KTab& kt, double2* As0, double2* Bs0, int tid,
+                                                 const KT& kt, double2* As0, double2* Bs0, int tid,
                                                  int* s_last, int64_t* tr, int sa, int sb) {
   const int i0 = w.mt * GN_MT, c0 = w.nt * GN_NT;
   const int mm = min(GN_MT, T.m - i0), nn = min(GN_NT, T.n - c0);
@@ -584,7 +587,7 @@ __device__ __forceinline__ void item_body_narrow(const FlowArgs& a, const GWork&
   const bool a_km = T.a_kmajor != 0, b_km = T.b_kmajor != 0;
   const int nsteps = (klen + KC - 1) / KC;
 #pragma unroll
-  for (int s = 0; s < NSTAGE - 1; ++s)
+  for (int s = 0; s < NS - 1; ++s)
     if (s < nsteps) issue_a<GN_MT, GN_NT>(kt, s * KC, klen, i0, mm, a_km, a.A, tid, As0 + s * sa);
   cp_commit();
   const double sgn = (double)T.sign;
@@ -616,15 +619,15 @@ __device__ __forceinline__ void item_body_narrow(const FlowArgs& a, const GWork&
   if (T.idep >= 0) load_init();
   if (tr) tr[3] = gtimer();
 #pragma unroll
-  for (int s = 0; s < NSTAGE - 1; ++s) {
+  for (int s = 0; s < NS - 1; ++s) {
     if (s < nsteps) issue_b<GN_MT, GN_NT>(kt, s * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + s * sb);
     cp_commit();
   }
   const bool live = (row < mm) && (cb < nn);
   for (int s = 0; s < nsteps; ++s) {
-    cp_wait<NSTAGE - 2>();
+    cp_wait<NS - 2>();
     bsync<WS>();
-    const int st = s % NSTAGE;
+    const int st = s % NS;
     if (live) {
       const double2* As = As0 + st * sa + row;
       const double2* Bs = Bs0 + st * sb + cb;
@@ -635,9 +638,9 @@ __device__ __forceinline__ void item_body_narrow(const FlowArgs& a, const GWork&
         cfma(acc[1], av, Bs[k * GN_NT + 1]);
       }
     }
-    const int sn = s + NSTAGE - 1;
+    const int sn = s + NS - 1;
     if (sn < nsteps) {
-      const int stn = sn % NSTAGE;
+      const int stn = sn % NS;
       issue_a<GN_MT, GN_NT>(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * sa);
       issue_b<GN_MT, GN_NT>(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * sb);
     }
@@ -722,7 +725,7 @@ flow_kernel(const FlowArgs a) {
       }
     } else
     switch (RM) {
-      case 0: item_body_narrow<false>(a, w, T, kt, As0, Bs0, tid, &s_last, tr, STAGE_A, STAGE_B); break;
+      case 0: item_body_narrow<false, NSTAGE>(a, w, T, kt, As0, Bs0, tid, &s_last, tr, STAGE_A, STAGE_B); break;
 #define PS_RM_CASE(R) \
       case R: item_body<R>(a, w, T, kt, As0, Bs0, tid, lane, wm, wn, &s_last, tr); break;
       PS_RM_CASE(1) PS_RM_CASE(2) PS_RM_CASE(3) PS_RM_CASE(4) PS_RM_CASE(5) PS_RM_CASE(6)
@@ -755,13 +758,149 @@ struct SlotWS {
   int64_t item;
   GTerm seg[GM_MAXSEG];
 };
-constexpr int WS_SA = KC * GN_MT + KC * GN_NT;      // one narrow stage: A tile then B tile
-constexpr size_t FLOW_WS_SMEM = (size_t)NSTAGE * WS_SA * sizeof(double2) + 2 * sizeof(KTab) + 2 * sizeof(SlotWS);
+constexpr int WS_A = KC * GN_MT;                      // A tile of a narrow stage: 1024 complex
+constexpr int WS_SA = WS_A + 64 * GN_NT;              // + B tile (<= 64 k x 8 columns)
+constexpr int WS_NSTAGE = 3;
+
+// Narrow item body of the warp-specialised kernel with a row-adaptive tile:
+// MTW = 16 / 32 / 64 rows x KCW = 1024 / MTW k per stage, so a short task (a
+// 16-19 row leaf) still streams 1024 operator entries per stage instead of
+// leaving 3/4 of a 64-row tile empty. Thread t: row t % MTW, column pair
+// 2 ((t / MTW) % 4), k slice (t / MTW) / 4 of NKS = 64 / MTW slices of 16 k;
+// the slices are summed through shared memory at the end (fixed order).
+template <int MTW>
+__device__ __forceinline__ void item_body_nk(const FlowArgs& a, const GWork& w, const GTask& T,
+                                             const KTabN& kt, double2* stages, int tid, int* s_last,
+                                             int64_t* tr) {
+  constexpr int KCW = 1024 / MTW, NKS = 64 / MTW;
+  const int i0 = w.mt * GN_MT, c0 = w.nt * GN_NT;
+  const int mm = min(GN_MT, T.m - i0), nn = min(GN_NT, T.n - c0);
+  const int klen = w.kb - w.ka;
+  const int row = tid % MTW, rest = tid / MTW, cb = 2 * (rest & 3), ks = rest >> 2;
+  int32_t* done = a.counters + 1;
+  const bool a_km = T.a_kmajor != 0, b_km = T.b_kmajor != 0;
+  const int nsteps = (klen + KCW - 1) / KCW;
+  auto issue_a = [&](int k0, double2* As) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + q * 256;
+      int i, k;
+      if (a_km) { k = e % KCW; i = e / KCW; } else { i = e % MTW; k = e / MTW; }
+      const int kk = k0 + k;
+      const bool v = (i < mm && kk < klen);
+      const double2* src = v ? a.A + kt.kA[kk] + (int64_t)(i0 + i) * kt.kSi[kk] : a.A;
+      cp_async16(As + k * MTW + i, src, v);
+    }
+  };
+  auto issue_b = [&](int k0, double2* Bs) {
+#pragma unroll
+    for (int q = 0; q < (KCW * GN_NT + 255) / 256; ++q) {
+      const int e = tid + q * 256;
+      if ((KCW * GN_NT) % 256 != 0 && e >= KCW * GN_NT) break;
+      int c, k;
+      if (b_km) { k = e % KCW; c = e / KCW; } else { c = e % GN_NT; k = e / GN_NT; }
+      const int kk = k0 + k;
+      const bool v = (c < nn && kk < klen);
+      const double2* src = v ? kt.kB[kk] + (int64_t)(c0 + c) * kt.kSc[kk] : a.B;
+      cp_async16(Bs + k * GN_NT + c, src, v);
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < WS_NSTAGE - 1; ++s)
+    if (s < nsteps) issue_a(s * KCW, stages + s * WS_SA);
+  cp_commit();
+  const double sgn = (double)T.sign;
+  const bool crit_fin = (w.nchunks > 1 && w.crit >= 0 && w.chunk == w.crit);
+  const bool owns_init = (w.nchunks == 1) || (w.crit >= 0 ? w.chunk == w.crit : w.chunk == 0);
+  double2 acc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+  if (crit_fin && ks == 0) {
+    const double2* Gs = a.partial + (w.slot + w.crit) * (int64_t)(GM_MT * GM_NT);
+    acc[0] = __ldcg(Gs + row * GN_NT + cb);
+    acc[1] = __ldcg(Gs + row * GN_NT + cb + 1);
+  }
+  if (owns_init && T.oI >= 0 && row < mm && ks == 0) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+      if (cb + e < nn) {
+        const double2 z = __ldcg(((T.osel & 2) ? (const double2*)a.S : a.I) + T.oI + (int64_t)(i0 + row) * T.sIi +
+                                 (int64_t)(c0 + cb + e) * T.sIc);
+        acc[e].x += sgn * z.x;
+        acc[e].y += sgn * z.y;
+      }
+  }
+  if (tr) tr[3] = gtimer();
+#pragma unroll
+  for (int s = 0; s < WS_NSTAGE - 1; ++s) {
+    if (s < nsteps) issue_b(s * KCW, stages + s * WS_SA + WS_A);
+    cp_commit();
+  }
+  const bool live = (row < mm) && (cb < nn);
+  for (int s = 0; s < nsteps; ++s) {
+    cp_wait<WS_NSTAGE - 2>();
+    bsync<true>();
+    const int st = s % WS_NSTAGE;
+    if (live) {
+      const double2* As = stages + st * WS_SA + (16 * ks) * MTW + row;
+      const double2* Bs = stages + st * WS_SA + WS_A + (16 * ks) * GN_NT + cb;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const double2 av = As[k * MTW];
+        cfma(acc[0], av, Bs[k * GN_NT]);
+        cfma(acc[1], av, Bs[k * GN_NT + 1]);
+      }
+    }
+    const int sn = s + WS_NSTAGE - 1;
+    if (sn < nsteps) {
+      const int stn = sn % WS_NSTAGE;
+      issue_a(sn * KCW, stages + stn * WS_SA);
+      issue_b(sn * KCW, stages + stn * WS_SA + WS_A);
+    }
+    cp_commit();
+  }
+  cp_wait<0>();
+  bsync<true>();
+  if (tr) tr[4] = gtimer();
+  if constexpr (NKS > 1) {                           // sum the k slices: ks 0 + 1 + ... (fixed order)
+    double2* red = stages;                           // NKS x MTW x 8 <= 512 complex
+    if (ks > 0) {
+      red[(ks * MTW + row) * GN_NT + cb] = acc[0];
+      red[(ks * MTW + row) * GN_NT + cb + 1] = acc[1];
+    }
+    bsync<true>();
+    if (ks == 0) {
+#pragma unroll
+      for (int q = 1; q < NKS; ++q) {
+        const double2 v0 = red[(q * MTW + row) * GN_NT + cb], v1 = red[(q * MTW + row) * GN_NT + cb + 1];
+        acc[0].x += v0.x; acc[0].y += v0.y;
+        acc[1].x += v1.x; acc[1].y += v1.y;
+      }
+    }
+    bsync<true>();
+  }
+  int off[2] = {row * GN_NT + cb, row * GN_NT + cb + 1};
+  bool own[2] = {ks == 0, ks == 0};
+  const bool finalize = crit_fin ? true : splitk_combine<2, true>(a, w, acc, off, own, tid, s_last);
+  if (finalize) {
+    if (row < mm && ks == 0) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = cb + e;
+        if (col < nn) {
+          const double2 v = make_double2(sgn * acc[e].x, sgn * acc[e].y);   // O = I + sign * sum
+          __stcg(((T.osel & 1) ? a.S : a.O) + T.oO + (int64_t)(i0 + row) * T.sOi + (int64_t)(c0 + col) * T.sOc, v);
+        }
+      }
+    }
+    bsync<true>();
+    if (tid == 0) red_release(done + T.unit0 + w.nt, 1);
+  }
+}
+constexpr size_t FLOW_WS_SMEM = (size_t)WS_NSTAGE * WS_SA * sizeof(double2) + 2 * sizeof(KTabN) + 2 * sizeof(SlotWS);
 
 __device__ __forceinline__ void bar_sync_n(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void bar_arrive_n(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-__device__ void ws_scheduler(const FlowArgs& a, SlotWS* slots, KTab* kts, int lane) {
+__device__ void ws_scheduler(const FlowArgs& a, SlotWS* slots, KTabN* kts, int lane) {
   int32_t* ticket = a.counters;
   for (int64_t j = 0;; ++j) {
     const int s = (int)(j & 1);
@@ -795,7 +934,7 @@ __device__ void ws_scheduler(const FlowArgs& a, SlotWS* slots, KTab* kts, int la
     }
     if (lane == 0) sl.item = it;
     __syncwarp();
-    KTab& kt = kts[s];
+    KTabN& kt = kts[s];
     for (int t = 0; t < tb - ta; ++t) {
       const GTerm& g = sl.seg[t];
       const int lo = max(g.kstart, ka), hi = min(g.kstart + g.K, kb);
@@ -826,7 +965,7 @@ __global__ void __launch_bounds__(288, 2)
 flow_kernel_ws(const FlowArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* stages = reinterpret_cast<double2*>(smem_raw);
-  KTab* kts = reinterpret_cast<KTab*>(stages + NSTAGE * WS_SA);
+  KTabN* kts = reinterpret_cast<KTabN*>(stages + WS_NSTAGE * WS_SA);
   SlotWS* slots = reinterpret_cast<SlotWS*>(kts + 2);
   __shared__ int s_last;
   const int tid = threadIdx.x;
@@ -842,7 +981,10 @@ flow_kernel_ws(const FlowArgs a) {
     if (item < 0) return;
     int64_t* tr = (a.trace != nullptr && tid == 0) ? a.trace + 6 * item : nullptr;
     if (tr) { tr[0] = item; tr[1] = smid(); tr[2] = gtimer(); }
-    item_body_narrow<true>(a, sl.w, sl.T, kts[s], stages, stages + KC * GN_MT, tid, &s_last, tr, WS_SA, WS_SA);
+    const int mrows = min(GN_MT, sl.T.m - sl.w.mt * GN_MT);
+    if (mrows <= 16) item_body_nk<16>(a, sl.w, sl.T, kts[s], stages, tid, &s_last, tr);
+    else if (mrows <= 32) item_body_nk<32>(a, sl.w, sl.T, kts[s], stages, tid, &s_last, tr);
+    else item_body_nk<64>(a, sl.w, sl.T, kts[s], stages, tid, &s_last, tr);
     if (tr) tr[5] = gtimer();
     bsync<true>();                                    // every compute warp is done with slot s
     bar_arrive_n(3 + s, 288);                         // slot s empty
