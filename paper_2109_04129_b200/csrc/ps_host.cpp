@@ -410,6 +410,9 @@ struct Table {
       return -1;
     }();
     fa.mma = mma_env >= 0 ? mma_env : mma;
+    static const int ks_env = env_int("PS_DFMA_KS", 0);
+    fa.dfma_ks = ks_env;
+    fa.pad2 = 0;
     if (pf && pf->trace_on && cls == pf->trace_cls) {
       pf->trace_buf.alloc(6 * bt.nw);
       fa.trace = pf->trace_buf.p;
