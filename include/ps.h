@@ -209,6 +209,9 @@ enum {
   PS_INFO_NRANKS,            /* ranks of the row partition (1 otherwise) */
   PS_INFO_OWN_ROWS,          /* unknowns in this rank's interior subtrees */
   PS_INFO_SEP_ROWS,          /* unknowns in the replicated separator nodes */
+  PS_INFO_CHAINS,            /* elimination-tree chain pieces with >= 2 leaves (applied through T_c) */
+  PS_INFO_CHAIN_HEIGHT,      /* levels of the chain graph (dependent stages of a sweep / 2) */
+  PS_INFO_T_ENTRIES,         /* complex entries of all T_c (U_c x U_c each) */
   PS_INFO_COUNT
 };
 int ps_info(const ps_handle* h, double* out, int n);

@@ -2603,6 +2603,17 @@ int ps_info(const ps_handle* h, double* out, int n) {
   v[PS_INFO_NRANKS] = h->part_mode ? h->nranks : 1;
   v[PS_INFO_OWN_ROWS] = h->part_mode ? (double)h->own_rows : (double)h->N;
   v[PS_INFO_SEP_ROWS] = h->part_mode ? (double)h->Nsep : 0.0;
+  {
+    double nchain = 0, tent = 0;
+    for (size_t c = 0; c < h->chains.size(); ++c)
+      if (h->chains[c].size() >= 2) {
+        nchain += 1;
+        tent += (double)h->ch_U[c] * (double)h->ch_U[c];
+      }
+    v[PS_INFO_CHAINS] = nchain;
+    v[PS_INFO_CHAIN_HEIGHT] = h->max_ch_height + 1;
+    v[PS_INFO_T_ENTRIES] = tent;
+  }
   int m = std::min(n, (int)PS_INFO_COUNT);
   std::memcpy(out, v, sizeof(double) * m);
   return m;

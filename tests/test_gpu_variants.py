@@ -1,0 +1,64 @@
+"""GPU parity of the alternative execution paths selected by environment knobs
+(each read once per process, so every variant runs in a subprocess):
+
+  PS_CHAINS=0      sweeps as one dependent hop per elimination-tree level
+                   (no chain matrices T_c, DESIGN.md §6 / R23)
+  PS_NARROW_WS=0   nrhs <= 8 through the non-specialised kernel (64 x 8 tile)
+  PS_MMA=dmma      every wide table on the FP64 tensor-core consumer
+  PS_MMA=dfma      every wide table on the DFMA consumer (far field included)
+  PS_DFMA_KS=1     the k-split DFMA consumer
+  PS_SOLVE=program the whole solve as one dataflow launch
+
+Each must match the oracle to the north-star bar (relative L2 <= 1e-11 per RHS).
+"""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+_SCRIPT = r"""
+import sys, warnings
+import numpy as np, torch
+sys.path.insert(0, {root!r})
+from paper_2109_04129_b200 import PsHandle
+from hmgen.synth import random_rhs
+warnings.simplefilter("ignore")
+h = PsHandle({path!r}); h.setup()
+B = random_rhs(h.N, {nrhs}, 4)
+Bd = torch.from_numpy(np.ascontiguousarray(np.asfortranarray(B).T)).cuda().T
+Xd = torch.empty_like(Bd)
+st, rep = h.solve(Bd, Xd)
+np.save({out!r}, Xd.T.cpu().numpy().T)
+np.save({out!r} + ".it.npy", np.stack([rep["it0"], rep["it1"]]))
+"""
+
+
+def _run(path, nrhs, env, out):
+    e = dict(os.environ)
+    e.update(env)
+    code = _SCRIPT.format(root=ROOT, path=path, nrhs=nrhs, out=out)
+    r = subprocess.run([sys.executable, "-c", code], env=e, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return np.load(out), np.load(out + ".it.npy")
+
+
+@pytest.mark.parametrize("env", [{"PS_CHAINS": "0"}, {"PS_NARROW_WS": "0"}, {"PS_MMA": "dmma"},
+                                 {"PS_MMA": "dfma"}, {"PS_DFMA_KS": "1"}, {"PS_SOLVE": "program"}, {}],
+                         ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default")
+@pytest.mark.parametrize("nrhs", [1, 70])
+def test_variant_matches_oracle(cfgdata, tmp_path, env, nrhs):
+    from hmgen.synth import random_rhs
+    from oracle import compute_scaling, read_hm, solve
+    from tests.conftest import rel_l2_cols
+    path = cfgdata("C1")["hm"]
+    x, it = _run(path, nrhs, env, str(tmp_path / "x.npy"))
+    H = read_hm(path)
+    ref = solve(H, compute_scaling(H), random_rhs(H.N, nrhs, 4))
+    assert rel_l2_cols(x, ref.x).max() <= 1e-11
+    assert np.allclose(it[0], ref.it0, rtol=1e-11)
+    assert np.allclose(it[1], ref.it1, rtol=1e-10)

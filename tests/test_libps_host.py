@@ -90,3 +90,54 @@ def test_symbolic_fill_matches_oracle(case, cfgdata, synthfile):
     assert info["nR"] == nR
     assert info["nD"] == nD
     assert info["N"] == S.N
+
+
+def _chains_from_oracle(S, tmax=2048):
+    """Chain pieces of the elimination tree, written from the definition
+    (DESIGN.md §6): maximal paths p -> parent(p) whose upper nodes have a single
+    child, cut before exceeding tmax unknowns. Returns (pieces, chain-graph height)."""
+    n = S.n
+    st = [sorted(S.alpha[k].keys()) for k in range(n)]
+    par = [s[0] if s else -1 for s in st]
+    nchild = [0] * n
+    for p in range(n):
+        if par[p] >= 0:
+            nchild[par[p]] += 1
+    cid = [-1] * n
+    pieces = []
+    for p in range(n):
+        if cid[p] >= 0:
+            continue
+        c, U, q = [p], int(S.sizes[p]), p
+        while par[q] >= 0 and nchild[par[q]] == 1 and cid[par[q]] < 0 and U + int(S.sizes[par[q]]) <= tmax:
+            q = par[q]
+            c.append(q)
+            U += int(S.sizes[q])
+        for x in c:
+            cid[x] = len(pieces)
+        pieces.append(c)
+    height = [0] * len(pieces)
+    for i in sorted(range(len(pieces)), key=lambda i: pieces[i][-1]):
+        up = par[pieces[i][-1]]
+        if up >= 0:
+            j = cid[up]
+            assert pieces[j][0] == up          # a piece's top hangs below another piece's first node
+            height[j] = max(height[j], height[i] + 1)
+    return pieces, max(height) + 1
+
+
+@pytest.mark.parametrize("case", ["C1", "T2", "synth"])
+def test_chain_pieces_match_definition(case, cfgdata, synthfile):
+    """The chain pieces libps collapses through T_c (ps_info) agree with the
+    definition applied to the elimination tree the oracle discovers."""
+    from oracle import compute_scaling, read_hm
+    path = cfgdata(case)["hm"] if case != "synth" else synthfile(n_points=900, seed=7, clustered=True)[0]
+    st, info = _analyze(path)
+    assert st == 0, info
+    S = compute_scaling(read_hm(path))
+    pieces, height = _chains_from_oracle(S)
+    multi = [c for c in pieces if len(c) >= 2]
+    assert info["chains"] == len(multi)
+    assert info["chain_height"] == height
+    assert info["T_entries"] == sum(int(sum(S.sizes[p] for p in c)) ** 2 for c in multi)
+    assert height < info["height"]           # collapsing chains shortens the dependency path
