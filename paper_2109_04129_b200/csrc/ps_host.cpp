@@ -1144,7 +1144,13 @@ void build_chain_sweeps(ps_handle* h, SolvePlan& sp, int64_t R, int narrow, int 
   // [2, maxs] k-steps (a stage lasts as long as its longest item)
   static const int maxs = env_int("PS_SWEEP_MAXSTEPS", 16), ipc = env_int("PS_SWEEP_IPC", 2);
   auto steps_of = [&](const std::vector<std::pair<int64_t, int64_t>>& mk) {   // (m, K) of a stage's tasks
-    if (narrow) return NARROW_STEPS();
+    if (narrow) {   // operator streaming: enough items per stage to occupy every CTA
+      static const int nadapt = env_int("PS_NARROW_ADAPT", 1);
+      if (!nadapt) return NARROW_STEPS();
+      double ks = 0;
+      for (auto [m, K] : mk) ks += std::ceil((double)m / GN_MT) * std::ceil((double)K / GM_KC);
+      return std::max(2, std::min(NARROW_STEPS(), (int)std::ceil(ks / (double)resident)));
+    }
     double ks = 0;
     for (auto [m, K] : mk) ks += std::ceil((double)m / GM_MT) * std::ceil((double)R / GM_NT) * std::ceil((double)K / GM_KC);
     return std::max(2, std::min(maxs, (int)std::ceil(ks / ((double)ipc * resident))));
