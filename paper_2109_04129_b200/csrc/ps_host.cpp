@@ -410,8 +410,7 @@ struct Table {
       return -1;
     }();
     fa.mma = mma_env >= 0 ? mma_env : mma;
-    static const int ks_env = env_int("PS_DFMA_KS", 0);
-    fa.dfma_ks = ks_env;
+    fa.dfma_ks = 0;
     fa.pad2 = 0;
     if (pf && pf->trace_on && cls == pf->trace_cls) {
       pf->trace_buf.alloc(6 * bt.nw);

@@ -80,7 +80,7 @@ struct FlowArgs {
   int64_t* trace;          // optional: 6 x int64 per item (item, smid, t_fetch, t_ready, t_computed, t_done), ns
   int32_t narrow;          // 1: narrow 64 x 8 tiles (small nrhs), 0: 32 x 64 tiles
   int32_t mma;             // wide tiles: 0 = DFMA consumer, 1 = FP64 tensor-core (DMMA) consumer
-  int32_t dfma_ks;         // DFMA consumer: 1 = k split across warp pairs (item_body_ks), 0 = 4 x 2 warps
+  int32_t dfma_ks;         // reserved (0)
   int32_t pad2;
 };
 

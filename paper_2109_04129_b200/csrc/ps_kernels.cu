@@ -390,145 +390,6 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
 }
 
 
-// Wide DFMA tile with the k dimension split across warp pairs: warp w = (wm,
-// kh) = (w % 4, w / 4) owns rows [wm*RM, (wm+1)*RM) x all 64 columns (lane and
-// lane + 32) over the k rows [8 kh, 8 kh + 8) of every stage; the two k
-// halves are summed through shared memory at the end (kh 0 + kh 1). Per k a
-// warp issues RM A broadcasts + 2 B loads for 8 RM DFMAs, so the shared /
-// L1 traffic per FMA drops ~30 % against the 4 x 2 (rows x columns) layout,
-// whose B loads every warp repeats.
-template <int RM>
-__device__ __forceinline__ void item_body_ks(const FlowArgs& a, const GWork& w, const GTask& T,
-                                             const KTab& kt, double2* As0, double2* Bs0, int tid,
-                                             int lane, int warp, int* s_last, int64_t* tr) {
-  const int i0 = w.mt * GM_MT, c0 = w.nt * GM_NT;
-  const int mm = min(GM_MT, T.m - i0), nn = min(GM_NT, T.n - c0);
-  const int klen = w.kb - w.ka;
-  const int wm = warp & 3, kh = warp >> 2;
-  const int rbase = wm * RM;
-  int32_t* done = a.counters + 1;
-  const bool a_km = T.a_kmajor != 0, b_km = T.b_kmajor != 0;
-  const int nsteps = (klen + KC - 1) / KC;
-#pragma unroll
-  for (int s = 0; s < NSTAGE - 1; ++s)
-    if (s < nsteps) issue_a<GM_MT, GM_NT>(kt, s * KC, klen, i0, mm, a_km, a.A, tid, As0 + s * STAGE_A);
-  cp_commit();
-  const double sgn = (double)T.sign;
-  const bool crit_fin = (w.nchunks > 1 && w.crit >= 0 && w.chunk == w.crit);
-  const bool owns_init = (w.nchunks == 1) || (w.crit >= 0 ? w.chunk == w.crit : w.chunk == 0);
-  double2 acc[RM][2];
-#pragma unroll
-  for (int r = 0; r < RM; ++r) acc[r][0] = acc[r][1] = make_double2(0.0, 0.0);
-  if (crit_fin) {
-    wait_group_sum(a, w, tid);
-    if (kh == 0) {
-      const double2* Gs = a.partial + (w.slot + w.crit) * (int64_t)(GM_MT * GM_NT);
-#pragma unroll
-      for (int r = 0; r < RM; ++r)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) acc[r][e] = __ldcg(Gs + (rbase + r) * GM_NT + lane + 32 * e);
-    }
-  }
-  auto load_init = [&]() {
-    if (!(owns_init && T.oI >= 0 && kh == 0)) return;
-#pragma unroll
-    for (int r = 0; r < RM; ++r)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int c = lane + 32 * e;
-        if (rbase + r < mm && c < nn) {
-          const double2 z = __ldcg(((T.osel & 2) ? (const double2*)a.S : a.I) + T.oI +
-                                   (int64_t)(i0 + rbase + r) * T.sIi + (int64_t)(c0 + c) * T.sIc);
-          acc[r][e].x += sgn * z.x;
-          acc[r][e].y += sgn * z.y;
-        }
-      }
-  };
-  if (T.idep < 0) load_init();
-  if (tid < 32) wait_deps(a, w, T, tid);
-  __syncthreads();
-  if (T.idep >= 0) load_init();
-  if (tr) tr[3] = gtimer();
-#pragma unroll
-  for (int s = 0; s < NSTAGE - 1; ++s) {
-    if (s < nsteps) issue_b<GM_MT, GM_NT>(kt, s * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + s * STAGE_B);
-    cp_commit();
-  }
-  for (int s = 0; s < nsteps; ++s) {
-    cp_wait<NSTAGE - 2>();
-    __syncthreads();
-    const int st = s % NSTAGE;
-    const double2* As = As0 + st * STAGE_A + (8 * kh) * AS_LD + rbase;
-    const double2* Bs = Bs0 + st * STAGE_B + (8 * kh) * BS_LD + lane;
-#pragma unroll
-    for (int k = 0; k < KC / 2; ++k) {
-      const double2 b0 = Bs[k * BS_LD], b1 = Bs[k * BS_LD + 32];
-#pragma unroll
-      for (int r = 0; r < RM; ++r) {
-        const double2 av = As[k * AS_LD + r];
-        cfma(acc[r][0], av, b0);
-        cfma(acc[r][1], av, b1);
-      }
-    }
-    const int sn = s + NSTAGE - 1;
-    if (sn < nsteps) {
-      const int stn = sn % NSTAGE;
-      issue_a<GM_MT, GM_NT>(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * STAGE_A);
-      issue_b<GM_MT, GM_NT>(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * STAGE_B);
-    }
-    cp_commit();
-  }
-  cp_wait<0>();
-  __syncthreads();
-  if (tr) tr[4] = gtimer();
-  // k-half reduction through shared memory (stage buffers are free now)
-  double2* red = As0;                                // 32 x 64 complex <= NSTAGE * STAGE_A
-  if (kh == 1) {
-#pragma unroll
-    for (int r = 0; r < RM; ++r)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) red[(rbase + r) * GM_NT + lane + 32 * e] = acc[r][e];
-  }
-  __syncthreads();
-  constexpr int E = 2 * RM;
-  double2 accf[E];
-  int off[E];
-  bool own[E];
-#pragma unroll
-  for (int r = 0; r < RM; ++r)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int x = 2 * r + e;
-      off[x] = (rbase + r) * GM_NT + lane + 32 * e;
-      own[x] = (kh == 0);
-      if (kh == 0) {
-        const double2 v = red[off[x]];
-        accf[x] = make_double2(acc[r][e].x + v.x, acc[r][e].y + v.y);
-      } else {
-        accf[x] = make_double2(0.0, 0.0);
-      }
-    }
-  __syncthreads();
-  const bool finalize = crit_fin ? true : splitk_combine<E>(a, w, accf, off, own, tid, s_last);
-  if (finalize) {
-    if (kh == 0) {
-#pragma unroll
-      for (int r = 0; r < RM; ++r)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int i = rbase + r, c = lane + 32 * e;
-          if (i < mm && c < nn) {
-            const double2 v = accf[2 * r + e];
-            __stcg(((T.osel & 1) ? a.S : a.O) + T.oO + (int64_t)(i0 + i) * T.sOi + (int64_t)(c0 + c) * T.sOc,
-                   make_double2(sgn * v.x, sgn * v.y));      // O = I + sign * sum
-          }
-        }
-    }
-    __syncthreads();
-    if (tid == 0) red_release(done + T.unit0 + w.nt, 1);
-  }
-}
-
 // FP64 tensor-core MMA: D(8x8) += A(8x4, row) * B(4x8, col); per lane
 // A[g][q], B[q][g], C[g][2q], C[g][2q+1] with g = lane / 4, q = lane % 4.
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
@@ -811,7 +672,8 @@ __device__ __forceinline__ void item_body_narrow(const FlowArgs& a, const GWork&
 // [wm*RM, min(mm, (wm+1)*RM)) with RM = ceil(mm / 4) <= 8 (so the tile is
 // only as tall as the task) and column wn*32 + lane. A values are broadcast
 // shared loads, one B load feeds RM complex FMAs.
-__global__ void __launch_bounds__(256, 2)
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB)
 flow_kernel(const FlowArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* As0 = reinterpret_cast<double2*>(smem_raw);
@@ -823,7 +685,6 @@ flow_kernel(const FlowArgs a) {
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int wm = warp % GM_WM, wn = warp / GM_WM;
-  const bool ks = a.dfma_ks != 0;
   int32_t* ticket = a.counters;
   for (;;) {
     if (tid == 0) {
@@ -867,8 +728,7 @@ flow_kernel(const FlowArgs a) {
     switch (RM) {
       case 0: item_body_narrow<false, NSTAGE>(a, w, T, kt, As0, Bs0, tid, &s_last, tr, STAGE_A, STAGE_B); break;
 #define PS_RM_CASE(R) \
-      case R: if (ks) item_body_ks<R>(a, w, T, kt, As0, Bs0, tid, lane, warp, &s_last, tr); \
-              else item_body<R>(a, w, T, kt, As0, Bs0, tid, lane, wm, wn, &s_last, tr); break;
+      case R: item_body<R>(a, w, T, kt, As0, Bs0, tid, lane, wm, wn, &s_last, tr); break;
       PS_RM_CASE(1) PS_RM_CASE(2) PS_RM_CASE(3) PS_RM_CASE(4) PS_RM_CASE(5) PS_RM_CASE(6)
       PS_RM_CASE(7) PS_RM_CASE(8)
 #undef PS_RM_CASE
@@ -1145,16 +1005,25 @@ int flow_ws_resident_ctas() {
   return n;
 }
 
+template <int MINB>
+static int resident_of() {
+  int per_sm = 0, dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaFuncSetAttribute(flow_kernel<MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FLOW_SMEM);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, flow_kernel<MINB>, 256, FLOW_SMEM);
+  return sms * (per_sm > 0 ? per_sm : 1);
+}
 int flow_resident_ctas() {
   static int n = 0;
-  if (n == 0) {
-    int per_sm = 0, dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(flow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FLOW_SMEM);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, flow_kernel, 256, FLOW_SMEM);
-    n = sms * (per_sm > 0 ? per_sm : 1);
-  }
+  if (n == 0) n = resident_of<2>();
+  return n;
+}
+// tensor-core (DMMA) tables: one CTA per SM, so the consumer keeps its fragments
+// and accumulator pairs in registers without the 128-register cap
+static int flow1_resident_ctas() {
+  static int n = 0;
+  if (n == 0) n = resident_of<1>();
   return n;
 }
 
@@ -1170,9 +1039,19 @@ void launch_flow(const FlowArgs& a, int grid, cudaStream_t st) {
     flow_kernel_ws<<<g, 288, FLOW_WS_SMEM, st>>>(a);
     return;
   }
+  static const bool one = [] {
+    const char* e = std::getenv("PS_MMA_1CTA");
+    return e && e[0] == '1';
+  }();
+  if (a.mma && !a.narrow && one) {
+    int g = grid > 0 ? grid : flow1_resident_ctas();
+    if (g > a.nwork) g = (int)a.nwork;
+    flow_kernel<1><<<g, 256, FLOW_SMEM, st>>>(a);
+    return;
+  }
   int g = grid > 0 ? grid : flow_resident_ctas();
   if (g > a.nwork) g = (int)a.nwork;
-  flow_kernel<<<g, 256, FLOW_SMEM, st>>>(a);
+  flow_kernel<2><<<g, 256, FLOW_SMEM, st>>>(a);
 }
 
 // ---------------------------------------------------------------------------
