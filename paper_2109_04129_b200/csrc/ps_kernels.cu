@@ -1049,7 +1049,12 @@ void launch_flow(const FlowArgs& a, int grid, cudaStream_t st) {
     flow_kernel<1><<<g, 256, FLOW_SMEM, st>>>(a);
     return;
   }
-  int g = grid > 0 ? grid : flow_resident_ctas();
+  static const int grid_env = [] {               // experiments: persistent grid override
+    const char* e = std::getenv("PS_GRID");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int resident = flow_resident_ctas();        // also sets the dynamic shared-memory attribute
+  int g = grid > 0 ? grid : (grid_env > 0 ? grid_env : resident);
   if (g > a.nwork) g = (int)a.nwork;
   flow_kernel<2><<<g, 256, FLOW_SMEM, st>>>(a);
 }
