@@ -177,6 +177,28 @@ def run_reference(args):
     return 0
 
 
+def _ncu_traffic(config, nrhs):
+    """Mean DRAM bytes (read + write) per flow_kernel launch of one solve, from the
+    committed ncu --set full summary of this config (profiles/*/ncu_full_<cfg>_<nrhs>_*.json,
+    written by scripts/ncu_summary.py), or (None, None)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", f"ncu_full_{config}_{nrhs}_*.json")))
+    if not files:
+        return None, None
+    try:
+        with open(files[-1]) as f:
+            rows = json.load(f)
+
+        def mb(v):
+            x, u = v.split()
+            return float(x) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
+        vals = [mb(r["dram__bytes_read.sum"]) + mb(r["dram__bytes_write.sum"]) for r in rows
+                if "flow_kernel" in r.get("Kernel Name", "")]
+        return (sum(vals) / len(vals) if vals else None), os.path.relpath(files[-1], ROOT)
+    except Exception:
+        return None, None
+
+
 def _config(args, meta, nrhs, world):
     rows = getattr(args, "mode", "cols") == "rows" and world > 1
     return {"workload": f"{args.config}: {meta['desc']}", "N": meta["N"],
@@ -319,13 +341,25 @@ def main():
     fp64_peak = 37.02
     achieved = g_fl / (g_ms * 1e-3) / 1e12 if g_ms > 0 else 0.0
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    roof = {"bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
-            "frac": achieved / fp64_peak, "traffic": None,
+    launches_k = sum(prof[c]["launches"] for c in prof if c != "aux") / max(1, args.profile_steps)
+    traffic, traffic_src = _ncu_traffic(args.config, nrhs)
+    if nrhs <= 8:
+        # operator streaming (0.5 flop/B at nrhs = 1): HBM-bound; achieved = the operator
+        # bytes the launches must read (alpha panels, T_c, D^-1, far factors) / their time
+        gbs = g_by / (g_ms * 1e-3) / 1e9 if g_ms > 0 else 0.0
+        roof = {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak}
+    else:
+        roof = {"bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp64_peak}
+    roof.update({"traffic": traffic, "traffic_source": traffic_src,
+                 "algorithmic_per_launch": {"flop": g_fl / max(1, args.profile_steps) / max(1.0, launches_k),
+                                            "bytes": g_by / max(1, args.profile_steps) / max(1.0, launches_k)},
             "kernel": "flow_kernel (persistent gather-GEMM: all sweep / D^-1 / far-field launches)",
             "kernel_share_of_step": g_ms / tot_ms if tot_ms > 0 else None,
-            "peak_source": "measured FP64 ceiling on this pool's B200 (mma.sync f64 37.0 TF, DFMA loop "
-                           "34.0 TF; profiles/r1/fp64_peak_b200.json) = derived 148 SM x 64 FMA/clk x 2 x "
-                           "1.965 GHz; FP64 has no tcgen05 kind",
+            "peak_source": ("MEASURED_PEAKS.json hbm_gbs (copy bandwidth, burst)" if nrhs <= 8 else
+                            "measured FP64 ceiling on this pool's B200 (mma.sync f64 37.0 TF, DFMA loop "
+                            "34.0 TF; profiles/r1/fp64_peak_b200.json) = derived 148 SM x 64 FMA/clk x 2 x "
+                            "1.965 GHz; FP64 has no tcgen05 kind"),
             "kernel_name_in_ncu": "ps::flow_kernel",
             "hbm_view": {"operator_bytes_per_step": g_by / max(1, args.profile_steps),
                          "achieved_GBs": g_by / (g_ms * 1e-3) / 1e9 if g_ms > 0 else 0.0,
@@ -333,7 +367,7 @@ def main():
             "per_class": {c: {"ms_per_step": prof[c]["ms"] / args.profile_steps,
                               "launches_per_step": prof[c]["launches"] / args.profile_steps,
                               "gflop_per_step": prof[c]["flops"] / args.profile_steps / 1e9}
-                          for c in prof}}
+                          for c in prof}})
 
     total_cols = nrhs * world if (mode == "cols" and args.rhs_split == "weak") else nrhs_global
     value = N * total_cols / (ms * 1e-3)

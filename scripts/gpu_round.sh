@@ -13,6 +13,8 @@ timeout 300 python bench.py --config C3 --no-cpu-baseline > gpurun_out/bench_C3_
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/ncu_launches_C2_$TAG.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > /dev/null 2>&1; echo "ncu_list=$?"
 timeout 900 ncu --profile-from-start off --set full --clock-control none -k regex:flow_kernel -o /tmp/full_$TAG python scripts/ncu_solve.py --config C2 > /dev/null 2>&1; echo "ncu_full=$?"
 ncu -i /tmp/full_$TAG.ncu-rep --page raw --csv > /tmp/full_raw.csv 2>/dev/null
-python scripts/ncu_summary.py /tmp/full_$TAG.ncu-rep > gpurun_out/ncu_full_C2_$TAG.json 2>/dev/null
+python scripts/ncu_summary.py /tmp/full_$TAG.ncu-rep > gpurun_out/ncu_full_C2_181_$TAG.json 2>/dev/null
+timeout 600 ncu --profile-from-start off --set full --clock-control none -k regex:flow_kernel -o /tmp/full3_$TAG python scripts/ncu_solve.py --config C3 --nrhs 1 > /dev/null 2>&1; echo "ncu_full3=$?"
+python scripts/ncu_summary.py /tmp/full3_$TAG.ncu-rep > gpurun_out/ncu_full_C3_1_$TAG.json 2>/dev/null
 python scripts/launch_summary.py gpurun_out/ncu_launches_C2_$TAG.csv > gpurun_out/ncu_launches_C2_${TAG}_summary.json 2>/dev/null
 ls -la gpurun_out | tail -20
