@@ -441,8 +441,8 @@ struct SolvePlan {
   int64_t nrhs = 0;
   Table fwd, bwd, dinv, far1, far2;        // per-operator tables (ps_apply, PS_SOLVE=stages)
   Table prog;                              // the whole two-term solve as one dataflow program
-  DevBuf<double2> ws;                      // program workspace: Y BO W Z XT X TMP (offsets below)
-  int64_t oY = 0, oBO = 0, oW = 0, oZ = 0, oXT = 0, oX = 0, oTMP = 0;
+  DevBuf<double2> ws;                      // program workspace: Y BO W Z XT X TMP SC (offsets below)
+  int64_t oY = 0, oBO = 0, oW = 0, oZ = 0, oXT = 0, oX = 0, oTMP = 0, oSC = 0;
   DevBuf<double2> y, bo, w, u, xt, wm, tm, part, norms, stage, sc;
   int64_t nchunks = 0, rpc = 64;
   int64_t launches_per_solve = 0;
@@ -777,7 +777,25 @@ void symbolic(ps_handle* h) {
       h->max_ch_height = std::max(h->max_ch_height, h->ch_height[c]);
       h->max_ch_depth = std::max(h->max_ch_depth, h->ch_depth[c]);
     }
-    if (!h->use_chains) h->Tlen = 0;
+    if (!h->use_chains) {                          // every node its own piece (no T_c)
+      h->Tlen = 0;
+      std::vector<std::vector<int32_t>> single;
+      for (int64_t p = 0; p < nl; ++p) single.push_back({(int32_t)p});
+      h->chains.swap(single);
+      h->ch_U.assign(nl, 0);
+      h->ch_Toff.assign(nl, -1);
+      h->ch_height.assign(nl, 0);
+      h->ch_depth.assign(nl, 0);
+      for (int64_t p = 0; p < nl; ++p) {
+        h->chain_of[p] = (int32_t)p;
+        h->cpos[p] = 0;
+        h->ch_U[p] = h->nsz[p];
+        h->ch_height[p] = h->height[p];
+        h->ch_depth[p] = h->depth[p];
+      }
+      h->max_ch_height = h->max_height;
+      h->max_ch_depth = h->max_depth;
+    }
   }
   // unknown maps
   h->e2mort.resize(h->N);
@@ -1500,9 +1518,12 @@ void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
     }
     return std::max(4, std::min(32, (int)std::ceil(ks / (2.0 * resident))));
   };
-  const int nnt = (int)((R + P.NT() - 1) / P.NT());
-  const double Ltot = 2.0 * (h->max_height + 1) + 2.0 * (h->max_depth + 1) + 4.0;
-  P.key_stagger = nnt > 1 ? Ltot / nnt : 0.0;
+  P.key_stagger = 0.0;
+  P.early_keys = true;
+  // far field on the tensor-core consumer with long chunks, as in the stage tables
+  const bool far_mma = !P.narrow && env_int("PS_FAR_MMA", 1) != 0;
+  const int far_steps = P.narrow ? NARROW_STEPS() : env_int("PS_FAR_STEPS", 32);
+  sp.oSC = sp.oTMP + Ttot;                             // chain scratch (e / f), N x R
   double lev = 0;
   const int64_t Fb = h->Fbase, Pb = h->Pbase, Db = h->Dbase;
   auto leaf_of_pos = [&](int64_t m) {
@@ -1510,28 +1531,89 @@ void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
   };
   std::vector<int32_t> s1(nl, -1), s2(nl, -1), s3(nl, -1), s4(ncl, -1), s5(nl, -1), s6(nl, -1), s7(nl, -1),
       s8(nl, -1);
-  // forward sweep over buffer `buf` (in place), producers of the init / of untouched rows given
+  // Chain-collapsed sweeps inside the program (as build_chain_sweeps, all vectors and
+  // the chain scratch in the one workspace arena): per chain level an E / F stage
+  // (gathers from outside the piece, to scratch) and a Y / W stage (T_c products).
+  const int64_t Tb = h->Tbase, nc = (int64_t)h->chains.size();
+  // each sweep of the program owns a scratch region: with all stages in one launch a
+  // later sweep's gathers (F / E tasks) may run while an earlier sweep's T products
+  // still read their e / f rows (write-after-read across sweeps)
+  int64_t SC = sp.oSC;
+  std::vector<std::vector<int32_t>> lev_f(h->max_ch_height + 1), lev_b(h->max_ch_depth + 1);
+  for (int64_t c = 0; c < nc; ++c) {
+    lev_f[h->ch_height[c]].push_back((int32_t)c);
+    lev_b[h->ch_depth[c]].push_back((int32_t)c);
+  }
+  auto steps_of = [&](const std::vector<std::pair<int64_t, int64_t>>& mk) {
+    double ks = 0;
+    if (P.narrow) {
+      for (auto [m, K] : mk) ks += std::ceil((double)m / GN_MT) * std::ceil((double)K / GM_KC);
+      return std::max(2, std::min(NARROW_STEPS(), (int)std::ceil(ks / (double)resident)));
+    }
+    for (auto [m, K] : mk) ks += std::ceil((double)m / GM_MT) * std::ceil((double)R / GM_NT) * std::ceil((double)K / GM_KC);
+    return std::max(2, std::min(16, (int)std::ceil(ks / (2.0 * resident))));
+  };
+  auto by_height = [&](std::vector<std::pair<int32_t, int32_t>> v) {
+    std::stable_sort(v.begin(), v.end(), [&](const std::pair<int32_t, int32_t>& x, const std::pair<int32_t, int32_t>& y) {
+      return h->height[x.first] < h->height[y.first];
+    });
+    return v;
+  };
+  // forward sweep in place on `buf`; init_dep[p] produces the initial rows p (or none)
   auto fwd_stage = [&](int64_t buf, std::vector<int32_t>& out, const std::vector<int32_t>* init_dep) {
-    for (int L = 0; L <= h->max_height; ++L) {
-      P.key_base = lev++;
-      const int stp = steps_for(byh[L], true);
-      for (int32_t q : byh[L]) {
-        if (h->gath[q].empty()) continue;
-        const int64_t nq = h->nsz[q];
-        int32_t t = P.add_task(buf + h->eoff[q] * R, R, 1, buf + h->eoff[q] * R, R, 1, (int)nq, (int)R, +1);
-        if (init_dep) P.tasks[t].idep = (*init_dep)[q];
-        auto gl = h->gath[q];
-        std::stable_sort(gl.begin(), gl.end(), [&](const std::pair<int32_t, int32_t>& x,
-                                                   const std::pair<int32_t, int32_t>& y) {
-          return h->height[x.first] < h->height[y.first];
-        });
-        for (auto [d, idx] : gl) {
-          const int64_t nd = h->nsz[d];
-          const int32_t dep = out[d] >= 0 ? out[d] : (init_dep ? (*init_dep)[d] : -1);
-          P.add_term(t, Pb + h->Poff[d] + h->pcol[d][idx] * nd, nd, 1, buf + h->eoff[d] * R, R, 1, (int)nd, dep);
+    auto prod = [&](int32_t d) { return out[d] >= 0 ? out[d] : (init_dep ? (*init_dep)[d] : -1); };
+    std::vector<int32_t> et(nl, -1);
+    for (const auto& cl : lev_f) {
+      std::vector<std::pair<int64_t, int64_t>> mk;
+      for (int32_t c : cl)
+        for (int32_t p : h->chains[c]) {
+          int64_t K = 0;
+          for (auto [d, idx] : h->gath[p])
+            if (h->chain_of[d] != c) K += h->nsz[d];
+          mk.push_back({h->nsz[p], K});
         }
-        P.tile(t, -1, stp);
-        out[q] = t;
+      const int stpE = steps_of(mk);
+      P.key_base = lev++;
+      for (int32_t c : cl) {
+        const bool single = h->chains[c].size() == 1;
+        for (int32_t p : h->chains[c]) {
+          std::vector<std::pair<int32_t, int32_t>> gl;
+          for (auto [d, idx] : h->gath[p])
+            if (h->chain_of[d] != c) gl.push_back({d, idx});
+          if (single && gl.empty()) continue;
+          const int64_t np_ = h->nsz[p];
+          const int64_t o = (single ? buf : SC) + h->eoff[p] * R;
+          int32_t t = P.add_task(o, R, 1, buf + h->eoff[p] * R, R, 1, (int)np_, (int)R, +1);
+          if (init_dep) P.tasks[t].idep = (*init_dep)[p];
+          for (auto [d, idx] : by_height(gl)) {
+            const int64_t nd = h->nsz[d];
+            P.add_term(t, Pb + h->Poff[d] + h->pcol[d][idx] * nd, nd, 1, buf + h->eoff[d] * R, R, 1, (int)nd, prod(d));
+          }
+          P.tile(t, -1, stpE);
+          (single ? out : et)[p] = t;
+        }
+      }
+      mk.clear();
+      for (int32_t c : cl)
+        if (h->chains[c].size() > 1)
+          for (int32_t p : h->chains[c]) mk.push_back({h->nsz[p], h->cpos[p]});
+      const int stpY = steps_of(mk);
+      P.key_base = lev++;
+      for (int32_t c : cl) {
+        if (h->chains[c].size() == 1) continue;
+        const int64_t U = h->ch_U[c], To = Tb + h->ch_Toff[c];
+        for (size_t i = 0; i < h->chains[c].size(); ++i) {
+          const int32_t p = h->chains[c][i];
+          const int64_t np_ = h->nsz[p];
+          int32_t t = P.add_task(buf + h->eoff[p] * R, R, 1, SC + h->eoff[p] * R, R, 1, (int)np_, (int)R, +1);
+          P.tasks[t].idep = et[p];
+          for (size_t j = 0; j < i; ++j) {
+            const int32_t q = h->chains[c][j];
+            P.add_term(t, To + h->cpos[p] + h->cpos[q] * U, 1, U, SC + h->eoff[q] * R, R, 1, (int)h->nsz[q], et[q]);
+          }
+          P.tile(t, 0, stpY);
+          out[p] = t;
+        }
       }
     }
   };
@@ -1548,27 +1630,67 @@ void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
       out[p] = t;
     }
   };
+  // backward sweep out_buf = R init; init_dep[p] produces the rows p of init
   auto bwd_stage = [&](int64_t init, int64_t out_buf, std::vector<int32_t>& out,
                        const std::vector<int32_t>& init_dep) {
-    for (int L = 0; L <= h->max_depth; ++L) {
-      P.key_base = lev++;
-      const int stp = steps_for(byd[L], false);
-      for (int32_t p : byd[L]) {
-        const int64_t np_ = h->nsz[p];
-        int32_t t = P.add_task(out_buf + h->eoff[p] * R, R, 1, init + h->eoff[p] * R, R, 1, (int)np_, (int)R, +1);
-        P.tasks[t].idep = init_dep[p];
-        for (size_t i = 0; i < h->st[p].size(); ++i) {
-          const int32_t j = h->st[p][i];
-          P.add_term(t, Pb + h->Poff[p] + h->pcol[p][i] * np_, 1, np_, out_buf + h->eoff[j] * R, R, 1,
-                     (int)h->nsz[j], out[j]);
+    std::vector<int32_t> ft(nl, -1);
+    for (const auto& cl : lev_b) {
+      std::vector<std::pair<int64_t, int64_t>> mk;
+      for (int32_t c : cl)
+        for (int32_t p : h->chains[c]) {
+          int64_t K = 0;
+          for (int32_t j : h->st[p])
+            if (h->chain_of[j] != c) K += h->nsz[j];
+          mk.push_back({h->nsz[p], K});
         }
-        P.tile(t, +1, stp);
-        out[p] = t;
+      const int stpF = steps_of(mk);
+      P.key_base = lev++;
+      for (int32_t c : cl) {
+        const bool single = h->chains[c].size() == 1;
+        for (int32_t p : h->chains[c]) {
+          const int64_t np_ = h->nsz[p];
+          const int64_t o = (single ? out_buf : SC) + h->eoff[p] * R;
+          int32_t t = P.add_task(o, R, 1, init + h->eoff[p] * R, R, 1, (int)np_, (int)R, +1);
+          P.tasks[t].idep = init_dep[p];
+          for (size_t i = 0; i < h->st[p].size(); ++i) {
+            const int32_t j = h->st[p][i];
+            if (h->chain_of[j] == c) continue;
+            P.add_term(t, Pb + h->Poff[p] + h->pcol[p][i] * np_, 1, np_, out_buf + h->eoff[j] * R, R, 1,
+                       (int)h->nsz[j], out[j]);
+          }
+          P.tile(t, +1, stpF);
+          (single ? out : ft)[p] = t;
+        }
+      }
+      mk.clear();
+      for (int32_t c : cl)
+        if (h->chains[c].size() > 1)
+          for (int32_t p : h->chains[c]) mk.push_back({h->nsz[p], h->ch_U[c] - h->cpos[p] - h->nsz[p]});
+      const int stpW = steps_of(mk);
+      P.key_base = lev++;
+      for (int32_t c : cl) {
+        if (h->chains[c].size() == 1) continue;
+        const int64_t U = h->ch_U[c], To = Tb + h->ch_Toff[c];
+        const auto& ch = h->chains[c];
+        for (size_t i = 0; i < ch.size(); ++i) {
+          const int32_t p = ch[i];
+          const int64_t np_ = h->nsz[p];
+          int32_t t = P.add_task(out_buf + h->eoff[p] * R, R, 1, SC + h->eoff[p] * R, R, 1, (int)np_, (int)R, +1);
+          P.tasks[t].idep = ft[p];
+          for (size_t j = i + 1; j < ch.size(); ++j) {
+            const int32_t q = ch[j];
+            P.add_term(t, To + h->cpos[q] + h->cpos[p] * U, U, 1, SC + h->eoff[q] * R, R, 1, (int)h->nsz[q], ft[q]);
+          }
+          P.tile(t, 0, stpW);
+          out[p] = t;
+        }
       }
     }
   };
+  SC = sp.oSC;
   fwd_stage(sp.oY, s1, nullptr);                                         // S1
   dinv_stage(sp.oY, sp.oBO, -1, +1, s2, s1, nullptr);                    // S2
+  SC = sp.oSC + NR;
   bwd_stage(sp.oBO, sp.oW, s3, s2);                                      // S3
   // S4 far stage 1: per cluster, rows gathered per leaf from W (elimination order)
   P.key_base = lev++;
@@ -1576,12 +1698,13 @@ void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
     if (h->cl_sr[c] == 0) continue;
     const int64_t sr = h->cl_sr[c], a0 = h->cl_start[c], len = h->cl_len[c];
     int32_t t = P.add_task(toff[c], R, 1, -1, 0, 0, (int)sr, (int)R, +1);
+    if (far_mma) P.tasks[t].osel |= 4;
     for (int64_t l = leaf_of_pos(a0); l < nl && h->leaf_off[l] < a0 + len; ++l) {
       const int32_t pos = h->pos_of[l];
       P.add_term(t, Fb + h->cl_soff[c] + (h->leaf_off[l] - a0) * sr, 1, sr, sp.oW + h->eoff[pos] * R, R, 1,
                  (int)(h->leaf_off[l + 1] - h->leaf_off[l]), s3[pos]);
     }
-    P.tile(t);
+    P.tile(t, 0, far_steps);
     s4[c] = t;
   }
   // S5 far stage 2: per leaf, written in elimination order into Z
@@ -1622,20 +1745,31 @@ void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
       const int32_t pos = h->pos_of[l];
       const int64_t nlf = h->leaf_off[l + 1] - h->leaf_off[l];
       int32_t t = P.add_task(sp.oZ + h->eoff[pos] * R, R, 1, -1, 0, 0, (int)nlf, (int)R, +1);
+      if (far_mma) P.tasks[t].osel |= 4;
       for (auto& g : contrib[l]) P.add_term(t, g.oA, g.sAi, g.sAk, g.oB, R, 1, g.K, g.dep);
-      P.tile(t);
+      P.tile(t, 0, far_steps);
       s5[pos] = t;
     }
   }
+  SC = sp.oSC + 2 * NR;
   fwd_stage(sp.oZ, s6, &s5);                                             // S6
   std::vector<int32_t> zfin(nl);
   for (int64_t p = 0; p < nl; ++p) zfin[p] = s6[p] >= 0 ? s6[p] : s5[p];
   dinv_stage(sp.oZ, sp.oXT, sp.oBO, -1, s7, zfin, &s2);                  // S7: xt = bo - D^-1 z
+  SC = sp.oSC + 3 * NR;
   bwd_stage(sp.oXT, sp.oX, s8, s7);                                      // S8
   P.sort_by_key();
   P.close_batch();
   P.upload(h->stream);
-  sp.ws.alloc(6 * NR + std::max<int64_t>(Ttot, 1));
+  sp.ws.alloc(10 * NR + std::max<int64_t>(Ttot, 1));
+}
+
+bool use_stages() {
+  static const bool v = [] {
+    const char* e = std::getenv("PS_SOLVE");
+    return e && std::string(e) == "stages";
+  }();
+  return v;
 }
 
 SolvePlan& get_plan(ps_handle* h, int64_t nrhs) {
@@ -1643,8 +1777,7 @@ SolvePlan& get_plan(ps_handle* h, int64_t nrhs) {
     h->plan.reset();
     auto sp = std::make_unique<SolvePlan>();
     build_solve_plan(h, *sp, nrhs);
-    const char* e = std::getenv("PS_SOLVE");
-    if (e && std::string(e) == "program") build_program(h, *sp, nrhs);
+    if (!use_stages()) build_program(h, *sp, nrhs);
     h->plan = std::move(sp);
   }
   return *h->plan;
@@ -2335,12 +2468,10 @@ ps_status ps_solve(ps_handle* h, int64_t nrhs, const void* B, int64_t ldb, void*
       ldb_d = N;
     }
     CK(cudaEventRecord(h->ev0, s));
-    // default: one launch per stage (measured faster on C2 than the single-launch
-    // program); PS_SOLVE=program selects the whole-solve dataflow program
-    static const bool stages_env = [] {
-      const char* e = std::getenv("PS_SOLVE");
-      return !(e && std::string(e) == "program");
-    }();
+    // default: the whole solve as one dataflow launch (build_program: chain-collapsed
+    // sweeps, E-order far field, producer-keyed tickets); PS_SOLVE=stages runs one
+    // launch per operator (the tables ps_apply uses)
+    static const bool stages_env = use_stages();
     double2* xres = sp.xt.p;   // where x ends up (elimination order)
     if (!stages_env) {
       // the whole solve as one dataflow program (build_program)

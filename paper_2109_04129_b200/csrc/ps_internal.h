@@ -24,7 +24,8 @@ struct GTask {
   int32_t b_kmajor;        // 1: B's unit stride is along k, 0: along c
   int32_t idep;            // task (same launch) producing the init rows I; -1: none
   int32_t osel;            // bit 0: O offsets address the scratch base S instead of O;
-                           // bit 1: I offsets address S instead of I
+                           // bit 1: I offsets address S instead of I;
+                           // bit 2: wide tile on the FP64 tensor-core consumer (per task)
 };
 
 // A segment of a task's K dimension: K_s consecutive k's starting at virtual

@@ -717,7 +717,7 @@ flow_kernel(const FlowArgs a) {
       }
     }
     __syncthreads();
-    if (!a.narrow && a.mma) {
+    if (!a.narrow && (a.mma || (T.osel & 4))) {
       switch ((mm + 7) / 8) {
         case 1: item_body_dmma<1>(a, w, T, kt, As0, Bs0, tid, lane, warp, &s_last, tr); break;
         case 2: item_body_dmma<2>(a, w, T, kt, As0, Bs0, tid, lane, warp, &s_last, tr); break;

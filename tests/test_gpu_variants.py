@@ -7,7 +7,7 @@
   PS_MMA=dmma      every wide table on the FP64 tensor-core consumer
   PS_MMA=dfma      every wide table on the DFMA consumer (far field included)
   PS_MMA_1CTA=1    tensor-core tables on the one-CTA-per-SM kernel instance
-  PS_SOLVE=program the whole solve as one dataflow launch
+  PS_SOLVE=stages  one launch per operator instead of the single-launch program
 
 Each must match the oracle to the north-star bar (relative L2 <= 1e-11 per RHS).
 """
@@ -48,7 +48,7 @@ def _run(path, nrhs, env, out):
 
 
 @pytest.mark.parametrize("env", [{"PS_CHAINS": "0"}, {"PS_NARROW_WS": "0"}, {"PS_MMA": "dmma"},
-                                 {"PS_MMA": "dfma"}, {"PS_MMA_1CTA": "1"}, {"PS_SOLVE": "program"}, {}],
+                                 {"PS_MMA": "dfma"}, {"PS_MMA_1CTA": "1"}, {"PS_SOLVE": "stages"}, {}],
                          ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default")
 @pytest.mark.parametrize("nrhs", [1, 70])
 def test_variant_matches_oracle(cfgdata, tmp_path, env, nrhs):
