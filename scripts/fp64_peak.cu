@@ -79,6 +79,40 @@ __global__ void dmma16816_kernel(double* out, int iters) {
   if (s == 12345.678) out[0] = s;
 }
 
+// mixed: even warps run DFMA chains, odd warps m8n8k4 DMMA, concurrently — does the FP64
+// vector pipe add to the tensor pipe, or do they share one ceiling?
+__global__ void mixed_kernel(double* out, int iters_f, int iters_m) {
+  const int warp = threadIdx.x >> 5;
+  if (warp & 1) {
+    double a = threadIdx.x * 1e-3, b = 1.0001;
+    double c[4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) c[i][0] = c[i][1] = 0.0;
+    for (int it = 0; it < iters_m; ++it) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s += c[i][0] + c[i][1];
+    if (s == 12345.678) out[0] = s;
+  } else {
+    double x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * 1e-3 + i;
+    for (int it = 0; it < iters_f; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[i] = fma(x[i], 1.0000001, 1e-9);
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += x[i];
+    if (s == 12345.678) out[0] = s;
+  }
+}
+
 int main() {
   double* d;
   CK(cudaMalloc(&d, 8));
@@ -128,6 +162,19 @@ int main() {
     cudaEventElapsedTime(&ms, e0, e1);
     double fl = 2.0 * 16 * 8 * 16 * 2.0 * (iters / 4) * (double)blocks * (threads / 32);
     printf("{\"kernel\": \"dmma_m16n8k16\", \"tflops\": %.2f, \"ms\": %.3f}\n", fl / ms / 1e9, ms);
+  }
+  // mixed: iteration counts chosen so each half alone would take about the same time
+  for (int ratio = 0; ratio < 3; ++ratio) {
+    const int itf = iters, itm = iters * (ratio == 0 ? 1 : ratio == 1 ? 2 : 4) / 2;
+    cudaEventRecord(e0);
+    mixed_kernel<<<blocks, threads>>>(d, itf, itm);
+    cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1));
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double warps_half = (double)blocks * (threads / 64);
+    const double fl_f = 2.0 * 8 * itf * warps_half * 32, fl_m = 2.0 * 8 * 8 * 4 * 4.0 * itm * warps_half;
+    printf("{\"kernel\": \"mixed dfma+dmma\", \"tflops\": %.2f, \"dfma_tf\": %.2f, \"dmma_tf\": %.2f, \"ms\": %.3f}\n",
+           (fl_f + fl_m) / ms / 1e9, fl_f / ms / 1e9, fl_m / ms / 1e9, ms);
   }
   printf("{\"sms\": %d, \"clock_khz\": %d}\n", sms, clk);
   return 0;
