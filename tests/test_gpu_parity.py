@@ -218,3 +218,23 @@ def test_solve_c4_plane_waves(cfgdata):
     cols = [0, 90, 180, 270]                 # theta-pol and phi-pol incidences
     _solve_check(meta["hm"], np.asfortranarray(B[:, cols]), check_host=False)
     _ops_check(meta["hm"], nrhs=2)
+
+
+@pytest.mark.slow
+def test_solve_c4_bench_config_sampled(cfgdata):
+    """BASELINE config 3 in the bench's launch configuration (all 360 RHS in one solve:
+    wide tiles, the single-launch program), checked on sampled columns the oracle
+    solves one by one (columns are independent problems)."""
+    meta = cfgdata("C4")
+    B, _ = read_rhs(meta["rhs"])
+    H, S, h = _load(meta["hm"])
+    Bd = _dev(np.asfortranarray(B))
+    Xd = torch.empty_like(Bd)
+    st, rep = h.solve(Bd, Xd)
+    x = _host(Xd)
+    cols = [0, 1, 90, 179, 180, 181, 270, 359]
+    ref = solve(H, S, np.asfortranarray(B[:, cols]))
+    err = rel_l2_cols(x[:, cols], ref.x)
+    assert err.max() <= TOL, err.max()
+    assert np.allclose(rep["it0"][cols], ref.it0, rtol=1e-11)
+    assert np.allclose(rep["it1"][cols], ref.it1, rtol=1e-10)
