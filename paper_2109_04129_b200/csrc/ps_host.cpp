@@ -273,7 +273,7 @@ struct Table {
   // the others); the NEAR - 1 segments next to it (the next-latest
   // dependencies) become single-segment chunks in subgroups of their own, the
   // bulk is chunked normally and combined in subgroups of SUBG.
-  static inline const int NEAR = env_int("PS_NEAR", 4), SUBG = env_int("PS_SUBG", 16);
+  static inline const int NEAR = env_int("PS_NEAR", 1), SUBG = env_int("PS_SUBG", 16);
   // segments in the critical chunk: the chain predecessor AND the one before it,
   // so the group sum the critical chunk adds never waits on a just-finished
   // producer (its latest input is >= 2 hops old)
@@ -1554,8 +1554,9 @@ void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
       for (auto [m, K] : mk) ks += std::ceil((double)m / GN_MT) * std::ceil((double)K / GM_KC);
       return std::max(2, std::min(NARROW_STEPS(), (int)std::ceil(ks / (double)resident)));
     }
+    static const int pmax = env_int("PS_SWEEP_MAXSTEPS", 16), pipc = env_int("PS_SWEEP_IPC", 2);
     for (auto [m, K] : mk) ks += std::ceil((double)m / GM_MT) * std::ceil((double)R / GM_NT) * std::ceil((double)K / GM_KC);
-    return std::max(2, std::min(16, (int)std::ceil(ks / (2.0 * resident))));
+    return std::max(2, std::min(pmax, (int)std::ceil(ks / ((double)pipc * resident))));
   };
   auto by_height = [&](std::vector<std::pair<int32_t, int32_t>> v) {
     std::stable_sort(v.begin(), v.end(), [&](const std::pair<int32_t, int32_t>& x, const std::pair<int32_t, int32_t>& y) {
