@@ -1554,7 +1554,7 @@ void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
       for (auto [m, K] : mk) ks += std::ceil((double)m / GN_MT) * std::ceil((double)K / GM_KC);
       return std::max(2, std::min(NARROW_STEPS(), (int)std::ceil(ks / (double)resident)));
     }
-    static const int pmax = env_int("PS_SWEEP_MAXSTEPS", 16), pipc = env_int("PS_SWEEP_IPC", 2);
+    static const int pmax = env_int("PS_SWEEP_MAXSTEPS", 32), pipc = env_int("PS_SWEEP_IPC", 1);
     for (auto [m, K] : mk) ks += std::ceil((double)m / GM_MT) * std::ceil((double)R / GM_NT) * std::ceil((double)K / GM_KC);
     return std::max(2, std::min(pmax, (int)std::ceil(ks / ((double)pipc * resident))));
   };
