@@ -283,8 +283,10 @@ struct Table {
     GTask& t = tasks[task];
     // consumer per task: tall tasks (>= 32 rows: full 32-row tiles, little 8-row
     // padding) on the FP64 tensor cores, short ones (single 16-19 row leaves) on DFMA
-    static const int auto_mma = env_int("PS_AUTO_MMA", 1);
-    if (auto_mma && !narrow && t.m >= 32) t.osel |= 4;
+    static const int auto_mma = env_int("PS_AUTO_MMA", 1), mma_rows = env_int("PS_MMA_MINROWS", 32);
+    if (auto_mma && !narrow && t.m >= mma_rows) t.osel |= 4;
+    static const int iso_env = env_int("PS_ISOLATE", 0);
+    if (!iso_env) isolate = 0;
     t.n_mt = (t.m + MT() - 1) / MT();
     const int nmt = t.n_mt, nnt = (t.n + NT() - 1) / NT();
     t.unit0 = n_units;
