@@ -238,3 +238,21 @@ def test_solve_c4_bench_config_sampled(cfgdata):
     assert err.max() <= TOL, err.max()
     assert np.allclose(rep["it0"][cols], ref.it0, rtol=1e-11)
     assert np.allclose(rep["it1"][cols], ref.it1, rtol=1e-10)
+
+
+@pytest.mark.parametrize("nrhs", [8, 9, 63, 64, 65, 128, 129, 200])
+def test_solve_column_tile_boundaries(cfgdata, nrhs):
+    """nrhs at and around the narrow / wide column-tile edges (8, 64): ragged last
+    tiles, the narrow -> wide switch, several column tiles per task."""
+    meta = cfgdata("C1")
+    H, S, h = _load(meta["hm"])
+    B = random_rhs(H.N, nrhs, 17)
+    Bd = _dev(B)
+    Xd = torch.empty_like(Bd)
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        st, rep = h.solve(Bd, Xd)
+    ref = solve(H, S, B)
+    assert rel_l2_cols(_host(Xd), ref.x).max() <= TOL
+    assert np.allclose(rep["it0"], ref.it0, rtol=1e-11)
