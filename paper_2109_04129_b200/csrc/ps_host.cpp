@@ -720,7 +720,7 @@ void symbolic(ps_handle* h) {
   h->Dlen = D;
   // chains of the elimination tree (see ps_handle), bottom-up by position
   {
-    const int64_t tmax = env_int("PS_TMAX", 2048);
+    const int64_t tmax = env_int("PS_TMAX", 4096);
     h->use_chains = env_int("PS_CHAINS", 1) != 0;
     std::vector<int32_t> nch(nl, 0);
     for (int64_t p = 0; p < nl; ++p)

@@ -92,7 +92,7 @@ def test_symbolic_fill_matches_oracle(case, cfgdata, synthfile):
     assert info["N"] == S.N
 
 
-def _chains_from_oracle(S, tmax=2048):
+def _chains_from_oracle(S, tmax=4096):
     """Chain pieces of the elimination tree, written from the definition
     (DESIGN.md §6): maximal paths p -> parent(p) whose upper nodes have a single
     child, cut before exceeding tmax unknowns. Returns (pieces, chain-graph height)."""
