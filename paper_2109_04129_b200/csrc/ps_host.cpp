@@ -1318,15 +1318,8 @@ void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
   const int64_t nl = h->nl;
   const int64_t R = nrhs;
   sp.nrhs = nrhs;
-  // forward sweep (gather form of Eq. 24), batches by height:
-  //   y_q = y_q + sum_{d: q in struct(d)} alpha_dq^T y_d
-  std::vector<std::vector<int32_t>> byh(h->max_height + 1), byd(h->max_depth + 1);
-  for (int64_t p = 0; p < nl; ++p) {
-    byh[h->height[p]].push_back((int32_t)p);
-    byd[h->depth[p]].push_back((int32_t)p);
-  }
   const int narrow = (R <= 8) ? 1 : 0;
-  if (h->use_chains) sp.sc.alloc(h->N * R);        // chain-stage scratch (e / f)
+  sp.sc.alloc(h->N * R);                           // chain-stage scratch (e / f)
   for (Table* tb : {&sp.fwd, &sp.bwd, &sp.dinv, &sp.far1, &sp.far2}) {
     tb->narrow = narrow;
     if (narrow) tb->chunk_steps = NARROW_STEPS();
@@ -1335,81 +1328,9 @@ void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
     sp.far1.chunk_steps = sp.far2.chunk_steps = env_int("PS_FAR_STEPS", 32);
     sp.far1.mma = sp.far2.mma = env_int("PS_FAR_MMA", 1);
   }
-  std::vector<int32_t> ftask(nl, -1), btask(nl, -1);
-  // narrow levels (the separator chains) get small split-K chunks so each hop
-  // waits on ~1-4 k-steps; wide levels keep large chunks (less overhead)
-  // split-K chunk size per elimination level: aim at ~2 work items per
-  // resident CTA for the level's total k-steps (clamped to [4, 32] steps), so
-  // thin chain levels get short chunks (short hops) and heavy levels long ones
-  // (less per-item overhead). Narrow tiles stream the operator: short chunks.
   const int resident = flow_resident_ctas();
-  auto steps_for = [&](const std::vector<int32_t>& lev_nodes, bool fwd) {
-    if (narrow) return NARROW_STEPS();
-    double ks = 0;
-    const int MTw = GM_MT, NTw = GM_NT;
-    for (int32_t p : lev_nodes) {
-      double K = 0;
-      if (fwd) { for (auto [d, idx] : h->gath[p]) K += h->nsz[d]; }
-      else K = (double)h->S[p];
-      ks += std::ceil((double)h->nsz[p] / MTw) * std::ceil((double)R / NTw) * std::ceil(K / GM_KC);
-    }
-    const int st = (int)std::ceil(ks / (2.0 * resident));
-    return std::max(4, std::min(32, st));
-  };
-  // wide levels (enough tiles to fill the machine without split-K): no critical-chunk
-  // isolation and long chunks (PS_WIDE = tiles per resident CTA in percent, 0 = off)
-  const int wide_pct = env_int("PS_WIDE", 0), wide_steps = env_int("PS_WIDE_STEPS", 32);
-  auto is_wide = [&](const std::vector<int32_t>& nodes) {
-    if (wide_pct <= 0 || narrow) return false;
-    double tiles = 0;
-    for (int32_t p : nodes) tiles += std::ceil((double)h->nsz[p] / GM_MT) * std::ceil((double)R / GM_NT);
-    return tiles * 100.0 >= (double)wide_pct * resident;
-  };
-  if (h->use_chains) {
-    build_chain_sweeps(h, sp, R, narrow, resident);
-  } else {
-    for (int lev = 0; lev <= h->max_height; ++lev) {
-      const bool wide = is_wide(byh[lev]);
-      const int stp = wide ? wide_steps : steps_for(byh[lev], true);
-      for (int32_t q : byh[lev]) {
-        if (h->gath[q].empty()) continue;
-        const int64_t nq = h->nsz[q];
-        int32_t t = sp.fwd.add_task(h->eoff[q] * R, R, 1, h->eoff[q] * R, R, 1, (int)nq, (int)R, +1);
-        // segments in producer completion order (height), so the chained prefix
-        // accumulation follows readiness; the last one (the chain child) is isolated
-        auto gl = h->gath[q];
-        std::stable_sort(gl.begin(), gl.end(), [&](const std::pair<int32_t, int32_t>& x,
-                                                   const std::pair<int32_t, int32_t>& y) {
-          return h->height[x.first] < h->height[y.first];
-        });
-        for (auto [d, idx] : gl) {
-          const int64_t nd = h->nsz[d];
-          sp.fwd.add_term(t, h->Poff[d] + h->pcol[d][idx] * nd, nd, 1, h->eoff[d] * R, R, 1, (int)nd,
-                          ftask[d]);
-        }
-        sp.fwd.tile(t, wide ? 0 : -1, stp);
-        ftask[q] = t;
-      }
-    }
-    sp.fwd.close_batch();
-    // backward sweep (Eq. 26), ordered by depth: w_p = v_p + sum_j alpha_pj w_j
-    for (int lev = 0; lev <= h->max_depth; ++lev) {
-      const bool wide = is_wide(byd[lev]);
-      const int stp = wide ? wide_steps : steps_for(byd[lev], false);
-      for (int32_t p : byd[lev]) {
-        const int64_t np_ = h->nsz[p];
-        int32_t t = sp.bwd.add_task(h->eoff[p] * R, R, 1, h->eoff[p] * R, R, 1, (int)np_, (int)R, +1);
-        for (size_t i = 0; i < h->st[p].size(); ++i) {
-          const int32_t j = h->st[p][i];
-          sp.bwd.add_term(t, h->Poff[p] + h->pcol[p][i] * np_, 1, np_, h->eoff[j] * R, R, 1,
-                          (int)h->nsz[j], btask[j]);
-        }
-        sp.bwd.tile(t, wide ? 0 : +1, stp);
-        btask[p] = t;
-      }
-    }
-    sp.bwd.close_batch();
-  }
+  // forward sweep (gather form of Eq. 24) and backward sweep (Eq. 26), chain-collapsed
+  build_chain_sweeps(h, sp, R, narrow, resident);     // PS_CHAINS=0: every node its own piece
   // D^{-1} (Eq. 32), one batch
   for (int64_t p = 0; p < nl; ++p) {
     const int64_t np_ = h->nsz[p];
