@@ -461,7 +461,7 @@ struct DistPlan {
   int64_t nrhs = 0;
   Table fwdIA, fwdSA, dinvA, bwdA, far1, far2, fwdIC, fwdSC, dinvC, bwdC;
   DevBuf<double2> ws, part, sums, scratch;
-  int64_t oY = 0, oBO = 0, oW = 0, oZ = 0, oXT = 0, oX = 0, oTMP = 0;
+  int64_t oY = 0, oBO = 0, oW = 0, oZ = 0, oXT = 0, oX = 0, oTMP = 0, oSC = 0;
   int64_t rpc = 64, nchI = 0, nchS = 0;
 };
 
@@ -1858,6 +1858,7 @@ void build_dist_plan(ps_handle* h, DistPlan& dp, int64_t R) {
   std::vector<int64_t> toff(ncl);
   int64_t Ttot = 0;
   for (int64_t c = 0; c < ncl; ++c) { toff[c] = dp.oTMP + Ttot; Ttot += h->cl_sr[c] * R; }
+  dp.oSC = dp.oTMP + Ttot;                           // chain scratch (e / f) of the sweeps
   const int narrow = (R <= 8) ? 1 : 0;
   for (Table* tb : {&dp.fwdIA, &dp.fwdSA, &dp.dinvA, &dp.bwdA, &dp.far1, &dp.far2, &dp.fwdIC, &dp.fwdSC,
                     &dp.dinvC, &dp.bwdC}) {
@@ -1885,33 +1886,99 @@ void build_dist_plan(ps_handle* h, DistPlan& dp, int64_t R) {
     return std::max(4, std::min(32, (int)std::ceil(ks / (2.0 * resident))));
   };
   const int64_t Pb = h->Pbase, Db = h->Dbase, Fb = h->Fbase;
-  // forward sweep (gather form of Eq. 24), in place on `buf`; interior = this
-  // rank's subtrees plus their partial sums into separator rows, else the
-  // separator nodes fed by separator descendants only
+  // Chain-collapsed sweeps of the partitioned solve (as build_chain_sweeps): the
+  // chain pieces are cut where the owner changes (interior of this rank / another
+  // rank / separator); a cut piece uses the principal sub-block of its chain's T_c
+  // (the inverse of a block-triangular matrix restricted to a contiguous range of
+  // block rows is the inverse of that range's block). Every table gets producer keys.
+  struct DPiece { int32_t c, i0, i1, own; };           // chain c nodes [i0, i1), owner value
+  std::vector<DPiece> dpieces;
+  std::vector<int32_t> dpiece_of(nl, -1);
+  for (size_t c = 0; c < h->chains.size(); ++c) {
+    const auto& ch = h->chains[c];
+    size_t i = 0;
+    while (i < ch.size()) {
+      size_t j = i + 1;
+      while (j < ch.size() && h->owner[ch[j]] == h->owner[ch[i]]) ++j;
+      for (size_t q = i; q < j; ++q) dpiece_of[ch[q]] = (int32_t)dpieces.size();
+      dpieces.push_back({(int32_t)c, (int32_t)i, (int32_t)j, h->owner[ch[i]]});
+      i = j;
+    }
+  }
+  const int64_t SCo = dp.oSC;
+  const int wsteps = narrow ? NARROW_STEPS() : 16;
+  auto piece_nodes = [&](const DPiece& P) {
+    std::vector<int32_t> v;
+    for (int32_t i = P.i0; i < P.i1; ++i) v.push_back(h->chains[P.c][i]);
+    return v;
+  };
+  // forward sweep in place on `buf`; interior: this rank's pieces (gathers from its own
+  // subtrees) and then the partial sums into separator rows; else the separator pieces
+  // (gathers from separator descendants; interior partial sums are already in buf)
   auto fwd = [&](Table& T, int64_t buf, bool interior) {
-    std::vector<int32_t> ft(nl, -1);
-    for (int L = 0; L <= h->max_height; ++L) {
-      const int stp = steps_for(byh[L], true);
-      for (int32_t q : byh[L]) {
-        if (interior ? !(mine(q) || sep(q)) : !sep(q)) continue;
+    T.early_keys = true;
+    double key = 0;
+    std::vector<int32_t> ft(nl, -1), et(nl, -1);
+    std::vector<int32_t> order;
+    for (size_t k = 0; k < dpieces.size(); ++k)
+      if (interior ? dpieces[k].own == g : dpieces[k].own < 0) order.push_back((int32_t)k);
+    std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) {
+      return h->height[h->chains[dpieces[x].c][dpieces[x].i0]] < h->height[h->chains[dpieces[y].c][dpieces[y].i0]];
+    });
+    for (int32_t k : order) {
+      const DPiece& Pc = dpieces[k];
+      const auto nodes = piece_nodes(Pc);
+      const bool single = nodes.size() == 1;
+      T.key_base = key++;
+      for (int32_t p : nodes) {
+        std::vector<std::pair<int32_t, int32_t>> gl;
+        for (auto [d, idx] : h->gath[p])
+          if (dpiece_of[d] != k && (interior ? mine(d) : sep(d))) gl.push_back({d, idx});
+        if (single && gl.empty()) continue;
+        const int64_t np_ = h->nsz[p];
+        int32_t t = T.add_task((single ? buf : SCo) + h->doff[p] * R, R, 1, buf + h->doff[p] * R, R, 1, (int)np_,
+                               (int)R, +1);
+        for (auto [d, idx] : gl) {
+          const int64_t nd = h->nsz[d];
+          T.add_term(t, Pb + h->Poff[d] + h->pcol[d][idx] * nd, nd, 1, buf + h->doff[d] * R, R, 1, (int)nd, ft[d]);
+        }
+        T.tile(t, 0, wsteps);
+        (single ? ft : et)[p] = t;
+      }
+      if (single) continue;
+      const int64_t U = h->ch_U[Pc.c], To = h->Tbase + h->ch_Toff[Pc.c];
+      T.key_base = key++;
+      for (size_t i = 0; i < nodes.size(); ++i) {
+        const int32_t p = nodes[i];
+        const int64_t np_ = h->nsz[p];
+        int32_t t = T.add_task(buf + h->doff[p] * R, R, 1, SCo + h->doff[p] * R, R, 1, (int)np_, (int)R, +1);
+        T.tasks[t].idep = et[p];
+        for (size_t j = 0; j < i; ++j) {
+          const int32_t q = nodes[j];
+          T.add_term(t, To + h->cpos[p] + h->cpos[q] * U, 1, U, SCo + h->doff[q] * R, R, 1, (int)h->nsz[q], et[q]);
+        }
+        T.tile(t, 0, wsteps);
+        ft[p] = t;
+      }
+    }
+    if (interior) {                                   // partial sums into the separator rows
+      T.key_base = key++;
+      for (int64_t q = 0; q < nl; ++q) {
+        if (!sep(q)) continue;
         std::vector<std::pair<int32_t, int32_t>> gl;
         for (auto [d, idx] : h->gath[q])
-          if (interior ? mine(d) : sep(d)) gl.push_back({d, idx});
+          if (mine(d)) gl.push_back({d, idx});
         if (gl.empty()) continue;
-        std::stable_sort(gl.begin(), gl.end(), [&](const std::pair<int32_t, int32_t>& x,
-                                                   const std::pair<int32_t, int32_t>& y) {
-          return h->height[x.first] < h->height[y.first];
-        });
         const int64_t nq = h->nsz[q];
         int32_t t = T.add_task(buf + h->doff[q] * R, R, 1, buf + h->doff[q] * R, R, 1, (int)nq, (int)R, +1);
         for (auto [d, idx] : gl) {
           const int64_t nd = h->nsz[d];
           T.add_term(t, Pb + h->Poff[d] + h->pcol[d][idx] * nd, nd, 1, buf + h->doff[d] * R, R, 1, (int)nd, ft[d]);
         }
-        T.tile(t, -1, stp);
-        ft[q] = t;
+        T.tile(t, 0, wsteps);
       }
     }
+    T.sort_by_key();
     T.close_batch();
   };
   // D^-1 on this rank's interior and the separators: dst = init + sign D^-1 src
@@ -1926,26 +1993,54 @@ void build_dist_plan(ps_handle* h, DistPlan& dp, int64_t R) {
     }
     T.close_batch();
   };
-  // backward sweep (Eq. 26): separators (depth order puts them first), then the
-  // interior subtrees, whose struct lies in the subtree or the separators
+  // backward sweep (Eq. 26): separator pieces, then this rank's pieces, top-down; the
+  // struct of a node lies in its own subtree's ancestors: this rank or the separators
   auto bwd = [&](Table& T, int64_t in, int64_t out) {
-    std::vector<int32_t> bt(nl, -1);
-    for (int L = 0; L <= h->max_depth; ++L) {
-      const int stp = steps_for(byd[L], false);
-      for (int32_t p : byd[L]) {
-        if (!(mine(p) || sep(p))) continue;
+    T.early_keys = true;
+    double key = 0;
+    std::vector<int32_t> wt(nl, -1), ft(nl, -1);
+    std::vector<int32_t> order;
+    for (size_t k = 0; k < dpieces.size(); ++k)
+      if (dpieces[k].own == g || dpieces[k].own < 0) order.push_back((int32_t)k);
+    std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) {
+      return h->height[h->chains[dpieces[x].c][dpieces[x].i1 - 1]] > h->height[h->chains[dpieces[y].c][dpieces[y].i1 - 1]];
+    });
+    for (int32_t k : order) {
+      const DPiece& Pc = dpieces[k];
+      const auto nodes = piece_nodes(Pc);
+      const bool single = nodes.size() == 1;
+      T.key_base = key++;
+      for (int32_t p : nodes) {
         const int64_t np_ = h->nsz[p];
-        int32_t t = T.add_task(out + h->doff[p] * R, R, 1, in + h->doff[p] * R, R, 1, (int)np_, (int)R, +1);
+        int32_t t = T.add_task((single ? out : SCo) + h->doff[p] * R, R, 1, in + h->doff[p] * R, R, 1, (int)np_,
+                               (int)R, +1);
         for (size_t i = 0; i < h->st[p].size(); ++i) {
           const int32_t j = h->st[p][i];
           if (!(mine(j) || sep(j))) throw PsError{PS_ECUDA, "internal: struct leaves the rank's subtree"};
+          if (dpiece_of[j] == k) continue;
           T.add_term(t, Pb + h->Poff[p] + h->pcol[p][i] * np_, 1, np_, out + h->doff[j] * R, R, 1,
-                     (int)h->nsz[j], bt[j]);
+                     (int)h->nsz[j], wt[j]);
         }
-        T.tile(t, +1, stp);
-        bt[p] = t;
+        T.tile(t, 0, wsteps);
+        (single ? wt : ft)[p] = t;
+      }
+      if (single) continue;
+      const int64_t U = h->ch_U[Pc.c], To = h->Tbase + h->ch_Toff[Pc.c];
+      T.key_base = key++;
+      for (size_t i = 0; i < nodes.size(); ++i) {
+        const int32_t p = nodes[i];
+        const int64_t np_ = h->nsz[p];
+        int32_t t = T.add_task(out + h->doff[p] * R, R, 1, SCo + h->doff[p] * R, R, 1, (int)np_, (int)R, +1);
+        T.tasks[t].idep = ft[p];
+        for (size_t j = i + 1; j < nodes.size(); ++j) {
+          const int32_t q = nodes[j];
+          T.add_term(t, To + h->cpos[q] + h->cpos[p] * U, U, 1, SCo + h->doff[q] * R, R, 1, (int)h->nsz[q], ft[q]);
+        }
+        T.tile(t, 0, wsteps);
+        wt[p] = t;
       }
     }
+    T.sort_by_key();
     T.close_batch();
   };
   fwd(dp.fwdIA, dp.oY, true);
@@ -2032,7 +2127,7 @@ void build_dist_plan(ps_handle* h, DistPlan& dp, int64_t R) {
   for (Table* tb : {&dp.fwdIA, &dp.fwdSA, &dp.dinvA, &dp.bwdA, &dp.far1, &dp.far2, &dp.fwdIC, &dp.fwdSC,
                     &dp.dinvC, &dp.bwdC})
     tb->upload(h->stream);
-  dp.ws.alloc(6 * NP + std::max<int64_t>(Ttot, 1));
+  dp.ws.alloc(7 * NP + std::max<int64_t>(Ttot, 1));
   CK(cudaMemsetAsync(dp.ws.p, 0, sizeof(double2) * dp.ws.n, h->stream));   // padding rows stay 0
   dp.nchI = (h->own_rows + dp.rpc - 1) / dp.rpc;
   dp.nchS = h->rank == 0 ? (h->Nsep + dp.rpc - 1) / dp.rpc : 0;
