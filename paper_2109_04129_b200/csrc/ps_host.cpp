@@ -1428,23 +1428,7 @@ void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
   std::vector<int64_t> toff(ncl);
   int64_t Ttot = 0;
   for (int64_t c = 0; c < ncl; ++c) { toff[c] = sp.oTMP + Ttot; Ttot += h->cl_sr[c] * R; }
-  std::vector<std::vector<int32_t>> byh(h->max_height + 1), byd(h->max_depth + 1);
-  for (int64_t p = 0; p < nl; ++p) {
-    byh[h->height[p]].push_back((int32_t)p);
-    byd[h->depth[p]].push_back((int32_t)p);
-  }
   const int resident = flow_resident_ctas();
-  auto steps_for = [&](const std::vector<int32_t>& nodes, bool fwd) {
-    if (P.narrow) return NARROW_STEPS();
-    double ks = 0;
-    for (int32_t p : nodes) {
-      double K = 0;
-      if (fwd) { for (auto [d, idx] : h->gath[p]) K += h->nsz[d]; }
-      else K = (double)h->S[p];
-      ks += std::ceil((double)h->nsz[p] / GM_MT) * std::ceil((double)R / GM_NT) * std::ceil(K / GM_KC);
-    }
-    return std::max(4, std::min(32, (int)std::ceil(ks / (2.0 * resident))));
-  };
   P.key_stagger = 0.0;
   P.early_keys = true;
   // far field on the tensor-core consumer with long chunks, as in the stage tables
@@ -1867,24 +1851,6 @@ void build_dist_plan(ps_handle* h, DistPlan& dp, int64_t R) {
   }
   auto mine = [&](int64_t p) { return h->owner[p] == g; };
   auto sep = [&](int64_t p) { return h->owner[p] < 0; };
-  std::vector<std::vector<int32_t>> byh(h->max_height + 1), byd(h->max_depth + 1);
-  for (int64_t p = 0; p < nl; ++p) {
-    byh[h->height[p]].push_back((int32_t)p);
-    byd[h->depth[p]].push_back((int32_t)p);
-  }
-  const int resident = flow_resident_ctas();
-  auto steps_for = [&](const std::vector<int32_t>& nodes, bool fwd) {
-    if (narrow) return NARROW_STEPS();
-    double ks = 0;
-    for (int32_t p : nodes) {
-      if (!(mine(p) || sep(p))) continue;
-      double K = 0;
-      if (fwd) { for (auto [d, idx] : h->gath[p]) K += h->nsz[d]; }
-      else K = (double)h->S[p];
-      ks += std::ceil((double)h->nsz[p] / GM_MT) * std::ceil((double)R / GM_NT) * std::ceil(K / GM_KC);
-    }
-    return std::max(4, std::min(32, (int)std::ceil(ks / (2.0 * resident))));
-  };
   const int64_t Pb = h->Pbase, Db = h->Dbase, Fb = h->Fbase;
   // Chain-collapsed sweeps of the partitioned solve (as build_chain_sweeps): the
   // chain pieces are cut where the owner changes (interior of this rank / another
