@@ -96,7 +96,10 @@ typedef struct {
 
 typedef struct {
   int deterministic;        /* 1 (default): fixed summation order, bitwise repeatable (always true in v1) */
-  int ordering;             /* 0 (default): elimination order from the file (nested dissection) */
+  int ordering;             /* 0 (default): elimination order from the file (nested dissection);
+                               2: reverse Cuthill-McKee on the leaf near-field graph (recomputed in
+                               ps_setup; not with a row partition). x is order-invariant, the
+                               scaling (hence it_0 / it_1) is not. Others: PS_EINVAL. */
   int amalgamate_separators;/* reserved, must be 0 */
   double ratio_threshold;   /* divergence threshold of Eq. 45 / P:245; default 0.1; ratio >= thr => diverged */
 } ps_setup_opts;

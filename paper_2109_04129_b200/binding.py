@@ -176,8 +176,9 @@ class PsHandle:
         except Exception:
             pass
 
-    def setup(self, ratio_threshold: float = 0.1):
-        o = _Opts(1, 0, 0, float(ratio_threshold))
+    def setup(self, ratio_threshold: float = 0.1, ordering: int = 0):
+        """ordering 0: the file's nested-dissection order; 2: reverse Cuthill-McKee."""
+        o = _Opts(1, int(ordering), 0, float(ratio_threshold))
         self._check(load_library().ps_setup(self._h, ctypes.byref(o)))
 
     def solve(self, B, X, stream=None, want_norms: bool = True):

@@ -1313,6 +1313,63 @@ void build_chain_sweeps(ps_handle* h, SolvePlan& sp, int64_t R, int narrow, int 
   sp.bwd.close_batch();
 }
 
+// Elimination order = reverse Cuthill-McKee on the leaf near-field graph (ps_setup
+// ordering = 2; PAPER.md P:171 names a bandwidth-reducing (Sloan) order). x does
+// not depend on the order; the scaling, hence it_0 / it_1, does.
+// Re-runs the symbolic analysis and re-lays the operator arena (the far stacks move).
+void reorder_rcm(ps_handle* h, cudaStream_t s) {
+  const int64_t nl = h->nl;
+  std::vector<std::vector<int32_t>> adj(nl);
+  for (int64_t b = 0; b < h->nnear; ++b) {
+    const int32_t i = (int32_t)h->near_list[3 * b], j = (int32_t)h->near_list[3 * b + 1];
+    if (i == j) continue;
+    adj[i].push_back(j);
+    adj[j].push_back(i);
+  }
+  auto deg = [&](int32_t v) { return adj[v].size(); };
+  for (auto& a : adj) std::sort(a.begin(), a.end(), [&](int32_t x, int32_t y) { return deg(x) < deg(y) || (deg(x) == deg(y) && x < y); });
+  std::vector<char> seen(nl, 0);
+  std::vector<int32_t> order;
+  order.reserve(nl);
+  while ((int64_t)order.size() < nl) {
+    int32_t start = -1;
+    for (int32_t v = 0; v < nl; ++v)
+      if (!seen[v] && (start < 0 || deg(v) < deg(start))) start = v;
+    size_t head = order.size();
+    order.push_back(start);
+    seen[start] = 1;
+    while (head < order.size()) {
+      const int32_t u = order[head++];
+      for (int32_t v : adj[u])
+        if (!seen[v]) { seen[v] = 1; order.push_back(v); }
+    }
+  }
+  std::reverse(order.begin(), order.end());
+  // keep the far stacks (device), rebuild everything that depends on the order
+  const int64_t far_len = h->Tbase - h->Fbase;
+  DevBuf<double2> far_save;
+  far_save.alloc(std::max<int64_t>(far_len, 1));
+  if (far_len > 0)
+    CK(cudaMemcpyAsync(far_save.p, h->d_op.p + h->Fbase, sizeof(double2) * far_len, cudaMemcpyDeviceToDevice, s));
+  h->elim = order;
+  symbolic(h);
+  h->Pbase = 0;
+  h->Dbase = h->Plen;
+  h->Fbase = h->Plen + h->Dlen;
+  h->Tbase = h->Fbase + far_len;
+  h->d_op.alloc(h->Tbase + h->Tlen);
+  h->d_P.p = h->d_op.p + h->Pbase;
+  h->d_D.p = h->d_op.p + h->Dbase;
+  h->d_far.p = h->d_op.p + h->Fbase;
+  if (far_len > 0)
+    CK(cudaMemcpyAsync(h->d_far.p, far_save.p, sizeof(double2) * far_len, cudaMemcpyDeviceToDevice, s));
+  h->d_e2rwg.upload(h->e2rwg, s);
+  h->d_e2mort.upload(h->e2mort, s);
+  h->d_m2e.upload(h->m2e, s);
+  CK(cudaStreamSynchronize(s));
+  h->plan.reset();
+}
+
 // ------------------------------------------------------------------ solve plan
 void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
   const int64_t nl = h->nl;
@@ -2374,14 +2431,17 @@ ps_status ps_setup(ps_handle* h, const ps_setup_opts* opts) {
   if (!h) return fail(nullptr, PS_EINVAL, "ps_setup: handle is NULL");
   if (h->setup_done) return fail(h, PS_ESTATE, "ps_setup: already set up");
   if (opts) {
-    if (opts->ordering != 0 || opts->amalgamate_separators != 0)
-      return fail(h, PS_EINVAL, "ps_setup: only ordering=0 and amalgamate_separators=0 are supported");
+    if ((opts->ordering != 0 && opts->ordering != 2) || opts->amalgamate_separators != 0)
+      return fail(h, PS_EINVAL, "ps_setup: ordering must be 0 (file ND) or 2 (RCM); amalgamate_separators 0");
+    if (opts->ordering == 2 && h->part_mode)
+      return fail(h, PS_EINVAL, "ps_setup: ordering=2 is not supported with a row partition");
     if (!(opts->ratio_threshold > 0.0)) return fail(h, PS_EINVAL, "ps_setup: ratio_threshold must be > 0");
     h->ratio_threshold = opts->ratio_threshold;
   }
   try {
     CK(cudaSetDevice(h->device));
     cudaStream_t s = h->stream;
+    if (opts && opts->ordering == 2) reorder_rcm(h, s);
     h->d_W.alloc(std::max<int64_t>(h->Wlen, 1));
     SetupPlan sp;
     build_setup_plan(h, sp);

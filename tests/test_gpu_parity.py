@@ -256,3 +256,31 @@ def test_solve_column_tile_boundaries(cfgdata, nrhs):
     ref = solve(H, S, B)
     assert rel_l2_cols(_host(Xd), ref.x).max() <= TOL
     assert np.allclose(rep["it0"], ref.it0, rtol=1e-11)
+
+
+@pytest.mark.parametrize("which", ["C1", "synth"])
+def test_rcm_ordering(cfgdata, synthfile, which):
+    """ps_setup ordering = 2 (reverse Cuthill-McKee, recomputed by libps): x is the
+    order-invariant two-term solution (oracle in the file's ND order), it_0 / it_1
+    are those of the oracle run in libps's RCM order (read back with ps_elim_leaf)."""
+    path = cfgdata("C1")["hm"] if which == "C1" else synthfile(n_points=900, seed=7, clustered=True)[0]
+    H = read_hm(path)
+    h = PsHandle(path)
+    h.setup(ordering=2)
+    order = np.array([h.elim_leaf(p) for p in range(H.n_leaves)])
+    assert sorted(order.tolist()) == list(range(H.n_leaves))
+    assert not np.array_equal(order, H.elim)              # a different order really is used
+    B = random_rhs(H.N, 3, 9)
+    Bd = _dev(B)
+    Xd = torch.empty_like(Bd)
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        st, rep = h.solve(Bd, Xd)
+    ref_nd = solve(H, compute_scaling(H), B)
+    ref_rcm = solve(H, compute_scaling(H, order), B)
+    assert rel_l2_cols(_host(Xd), ref_nd.x).max() <= TOL
+    assert rel_l2_cols(_host(Xd), ref_rcm.x).max() <= TOL
+    assert np.allclose(rep["it0"], ref_rcm.it0, rtol=1e-11)
+    assert np.allclose(rep["it1"], ref_rcm.it1, rtol=1e-10)
+    h.close()
