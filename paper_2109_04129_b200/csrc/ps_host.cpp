@@ -174,8 +174,12 @@ struct Table {
   DevBuf<int32_t> d_counters;
   DevBuf<double2> d_partial;
   int64_t cur_batch_start = 0;
+  // completion units, split-K tiles and partial slots are numbered per batch (one
+  // launch each; counters are cleared per launch), the buffers sized for the largest
   int32_t n_units = 0, n_tiles = 0;
   int64_t n_slots = 0;
+  int32_t max_units = 0, max_tiles = 0;
+  int64_t max_slots = 0;
   int chunk_steps = CHUNK_STEPS;
   int narrow = 0;          // 1: 64 x 8 tiles (small nrhs)
   double2* S = nullptr;    // scratch vector base of osel / bsel offsets (chain stages)
@@ -374,6 +378,14 @@ struct Table {
     int64_t n = (int64_t)work.size() - cur_batch_start;
     batches.push_back({cur_batch_start, n});
     cur_batch_start = (int64_t)work.size();
+    max_units = std::max(max_units, n_units);
+    max_tiles = std::max(max_tiles, n_tiles);
+    max_slots = std::max(max_slots, n_slots);
+    static const int per_batch = env_int("PS_BATCH_SLOTS", 1);
+    if (per_batch) {
+      n_units = n_tiles = 0;
+      n_slots = 0;
+    }
   }
   double alg_flops = 0, alg_bytes = 0;   // useful flops / operator (A) bytes of one full pass
   void upload(cudaStream_t st) {
@@ -386,8 +398,8 @@ struct Table {
     d_tasks.upload(tasks, st);
     d_terms.upload(terms, st);
     d_work.upload(work, st);
-    d_counters.alloc(1 + (int64_t)n_units + n_tiles);
-    d_partial.alloc(std::max<int64_t>(n_slots, 1) * GM_MT * GM_NT);
+    d_counters.alloc(1 + (int64_t)max_units + max_tiles);
+    d_partial.alloc(std::max<int64_t>(max_slots, 1) * GM_MT * GM_NT);
   }
   int64_t launch(int b, double2* O, const double2* I, const double2* A, const double2* B,
                  cudaStream_t st, Prof* pf = nullptr, int cls = 0) const {
@@ -402,7 +414,7 @@ struct Table {
     fa.terms = d_terms.p;
     fa.O = O; fa.I = I; fa.A = A; fa.B = B; fa.S = S;
     fa.counters = d_counters.p;
-    fa.n_units = n_units;
+    fa.n_units = max_units;
     fa.pad = 0;
     fa.partial = d_partial.p;
     fa.trace = nullptr;
@@ -452,6 +464,7 @@ struct SolvePlan {
   DevBuf<double2> y, bo, w, u, xt, wm, tm, part, norms, stage, sc;
   int64_t nchunks = 0, rpc = 64;
   int64_t launches_per_solve = 0;
+  bool stages_built = false;
 };
 
 // Per-nrhs plan of the row-partitioned solve: this rank's tables
@@ -516,6 +529,11 @@ struct ps_handle {
   // ---- device ----
   // operator arena: [ alpha panels P (Plen) | D^-1 (Dlen) | far stacks + dense far blocks ]
   DevBuf<double2> d_near, d_W, d_op;
+  // far stacks and chain matrices live in their own allocations, made after the
+  // setup-only arenas (W, near) are freed (peak device memory of ps_setup); tables
+  // address them from the d_op base through the pointer differences Fbase / Tbase
+  DevBuf<double2> d_farbuf, d_T;
+  std::vector<double2> far_host;            // restacked far factors until uploaded
   struct RawBuf { double2* p = nullptr; } d_P, d_D, d_far;   // views into d_op
   int64_t Pbase = 0, Dbase = 0, Fbase = 0;
   DevBuf<int64_t> d_e2rwg, d_e2mort, d_m2e;
@@ -1112,6 +1130,20 @@ void build_setup_plan(ps_handle* h, SetupPlan& sp) {
   }
 }
 
+// Upload the restacked far factors (once) and point Fbase at them.
+void ensure_far(ps_handle* h, cudaStream_t s) {
+  if (!h->d_farbuf.p) {
+    h->d_farbuf.alloc(std::max<int64_t>((int64_t)h->far_host.size(), 1));
+    if (!h->far_host.empty())
+      CK(cudaMemcpyAsync(h->d_farbuf.p, h->far_host.data(), sizeof(double2) * h->far_host.size(),
+                         cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    std::vector<double2>().swap(h->far_host);
+  }
+  h->d_far.p = h->d_farbuf.p;
+  h->Fbase = (int64_t)(h->d_farbuf.p - h->d_op.p);
+}
+
 // T_c = (I - A_c^T)^{-1} of every chain piece with L >= 2 (see ps_handle): the
 // forward sweep (Eq. 24) restricted to the piece, applied to the identity:
 //   X_i = delta_i + sum_{k < i, p_i in struct(p_k)} alpha_{p_k p_i}^T X_k,
@@ -1119,22 +1151,27 @@ void build_setup_plan(ps_handle* h, SetupPlan& sp) {
 // dataflow launch; pieces are independent, hops within a piece are ordered.
 void chain_setup(ps_handle* h, cudaStream_t s) {
   if (h->Tlen == 0) return;
-  CK(cudaMemsetAsync(h->d_op.p + h->Tbase, 0, sizeof(double2) * h->Tlen, s));
+  // T lives in its own allocation: its rows are addressed through the table's
+  // scratch base (offsets >= 0; a negative offset would read as "no init")
+  double2* Tp = h->d_T.p;
+  CK(cudaMemsetAsync(Tp, 0, sizeof(double2) * h->Tlen, s));
   std::vector<int64_t> ones;
   Table Tt;
+  Tt.S = Tp;
   std::vector<int32_t> tk(h->nl, -1);
-  const int64_t Tb = h->Tbase, Pb = h->Pbase;
+  const int64_t Pb = h->Pbase;
   for (size_t c = 0; c < h->chains.size(); ++c) {
     if (h->ch_Toff[c] < 0) continue;
-    const int64_t U = h->ch_U[c], To = Tb + h->ch_Toff[c];
+    const int64_t U = h->ch_U[c], To = h->ch_Toff[c];
     for (int64_t i = 0; i < U; ++i) ones.push_back(To + i + i * U);
     for (int32_t p : h->chains[c]) {
       const int64_t np_ = h->nsz[p], cp = h->cpos[p];
       int32_t t = Tt.add_task(To + cp, 1, U, To + cp, 1, U, (int)np_, (int)(cp + np_), +1);
+      Tt.tasks[t].osel = 1 | 2;                      // O and I in T (scratch base)
       for (auto [d, idx] : h->gath[p]) {
         if (h->chain_of[d] != (int32_t)c) continue;
         const int64_t nd = h->nsz[d];
-        Tt.add_term(t, Pb + h->Poff[d] + h->pcol[d][idx] * nd, nd, 1, To + h->cpos[d], 1, U, (int)nd, tk[d]);
+        Tt.add_term(t, Pb + h->Poff[d] + h->pcol[d][idx] * nd, nd, 1, To + h->cpos[d], 1, U, (int)nd, tk[d], 1);
       }
       Tt.tile(t, -1, 8);
       tk[p] = t;
@@ -1144,7 +1181,7 @@ void chain_setup(ps_handle* h, cudaStream_t s) {
   Tt.upload(s);
   DevBuf<int64_t> d_ones;
   d_ones.upload(ones, s);
-  launch_set_ones(h->d_op.p, d_ones.p, (int64_t)ones.size(), s);
+  launch_set_ones(Tp, d_ones.p, (int64_t)ones.size(), s);
   Tt.launch_all(h->d_op.p, h->d_op.p, h->d_op.p, h->d_op.p, s);
   CK(cudaStreamSynchronize(s));
 }
@@ -1345,24 +1382,15 @@ void reorder_rcm(ps_handle* h, cudaStream_t s) {
     }
   }
   std::reverse(order.begin(), order.end());
-  // keep the far stacks (device), rebuild everything that depends on the order
-  const int64_t far_len = h->Tbase - h->Fbase;
-  DevBuf<double2> far_save;
-  far_save.alloc(std::max<int64_t>(far_len, 1));
-  if (far_len > 0)
-    CK(cudaMemcpyAsync(far_save.p, h->d_op.p + h->Fbase, sizeof(double2) * far_len, cudaMemcpyDeviceToDevice, s));
+  // rebuild everything that depends on the order (the far stacks do not)
   h->elim = order;
   symbolic(h);
   h->Pbase = 0;
   h->Dbase = h->Plen;
-  h->Fbase = h->Plen + h->Dlen;
-  h->Tbase = h->Fbase + far_len;
-  h->d_op.alloc(h->Tbase + h->Tlen);
+  h->d_op.alloc(h->Plen + h->Dlen);
   h->d_P.p = h->d_op.p + h->Pbase;
   h->d_D.p = h->d_op.p + h->Dbase;
-  h->d_far.p = h->d_op.p + h->Fbase;
-  if (far_len > 0)
-    CK(cudaMemcpyAsync(h->d_far.p, far_save.p, sizeof(double2) * far_len, cudaMemcpyDeviceToDevice, s));
+  if (h->d_farbuf.p) ensure_far(h, s);
   h->d_e2rwg.upload(h->e2rwg, s);
   h->d_e2mort.upload(h->e2mort, s);
   h->d_m2e.upload(h->m2e, s);
@@ -1449,11 +1477,17 @@ void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
   for (Table* tb : {&sp.fwd, &sp.bwd, &sp.dinv, &sp.far1, &sp.far2}) tb->upload(h->stream);
   const int64_t NR = h->N * R;
   sp.y.alloc(NR); sp.bo.alloc(NR); sp.w.alloc(NR); sp.u.alloc(NR); sp.xt.alloc(NR);
-  sp.wm.alloc(NR + std::max<int64_t>(T, 1)); sp.tm.alloc(NR); sp.stage.alloc(NR);
-  sp.nchunks = (h->N + sp.rpc - 1) / sp.rpc;
-  sp.part.alloc(sp.nchunks * R);
-  sp.norms.alloc(R);
+  sp.wm.alloc(NR + std::max<int64_t>(T, 1)); sp.tm.alloc(NR);
   CK(cudaStreamSynchronize(h->stream));
+}
+
+// buffers every solve path needs: host staging, norm partial sums
+void build_common(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
+  sp.nrhs = nrhs;
+  sp.stage.alloc(h->N * nrhs);
+  sp.nchunks = (h->N + sp.rpc - 1) / sp.rpc;
+  sp.part.alloc(sp.nchunks * nrhs);
+  sp.norms.alloc(nrhs);
 }
 
 
@@ -1741,13 +1775,19 @@ bool use_stages() {
   return v;
 }
 
-SolvePlan& get_plan(ps_handle* h, int64_t nrhs) {
+// Per-nrhs plan, built on first use: the single-launch program for ps_solve and,
+// only when needed (ps_apply, PS_SOLVE=stages), the per-operator stage tables.
+SolvePlan& get_plan(ps_handle* h, int64_t nrhs, bool need_stages = false) {
   if (!h->plan || h->plan->nrhs != nrhs) {
     h->plan.reset();
     auto sp = std::make_unique<SolvePlan>();
-    build_solve_plan(h, *sp, nrhs);
+    build_common(h, *sp, nrhs);
     if (!use_stages()) build_program(h, *sp, nrhs);
     h->plan = std::move(sp);
+  }
+  if ((need_stages || use_stages()) && !h->plan->stages_built) {
+    build_solve_plan(h, *h->plan, nrhs);
+    h->plan->stages_built = true;
   }
   return *h->plan;
 }
@@ -2390,21 +2430,14 @@ ps_status hm_load(const char* path, const ps_dist* dist, ps_handle** out) {
     CK(cudaEventCreate(&h->ev1));
     h->d_near.upload(near_arena, h->stream);
     {
-      std::vector<double2> stacked;
-      far_layout(h.get(), far_arena, stacked);
+      far_layout(h.get(), far_arena, h->far_host);
       far_arena.clear();
       far_arena.shrink_to_fit();
       h->Pbase = 0;
       h->Dbase = h->Plen;
-      h->Fbase = h->Plen + h->Dlen;
-      h->Tbase = h->Fbase + (int64_t)stacked.size();
-      h->d_op.alloc(h->Tbase + h->Tlen);
+      h->d_op.alloc(h->Plen + h->Dlen);
       h->d_P.p = h->d_op.p + h->Pbase;
       h->d_D.p = h->d_op.p + h->Dbase;
-      h->d_far.p = h->d_op.p + h->Fbase;
-      CK(cudaMemcpyAsync(h->d_far.p, stacked.data(), sizeof(double2) * stacked.size(), cudaMemcpyHostToDevice,
-                         h->stream));
-      CK(cudaStreamSynchronize(h->stream));
     }
     h->d_e2rwg.upload(h->e2rwg, h->stream);
     h->d_e2mort.upload(h->e2mort, h->stream);
@@ -2471,10 +2504,16 @@ ps_status ps_setup(ps_handle* h, const ps_setup_opts* opts) {
       sp.panel.launch(lev, h->d_P.p, nullptr, h->d_D.p, h->d_W.p, s);
     }
     CK(cudaGetLastError());
-    chain_setup(h, s);
     CK(cudaStreamSynchronize(s));
     h->d_W.release();
     h->d_near.release();
+    ensure_far(h, s);
+    h->d_T.alloc(std::max<int64_t>(h->Tlen, 1));
+    h->Tbase = (int64_t)(h->d_T.p - h->d_op.p);
+    chain_setup(h, s);
+    CK(cudaStreamSynchronize(s));
+    h->plan.reset();                                  // plans made before setup (ps_apply Z_F) are stale
+    h->dplan.reset();
     h->setup_done = true;
   } catch (const PsError& e) {
     return fail(h, e.st, "ps_setup: " + e.msg);
@@ -2595,7 +2634,8 @@ ps_status ps_apply(ps_handle* h, int op, int64_t nrhs, const void* Xin, void* Yo
   try {
     CK(cudaSetDevice(h->device));
     cudaStream_t s = h->stream;
-    SolvePlan& sp = get_plan(h, nrhs);
+    ensure_far(h, s);                                 // Z_F is legal before ps_setup
+    SolvePlan& sp = get_plan(h, nrhs, true);
     const int64_t N = h->N, R = nrhs;
     launch_permute_in(N, R, h->d_e2rwg.p, (const double2*)Xin, N, sp.y.p, s);
     double2* res = sp.y.p;
