@@ -31,6 +31,8 @@
 #include <string>
 #include <unordered_map>
 #include <vector>
+#include <queue>
+#include <tuple>
 
 using namespace ps;
 
@@ -72,7 +74,17 @@ struct DevBuf {
   void alloc(int64_t count) {
     release();
     if (count <= 0) return;
-    CK(cudaMalloc(&p, sizeof(T) * (size_t)count));
+    const cudaError_t e = cudaMalloc(&p, sizeof(T) * (size_t)count);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      cudaGetLastError();
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      throw PsError{e == cudaErrorMemoryAllocation ? PS_ENOMEM : PS_ECUDA,
+                    std::string("device allocation of ") + std::to_string((sizeof(T) * (size_t)count) >> 20) +
+                        " MiB failed (" + cudaGetErrorString(e) + "; " + std::to_string(fr >> 20) + " of " +
+                        std::to_string(tot >> 20) + " MiB free)"};
+    }
     n = count;
   }
   void upload(const std::vector<T>& v, cudaStream_t st) {
@@ -187,7 +199,7 @@ struct Table {
   // optional global ordering of work items (ticket order): key = key_base + nt * key_stagger,
   // stable-sorted by sort_by_key() (valid when every dependency has a smaller key)
   double key_base = 0, key_stagger = 0;
-  std::vector<double> keys;
+  std::vector<double> keys, keys_late;
   std::vector<double> task_key;      // key_base of every task at creation
   // early_keys: a chunk is keyed just after the latest of its producers' tasks
   // (not at its own task's key), so a gather's bulk chunks enter the ticket
@@ -202,8 +214,36 @@ struct Table {
     for (size_t i = 0; i < idx.size(); ++i) w2[i] = work[idx[i]];
     work.swap(w2);
     keys.clear();
+    keys_late.clear();
   }
+  // sort_by_key + close_batch for a one-batch table, bounded partial-slot memory: with
+  // early keys a split tile's chunks spread over the ticket order and its slots stay
+  // live meanwhile; if the recycled pool still exceeds the budget (C5), the batch is
+  // re-ordered by its tasks' own keys (chunks of a tile adjacent) and re-assigned.
+  void sort_close_bounded() {
+    static const int64_t budget = (int64_t)env_int("PS_SLOT_BUDGET_MB", 4096) << 20;
+    const bool can_redo = early_keys && budget > 0;
+    std::vector<GWork> w0;
+    std::vector<double> kl;
+    if (can_redo) { w0 = work; kl = keys_late; }
+    const int32_t nu = n_units, ntl = n_tiles, mu = max_units, mtl = max_tiles;
+    const int64_t ns = n_slots, ms = max_slots, cb0 = cur_batch_start;
+    sort_by_key();
+    close_batch();
+    if (can_redo && max_slots * slot_elems() * 16 > budget) {
+      work.swap(w0);
+      keys = kl;
+      batches.pop_back();
+      n_units = nu; n_tiles = ntl; max_units = mu; max_tiles = mtl;
+      n_slots = ns; max_slots = ms; cur_batch_start = cb0;
+      sort_by_key();
+      close_batch();
+      late_keys_used = true;
+    }
+  }
+  bool late_keys_used = false;
   int MT() const { return narrow ? GN_MT : GM_MT; }
+  int64_t slot_elems() const { return narrow ? (int64_t)GN_MT * GN_NT : (int64_t)GM_MT * GM_NT; }
   int NT() const { return narrow ? GN_NT : GM_NT; }
 
   int32_t add_task(int64_t oO, int64_t sOi, int64_t sOc, int64_t oI, int64_t sIi, int64_t sIc, int m,
@@ -358,7 +398,7 @@ struct Table {
         auto push = [&](int c) {
           const int sg = sub_of[c];
           work.push_back({task, a, b, ch[c][2], ch[c][3], ch[c][0], ch[c][1], c, nch, tile_id, crit,
-                          sg, sg >= 0 ? sub_r0[sg] : 0, sg >= 0 ? sub_r1[sg] : 0, nsub, 0, slot});
+                          sg, sg >= 0 ? sub_r0[sg] : 0, sg >= 0 ? sub_r1[sg] : 0, nsub, -1, 0, 0, slot});
           double k = key_base;
           if (early_keys && c != crit) {
             double kp = -1.0;
@@ -368,15 +408,67 @@ struct Table {
             k = std::min(key_base, kp + 0.5);
           }
           keys.push_back(k + b * key_stagger);
+          keys_late.push_back(key_base + b * key_stagger);
         };
         for (int c = 0; c < nch; ++c)
           if (c != crit) push(c);
         if (crit >= 0) push(crit);
       }
   }
+  // Partial-sum slots of the batch's split tiles, recycled in ticket order: a
+  // tile takes a block (power-of-two size class >= nchunks + nsub) whose previous
+  // tile's unit has ALL its items at least SLOT_SLACK tickets before this tile's
+  // first item; the tile's items wait for that unit (ticket-ordered, so
+  // deadlock-free) before writing. Bounds the partial buffer by the tiles in
+  // flight instead of every split tile of the launch (C5: >100 GB otherwise).
+  static inline const int SLOT_REUSE = env_int("PS_SLOT_REUSE", 1);
+  static inline const int SLOT_SLACK = env_int("PS_SLOT_SLACK", 2048);
+  void assign_slots(int64_t w0, int64_t w1) {
+    if (!SLOT_REUSE || w1 <= w0) return;
+    std::vector<int64_t> ulast(n_units, -1);
+    for (int64_t i = w0; i < w1; ++i) ulast[tasks[work[i].task].unit0 + work[i].nt] = i;
+    struct Blk { int64_t base; int32_t unit, need; };
+    std::vector<std::vector<Blk>> free_(32);
+    using Pend = std::tuple<int64_t, int, Blk>;             // (release ticket, class, block)
+    auto cmp = [](const Pend& x, const Pend& y) { return std::get<0>(x) > std::get<0>(y); };
+    std::priority_queue<Pend, std::vector<Pend>, decltype(cmp)> pend(cmp);
+    std::unordered_map<int32_t, Blk> of_tile;                 // tile -> (slot base, wait unit, need)
+    int64_t pool = 0;
+    for (int64_t i = w0; i < w1; ++i) {
+      GWork& w = work[i];
+      if (w.nchunks <= 1) continue;
+      auto it = of_tile.find(w.tile);
+      if (it == of_tile.end()) {
+        while (!pend.empty() && std::get<0>(pend.top()) + SLOT_SLACK < i) {
+          free_[std::get<1>(pend.top())].push_back(std::get<2>(pend.top()));
+          pend.pop();
+        }
+        const int64_t len = (int64_t)w.nchunks + w.nsub;
+        int c = 0;
+        while ((int64_t(1) << c) < len) ++c;
+        Blk b;
+        if (!free_[c].empty()) {
+          b = free_[c].back();
+          free_[c].pop_back();
+        } else {
+          b = {pool, -1, 0};
+          pool += int64_t(1) << c;
+        }
+        it = of_tile.emplace(w.tile, b).first;
+        const GTask& T = tasks[w.task];
+        const int32_t u = T.unit0 + w.nt;
+        pend.push({ulast[u], c, Blk{b.base, u, T.n_mt}});
+      }
+      w.slot = it->second.base;
+      w.sw_unit = it->second.unit;
+      w.sw_need = it->second.need;
+    }
+    n_slots = pool;
+  }
   void close_batch() {
     int64_t n = (int64_t)work.size() - cur_batch_start;
     batches.push_back({cur_batch_start, n});
+    assign_slots(cur_batch_start, (int64_t)work.size());
     cur_batch_start = (int64_t)work.size();
     max_units = std::max(max_units, n_units);
     max_tiles = std::max(max_tiles, n_tiles);
@@ -399,7 +491,12 @@ struct Table {
     d_terms.upload(terms, st);
     d_work.upload(work, st);
     d_counters.alloc(1 + (int64_t)max_units + max_tiles);
-    d_partial.alloc(std::max<int64_t>(max_slots, 1) * GM_MT * GM_NT);
+    d_partial.alloc(std::max<int64_t>(max_slots, 1) * slot_elems());
+    static const int verbose = env_int("PS_VERBOSE", 0);
+    if (verbose)
+      std::fprintf(stderr, "[ps] table: %zu tasks, %zu terms, %zu items, %zu batches, %lld partial slots (%lld MiB)%s\n",
+                   tasks.size(), terms.size(), work.size(), batches.size(), (long long)max_slots,
+                   (long long)((max_slots * slot_elems() * 16) >> 20), late_keys_used ? ", task-keyed" : "");
   }
   int64_t launch(int b, double2* O, const double2* I, const double2* A, const double2* B,
                  cudaStream_t st, Prof* pf = nullptr, int cls = 0) const {
@@ -429,7 +526,8 @@ struct Table {
     }();
     fa.mma = mma_env >= 0 ? mma_env : mma;
     fa.dfma_ks = 0;
-    fa.pad2 = 0;
+    static const int issue_first = env_int("PS_ISSUE_FIRST", 0);
+    fa.issue_first = issue_first;
     if (pf && pf->trace_on && cls == pf->trace_cls) {
       pf->trace_buf.alloc(6 * bt.nw);
       fa.trace = pf->trace_buf.p;
@@ -1038,20 +1136,21 @@ int64_t wcol(const ps_handle* h, int32_t p, int32_t j) {
 }
 
 // ------------------------------------------------------------------ setup
-struct SetupPlan {
+// Setup tables of ONE elimination level (built, launched and freed level by
+// level, so the host/device work lists never hold more than one level: C5's
+// whole-setup lists would be several GB).
+struct SetupLevel {
   Table asmb, panel;
-  std::vector<std::vector<int32_t>> level_leaves;
-  std::vector<DevBuf<int32_t>> d_ids, d_sz;
-  std::vector<DevBuf<int64_t>> d_src, d_ld, d_dst;
-  std::vector<int> level_maxn;
+  DevBuf<int32_t> d_ids, d_sz;
+  DevBuf<int64_t> d_src, d_ld, d_dst;
+  int64_t nlev = 0;
+  int maxn = 0;
 };
 
-void build_setup_plan(ps_handle* h, SetupPlan& sp) {
+void build_setup_level(ps_handle* h, const std::vector<int32_t>& leaves, SetupLevel& sp) {
   const int64_t nl = h->nl;
-  sp.level_leaves.assign(h->max_height + 1, {});
-  for (int64_t p = 0; p < nl; ++p) sp.level_leaves[h->height[p]].push_back((int32_t)p);
-  for (int lev = 0; lev <= h->max_height; ++lev) {
-    for (int32_t p : sp.level_leaves[lev]) {
+  {
+    for (int32_t p : leaves) {
       const int64_t np_ = h->nsz[p];
       const int32_t lp = h->leaf_at[p];
       // targets j in {p} U struct(p): W_pj = Z_pj + sum_d alpha_dp^T W_dj
@@ -1093,7 +1192,7 @@ void build_setup_plan(ps_handle* h, SetupPlan& sp) {
     }
     sp.asmb.close_batch();
     // panel: P_p = -Dinv_p W_p[:, n_p:]
-    for (int32_t p : sp.level_leaves[lev]) {
+    for (int32_t p : leaves) {
       const int64_t np_ = h->nsz[p];
       if (h->S[p] == 0) continue;
       int32_t t = sp.panel.add_task(h->Poff[p], 1, np_, -1, 0, 0, (int)np_, (int)h->S[p], -1);
@@ -1104,30 +1203,21 @@ void build_setup_plan(ps_handle* h, SetupPlan& sp) {
   }
   sp.asmb.upload(h->stream);
   sp.panel.upload(h->stream);
-  const int L = h->max_height + 1;
-  sp.d_ids.resize(L);
-  sp.d_sz.resize(L);
-  sp.d_src.resize(L);
-  sp.d_ld.resize(L);
-  sp.d_dst.resize(L);
-  sp.level_maxn.assign(L, 0);
-  for (int lev = 0; lev < L; ++lev) {
-    std::vector<int32_t> ids, sz;
-    std::vector<int64_t> src, ld, dst;
-    for (int32_t p : sp.level_leaves[lev]) {
-      ids.push_back(p);
-      sz.push_back(h->nsz[p]);
-      src.push_back(h->Woff[p]);
-      ld.push_back(h->nsz[p]);
-      dst.push_back(h->Doff[p]);
-      sp.level_maxn[lev] = std::max(sp.level_maxn[lev], h->nsz[p]);
-    }
-    sp.d_ids[lev].upload(ids, h->stream);
-    sp.d_sz[lev].upload(sz, h->stream);
-    sp.d_src[lev].upload(src, h->stream);
-    sp.d_ld[lev].upload(ld, h->stream);
-    sp.d_dst[lev].upload(dst, h->stream);
+  std::vector<int32_t> sz;
+  std::vector<int64_t> src, ld, dst;
+  for (int32_t p : leaves) {
+    sz.push_back(h->nsz[p]);
+    src.push_back(h->Woff[p]);
+    ld.push_back(h->nsz[p]);
+    dst.push_back(h->Doff[p]);
+    sp.maxn = std::max(sp.maxn, h->nsz[p]);
   }
+  sp.nlev = (int64_t)leaves.size();
+  sp.d_ids.upload(leaves, h->stream);
+  sp.d_sz.upload(sz, h->stream);
+  sp.d_src.upload(src, h->stream);
+  sp.d_ld.upload(ld, h->stream);
+  sp.d_dst.upload(dst, h->stream);
 }
 
 // Upload the restacked far factors (once) and point Fbase at them.
@@ -1290,8 +1380,7 @@ void build_chain_sweeps(ps_handle* h, SolvePlan& sp, int64_t R, int narrow, int 
       }
     }
   }
-  sp.fwd.sort_by_key();
-  sp.fwd.close_batch();
+  sp.fwd.sort_close_bounded();
   stage = 0;
   // ---- backward sweep (O = out, I = in, B = out; f in scratch) ----
   std::vector<int32_t> wt(nl, -1), ft(nl, -1);
@@ -1346,8 +1435,7 @@ void build_chain_sweeps(ps_handle* h, SolvePlan& sp, int64_t R, int narrow, int 
       }
     }
   }
-  sp.bwd.sort_by_key();
-  sp.bwd.close_batch();
+  sp.bwd.sort_close_bounded();
 }
 
 // Elimination order = reverse Cuthill-McKee on the leaf near-field graph (ps_setup
@@ -1761,8 +1849,7 @@ void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
   dinv_stage(sp.oZ, sp.oXT, sp.oBO, -1, s7, zfin, &s2);                  // S7: xt = bo - D^-1 z
   SC = sp.oSC + 3 * NR;
   bwd_stage(sp.oXT, sp.oX, s8, s7);                                      // S8
-  P.sort_by_key();
-  P.close_batch();
+  P.sort_close_bounded();
   P.upload(h->stream);
   sp.ws.alloc(10 * NR + std::max<int64_t>(Ttot, 1));
 }
@@ -2041,8 +2128,7 @@ void build_dist_plan(ps_handle* h, DistPlan& dp, int64_t R) {
         T.tile(t, 0, wsteps);
       }
     }
-    T.sort_by_key();
-    T.close_batch();
+    T.sort_close_bounded();
   };
   // D^-1 on this rank's interior and the separators: dst = init + sign D^-1 src
   auto dinv = [&](Table& T, int64_t src, int64_t dst, int64_t init, int sign) {
@@ -2103,8 +2189,7 @@ void build_dist_plan(ps_handle* h, DistPlan& dp, int64_t R) {
         wt[p] = t;
       }
     }
-    T.sort_by_key();
-    T.close_batch();
+    T.sort_close_bounded();
   };
   fwd(dp.fwdIA, dp.oY, true);
   fwd(dp.fwdSA, dp.oY, false);
@@ -2476,32 +2561,35 @@ ps_status ps_setup(ps_handle* h, const ps_setup_opts* opts) {
     cudaStream_t s = h->stream;
     if (opts && opts->ordering == 2) reorder_rcm(h, s);
     h->d_W.alloc(std::max<int64_t>(h->Wlen, 1));
-    SetupPlan sp;
-    build_setup_plan(h, sp);
+    std::vector<std::vector<int32_t>> level_leaves(h->max_height + 1);
+    for (int64_t p = 0; p < h->nl; ++p) level_leaves[h->height[p]].push_back((int32_t)p);
     DevBuf<int32_t> d_status;
     d_status.alloc(h->nl);
     CK(cudaMemsetAsync(d_status.p, 0, sizeof(int32_t) * h->nl, s));
     std::vector<int32_t> status(h->nl, 0);
     for (int lev = 0; lev <= h->max_height; ++lev) {
+      SetupLevel sp;
+      build_setup_level(h, level_leaves[lev], sp);
       // Eq. 21 (left-looking): assemble W_p = [Z~_pp | Z~_p,struct(p)]
-      sp.asmb.launch(lev, h->d_W.p, h->d_near.p, h->d_P.p, h->d_W.p, s);
+      sp.asmb.launch_all(h->d_W.p, h->d_near.p, h->d_P.p, h->d_W.p, s);
       // Eqs. 23/30: D_p^{-1}
-      const int64_t nlev = (int64_t)sp.level_leaves[lev].size();
-      launch_inverse(nlev, sp.d_ids[lev].p, sp.d_sz[lev].p, sp.d_src[lev].p, sp.d_ld[lev].p,
-                     sp.d_dst[lev].p, h->d_W.p, h->d_D.p, d_status.p, sp.level_maxn[lev], s);
+      const int64_t nlev = sp.nlev;
+      launch_inverse(nlev, sp.d_ids.p, sp.d_sz.p, sp.d_src.p, sp.d_ld.p, sp.d_dst.p, h->d_W.p, h->d_D.p,
+                     d_status.p, sp.maxn, s);
       // per-level status slot: leaves of this level write status[0..nlev)
       CK(cudaMemcpyAsync(status.data(), d_status.p, sizeof(int32_t) * nlev, cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
       for (int64_t i = 0; i < nlev; ++i)
         if (status[i]) {
-          int32_t p = sp.level_leaves[lev][i];
+          int32_t p = level_leaves[lev][i];
           h->d_W.release();
           return fail(h, PS_ESINGULAR,
                       "ps_setup: singular scaled diagonal block at elimination position " +
                           std::to_string(p) + " (leaf " + std::to_string(h->leaf_at[p]) + ")");
         }
       // Eq. 16: alpha_p* = -D_p^{-1} Z~_p*
-      sp.panel.launch(lev, h->d_P.p, nullptr, h->d_D.p, h->d_W.p, s);
+      sp.panel.launch_all(h->d_P.p, nullptr, h->d_D.p, h->d_W.p, s);
+      CK(cudaStreamSynchronize(s));                  // the level's tables are freed here
     }
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(s));

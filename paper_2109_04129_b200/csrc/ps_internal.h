@@ -52,7 +52,9 @@ struct GWork {
   int32_t sub;             // combine subgroup of this chunk: members are the non-critical chunks
   int32_t sub_r0, sub_r1;  // of rank [sub_r0, sub_r1) (rank = chunk index skipping crit)
   int32_t nsub;            // number of subgroups of the tile
-  int32_t pad;
+  int32_t sw_unit;         // slot reuse: the tile's partial-sum slots were last used by the
+  int32_t sw_need;         // unit sw_unit (>= 0); wait until done[sw_unit] >= sw_need (all its
+  int32_t pad;             // items precede this one in ticket order) before writing them
   int64_t slot;
 };
 
@@ -82,7 +84,7 @@ struct FlowArgs {
   int32_t narrow;          // 1: narrow 64 x 8 tiles (small nrhs), 0: 32 x 64 tiles
   int32_t mma;             // wide tiles: 0 = DFMA consumer, 1 = FP64 tensor-core (DMMA) consumer
   int32_t dfma_ks;         // reserved (0)
-  int32_t pad2;
+  int32_t issue_first;     // 1: a stage's refill is issued before its compute (PS_ISSUE_FIRST; measured 2-5 % slower)
 };
 
 // Tile geometry of the gather-GEMM kernel (ps_kernels.cu).

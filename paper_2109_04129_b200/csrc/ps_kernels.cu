@@ -166,12 +166,17 @@ __device__ __forceinline__ void bsync() {
   else __syncthreads();
 }
 
+// elements of one partial-sum slot: one output tile (narrow tiles are 4x smaller)
+__device__ __forceinline__ int64_t slot_elems(const FlowArgs& a) {
+  return a.narrow ? (int64_t)(GN_MT * GN_NT) : (int64_t)(GM_MT * GM_NT);
+}
+
 template <int E, bool WS = false>
 __device__ __forceinline__ bool splitk_combine(const FlowArgs& a, const GWork& w, double2 (&acc)[E],
                                                const int (&off)[E], const bool (&own)[E], int tid,
                                                int* s_flag) {
   if (w.nchunks <= 1) return true;
-  const int64_t TS = (int64_t)(GM_MT * GM_NT);
+  const int64_t TS = slot_elems(a);
   int32_t* ctr = a.counters + 1 + a.n_units + w.tile;
   const bool crit_mode = w.crit >= 0;
   const int nsub = w.nsub;
@@ -258,8 +263,16 @@ __device__ __forceinline__ void wait_dep_task(const FlowArgs& a, int dep, int nt
   const int32_t* flag = a.counters + 1 + P.unit0 + nt;
   while (ld_acquire(flag) < P.n_mt) __nanosleep(32);
 }
+// A split tile's partial-sum slots are recycled (Table::assign_slots): the
+// previous user's unit must be complete before this item writes them.
+__device__ __forceinline__ void wait_slot_reuse(const FlowArgs& a, const GWork& w) {
+  if (w.sw_unit < 0) return;
+  const int32_t* flag = a.counters + 1 + w.sw_unit;
+  while (ld_acquire(flag) < w.sw_need) __nanosleep(32);
+}
 __device__ __forceinline__ void wait_deps(const FlowArgs& a, const GWork& w, const GTask& T, int tid) {
   if (tid == 0 && T.idep >= 0) wait_dep_task(a, T.idep, w.nt);
+  if (tid == 1) wait_slot_reuse(a, w);
   for (int t = w.ta + tid; t < w.tb; t += 32) {
     const int dep = a.terms[t].dep;
     if (dep >= 0) wait_dep_task(a, dep, w.nt);
@@ -310,7 +323,7 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
   for (int r = 0; r < RM; ++r) acc[r] = make_double2(0.0, 0.0);
   if (crit_fin) {
     wait_group_sum(a, w, tid);
-    const double2* Gs = a.partial + (w.slot + w.crit) * (int64_t)(GM_MT * GM_NT);
+    const double2* Gs = a.partial + (w.slot + w.crit) * slot_elems(a);
 #pragma unroll
     for (int r = 0; r < RM; ++r) acc[r] = __ldcg(Gs + (rbase + r) * GM_NT + col);
   }
@@ -344,6 +357,16 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
     cp_wait<NSTAGE - 2>();
     __syncthreads();
     const int st = s % NSTAGE;
+    if (a.issue_first) {   // refill the stage computed last iteration before computing this one
+      // refill the stage consumed one iteration ago (all threads are past the barrier above)
+      const int sn = s + NSTAGE - 1;
+      if (sn < nsteps) {
+        const int stn = sn % NSTAGE;
+        issue_a<GM_MT, GM_NT>(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * STAGE_A);
+        issue_b<GM_MT, GM_NT>(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * STAGE_B);
+      }
+      cp_commit();
+    }
     const double2* As = As0 + st * STAGE_A + rbase;
     const double2* Bs = Bs0 + st * STAGE_B + col;
 #pragma unroll
@@ -352,14 +375,16 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
 #pragma unroll
       for (int r = 0; r < RM; ++r) cfma(acc[r], As[k * AS_LD + r], b);
     }
-    // refill the stage consumed one iteration ago (all threads are past the barrier above)
-    const int sn = s + NSTAGE - 1;
-    if (sn < nsteps) {
-      const int stn = sn % NSTAGE;
-      issue_a<GM_MT, GM_NT>(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * STAGE_A);
-      issue_b<GM_MT, GM_NT>(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * STAGE_B);
+    if (!a.issue_first) {
+      // refill the stage consumed one iteration ago (all threads are past the barrier above)
+      const int sn = s + NSTAGE - 1;
+      if (sn < nsteps) {
+        const int stn = sn % NSTAGE;
+        issue_a<GM_MT, GM_NT>(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * STAGE_A);
+        issue_b<GM_MT, GM_NT>(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * STAGE_B);
+      }
+      cp_commit();
     }
-    cp_commit();
   }
   cp_wait<0>();
   __syncthreads();          // all warps done with the stage buffers before the next item
@@ -440,7 +465,7 @@ __device__ __forceinline__ void item_body_dmma(const FlowArgs& a, const GWork& w
   if (crit_fin) {
     wait_group_sum(a, w, tid);
     if (kh == 0) {
-      const double2* Gs = a.partial + (w.slot + w.crit) * (int64_t)(GM_MT * GM_NT);
+      const double2* Gs = a.partial + (w.slot + w.crit) * slot_elems(a);
 #pragma unroll
       for (int m = 0; m < MT; ++m)
 #pragma unroll
@@ -483,6 +508,15 @@ __device__ __forceinline__ void item_body_dmma(const FlowArgs& a, const GWork& w
     cp_wait<NSTAGE - 2>();
     __syncthreads();
     const int st = s % NSTAGE;
+    if (a.issue_first) {   // refill the stage computed last iteration before computing this one
+      const int sn = s + NSTAGE - 1;
+      if (sn < nsteps) {
+        const int stn = sn % NSTAGE;
+        issue_a<GM_MT, GM_NT>(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * STAGE_A);
+        issue_b<GM_MT, GM_NT>(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * STAGE_B);
+      }
+      cp_commit();
+    }
     const double2* As = As0 + st * STAGE_A + (8 * kh + q) * GM_MT + g;
     const double2* Bs = Bs0 + st * STAGE_B + (8 * kh + q) * GM_NT + 16 * wc + g;
 #pragma unroll
@@ -507,13 +541,15 @@ __device__ __forceinline__ void item_body_dmma(const FlowArgs& a, const GWork& w
           dmma(cim[m][n][0], cim[m][n][1], av[m].y, bv[n].x);
         }
     }
-    const int sn = s + NSTAGE - 1;
-    if (sn < nsteps) {
-      const int stn = sn % NSTAGE;
-      issue_a<GM_MT, GM_NT>(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * STAGE_A);
-      issue_b<GM_MT, GM_NT>(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * STAGE_B);
+    if (!a.issue_first) {
+      const int sn = s + NSTAGE - 1;
+      if (sn < nsteps) {
+        const int stn = sn % NSTAGE;
+        issue_a<GM_MT, GM_NT>(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * STAGE_A);
+        issue_b<GM_MT, GM_NT>(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * STAGE_B);
+      }
+      cp_commit();
     }
-    cp_commit();
   }
   cp_wait<0>();
   __syncthreads();
@@ -596,7 +632,7 @@ __device__ __forceinline__ void item_body_narrow(const FlowArgs& a, const GWork&
   double2 acc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
   if (crit_fin) {
     if constexpr (!WS) wait_group_sum(a, w, tid);
-    const double2* Gs = a.partial + (w.slot + w.crit) * (int64_t)(GM_MT * GM_NT);
+    const double2* Gs = a.partial + (w.slot + w.crit) * slot_elems(a);
     acc[0] = __ldcg(Gs + row * GN_NT + cb);
     acc[1] = __ldcg(Gs + row * GN_NT + cb + 1);
   }
@@ -628,6 +664,15 @@ __device__ __forceinline__ void item_body_narrow(const FlowArgs& a, const GWork&
     cp_wait<NS - 2>();
     bsync<WS>();
     const int st = s % NS;
+    if (a.issue_first) {   // refill the stage computed last iteration before computing this one
+      const int sn = s + NS - 1;
+      if (sn < nsteps) {
+        const int stn = sn % NS;
+        issue_a<GN_MT, GN_NT>(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * sa);
+        issue_b<GN_MT, GN_NT>(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * sb);
+      }
+      cp_commit();
+    }
     if (live) {
       const double2* As = As0 + st * sa + row;
       const double2* Bs = Bs0 + st * sb + cb;
@@ -638,13 +683,15 @@ __device__ __forceinline__ void item_body_narrow(const FlowArgs& a, const GWork&
         cfma(acc[1], av, Bs[k * GN_NT + 1]);
       }
     }
-    const int sn = s + NS - 1;
-    if (sn < nsteps) {
-      const int stn = sn % NS;
-      issue_a<GN_MT, GN_NT>(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * sa);
-      issue_b<GN_MT, GN_NT>(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * sb);
+    if (!a.issue_first) {
+      const int sn = s + NS - 1;
+      if (sn < nsteps) {
+        const int stn = sn % NS;
+        issue_a<GN_MT, GN_NT>(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * sa);
+        issue_b<GN_MT, GN_NT>(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * sb);
+      }
+      cp_commit();
     }
-    cp_commit();
   }
   cp_wait<0>();
   bsync<WS>();
@@ -815,7 +862,7 @@ __device__ __forceinline__ void item_body_nk(const FlowArgs& a, const GWork& w, 
   const bool owns_init = (w.nchunks == 1) || (w.crit >= 0 ? w.chunk == w.crit : w.chunk == 0);
   double2 acc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
   if (crit_fin && ks == 0) {
-    const double2* Gs = a.partial + (w.slot + w.crit) * (int64_t)(GM_MT * GM_NT);
+    const double2* Gs = a.partial + (w.slot + w.crit) * slot_elems(a);
     acc[0] = __ldcg(Gs + row * GN_NT + cb);
     acc[1] = __ldcg(Gs + row * GN_NT + cb + 1);
   }
@@ -840,6 +887,15 @@ __device__ __forceinline__ void item_body_nk(const FlowArgs& a, const GWork& w, 
     cp_wait<WS_NSTAGE - 2>();
     bsync<true>();
     const int st = s % WS_NSTAGE;
+    if (a.issue_first) {   // refill the stage computed last iteration before computing this one
+      const int sn = s + WS_NSTAGE - 1;
+      if (sn < nsteps) {
+        const int stn = sn % WS_NSTAGE;
+        issue_a(sn * KCW, stages + stn * WS_SA);
+        issue_b(sn * KCW, stages + stn * WS_SA + WS_A);
+      }
+      cp_commit();
+    }
     if (live) {
       const double2* As = stages + st * WS_SA + (16 * ks) * MTW + row;
       const double2* Bs = stages + st * WS_SA + WS_A + (16 * ks) * GN_NT + cb;
@@ -850,13 +906,15 @@ __device__ __forceinline__ void item_body_nk(const FlowArgs& a, const GWork& w, 
         cfma(acc[1], av, Bs[k * GN_NT + 1]);
       }
     }
-    const int sn = s + WS_NSTAGE - 1;
-    if (sn < nsteps) {
-      const int stn = sn % WS_NSTAGE;
-      issue_a(sn * KCW, stages + stn * WS_SA);
-      issue_b(sn * KCW, stages + stn * WS_SA + WS_A);
+    if (!a.issue_first) {
+      const int sn = s + WS_NSTAGE - 1;
+      if (sn < nsteps) {
+        const int stn = sn % WS_NSTAGE;
+        issue_a(sn * KCW, stages + stn * WS_SA);
+        issue_b(sn * KCW, stages + stn * WS_SA + WS_A);
+      }
+      cp_commit();
     }
-    cp_commit();
   }
   cp_wait<0>();
   bsync<true>();
@@ -951,6 +1009,7 @@ __device__ void ws_scheduler(const FlowArgs& a, SlotWS* slots, KTabN* kts, int l
     // producers (lanes over segments), init producer, split-K group sum
     const int nt = sl.w.nt;
     if (lane == 0 && sl.T.idep >= 0) wait_dep_task(a, sl.T.idep, nt);
+    if (lane == 1) wait_slot_reuse(a, sl.w);
     for (int t = lane; t < tb - ta; t += 32)
       if (sl.seg[t].dep >= 0) wait_dep_task(a, sl.seg[t].dep, nt);
     if (lane == 0 && sl.w.nchunks > 1 && sl.w.crit >= 0 && sl.w.chunk == sl.w.crit) {

@@ -1,16 +1,65 @@
-"""Summarise a trace_flow.py capture (per-item timing of the dataflow kernel)."""
-import sys
+"""Summarise a program trace written by scripts/trace_prog.py:
+  python scripts/trace_stats.py gpurun_out/trace_prog.npz [--bin-us 5]
+Prints the busy/waiting CTA profile over time and the tasks whose completion
+gates the longest idle stretches (the critical path of the dataflow program)."""
+import argparse
+
 import numpy as np
-d = np.load(sys.argv[1] if len(sys.argv) > 1 else 'gpurun_out/trace_C2.npz')
-for nm in ['fwd', 'bwd', 'dinv', 'far1', 'far2']:
-    tr = d[nm].astype(np.float64)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("path")
+    ap.add_argument("--bin-us", type=float, default=5.0)
+    ap.add_argument("--top", type=int, default=25)
+    a = ap.parse_args()
+    tr = np.load(a.path)["prog"].astype(np.int64)
+    if len(tr) == 0:
+        print("empty trace")
+        return
     t0 = tr[:, 2].min()
-    f, r, c, e = [(tr[:, j] - t0) / 1e3 for j in (2, 3, 4, 5)]
-    wait, comp, pub = r - f, c - r, e - c
-    klen = tr[:, 11]
-    ks = np.ceil(klen / 16)
-    m = ks > 0
-    T = np.linspace(0, e.max(), 10)
-    busy = [int(((r <= t) & (c > t)).sum()) for t in T]
-    print(f"{nm:5s} items {len(tr):6d} span {e.max():7.0f}us wait {wait.mean():6.1f} comp {comp.mean():6.2f} "
-          f"pub {pub.mean():5.2f} us/kstep {np.median(comp[m] / ks[m]):.3f} ksteps {ks.sum():.0f} busy {busy}")
+    f, r, c, d = (tr[:, k] - t0 for k in (2, 3, 4, 5))
+    task, nch, klen = tr[:, 6], tr[:, 10], tr[:, 11]
+    T = d.max()
+    nsm = len(np.unique(tr[:, 1]))
+    print(f"items {len(tr)}  span {T / 1e3:.1f} us  SMs {nsm}")
+    wait, comp, fin = (r - f).sum(), (c - r).sum(), (d - c).sum()
+    tot = wait + comp + fin
+    print(f"item time: wait {wait / tot:.2%}  compute {comp / tot:.2%}  combine/finalise {fin / tot:.2%}")
+    b = a.bin_us * 1e3
+    nb = int(T // b) + 1
+    busy = np.zeros(nb)
+    waiting = np.zeros(nb)
+    for lo, hi, acc in ((r, c, busy), (f, r, waiting)):
+        for x0, x1 in zip(lo, hi):
+            i0, i1 = int(x0 // b), int(x1 // b)
+            if i0 == i1:
+                acc[i0] += (x1 - x0) / b
+            else:
+                acc[i0] += (b * (i0 + 1) - x0) / b
+                acc[i0 + 1:i1] += 1
+                acc[i1] += (x1 - b * i1) / b
+    print(f"\n{'t(us)':>8} {'computing':>10} {'waiting':>8}")
+    for i in range(nb):
+        print(f"{i * a.bin_us:8.1f} {busy[i]:10.1f} {waiting[i]:8.1f}")
+    # per task: first fetch, last ready, last done, items, k
+    order = np.argsort(task, kind="stable")
+    ts, idx = np.unique(task[order], return_index=True)
+    rows = []
+    for j, t in enumerate(ts):
+        sl = order[idx[j]: idx[j + 1] if j + 1 < len(idx) else len(order)]
+        rows.append((int(t), len(sl), f[sl].min(), r[sl].max(), d[sl].max(), int(klen[sl].sum()), int(nch[sl].max())))
+    rows.sort(key=lambda x: x[4])
+    # tasks with the longest wait-to-done (candidates for the critical path)
+    print(f"\ntasks {len(rows)}; longest ready->done spans:")
+    rows_span = sorted(rows, key=lambda x: -(x[4] - x[3]))[: a.top]
+    print(f"{'task':>7} {'items':>6} {'fetch':>8} {'ready':>8} {'done':>8} {'span':>7} {'k':>8} {'nch':>4}")
+    for t, n, ff, rr, dd, k, nc in rows_span:
+        print(f"{t:7d} {n:6d} {ff / 1e3:8.1f} {rr / 1e3:8.1f} {dd / 1e3:8.1f} {(dd - rr) / 1e3:7.1f} {k:8d} {nc:4d}")
+    # completion profile: done times of tasks by decile
+    dn = np.array([x[4] for x in rows]) / 1e3
+    print("\ntask completion percentiles (us):", np.percentile(dn, [10, 25, 50, 75, 90, 99, 100]).round(1))
+
+
+if __name__ == "__main__":
+    main()
