@@ -525,7 +525,8 @@ struct Table {
       return -1;
     }();
     fa.mma = mma_env >= 0 ? mma_env : mma;
-    fa.dfma_ks = 0;
+    static const int lean_issue = env_int("PS_LEAN_ISSUE", 1);
+    fa.lean_issue = lean_issue;
     static const int issue_first = env_int("PS_ISSUE_FIRST", 0);
     fa.issue_first = issue_first;
     if (pf && pf->trace_on && cls == pf->trace_cls) {

@@ -83,7 +83,7 @@ struct FlowArgs {
   int64_t* trace;          // optional: 6 x int64 per item (item, smid, t_fetch, t_ready, t_computed, t_done), ns
   int32_t narrow;          // 1: narrow 64 x 8 tiles (small nrhs), 0: 32 x 64 tiles
   int32_t mma;             // wide tiles: 0 = DFMA consumer, 1 = FP64 tensor-core (DMMA) consumer
-  int32_t dfma_ks;         // reserved (0)
+  int32_t lean_issue;      // narrow WS items: lean operand issue (PS_LEAN_ISSUE, default 1)
   int32_t issue_first;     // 1: a stage's refill is issued before its compute (PS_ISSUE_FIRST; measured 2-5 % slower)
 };
 

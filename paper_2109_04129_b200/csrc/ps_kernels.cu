@@ -97,6 +97,11 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool va
   const int n = valid ? 16 : 0;
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(n) : "memory");
 }
+// 16-byte global -> shared async copy, always valid (no zero-fill operand)
+__device__ __forceinline__ void cp_async16_all(void* smem, const void* gmem) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -853,9 +858,50 @@ __device__ __forceinline__ void item_body_nk(const FlowArgs& a, const GWork& w, 
       cp_async16(Bs + k * GN_NT + c, src, v);
     }
   };
+  // Lean variants (a.lean_issue): one k-table lookup per thread and stage when A is
+  // k-major, elements outside the tile simply not copied (shared stages are zeroed at
+  // kernel start and only ever hold finite values; B rows k >= klen are still
+  // zero-filled, so stale A there contributes 0), B columns >= nn skipped.
+  auto issue_a_lean = [&](int k0, double2* As) {
+    if (a_km) {
+      constexpr int QS = 256 / KCW;
+      const int k = tid % KCW, i = tid / KCW, kk = k0 + k;
+      if (kk < klen) {
+        const int64_t si = kt.kSi[kk];
+        const double2* base = a.A + kt.kA[kk] + (int64_t)(i0 + i) * si;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (i + q * QS < mm) cp_async16_all(As + k * MTW + i + q * QS, base + q * QS * si);
+      }
+    } else {
+      const int i = tid % MTW;
+      if (i < mm) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int kk = k0 + tid / MTW + q * (256 / MTW);
+          if (kk < klen) cp_async16_all(As + (kk - k0) * MTW + i, a.A + kt.kA[kk] + (int64_t)(i0 + i) * kt.kSi[kk]);
+        }
+      }
+    }
+  };
+  auto issue_b_lean = [&](int k0, double2* Bs) {
+#pragma unroll
+    for (int q = 0; q < (KCW * GN_NT + 255) / 256; ++q) {
+      const int e = tid + q * 256;
+      if ((KCW * GN_NT) % 256 != 0 && e >= KCW * GN_NT) break;
+      int c, k;
+      if (b_km) { k = e % KCW; c = e / KCW; } else { c = e % GN_NT; k = e / GN_NT; }
+      if (c < nn) {
+        const int kk = k0 + k;
+        const bool v = kk < klen;
+        cp_async16(Bs + k * GN_NT + c, v ? kt.kB[kk] + (int64_t)(c0 + c) * kt.kSc[kk] : a.B, v);
+      }
+    }
+  };
+  const bool lean = a.lean_issue != 0;
 #pragma unroll
   for (int s = 0; s < WS_NSTAGE - 1; ++s)
-    if (s < nsteps) issue_a(s * KCW, stages + s * WS_SA);
+    if (s < nsteps) { if (lean) issue_a_lean(s * KCW, stages + s * WS_SA); else issue_a(s * KCW, stages + s * WS_SA); }
   cp_commit();
   const double sgn = (double)T.sign;
   const bool crit_fin = (w.nchunks > 1 && w.crit >= 0 && w.chunk == w.crit);
@@ -879,10 +925,11 @@ __device__ __forceinline__ void item_body_nk(const FlowArgs& a, const GWork& w, 
   if (tr) tr[3] = gtimer();
 #pragma unroll
   for (int s = 0; s < WS_NSTAGE - 1; ++s) {
-    if (s < nsteps) issue_b(s * KCW, stages + s * WS_SA + WS_A);
+    if (s < nsteps) { if (lean) issue_b_lean(s * KCW, stages + s * WS_SA + WS_A); else issue_b(s * KCW, stages + s * WS_SA + WS_A); }
     cp_commit();
   }
   const bool live = (row < mm) && (cb < nn);
+  const bool two = !lean || (cb + 1 < nn);           // second column of the pair is a real column
   for (int s = 0; s < nsteps; ++s) {
     cp_wait<WS_NSTAGE - 2>();
     bsync<true>();
@@ -891,27 +938,42 @@ __device__ __forceinline__ void item_body_nk(const FlowArgs& a, const GWork& w, 
       const int sn = s + WS_NSTAGE - 1;
       if (sn < nsteps) {
         const int stn = sn % WS_NSTAGE;
-        issue_a(sn * KCW, stages + stn * WS_SA);
-        issue_b(sn * KCW, stages + stn * WS_SA + WS_A);
+        if (lean) {
+          issue_a_lean(sn * KCW, stages + stn * WS_SA);
+          issue_b_lean(sn * KCW, stages + stn * WS_SA + WS_A);
+        } else {
+          issue_a(sn * KCW, stages + stn * WS_SA);
+          issue_b(sn * KCW, stages + stn * WS_SA + WS_A);
+        }
       }
       cp_commit();
     }
     if (live) {
       const double2* As = stages + st * WS_SA + (16 * ks) * MTW + row;
       const double2* Bs = stages + st * WS_SA + WS_A + (16 * ks) * GN_NT + cb;
+      if (two) {
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const double2 av = As[k * MTW];
-        cfma(acc[0], av, Bs[k * GN_NT]);
-        cfma(acc[1], av, Bs[k * GN_NT + 1]);
+        for (int k = 0; k < 16; ++k) {
+          const double2 av = As[k * MTW];
+          cfma(acc[0], av, Bs[k * GN_NT]);
+          cfma(acc[1], av, Bs[k * GN_NT + 1]);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) cfma(acc[0], As[k * MTW], Bs[k * GN_NT]);
       }
     }
     if (!a.issue_first) {
       const int sn = s + WS_NSTAGE - 1;
       if (sn < nsteps) {
         const int stn = sn % WS_NSTAGE;
-        issue_a(sn * KCW, stages + stn * WS_SA);
-        issue_b(sn * KCW, stages + stn * WS_SA + WS_A);
+        if (lean) {
+          issue_a_lean(sn * KCW, stages + stn * WS_SA);
+          issue_b_lean(sn * KCW, stages + stn * WS_SA + WS_A);
+        } else {
+          issue_a(sn * KCW, stages + stn * WS_SA);
+          issue_b(sn * KCW, stages + stn * WS_SA + WS_A);
+        }
       }
       cp_commit();
     }
@@ -1033,6 +1095,8 @@ flow_kernel_ws(const FlowArgs a) {
     ws_scheduler(a, slots, kts, tid & 31);
     return;
   }
+  for (int e = tid; e < WS_NSTAGE * WS_SA; e += 256) stages[e] = make_double2(0.0, 0.0);
+  bsync<true>();
   for (int64_t j = 0;; ++j) {
     const int s = (int)(j & 1);
     bar_sync_n(1 + s, 288);                           // slot s full
