@@ -999,7 +999,7 @@ __device__ __forceinline__ void item_body_nk(const FlowArgs& a, const GWork& w, 
     bsync<true>();
   }
   int off[2] = {row * GN_NT + cb, row * GN_NT + cb + 1};
-  bool own[2] = {ks == 0, ks == 0};
+  bool own[2] = {ks == 0, ks == 0 && two};           // no partial traffic for a padding column
   const bool finalize = crit_fin ? true : splitk_combine<2, true>(a, w, acc, off, own, tid, s_last);
   if (finalize) {
     if (row < mm && ks == 0) {
