@@ -512,7 +512,8 @@ struct Table {
     fa.O = O; fa.I = I; fa.A = A; fa.B = B; fa.S = S;
     fa.counters = d_counters.p;
     fa.n_units = max_units;
-    fa.pad = 0;
+    static const int defer_fin = env_int("PS_DEFER_FIN", 1);
+    fa.defer_fin = defer_fin;
     fa.partial = d_partial.p;
     fa.trace = nullptr;
     fa.narrow = narrow;

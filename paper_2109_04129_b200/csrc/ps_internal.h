@@ -78,7 +78,7 @@ struct FlowArgs {
   double2* S;              // scratch vector base (chain stages of the sweeps)
   int32_t* counters;       // [0] ticket, [1 .. 1+n_units) done, then arrive[n_tiles]
   int32_t n_units;
-  int32_t pad;
+  int32_t defer_fin;       // narrow WS items: split-K combine by the finisher warp (PS_DEFER_FIN)
   double2* partial;        // split-K partial tiles, GM_MT * GM_NT each
   int64_t* trace;          // optional: 6 x int64 per item (item, smid, t_fetch, t_ready, t_computed, t_done), ns
   int32_t narrow;          // 1: narrow 64 x 8 tiles (small nrhs), 0: 32 x 64 tiles

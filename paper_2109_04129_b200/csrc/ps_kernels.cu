@@ -171,6 +171,9 @@ __device__ __forceinline__ void bsync() {
   else __syncthreads();
 }
 
+__device__ __forceinline__ void bar_sync_n(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void bar_arrive_n(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
 // elements of one partial-sum slot: one output tile (narrow tiles are 4x smaller)
 __device__ __forceinline__ int64_t slot_elems(const FlowArgs& a) {
   return a.narrow ? (int64_t)(GN_MT * GN_NT) : (int64_t)(GM_MT * GM_NT);
@@ -811,6 +814,14 @@ struct SlotWS {
   int64_t item;
   GTerm seg[GM_MAXSEG];
 };
+// Split-K hand-over from the compute warps to the finisher warp (deferred combine):
+// the item's descriptor and output addressing, double-buffered (named barriers
+// MAIL_FULL 6 + f / MAIL_EMPTY 8 + f, 288 threads).
+struct MailWS {
+  GWork w;
+  int64_t oO, sOi, sOc;
+  int32_t osel, sign, unit0, m, n, live;   // live 0: terminate
+};
 constexpr int WS_A = KC * GN_MT;                      // A tile of a narrow stage: 1024 complex
 constexpr int WS_SA = WS_A + 64 * GN_NT;              // + B tile (<= 64 k x 8 columns)
 constexpr int WS_NSTAGE = 3;
@@ -824,7 +835,7 @@ constexpr int WS_NSTAGE = 3;
 template <int MTW>
 __device__ __forceinline__ void item_body_nk(const FlowArgs& a, const GWork& w, const GTask& T,
                                              const KTabN& kt, double2* stages, int tid, int* s_last,
-                                             int64_t* tr) {
+                                             int64_t* tr, MailWS* mail, int& jm) {
   constexpr int KCW = 1024 / MTW, NKS = 64 / MTW;
   const int i0 = w.mt * GN_MT, c0 = w.nt * GN_NT;
   const int mm = min(GN_MT, T.m - i0), nn = min(GN_NT, T.n - c0);
@@ -1000,6 +1011,24 @@ __device__ __forceinline__ void item_body_nk(const FlowArgs& a, const GWork& w, 
   }
   int off[2] = {row * GN_NT + cb, row * GN_NT + cb + 1};
   bool own[2] = {ks == 0, ks == 0 && two};           // no partial traffic for a padding column
+  // publish the partial; the finisher warp combines (one warp: only for 1-2 column tiles,
+  // at 8 columns it becomes the bottleneck, measured)
+  if (a.defer_fin && w.nchunks > 1 && w.crit < 0 && nn <= 2) {
+    double2* P = a.partial + (w.slot + w.chunk) * slot_elems(a);
+    if (own[0]) __stcg(P + off[0], acc[0]);
+    if (own[1]) __stcg(P + off[1], acc[1]);
+    const int f = jm & 1;
+    if (jm >= 2) bar_sync_n(8 + f, 288);             // mail f consumed by the finisher
+    if (tid == 0) {
+      MailWS& M = mail[f];
+      M.w = w;
+      M.oO = T.oO; M.sOi = T.sOi; M.sOc = T.sOc;
+      M.osel = T.osel; M.sign = T.sign; M.unit0 = T.unit0; M.m = T.m; M.n = T.n; M.live = 1;
+    }
+    bar_arrive_n(6 + f, 288);                         // mail f full (partials stored before)
+    ++jm;
+    return;
+  }
   const bool finalize = crit_fin ? true : splitk_combine<2, true>(a, w, acc, off, own, tid, s_last);
   if (finalize) {
     if (row < mm && ks == 0) {
@@ -1017,9 +1046,6 @@ __device__ __forceinline__ void item_body_nk(const FlowArgs& a, const GWork& w, 
   }
 }
 constexpr size_t FLOW_WS_SMEM = (size_t)WS_NSTAGE * WS_SA * sizeof(double2) + 2 * sizeof(KTabN) + 2 * sizeof(SlotWS);
-
-__device__ __forceinline__ void bar_sync_n(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ void bar_arrive_n(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 __device__ void ws_scheduler(const FlowArgs& a, SlotWS* slots, KTabN* kts, int lane) {
   int32_t* ticket = a.counters;
@@ -1083,32 +1109,106 @@ __device__ void ws_scheduler(const FlowArgs& a, SlotWS* slots, KTabN* kts, int l
   }
 }
 
-__global__ void __launch_bounds__(288, 2)
+// Finisher warp (deferred split-K combine): for each handed-over chunk, count it in
+// its subgroup; the last arriver sums the subgroup's chunk slots in rank order
+// (then, with several subgroups, the last subgroup sums the subgroup sums) and
+// stores O = sign * sum — the same arithmetic and order as splitk_combine — and
+// publishes the tile. Never waits on other items, so it cannot deadlock; the
+// compute warps stream the next item meanwhile.
+__device__ void ws_finisher(const FlowArgs& a, MailWS* mail, int lane) {
+  int32_t* done = a.counters + 1;
+  const int64_t TS = slot_elems(a);
+  for (int64_t j = 0;; ++j) {
+    const int f = (int)(j & 1);
+    bar_sync_n(6 + f, 288);                           // mail f full
+    const MailWS M = mail[f];
+    bar_arrive_n(8 + f, 288);                         // mail f consumed
+    if (!M.live) return;
+    const GWork& w = M.w;
+    int32_t* ctr = a.counters + 1 + a.n_units + w.tile;
+    const int sg = w.sub, r0 = w.sub_r0, r1 = w.sub_r1, nsub = w.nsub;
+    int last = 0;
+    if (lane == 0) last = (atom_acq_rel(ctr + 1 + sg, 1) == (r1 - r0) - 1);
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (!last) continue;
+    const int i0 = w.mt * GN_MT, c0 = w.nt * GN_NT;
+    const int mm = min(GN_MT, M.m - i0), nn = min(GN_NT, M.n - c0), ne = mm * nn;
+    double2* Ob = ((M.osel & 1) ? a.S : a.O) + M.oO;
+    const double sgn = (double)M.sign;
+    auto store = [&](int row, int col, double2 v) {
+      __stcg(Ob + (int64_t)(i0 + row) * M.sOi + (int64_t)(c0 + col) * M.sOc, make_double2(sgn * v.x, sgn * v.y));
+    };
+    for (int el = lane; el < ne; el += 32) {
+      const int row = el / nn, col = el - row * nn, off = row * GN_NT + col;
+      double2 acc = make_double2(0.0, 0.0);
+      for (int r = r0; r < r1; ++r) {
+        const double2 v = __ldcg(a.partial + (w.slot + r) * TS + off);
+        acc.x += v.x;
+        acc.y += v.y;
+      }
+      if (nsub > 1) __stcg(a.partial + (w.slot + w.nchunks + sg) * TS + off, acc);
+      else store(row, col, acc);
+    }
+    if (nsub > 1) {
+      __syncwarp();
+      int last2 = 0;
+      if (lane == 0) last2 = (atom_acq_rel(ctr, 1) == nsub - 1);
+      last2 = __shfl_sync(0xffffffffu, last2, 0);
+      if (!last2) continue;
+      for (int el = lane; el < ne; el += 32) {
+        const int row = el / nn, col = el - row * nn, off = row * GN_NT + col;
+        double2 acc = make_double2(0.0, 0.0);
+        for (int q = 0; q < nsub; ++q) {
+          const double2 v = __ldcg(a.partial + (w.slot + w.nchunks + q) * TS + off);
+          acc.x += v.x;
+          acc.y += v.y;
+        }
+        store(row, col, acc);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) red_release(done + M.unit0 + w.nt, 1);
+  }
+}
+
+__global__ void __launch_bounds__(320, 2)
 flow_kernel_ws(const FlowArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* stages = reinterpret_cast<double2*>(smem_raw);
   KTabN* kts = reinterpret_cast<KTabN*>(stages + WS_NSTAGE * WS_SA);
   SlotWS* slots = reinterpret_cast<SlotWS*>(kts + 2);
   __shared__ int s_last;
+  __shared__ MailWS s_mail[2];
   const int tid = threadIdx.x;
+  if (tid >= 288) {
+    ws_finisher(a, s_mail, tid & 31);
+    return;
+  }
   if (tid >= 256) {
     ws_scheduler(a, slots, kts, tid & 31);
     return;
   }
   for (int e = tid; e < WS_NSTAGE * WS_SA; e += 256) stages[e] = make_double2(0.0, 0.0);
   bsync<true>();
+  int jm = 0;                                         // mails handed to the finisher
   for (int64_t j = 0;; ++j) {
     const int s = (int)(j & 1);
     bar_sync_n(1 + s, 288);                           // slot s full
     const SlotWS& sl = slots[s];
     const int64_t item = sl.item;
-    if (item < 0) return;
+    if (item < 0) {                                   // terminate the finisher
+      const int f = jm & 1;
+      if (jm >= 2) bar_sync_n(8 + f, 288);
+      if (tid == 0) s_mail[f].live = 0;
+      bar_arrive_n(6 + f, 288);
+      return;
+    }
     int64_t* tr = (a.trace != nullptr && tid == 0) ? a.trace + 6 * item : nullptr;
     if (tr) { tr[0] = item; tr[1] = smid(); tr[2] = gtimer(); }
     const int mrows = min(GN_MT, sl.T.m - sl.w.mt * GN_MT);
-    if (mrows <= 16) item_body_nk<16>(a, sl.w, sl.T, kts[s], stages, tid, &s_last, tr);
-    else if (mrows <= 32) item_body_nk<32>(a, sl.w, sl.T, kts[s], stages, tid, &s_last, tr);
-    else item_body_nk<64>(a, sl.w, sl.T, kts[s], stages, tid, &s_last, tr);
+    if (mrows <= 16) item_body_nk<16>(a, sl.w, sl.T, kts[s], stages, tid, &s_last, tr, s_mail, jm);
+    else if (mrows <= 32) item_body_nk<32>(a, sl.w, sl.T, kts[s], stages, tid, &s_last, tr, s_mail, jm);
+    else item_body_nk<64>(a, sl.w, sl.T, kts[s], stages, tid, &s_last, tr, s_mail, jm);
     if (tr) tr[5] = gtimer();
     bsync<true>();                                    // every compute warp is done with slot s
     bar_arrive_n(3 + s, 288);                         // slot s empty
@@ -1122,7 +1222,7 @@ int flow_ws_resident_ctas() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(flow_kernel_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FLOW_WS_SMEM);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, flow_kernel_ws, 288, FLOW_WS_SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, flow_kernel_ws, 320, FLOW_WS_SMEM);
     n = sms * (per_sm > 0 ? per_sm : 1);
   }
   return n;
@@ -1159,7 +1259,7 @@ void launch_flow(const FlowArgs& a, int grid, cudaStream_t st) {
   if (a.narrow && ws) {
     int g = grid > 0 ? grid : flow_ws_resident_ctas();
     if (g > a.nwork) g = (int)a.nwork;
-    flow_kernel_ws<<<g, 288, FLOW_WS_SMEM, st>>>(a);
+    flow_kernel_ws<<<g, 320, FLOW_WS_SMEM, st>>>(a);
     return;
   }
   static const bool one = [] {
