@@ -1610,7 +1610,7 @@ void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
   int64_t Ttot = 0;
   for (int64_t c = 0; c < ncl; ++c) { toff[c] = sp.oTMP + Ttot; Ttot += h->cl_sr[c] * R; }
   const int resident = flow_resident_ctas();
-  P.key_stagger = 0.0;
+  P.key_stagger = env_int("PS_PROG_STAGGER", 0);     // column tile b enters b * this many key levels later
   P.early_keys = true;
   // far field on the tensor-core consumer with long chunks, as in the stage tables
   const bool far_mma = !P.narrow && env_int("PS_FAR_MMA", 1) != 0;
