@@ -405,7 +405,8 @@ struct Table {
             for (int32_t q = ch[c][2]; q < ch[c][3]; ++q)
               if (terms[q].dep >= 0) kp = std::max(kp, task_key[terms[q].dep]);
             if (t.idep >= 0) kp = std::max(kp, task_key[t.idep]);
-            k = std::min(key_base, kp + 0.5);
+            static const double early_off = 0.01 * env_int("PS_EARLY_OFF", 50);   // key levels after the producer
+            k = std::min(key_base, kp + early_off);
           }
           keys.push_back(k + b * key_stagger);
           keys_late.push_back(key_base + b * key_stagger);
