@@ -221,8 +221,9 @@ struct Table {
   // live meanwhile; if the recycled pool still exceeds the budget (C5), the batch is
   // re-ordered by its tasks' own keys (chunks of a tile adjacent) and re-assigned.
   void sort_close_bounded() {
-    static const int64_t budget = (int64_t)env_int("PS_SLOT_BUDGET_MB", 4096) << 20;
-    const bool can_redo = early_keys && budget > 0;
+    static const int64_t budget_mb = env_int("PS_SLOT_BUDGET_MB", 4096);   // < 0: always task-keyed
+    const int64_t budget = budget_mb < 0 ? 0 : budget_mb << 20;
+    const bool can_redo = early_keys && budget_mb != 0;
     std::vector<GWork> w0;
     std::vector<double> kl;
     if (can_redo) { w0 = work; kl = keys_late; }
@@ -230,7 +231,7 @@ struct Table {
     const int64_t ns = n_slots, ms = max_slots, cb0 = cur_batch_start;
     sort_by_key();
     close_batch();
-    if (can_redo && max_slots * slot_elems() * 16 > budget) {
+    if (can_redo && max_slots * slot_elems() * 16 >= budget) {
       work.swap(w0);
       keys = kl;
       batches.pop_back();

@@ -8,6 +8,11 @@
   PS_MMA=dfma      every wide table on the DFMA consumer (far field included)
   PS_MMA_1CTA=1    tensor-core tables on the one-CTA-per-SM kernel instance
   PS_SOLVE=stages  one launch per operator instead of the single-launch program
+  PS_SLOT_BUDGET_MB=-1 partial-slot budget exceeded: the program falls back to task-keyed
+                   ticket order (the path C5 takes)
+  PS_LEAN_ISSUE=0  narrow items with the zero-filling operand issue
+  PS_DEFER_FIN=0   narrow split-K combine in line (no finisher warp)
+  PS_SLOT_REUSE=0  one partial slot per split chunk (no recycling)
 
 Each must match the oracle to the north-star bar (relative L2 <= 1e-11 per RHS).
 """
@@ -48,7 +53,9 @@ def _run(path, nrhs, env, out):
 
 
 @pytest.mark.parametrize("env", [{"PS_CHAINS": "0"}, {"PS_NARROW_WS": "0"}, {"PS_MMA": "dmma"},
-                                 {"PS_MMA": "dfma"}, {"PS_MMA_1CTA": "1"}, {"PS_SOLVE": "stages"}, {}],
+                                 {"PS_MMA": "dfma"}, {"PS_MMA_1CTA": "1"}, {"PS_SOLVE": "stages"},
+                                 {"PS_SLOT_BUDGET_MB": "-1"}, {"PS_LEAN_ISSUE": "0"}, {"PS_DEFER_FIN": "0"},
+                                 {"PS_SLOT_REUSE": "0"}, {}],
                          ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default")
 @pytest.mark.parametrize("nrhs", [1, 70])
 def test_variant_matches_oracle(cfgdata, tmp_path, env, nrhs):
