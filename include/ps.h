@@ -215,6 +215,8 @@ enum {
   PS_INFO_CHAINS,            /* elimination-tree chain pieces with >= 2 leaves (applied through T_c) */
   PS_INFO_CHAIN_HEIGHT,      /* levels of the chain graph (dependent stages of a sweep / 2) */
   PS_INFO_T_ENTRIES,         /* complex entries of all T_c (U_c x U_c each) */
+  PS_INFO_OP_BYTES,          /* device bytes of the operator this handle holds (alpha panels, D^-1, T, far
+                                stacks); a row-partition rank holds only its share after ps_setup */
   PS_INFO_COUNT
 };
 int ps_info(const ps_handle* h, double* out, int n);

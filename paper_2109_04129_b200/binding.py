@@ -22,7 +22,7 @@ STATUS_NAMES = ["PS_OK", "PS_EINVAL", "PS_EIO", "PS_EFORMAT", "PS_ENOMEM", "PS_E
 PS_OP_RT, PS_OP_DINV, PS_OP_R, PS_OP_ZF, PS_OP_U = 1, 2, 3, 4, 5
 INFO_KEYS = ["N", "n_leaves", "n_near", "n_far", "alpha_blocks", "nR", "nD", "nF", "height",
              "depth", "setup_madds", "setup_done", "nranks", "own_rows", "sep_rows", "chains",
-             "chain_height", "T_entries"]
+             "chain_height", "T_entries", "op_bytes"]
 
 
 class PsError(RuntimeError):

@@ -646,6 +646,7 @@ struct ps_handle {
   Prof prof;
   // ---- row partition (ps_dist.partition = 1) ----
   int rank = 0, nranks = 1, part_mode = 0;
+  bool sharded = false;                    // operator reduced to this rank's share (shard_operator)
   std::vector<int32_t> owner, far_owner;   // per position: interior rank (-1 separator); far-row rank
   std::vector<int64_t> doff;               // first row of position p in the partitioned layout:
                                            // [rank 0 interior | ... | rank P-1 interior | separators],
@@ -1236,6 +1237,63 @@ void ensure_far(ps_handle* h, cudaStream_t s) {
   }
   h->d_far.p = h->d_farbuf.p;
   h->Fbase = (int64_t)(h->d_farbuf.p - h->d_op.p);
+}
+
+// Row partition: after setup, keep only the operator blocks this rank's
+// tables read — alpha panels P_p and D_p^-1 of its interior positions and the separators,
+// and T_c of the chains that touch them — in new, compact allocations (the far stacks
+// stay whole). Setup itself ran replicated; the solve then holds ~1/P of P, D and T.
+void shard_operator(ps_handle* h, cudaStream_t s) {
+  const int64_t nl = h->nl;
+  const int g = h->rank;
+  auto need = [&](int64_t p) { return h->owner[p] == g || h->owner[p] < 0; };
+  std::vector<int64_t> Poff2(nl, -1), Doff2(nl, -1);
+  int64_t P2 = 0, D2 = 0;
+  for (int64_t p = 0; p < nl; ++p)
+    if (need(p)) { Poff2[p] = P2; P2 += h->nsz[p] * h->S[p]; }
+  for (int64_t p = 0; p < nl; ++p)
+    if (need(p)) { Doff2[p] = D2; D2 += h->nsz[p] * h->nsz[p]; }
+  DevBuf<double2> op2;
+  op2.alloc(std::max<int64_t>(P2 + D2, 1));
+  for (int64_t p = 0; p < nl; ++p) {
+    if (!need(p)) continue;
+    const int64_t np_ = h->nsz[p];
+    if (np_ * h->S[p] > 0)
+      CK(cudaMemcpyAsync(op2.p + Poff2[p], h->d_op.p + h->Pbase + h->Poff[p], 16 * np_ * h->S[p],
+                         cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(op2.p + P2 + Doff2[p], h->d_op.p + h->Dbase + h->Doff[p], 16 * np_ * np_,
+                       cudaMemcpyDeviceToDevice, s));
+  }
+  const int64_t nc = (int64_t)h->chains.size();
+  std::vector<int64_t> Toff2(h->ch_Toff.size(), -1);
+  int64_t T2 = 0;
+  for (int64_t c = 0; c < nc; ++c) {
+    if (h->ch_Toff[c] < 0) continue;
+    bool any = false;
+    for (int32_t q : h->chains[c]) any = any || need(q);
+    if (any) { Toff2[c] = T2; T2 += h->ch_U[c] * h->ch_U[c]; }
+  }
+  DevBuf<double2> t2;
+  t2.alloc(std::max<int64_t>(T2, 1));
+  for (int64_t c = 0; c < nc; ++c)
+    if (Toff2[c] >= 0)
+      CK(cudaMemcpyAsync(t2.p + Toff2[c], h->d_T.p + h->ch_Toff[c], 16 * h->ch_U[c] * h->ch_U[c],
+                         cudaMemcpyDeviceToDevice, s));
+  CK(cudaStreamSynchronize(s));
+  h->d_op = std::move(op2);
+  h->d_T = std::move(t2);
+  h->Poff.swap(Poff2);
+  h->Doff.swap(Doff2);
+  h->ch_Toff.swap(Toff2);
+  h->Plen = P2; h->Dlen = D2; h->Tlen = T2;
+  h->Pbase = 0; h->Dbase = P2;
+  h->d_P.p = h->d_op.p;
+  h->d_D.p = h->d_op.p + P2;
+  h->Tbase = (int64_t)(h->d_T.p - h->d_op.p);
+  ensure_far(h, s);                                   // re-derive Fbase from the new d_op
+  h->plan.reset();
+  h->dplan.reset();
+  h->sharded = true;
 }
 
 // T_c = (I - A_c^T)^{-1} of every chain piece with L >= 2 (see ps_handle): the
@@ -2604,6 +2662,8 @@ ps_status ps_setup(ps_handle* h, const ps_setup_opts* opts) {
     h->Tbase = (int64_t)(h->d_T.p - h->d_op.p);
     chain_setup(h, s);
     CK(cudaStreamSynchronize(s));
+    static const int shard_env = env_int("PS_SHARD", 1);
+    if (h->part_mode && shard_env) shard_operator(h, s);
     h->plan.reset();                                  // plans made before setup (ps_apply Z_F) are stale
     h->dplan.reset();
     h->setup_done = true;
@@ -2723,6 +2783,8 @@ ps_status ps_apply(ps_handle* h, int op, int64_t nrhs, const void* Xin, void* Yo
   if (op < PS_OP_RT || op > PS_OP_U || nrhs < 1 || !Xin || !Yout)
     return fail(h, PS_EINVAL, "ps_apply: bad arguments");
   if (op != PS_OP_ZF && !h->setup_done) return fail(h, PS_ESTATE, "ps_apply: ps_setup has not run");
+  if (h->sharded)
+    return fail(h, PS_ESTATE, "ps_apply: the operator of a row-partition rank is sharded (use ps_solve)");
   try {
     CK(cudaSetDevice(h->device));
     cudaStream_t s = h->stream;
@@ -2920,6 +2982,7 @@ int ps_info(const ps_handle* h, double* out, int n) {
   v[PS_INFO_NRANKS] = h->part_mode ? h->nranks : 1;
   v[PS_INFO_OWN_ROWS] = h->part_mode ? (double)h->own_rows : (double)h->N;
   v[PS_INFO_SEP_ROWS] = h->part_mode ? (double)h->Nsep : 0.0;
+  v[PS_INFO_OP_BYTES] = 16.0 * ((double)h->d_op.n + (double)h->d_T.n + (double)h->d_farbuf.n);
   {
     double nchain = 0, tent = 0;
     for (size_t c = 0; c < h->chains.size(); ++c)
@@ -2937,7 +3000,7 @@ int ps_info(const ps_handle* h, double* out, int n) {
 }
 
 int64_t ps_get_dinv(ps_handle* h, int64_t pos, void* out) {
-  if (!h || !out || pos < 0 || pos >= h->nl || !h->setup_done) return -1;
+  if (!h || !out || pos < 0 || pos >= h->nl || !h->setup_done || h->Doff[pos] < 0) return -1;   // < 0: not this rank's
   const int64_t n = h->nsz[pos];
   if (cudaMemcpy(out, h->d_D.p + h->Doff[pos], 16 * n * n, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
   return n;

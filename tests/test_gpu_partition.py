@@ -106,6 +106,18 @@ def test_group_c2_bench_size(cfgdata):
         warnings.simplefilter("ignore")
         solve_group(hs, Bd, Xd)
     assert rel_l2_cols(_host(Xd), ref.x).max() <= TOL
+    # every rank holds only its share of alpha panels, D^-1 and T (the far stacks stay whole)
+    h1 = PsHandle(meta["hm"], device=0)
+    h1.setup()
+    whole = h1.info()["op_bytes"]
+    h1.close()
+    held = [h.info()["op_bytes"] for h in hs]
+    assert max(held) < whole, (held, whole)
+    with pytest.raises(PsError) as e:          # per-operator diagnostics need the whole operator
+        hs[0].apply(1, Bd, torch.empty_like(Bd))
+    assert e.value.status == PS_ESTATE
+    for h in hs:
+        h.close()
 
 
 def test_group_errors(cfgdata):
