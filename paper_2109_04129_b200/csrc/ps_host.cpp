@@ -1713,9 +1713,11 @@ void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
     return v;
   };
   // forward sweep in place on `buf`; init_dep[p] produces the initial rows p (or none)
+  static const int direct_ends = env_int("PS_DIRECT_ENDS", 1);   // chain end pieces skip the identity T copy
   auto fwd_stage = [&](int64_t buf, std::vector<int32_t>& out, const std::vector<int32_t>* init_dep) {
     auto prod = [&](int32_t d) { return out[d] >= 0 ? out[d] : (init_dep ? (*init_dep)[d] : -1); };
     std::vector<int32_t> et(nl, -1);
+    std::vector<char> in_buf(nl, 0);
     for (const auto& cl : lev_f) {
       std::vector<std::pair<int64_t, int64_t>> mk;
       for (int32_t c : cl)
@@ -1733,9 +1735,12 @@ void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
           std::vector<std::pair<int32_t, int32_t>> gl;
           for (auto [d, idx] : h->gath[p])
             if (h->chain_of[d] != c) gl.push_back({d, idx});
-          if (single && gl.empty()) continue;
+          // the chain's first piece has no T product (T_c[0, 0] = I): its e is its y, written in place
+          const bool direct = single || (direct_ends && p == h->chains[c][0]);
+          if (direct) in_buf[p] = 1;
+          if (direct && gl.empty()) continue;            // y_p = its input rows: nothing to do
           const int64_t np_ = h->nsz[p];
-          const int64_t o = (single ? buf : SC) + h->eoff[p] * R;
+          const int64_t o = (direct ? buf : SC) + h->eoff[p] * R;
           int32_t t = P.add_task(o, R, 1, buf + h->eoff[p] * R, R, 1, (int)np_, (int)R, +1);
           if (init_dep) P.tasks[t].idep = (*init_dep)[p];
           for (auto [d, idx] : by_height(gl)) {
@@ -1743,7 +1748,7 @@ void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
             P.add_term(t, Pb + h->Poff[d] + h->pcol[d][idx] * nd, nd, 1, buf + h->eoff[d] * R, R, 1, (int)nd, prod(d));
           }
           P.tile(t, -1, stpE);
-          (single ? out : et)[p] = t;
+          (direct ? out : et)[p] = t;
         }
       }
       mk.clear();
@@ -1757,12 +1762,14 @@ void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
         const int64_t U = h->ch_U[c], To = Tb + h->ch_Toff[c];
         for (size_t i = 0; i < h->chains[c].size(); ++i) {
           const int32_t p = h->chains[c][i];
+          if (in_buf[p]) continue;                       // first piece: y written by its E task (or input)
           const int64_t np_ = h->nsz[p];
           int32_t t = P.add_task(buf + h->eoff[p] * R, R, 1, SC + h->eoff[p] * R, R, 1, (int)np_, (int)R, +1);
           P.tasks[t].idep = et[p];
           for (size_t j = 0; j < i; ++j) {
             const int32_t q = h->chains[c][j];
-            P.add_term(t, To + h->cpos[p] + h->cpos[q] * U, 1, U, SC + h->eoff[q] * R, R, 1, (int)h->nsz[q], et[q]);
+            P.add_term(t, To + h->cpos[p] + h->cpos[q] * U, 1, U, (in_buf[q] ? buf : SC) + h->eoff[q] * R, R, 1,
+                       (int)h->nsz[q], in_buf[q] ? prod(q) : et[q]);
           }
           P.tile(t, 0, stpY);
           out[p] = t;
@@ -1787,6 +1794,7 @@ void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
   auto bwd_stage = [&](int64_t init, int64_t out_buf, std::vector<int32_t>& out,
                        const std::vector<int32_t>& init_dep) {
     std::vector<int32_t> ft(nl, -1);
+    std::vector<char> in_buf(nl, 0);
     for (const auto& cl : lev_b) {
       std::vector<std::pair<int64_t, int64_t>> mk;
       for (int32_t c : cl)
@@ -1802,7 +1810,10 @@ void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
         const bool single = h->chains[c].size() == 1;
         for (int32_t p : h->chains[c]) {
           const int64_t np_ = h->nsz[p];
-          const int64_t o = (single ? out_buf : SC) + h->eoff[p] * R;
+          // the chain's top piece has no T product: its f is its w, written directly
+          const bool direct = single || (direct_ends && p == h->chains[c].back());
+          if (direct) in_buf[p] = 1;
+          const int64_t o = (direct ? out_buf : SC) + h->eoff[p] * R;
           int32_t t = P.add_task(o, R, 1, init + h->eoff[p] * R, R, 1, (int)np_, (int)R, +1);
           P.tasks[t].idep = init_dep[p];
           for (size_t i = 0; i < h->st[p].size(); ++i) {
@@ -1812,7 +1823,7 @@ void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
                        (int)h->nsz[j], out[j]);
           }
           P.tile(t, +1, stpF);
-          (single ? out : ft)[p] = t;
+          (direct ? out : ft)[p] = t;
         }
       }
       mk.clear();
@@ -1827,12 +1838,14 @@ void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
         const auto& ch = h->chains[c];
         for (size_t i = 0; i < ch.size(); ++i) {
           const int32_t p = ch[i];
+          if (in_buf[p]) continue;                       // top piece: w written by its F task
           const int64_t np_ = h->nsz[p];
           int32_t t = P.add_task(out_buf + h->eoff[p] * R, R, 1, SC + h->eoff[p] * R, R, 1, (int)np_, (int)R, +1);
           P.tasks[t].idep = ft[p];
           for (size_t j = i + 1; j < ch.size(); ++j) {
             const int32_t q = ch[j];
-            P.add_term(t, To + h->cpos[q] + h->cpos[p] * U, U, 1, SC + h->eoff[q] * R, R, 1, (int)h->nsz[q], ft[q]);
+            P.add_term(t, To + h->cpos[q] + h->cpos[p] * U, U, 1, (in_buf[q] ? out_buf : SC) + h->eoff[q] * R, R, 1,
+                       (int)h->nsz[q], in_buf[q] ? out[q] : ft[q]);
           }
           P.tile(t, 0, stpW);
           out[p] = t;
