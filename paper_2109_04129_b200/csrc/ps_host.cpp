@@ -2111,6 +2111,7 @@ void build_dist_plan(ps_handle* h, DistPlan& dp, int64_t R) {
   auto mine = [&](int64_t p) { return h->owner[p] == g; };
   auto sep = [&](int64_t p) { return h->owner[p] < 0; };
   const int64_t Pb = h->Pbase, Db = h->Dbase, Fb = h->Fbase;
+  static const int direct_ends = env_int("PS_DIRECT_ENDS", 1);   // as build_program
   // Chain-collapsed sweeps of the partitioned solve (as build_chain_sweeps): the
   // chain pieces are cut where the owner changes (interior of this rank / another
   // rank / separator); a cut piece uses the principal sub-block of its chain's T_c
@@ -2144,6 +2145,7 @@ void build_dist_plan(ps_handle* h, DistPlan& dp, int64_t R) {
     T.early_keys = true;
     double key = 0;
     std::vector<int32_t> ft(nl, -1), et(nl, -1);
+    std::vector<char> in_buf(nl, 0);
     std::vector<int32_t> order;
     for (size_t k = 0; k < dpieces.size(); ++k)
       if (interior ? dpieces[k].own == g : dpieces[k].own < 0) order.push_back((int32_t)k);
@@ -2159,28 +2161,32 @@ void build_dist_plan(ps_handle* h, DistPlan& dp, int64_t R) {
         std::vector<std::pair<int32_t, int32_t>> gl;
         for (auto [d, idx] : h->gath[p])
           if (dpiece_of[d] != k && (interior ? mine(d) : sep(d))) gl.push_back({d, idx});
-        if (single && gl.empty()) continue;
+        const bool direct = single || (direct_ends && p == nodes[0]);   // no T product: write y directly
+        if (direct) in_buf[p] = 1;
+        if (direct && gl.empty()) continue;
         const int64_t np_ = h->nsz[p];
-        int32_t t = T.add_task((single ? buf : SCo) + h->doff[p] * R, R, 1, buf + h->doff[p] * R, R, 1, (int)np_,
+        int32_t t = T.add_task((direct ? buf : SCo) + h->doff[p] * R, R, 1, buf + h->doff[p] * R, R, 1, (int)np_,
                                (int)R, +1);
         for (auto [d, idx] : gl) {
           const int64_t nd = h->nsz[d];
           T.add_term(t, Pb + h->Poff[d] + h->pcol[d][idx] * nd, nd, 1, buf + h->doff[d] * R, R, 1, (int)nd, ft[d]);
         }
         T.tile(t, 0, wsteps);
-        (single ? ft : et)[p] = t;
+        (direct ? ft : et)[p] = t;
       }
       if (single) continue;
       const int64_t U = h->ch_U[Pc.c], To = h->Tbase + h->ch_Toff[Pc.c];
       T.key_base = key++;
       for (size_t i = 0; i < nodes.size(); ++i) {
         const int32_t p = nodes[i];
+        if (in_buf[p]) continue;
         const int64_t np_ = h->nsz[p];
         int32_t t = T.add_task(buf + h->doff[p] * R, R, 1, SCo + h->doff[p] * R, R, 1, (int)np_, (int)R, +1);
         T.tasks[t].idep = et[p];
         for (size_t j = 0; j < i; ++j) {
           const int32_t q = nodes[j];
-          T.add_term(t, To + h->cpos[p] + h->cpos[q] * U, 1, U, SCo + h->doff[q] * R, R, 1, (int)h->nsz[q], et[q]);
+          T.add_term(t, To + h->cpos[p] + h->cpos[q] * U, 1, U, (in_buf[q] ? buf : SCo) + h->doff[q] * R, R, 1,
+                     (int)h->nsz[q], in_buf[q] ? ft[q] : et[q]);
         }
         T.tile(t, 0, wsteps);
         ft[p] = t;
@@ -2223,6 +2229,7 @@ void build_dist_plan(ps_handle* h, DistPlan& dp, int64_t R) {
     T.early_keys = true;
     double key = 0;
     std::vector<int32_t> wt(nl, -1), ft(nl, -1);
+    std::vector<char> in_buf(nl, 0);
     std::vector<int32_t> order;
     for (size_t k = 0; k < dpieces.size(); ++k)
       if (dpieces[k].own == g || dpieces[k].own < 0) order.push_back((int32_t)k);
@@ -2236,7 +2243,9 @@ void build_dist_plan(ps_handle* h, DistPlan& dp, int64_t R) {
       T.key_base = key++;
       for (int32_t p : nodes) {
         const int64_t np_ = h->nsz[p];
-        int32_t t = T.add_task((single ? out : SCo) + h->doff[p] * R, R, 1, in + h->doff[p] * R, R, 1, (int)np_,
+        const bool direct = single || (direct_ends && p == nodes.back());   // no T product: write w directly
+        if (direct) in_buf[p] = 1;
+        int32_t t = T.add_task((direct ? out : SCo) + h->doff[p] * R, R, 1, in + h->doff[p] * R, R, 1, (int)np_,
                                (int)R, +1);
         for (size_t i = 0; i < h->st[p].size(); ++i) {
           const int32_t j = h->st[p][i];
@@ -2246,19 +2255,21 @@ void build_dist_plan(ps_handle* h, DistPlan& dp, int64_t R) {
                      (int)h->nsz[j], wt[j]);
         }
         T.tile(t, 0, wsteps);
-        (single ? wt : ft)[p] = t;
+        (direct ? wt : ft)[p] = t;
       }
       if (single) continue;
       const int64_t U = h->ch_U[Pc.c], To = h->Tbase + h->ch_Toff[Pc.c];
       T.key_base = key++;
       for (size_t i = 0; i < nodes.size(); ++i) {
         const int32_t p = nodes[i];
+        if (in_buf[p]) continue;
         const int64_t np_ = h->nsz[p];
         int32_t t = T.add_task(out + h->doff[p] * R, R, 1, SCo + h->doff[p] * R, R, 1, (int)np_, (int)R, +1);
         T.tasks[t].idep = ft[p];
         for (size_t j = i + 1; j < nodes.size(); ++j) {
           const int32_t q = nodes[j];
-          T.add_term(t, To + h->cpos[q] + h->cpos[p] * U, U, 1, SCo + h->doff[q] * R, R, 1, (int)h->nsz[q], ft[q]);
+          T.add_term(t, To + h->cpos[q] + h->cpos[p] * U, U, 1, (in_buf[q] ? out : SCo) + h->doff[q] * R, R, 1,
+                     (int)h->nsz[q], in_buf[q] ? wt[q] : ft[q]);
         }
         T.tile(t, 0, wsteps);
         wt[p] = t;
