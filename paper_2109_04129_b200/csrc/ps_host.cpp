@@ -256,7 +256,7 @@ struct Table {
     t.t0 = t.t1 = (int32_t)terms.size();
     t.K = 0;
     t.unit0 = 0; t.n_mt = (m + GM_MT - 1) / GM_MT;
-    t.a_kmajor = 0; t.b_kmajor = 0; t.idep = -1; t.osel = 0;
+    t.a_kmajor = 0; t.b_kmajor = 0; t.idep = -1; t.osel = 0; t.idep_nmt = 0; t.idep_ntp = 0;
     tasks.push_back(t);
     task_key.push_back(key_base);
     return (int32_t)tasks.size() - 1;
@@ -489,8 +489,30 @@ struct Table {
         alg_flops += 8.0 * t.m * (double)t.n * terms[k].K;
         alg_bytes += 16.0 * t.m * (double)terms[k].K;
       }
-    d_tasks.upload(tasks, st);
-    d_terms.upload(terms, st);
+    // device copies: dependencies as the producer's completion unit, row tiles and
+    // column tiles (the kernels wait without loading the producer's descriptor)
+    std::vector<GTask> dtasks = tasks;
+    std::vector<GTerm> dterms = terms;
+    auto ntp_of = [&](const GTask& P) { return (P.n + NT() - 1) / NT(); };
+    for (GTask& t : dtasks) {
+      t.idep_nmt = t.idep_ntp = 0;
+      if (t.idep >= 0) {
+        const GTask& P = tasks[t.idep];
+        t.idep_nmt = P.n_mt;
+        t.idep_ntp = ntp_of(P);
+        t.idep = P.unit0;
+      }
+    }
+    for (GTerm& g : dterms)
+      if (g.dep >= 0) {
+        const GTask& P = tasks[g.dep];
+        if (P.n_mt >= (1 << 15) || ntp_of(P) >= (1 << 16))
+          throw PsError{PS_ECUDA, "internal: dependency descriptor out of range"};
+        g.bsel = (g.bsel & 1) | (P.n_mt << 1) | (int32_t)((uint32_t)ntp_of(P) << 16);
+        g.dep = P.unit0;
+      }
+    d_tasks.upload(dtasks, st);
+    d_terms.upload(dterms, st);
     d_work.upload(work, st);
     d_counters.alloc(1 + (int64_t)max_units + max_tiles);
     d_partial.alloc(std::max<int64_t>(max_slots, 1) * slot_elems());

@@ -23,9 +23,12 @@ struct GTask {
   int32_t a_kmajor;        // 1: A's unit stride is along k (transposed views), 0: along i
   int32_t b_kmajor;        // 1: B's unit stride is along k, 0: along c
   int32_t idep;            // task (same launch) producing the init rows I; -1: none
+                           // (device copy: that task's first completion unit, see Table::upload)
   int32_t osel;            // bit 0: O offsets address the scratch base S instead of O;
                            // bit 1: I offsets address S instead of I;
                            // bit 2: wide tile on the FP64 tensor-core consumer (per task)
+  int32_t idep_nmt;        // device copy: the init producer's row tiles (its unit is complete at this count)
+  int32_t idep_ntp;        // device copy: the init producer's column tiles (no wait for nt >= this)
 };
 
 // A segment of a task's K dimension: K_s consecutive k's starting at virtual
@@ -36,7 +39,9 @@ struct GTerm {
   int64_t sAi, sAk, sBk, sBc;
   int32_t kstart, K;
   int32_t dep;             // task (same launch) producing this segment's B rows; -1: none
-  int32_t bsel;            // 1: oB addresses the scratch base S instead of B
+                           // (device copy: that task's first completion unit)
+  int32_t bsel;            // bit 0: oB addresses the scratch base S instead of B; device copy adds
+                           // the producer's row tiles (bits 1-15) and column tiles (bits 16-31)
 };
 
 // One CTA-sized piece of work: output tile (mt, nt) of `task`, virtual k in

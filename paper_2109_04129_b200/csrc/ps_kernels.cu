@@ -260,17 +260,6 @@ __device__ __forceinline__ bool splitk_combine(const FlowArgs& a, const GWork& w
   return false;
 }
 
-// Wait (warp 0) until every producer task of this item's B rows (and of its
-// init rows) has completed column tile w.nt. A producer with fewer columns than
-// the consumer (chain setup: T row blocks widen up the chain) has no tile w.nt:
-// the consumer's extra columns read zeros nobody writes, so there is no wait.
-__device__ __forceinline__ void wait_dep_task(const FlowArgs& a, int dep, int nt) {
-  const GTask& P = a.tasks[dep];
-  const int NTw = a.narrow ? GN_NT : GM_NT;
-  if (nt * NTw >= P.n) return;
-  const int32_t* flag = a.counters + 1 + P.unit0 + nt;
-  while (ld_acquire(flag) < P.n_mt) __nanosleep(32);
-}
 // A split tile's partial-sum slots are recycled (Table::assign_slots): the
 // previous user's unit must be complete before this item writes them.
 __device__ __forceinline__ void wait_slot_reuse(const FlowArgs& a, const GWork& w) {
@@ -278,12 +267,25 @@ __device__ __forceinline__ void wait_slot_reuse(const FlowArgs& a, const GWork& 
   const int32_t* flag = a.counters + 1 + w.sw_unit;
   while (ld_acquire(flag) < w.sw_need) __nanosleep(32);
 }
+// Wait (warp 0) until every producer task of this item's B rows (and of its init
+// rows) has completed column tile nt, from the producer's completion unit, row tiles
+// and column tiles precomputed at upload (Table::upload: no load of the producer's
+// descriptor on the item's critical path). A producer with fewer columns than the
+// consumer (chain setup: T row blocks widen up the chain) has no tile nt: the
+// consumer's extra columns read zeros nobody writes, so there is no wait.
+__device__ __forceinline__ void wait_unit(const FlowArgs& a, int unit, int nmt, int ntp, int nt) {
+  if (nt >= ntp) return;
+  const int32_t* flag = a.counters + 1 + unit + nt;
+  while (ld_acquire(flag) < nmt) __nanosleep(32);
+}
+__device__ __forceinline__ void wait_term(const FlowArgs& a, const GTerm& g, int nt) {
+  if (g.dep >= 0) wait_unit(a, g.dep, (g.bsel >> 1) & 0x7fff, (int)((unsigned)g.bsel >> 16), nt);
+}
 __device__ __forceinline__ void wait_deps(const FlowArgs& a, const GWork& w, const GTask& T, int tid) {
-  if (tid == 0 && T.idep >= 0) wait_dep_task(a, T.idep, w.nt);
+  if (tid == 0 && T.idep >= 0) wait_unit(a, T.idep, T.idep_nmt, T.idep_ntp, w.nt);
   if (tid == 1) wait_slot_reuse(a, w);
   for (int t = w.ta + tid; t < w.tb; t += 32) {
-    const int dep = a.terms[t].dep;
-    if (dep >= 0) wait_dep_task(a, dep, w.nt);
+    wait_term(a, a.terms[t], w.nt);
   }
 }
 
@@ -766,7 +768,7 @@ flow_kernel(const FlowArgs a) {
       for (int k = lo; k < hi; ++k) {
         const int64_t d = k - g.kstart;
         kt.kA[k - w.ka] = g.oA + d * g.sAk;
-        kt.kB[k - w.ka] = (g.bsel ? a.S : a.B) + g.oB + d * g.sBk;
+        kt.kB[k - w.ka] = ((g.bsel & 1) ? a.S : a.B) + g.oB + d * g.sBk;
         kt.kSi[k - w.ka] = (int32_t)g.sAi;
         kt.kSc[k - w.ka] = (int32_t)g.sBc;
       }
@@ -1085,7 +1087,7 @@ __device__ void ws_scheduler(const FlowArgs& a, SlotWS* slots, KTabN* kts, int l
     for (int t = 0; t < tb - ta; ++t) {
       const GTerm& g = sl.seg[t];
       const int lo = max(g.kstart, ka), hi = min(g.kstart + g.K, kb);
-      const double2* bb = (g.bsel ? a.S : a.B) + g.oB;
+      const double2* bb = ((g.bsel & 1) ? a.S : a.B) + g.oB;
       for (int k = lo + lane; k < hi; k += 32) {
         const int64_t d = k - g.kstart;
         kt.kA[k - ka] = g.oA + d * g.sAk;
@@ -1096,10 +1098,10 @@ __device__ void ws_scheduler(const FlowArgs& a, SlotWS* slots, KTabN* kts, int l
     }
     // producers (lanes over segments), init producer, split-K group sum
     const int nt = sl.w.nt;
-    if (lane == 0 && sl.T.idep >= 0) wait_dep_task(a, sl.T.idep, nt);
+    if (lane == 0 && sl.T.idep >= 0) wait_unit(a, sl.T.idep, sl.T.idep_nmt, sl.T.idep_ntp, nt);
     if (lane == 1) wait_slot_reuse(a, sl.w);
     for (int t = lane; t < tb - ta; t += 32)
-      if (sl.seg[t].dep >= 0) wait_dep_task(a, sl.seg[t].dep, nt);
+      wait_term(a, sl.seg[t], nt);
     if (lane == 0 && sl.w.nchunks > 1 && sl.w.crit >= 0 && sl.w.chunk == sl.w.crit) {
       const int32_t* ctr = a.counters + 1 + a.n_units + sl.w.tile;
       while (ld_acquire(ctr) < sl.w.nsub + 1) __nanosleep(32);
