@@ -747,10 +747,7 @@ flow_kernel(const FlowArgs a) {
     if (tid == 0) {
       const int it = atomicAdd(ticket, 1);
       s_item = it;
-      if (it < a.nwork) {
-        s_w = a.work[it];
-        s_T = a.tasks[s_w.task];
-      }
+      if (it < a.nwork) s_w = a.work[it];
     }
     __syncthreads();
     const int64_t item = s_item;
@@ -759,8 +756,10 @@ flow_kernel(const FlowArgs a) {
     if (tr) { tr[0] = item; tr[1] = smid(); tr[2] = gtimer(); }
     const GWork& w = s_w;       // shared: one copy per CTA, not per-thread registers
     const GTask& T = s_T;
-    const int mm = min(GM_MT, T.m - w.mt * GM_MT);
-    const int RM = a.narrow ? 0 : (mm + GM_WM - 1) / GM_WM;
+    // the task descriptor is loaded by the last warp while the others load the segments
+    if (tid >= 256 - 32 && tid - (256 - 32) < (int)(sizeof(GTask) / 4))
+      reinterpret_cast<int32_t*>(&s_T)[tid - (256 - 32)] =
+          __ldg(reinterpret_cast<const int32_t*>(a.tasks + w.task) + (tid - (256 - 32)));
     // ---- k tables of this item (segments [ta, tb) clipped to [ka, kb)) ----
     for (int t = w.ta + tid; t < w.tb; t += 256) {
       const GTerm g = a.terms[t];
@@ -774,6 +773,8 @@ flow_kernel(const FlowArgs a) {
       }
     }
     __syncthreads();
+    const int mm = min(GM_MT, T.m - w.mt * GM_MT);
+    const int RM = a.narrow ? 0 : (mm + GM_WM - 1) / GM_WM;
     if (!a.narrow && (a.mma || (T.osel & 4))) {
       switch ((mm + 7) / 8) {
         case 1: item_body_dmma<1>(a, w, T, kt, As0, Bs0, tid, lane, warp, &s_last, tr); break;
@@ -1072,14 +1073,23 @@ __device__ void ws_scheduler(const FlowArgs& a, SlotWS* slots, KTabN* kts, int l
     __syncwarp();
     const int ta = sl.w.ta, tb = sl.w.tb, ka = sl.w.ka, kb = sl.w.kb;
     {
+      // task descriptor and segment list (<= GM_MAXSEG): all lanes' loads of the task and
+      // of the first 4 x 32 segment words are issued before any store (one round trip)
+      static_assert(sizeof(GTask) / 4 <= 32, "one task word per lane");
       const int32_t* src = reinterpret_cast<const int32_t*>(a.tasks + sl.w.task);
-      int32_t* dst = reinterpret_cast<int32_t*>(&sl.T);
-      for (int q = lane; q < (int)(sizeof(GTask) / 4); q += 32) dst[q] = src[q];
-      // segment list (<= GM_MAXSEG), lanes in parallel
       const int32_t* ts = reinterpret_cast<const int32_t*>(a.terms + ta);
-      int32_t* td = reinterpret_cast<int32_t*>(sl.seg);
       const int n4 = (tb - ta) * (int)(sizeof(GTerm) / 4);
-      for (int q = lane; q < n4; q += 32) td[q] = ts[q];
+      int32_t tw = 0, r[4];
+      if (lane < (int)(sizeof(GTask) / 4)) tw = __ldg(src + lane);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) r[i] = (lane + 32 * i < n4) ? __ldg(ts + lane + 32 * i) : 0;
+      int32_t* dst = reinterpret_cast<int32_t*>(&sl.T);
+      int32_t* td = reinterpret_cast<int32_t*>(sl.seg);
+      if (lane < (int)(sizeof(GTask) / 4)) dst[lane] = tw;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (lane + 32 * i < n4) td[lane + 32 * i] = r[i];
+      for (int q = lane + 128; q < n4; q += 32) td[q] = ts[q];
     }
     if (lane == 0) sl.item = it;
     __syncwarp();
