@@ -160,8 +160,8 @@ def run_reference(args):
     vals = []
     det = None
     for s in range(args.warmup + args.steps):
-        v, det = cpu_oracle_arm(meta, B, seconds=max(2.0, min(20.0, 60.0 / max(1, args.steps))),
-                                max_cols=min(nrhs, 16))
+        secs = args.ref_seconds or max(2.0, min(20.0, 60.0 / max(1, args.steps)))
+        v, det = cpu_oracle_arm(meta, B, seconds=secs, max_cols=min(nrhs, 16))
         if s >= args.warmup:
             vals.append(v)
     v = float(np.median(vals))
@@ -229,6 +229,8 @@ def main():
     ap.add_argument("--rhs-split", default="weak", choices=["weak", "strong"],
                     help="cols mode: weak = every rank solves the config's full RHS block; strong = the "
                          "block is split")
+    ap.add_argument("--ref-seconds", type=float, default=0.0,
+                    help="--impl reference: seconds of oracle work per step (default: 60 s / steps, 2..20 s)")
     ap.add_argument("--flush-l2", default="auto", choices=["auto", "on", "off"],
                     help="write a 256 MB buffer before every timed step (auto: when the operator is "
                          "smaller than 2 x L2, e.g. C1)")
