@@ -326,6 +326,11 @@ struct Table {
   void tile(int32_t task, int isolate = 0, int steps = 0) {
     if (steps <= 0) steps = chunk_steps;
     GTask& t = tasks[task];
+    // narrow items of short tasks (<= 32 rows: 16/32-row tiles stream 64/32 k per stage) take
+    // twice the k per chunk in stages big enough to hit the chunk cap, so an item streams as
+    // many operator bytes as a 64-row one (C4-1 -5 %; in small stages it would cost parallelism)
+    static const int short_x2 = env_int("PS_NARROW_SHORT_X2", 1);
+    if (narrow && short_x2 && t.m <= 32 && steps >= NARROW_STEPS()) steps *= 2;   // only where the stage is capped
     // consumer per task: tall tasks (>= 32 rows: full 32-row tiles, little 8-row
     // padding) on the FP64 tensor cores, short ones (single 16-19 row leaves) on DFMA
     static const int auto_mma = env_int("PS_AUTO_MMA", 1), mma_rows = env_int("PS_MMA_MINROWS", 32);

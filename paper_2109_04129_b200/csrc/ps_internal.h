@@ -102,7 +102,7 @@ constexpr int GM_KC = 16;
 constexpr int GN_MT = 64;
 constexpr int GN_NT = 8;
 constexpr int GM_CHUNK_K = 512;   // max virtual k per work item (shared-memory k tables)
-constexpr int GN_CHUNK_K = 256;   // same for narrow tiles (warp-specialised kernel, two tables)
+constexpr int GN_CHUNK_K = 512;   // same for narrow tiles (warp-specialised kernel, two tables)
 constexpr int GM_MAXSEG = 96;     // max segments per work item
 
 // ---- kernel launchers (ps_kernels.cu) ----
