@@ -7,11 +7,16 @@ backward sweep R, far field Z_F, forward sweep + D^-1, combine + norms,
 backward sweep), device-resident B and X. The O(N) setup (rows a1-a3) is run
 once before the timed region and reported separately as `setup_ms`.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
 
-Multi-GPU (torchrun, one process per GPU): RHS columns are independent, so
-every rank solves its own block of the monostatic sweep against a replicated
-operator — no data-path collective; `scaling: weak`. Time = max over ranks.
+Default workload: C4 (BASELINE configs[3], the largest config that fits one GPU's
+measurement budget: cylinder, N = 96000, 360 RHS), plus the same handle at nrhs = 1
+in the line's "nrhs1" object (the HBM-bound half of the metric).
+
+Multi-GPU (torchrun, one process per GPU): with >= 16 columns per rank the config's
+RHS block is split into distinct column blocks (replicated operator, no data-path
+collective; `scaling: strong`); with fewer (nrhs = 1) the operator is row-partitioned
+over the ranks with NCCL exchanges. Time = max over ranks.
 
 --impl reference runs the CPU oracle (oracle/, numpy complex128) on the host
 cores as the reference arm (rank 0 only).
@@ -120,14 +125,36 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+_ORACLE_CACHE = {}
+
+
+def _oracle_state(meta):
+    """(H, S) of the oracle for this config, computed once per process (the reference
+    arm's steps time the solve on the cached scaling)."""
+    from oracle import compute_scaling, read_hm
+    key = meta["hm"]
+    if key not in _ORACLE_CACHE:
+        H = read_hm(meta["hm"])
+        t0 = time.perf_counter()
+        S = compute_scaling(H)
+        _ORACLE_CACHE[key] = (H, S, time.perf_counter() - t0)
+    return _ORACLE_CACHE[key]
+
+
+def _cores():
+    try:
+        from threadpoolctl import threadpool_info
+        return int(max([d.get("num_threads", 1) for d in threadpool_info()] + [1]))
+    except Exception:
+        return os.cpu_count()
+
+
 def cpu_oracle_arm(meta, B, seconds=12.0, max_cols=16):
-    """The oracle (as it stands) on a bounded sample: first `max_cols` RHS columns,
-    repeated solves until ~`seconds` of CPU work. Returns (N*nrhs/s, details)."""
-    from oracle import compute_scaling, read_hm, solve
-    H = read_hm(meta["hm"])
-    t0 = time.perf_counter()
-    S = compute_scaling(H)
-    t_setup = time.perf_counter() - t0
+    """The oracle (as it stands) on a bounded sample: the first `max_cols` RHS columns,
+    solved repeatedly until ~`seconds` of CPU work (the oracle's scaling, computed once
+    per process, is excluded). Returns (N*nrhs/s, details)."""
+    from oracle import solve
+    H, S, t_setup = _oracle_state(meta)
     cols = B[:, :max_cols]
     n_done = 0
     t0 = time.perf_counter()
@@ -137,15 +164,11 @@ def cpu_oracle_arm(meta, B, seconds=12.0, max_cols=16):
         el = time.perf_counter() - t0
         if el >= seconds:
             break
-    try:
-        from threadpoolctl import threadpool_info
-        cores = max([d.get("num_threads", 1) for d in threadpool_info()] + [1])
-    except Exception:
-        cores = os.cpu_count()
     v = H.N * n_done / el
-    return v, dict(cores=int(cores), t_setup_s=t_setup, solved_cols=n_done, seconds=el,
-                   sample=f"{cols.shape[1]} RHS columns of the same block, solved repeatedly for "
-                          f"{el:.1f} s (oracle setup {t_setup:.1f} s excluded)")
+    return v, dict(cores=_cores(), t_setup_s=t_setup, solved_cols=n_done, seconds=el,
+                   sample=f"the first {cols.shape[1]} of the workload's {B.shape[1]} RHS columns, solved "
+                          f"repeatedly for {el:.1f} s (oracle scaling, {t_setup:.1f} s once per process, "
+                          f"excluded)")
 
 
 def run_reference(args):
@@ -156,6 +179,8 @@ def run_reference(args):
     meta = load_or_generate(args.config)
     B, _ = read_rhs(meta["rhs"])
     nrhs = args.nrhs or B.shape[1]
+    if nrhs > B.shape[1]:
+        B = np.tile(B, (1, -(-nrhs // B.shape[1])))
     B = np.asfortranarray(B[:, :nrhs])
     vals = []
     det = None
@@ -167,9 +192,9 @@ def run_reference(args):
     v = float(np.median(vals))
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * meta["N"] * nrhs / v, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": 1e3 * meta["N"] * nrhs / v, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-            "config": _config(args, meta, nrhs, args.gpus),
+            "config": _config(args, meta, nrhs, 1),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": det["cores"], "kind": "oracle",
                              "sample": det["sample"]},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -178,36 +203,43 @@ def run_reference(args):
 
 
 def _ncu_traffic(config, nrhs):
-    """Mean DRAM bytes (read + write) per flow_kernel launch of one solve, from the
-    committed ncu --set full summary of this config (profiles/*/ncu_full_<cfg>_<nrhs>_*.json,
-    written by scripts/ncu_summary.py), or (None, None)."""
+    """Mean DRAM bytes (read + write) per flow_kernel launch of one solve, from the committed
+    ncu --set full summary of this config (profiles/*/ncu_full_<cfg>_<nrhs>_*.json, written by
+    scripts/ncu_summary.py) — only when it was captured on the build this run uses (same libps
+    source hash); else (None, reason)."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", f"ncu_full_{config}_{nrhs}_*.json")))
-    if not files:
-        return None, None
-    try:
-        with open(files[-1]) as f:
-            rows = json.load(f)
+    from paper_2109_04129_b200.build import source_hash
+    cur = source_hash()
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", f"ncu_full_{config}_{nrhs}_*.json")),
+                   key=os.path.getmtime)
+    for fn in reversed(files):
+        try:
+            with open(fn) as f:
+                d = json.load(f)
+        except Exception:
+            continue
+        if not isinstance(d, dict) or d.get("src_hash") != cur:
+            continue
 
         def mb(v):
             x, u = v.split()
             return float(x) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
-        vals = [mb(r["dram__bytes_read.sum"]) + mb(r["dram__bytes_write.sum"]) for r in rows
+        vals = [mb(r["dram__bytes_read.sum"]) + mb(r["dram__bytes_write.sum"]) for r in d["rows"]
                 if "flow_kernel" in r.get("Kernel Name", "")]
-        return (sum(vals) / len(vals) if vals else None), os.path.relpath(files[-1], ROOT)
-    except Exception:
-        return None, None
+        if vals:
+            return sum(vals) / len(vals), os.path.relpath(fn, ROOT)
+    return None, f"no committed ncu --set full capture of {config}-{nrhs} on this build (libps {cur})"
 
 
 def _config(args, meta, nrhs, world):
     rows = getattr(args, "mode", "cols") == "rows" and world > 1
-    return {"workload": f"{args.config}: {meta['desc']}", "N": meta["N"],
-            "nrhs_per_gpu": nrhs, "global_nrhs": nrhs if rows else (
-                nrhs * world if args.rhs_split == "weak" else args.nrhs or nrhs * world),
+    return {"workload": f"{args.config}-{nrhs}: {meta['desc']}", "N": meta["N"],
+            "nrhs_per_gpu": nrhs, "global_nrhs": getattr(args, "nrhs_global", nrhs),
             "n_leaves": meta["n_leaves"],
             "parallelism": (f"row partition x{world} (elimination-tree subtrees per rank, replicated "
                             f"separators; NCCL all-reduce of separator rows, all-gather of w and x)"
-                            if rows else f"rhs-columns x{world} (replicated operator)"),
+                            if rows else f"rhs-columns x{world} (replicated operator, distinct columns per "
+                                         f"rank, no data-path collective)"),
             "l2": ("host oracle (no GPU L2)" if not hasattr(args, "op_mb") else
                    f"operator {getattr(args, 'op_mb', 0):.0f} MB < 2 x the 126 MB L2: a 256 MB buffer is "
                    "written before every timed step (per-step CUDA events exclude it)"
@@ -216,28 +248,105 @@ def _config(args, meta, nrhs, world):
                    "exceeds the 126 MB L2; no flush")}
 
 
+FP64_PEAK = 37.02   # TF/s: measured on this pool's B200 (scripts/fp64_peak.cu, profiles/r1/fp64_peak_b200.json)
+
+
+def _time_solves(h, Bd, Xd, st, steps, flush_buf, dist, world):
+    """Device ms per solve over `steps` timed solves (CUDA events on the solve stream)."""
+    import torch
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    if flush_buf is not None:                  # per-step events, L2 written between steps
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for a_, b_ in evs:
+            flush_buf.fill_(1)
+            a_.record(st)
+            h.solve(Bd, Xd, stream=st, want_norms=False)
+            b_.record(st)
+        torch.cuda.synchronize()
+        ms = sum(a_.elapsed_time(b_) for a_, b_ in evs) / steps
+    else:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(steps):
+            h.solve(Bd, Xd, stream=st, want_norms=False)
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+    if world > 1:
+        dist.barrier()
+    return ms
+
+
+def _roofline(h, Bd, Xd, st, nrhs, args, info, rep):
+    """Roofline object of the dominant kernel (the one dataflow-program launch per solve):
+    SURVEY §8(d)'s algorithmic work of one solve (rep: 8 nrhs (4 n_R + 2 n_D + 2 n_F) flop;
+    16 (4 n_R + 2 n_D + n_F) + 16 * 12 N nrhs bytes) / that kernel's mean launch time, timed
+    with CUDA events on the launching stream (ps_profile)."""
+    steps = max(1, args.profile_steps)
+    h.profile(True)
+    for _ in range(steps):
+        h.solve(Bd, Xd, stream=st, want_norms=False)
+    prof = h.profile_read()
+    h.profile(False)
+    k_ms = prof["solve_program"]["ms"] / max(1, prof["solve_program"]["launches"])
+    tot_ms = sum(prof[c]["ms"] for c in prof) / steps
+    exe_fl = prof["solve_program"]["flops"] / steps
+    exe_by = prof["solve_program"]["bytes"] / steps
+    peaks = _peaks()
+    hbm_peak = float(peaks.get("hbm_gbs", 6548.2))
+    alg_fl, alg_by = rep["flops"], rep["bytes"]
+    traffic, traffic_src = _ncu_traffic(args.config, nrhs)
+    if nrhs <= 8:
+        gbs = alg_by / (k_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, burst)"}
+    else:
+        tf = alg_fl / (k_ms * 1e-3) / 1e12
+        roof = {"bound": "alu", "achieved": tf, "peak": FP64_PEAK, "unit": "TFLOP/s", "frac": tf / FP64_PEAK,
+                "peak_source": ("FP64 (DFMA and mma.sync f64 share one pipe budget; tcgen05 has no f64 kind): "
+                                "measured 37.02 TF on this pool's B200 (profiles/r1/fp64_peak_b200.json) = "
+                                "148 SM x 64 FP64 FMA/clk x 2 flop x 1.965 GHz (37.2 TF derived); "
+                                "MEASURED_PEAKS.json has no FP64 entry")}
+    roof.update({
+        "traffic": traffic, "traffic_source": traffic_src,
+        "algorithmic_per_launch": {"flop": alg_fl, "bytes": alg_by,
+                                   "formula": "SURVEY 8(d): flop = 8 nrhs (4 n_R + 2 n_D + 2 n_F); bytes = "
+                                              "16 (4 n_R + 2 n_D + n_F) + 16 x 12 N nrhs"},
+        "executed_per_launch": {"flop": exe_fl, "bytes": exe_by,
+                                "note": "products the kernel's task tables execute: chain-internal alpha "
+                                        "blocks replaced by the T_c products (DESIGN.md R23), operator "
+                                        "bytes only"},
+        "executed_over_algorithmic_operator_bytes": exe_by / (16.0 * (4 * info["nR"] + 2 * info["nD"] + info["nF"])),
+        "kernel": "ps::flow_kernel / flow_kernel_ws (persistent dataflow gather-GEMM: the whole two-term "
+                  "solve as one launch)",
+        "kernel_ms_per_launch": k_ms,
+        "kernel_share_of_step": prof["solve_program"]["ms"] / steps / tot_ms if tot_ms > 0 else None})
+    return roof
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2")
-    ap.add_argument("--nrhs", type=int, default=0)
+    ap.add_argument("--config", default="C4",
+                    help="BASELINE config (default C4: the largest single-GPU config, 360 RHS)")
+    ap.add_argument("--nrhs", type=int, default=0, help="RHS columns (default: the config's full table)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-nrhs1", action="store_true", help="skip the embedded nrhs = 1 (HBM-bound) measurement")
     ap.add_argument("--profile-steps", type=int, default=2)
-    ap.add_argument("--rhs-split", default="weak", choices=["weak", "strong"],
-                    help="cols mode: weak = every rank solves the config's full RHS block; strong = the "
-                         "block is split")
     ap.add_argument("--ref-seconds", type=float, default=0.0,
                     help="--impl reference: seconds of oracle work per step (default: 60 s / steps, 2..20 s)")
     ap.add_argument("--flush-l2", default="auto", choices=["auto", "on", "off"],
                     help="write a 256 MB buffer before every timed step (auto: when the operator is "
                          "smaller than 2 x L2, e.g. C1)")
     ap.add_argument("--partition", default="auto", choices=["auto", "cols", "rows"],
-                    help="N > 1: cols = replicated operator, RHS columns per rank (no collective); rows = "
-                         "row partition of the operator over the ranks (NCCL exchanges, every rank solves "
-                         "the whole block: strong scaling); auto = cols when nrhs >= 16 N, else rows")
+                    help="N > 1: cols = replicated operator, the config's RHS block split into distinct "
+                         "column blocks per rank (no collective); rows = row partition of the operator (NCCL "
+                         "exchanges, every rank works on the whole block); auto = cols when nrhs >= 16 N, else rows")
     args = ap.parse_args()
     warnings.simplefilter("ignore", RuntimeWarning)
     if args.impl == "reference":
@@ -269,11 +378,11 @@ def main():
     if mode == "auto":
         mode = "cols" if (world == 1 or nrhs_global >= 16 * world) else "rows"
     args.mode = mode
+    args.nrhs_global = nrhs_global
     if mode == "rows":
-        args.rhs_split = "strong"
         B = np.asfortranarray(Bfull[:, :nrhs_global])
-    else:
-        B = np.asfortranarray(Bfull[:, :nrhs_global][:, column_slice(nrhs_global, world, rank, args.rhs_split)])
+    else:                                   # distinct columns per rank (strong split of the block)
+        B = np.asfortranarray(Bfull[:, :nrhs_global][:, column_slice(nrhs_global, world, rank, "strong")])
     nrhs = B.shape[1]
     N = meta["N"]
 
@@ -285,7 +394,6 @@ def main():
     else:
         h = PsHandle(meta["hm"], device=local, rank=rank, nranks=world)
     st = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     h.setup()
@@ -303,31 +411,12 @@ def main():
     for _ in range(args.warmup):
         _, rep = h.solve(Bd, Xd, stream=st)
     with ClockSampler(local) as clk:
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
         clk.mark()
-        if args.flush:                        # per-step events, L2 written between steps
-            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                   for _ in range(args.steps)]
-            for a_, b_ in evs:
-                flush_buf.fill_(1)
-                a_.record(st)
-                _, rep = h.solve(Bd, Xd, stream=st, want_norms=False)
-                b_.record(st)
-        else:
-            e0.record(st)
-            for _ in range(args.steps):
-                _, rep = h.solve(Bd, Xd, stream=st, want_norms=False)
-            e1.record(st)
-        torch.cuda.synchronize()
+        step_ms = _time_solves(h, Bd, Xd, st, args.steps, flush_buf, dist, world)
         clk.stop()
-        if world > 1:
-            dist.barrier()
-    step_ms = (sum(a_.elapsed_time(b_) for a_, b_ in evs) if args.flush else e0.elapsed_time(e1)) / args.steps
     ms = max_over_ranks(step_ms, dist, "cuda")
-    launches = int(rep["launches"])
     _, rep = h.solve(Bd, Xd, stream=st)
+    launches = int(rep["launches"])
     ratio = rep["ratio"]
 
     # ---- end to end: host (pinned) buffers through the C ABI, copies inside ----
@@ -335,83 +424,48 @@ def main():
     Xh = torch.empty((nrhs, N), dtype=torch.complex128).pin_memory().T
     for _ in range(max(1, args.warmup)):
         h.solve(Bh, Xh, stream=st, want_norms=False)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    e0.record(st)
-    for _ in range(args.steps):
-        h.solve(Bh, Xh, stream=st, want_norms=False)
-    e1.record(st)
-    torch.cuda.synchronize()
-    ms_e2e = max_over_ranks(e0.elapsed_time(e1) / args.steps, dist, "cuda")
+    ms_e2e = max_over_ranks(_time_solves(h, Bh, Xh, st, args.steps, None, dist, world), dist, "cuda")
 
-    # ---- roofline of the dominant kernel (gather-GEMM), per-launch events ----
-    args.profile_steps = max(1, args.profile_steps)
-    h.profile(True)
-    for _ in range(args.profile_steps):
-        h.solve(Bd, Xd, stream=st, want_norms=False)
-    prof = h.profile_read()
-    h.profile(False)
-    g_ms = sum(prof[c]["ms"] for c in prof if c != "aux")
-    g_fl = sum(prof[c]["flops"] for c in prof if c != "aux")
-    g_by = sum(prof[c]["bytes"] for c in prof if c != "aux")
-    tot_ms = g_ms + prof["aux"]["ms"]
-    peaks = _peaks()
-    clocks = clk.summary()
-    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    # measured FP64 ceiling on this pool's B200 (scripts/fp64_peak.cu, profiles/r1/fp64_peak_b200.json):
-    # mma.sync f64 37.0 TF, DFMA loop 34.0 TF; derived 148 SM x 64 FMA/clk x 2 x 1965 MHz = 37.2 TF
-    fp64_peak = 37.02
-    achieved = g_fl / (g_ms * 1e-3) / 1e12 if g_ms > 0 else 0.0
-    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    launches_k = sum(prof[c]["launches"] for c in prof if c != "aux") / max(1, args.profile_steps)
-    traffic, traffic_src = _ncu_traffic(args.config, nrhs)
-    if nrhs <= 8:
-        # operator streaming (0.5 flop/B at nrhs = 1): HBM-bound; achieved = the operator
-        # bytes the launches must read (alpha panels, T_c, D^-1, far factors) / their time
-        gbs = g_by / (g_ms * 1e-3) / 1e9 if g_ms > 0 else 0.0
-        roof = {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak}
-    else:
-        roof = {"bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
-                "frac": achieved / fp64_peak}
-    roof.update({"traffic": traffic, "traffic_source": traffic_src,
-                 "algorithmic_per_launch": {"flop": g_fl / max(1, args.profile_steps) / max(1.0, launches_k),
-                                            "bytes": g_by / max(1, args.profile_steps) / max(1.0, launches_k)},
-            "kernel": "flow_kernel (persistent gather-GEMM: all sweep / D^-1 / far-field launches)",
-            "kernel_share_of_step": g_ms / tot_ms if tot_ms > 0 else None,
-            "peak_source": ("MEASURED_PEAKS.json hbm_gbs (copy bandwidth, burst)" if nrhs <= 8 else
-                            "measured FP64 ceiling on this pool's B200 (mma.sync f64 37.0 TF, DFMA loop "
-                            "34.0 TF; profiles/r1/fp64_peak_b200.json) = derived 148 SM x 64 FMA/clk x 2 x "
-                            "1.965 GHz; FP64 has no tcgen05 kind"),
-            "kernel_name_in_ncu": "ps::flow_kernel",
-            "hbm_view": {"operator_bytes_per_step": g_by / max(1, args.profile_steps),
-                         "achieved_GBs": g_by / (g_ms * 1e-3) / 1e9 if g_ms > 0 else 0.0,
-                         "peak_GBs": hbm_peak},
-            "per_class": {c: {"ms_per_step": prof[c]["ms"] / args.profile_steps,
-                              "launches_per_step": prof[c]["launches"] / args.profile_steps,
-                              "gflop_per_step": prof[c]["flops"] / args.profile_steps / 1e9}
-                          for c in prof}})
-
-    total_cols = nrhs * world if (mode == "cols" and args.rhs_split == "weak") else nrhs_global
+    roof = _roofline(h, Bd, Xd, st, nrhs, args, info, rep)
+    total_cols = nrhs_global
     value = N * total_cols / (ms * 1e-3)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": args.rhs_split,
+            "scaling": "strong",
             "vs_baseline": None, "dtype": "c128",
             "data": "synthetic (seeded EFIE H-matrix from hmgen; plane-wave RHS)",
             "config": _config(args, meta, nrhs, world),
             "setup_ms": setup_ms,
-            "structure": {k: info[k] for k in ("n_leaves", "alpha_blocks", "nR", "nD", "nF", "height", "depth")},
+            "setup_tflops": 8.0 * info["setup_madds"] / (setup_ms * 1e-3) / 1e12,
+            "structure": {k: info[k] for k in ("n_leaves", "alpha_blocks", "nR", "nD", "nF", "height", "depth",
+                                               "T_entries")},
             "series": {"ratio_min": float(ratio.min()), "ratio_max": float(ratio.max()),
                        "n_diverged": int(rep["n_diverged"]),
-                       "note": "ratio >= 0.1 flags divergence (Eq. 45); BASELINE configs use 0.25-lambda "
-                               "leaves, below the paper's 0.5-lambda accuracy threshold (DESIGN.md R14)"},
+                       "note": "ratio = ||it_1||/||it_0|| from the C ABI (Eq. 45); >= 0.1 flags divergence. "
+                               "BASELINE configs use 0.25-lambda leaves, below the paper's 0.5-lambda accuracy "
+                               "threshold (DESIGN.md R14)"},
             "roofline": roof,
             "e2e": {"value": N * total_cols / (ms_e2e * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": 16 * N * nrhs, "d2h_bytes_per_step": 16 * N * nrhs,
                     "ms_per_step": ms_e2e},
             "gpu_launches": launches * args.steps,
-            "clocks": clocks}
+            "clocks": clk.summary()}
+
+    # ---- nrhs = 1 (operator streaming, HBM-bound) on the same handle: the metric's other half ----
+    if nrhs > 1 and not args.no_nrhs1 and mode == "cols":
+        B1 = Bd[:, :1].contiguous()
+        X1 = torch.empty_like(B1)
+        for _ in range(args.warmup):
+            _, rep1 = h.solve(B1, X1, stream=st)
+        with ClockSampler(local) as clk1:
+            clk1.mark()
+            ms1 = max_over_ranks(_time_solves(h, B1, X1, st, args.steps, flush_buf, dist, world), dist, "cuda")
+            clk1.stop()
+        _, rep1 = h.solve(B1, X1, stream=st)
+        roof1 = _roofline(h, B1, X1, st, 1, args, info, rep1)
+        line["nrhs1"] = {"workload": f"{args.config}-1 (first column of the same block)",
+                         "value": N * world / (ms1 * 1e-3), "unit": UNIT, "ms_per_step": ms1,
+                         "roofline": roof1, "clocks": clk1.summary()}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, det = cpu_oracle_arm(meta, B)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": det["cores"], "kind": "oracle",

@@ -197,34 +197,57 @@ def cube_mesh(side: float, div: int) -> Mesh:
 
 
 def cylinder_mesh(radius: float, length: float, h: float) -> Mesh:
-    """Closed circular cylinder (axis z) with flat caps; target edge h."""
+    """Closed circular cylinder (axis z) with flat caps, near-equilateral triangles of
+    edge ~h: the lateral rings are staggered by half a step (ring spacing h*sqrt(3)/2),
+    each cap is concentric rings of spacing h*sqrt(3)/2 and circumferential step ~h,
+    zipped ring to ring and fanned to the centre."""
     nphi = max(6, int(round(2 * math.pi * radius / h)))
-    nz = max(1, int(round(length / h)))
-    nr = max(1, int(round(radius / h)))
+    nz = max(1, int(round(length / (h * math.sqrt(3) / 2))))
+    nr = max(1, int(round(radius / (h * math.sqrt(3) / 2))))
     pts = []
-    phis = 2 * math.pi * np.arange(nphi) / nphi
     lat = np.zeros((nz + 1, nphi), dtype=np.int64)
+    ring_ang = []
     for iz in range(nz + 1):
         z = -length / 2 + length * iz / nz
+        a = 2 * math.pi * (np.arange(nphi) + 0.5 * (iz % 2)) / nphi
+        ring_ang.append(a)
         for ip in range(nphi):
             lat[iz, ip] = len(pts)
-            pts.append((radius * math.cos(phis[ip]), radius * math.sin(phis[ip]), z))
+            pts.append((radius * math.cos(a[ip]), radius * math.sin(a[ip]), z))
     tris = []
-    for iz in range(nz):
-        for ip in range(nphi):
-            a, b = lat[iz, ip], lat[iz, (ip + 1) % nphi]
-            c, d = lat[iz + 1, (ip + 1) % nphi], lat[iz + 1, ip]
-            tris.append([a, b, c])
-            tris.append([a, c, d])
 
-    def cap(rim_ids, z, outward_up):
+    def zipper(A, aa, B, bb, out):
+        """Triangulate the band between two closed rings (ids A, B; angles aa, bb)."""
+        oa, ob = np.argsort(aa % (2 * math.pi)), np.argsort(bb % (2 * math.pi))
+        A, aa = A[oa], aa[oa] % (2 * math.pi)
+        B, bb = B[ob], bb[ob] % (2 * math.pi)
+        # start both rings at the point closest to angle 0 (deterministic)
+        ia = ib = 0
+        na, nb = len(A), len(B)
+        while ia < na or ib < nb:
+            a0, a1 = A[ia % na], A[(ia + 1) % na]
+            b0, b1 = B[ib % nb], B[(ib + 1) % nb]
+            ta = aa[(ia + 1) % na] + (2 * math.pi if ia + 1 >= na else 0)
+            tb = bb[(ib + 1) % nb] + (2 * math.pi if ib + 1 >= nb else 0)
+            if ib >= nb or (ia < na and ta <= tb):
+                out.append([a0, a1, b0])
+                ia += 1
+            else:
+                out.append([a0, b1, b0])
+                ib += 1
+
+    for iz in range(nz):
+        band = []
+        zipper(lat[iz], ring_ang[iz], lat[iz + 1], ring_ang[iz + 1], band)
+        tris.extend(band)
+
+    def cap(rim_ids, rim_ang, z, outward_up):
         rings = [rim_ids]
-        angs = [phis.copy()]
+        angs = [rim_ang]
         for ir in range(nr - 1, 0, -1):
             rr = radius * ir / nr
-            n = max(6, int(round(nphi * ir / nr)))
-            off = 0.5 * (2 * math.pi / n) * (ir % 2)
-            a = off + 2 * math.pi * np.arange(n) / n
+            n = max(6, int(round(2 * math.pi * rr / h)))
+            a = 2 * math.pi * (np.arange(n) + 0.5 * ((nr - ir) % 2)) / n
             ids = []
             for t in a:
                 ids.append(len(pts))
@@ -235,27 +258,10 @@ def cylinder_mesh(radius: float, length: float, h: float) -> Mesh:
         pts.append((0.0, 0.0, z))
         out = []
         for k in range(len(rings) - 1):
-            A, aa = rings[k], angs[k] % (2 * math.pi)
-            B, bb = rings[k + 1], angs[k + 1] % (2 * math.pi)
-            # zipper triangulation between two concentric rings
-            ia = ib = 0
-            na, nb = len(A), len(B)
-            oa = np.argsort(aa)
-            ob = np.argsort(bb)
-            A, aa = A[oa], aa[oa]
-            B, bb = B[ob], bb[ob]
-            while ia < na or ib < nb:
-                a0, a1 = A[ia % na], A[(ia + 1) % na]
-                b0, b1 = B[ib % nb], B[(ib + 1) % nb]
-                ta = aa[(ia + 1) % na] + (2 * math.pi if ia + 1 >= na else 0)
-                tb = bb[(ib + 1) % nb] + (2 * math.pi if ib + 1 >= nb else 0)
-                if ib >= nb or (ia < na and ta <= tb):
-                    out.append([a0, a1, b0])
-                    ia += 1
-                else:
-                    out.append([a0, b1, b0])
-                    ib += 1
+            zipper(rings[k], angs[k], rings[k + 1], angs[k + 1], out)
         last = rings[-1]
+        order = np.argsort(angs[-1] % (2 * math.pi))
+        last = last[order]
         for i in range(len(last)):
             out.append([last[i], last[(i + 1) % len(last)], center])
         for t in out:
@@ -263,9 +269,27 @@ def cylinder_mesh(radius: float, length: float, h: float) -> Mesh:
                 t = [t[0], t[2], t[1]]
             tris.append(t)
 
-    cap(lat[0], -length / 2, False)
-    cap(lat[nz], length / 2, True)
+    cap(lat[0], ring_ang[0], -length / 2, False)
+    cap(lat[nz], ring_ang[nz], length / 2, True)
     return Mesh(np.array(pts, dtype=np.float64), np.array(tris, dtype=np.int64))
+
+
+def mean_edge(mesh: Mesh) -> float:
+    """Mean length over all (unique) mesh edges."""
+    e = np.concatenate([mesh.tris[:, [0, 1]], mesh.tris[:, [1, 2]], mesh.tris[:, [2, 0]]])
+    e = np.unique(np.sort(e, axis=1), axis=0)
+    return float(np.linalg.norm(mesh.nodes[e[:, 0]] - mesh.nodes[e[:, 1]], axis=1).mean())
+
+
+def cylinder_mesh_mean_edge(radius: float, length: float, target: float) -> Mesh:
+    """cylinder_mesh whose MEASURED mean edge (over all edges) is `target` to within
+    ~1 %: two fixed-point rescalings of the lattice step (deterministic)."""
+    h = target
+    m = cylinder_mesh(radius, length, h)
+    for _ in range(2):
+        h *= target / mean_edge(m)
+        m = cylinder_mesh(radius, length, h)
+    return m
 
 
 @dataclass
@@ -477,7 +501,7 @@ def make_mesh(cfg: Config) -> Mesh:
     if cfg.kind == "cube":
         return cube_mesh(cfg.params["side"], cfg.params["div"])
     if cfg.kind == "cylinder":
-        return cylinder_mesh(cfg.params["radius"], cfg.params["length"], cfg.lam / 10)
+        return cylinder_mesh_mean_edge(cfg.params["radius"], cfg.params["length"], cfg.lam / 10)
     raise ValueError(cfg.kind)
 
 

@@ -113,6 +113,8 @@ typedef struct {
   double bytes_moved;       /* out: algorithmic operator + vector bytes of this solve */
   double flops;             /* out: algorithmic flops of this solve */
   int64_t kernel_launches;  /* out: libps kernels launched by this call */
+  double* ratio;            /* out [nrhs] or NULL: ||it_1|| / ||it_0|| per column (Eq. 45 LHS; 0 when
+                               ||it_0|| = 0); the quantity compared with ratio_threshold */
 } ps_report;
 
 /* hm_load — read and verify an ".hm" file (layout above), copy the near and far
@@ -252,8 +254,10 @@ int64_t ps_trace_read(ps_handle* h, int64_t* out, int64_t cap_items);
 
 /* ps_get_dinv — copy D_k^{-1} of the leaf at elimination position `pos`
  * (n_k x n_k column-major, in the leaf's Morton-local unknown order) to host
- * memory `out` (capacity n_k^2 complex). Returns n_k, or -1 on error. */
-int64_t ps_get_dinv(ps_handle* h, int64_t pos, void* out);
+ * memory `out` of capacity `cap` complex entries. Returns n_k on success;
+ * -(n_k^2) without copying when cap < n_k^2 (call again with that capacity);
+ * 0 on error (bad handle / position, no setup, or not this rank's block). */
+int64_t ps_get_dinv(ps_handle* h, int64_t pos, void* out, int64_t cap);
 
 /* ps_elim_leaf — Morton leaf id at elimination position pos; -1 if invalid. */
 int64_t ps_elim_leaf(const ps_handle* h, int64_t pos);

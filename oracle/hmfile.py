@@ -1,6 +1,6 @@
 """Oracle-side reader of the `.hm` H-matrix file (TEST INFRASTRUCTURE ONLY).
 
-Independent of libps's C++ loader (paper_2109_04129_b200/csrc/hm_load.cpp):
+Independent of libps's C++ loader (read_file in paper_2109_04129_b200/csrc/ps_host.cpp):
 written separately from the layout documented in include/ps.h.
 
 Z = Z_N + Z_F (Eq. 13):
@@ -50,9 +50,14 @@ class HMatrix:
         return int(self.leaf_off[leaf + 1] - self.leaf_off[leaf])
 
 
-def read_hm(path: str, verify: bool = True) -> HMatrix:
-    with open(path, "rb") as f:
-        data = f.read()
+def read_hm(path: str, verify: bool = True, mmap: bool = False) -> HMatrix:
+    """mmap=True maps the file read-only instead of reading it into memory (large
+    configs: the block views then page in on use). The values are the same."""
+    if mmap:
+        data = np.memmap(path, dtype=np.uint8, mode="r")
+    else:
+        with open(path, "rb") as f:
+            data = f.read()
     o = 0
 
     def take(nbytes):
@@ -61,7 +66,7 @@ def read_hm(path: str, verify: bool = True) -> HMatrix:
         o += nbytes
         return b
 
-    hdr = take(4 + 4 + 5 * 8 + 3 * 8 + 8 + 4 * 8 + 2 * 8)
+    hdr = bytes(take(4 + 4 + 5 * 8 + 3 * 8 + 8 + 4 * 8 + 2 * 8))
     if hdr[:4] != b"HMPS":
         raise ValueError("bad magic")
     (ver,) = struct.unpack_from("<I", hdr, 4)
@@ -70,7 +75,7 @@ def read_hm(path: str, verify: bool = True) -> HMatrix:
     N, nl, nn, nf, flags = struct.unpack_from("<5q", hdr, 8)
     lam, k, _leaf_edge = struct.unpack_from("<3d", hdr, 48)
     n_near_arena, n_far_arena = struct.unpack_from("<2q", hdr, 112)
-    (ck,) = struct.unpack("<Q", take(8))
+    (ck,) = struct.unpack("<Q", bytes(take(8)))
     if verify and ck != _checksum(hdr):
         raise ValueError("header checksum mismatch")
 
@@ -78,7 +83,7 @@ def read_hm(path: str, verify: bool = True) -> HMatrix:
         nb = np.dtype(dtype).itemsize * count
         raw = take(nb)
         take((-nb) % 8)
-        (c,) = struct.unpack("<Q", take(8))
+        (c,) = struct.unpack("<Q", bytes(take(8)))
         if verify and c != _checksum(raw):
             raise ValueError("section checksum mismatch")
         return np.frombuffer(raw, dtype=dtype, count=count)

@@ -65,8 +65,34 @@ def inverse_lu(A: np.ndarray, pos: int = -1, leaf: int = -1) -> np.ndarray:
     return sla.lu_solve((lu, piv), np.eye(A.shape[0], dtype=A.dtype))
 
 
-def compute_scaling(H: HMatrix, order: np.ndarray | None = None) -> Scaling:
-    """Eqs. (14)-(23) with exact fill-in. `order` overrides the file's elimination order."""
+class _Spill:
+    """Append-only file of finished alpha blocks (large configs whose alpha panels exceed
+    host memory): a block is written once its row is scaled out and read back through a
+    read-only memory map. Storage only; the values are the same."""
+
+    def __init__(self, path: str):
+        self.path = path
+        self.f = open(path, "wb")
+        self.off = 0
+        self.index = []                         # (k, j, offset, n_k, n_j)
+
+    def put(self, k: int, j: int, a: np.ndarray) -> None:
+        a = np.ascontiguousarray(a, dtype=np.complex128)
+        self.f.write(a.tobytes())
+        self.index.append((k, j, self.off, a.shape[0], a.shape[1]))
+        self.off += a.size
+
+    def close(self, alpha: list) -> None:
+        self.f.close()
+        mm = np.memmap(self.path, dtype=np.complex128, mode="r", shape=(max(self.off, 1),))
+        for k, j, off, m, n in self.index:
+            alpha[k][j] = mm[off:off + m * n].reshape(m, n)
+
+
+def compute_scaling(H: HMatrix, order: np.ndarray | None = None, spill: str | None = None) -> Scaling:
+    """Eqs. (14)-(23) with exact fill-in. `order` overrides the file's elimination order.
+    spill: file name; finished alpha blocks are kept there (memory-mapped) instead of in
+    memory (C5: 67 GB of panels)."""
     order = np.asarray(H.elim if order is None else order, dtype=np.int64)
     n = len(order)
     pos_of = np.empty(n, dtype=np.int64)
@@ -89,6 +115,7 @@ def compute_scaling(H: HMatrix, order: np.ndarray | None = None) -> Scaling:
             rows[a].add(b)
 
     alpha = [dict() for _ in range(n)]
+    sp = _Spill(spill) if spill else None
     Dinv = [None] * n
     D = [None] * n
     for k in range(n):
@@ -111,6 +138,12 @@ def compute_scaling(H: HMatrix, order: np.ndarray | None = None) -> Scaling:
         # row k is now scaled out (Eq. 21 first row/column = 0); drop it
         for j in row:
             del Zt[(k, j)]
+        if sp is not None:
+            for j in row:
+                sp.put(k, j, alpha[k][j])
+            alpha[k] = {j: None for j in row}
+    if sp is not None:
+        sp.close(alpha)
 
     # unknown maps: elimination-ordered unknown -> Morton position -> RWG index
     e2mort = np.concatenate([np.arange(H.leaf_off[l], H.leaf_off[l + 1]) for l in order]).astype(np.int64)

@@ -45,7 +45,7 @@ class _Report(ctypes.Structure):
     _fields_ = [("nrhs", ctypes.c_int64), ("it0_norm", ctypes.c_void_p), ("it1_norm", ctypes.c_void_p),
                 ("n_diverged", ctypes.c_int), ("t_solve_ms", ctypes.c_double),
                 ("bytes_moved", ctypes.c_double), ("flops", ctypes.c_double),
-                ("kernel_launches", ctypes.c_int64)]
+                ("kernel_launches", ctypes.c_int64), ("ratio", ctypes.c_void_p)]
 
 
 _lib = None
@@ -85,7 +85,7 @@ def load_library():
     L.ps_info.restype = I
     L.ps_info.argtypes = [P, ctypes.POINTER(D), I]
     L.ps_get_dinv.restype = I64
-    L.ps_get_dinv.argtypes = [P, I64, P]
+    L.ps_get_dinv.argtypes = [P, I64, P, I64]
     L.ps_profile.restype = I
     L.ps_profile.argtypes = [P, I]
     L.ps_profile_read.restype = I
@@ -188,10 +188,7 @@ class PsHandle:
         xp, ldx, nrhs2, xdev = _ptr_ld(X, self.N)
         if nrhs != nrhs2 or bdev != xdev:
             raise ValueError("B and X must have the same shape and location")
-        it0 = np.zeros(nrhs) if want_norms else None
-        it1 = np.zeros(nrhs) if want_norms else None
-        rep = _Report(nrhs, it0.ctypes.data if want_norms else None, it1.ctypes.data if want_norms else None,
-                      0, 0.0, 0.0, 0.0, 0)
+        rep, it0, it1, ratio = _report(nrhs, want_norms)
         s = None
         if stream is not None:
             s = ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
@@ -201,7 +198,7 @@ class PsHandle:
                  bytes=rep.bytes_moved, flops=rep.flops, launches=rep.kernel_launches,
                  status=STATUS_NAMES[st])
         if want_norms:
-            r["ratio"] = it1 / np.where(it0 > 0, it0, 1.0)
+            r["ratio"] = ratio
         if st == PS_EDIVERGED:
             warnings.warn(load_library().ps_last_error(self._h).decode(), RuntimeWarning, stacklevel=2)
         self.last_report = r
@@ -221,11 +218,13 @@ class PsHandle:
         return {k: out[i] for i, k in enumerate(INFO_KEYS[:n])}
 
     def dinv(self, pos: int) -> np.ndarray:
-        info = self.info()
-        cap = int(self.N) ** 2 if info["N"] < 4096 else 400 * 400
-        buf = np.zeros(cap, dtype=np.complex128)
-        n = load_library().ps_get_dinv(self._h, pos, buf.ctypes.data)
-        if n < 0:
+        L = load_library()
+        need = L.ps_get_dinv(self._h, pos, None, 0)      # -(n_k^2): the capacity to pass
+        if need >= 0:
+            raise PsError(PS_EINVAL, "ps_get_dinv failed")
+        buf = np.zeros(-need, dtype=np.complex128)
+        n = L.ps_get_dinv(self._h, pos, buf.ctypes.data, -need)
+        if n <= 0:
             raise PsError(PS_EINVAL, "ps_get_dinv failed")
         return buf[:n * n].reshape(n, n, order="F")
 
@@ -256,9 +255,10 @@ class PsHandle:
 def _report(nrhs, want_norms):
     it0 = np.zeros(nrhs) if want_norms else None
     it1 = np.zeros(nrhs) if want_norms else None
+    ratio = np.zeros(nrhs) if want_norms else None
     rep = _Report(nrhs, it0.ctypes.data if want_norms else None, it1.ctypes.data if want_norms else None,
-                  0, 0.0, 0.0, 0.0, 0)
-    return rep, it0, it1
+                  0, 0.0, 0.0, 0.0, 0, ratio.ctypes.data if want_norms else None)
+    return rep, it0, it1, ratio
 
 
 def solve_group(handles, B, X, stream=None, want_norms: bool = True):
@@ -272,7 +272,7 @@ def solve_group(handles, B, X, stream=None, want_norms: bool = True):
     if nrhs != nrhs2 or not (bdev and xdev):
         raise ValueError("solve_group takes device tensors of equal shape")
     arr = (ctypes.c_void_p * len(handles))(*[h._h for h in handles])
-    rep, it0, it1 = _report(nrhs, want_norms)
+    rep, it0, it1, ratio = _report(nrhs, want_norms)
     s = None
     if stream is not None:
         s = ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
@@ -282,7 +282,7 @@ def solve_group(handles, B, X, stream=None, want_norms: bool = True):
     r = dict(it0=it0, it1=it1, n_diverged=rep.n_diverged, t_solve_ms=rep.t_solve_ms,
              launches=rep.kernel_launches, status=STATUS_NAMES[st])
     if want_norms:
-        r["ratio"] = it1 / np.where(it0 > 0, it0, 1.0)
+        r["ratio"] = ratio
     return st, r
 
 

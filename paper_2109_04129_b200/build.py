@@ -15,6 +15,16 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", 
               "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--shared"]
 
 
+def source_hash() -> str:
+    """sha256 (16 hex) of libps's sources: identifies the build a profile was taken on."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in SOURCES + HEADERS:
+        with open(os.path.join(CSRC, f), "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
 def nvcc_available() -> bool:
     return os.path.exists(os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc"))
 

@@ -1954,6 +1954,9 @@ void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
   P.sort_close_bounded();
   P.upload(h->stream);
   sp.ws.alloc(10 * NR + std::max<int64_t>(Ttot, 1));
+  // the tables were copied from pageable host memory on h->stream (non-blocking):
+  // complete them before ps_solve launches the program on the caller's stream
+  CK(cudaStreamSynchronize(h->stream));
 }
 
 bool use_stages() {
@@ -2580,6 +2583,7 @@ ps_status finish_dist(ps_handle* const* hs, int nh, int64_t nrhs, const void* B,
       for (int64_t c = 0; c < cap; ++c) {
         if (rep->it0_norm) rep->it0_norm[c] = norms[c].x;
         if (rep->it1_norm) rep->it1_norm[c] = norms[c].y;
+        if (rep->ratio) rep->ratio[c] = norms[c].x > 0 ? norms[c].y / norms[c].x : 0.0;
       }
     }
     if (ndiv > 0)
@@ -2816,6 +2820,7 @@ ps_status ps_solve(ps_handle* h, int64_t nrhs, const void* B, int64_t ldb, void*
       for (int64_t c = 0; c < cap; ++c) {
         if (rep->it0_norm) rep->it0_norm[c] = norms[c].x;
         if (rep->it1_norm) rep->it1_norm[c] = norms[c].y;
+        if (rep->ratio) rep->ratio[c] = norms[c].x > 0 ? norms[c].y / norms[c].x : 0.0;
       }
     }
     if (ndiv > 0)
@@ -3050,10 +3055,11 @@ int ps_info(const ps_handle* h, double* out, int n) {
   return m;
 }
 
-int64_t ps_get_dinv(ps_handle* h, int64_t pos, void* out) {
-  if (!h || !out || pos < 0 || pos >= h->nl || !h->setup_done || h->Doff[pos] < 0) return -1;   // < 0: not this rank's
+int64_t ps_get_dinv(ps_handle* h, int64_t pos, void* out, int64_t cap) {
+  if (!h || pos < 0 || pos >= h->nl || !h->setup_done || h->Doff[pos] < 0) return 0;   // Doff < 0: not this rank's
   const int64_t n = h->nsz[pos];
-  if (cudaMemcpy(out, h->d_D.p + h->Doff[pos], 16 * n * n, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  if (!out || cap < n * n) return -(n * n);
+  if (cudaMemcpy(out, h->d_D.p + h->Doff[pos], 16 * n * n, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
   return n;
 }
 

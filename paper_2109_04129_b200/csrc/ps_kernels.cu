@@ -1049,6 +1049,12 @@ __device__ __forceinline__ void item_body_nk(const FlowArgs& a, const GWork& w, 
   }
 }
 constexpr size_t FLOW_WS_SMEM = (size_t)WS_NSTAGE * WS_SA * sizeof(double2) + 2 * sizeof(KTabN) + 2 * sizeof(SlotWS);
+// two CTAs per SM (__launch_bounds__(320, 2)): dynamic + static shared memory (s_mail,
+// s_last) + the 1 KB per-CTA reservation must fit twice in the SM's 228 KB
+static_assert(2 * (FLOW_WS_SMEM + 2 * sizeof(MailWS) + 64 + 1024) <= 228 * 1024,
+              "flow_kernel_ws no longer fits 2 CTAs per SM");
+static_assert(2 * (FLOW_SMEM + sizeof(GWork) + sizeof(GTask) + 64 + 1024) <= 228 * 1024,
+              "flow_kernel no longer fits 2 CTAs per SM");
 
 __device__ void ws_scheduler(const FlowArgs& a, SlotWS* slots, KTabN* kts, int lane) {
   int32_t* ticket = a.counters;

@@ -1,12 +1,26 @@
-"""Summarise an ncu --set full report (raw page) for the launches it holds."""
+"""Summarise an ncu --set full report (raw page) for the launches it holds.
+
+  python scripts/ncu_summary.py REPORT.ncu-rep [--config C4 --nrhs 360]
+
+Writes JSON {"src_hash", "config", "nrhs", "rows": [...]} to stdout; src_hash is the
+libps source hash of the build that was profiled (bench.py only quotes the DRAM
+traffic of a summary whose hash matches the build it runs)."""
+import argparse
 import csv
 import io
 import json
+import os
 import subprocess
 import sys
 
-rep = sys.argv[1]
-out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+ap = argparse.ArgumentParser()
+ap.add_argument("report")
+ap.add_argument("--config", default=None)
+ap.add_argument("--nrhs", type=int, default=None)
+args = ap.parse_args()
+out = subprocess.run(["ncu", "-i", args.report, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr, units = rows[0], rows[1]
 want = ["Kernel Name", "launch__grid_size", "launch__registers_per_thread", "gpu__time_duration.sum",
@@ -14,8 +28,10 @@ want = ["Kernel Name", "launch__grid_size", "launch__registers_per_thread", "gpu
         "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_elapsed",
         "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
         "dram__throughput.avg.pct_of_peak_sustained_elapsed",
         "l1tex__throughput.avg.pct_of_peak_sustained_active",
+        "lts__throughput.avg.pct_of_peak_sustained_elapsed",
         "sm__warps_active.avg.pct_of_peak_sustained_active",
         "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smsp__inst_executed.sum",
@@ -36,4 +52,5 @@ for r in rows[2:]:
             i = hdr.index(w)
             d[w] = r[i] + ((" " + units[i]) if units[i] else "")
     res.append(d)
-print(json.dumps(res, indent=1))
+from paper_2109_04129_b200.build import source_hash
+print(json.dumps({"src_hash": source_hash(), "config": args.config, "nrhs": args.nrhs, "rows": res}, indent=1))

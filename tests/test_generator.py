@@ -204,3 +204,15 @@ def test_plane_wave_table():
     assert ang.shape == (360, 2)
     assert np.allclose(np.abs(np.einsum("ij,ij->i", kh, ep.real)), 0, atol=1e-12)   # transverse
     assert np.allclose(np.linalg.norm(ep, axis=1), 1)
+
+
+def test_c4_cylinder_mesh_matches_baseline():
+    """BASELINE configs[3]: closed cylinder r=1 m, L=10 m at 600 MHz, MEAN edge lambda/10
+    over all edges, ~64k triangles, N ~ 96k."""
+    from hmgen.build import make_mesh, mean_edge
+    cfg = CONFIGS["C4"]
+    m = make_mesh(cfg)
+    assert abs(mean_edge(m) / (cfg.lam / 10) - 1) < 0.01
+    assert 62000 <= len(m.tris) <= 66000
+    b = rwg_basis(m)
+    assert b.N == 3 * len(m.tris) // 2 and 93000 <= b.N <= 99000

@@ -284,3 +284,22 @@ def test_hmfile_checksum_detects_corruption(tmp_path):
     open(q, "wb").write(bytes(raw))
     with pytest.raises(ValueError):
         read_hm(q)
+
+
+def test_spill_and_mmap_storage_are_value_identical(cfgdata, tmp_path):
+    """The large-config storage options (memory-mapped file read, alpha blocks spilled to
+    a memory-mapped file; used for C5's golden) hold exactly the in-memory values."""
+    from oracle import compute_scaling, read_hm, solve
+    meta = cfgdata("C1")
+    H0 = read_hm(meta["hm"])
+    H1 = read_hm(meta["hm"], mmap=True)
+    assert all(np.array_equal(a[2], b[2]) for a, b in zip(H0.near, H1.near))
+    assert all(np.array_equal(a[5], b[5]) and np.array_equal(a[6], b[6]) for a, b in zip(H0.far, H1.far))
+    S0 = compute_scaling(H0)
+    S1 = compute_scaling(H1, spill=str(tmp_path / "alpha.bin"))
+    for k in range(S0.n):
+        assert list(S0.alpha[k]) == list(S1.alpha[k])
+        for j in S0.alpha[k]:
+            assert np.array_equal(S0.alpha[k][j], S1.alpha[k][j])
+    B, _ = read_rhs(meta["rhs"])
+    assert np.array_equal(solve(H0, S0, B).x, solve(H1, S1, B).x)
