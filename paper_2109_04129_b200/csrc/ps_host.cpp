@@ -559,6 +559,8 @@ struct Table {
     fa.lean_issue = lean_issue;
     static const int issue_first = env_int("PS_ISSUE_FIRST", 0);
     fa.issue_first = issue_first;
+    static const int ksplit = env_int("PS_KSPLIT", 1);
+    fa.ksplit = ksplit;
     if (pf && pf->trace_on && cls == pf->trace_cls) {
       pf->trace_buf.alloc(6 * bt.nw);
       fa.trace = pf->trace_buf.p;

@@ -90,6 +90,7 @@ struct FlowArgs {
   int32_t mma;             // wide tiles: 0 = DFMA consumer, 1 = FP64 tensor-core (DMMA) consumer
   int32_t lean_issue;      // narrow WS items: lean operand issue (PS_LEAN_ISSUE, default 1)
   int32_t issue_first;     // 1: a stage's refill is issued before its compute (PS_ISSUE_FIRST; measured 2-5 % slower)
+  int32_t ksplit;          // wide DFMA tiles: 1 = k-split two-column layout (item_body_ks), 0 = one column per lane
 };
 
 // Tile geometry of the gather-GEMM kernel (ps_kernels.cu).

@@ -425,6 +425,150 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
 }
 
 
+// DFMA wide tile, k-split layout: 8 warps = 4 row groups (wm) x 2 k-halves (wk); lane
+// owns columns lane and lane + 32 of the 64-column tile and RM rows. Per k a warp loads
+// two B values (8 shared wavefronts) and RM broadcast A values for 2 RM complex FMAs —
+// against 4 + RM wavefronts for RM FMAs in the one-column layout — so the shared-memory
+// pipe, the binding limit of the DFMA consumer, carries ~25 % less per
+// FMA. The two k-halves are summed through shared memory (kh 0 + kh 1, fixed order).
+template <int RM>
+__device__ __forceinline__ void item_body_ks(const FlowArgs& a, const GWork& w, const GTask& T,
+                                             const KTab& kt, double2* As0, double2* Bs0, int tid,
+                                             int lane, int warp, int* s_last, int64_t* tr) {
+  const int wm = warp & 3, wk = warp >> 2;
+  const int i0 = w.mt * GM_MT, c0 = w.nt * GM_NT;
+  const int mm = min(GM_MT, T.m - i0), nn = min(GM_NT, T.n - c0);
+  const int klen = w.kb - w.ka;
+  const int rbase = wm * RM;
+  int32_t* done = a.counters + 1;
+  const bool a_km = T.a_kmajor != 0, b_km = T.b_kmajor != 0;
+  const int nsteps = (klen + KC - 1) / KC;
+#pragma unroll
+  for (int s = 0; s < NSTAGE - 1; ++s)
+    if (s < nsteps) issue_a<GM_MT, GM_NT>(kt, s * KC, klen, i0, mm, a_km, a.A, tid, As0 + s * STAGE_A);
+  cp_commit();
+  const double sgn = (double)T.sign;
+  const bool crit_fin = (w.nchunks > 1 && w.crit >= 0 && w.chunk == w.crit);
+  const bool owns_init = (w.nchunks == 1) || (w.crit >= 0 ? w.chunk == w.crit : w.chunk == 0);
+  double2 acc[RM][2];
+#pragma unroll
+  for (int r = 0; r < RM; ++r) acc[r][0] = acc[r][1] = make_double2(0.0, 0.0);
+  if (crit_fin) {
+    wait_group_sum(a, w, tid);
+    if (wk == 0) {
+      const double2* Gs = a.partial + (w.slot + w.crit) * slot_elems(a);
+#pragma unroll
+      for (int r = 0; r < RM; ++r) {
+        acc[r][0] = __ldcg(Gs + (rbase + r) * GM_NT + lane);
+        acc[r][1] = __ldcg(Gs + (rbase + r) * GM_NT + lane + 32);
+      }
+    }
+  }
+  auto load_init = [&]() {
+    if (!(owns_init && T.oI >= 0 && wk == 0)) return;
+    const double2* Ib = ((T.osel & 2) ? (const double2*)a.S : a.I) + T.oI;
+#pragma unroll
+    for (int r = 0; r < RM; ++r)
+      if (rbase + r < mm)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = lane + 32 * e;
+          if (col < nn) {
+            const double2 z = __ldcg(Ib + (int64_t)(i0 + rbase + r) * T.sIi + (int64_t)(c0 + col) * T.sIc);
+            acc[r][e].x += sgn * z.x;
+            acc[r][e].y += sgn * z.y;
+          }
+        }
+  };
+  if (T.idep < 0) load_init();
+  if (tid < 32) wait_deps(a, w, T, tid);
+  __syncthreads();
+  if (T.idep >= 0) load_init();
+  if (tr) tr[3] = gtimer();
+#pragma unroll
+  for (int s = 0; s < NSTAGE - 1; ++s) {
+    if (s < nsteps) issue_b<GM_MT, GM_NT>(kt, s * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + s * STAGE_B);
+    cp_commit();
+  }
+  for (int s = 0; s < nsteps; ++s) {
+    cp_wait<NSTAGE - 2>();
+    __syncthreads();
+    const int st = s % NSTAGE;
+    const double2* As = As0 + st * STAGE_A + (KC / 2) * wk * AS_LD + rbase;
+    const double2* Bs = Bs0 + st * STAGE_B + (KC / 2) * wk * BS_LD + lane;
+#pragma unroll
+    for (int k = 0; k < KC / 2; ++k) {
+      const double2 b0 = Bs[k * BS_LD], b1 = Bs[k * BS_LD + 32];
+#pragma unroll
+      for (int r = 0; r < RM; ++r) {
+        const double2 av = As[k * AS_LD + r];
+        cfma(acc[r][0], av, b0);
+        cfma(acc[r][1], av, b1);
+      }
+    }
+    const int sn = s + NSTAGE - 1;
+    if (sn < nsteps) {
+      const int stn = sn % NSTAGE;
+      issue_a<GM_MT, GM_NT>(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * STAGE_A);
+      issue_b<GM_MT, GM_NT>(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * STAGE_B);
+    }
+    cp_commit();
+  }
+  cp_wait<0>();
+  __syncthreads();
+  if (tr) tr[4] = gtimer();
+  // k-half reduction through shared memory (the stage buffers are free now)
+  double2* red = As0;
+  if (wk == 1) {
+#pragma unroll
+    for (int r = 0; r < RM; ++r) {
+      red[(rbase + r) * GM_NT + lane] = acc[r][0];
+      red[(rbase + r) * GM_NT + lane + 32] = acc[r][1];
+    }
+  }
+  __syncthreads();
+  constexpr int E = 2 * RM;
+  double2 accf[E];
+  int off[E];
+  bool own[E];
+#pragma unroll
+  for (int r = 0; r < RM; ++r)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int x = 2 * r + e;
+      off[x] = (rbase + r) * GM_NT + lane + 32 * e;
+      own[x] = (wk == 0);
+      if (wk == 0) {
+        const double2 v = red[off[x]];
+        accf[x] = make_double2(acc[r][e].x + v.x, acc[r][e].y + v.y);
+      } else {
+        accf[x] = make_double2(0.0, 0.0);
+      }
+    }
+  __syncthreads();          // red (= stage buffers) free again before the next item
+  const bool finalize = crit_fin ? true : splitk_combine<E>(a, w, accf, off, own, tid, s_last);
+  if (finalize) {
+    if (wk == 0) {
+      double2* Ob = ((T.osel & 1) ? a.S : a.O) + T.oO;
+#pragma unroll
+      for (int r = 0; r < RM; ++r) {
+        const int i = rbase + r;
+        if (i < mm)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int col = lane + 32 * e;
+            if (col < nn) {
+              const double2 v = accf[2 * r + e];
+              __stcg(Ob + (int64_t)(i0 + i) * T.sOi + (int64_t)(c0 + col) * T.sOc, make_double2(sgn * v.x, sgn * v.y));
+            }
+          }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) red_release(done + T.unit0 + w.nt, 1);
+  }
+}
+
 // FP64 tensor-core MMA: D(8x8) += A(8x4, row) * B(4x8, col); per lane
 // A[g][q], B[q][g], C[g][2q], C[g][2q+1] with g = lane / 4, q = lane % 4.
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
@@ -786,10 +930,14 @@ flow_kernel(const FlowArgs a) {
     switch (RM) {
       case 0: item_body_narrow<false, NSTAGE>(a, w, T, kt, As0, Bs0, tid, &s_last, tr, STAGE_A, STAGE_B); break;
 #define PS_RM_CASE(R) \
-      case R: item_body<R>(a, w, T, kt, As0, Bs0, tid, lane, wm, wn, &s_last, tr); break;
-      PS_RM_CASE(1) PS_RM_CASE(2) PS_RM_CASE(3) PS_RM_CASE(4) PS_RM_CASE(5) PS_RM_CASE(6)
-      PS_RM_CASE(7) PS_RM_CASE(8)
+      case R: if (a.ksplit) item_body_ks<R>(a, w, T, kt, As0, Bs0, tid, lane, warp, &s_last, tr); \
+              else item_body<R>(a, w, T, kt, As0, Bs0, tid, lane, wm, wn, &s_last, tr); break;
+      PS_RM_CASE(1) PS_RM_CASE(2) PS_RM_CASE(3) PS_RM_CASE(4) PS_RM_CASE(5)
 #undef PS_RM_CASE
+      // 6-8 rows per warp: 2 RM accumulator pairs would exceed the 128-register budget
+      case 6: item_body<6>(a, w, T, kt, As0, Bs0, tid, lane, wm, wn, &s_last, tr); break;
+      case 7: item_body<7>(a, w, T, kt, As0, Bs0, tid, lane, wm, wn, &s_last, tr); break;
+      case 8: item_body<8>(a, w, T, kt, As0, Bs0, tid, lane, wm, wn, &s_last, tr); break;
       default: break;
     }
     if (tr) tr[5] = gtimer();
