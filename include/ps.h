@@ -246,9 +246,11 @@ int ps_profile_read(const ps_handle* h, double* out, int n);
 /* ps_trace / ps_trace_read — debug instrumentation of the persistent dataflow
  * kernel: ps_trace(h, c) records, for the next launches of kernel class c
  * (as in ps_profile_read; -1 disables), per work item: item, SM id, and the
- * globaltimer (ns) at fetch, dependencies satisfied, compute done, published.
- * ps_trace_read copies the last traced launch, 12 int64 per item (those 6 plus
- * task, row tile, column tile, chunk, n_chunks, k-length); returns the item count. */
+ * globaltimer (ns) at fetch, dependencies satisfied, compute done, published, and
+ * (narrow warp-specialised kernel; else 0) when the scheduler warp took the item's
+ * ticket and when it handed the prepared item over. ps_trace_read copies the last
+ * traced launch, 14 int64 per item (those 8 plus task, row tile, column tile, chunk,
+ * n_chunks, k-length); returns the item count. out: capacity 14 * cap_items. */
 ps_status ps_trace(ps_handle* h, int cls);
 int64_t ps_trace_read(ps_handle* h, int64_t* out, int64_t cap_items);
 

@@ -244,9 +244,9 @@ class PsHandle:
         self._check(load_library().ps_trace(self._h, cls))
 
     def trace_read(self, cap: int = 2_000_000) -> np.ndarray:
-        buf = np.zeros(12 * cap, dtype=np.int64)
+        buf = np.zeros(14 * cap, dtype=np.int64)
         n = load_library().ps_trace_read(self._h, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), cap)
-        return buf[:12 * n].reshape(n, 12)
+        return buf[:14 * n].reshape(n, 14)
 
     def elim_leaf(self, pos: int) -> int:
         return int(load_library().ps_elim_leaf(self._h, pos))

@@ -562,7 +562,8 @@ struct Table {
     static const int ksplit = env_int("PS_KSPLIT", 1);
     fa.ksplit = ksplit;
     if (pf && pf->trace_on && cls == pf->trace_cls) {
-      pf->trace_buf.alloc(6 * bt.nw);
+      pf->trace_buf.alloc(8 * bt.nw);
+      CK(cudaMemsetAsync(pf->trace_buf.p, 0, 8 * sizeof(int64_t) * bt.nw, st));
       fa.trace = pf->trace_buf.p;
       pf->trace_work = &work;
       pf->trace_tasks = &tasks;
@@ -2911,9 +2912,9 @@ int ps_profile_read(const ps_handle* h, double* out, int n) {
 }
 
 // Debug: trace every work item of the next flow launches of kernel class
-// `cls` (0..4; -1 disables). ps_trace_read copies the last one: 12 int64 per
-// item (item, smid, t_fetch, t_ready, t_computed, t_done [ns, globaltimer],
-// task, mt, nt, chunk, nchunks, klen). Returns the number of items.
+// `cls` (0..6; -1 disables). ps_trace_read copies the last one: 14 int64 per
+// item (item, smid, t_fetch, t_ready, t_computed, t_done, t_sched0, t_sched1
+// [ns, globaltimer], task, mt, nt, chunk, nchunks, klen). Returns the number of items.
 ps_status ps_trace(ps_handle* h, int cls) {
   if (!h) return fail(nullptr, PS_EINVAL, "ps_trace: handle is NULL");
   h->prof.trace_on = cls >= 0;
@@ -2924,18 +2925,18 @@ ps_status ps_trace(ps_handle* h, int cls) {
 int64_t ps_trace_read(ps_handle* h, int64_t* out, int64_t cap_items) {
   if (!h || !out || !h->prof.trace_work || h->prof.trace_buf.n == 0) return 0;
   const int64_t n = std::min(cap_items, h->prof.trace_nw);
-  std::vector<int64_t> raw(6 * h->prof.trace_nw);
+  std::vector<int64_t> raw(8 * h->prof.trace_nw);
   if (cudaMemcpy(raw.data(), h->prof.trace_buf.p, 8 * raw.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
     return 0;
   for (int64_t i = 0; i < n; ++i) {
-    for (int k = 0; k < 6; ++k) out[12 * i + k] = raw[6 * i + k];
+    for (int k = 0; k < 8; ++k) out[14 * i + k] = raw[8 * i + k];
     const GWork& w = (*h->prof.trace_work)[h->prof.trace_w0 + i];
-    out[12 * i + 6] = w.task;
-    out[12 * i + 7] = w.mt;
-    out[12 * i + 8] = w.nt;
-    out[12 * i + 9] = w.chunk;
-    out[12 * i + 10] = w.nchunks;
-    out[12 * i + 11] = w.kb - w.ka;
+    out[14 * i + 8] = w.task;
+    out[14 * i + 9] = w.mt;
+    out[14 * i + 10] = w.nt;
+    out[14 * i + 11] = w.chunk;
+    out[14 * i + 12] = w.nchunks;
+    out[14 * i + 13] = w.kb - w.ka;
   }
   return n;
 }

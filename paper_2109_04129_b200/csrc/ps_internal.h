@@ -85,7 +85,8 @@ struct FlowArgs {
   int32_t n_units;
   int32_t defer_fin;       // narrow WS items: split-K combine by the finisher warp (PS_DEFER_FIN)
   double2* partial;        // split-K partial tiles, GM_MT * GM_NT each
-  int64_t* trace;          // optional: 6 x int64 per item (item, smid, t_fetch, t_ready, t_computed, t_done), ns
+  int64_t* trace;          // optional: 8 x int64 per item (item, smid, t_fetch, t_ready, t_computed, t_done,
+                           // narrow WS kernel: scheduler ticket taken, slot handed over), ns
   int32_t narrow;          // 1: narrow 64 x 8 tiles (small nrhs), 0: 32 x 64 tiles
   int32_t mma;             // wide tiles: 0 = DFMA consumer, 1 = FP64 tensor-core (DMMA) consumer
   int32_t lean_issue;      // narrow WS items: lean operand issue (PS_LEAN_ISSUE, default 1)

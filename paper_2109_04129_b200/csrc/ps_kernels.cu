@@ -896,7 +896,7 @@ flow_kernel(const FlowArgs a) {
     __syncthreads();
     const int64_t item = s_item;
     if (item >= a.nwork) return;
-    int64_t* tr = (a.trace != nullptr && tid == 0) ? a.trace + 6 * item : nullptr;
+    int64_t* tr = (a.trace != nullptr && tid == 0) ? a.trace + 8 * item : nullptr;
     if (tr) { tr[0] = item; tr[1] = smid(); tr[2] = gtimer(); }
     const GWork& w = s_w;       // shared: one copy per CTA, not per-thread registers
     const GTask& T = s_T;
@@ -973,16 +973,34 @@ struct MailWS {
   int64_t oO, sOi, sOc;
   int32_t osel, sign, unit0, m, n, live;   // live 0: terminate
 };
-constexpr int WS_A = KC * GN_MT;                      // A tile of a narrow stage: 1024 complex
-constexpr int WS_SA = WS_A + 64 * GN_NT;              // + B tile (<= 64 k x 8 columns)
-constexpr int WS_NSTAGE = 3;
 
 // Narrow item body of the warp-specialised kernel with a row-adaptive tile:
-// MTW = 16 / 32 / 64 rows x KCW = 1024 / MTW k per stage, so a short task (a
-// 16-19 row leaf) still streams 1024 operator entries per stage instead of
-// leaving 3/4 of a 64-row tile empty. Thread t: row t % MTW, column pair
-// 2 ((t / MTW) % 4), k slice (t / MTW) / 4 of NKS = 64 / MTW slices of 16 k;
-// the slices are summed through shared memory at the end (fixed order).
+// MTW = 16 / 32 / 64 rows x KCW = 1024 / MTW k per stage. Thread t: row t % MTW,
+// column pair 2 ((t / MTW) % 4), k slice (t / MTW) / 4 of NKS = 64 / MTW slices of
+// 16 k; the slices are summed through shared memory at the end (fixed order).
+// Variable-depth ring: a stage holds only the item's real rows (mm x KCW operator
+// entries, B rows padded to the even column count), so a short task (a 4-8 or 17-24
+// row leaf) keeps as many stages in flight as fit the 3 x 1024-entry A ring / the
+// 1536-entry B ring (3..8) — the operator bytes in flight per CTA no longer shrink
+// with the leaf size. Operand issue is lean: one k-table lookup per thread and stage
+// for k-major A, elements outside the tile simply not copied (the ring is zeroed at
+// kernel start and only ever holds finite values; B rows k >= klen are zero-filled,
+// so stale A there contributes 0), B columns >= nn skipped.
+constexpr int WS_ARING = 3 * KC * GN_MT;              // A ring: 3072 complex
+constexpr int WS_BRING = 3 * 64 * GN_NT;              // B ring: 1536 complex
+constexpr int WS_RING = WS_ARING + WS_BRING;
+constexpr int WS_MAXNS = 8;
+
+template <int N>
+__device__ __forceinline__ void cp_wait_rt(int n) {   // cp.async.wait_group with a run-time count <= N
+  if constexpr (N > 0) {
+    if (n >= N) { cp_wait<N>(); return; }
+    cp_wait_rt<N - 1>(n);
+  } else {
+    cp_wait<0>();
+  }
+}
+
 template <int MTW>
 __device__ __forceinline__ void item_body_nk(const FlowArgs& a, const GWork& w, const GTask& T,
                                              const KTabN& kt, double2* stages, int tid, int* s_last,
@@ -995,36 +1013,12 @@ __device__ __forceinline__ void item_body_nk(const FlowArgs& a, const GWork& w, 
   int32_t* done = a.counters + 1;
   const bool a_km = T.a_kmajor != 0, b_km = T.b_kmajor != 0;
   const int nsteps = (klen + KCW - 1) / KCW;
+  const int nnp = (nn + 1) & ~1;                       // B row stride in the ring (even column count)
+  const int SA = mm * KCW, SB = nnp * KCW;             // stage sizes (complex)
+  const int NS = min(WS_MAXNS, min(WS_ARING / SA, WS_BRING / SB));
+  double2* Aring = stages;
+  double2* Bring = stages + WS_ARING;
   auto issue_a = [&](int k0, double2* As) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int e = tid + q * 256;
-      int i, k;
-      if (a_km) { k = e % KCW; i = e / KCW; } else { i = e % MTW; k = e / MTW; }
-      const int kk = k0 + k;
-      const bool v = (i < mm && kk < klen);
-      const double2* src = v ? a.A + kt.kA[kk] + (int64_t)(i0 + i) * kt.kSi[kk] : a.A;
-      cp_async16(As + k * MTW + i, src, v);
-    }
-  };
-  auto issue_b = [&](int k0, double2* Bs) {
-#pragma unroll
-    for (int q = 0; q < (KCW * GN_NT + 255) / 256; ++q) {
-      const int e = tid + q * 256;
-      if ((KCW * GN_NT) % 256 != 0 && e >= KCW * GN_NT) break;
-      int c, k;
-      if (b_km) { k = e % KCW; c = e / KCW; } else { c = e % GN_NT; k = e / GN_NT; }
-      const int kk = k0 + k;
-      const bool v = (c < nn && kk < klen);
-      const double2* src = v ? kt.kB[kk] + (int64_t)(c0 + c) * kt.kSc[kk] : a.B;
-      cp_async16(Bs + k * GN_NT + c, src, v);
-    }
-  };
-  // Lean variants (a.lean_issue): one k-table lookup per thread and stage when A is
-  // k-major, elements outside the tile simply not copied (shared stages are zeroed at
-  // kernel start and only ever hold finite values; B rows k >= klen are still
-  // zero-filled, so stale A there contributes 0), B columns >= nn skipped.
-  auto issue_a_lean = [&](int k0, double2* As) {
     if (a_km) {
       constexpr int QS = 256 / KCW;
       const int k = tid % KCW, i = tid / KCW, kk = k0 + k;
@@ -1033,7 +1027,7 @@ __device__ __forceinline__ void item_body_nk(const FlowArgs& a, const GWork& w, 
         const double2* base = a.A + kt.kA[kk] + (int64_t)(i0 + i) * si;
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          if (i + q * QS < mm) cp_async16_all(As + k * MTW + i + q * QS, base + q * QS * si);
+          if (i + q * QS < mm) cp_async16_all(As + k * mm + i + q * QS, base + q * QS * si);
       }
     } else {
       const int i = tid % MTW;
@@ -1041,29 +1035,25 @@ __device__ __forceinline__ void item_body_nk(const FlowArgs& a, const GWork& w, 
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int kk = k0 + tid / MTW + q * (256 / MTW);
-          if (kk < klen) cp_async16_all(As + (kk - k0) * MTW + i, a.A + kt.kA[kk] + (int64_t)(i0 + i) * kt.kSi[kk]);
+          if (kk < klen) cp_async16_all(As + (kk - k0) * mm + i, a.A + kt.kA[kk] + (int64_t)(i0 + i) * kt.kSi[kk]);
         }
       }
     }
   };
-  auto issue_b_lean = [&](int k0, double2* Bs) {
-#pragma unroll
-    for (int q = 0; q < (KCW * GN_NT + 255) / 256; ++q) {
-      const int e = tid + q * 256;
-      if ((KCW * GN_NT) % 256 != 0 && e >= KCW * GN_NT) break;
+  auto issue_b = [&](int k0, double2* Bs) {
+    const int ne = KCW * nnp;
+    for (int e = tid; e < ne; e += 256) {
       int c, k;
-      if (b_km) { k = e % KCW; c = e / KCW; } else { c = e % GN_NT; k = e / GN_NT; }
+      if (b_km) { k = e % KCW; c = e / KCW; } else { c = e % nnp; k = e / nnp; }
       if (c < nn) {
         const int kk = k0 + k;
         const bool v = kk < klen;
-        cp_async16(Bs + k * GN_NT + c, v ? kt.kB[kk] + (int64_t)(c0 + c) * kt.kSc[kk] : a.B, v);
+        cp_async16(Bs + k * nnp + c, v ? kt.kB[kk] + (int64_t)(c0 + c) * kt.kSc[kk] : a.B, v);
       }
     }
   };
-  const bool lean = a.lean_issue != 0;
-#pragma unroll
-  for (int s = 0; s < WS_NSTAGE - 1; ++s)
-    if (s < nsteps) { if (lean) issue_a_lean(s * KCW, stages + s * WS_SA); else issue_a(s * KCW, stages + s * WS_SA); }
+  for (int s = 0; s < NS - 1; ++s)
+    if (s < nsteps) issue_a(s * KCW, Aring + s * SA);
   cp_commit();
   const double sgn = (double)T.sign;
   const bool crit_fin = (w.nchunks > 1 && w.crit >= 0 && w.chunk == w.crit);
@@ -1085,60 +1075,39 @@ __device__ __forceinline__ void item_body_nk(const FlowArgs& a, const GWork& w, 
       }
   }
   if (tr) tr[3] = gtimer();
-#pragma unroll
-  for (int s = 0; s < WS_NSTAGE - 1; ++s) {
-    if (s < nsteps) { if (lean) issue_b_lean(s * KCW, stages + s * WS_SA + WS_A); else issue_b(s * KCW, stages + s * WS_SA + WS_A); }
+  for (int s = 0; s < NS - 1; ++s) {
+    if (s < nsteps) issue_b(s * KCW, Bring + s * SB);
     cp_commit();
   }
   const bool live = (row < mm) && (cb < nn);
-  const bool two = !lean || (cb + 1 < nn);           // second column of the pair is a real column
+  const bool two = cb + 1 < nn;                      // second column of the pair is a real column
+  int st = 0, stn = NS - 1;                          // stage computed / stage refilled
   for (int s = 0; s < nsteps; ++s) {
-    cp_wait<WS_NSTAGE - 2>();
+    cp_wait_rt<WS_MAXNS - 2>(NS - 2);
     bsync<true>();
-    const int st = s % WS_NSTAGE;
-    if (a.issue_first) {   // refill the stage computed last iteration before computing this one
-      const int sn = s + WS_NSTAGE - 1;
-      if (sn < nsteps) {
-        const int stn = sn % WS_NSTAGE;
-        if (lean) {
-          issue_a_lean(sn * KCW, stages + stn * WS_SA);
-          issue_b_lean(sn * KCW, stages + stn * WS_SA + WS_A);
-        } else {
-          issue_a(sn * KCW, stages + stn * WS_SA);
-          issue_b(sn * KCW, stages + stn * WS_SA + WS_A);
-        }
-      }
-      cp_commit();
-    }
     if (live) {
-      const double2* As = stages + st * WS_SA + (16 * ks) * MTW + row;
-      const double2* Bs = stages + st * WS_SA + WS_A + (16 * ks) * GN_NT + cb;
+      const double2* As = Aring + st * SA + (16 * ks) * mm + row;
+      const double2* Bs = Bring + st * SB + (16 * ks) * nnp + cb;
       if (two) {
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
-          const double2 av = As[k * MTW];
-          cfma(acc[0], av, Bs[k * GN_NT]);
-          cfma(acc[1], av, Bs[k * GN_NT + 1]);
+          const double2 av = As[k * mm];
+          cfma(acc[0], av, Bs[k * nnp]);
+          cfma(acc[1], av, Bs[k * nnp + 1]);
         }
       } else {
 #pragma unroll
-        for (int k = 0; k < 16; ++k) cfma(acc[0], As[k * MTW], Bs[k * GN_NT]);
+        for (int k = 0; k < 16; ++k) cfma(acc[0], As[k * mm], Bs[k * nnp]);
       }
     }
-    if (!a.issue_first) {
-      const int sn = s + WS_NSTAGE - 1;
-      if (sn < nsteps) {
-        const int stn = sn % WS_NSTAGE;
-        if (lean) {
-          issue_a_lean(sn * KCW, stages + stn * WS_SA);
-          issue_b_lean(sn * KCW, stages + stn * WS_SA + WS_A);
-        } else {
-          issue_a(sn * KCW, stages + stn * WS_SA);
-          issue_b(sn * KCW, stages + stn * WS_SA + WS_A);
-        }
-      }
-      cp_commit();
+    const int sn = s + NS - 1;
+    if (sn < nsteps) {
+      issue_a(sn * KCW, Aring + stn * SA);
+      issue_b(sn * KCW, Bring + stn * SB);
     }
+    cp_commit();
+    st = (st + 1 == NS) ? 0 : st + 1;
+    stn = (stn + 1 == NS) ? 0 : stn + 1;
   }
   cp_wait<0>();
   bsync<true>();
@@ -1196,7 +1165,7 @@ __device__ __forceinline__ void item_body_nk(const FlowArgs& a, const GWork& w, 
     if (tid == 0) red_release(done + T.unit0 + w.nt, 1);
   }
 }
-constexpr size_t FLOW_WS_SMEM = (size_t)WS_NSTAGE * WS_SA * sizeof(double2) + 2 * sizeof(KTabN) + 2 * sizeof(SlotWS);
+constexpr size_t FLOW_WS_SMEM = (size_t)WS_RING * sizeof(double2) + 2 * sizeof(KTabN) + 2 * sizeof(SlotWS);
 // two CTAs per SM (__launch_bounds__(320, 2)): dynamic + static shared memory (s_mail,
 // s_last) + the 1 KB per-CTA reservation must fit twice in the SM's 228 KB
 static_assert(2 * (FLOW_WS_SMEM + 2 * sizeof(MailWS) + 64 + 1024) <= 228 * 1024,
@@ -1210,6 +1179,7 @@ __device__ void ws_scheduler(const FlowArgs& a, SlotWS* slots, KTabN* kts, int l
     const int s = (int)(j & 1);
     if (j >= 2) bar_sync_n(3 + s, 288);               // compute warps released slot s
     int it = 0;
+    const int64_t t_s0 = a.trace ? gtimer() : 0;
     if (lane == 0) it = atomicAdd(ticket, 1);
     it = __shfl_sync(0xffffffffu, it, 0);
     SlotWS& sl = slots[s];
@@ -1271,6 +1241,10 @@ __device__ void ws_scheduler(const FlowArgs& a, SlotWS* slots, KTabN* kts, int l
       while (ld_acquire(ctr) < sl.w.nsub + 1) __nanosleep(32);
     }
     __syncwarp();
+    if (a.trace && lane == 0) {                       // scheduler: ticket taken, slot ready
+      a.trace[8 * (int64_t)it + 6] = t_s0;
+      a.trace[8 * (int64_t)it + 7] = gtimer();
+    }
     bar_arrive_n(1 + s, 288);                         // slot s full
   }
 }
@@ -1341,7 +1315,7 @@ __global__ void __launch_bounds__(320, 2)
 flow_kernel_ws(const FlowArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* stages = reinterpret_cast<double2*>(smem_raw);
-  KTabN* kts = reinterpret_cast<KTabN*>(stages + WS_NSTAGE * WS_SA);
+  KTabN* kts = reinterpret_cast<KTabN*>(stages + WS_RING);
   SlotWS* slots = reinterpret_cast<SlotWS*>(kts + 2);
   __shared__ int s_last;
   __shared__ MailWS s_mail[2];
@@ -1354,7 +1328,7 @@ flow_kernel_ws(const FlowArgs a) {
     ws_scheduler(a, slots, kts, tid & 31);
     return;
   }
-  for (int e = tid; e < WS_NSTAGE * WS_SA; e += 256) stages[e] = make_double2(0.0, 0.0);
+  for (int e = tid; e < WS_RING; e += 256) stages[e] = make_double2(0.0, 0.0);
   bsync<true>();
   int jm = 0;                                         // mails handed to the finisher
   for (int64_t j = 0;; ++j) {
@@ -1369,7 +1343,7 @@ flow_kernel_ws(const FlowArgs a) {
       bar_arrive_n(6 + f, 288);
       return;
     }
-    int64_t* tr = (a.trace != nullptr && tid == 0) ? a.trace + 6 * item : nullptr;
+    int64_t* tr = (a.trace != nullptr && tid == 0) ? a.trace + 8 * item : nullptr;
     if (tr) { tr[0] = item; tr[1] = smid(); tr[2] = gtimer(); }
     const int mrows = min(GN_MT, sl.T.m - sl.w.mt * GN_MT);
     if (mrows <= 16) item_body_nk<16>(a, sl.w, sl.T, kts[s], stages, tid, &s_last, tr, s_mail, jm);

@@ -19,13 +19,22 @@ def main():
         return
     t0 = tr[:, 2].min()
     f, r, c, d = (tr[:, k] - t0 for k in (2, 3, 4, 5))
-    task, nch, klen = tr[:, 6], tr[:, 10], tr[:, 11]
+    task, nch, klen = tr[:, 8], tr[:, 12], tr[:, 13]
+    s0, s1 = tr[:, 6], tr[:, 7]
     T = d.max()
     nsm = len(np.unique(tr[:, 1]))
     print(f"items {len(tr)}  span {T / 1e3:.1f} us  SMs {nsm}")
     wait, comp, fin = (r - f).sum(), (c - r).sum(), (d - c).sum()
     tot = wait + comp + fin
     print(f"item time: wait {wait / tot:.2%}  compute {comp / tot:.2%}  combine/finalise {fin / tot:.2%}")
+    if (s0 > 0).all():
+        prep = (s1 - s0) / 1e3
+        lag = (tr[:, 2] - s1) / 1e3
+        print(f"scheduler prep (ticket -> slot handed over) us: p10/50/90/99 = "
+              f"{np.percentile(prep, [10, 50, 90, 99]).round(2)}, mean {prep.mean():.2f}")
+        print(f"slot handed over -> compute warps start us: p10/50/90 = {np.percentile(lag, [10, 50, 90]).round(2)}; "
+              f"items whose compute warps waited on the scheduler (< 0.2 us): {(lag < 0.2).mean():.1%}")
+        print(f"item k-length: p10/50/90 = {np.percentile(klen, [10, 50, 90])}, mean {klen.mean():.0f}")
     b = a.bin_us * 1e3
     nb = int(T // b) + 1
     busy = np.zeros(nb)

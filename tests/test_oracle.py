@@ -303,3 +303,23 @@ def test_spill_and_mmap_storage_are_value_identical(cfgdata, tmp_path):
             assert np.array_equal(S0.alpha[k][j], S1.alpha[k][j])
     B, _ = read_rhs(meta["rhs"])
     assert np.array_equal(solve(H0, S0, B).x, solve(H1, S1, B).x)
+
+
+def test_truncation_size_report_c1(cfgdata):
+    """SURVEY §8(c) 'truncation size: reported number' (PAPER.md:313 metric): the committed
+    tests/golden/accuracy.json (scripts/accuracy_report.py: oracle two-term x vs dense LU of
+    Z = Z_N + Z_F) reproduces on C1, and the error is of the size the Eq. 45 ratio implies
+    for a two-term truncation (ratio 0.80 >= 0.1: the paper's divergence regime, R14)."""
+    import json
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts"))
+    from accuracy_report import report
+    cfgdata("C1")
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "accuracy.json")) as f:
+        stored = json.load(f)["C1"]
+    now = report("C1")
+    e0 = stored["rel_err_two_term_vs_dense_LU"]["max"]
+    assert abs(now["rel_err_two_term_vs_dense_LU"]["max"] - e0) <= 1e-10 * e0
+    assert abs(now["ratio_it1_it0"]["max"] - stored["ratio_it1_it0"]["max"]) <= 1e-12
+    assert 0.1 <= e0 <= 1.0 and now["ratio_it1_it0"]["max"] >= 0.1
