@@ -132,9 +132,23 @@ ps_status hm_load(const char* path, const ps_dist* dist, ps_handle** out);
  *   included), D_k^{-1} = Z~_kk^{-1} (LU-type elimination with partial pivoting,
  *   explicit inverse), alpha_kj = -D_k^{-1} Z~_kj (Eq. 16).
  * opts: NULL = defaults. Frees the near-field input arena when done.
+ * Row partition with NCCL (ps_dist.partition = 1, nccl_unique_id set): collective —
+ * every rank calls it; each factors only its own interior subtrees and the separators,
+ * with one NCCL sum all-reduce of the separator rows' partial W between the phases.
+ * An in-process partition handle must use ps_setup_group (PS_ESTATE otherwise).
  * Errors: PS_EINVAL, PS_ESTATE (already set up), PS_ESINGULAR (message names
  * the leaf), PS_ENOMEM, PS_ECUDA. */
 ps_status ps_setup(ps_handle* h, const ps_setup_opts* opts);
+
+/* ps_setup_group — ps_setup of an in-process row partition (handles of ranks
+ * 0..nranks-1 from hm_load with partition = 1 and nccl_unique_id = NULL, all on one
+ * device): every rank runs its sharded setup (its own interior subtrees, then its
+ * interior's Schur updates of the separator rows), the separator rows' partial W are
+ * summed over the ranks in rank order (the in-process stand-in of the NCCL all-reduce
+ * that ps_setup performs on an NCCL rank), then every rank eliminates the separators.
+ * opts as ps_setup (ordering must be 0). Errors as ps_setup, plus PS_EINVAL when the
+ * handles are not one consistent group. */
+ps_status ps_setup_group(ps_handle* const* hs, int nranks, const ps_setup_opts* opts);
 
 /* ps_solve — the two-term power-series solve (Eqs. 24, 26, 30-36):
  *   b~ = R^T b (Eq. 24), b_o = D^{-1} b~ (Eq. 32), u = U b_o = D^{-1} R^T Z_F R b_o
@@ -218,7 +232,9 @@ enum {
   PS_INFO_CHAIN_HEIGHT,      /* levels of the chain graph (dependent stages of a sweep / 2) */
   PS_INFO_T_ENTRIES,         /* complex entries of all T_c (U_c x U_c each) */
   PS_INFO_OP_BYTES,          /* device bytes of the operator this handle holds (alpha panels, D^-1, T, far
-                                stacks); a row-partition rank holds only its share after ps_setup */
+                                stacks); a row-partition rank holds only its share */
+  PS_INFO_SETUP_BYTES,       /* device bytes of the setup arenas of this handle (near blocks held, W, alpha
+                                panels, D^-1): a row-partition rank holds its interior plus the separators */
   PS_INFO_COUNT
 };
 int ps_info(const ps_handle* h, double* out, int n);

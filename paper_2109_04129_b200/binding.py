@@ -22,7 +22,7 @@ STATUS_NAMES = ["PS_OK", "PS_EINVAL", "PS_EIO", "PS_EFORMAT", "PS_ENOMEM", "PS_E
 PS_OP_RT, PS_OP_DINV, PS_OP_R, PS_OP_ZF, PS_OP_U = 1, 2, 3, 4, 5
 INFO_KEYS = ["N", "n_leaves", "n_near", "n_far", "alpha_blocks", "nR", "nD", "nF", "height",
              "depth", "setup_madds", "setup_done", "nranks", "own_rows", "sep_rows", "chains",
-             "chain_height", "T_entries", "op_bytes"]
+             "chain_height", "T_entries", "op_bytes", "setup_bytes"]
 
 
 class PsError(RuntimeError):
@@ -98,6 +98,8 @@ def load_library():
     L.ps_trace_read.argtypes = [P, ctypes.POINTER(I64), I64]
     L.ps_elim_leaf.restype = I64
     L.ps_elim_leaf.argtypes = [P, I64]
+    L.ps_setup_group.restype = I
+    L.ps_setup_group.argtypes = [ctypes.POINTER(P), I, ctypes.POINTER(_Opts)]
     L.ps_solve_group.restype = I
     L.ps_solve_group.argtypes = [ctypes.POINTER(P), I, I64, P, I64, P, I64, P, ctypes.POINTER(_Report)]
     L.ps_nccl_unique_id.restype = I
@@ -284,6 +286,17 @@ def solve_group(handles, B, X, stream=None, want_norms: bool = True):
     if want_norms:
         r["ratio"] = ratio
     return st, r
+
+
+def setup_group(handles, ratio_threshold: float = 0.1):
+    """ps_setup_group: the sharded setup of an in-process row partition (handles =
+    ranks 0..P-1, PsHandle(..., rank=g, nranks=P, partition=True))."""
+    L = load_library()
+    arr = (ctypes.c_void_p * len(handles))(*[h._h for h in handles])
+    o = _Opts(1, 0, 0, float(ratio_threshold))
+    st = L.ps_setup_group(arr, len(handles), ctypes.byref(o))
+    if st != PS_OK:
+        raise PsError(st, L.ps_last_error(handles[0]._h).decode())
 
 
 def nccl_unique_id() -> bytes:

@@ -172,6 +172,14 @@ int NARROW_STEPS() {
   return v;
 }
 
+// Tile mode of a plan with nrhs columns: 1 = narrow 64 x 8 tiles (nrhs <= 8, operator
+// streaming), 0 = wide 32 x 64 tiles.
+int narrow_mode(int64_t R) { return R <= 8 ? 1 : 0; }
+// concurrent work units of a launch (the split-K chunk heuristics aim at about one item
+// per unit per stage) and rows of a tile
+int resident_units(int) { return flow_resident_ctas(); }
+int mode_rows(int mode) { return mode ? GN_MT : GM_MT; }
+
 // A gather-GEMM table: tasks, segments, work items and batches (one launch each).
 constexpr int CHUNK_STEPS = 16;    // target k-steps (of GM_KC) per split-K work item
 
@@ -193,7 +201,7 @@ struct Table {
   int32_t max_units = 0, max_tiles = 0;
   int64_t max_slots = 0;
   int chunk_steps = CHUNK_STEPS;
-  int narrow = 0;          // 1: 64 x 8 tiles (small nrhs)
+  int narrow = 0;          // 1: 64 x 8 tiles (small nrhs), 0: 32 x 64 tiles
   double2* S = nullptr;    // scratch vector base of osel / bsel offsets (chain stages)
   int mma = 0;             // wide-tile consumer: 0 DFMA, 1 FP64 mma.sync (DMMA)
   // optional global ordering of work items (ticket order): key = key_base + nt * key_stagger,
@@ -555,10 +563,6 @@ struct Table {
       return -1;
     }();
     fa.mma = mma_env >= 0 ? mma_env : mma;
-    static const int lean_issue = env_int("PS_LEAN_ISSUE", 1);
-    fa.lean_issue = lean_issue;
-    static const int issue_first = env_int("PS_ISSUE_FIRST", 0);
-    fa.issue_first = issue_first;
     static const int ksplit = env_int("PS_KSPLIT", 1);
     fa.ksplit = ksplit;
     if (pf && pf->trace_on && cls == pf->trace_cls) {
@@ -676,7 +680,15 @@ struct ps_handle {
   Prof prof;
   // ---- row partition (ps_dist.partition = 1) ----
   int rank = 0, nranks = 1, part_mode = 0;
-  bool sharded = false;                    // operator reduced to this rank's share (shard_operator)
+  bool sharded = false;                    // operator held for this rank's share only (sharded setup)
+  std::vector<char> need;                  // per position: this rank holds its rows (own interior or separator)
+  std::vector<int64_t> near_dev;           // per near block: element offset in d_near, -1 if not held
+  int64_t near_dev_len = 0;
+  int64_t Wsep0 = 0, Wsep_len = 0;         // separator rows of the W arena (one contiguous range, summed
+                                           // over the ranks between the two setup phases)
+  int64_t near_file_off = -1;              // byte offset of the near arena in the .hm file (deferred read)
+  uint64_t near_file_ck = 0;
+  std::string path;
   std::vector<int32_t> owner, far_owner;   // per position: interior rank (-1 separator); far-row rank
   std::vector<int64_t> doff;               // first row of position p in the partitioned layout:
                                            // [rank 0 interior | ... | rank P-1 interior | separators],
@@ -698,7 +710,7 @@ ps_status fail(ps_handle* h, ps_status s, const std::string& msg) {
 
 // ------------------------------------------------------------------ file
 void read_file(ps_handle* h, const char* path, std::vector<double2>& near_arena,
-               std::vector<double2>& far_arena) {
+               std::vector<double2>& far_arena, bool defer_near = false) {
   FILE* f = std::fopen(path, "rb");
   if (!f) throw PsError{PS_EIO, std::string("cannot open ") + path};
   std::unique_ptr<FILE, int (*)(FILE*)> guard(f, std::fclose);
@@ -743,8 +755,15 @@ void read_file(ps_handle* h, const char* path, std::vector<double2>& near_arena,
   section(h->elim.data(), 4 * h->nl, "elim_order");
   h->near_list.resize(3 * h->nnear);
   section(h->near_list.data(), 24 * h->nnear, "near_list");
-  near_arena.resize(h->near_len);
-  section(near_arena.data(), 16 * h->near_len, "near_arena");
+  if (defer_near) {            // read later, only this rank's blocks (load_near)
+    h->near_file_off = (int64_t)std::ftell(f);
+    const int64_t nb = 16 * h->near_len, pad = (8 - nb % 8) % 8;
+    if (std::fseek(f, nb + pad, SEEK_CUR) != 0) throw PsError{PS_EFORMAT, "truncated file"};
+    rd(&h->near_file_ck, 8);
+  } else {
+    near_arena.resize(h->near_len);
+    section(near_arena.data(), 16 * h->near_len, "near_arena");
+  }
   h->far_list.resize(7 * h->nfar);
   section(h->far_list.data(), 56 * h->nfar, "far_list");
   far_arena.resize(h->far_len);
@@ -777,7 +796,147 @@ void read_file(ps_handle* h, const char* path, std::vector<double2>& near_arena,
   }
 }
 
+// Streamed read of the near arena (deferred by read_file): the whole section is read
+// in chunks for its checksum, and only the blocks with keep[b] != 0 are copied into
+// `out` (compact, in near-list order; h->near_dev[b] = element offset or -1). A rank
+// of a row partition thus never holds the other ranks' near field in host memory.
+void load_near(ps_handle* h, const std::vector<char>& keep, std::vector<double2>& out) {
+  FILE* f = std::fopen(h->path.c_str(), "rb");
+  if (!f) throw PsError{PS_EIO, "cannot reopen " + h->path};
+  std::unique_ptr<FILE, int (*)(FILE*)> guard(f, std::fclose);
+  if (std::fseek(f, h->near_file_off, SEEK_SET) != 0) throw PsError{PS_EFORMAT, "truncated file"};
+  const int64_t nb = h->nnear;
+  std::vector<std::array<int64_t, 3>> blk;            // (arena offset, length, block)
+  h->near_dev.assign(nb, -1);
+  int64_t tot = 0;
+  for (int64_t b = 0; b < nb; ++b) {
+    if (!keep[b]) continue;
+    const int64_t i = h->near_list[3 * b], j = h->near_list[3 * b + 1];
+    const int64_t len = (h->leaf_off[i + 1] - h->leaf_off[i]) * (h->leaf_off[j + 1] - h->leaf_off[j]);
+    blk.push_back({h->near_list[3 * b + 2], len, b});
+    h->near_dev[b] = tot;
+    tot += len;
+  }
+  out.assign(std::max<int64_t>(tot, 1), double2{0.0, 0.0});
+  h->near_dev_len = tot;
+  std::sort(blk.begin(), blk.end());
+  const int64_t CH = 1 << 22;                          // elements per chunk (64 MB)
+  std::vector<double2> buf(std::min<int64_t>(CH, std::max<int64_t>(h->near_len, 1)));
+  uint64_t ck = 0;
+  size_t bi = 0;
+  for (int64_t c0 = 0; c0 < h->near_len; c0 += CH) {
+    const int64_t n = std::min(CH, h->near_len - c0);
+    if (std::fread(buf.data(), 16, (size_t)n, f) != (size_t)n) throw PsError{PS_EFORMAT, "truncated file"};
+    const uint8_t* b8 = reinterpret_cast<const uint8_t*>(buf.data());
+    const uint64_t w0 = (uint64_t)c0 * 2;              // 8-byte words before this chunk
+    for (int64_t q = 0; q < 2 * n; ++q) {
+      uint64_t w;
+      std::memcpy(&w, b8 + 8 * q, 8);
+      ck += w * (2 * (w0 + (uint64_t)q) + 1);
+    }
+    while (bi < blk.size() && blk[bi][0] + blk[bi][1] <= c0) ++bi;
+    for (size_t k = bi; k < blk.size() && blk[k][0] < c0 + n; ++k) {
+      const int64_t lo = std::max(blk[k][0], c0), hi = std::min(blk[k][0] + blk[k][1], c0 + n);
+      std::copy(buf.data() + (lo - c0), buf.data() + (hi - c0), out.data() + h->near_dev[blk[k][2]] + (lo - blk[k][0]));
+    }
+  }
+  ck ^= (uint64_t)(16 * h->near_len);
+  if (ck != h->near_file_ck) throw PsError{PS_EFORMAT, "checksum mismatch in section near_arena"};
+}
+
+// Chains of the elimination tree (see ps_handle), bottom-up by position. With a row
+// partition (owner != NULL) a chain never crosses an owner change (rank interior /
+// separator), so every T_c belongs entirely to one owner class.
+void build_chains(ps_handle* h, const std::vector<int32_t>* owner) {
+  const int64_t nl = h->nl;
+  {
+    const int64_t tmax = env_int("PS_TMAX", 4096);
+    h->use_chains = env_int("PS_CHAINS", 1) != 0;
+    std::vector<int32_t> nch(nl, 0);
+    for (int64_t p = 0; p < nl; ++p)
+      if (h->parent[p] >= 0) ++nch[h->parent[p]];
+    h->chain_of.assign(nl, -1);
+    h->cpos.assign(nl, 0);
+    h->chains.clear();
+    h->ch_U.clear();
+    for (int64_t p = 0; p < nl; ++p) {
+      if (h->chain_of[p] >= 0) continue;
+      std::vector<int32_t> c{(int32_t)p};
+      int64_t U = h->nsz[p];
+      int32_t q = (int32_t)p;
+      while (h->parent[q] >= 0 && nch[h->parent[q]] == 1 && h->chain_of[h->parent[q]] < 0 &&
+             U + h->nsz[h->parent[q]] <= tmax && (!owner || (*owner)[h->parent[q]] == (*owner)[q])) {
+        q = h->parent[q];
+        h->cpos[q] = U;
+        U += h->nsz[q];
+        c.push_back(q);
+      }
+      static const int cmin = env_int("PS_CHAIN_MIN", 2);
+      if ((int)c.size() < cmin) {                   // too short to pay for a T_c: single nodes
+        for (int32_t x : c) {
+          h->chain_of[x] = (int32_t)h->chains.size();
+          h->cpos[x] = 0;
+          h->chains.push_back({x});
+          h->ch_U.push_back(h->nsz[x]);
+        }
+        continue;
+      }
+      const int32_t id = (int32_t)h->chains.size();
+      for (int32_t x : c) h->chain_of[x] = id;
+      h->chains.push_back(std::move(c));
+      h->ch_U.push_back(U);
+    }
+    const int64_t nc = (int64_t)h->chains.size();
+    h->ch_Toff.assign(nc, -1);
+    h->Tlen = 0;
+    for (int64_t c = 0; c < nc; ++c)
+      if (h->chains[c].size() >= 2) {
+        h->ch_Toff[c] = h->Tlen;
+        h->Tlen += h->ch_U[c] * h->ch_U[c];
+      }
+    // chain-graph levels: the parent of a piece's top is the first node of another piece
+    std::vector<int32_t> order(nc);
+    std::iota(order.begin(), order.end(), 0);
+    std::sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return h->chains[x].back() < h->chains[y].back(); });
+    h->ch_height.assign(nc, 0);
+    h->ch_depth.assign(nc, 0);
+    for (int32_t c : order) {
+      const int32_t up = h->parent[h->chains[c].back()];
+      if (up >= 0) h->ch_height[h->chain_of[up]] = std::max(h->ch_height[h->chain_of[up]], h->ch_height[c] + 1);
+    }
+    for (auto it = order.rbegin(); it != order.rend(); ++it) {
+      const int32_t up = h->parent[h->chains[*it].back()];
+      if (up >= 0) h->ch_depth[*it] = h->ch_depth[h->chain_of[up]] + 1;
+    }
+    h->max_ch_height = h->max_ch_depth = 0;
+    for (int64_t c = 0; c < nc; ++c) {
+      h->max_ch_height = std::max(h->max_ch_height, h->ch_height[c]);
+      h->max_ch_depth = std::max(h->max_ch_depth, h->ch_depth[c]);
+    }
+    if (!h->use_chains) {                          // every node its own piece (no T_c)
+      h->Tlen = 0;
+      std::vector<std::vector<int32_t>> single;
+      for (int64_t p = 0; p < nl; ++p) single.push_back({(int32_t)p});
+      h->chains.swap(single);
+      h->ch_U.assign(nl, 0);
+      h->ch_Toff.assign(nl, -1);
+      h->ch_height.assign(nl, 0);
+      h->ch_depth.assign(nl, 0);
+      for (int64_t p = 0; p < nl; ++p) {
+        h->chain_of[p] = (int32_t)p;
+        h->cpos[p] = 0;
+        h->ch_U[p] = h->nsz[p];
+        h->ch_height[p] = h->height[p];
+        h->ch_depth[p] = h->depth[p];
+      }
+      h->max_ch_height = h->max_height;
+      h->max_ch_depth = h->max_depth;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ symbolic
+void build_chains(ps_handle* h, const std::vector<int32_t>* owner);
 void symbolic(ps_handle* h) {
   const int64_t nl = h->nl;
   h->pos_of.assign(nl, 0);
@@ -869,91 +1028,7 @@ void symbolic(ps_handle* h) {
   h->Wlen = W;
   h->Plen = P;
   h->Dlen = D;
-  // chains of the elimination tree (see ps_handle), bottom-up by position
-  {
-    const int64_t tmax = env_int("PS_TMAX", 4096);
-    h->use_chains = env_int("PS_CHAINS", 1) != 0;
-    std::vector<int32_t> nch(nl, 0);
-    for (int64_t p = 0; p < nl; ++p)
-      if (h->parent[p] >= 0) ++nch[h->parent[p]];
-    h->chain_of.assign(nl, -1);
-    h->cpos.assign(nl, 0);
-    h->chains.clear();
-    h->ch_U.clear();
-    for (int64_t p = 0; p < nl; ++p) {
-      if (h->chain_of[p] >= 0) continue;
-      std::vector<int32_t> c{(int32_t)p};
-      int64_t U = h->nsz[p];
-      int32_t q = (int32_t)p;
-      while (h->parent[q] >= 0 && nch[h->parent[q]] == 1 && h->chain_of[h->parent[q]] < 0 &&
-             U + h->nsz[h->parent[q]] <= tmax) {
-        q = h->parent[q];
-        h->cpos[q] = U;
-        U += h->nsz[q];
-        c.push_back(q);
-      }
-      static const int cmin = env_int("PS_CHAIN_MIN", 2);
-      if ((int)c.size() < cmin) {                   // too short to pay for a T_c: single nodes
-        for (int32_t x : c) {
-          h->chain_of[x] = (int32_t)h->chains.size();
-          h->cpos[x] = 0;
-          h->chains.push_back({x});
-          h->ch_U.push_back(h->nsz[x]);
-        }
-        continue;
-      }
-      const int32_t id = (int32_t)h->chains.size();
-      for (int32_t x : c) h->chain_of[x] = id;
-      h->chains.push_back(std::move(c));
-      h->ch_U.push_back(U);
-    }
-    const int64_t nc = (int64_t)h->chains.size();
-    h->ch_Toff.assign(nc, -1);
-    h->Tlen = 0;
-    for (int64_t c = 0; c < nc; ++c)
-      if (h->chains[c].size() >= 2) {
-        h->ch_Toff[c] = h->Tlen;
-        h->Tlen += h->ch_U[c] * h->ch_U[c];
-      }
-    // chain-graph levels: the parent of a piece's top is the first node of another piece
-    std::vector<int32_t> order(nc);
-    std::iota(order.begin(), order.end(), 0);
-    std::sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return h->chains[x].back() < h->chains[y].back(); });
-    h->ch_height.assign(nc, 0);
-    h->ch_depth.assign(nc, 0);
-    for (int32_t c : order) {
-      const int32_t up = h->parent[h->chains[c].back()];
-      if (up >= 0) h->ch_height[h->chain_of[up]] = std::max(h->ch_height[h->chain_of[up]], h->ch_height[c] + 1);
-    }
-    for (auto it = order.rbegin(); it != order.rend(); ++it) {
-      const int32_t up = h->parent[h->chains[*it].back()];
-      if (up >= 0) h->ch_depth[*it] = h->ch_depth[h->chain_of[up]] + 1;
-    }
-    h->max_ch_height = h->max_ch_depth = 0;
-    for (int64_t c = 0; c < nc; ++c) {
-      h->max_ch_height = std::max(h->max_ch_height, h->ch_height[c]);
-      h->max_ch_depth = std::max(h->max_ch_depth, h->ch_depth[c]);
-    }
-    if (!h->use_chains) {                          // every node its own piece (no T_c)
-      h->Tlen = 0;
-      std::vector<std::vector<int32_t>> single;
-      for (int64_t p = 0; p < nl; ++p) single.push_back({(int32_t)p});
-      h->chains.swap(single);
-      h->ch_U.assign(nl, 0);
-      h->ch_Toff.assign(nl, -1);
-      h->ch_height.assign(nl, 0);
-      h->ch_depth.assign(nl, 0);
-      for (int64_t p = 0; p < nl; ++p) {
-        h->chain_of[p] = (int32_t)p;
-        h->cpos[p] = 0;
-        h->ch_U[p] = h->nsz[p];
-        h->ch_height[p] = h->height[p];
-        h->ch_depth[p] = h->depth[p];
-      }
-      h->max_ch_height = h->max_height;
-      h->max_ch_depth = h->max_depth;
-    }
-  }
+  build_chains(h, nullptr);
   // unknown maps
   h->e2mort.resize(h->N);
   h->e2rwg.resize(h->N);
@@ -1182,8 +1257,14 @@ struct SetupLevel {
   int maxn = 0;
 };
 
-void build_setup_level(ps_handle* h, const std::vector<int32_t>& leaves, SetupLevel& sp) {
+// mode 0: every descendant's update, near-block init (the whole tree on one rank, or a
+//         rank's own interior); mode 1: separator rows, updates from this rank's own
+//         interior only, near-block init where this rank holds the block (rank 0), no
+//         panels (phase B of the sharded setup); mode 2: separator rows, updates from
+//         separator descendants only, added in place to the rank-summed W (phase C).
+void build_setup_level(ps_handle* h, const std::vector<int32_t>& leaves, SetupLevel& sp, int mode = 0) {
   const int64_t nl = h->nl;
+  if (mode == 2) sp.asmb.S = h->d_W.p;
   {
     for (int32_t p : leaves) {
       const int64_t np_ = h->nsz[p];
@@ -1195,6 +1276,8 @@ void build_setup_level(ps_handle* h, const std::vector<int32_t>& leaves, SetupLe
       // terms of each target, from descendants d with p in struct(d), in increasing d
       std::map<int32_t, std::vector<std::array<int64_t, 3>>> terms_of;  // j -> (oA, oB, nd)
       for (auto [d, idx] : h->gath[p]) {
+        if (mode == 1 && h->owner[d] != h->rank) continue;
+        if (mode == 2 && h->owner[d] >= 0) continue;
         const int64_t nd = h->nsz[d];
         const auto& sd = h->st[d];
         const int64_t oA = h->Poff[d] + h->pcol[d][idx] * nd;   // alpha_dp (nd x np), transposed view
@@ -1210,15 +1293,17 @@ void build_setup_level(ps_handle* h, const std::vector<int32_t>& leaves, SetupLe
         int64_t oI = -1, sIi = 0, sIc = 0;
         uint64_t key_a = (uint64_t)std::min(lp, lj) * (uint64_t)nl + (uint64_t)std::max(lp, lj);
         auto it = h->near_idx.find(key_a);
-        if (it != h->near_idx.end()) {
+        if (it != h->near_idx.end() && mode != 2) {
           const int64_t* nb = &h->near_list[3 * it->second];
           const int64_t n_first = h->leaf_off[nb[0] + 1] - h->leaf_off[nb[0]];
-          oI = nb[2];
+          oI = h->near_dev.empty() ? nb[2] : h->near_dev[it->second];   // -1: block not held here
           if (lp == nb[0]) { sIi = 1; sIc = n_first; }   // Z_{lp,lj} as stored
           else { sIi = n_first; sIc = 1; }               // transpose view
         }
         const int64_t oO = h->Woff[p] + wcol(h, p, j) * np_;
+        if (mode == 2) { oI = oO; sIi = 1; sIc = np_; }  // in place: the rank-summed W_pj
         int32_t t = sp.asmb.add_task(oO, 1, np_, oI, sIi, sIc, (int)np_, (int)nj, +1);
+        if (mode == 2) sp.asmb.tasks[t].osel |= 2;
         auto tj = terms_of.find(j);
         if (tj != terms_of.end())
           for (auto& c : tj->second) sp.asmb.add_term(t, c[0], c[2], 1, c[1], 1, c[2], (int)c[2]);
@@ -1229,7 +1314,7 @@ void build_setup_level(ps_handle* h, const std::vector<int32_t>& leaves, SetupLe
     // panel: P_p = -Dinv_p W_p[:, n_p:]
     for (int32_t p : leaves) {
       const int64_t np_ = h->nsz[p];
-      if (h->S[p] == 0) continue;
+      if (h->S[p] == 0 || mode == 1) continue;
       int32_t t = sp.panel.add_task(h->Poff[p], 1, np_, -1, 0, 0, (int)np_, (int)h->S[p], -1);
       sp.panel.add_term(t, h->Doff[p], 1, np_, h->Woff[p] + np_ * np_, 1, np_, (int)np_);
       sp.panel.tile(t);
@@ -1267,63 +1352,6 @@ void ensure_far(ps_handle* h, cudaStream_t s) {
   }
   h->d_far.p = h->d_farbuf.p;
   h->Fbase = (int64_t)(h->d_farbuf.p - h->d_op.p);
-}
-
-// Row partition: after setup, keep only the operator blocks this rank's
-// tables read — alpha panels P_p and D_p^-1 of its interior positions and the separators,
-// and T_c of the chains that touch them — in new, compact allocations (the far stacks
-// stay whole). Setup itself ran replicated; the solve then holds ~1/P of P, D and T.
-void shard_operator(ps_handle* h, cudaStream_t s) {
-  const int64_t nl = h->nl;
-  const int g = h->rank;
-  auto need = [&](int64_t p) { return h->owner[p] == g || h->owner[p] < 0; };
-  std::vector<int64_t> Poff2(nl, -1), Doff2(nl, -1);
-  int64_t P2 = 0, D2 = 0;
-  for (int64_t p = 0; p < nl; ++p)
-    if (need(p)) { Poff2[p] = P2; P2 += h->nsz[p] * h->S[p]; }
-  for (int64_t p = 0; p < nl; ++p)
-    if (need(p)) { Doff2[p] = D2; D2 += h->nsz[p] * h->nsz[p]; }
-  DevBuf<double2> op2;
-  op2.alloc(std::max<int64_t>(P2 + D2, 1));
-  for (int64_t p = 0; p < nl; ++p) {
-    if (!need(p)) continue;
-    const int64_t np_ = h->nsz[p];
-    if (np_ * h->S[p] > 0)
-      CK(cudaMemcpyAsync(op2.p + Poff2[p], h->d_op.p + h->Pbase + h->Poff[p], 16 * np_ * h->S[p],
-                         cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemcpyAsync(op2.p + P2 + Doff2[p], h->d_op.p + h->Dbase + h->Doff[p], 16 * np_ * np_,
-                       cudaMemcpyDeviceToDevice, s));
-  }
-  const int64_t nc = (int64_t)h->chains.size();
-  std::vector<int64_t> Toff2(h->ch_Toff.size(), -1);
-  int64_t T2 = 0;
-  for (int64_t c = 0; c < nc; ++c) {
-    if (h->ch_Toff[c] < 0) continue;
-    bool any = false;
-    for (int32_t q : h->chains[c]) any = any || need(q);
-    if (any) { Toff2[c] = T2; T2 += h->ch_U[c] * h->ch_U[c]; }
-  }
-  DevBuf<double2> t2;
-  t2.alloc(std::max<int64_t>(T2, 1));
-  for (int64_t c = 0; c < nc; ++c)
-    if (Toff2[c] >= 0)
-      CK(cudaMemcpyAsync(t2.p + Toff2[c], h->d_T.p + h->ch_Toff[c], 16 * h->ch_U[c] * h->ch_U[c],
-                         cudaMemcpyDeviceToDevice, s));
-  CK(cudaStreamSynchronize(s));
-  h->d_op = std::move(op2);
-  h->d_T = std::move(t2);
-  h->Poff.swap(Poff2);
-  h->Doff.swap(Doff2);
-  h->ch_Toff.swap(Toff2);
-  h->Plen = P2; h->Dlen = D2; h->Tlen = T2;
-  h->Pbase = 0; h->Dbase = P2;
-  h->d_P.p = h->d_op.p;
-  h->d_D.p = h->d_op.p + P2;
-  h->Tbase = (int64_t)(h->d_T.p - h->d_op.p);
-  ensure_far(h, s);                                   // re-derive Fbase from the new d_op
-  h->plan.reset();
-  h->dplan.reset();
-  h->sharded = true;
 }
 
 // T_c = (I - A_c^T)^{-1} of every chain piece with L >= 2 (see ps_handle): the
@@ -1390,7 +1418,7 @@ void build_chain_sweeps(ps_handle* h, SolvePlan& sp, int64_t R, int narrow, int 
       static const int nadapt = env_int("PS_NARROW_ADAPT", 1);
       if (!nadapt) return NARROW_STEPS();
       double ks = 0;
-      for (auto [m, K] : mk) ks += std::ceil((double)m / GN_MT) * std::ceil((double)K / GM_KC);
+      for (auto [m, K] : mk) ks += std::ceil((double)m / mode_rows(narrow)) * std::ceil((double)K / GM_KC);
       return std::max(2, std::min(NARROW_STEPS(), (int)std::ceil(ks / (double)resident)));
     }
     double ks = 0;
@@ -1400,7 +1428,8 @@ void build_chain_sweeps(ps_handle* h, SolvePlan& sp, int64_t R, int narrow, int 
   // ticket order: (stage + column tile * stagger), so the column tiles enter the
   // stage sequence staggered and the window of fetched items holds ready work
   static const int stag_pct = env_int("PS_STAGGER", 0);
-  const int nnt = (int)((R + (narrow ? GN_NT : GM_NT) - 1) / (narrow ? GN_NT : GM_NT));
+  const int ntw = narrow ? GN_NT : GM_NT;
+  const int nnt = (int)((R + ntw - 1) / ntw);
   const double nst_f = 2.0 * (h->max_ch_height + 1), nst_b = 2.0 * (h->max_ch_depth + 1);
   sp.fwd.key_stagger = nnt > 1 ? 0.01 * stag_pct * nst_f / nnt : 0.0;
   sp.bwd.key_stagger = nnt > 1 ? 0.01 * stag_pct * nst_b / nnt : 0.0;
@@ -1583,7 +1612,7 @@ void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
   const int64_t nl = h->nl;
   const int64_t R = nrhs;
   sp.nrhs = nrhs;
-  const int narrow = (R <= 8) ? 1 : 0;
+  const int narrow = narrow_mode(R);
   sp.sc.alloc(h->N * R);                           // chain-stage scratch (e / f)
   for (Table* tb : {&sp.fwd, &sp.bwd, &sp.dinv, &sp.far1, &sp.far2}) {
     tb->narrow = narrow;
@@ -1593,7 +1622,7 @@ void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
     sp.far1.chunk_steps = sp.far2.chunk_steps = env_int("PS_FAR_STEPS", 32);
     sp.far1.mma = sp.far2.mma = env_int("PS_FAR_MMA", 1);
   }
-  const int resident = flow_resident_ctas();
+  const int resident = resident_units(narrow);
   // forward sweep (gather form of Eq. 24) and backward sweep (Eq. 26), chain-collapsed
   build_chain_sweeps(h, sp, R, narrow, resident);     // PS_CHAINS=0: every node its own piece
   // D^{-1} (Eq. 32), one batch
@@ -1691,7 +1720,7 @@ void build_common(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
 void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
   const int64_t nl = h->nl;
   Table& P = sp.prog;
-  P.narrow = (R <= 8) ? 1 : 0;
+  P.narrow = narrow_mode(R);
   if (P.narrow) P.chunk_steps = NARROW_STEPS();
   const int64_t NR = h->N * R;
   sp.oY = 0; sp.oBO = NR; sp.oW = 2 * NR; sp.oZ = 3 * NR; sp.oXT = 4 * NR; sp.oX = 5 * NR; sp.oTMP = 6 * NR;
@@ -1699,7 +1728,7 @@ void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
   std::vector<int64_t> toff(ncl);
   int64_t Ttot = 0;
   for (int64_t c = 0; c < ncl; ++c) { toff[c] = sp.oTMP + Ttot; Ttot += h->cl_sr[c] * R; }
-  const int resident = flow_resident_ctas();
+  const int resident = resident_units(P.narrow);
   P.key_stagger = env_int("PS_PROG_STAGGER", 0);     // column tile b enters b * this many key levels later
   P.early_keys = true;
   // far field on the tensor-core consumer with long chunks, as in the stage tables
@@ -1729,7 +1758,7 @@ void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
   auto steps_of = [&](const std::vector<std::pair<int64_t, int64_t>>& mk) {
     double ks = 0;
     if (P.narrow) {
-      for (auto [m, K] : mk) ks += std::ceil((double)m / GN_MT) * std::ceil((double)K / GM_KC);
+      for (auto [m, K] : mk) ks += std::ceil((double)m / mode_rows(P.narrow)) * std::ceil((double)K / GM_KC);
       return std::max(2, std::min(NARROW_STEPS(), (int)std::ceil(ks / (double)resident)));
     }
     static const int pmax = env_int("PS_SWEEP_MAXSTEPS", 32), pipc = env_int("PS_SWEEP_IPC", 1);
@@ -2114,6 +2143,56 @@ void dist_layout(ps_handle* h) {
   }
 }
 
+// Sharded layout of a row-partition rank: the rank holds the rows of
+// its own interior positions and of the replicated separators only — W, alpha panels
+// and D^-1 in compact arenas (W: interior first, then the separators as one contiguous
+// range, summed over the ranks between the two setup phases), the near blocks whose
+// row position it assembles (separator rows' near blocks on rank 0 only), and T_c of
+// the chains it uses (chains are cut where the owner changes).
+void shard_layout(ps_handle* h, std::vector<char>& keep_near) {
+  const int64_t nl = h->nl;
+  const int g = h->rank;
+  h->need.assign(nl, 0);
+  for (int64_t p = 0; p < nl; ++p) h->need[p] = (h->owner[p] == g || h->owner[p] < 0) ? 1 : 0;
+  build_chains(h, &h->owner);
+  int64_t W = 0, P = 0, D = 0;
+  h->Woff.assign(nl, -1);
+  h->Poff.assign(nl, -1);
+  h->Doff.assign(nl, -1);
+  for (int pass = 0; pass < 2; ++pass) {               // interior rows, then the separators
+    if (pass == 1) h->Wsep0 = W;
+    for (int64_t p = 0; p < nl; ++p) {
+      if (!(pass == 0 ? h->owner[p] == g : h->owner[p] < 0)) continue;
+      h->Woff[p] = W;
+      W += (int64_t)h->nsz[p] * (h->nsz[p] + h->S[p]);
+    }
+  }
+  h->Wsep_len = W - h->Wsep0;
+  for (int64_t p = 0; p < nl; ++p) {
+    if (!h->need[p]) continue;
+    h->Poff[p] = P;
+    P += (int64_t)h->nsz[p] * h->S[p];
+    h->Doff[p] = D;
+    D += (int64_t)h->nsz[p] * h->nsz[p];
+  }
+  h->Wlen = W; h->Plen = P; h->Dlen = D;
+  h->Tlen = 0;
+  for (size_t c = 0; c < h->chains.size(); ++c) {
+    h->ch_Toff[c] = -1;
+    if (h->chains[c].size() >= 2 && h->need[h->chains[c][0]]) {
+      h->ch_Toff[c] = h->Tlen;
+      h->Tlen += h->ch_U[c] * h->ch_U[c];
+    }
+  }
+  keep_near.assign(h->nnear, 0);
+  for (int64_t b = 0; b < h->nnear; ++b) {
+    const int32_t pi = h->pos_of[h->near_list[3 * b]], pj = h->pos_of[h->near_list[3 * b + 1]];
+    const int32_t r = std::min(pi, pj);
+    keep_near[b] = (h->owner[r] == g || (h->owner[r] < 0 && g == 0)) ? 1 : 0;
+  }
+  h->sharded = true;
+}
+
 // This rank's tables. Phases and the exchange after each:
 //   0  y = B; y[S] = 0 on ranks != 0; forward sweep of the interior subtrees
 //      plus their contributions to the separator rows            -> all-reduce y[S]
@@ -2135,7 +2214,7 @@ void build_dist_plan(ps_handle* h, DistPlan& dp, int64_t R) {
   int64_t Ttot = 0;
   for (int64_t c = 0; c < ncl; ++c) { toff[c] = dp.oTMP + Ttot; Ttot += h->cl_sr[c] * R; }
   dp.oSC = dp.oTMP + Ttot;                           // chain scratch (e / f) of the sweeps
-  const int narrow = (R <= 8) ? 1 : 0;
+  const int narrow = narrow_mode(R);
   for (Table* tb : {&dp.fwdIA, &dp.fwdSA, &dp.dinvA, &dp.bwdA, &dp.far1, &dp.far2, &dp.fwdIC, &dp.fwdSC,
                     &dp.dinvC, &dp.bwdC}) {
     tb->narrow = narrow;
@@ -2599,6 +2678,97 @@ ps_status finish_dist(ps_handle* const* hs, int nh, int64_t nrhs, const void* B,
   }
   return PS_OK;
 }
+
+// ------------------------------------------------------------------ setup driver
+// The positions, elimination level by elimination level (setup tables are built,
+// launched and freed per level): mode as build_setup_level; modes 0 and 2 also invert
+// the scaled diagonal blocks (Eqs. 23, 30) and form the alpha panels (Eq. 16).
+void setup_levels(ps_handle* h, cudaStream_t s, const std::vector<int32_t>& pos, int mode) {
+  if (pos.empty()) return;
+  std::vector<std::vector<int32_t>> lv(h->max_height + 1);
+  for (int32_t p : pos) lv[mode == 1 ? 0 : h->height[p]].push_back(p);   // phase B: one batch
+  DevBuf<int32_t> d_status;
+  d_status.alloc(std::max<int64_t>((int64_t)pos.size(), 1));
+  std::vector<int32_t> status;
+  for (const auto& leaves : lv) {
+    if (leaves.empty()) continue;
+    SetupLevel sp;
+    build_setup_level(h, leaves, sp, mode);
+    // Eq. 21 (left-looking): assemble W_p = [Z~_pp | Z~_p,struct(p)]
+    sp.asmb.launch_all(h->d_W.p, h->d_near.p, h->d_P.p, h->d_W.p, s);
+    if (mode != 1) {
+      const int64_t nlev = sp.nlev;
+      CK(cudaMemsetAsync(d_status.p, 0, sizeof(int32_t) * nlev, s));
+      // Eqs. 23/30: D_p^{-1}
+      launch_inverse(nlev, sp.d_ids.p, sp.d_sz.p, sp.d_src.p, sp.d_ld.p, sp.d_dst.p, h->d_W.p, h->d_D.p,
+                     d_status.p, sp.maxn, s);
+      status.assign(nlev, 0);
+      CK(cudaMemcpyAsync(status.data(), d_status.p, sizeof(int32_t) * nlev, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      for (int64_t i = 0; i < nlev; ++i)
+        if (status[i])
+          throw PsError{PS_ESINGULAR, "singular scaled diagonal block at elimination position " +
+                                          std::to_string(leaves[i]) + " (leaf " + std::to_string(h->leaf_at[leaves[i]]) +
+                                          ")"};
+      // Eq. 16: alpha_p* = -D_p^{-1} Z~_p*
+      sp.panel.launch_all(h->d_P.p, nullptr, h->d_D.p, h->d_W.p, s);
+    }
+    CK(cudaStreamSynchronize(s));                    // the level's tables are freed here
+  }
+}
+
+// After the scaling: free the setup-only arenas, upload the far stacks, form T_c.
+void setup_finish(ps_handle* h, cudaStream_t s) {
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(s));
+  h->d_W.release();
+  h->d_near.release();
+  ensure_far(h, s);
+  h->d_T.alloc(std::max<int64_t>(h->Tlen, 1));
+  h->Tbase = (int64_t)(h->d_T.p - h->d_op.p);
+  chain_setup(h, s);
+  CK(cudaStreamSynchronize(s));
+  h->plan.reset();                                  // plans made before setup (ps_apply Z_F) are stale
+  h->dplan.reset();
+  h->setup_done = true;
+}
+
+// Sharded setup of a row-partition rank, phase 0: the rank's own
+// interior subtrees completely (their updates never leave the subtree), then its
+// interior's partial Schur updates of every separator row (phase B; rank 0 adds the
+// separator rows' near blocks). Phase 1, after the W separator range has been summed
+// over the ranks: the separators themselves, level by level, replicated.
+void setup_sharded(ps_handle* h, cudaStream_t s, int phase) {
+  std::vector<int32_t> own, sep;
+  for (int64_t p = 0; p < h->nl; ++p) {
+    if (h->owner[p] == h->rank) own.push_back((int32_t)p);
+    else if (h->owner[p] < 0) sep.push_back((int32_t)p);
+  }
+  if (phase == 0) {
+    h->d_W.alloc(std::max<int64_t>(h->Wlen, 1));
+    if (h->Wsep_len > 0) CK(cudaMemsetAsync(h->d_W.p + h->Wsep0, 0, sizeof(double2) * h->Wsep_len, s));
+    setup_levels(h, s, own, 0);
+    setup_levels(h, s, sep, 1);
+    CK(cudaStreamSynchronize(s));
+  } else {
+    setup_levels(h, s, sep, 2);
+    setup_finish(h, s);
+  }
+}
+
+ps_status check_setup_opts(ps_handle* h, const ps_setup_opts* opts) {
+  if (h->setup_done) return fail(h, PS_ESTATE, "ps_setup: already set up");
+  if (opts) {
+    if ((opts->ordering != 0 && opts->ordering != 2) || opts->amalgamate_separators != 0)
+      return fail(h, PS_EINVAL, "ps_setup: ordering must be 0 (file ND) or 2 (RCM); amalgamate_separators 0");
+    if (opts->ordering == 2 && h->part_mode)
+      return fail(h, PS_EINVAL, "ps_setup: ordering=2 is not supported with a row partition");
+    if (!(opts->ratio_threshold > 0.0)) return fail(h, PS_EINVAL, "ps_setup: ratio_threshold must be > 0");
+    h->ratio_threshold = opts->ratio_threshold;
+  }
+  return PS_OK;
+}
+
 }  // namespace
 
 // ======================================================================= C ABI
@@ -2614,14 +2784,19 @@ ps_status hm_load(const char* path, const ps_dist* dist, ps_handle** out) {
   std::unique_ptr<ps_handle> h(new ps_handle());
   try {
     std::vector<double2> near_arena, far_arena;
-    read_file(h.get(), path, near_arena, far_arena);
+    const bool part = dist && dist->partition && dist->nranks > 1;
+    h->path = path;
+    read_file(h.get(), path, near_arena, far_arena, /*defer_near=*/part);
     symbolic(h.get());
     if (dist) {
       h->rank = dist->rank;
       h->nranks = dist->nranks;
-      if (dist->partition && dist->nranks > 1) {
+      if (part) {                                    // row partition: this rank's share only
         h->part_mode = 1;
         dist_layout(h.get());
+        std::vector<char> keep;
+        shard_layout(h.get(), keep);
+        load_near(h.get(), keep, near_arena);
       }
     }
     if (dist) {
@@ -2667,68 +2842,65 @@ ps_status hm_load(const char* path, const ps_dist* dist, ps_handle** out) {
 
 ps_status ps_setup(ps_handle* h, const ps_setup_opts* opts) {
   if (!h) return fail(nullptr, PS_EINVAL, "ps_setup: handle is NULL");
-  if (h->setup_done) return fail(h, PS_ESTATE, "ps_setup: already set up");
-  if (opts) {
-    if ((opts->ordering != 0 && opts->ordering != 2) || opts->amalgamate_separators != 0)
-      return fail(h, PS_EINVAL, "ps_setup: ordering must be 0 (file ND) or 2 (RCM); amalgamate_separators 0");
-    if (opts->ordering == 2 && h->part_mode)
-      return fail(h, PS_EINVAL, "ps_setup: ordering=2 is not supported with a row partition");
-    if (!(opts->ratio_threshold > 0.0)) return fail(h, PS_EINVAL, "ps_setup: ratio_threshold must be > 0");
-    h->ratio_threshold = opts->ratio_threshold;
+  if (ps_status st = check_setup_opts(h, opts); st != PS_OK) return st;
+  if (h->part_mode && !h->nccl)
+    return fail(h, PS_ESTATE, "ps_setup: in-process row-partition handle (no NCCL id): use ps_setup_group");
+  try {
+    CK(cudaSetDevice(h->device));
+    cudaStream_t s = h->stream;
+    if (h->part_mode) {
+      setup_sharded(h, s, 0);
+      if (h->Wsep_len > 0)                          // sum the separator rows' partial W over the ranks
+        NCK(nccl_api().allReduce(h->d_W.p + h->Wsep0, h->d_W.p + h->Wsep0, 2 * h->Wsep_len, ncclDouble, ncclSum,
+                                 (ncclComm_t)h->nccl, s));
+      setup_sharded(h, s, 1);
+    } else {
+      if (opts && opts->ordering == 2) reorder_rcm(h, s);
+      h->d_W.alloc(std::max<int64_t>(h->Wlen, 1));
+      std::vector<int32_t> all(h->nl);
+      std::iota(all.begin(), all.end(), 0);
+      setup_levels(h, s, all, 0);
+      setup_finish(h, s);
+    }
+  } catch (const PsError& e) {
+    h->d_W.release();
+    return fail(h, e.st, "ps_setup: " + e.msg);
+  } catch (const std::bad_alloc&) {
+    return fail(h, PS_ENOMEM, "ps_setup: host allocation failed");
+  }
+  return PS_OK;
+}
+
+ps_status ps_setup_group(ps_handle* const* hs, int nranks, const ps_setup_opts* opts) {
+  if (!hs || nranks < 2 || !hs[0]) return fail(nullptr, PS_EINVAL, "ps_setup_group: need nranks >= 2 handles");
+  ps_handle* h = hs[0];
+  for (int g = 0; g < nranks; ++g) {
+    if (!hs[g] || !hs[g]->part_mode || hs[g]->nccl || hs[g]->rank != g || hs[g]->nranks != nranks ||
+        hs[g]->N != h->N || hs[g]->device != h->device || hs[g]->Wsep_len != h->Wsep_len)
+      return fail(h, PS_EINVAL, "ps_setup_group: handles must be ranks 0..nranks-1 of one in-process row partition");
+    if (ps_status st = check_setup_opts(hs[g], opts); st != PS_OK) return st;
   }
   try {
     CK(cudaSetDevice(h->device));
     cudaStream_t s = h->stream;
-    if (opts && opts->ordering == 2) reorder_rcm(h, s);
-    h->d_W.alloc(std::max<int64_t>(h->Wlen, 1));
-    std::vector<std::vector<int32_t>> level_leaves(h->max_height + 1);
-    for (int64_t p = 0; p < h->nl; ++p) level_leaves[h->height[p]].push_back((int32_t)p);
-    DevBuf<int32_t> d_status;
-    d_status.alloc(h->nl);
-    CK(cudaMemsetAsync(d_status.p, 0, sizeof(int32_t) * h->nl, s));
-    std::vector<int32_t> status(h->nl, 0);
-    for (int lev = 0; lev <= h->max_height; ++lev) {
-      SetupLevel sp;
-      build_setup_level(h, level_leaves[lev], sp);
-      // Eq. 21 (left-looking): assemble W_p = [Z~_pp | Z~_p,struct(p)]
-      sp.asmb.launch_all(h->d_W.p, h->d_near.p, h->d_P.p, h->d_W.p, s);
-      // Eqs. 23/30: D_p^{-1}
-      const int64_t nlev = sp.nlev;
-      launch_inverse(nlev, sp.d_ids.p, sp.d_sz.p, sp.d_src.p, sp.d_ld.p, sp.d_dst.p, h->d_W.p, h->d_D.p,
-                     d_status.p, sp.maxn, s);
-      // per-level status slot: leaves of this level write status[0..nlev)
-      CK(cudaMemcpyAsync(status.data(), d_status.p, sizeof(int32_t) * nlev, cudaMemcpyDeviceToHost, s));
+    for (int g = 0; g < nranks; ++g) setup_sharded(hs[g], hs[g]->stream, 0);
+    if (h->Wsep_len > 0) {                          // in-process sum over the ranks, rank order
+      const size_t bytes = sizeof(double2) * h->Wsep_len;
+      DevBuf<double2> acc;
+      acc.alloc(h->Wsep_len);
+      CK(cudaMemcpyAsync(acc.p, h->d_W.p + h->Wsep0, bytes, cudaMemcpyDeviceToDevice, s));
+      for (int g = 1; g < nranks; ++g)
+        launch_add((double*)acc.p, (const double*)(hs[g]->d_W.p + hs[g]->Wsep0), 2 * h->Wsep_len, s);
+      for (int g = 0; g < nranks; ++g)
+        CK(cudaMemcpyAsync(hs[g]->d_W.p + hs[g]->Wsep0, acc.p, bytes, cudaMemcpyDeviceToDevice, s));
       CK(cudaStreamSynchronize(s));
-      for (int64_t i = 0; i < nlev; ++i)
-        if (status[i]) {
-          int32_t p = level_leaves[lev][i];
-          h->d_W.release();
-          return fail(h, PS_ESINGULAR,
-                      "ps_setup: singular scaled diagonal block at elimination position " +
-                          std::to_string(p) + " (leaf " + std::to_string(h->leaf_at[p]) + ")");
-        }
-      // Eq. 16: alpha_p* = -D_p^{-1} Z~_p*
-      sp.panel.launch_all(h->d_P.p, nullptr, h->d_D.p, h->d_W.p, s);
-      CK(cudaStreamSynchronize(s));                  // the level's tables are freed here
     }
-    CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(s));
-    h->d_W.release();
-    h->d_near.release();
-    ensure_far(h, s);
-    h->d_T.alloc(std::max<int64_t>(h->Tlen, 1));
-    h->Tbase = (int64_t)(h->d_T.p - h->d_op.p);
-    chain_setup(h, s);
-    CK(cudaStreamSynchronize(s));
-    static const int shard_env = env_int("PS_SHARD", 1);
-    if (h->part_mode && shard_env) shard_operator(h, s);
-    h->plan.reset();                                  // plans made before setup (ps_apply Z_F) are stale
-    h->dplan.reset();
-    h->setup_done = true;
+    for (int g = 0; g < nranks; ++g) setup_sharded(hs[g], hs[g]->stream, 1);
   } catch (const PsError& e) {
-    return fail(h, e.st, "ps_setup: " + e.msg);
+    for (int g = 0; g < nranks; ++g) hs[g]->d_W.release();
+    return fail(h, e.st, "ps_setup_group: " + e.msg);
   } catch (const std::bad_alloc&) {
-    return fail(h, PS_ENOMEM, "ps_setup: host allocation failed");
+    return fail(h, PS_ENOMEM, "ps_setup_group: host allocation failed");
   }
   return PS_OK;
 }
@@ -3042,6 +3214,8 @@ int ps_info(const ps_handle* h, double* out, int n) {
   v[PS_INFO_OWN_ROWS] = h->part_mode ? (double)h->own_rows : (double)h->N;
   v[PS_INFO_SEP_ROWS] = h->part_mode ? (double)h->Nsep : 0.0;
   v[PS_INFO_OP_BYTES] = 16.0 * ((double)h->d_op.n + (double)h->d_T.n + (double)h->d_farbuf.n);
+  v[PS_INFO_SETUP_BYTES] = 16.0 * ((double)(h->part_mode ? h->near_dev_len : h->near_len) + (double)h->Wlen +
+                                   (double)h->Plen + (double)h->Dlen);
   {
     double nchain = 0, tent = 0;
     for (size_t c = 0; c < h->chains.size(); ++c)

@@ -89,8 +89,6 @@ struct FlowArgs {
                            // narrow WS kernel: scheduler ticket taken, slot handed over), ns
   int32_t narrow;          // 1: narrow 64 x 8 tiles (small nrhs), 0: 32 x 64 tiles
   int32_t mma;             // wide tiles: 0 = DFMA consumer, 1 = FP64 tensor-core (DMMA) consumer
-  int32_t lean_issue;      // narrow WS items: lean operand issue (PS_LEAN_ISSUE, default 1)
-  int32_t issue_first;     // 1: a stage's refill is issued before its compute (PS_ISSUE_FIRST; measured 2-5 % slower)
   int32_t ksplit;          // wide DFMA tiles: 1 = k-split two-column layout (item_body_ks), 0 = one column per lane
 };
 

@@ -80,9 +80,10 @@ using KTabN = KTabT<GN_CHUNK_K>;     // narrow (warp-specialised) items: <= GN_C
 
 constexpr int AS_LD = GM_MT;                // As[k][i]
 constexpr int BS_LD = GM_NT;                // Bs[k][c]
-constexpr int NSTAGE = 3;                   // cp.async pipeline depth
-constexpr int STAGE_A = KC * (GM_MT > GN_MT ? GM_MT : GN_MT);   // both tile geometries fit a stage
-constexpr int STAGE_B = KC * (GM_NT > GN_NT ? GM_NT : GN_NT);
+constexpr int NSTAGE = 4;                   // cp.async pipeline depth (wide tiles)
+constexpr int STAGE_A = KC * GM_MT;
+constexpr int STAGE_B = KC * GM_NT;
+static_assert(NSTAGE * STAGE_A >= GM_MT * GM_NT, "the k-half reductions reuse the A stages");
 
 __device__ __forceinline__ void a_map(bool a_km, int e, int& i, int& k) {
   if (a_km) { k = e & (KC - 1); i = e / KC; } else { i = e % GM_MT; k = e / GM_MT; }
@@ -367,16 +368,6 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
     cp_wait<NSTAGE - 2>();
     __syncthreads();
     const int st = s % NSTAGE;
-    if (a.issue_first) {   // refill the stage computed last iteration before computing this one
-      // refill the stage consumed one iteration ago (all threads are past the barrier above)
-      const int sn = s + NSTAGE - 1;
-      if (sn < nsteps) {
-        const int stn = sn % NSTAGE;
-        issue_a<GM_MT, GM_NT>(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * STAGE_A);
-        issue_b<GM_MT, GM_NT>(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * STAGE_B);
-      }
-      cp_commit();
-    }
     const double2* As = As0 + st * STAGE_A + rbase;
     const double2* Bs = Bs0 + st * STAGE_B + col;
 #pragma unroll
@@ -385,16 +376,14 @@ __device__ __forceinline__ void item_body(const FlowArgs& a, const GWork& w, con
 #pragma unroll
       for (int r = 0; r < RM; ++r) cfma(acc[r], As[k * AS_LD + r], b);
     }
-    if (!a.issue_first) {
-      // refill the stage consumed one iteration ago (all threads are past the barrier above)
-      const int sn = s + NSTAGE - 1;
-      if (sn < nsteps) {
-        const int stn = sn % NSTAGE;
-        issue_a<GM_MT, GM_NT>(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * STAGE_A);
-        issue_b<GM_MT, GM_NT>(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * STAGE_B);
-      }
-      cp_commit();
+    // refill the stage consumed one iteration ago (all threads are past the barrier above)
+    const int sn = s + NSTAGE - 1;
+    if (sn < nsteps) {
+      const int stn = sn % NSTAGE;
+      issue_a<GM_MT, GM_NT>(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * STAGE_A);
+      issue_b<GM_MT, GM_NT>(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * STAGE_B);
     }
+    cp_commit();
   }
   cp_wait<0>();
   __syncthreads();          // all warps done with the stage buffers before the next item
@@ -662,15 +651,6 @@ __device__ __forceinline__ void item_body_dmma(const FlowArgs& a, const GWork& w
     cp_wait<NSTAGE - 2>();
     __syncthreads();
     const int st = s % NSTAGE;
-    if (a.issue_first) {   // refill the stage computed last iteration before computing this one
-      const int sn = s + NSTAGE - 1;
-      if (sn < nsteps) {
-        const int stn = sn % NSTAGE;
-        issue_a<GM_MT, GM_NT>(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * STAGE_A);
-        issue_b<GM_MT, GM_NT>(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * STAGE_B);
-      }
-      cp_commit();
-    }
     const double2* As = As0 + st * STAGE_A + (8 * kh + q) * GM_MT + g;
     const double2* Bs = Bs0 + st * STAGE_B + (8 * kh + q) * GM_NT + 16 * wc + g;
 #pragma unroll
@@ -695,15 +675,13 @@ __device__ __forceinline__ void item_body_dmma(const FlowArgs& a, const GWork& w
           dmma(cim[m][n][0], cim[m][n][1], av[m].y, bv[n].x);
         }
     }
-    if (!a.issue_first) {
-      const int sn = s + NSTAGE - 1;
-      if (sn < nsteps) {
-        const int stn = sn % NSTAGE;
-        issue_a<GM_MT, GM_NT>(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * STAGE_A);
-        issue_b<GM_MT, GM_NT>(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * STAGE_B);
-      }
-      cp_commit();
+    const int sn = s + NSTAGE - 1;
+    if (sn < nsteps) {
+      const int stn = sn % NSTAGE;
+      issue_a<GM_MT, GM_NT>(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * STAGE_A);
+      issue_b<GM_MT, GM_NT>(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * STAGE_B);
     }
+    cp_commit();
   }
   cp_wait<0>();
   __syncthreads();
@@ -762,113 +740,6 @@ __device__ __forceinline__ void item_body_dmma(const FlowArgs& a, const GWork& w
   }
 }
 
-// Narrow tile (small nrhs): 64 rows x 8 columns; thread t owns row t % 64 and
-// columns 2 (t / 64) + {0, 1}. The operator panel is streamed through the same
-// cp.async ring (HBM-bound regime), B values are warp broadcasts.
-template <bool WS, int NS, class KT>
-__device__ __forceinline__ void item_body_narrow(const FlowArgs& a, const GWork& w, const GTask& T,
-                                                 const KT& kt, double2* As0, double2* Bs0, int tid,
-                                                 int* s_last, int64_t* tr, int sa, int sb) {
-  const int i0 = w.mt * GN_MT, c0 = w.nt * GN_NT;
-  const int mm = min(GN_MT, T.m - i0), nn = min(GN_NT, T.n - c0);
-  const int klen = w.kb - w.ka;
-  const int row = tid & (GN_MT - 1), cb = 2 * (tid / GN_MT);
-  int32_t* done = a.counters + 1;
-  const bool a_km = T.a_kmajor != 0, b_km = T.b_kmajor != 0;
-  const int nsteps = (klen + KC - 1) / KC;
-#pragma unroll
-  for (int s = 0; s < NS - 1; ++s)
-    if (s < nsteps) issue_a<GN_MT, GN_NT>(kt, s * KC, klen, i0, mm, a_km, a.A, tid, As0 + s * sa);
-  cp_commit();
-  const double sgn = (double)T.sign;
-  const bool crit_fin = (w.nchunks > 1 && w.crit >= 0 && w.chunk == w.crit);
-  const bool owns_init = (w.nchunks == 1) || (w.crit >= 0 ? w.chunk == w.crit : w.chunk == 0);
-  double2 acc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
-  if (crit_fin) {
-    if constexpr (!WS) wait_group_sum(a, w, tid);
-    const double2* Gs = a.partial + (w.slot + w.crit) * slot_elems(a);
-    acc[0] = __ldcg(Gs + row * GN_NT + cb);
-    acc[1] = __ldcg(Gs + row * GN_NT + cb + 1);
-  }
-  auto load_init = [&]() {    // after the producer's publication when idep >= 0
-    if (owns_init && T.oI >= 0 && row < mm) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e)
-        if (cb + e < nn) {
-          const double2 z = __ldcg(((T.osel & 2) ? (const double2*)a.S : a.I) + T.oI + (int64_t)(i0 + row) * T.sIi + (int64_t)(c0 + cb + e) * T.sIc);
-          acc[e].x += sgn * z.x;
-          acc[e].y += sgn * z.y;
-        }
-    }
-  };
-  if (T.idep < 0) load_init();
-  if constexpr (!WS) {                     // the scheduler warp waited already
-    if (tid < 32) wait_deps(a, w, T, tid);
-    bsync<WS>();
-  }
-  if (T.idep >= 0) load_init();
-  if (tr) tr[3] = gtimer();
-#pragma unroll
-  for (int s = 0; s < NS - 1; ++s) {
-    if (s < nsteps) issue_b<GN_MT, GN_NT>(kt, s * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + s * sb);
-    cp_commit();
-  }
-  const bool live = (row < mm) && (cb < nn);
-  for (int s = 0; s < nsteps; ++s) {
-    cp_wait<NS - 2>();
-    bsync<WS>();
-    const int st = s % NS;
-    if (a.issue_first) {   // refill the stage computed last iteration before computing this one
-      const int sn = s + NS - 1;
-      if (sn < nsteps) {
-        const int stn = sn % NS;
-        issue_a<GN_MT, GN_NT>(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * sa);
-        issue_b<GN_MT, GN_NT>(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * sb);
-      }
-      cp_commit();
-    }
-    if (live) {
-      const double2* As = As0 + st * sa + row;
-      const double2* Bs = Bs0 + st * sb + cb;
-#pragma unroll
-      for (int k = 0; k < KC; ++k) {
-        const double2 av = As[k * GN_MT];
-        cfma(acc[0], av, Bs[k * GN_NT]);
-        cfma(acc[1], av, Bs[k * GN_NT + 1]);
-      }
-    }
-    if (!a.issue_first) {
-      const int sn = s + NS - 1;
-      if (sn < nsteps) {
-        const int stn = sn % NS;
-        issue_a<GN_MT, GN_NT>(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * sa);
-        issue_b<GN_MT, GN_NT>(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * sb);
-      }
-      cp_commit();
-    }
-  }
-  cp_wait<0>();
-  bsync<WS>();
-  if (tr) tr[4] = gtimer();
-  int off[2] = {row * GN_NT + cb, row * GN_NT + cb + 1};
-  bool own[2] = {true, true};
-  const bool finalize = crit_fin ? true : splitk_combine<2, WS>(a, w, acc, off, own, tid, s_last);
-  if (finalize) {
-    if (row < mm) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int col = cb + e;
-        if (col < nn) {
-          const double2 v = make_double2(sgn * acc[e].x, sgn * acc[e].y);   // O = I + sign * sum
-          __stcg(((T.osel & 1) ? a.S : a.O) + T.oO + (int64_t)(i0 + row) * T.sOi + (int64_t)(c0 + col) * T.sOc, v);
-        }
-      }
-    }
-    bsync<WS>();
-    if (tid == 0) red_release(done + T.unit0 + w.nt, 1);
-  }
-}
-
 // Output tile: warp w = (wm, wn) = (w % 4, w / 4) owns rows
 // [wm*RM, min(mm, (wm+1)*RM)) with RM = ceil(mm / 4) <= 8 (so the tile is
 // only as tall as the task) and column wn*32 + lane. A values are broadcast
@@ -918,8 +789,8 @@ flow_kernel(const FlowArgs a) {
     }
     __syncthreads();
     const int mm = min(GM_MT, T.m - w.mt * GM_MT);
-    const int RM = a.narrow ? 0 : (mm + GM_WM - 1) / GM_WM;
-    if (!a.narrow && (a.mma || (T.osel & 4))) {
+    const int RM = (mm + GM_WM - 1) / GM_WM;
+    if (a.mma || (T.osel & 4)) {
       switch ((mm + 7) / 8) {
         case 1: item_body_dmma<1>(a, w, T, kt, As0, Bs0, tid, lane, warp, &s_last, tr); break;
         case 2: item_body_dmma<2>(a, w, T, kt, As0, Bs0, tid, lane, warp, &s_last, tr); break;
@@ -928,7 +799,6 @@ flow_kernel(const FlowArgs a) {
       }
     } else
     switch (RM) {
-      case 0: item_body_narrow<false, NSTAGE>(a, w, T, kt, As0, Bs0, tid, &s_last, tr, STAGE_A, STAGE_B); break;
 #define PS_RM_CASE(R) \
       case R: if (a.ksplit) item_body_ks<R>(a, w, T, kt, As0, Bs0, tid, lane, warp, &s_last, tr); \
               else item_body<R>(a, w, T, kt, As0, Bs0, tid, lane, wm, wn, &s_last, tr); break;
@@ -1382,42 +1252,16 @@ int flow_resident_ctas() {
   if (n == 0) n = resident_of<2>();
   return n;
 }
-// tensor-core (DMMA) tables: one CTA per SM, so the consumer keeps its fragments
-// and accumulator pairs in registers without the 128-register cap
-static int flow1_resident_ctas() {
-  static int n = 0;
-  if (n == 0) n = resident_of<1>();
-  return n;
-}
-
 void launch_flow(const FlowArgs& a, int grid, cudaStream_t st) {
   if (a.nwork <= 0) return;
-  static const bool ws = [] {
-    const char* e = std::getenv("PS_NARROW_WS");
-    return !(e && e[0] == '0');
-  }();
-  if (a.narrow && ws) {
+  if (a.narrow) {                                     // nrhs <= 8: warp-specialised narrow kernel
     int g = grid > 0 ? grid : flow_ws_resident_ctas();
     if (g > a.nwork) g = (int)a.nwork;
     flow_kernel_ws<<<g, 320, FLOW_WS_SMEM, st>>>(a);
     return;
   }
-  static const bool one = [] {
-    const char* e = std::getenv("PS_MMA_1CTA");
-    return e && e[0] == '1';
-  }();
-  if (a.mma && !a.narrow && one) {
-    int g = grid > 0 ? grid : flow1_resident_ctas();
-    if (g > a.nwork) g = (int)a.nwork;
-    flow_kernel<1><<<g, 256, FLOW_SMEM, st>>>(a);
-    return;
-  }
-  static const int grid_env = [] {               // experiments: persistent grid override
-    const char* e = std::getenv("PS_GRID");
-    return e ? std::atoi(e) : 0;
-  }();
   const int resident = flow_resident_ctas();        // also sets the dynamic shared-memory attribute
-  int g = grid > 0 ? grid : (grid_env > 0 ? grid_env : resident);
+  int g = grid > 0 ? grid : resident;
   if (g > a.nwork) g = (int)a.nwork;
   flow_kernel<2><<<g, 256, FLOW_SMEM, st>>>(a);
 }

@@ -20,6 +20,7 @@ torch = pytest.importorskip("torch")
 from hmgen.synth import random_rhs                          # noqa: E402
 from oracle import compute_scaling, read_hm, solve           # noqa: E402
 from paper_2109_04129_b200 import PsError, PsHandle, solve_group  # noqa: E402
+from paper_2109_04129_b200.binding import setup_group             # noqa: E402
 from paper_2109_04129_b200.binding import PS_ESTATE, PS_EINVAL    # noqa: E402
 from tests.conftest import rel_l2_cols                      # noqa: E402
 
@@ -37,9 +38,10 @@ def _host(T):
 
 
 def _group(path, P):
+    """P in-process ranks with the sharded setup (ps_setup_group: each rank factors its
+    own interior subtrees and the separators; separator rows summed over the ranks)."""
     hs = [PsHandle(path, device=0, rank=g, nranks=P, partition=True) for g in range(P)]
-    for h in hs:
-        h.setup()
+    setup_group(hs)
     return hs
 
 
@@ -106,13 +108,17 @@ def test_group_c2_bench_size(cfgdata):
         warnings.simplefilter("ignore")
         solve_group(hs, Bd, Xd)
     assert rel_l2_cols(_host(Xd), ref.x).max() <= TOL
-    # every rank holds only its share of alpha panels, D^-1 and T (the far stacks stay whole)
+    # every rank holds only its share of alpha panels, D^-1 and T (the far stacks stay whole),
+    # and set up only its interior plus the separators (near blocks, W, panels, D^-1)
     h1 = PsHandle(meta["hm"], device=0)
+    i1 = h1.info()
     h1.setup()
     whole = h1.info()["op_bytes"]
     h1.close()
     held = [h.info()["op_bytes"] for h in hs]
     assert max(held) < whole, (held, whole)
+    sb = [h.info()["setup_bytes"] for h in hs]
+    assert max(sb) < i1["setup_bytes"], (sb, i1["setup_bytes"])
     with pytest.raises(PsError) as e:          # per-operator diagnostics need the whole operator
         hs[0].apply(1, Bd, torch.empty_like(Bd))
     assert e.value.status == PS_ESTATE
@@ -128,6 +134,11 @@ def test_group_errors(cfgdata):
     with pytest.raises(PsError) as e:          # an in-process rank has no NCCL communicator
         hs[0].solve(B, X)
     assert e.value.status == PS_ESTATE
+    h2 = PsHandle(path, device=0, rank=0, nranks=2, partition=True)
+    with pytest.raises(PsError) as e:          # ... so its setup is the group's (ps_setup_group)
+        h2.setup()
+    assert e.value.status == PS_ESTATE
+    h2.close()
     with pytest.raises(PsError) as e:          # ranks out of order
         solve_group([hs[1], hs[0]], B, X)
     assert e.value.status == PS_EINVAL

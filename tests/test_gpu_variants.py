@@ -3,14 +3,12 @@
 
   PS_CHAINS=0      sweeps as one dependent hop per elimination-tree level
                    (no chain matrices T_c, DESIGN.md §6 / R23)
-  PS_NARROW_WS=0   nrhs <= 8 through the non-specialised kernel (64 x 8 tile)
   PS_MMA=dmma      every wide table on the FP64 tensor-core consumer
   PS_MMA=dfma      every wide table on the DFMA consumer (far field included)
-  PS_MMA_1CTA=1    tensor-core tables on the one-CTA-per-SM kernel instance
   PS_SOLVE=stages  one launch per operator instead of the single-launch program
   PS_SLOT_BUDGET_MB=-1 partial-slot budget exceeded: the program falls back to task-keyed
                    ticket order (the path C5 takes)
-  PS_LEAN_ISSUE=0  narrow items with the zero-filling operand issue
+  PS_KSPLIT=0      wide DFMA tiles in the one-column-per-lane layout (no k-split)
   PS_DEFER_FIN=0   narrow split-K combine in line (no finisher warp)
   PS_SLOT_REUSE=0  one partial slot per split chunk (no recycling)
 
@@ -52,9 +50,9 @@ def _run(path, nrhs, env, out):
     return np.load(out), np.load(out + ".it.npy")
 
 
-@pytest.mark.parametrize("env", [{"PS_CHAINS": "0"}, {"PS_NARROW_WS": "0"}, {"PS_MMA": "dmma"},
-                                 {"PS_MMA": "dfma"}, {"PS_MMA_1CTA": "1"}, {"PS_SOLVE": "stages"},
-                                 {"PS_SLOT_BUDGET_MB": "-1"}, {"PS_LEAN_ISSUE": "0"}, {"PS_DEFER_FIN": "0"},
+@pytest.mark.parametrize("env", [{"PS_CHAINS": "0"}, {"PS_MMA": "dmma"},
+                                 {"PS_MMA": "dfma"}, {"PS_SOLVE": "stages"},
+                                 {"PS_SLOT_BUDGET_MB": "-1"}, {"PS_KSPLIT": "0"}, {"PS_DEFER_FIN": "0"},
                                  {"PS_SLOT_REUSE": "0"}, {}],
                          ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default")
 @pytest.mark.parametrize("nrhs", [1, 70])
