@@ -245,6 +245,13 @@ int ps_info(const ps_handle* h, double* out, int n);
  * ps_last_error(NULL)). */
 int ps_analyze(const char* path, double* out, int n);
 
+/* ps_analyze_rank — host-only, as ps_analyze for rank `rank` of a row partition over
+ * nranks ranks (nranks = 1: the whole problem): the rank's own rows, separator rows,
+ * and the device bytes its handle would hold (PS_INFO_OP_BYTES after setup,
+ * PS_INFO_SETUP_BYTES during it). The near arena is skipped, not verified.
+ * Returns the number of values written, or -ps_status. */
+int ps_analyze_rank(const char* path, int rank, int nranks, double* out, int n);
+
 /* ps_profile — enable (1) / disable (0) per-launch CUDA-event timing inside
  * ps_solve / ps_apply (events on the launching stream around every kernel;
  * adds a few microseconds per launch, so timed benchmarks run with it off).

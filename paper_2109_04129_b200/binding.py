@@ -92,6 +92,8 @@ def load_library():
     L.ps_profile_read.argtypes = [P, ctypes.POINTER(D), I]
     L.ps_analyze.restype = I
     L.ps_analyze.argtypes = [ctypes.c_char_p, ctypes.POINTER(D), I]
+    L.ps_analyze_rank.restype = I
+    L.ps_analyze_rank.argtypes = [ctypes.c_char_p, I, I, ctypes.POINTER(D), I]
     L.ps_trace.restype = I
     L.ps_trace.argtypes = [P, I]
     L.ps_trace_read.restype = I64
@@ -297,6 +299,16 @@ def setup_group(handles, ratio_threshold: float = 0.1):
     st = L.ps_setup_group(arr, len(handles), ctypes.byref(o))
     if st != PS_OK:
         raise PsError(st, L.ps_last_error(handles[0]._h).decode())
+
+
+def analyze(path: str, rank: int = 0, nranks: int = 1) -> dict:
+    """Host-only ps_analyze_rank: structure and per-rank device bytes of a would-be handle."""
+    L = load_library()
+    out = (ctypes.c_double * len(INFO_KEYS))()
+    n = L.ps_analyze_rank(path.encode(), rank, nranks, out, len(INFO_KEYS))
+    if n < 0:
+        raise PsError(-n, L.ps_last_error(None).decode())
+    return {k: out[i] for i, k in enumerate(INFO_KEYS[:n])}
 
 
 def nccl_unique_id() -> bytes:

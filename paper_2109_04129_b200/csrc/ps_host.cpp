@@ -3047,13 +3047,31 @@ ps_status ps_apply(ps_handle* h, int op, int64_t nrhs, const void* Xin, void* Yo
   return PS_OK;
 }
 
-int ps_analyze(const char* path, double* out, int n) {
-  if (!path || !out || n <= 0) return -PS_EINVAL;
+int ps_analyze(const char* path, double* out, int n) { return ps_analyze_rank(path, 0, 1, out, n); }
+
+int ps_analyze_rank(const char* path, int rank, int nranks, double* out, int n) {
+  if (!path || !out || n <= 0 || nranks < 1 || rank < 0 || rank >= nranks) return -PS_EINVAL;
   ps_handle h;
   try {
     std::vector<double2> near_arena, far_arena;
-    read_file(&h, path, near_arena, far_arena);
+    h.path = path;
+    read_file(&h, path, near_arena, far_arena, /*defer_near=*/true);
     symbolic(&h);
+    if (nranks > 1) {
+      h.rank = rank;
+      h.nranks = nranks;
+      h.part_mode = 1;
+      dist_layout(&h);
+      std::vector<char> keep;
+      shard_layout(&h, keep);
+      h.near_dev_len = 0;
+      for (int64_t b = 0; b < h.nnear; ++b)
+        if (keep[b]) {
+          const int64_t i = h.near_list[3 * b], j = h.near_list[3 * b + 1];
+          h.near_dev_len += (h.leaf_off[i + 1] - h.leaf_off[i]) * (h.leaf_off[j + 1] - h.leaf_off[j]);
+        }
+    }
+    far_layout(&h, far_arena, h.far_host);
   } catch (const PsError& e) {
     g_err = "ps_analyze: " + e.msg;
     return -(int)e.st;
@@ -3213,7 +3231,8 @@ int ps_info(const ps_handle* h, double* out, int n) {
   v[PS_INFO_NRANKS] = h->part_mode ? h->nranks : 1;
   v[PS_INFO_OWN_ROWS] = h->part_mode ? (double)h->own_rows : (double)h->N;
   v[PS_INFO_SEP_ROWS] = h->part_mode ? (double)h->Nsep : 0.0;
-  v[PS_INFO_OP_BYTES] = 16.0 * ((double)h->d_op.n + (double)h->d_T.n + (double)h->d_farbuf.n);
+  v[PS_INFO_OP_BYTES] = 16.0 * ((double)h->Plen + (double)h->Dlen + (double)h->Tlen +
+                                (double)(h->d_farbuf.p ? h->d_farbuf.n : (int64_t)h->far_host.size()));
   v[PS_INFO_SETUP_BYTES] = 16.0 * ((double)(h->part_mode ? h->near_dev_len : h->near_len) + (double)h->Wlen +
                                    (double)h->Plen + (double)h->Dlen);
   {

@@ -141,3 +141,21 @@ def test_chain_pieces_match_definition(case, cfgdata, synthfile):
     assert info["chain_height"] == height
     assert info["T_entries"] == sum(int(sum(S.sizes[p] for p in c)) ** 2 for c in multi)
     assert height < info["height"]           # collapsing chains shortens the dependency path
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_rank_share_of_device_memory(cfgdata, P):
+    """Host-only per-rank analysis of the row partition (ps_analyze_rank): every rank
+    holds less than the single-GPU operator (alpha panels, D^-1, T: far stacks stay
+    whole) and less than the single-GPU setup arenas (near blocks, W, panels, D^-1);
+    the interiors and the separators tile the unknowns."""
+    from paper_2109_04129_b200.binding import analyze
+    path = cfgdata("C2")["hm"]
+    one = analyze(path)
+    ranks = [analyze(path, g, P) for g in range(P)]
+    assert sum(r["own_rows"] for r in ranks) + ranks[0]["sep_rows"] == one["N"]
+    assert all(r["nranks"] == P for r in ranks)
+    assert max(r["setup_bytes"] for r in ranks) < one["setup_bytes"]
+    assert max(r["op_bytes"] for r in ranks) < one["op_bytes"]
+    if P >= 4:                                   # the separators are a minority of the setup
+        assert max(r["setup_bytes"] for r in ranks) < 0.75 * one["setup_bytes"]
