@@ -245,6 +245,16 @@ int ps_info(const ps_handle* h, double* out, int n);
  * ps_last_error(NULL)). */
 int ps_analyze(const char* path, double* out, int n);
 
+/* ps_validate — host-only check of the single-launch solve program for nrhs columns
+ * (the task / segment / work-item tables ps_solve would launch): every
+ * operand access inside its arena, no workspace element written by two tasks, every
+ * read of a written range waiting on exactly that range's writer, and every item's
+ * producers at smaller tickets (deadlock freedom of the persistent kernel). stats
+ * (optional, up to 6): tasks, segments, work items, write ranges, read ranges, the
+ * largest ticket distance to a producer. Returns the number of work items, or
+ * -ps_status (PS_ESTATE: a property is violated; the message names it). */
+int64_t ps_validate(const char* path, int64_t nrhs, int64_t* stats, int nstats);
+
 /* ps_analyze_rank — host-only, as ps_analyze for rank `rank` of a row partition over
  * nranks ranks (nranks = 1: the whole problem): the rank's own rows, separator rows,
  * and the device bytes its handle would hold (PS_INFO_OP_BYTES after setup,

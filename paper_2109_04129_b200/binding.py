@@ -92,6 +92,8 @@ def load_library():
     L.ps_profile_read.argtypes = [P, ctypes.POINTER(D), I]
     L.ps_analyze.restype = I
     L.ps_analyze.argtypes = [ctypes.c_char_p, ctypes.POINTER(D), I]
+    L.ps_validate.restype = I64
+    L.ps_validate.argtypes = [ctypes.c_char_p, I64, P, I]
     L.ps_analyze_rank.restype = I
     L.ps_analyze_rank.argtypes = [ctypes.c_char_p, I, I, ctypes.POINTER(D), I]
     L.ps_trace.restype = I
@@ -309,6 +311,17 @@ def analyze(path: str, rank: int = 0, nranks: int = 1) -> dict:
     if n < 0:
         raise PsError(-n, L.ps_last_error(None).decode())
     return {k: out[i] for i, k in enumerate(INFO_KEYS[:n])}
+
+
+def validate(path: str, nrhs: int) -> dict:
+    """Host-only ps_validate of the solve program for nrhs columns (raises on a violation)."""
+    L = load_library()
+    st = np.zeros(6, dtype=np.int64)
+    n = L.ps_validate(path.encode(), nrhs, st.ctypes.data, 6)
+    if n < 0:
+        raise PsError(-n, L.ps_last_error(None).decode())
+    return dict(items=int(n), tasks=int(st[0]), segments=int(st[1]), work=int(st[2]), write_ranges=int(st[3]),
+                read_ranges=int(st[4]), max_ticket_distance=int(st[5]))
 
 
 def nccl_unique_id() -> bytes:

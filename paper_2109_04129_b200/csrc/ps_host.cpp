@@ -177,7 +177,8 @@ int NARROW_STEPS() {
 int narrow_mode(int64_t R) { return R <= 8 ? 1 : 0; }
 // concurrent work units of a launch (the split-K chunk heuristics aim at about one item
 // per unit per stage) and rows of a tile
-int resident_units(int) { return flow_resident_ctas(); }
+bool g_host_only = false;        // ps_validate: plans built on the host only (no device)
+int resident_units(int) { return g_host_only ? 296 : flow_resident_ctas(); }
 int mode_rows(int mode) { return mode ? GN_MT : GM_MT; }
 
 // A gather-GEMM table: tasks, segments, work items and batches (one launch each).
@@ -593,6 +594,7 @@ struct Table {
 // Per-nrhs solve plan: tables + workspaces.
 struct SolvePlan {
   int64_t nrhs = 0;
+  int64_t ws_len = 0;                      // program workspace (complex entries)
   Table fwd, bwd, dinv, far1, far2;        // per-operator tables (ps_apply, PS_SOLVE=stages)
   Table prog;                              // the whole two-term solve as one dataflow program
   DevBuf<double2> ws;                      // program workspace: Y BO W Z XT X TMP SC (offsets below)
@@ -1176,6 +1178,23 @@ void far_layout(ps_handle* h, const std::vector<double2>& far_arena, std::vector
   const int64_t nf = h->nfar;
   h->fb_ct.assign(nf, 0); h->fb_cs.assign(nf, 0); h->fb_rbt.assign(nf, 0); h->fb_rbs.assign(nf, 0);
   h->fb_dense.assign(nf, -1);
+  // Row partition: a rank keeps only the blocks with a row range (either side) of a leaf
+  // whose far-field rows it computes (far_owner); the others are never read there.
+  std::vector<char> keep(nf, 1);
+  if (h->part_mode) {
+    auto leaf_of_m = [&](int64_t m) {
+      return (int64_t)(std::upper_bound(h->leaf_off.begin(), h->leaf_off.end(), m) - h->leaf_off.begin()) - 1;
+    };
+    auto mine = [&](int64_t a0, int64_t len) {
+      for (int64_t l = leaf_of_m(a0); l < h->nl && h->leaf_off[l] < a0 + len; ++l)
+        if (h->far_owner[h->pos_of[l]] == h->rank) return true;
+      return false;
+    };
+    for (int64_t b = 0; b < nf; ++b) {
+      const int64_t* F = &h->far_list[7 * b];
+      keep[b] = (mine(F[0], F[1]) || mine(F[2], F[3])) ? 1 : 0;
+    }
+  }
   // Blocks stored exactly as dense x I (ACA rank cap, R18) are applied as the
   // dense block D (m x n) itself: multiplying by an exact identity is exact, so
   // this only removes work. D lives after the stacks in the same arena.
@@ -1184,6 +1203,7 @@ void far_layout(ps_handle* h, const std::vector<double2>& far_arena, std::vector
   for (int64_t b = 0; b < nf; ++b) {
     const int64_t* F = &h->far_list[7 * b];
     const int64_t m = F[1], n = F[3], r = F[5], fo = F[6];
+    if (!keep[b]) continue;
     if (r == n && is_identity(&far_arena[fo + m * r], n)) dense_src[b] = 0;
     else if (r == m && is_identity(&far_arena[fo], m)) dense_src[b] = 1;
     if (dense_src[b] >= 0) {
@@ -1196,7 +1216,7 @@ void far_layout(ps_handle* h, const std::vector<double2>& far_arena, std::vector
     const int64_t t = get(F[0], F[1]), c = get(F[2], F[3]), r = F[5];
     h->fb_ct[b] = t;
     h->fb_cs[b] = c;
-    if (dense_src[b] >= 0) continue;
+    if (dense_src[b] >= 0 || !keep[b]) continue;
     h->fb_rbt[b] = h->cl_sr[t];
     h->cl_sr[t] += r;
     h->fb_rbs[b] = h->cl_sr[c];
@@ -1216,6 +1236,7 @@ void far_layout(ps_handle* h, const std::vector<double2>& far_arena, std::vector
   for (int64_t b = 0; b < nf; ++b) {
     const int64_t* F = &h->far_list[7 * b];
     const int64_t m = F[1], n = F[3], r = F[5], fo = F[6];
+    if (!keep[b]) continue;
     if (dense_src[b] == 0) {          // D = U (m x n)
       std::copy(&far_arena[fo], &far_arena[fo] + m * n, &stacked[h->fb_dense[b]]);
       continue;
@@ -1984,11 +2005,157 @@ void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
   SC = sp.oSC + 3 * NR;
   bwd_stage(sp.oXT, sp.oX, s8, s7);                                      // S8
   P.sort_close_bounded();
+  sp.ws_len = 10 * NR + std::max<int64_t>(Ttot, 1);
+  if (g_host_only) return;                           // ps_validate: tables only
   P.upload(h->stream);
-  sp.ws.alloc(10 * NR + std::max<int64_t>(Ttot, 1));
+  sp.ws.alloc(sp.ws_len);
   // the tables were copied from pageable host memory on h->stream (non-blocking):
   // complete them before ps_solve launches the program on the caller's stream
   CK(cudaStreamSynchronize(h->stream));
+}
+
+// Host-only check of a solve program (ps_validate): the properties the persistent
+// dataflow kernel relies on, for every task, segment and work item of the table.
+//   bounds      every operand access lies inside its arena: O / I / B in the
+//               workspace, A inside one operator region (panels, D^-1, far, T);
+//   races       happens-before = the transitive closure of the dependencies (init
+//               producer, segment producers): any two tasks writing one element, and
+//               any task reading a range (segments B, init rows I) and any task
+//               writing into it, are ordered by it — no unordered write/write or
+//               read/write pair, so the kernel has no data race on the workspace;
+//   tickets     every item's producers (and the previous user of its partial slots)
+//               have all their items at smaller tickets: with all CTAs resident the
+//               smallest unfinished ticket can always run (deadlock freedom).
+std::string validate_program(const ps_handle* h, const SolvePlan& sp, std::vector<int64_t>& stats) {
+  const Table& P = sp.prog;
+  const int64_t WS = sp.ws_len;
+  struct Reg { int64_t lo, hi; };
+  const std::vector<Reg> opr = {{h->Pbase, h->Pbase + h->Plen}, {h->Dbase, h->Dbase + h->Dlen},
+                                {h->Fbase, h->Fbase + (int64_t)h->far_host.size()}, {h->Tbase, h->Tbase + h->Tlen}};
+  auto op_ok = [&](int64_t lo, int64_t hi) {
+    for (const Reg& r : opr)
+      if (lo >= r.lo && hi <= r.hi) return true;
+    return false;
+  };
+  auto msg = [](const char* what, int64_t a, int64_t b) {
+    return std::string(what) + " (" + std::to_string(a) + ", " + std::to_string(b) + ")";
+  };
+  struct Iv { int64_t lo, hi; int32_t task; };
+  std::vector<Iv> wr;
+  const int64_t nt = (int64_t)P.tasks.size();
+  // rows of a row-major block: [o + i s, o + i s + n) for i < m (contiguous when s == n)
+  auto rows = [&](int64_t o, int64_t si, int64_t sc, int m, int n, int32_t task, std::vector<Iv>& out) -> bool {
+    if (sc != 1) return false;
+    if (si == n) { out.push_back({o, o + (int64_t)m * n, task}); return true; }
+    for (int i = 0; i < m; ++i) out.push_back({o + i * si, o + i * si + n, task});
+    return true;
+  };
+  for (int64_t t = 0; t < nt; ++t) {
+    const GTask& T = P.tasks[t];
+    if (T.osel & 3) return msg("task addresses the scratch base (not used by the program)", t, T.osel);
+    if (!rows(T.oO, T.sOi, T.sOc, T.m, T.n, (int32_t)t, wr)) return msg("non-unit column stride of O", t, T.sOc);
+  }
+  for (const Iv& v : wr)
+    if (v.lo < 0 || v.hi > WS) return msg("write outside the workspace", v.task, v.lo);
+  std::sort(wr.begin(), wr.end(), [](const Iv& a, const Iv& b) { return a.lo < b.lo; });
+  // happens-before: b (transitively) waits on a through init / segment dependencies
+  std::vector<std::vector<int32_t>> deps(nt);
+  for (int64_t t = 0; t < nt; ++t) {
+    const GTask& T = P.tasks[t];
+    if (T.idep >= 0) deps[t].push_back(T.idep);
+    for (int32_t k = T.t0; k < T.t1; ++k)
+      if (P.terms[k].dep >= 0) deps[t].push_back(P.terms[k].dep);
+  }
+  std::vector<int64_t> seen(nt, -1);
+  int64_t gen = 0;
+  std::vector<int32_t> stack;
+  auto before = [&](int32_t a, int32_t b) -> bool {  // a happens before b
+    if (a == b) return false;
+    ++gen;
+    stack.assign(1, b);
+    while (!stack.empty()) {
+      const int32_t x = stack.back();
+      stack.pop_back();
+      for (int32_t d : deps[x]) {
+        if (d == a) return true;
+        if (d > a && seen[d] != gen) { seen[d] = gen; stack.push_back(d); }   // producers have smaller ids
+      }
+    }
+    return false;
+  };
+  auto ordered = [&](int32_t a, int32_t b) { return a == b || before(a, b) || before(b, a); };
+  {
+    std::vector<Iv> open_;                               // sweep over sorted starts
+    for (const Iv& v : wr) {
+      open_.erase(std::remove_if(open_.begin(), open_.end(), [&](const Iv& o) { return o.hi <= v.lo; }), open_.end());
+      for (const Iv& o : open_)
+        if (!ordered(o.task, v.task)) return msg("two unordered tasks write one element", o.task, v.task);
+      open_.push_back(v);
+    }
+  }
+  // writers overlapping [lo, hi)
+  auto writers = [&](int64_t lo, int64_t hi, std::vector<int32_t>& out) {
+    out.clear();
+    auto it = std::upper_bound(wr.begin(), wr.end(), lo, [](int64_t x, const Iv& v) { return x < v.lo; });
+    if (it != wr.begin()) --it;
+    for (; it != wr.end() && it->lo < hi; ++it)
+      if (it->hi > lo) out.push_back(it->task);
+  };
+  std::vector<int32_t> ws;
+  std::vector<Iv> rd;
+  int64_t nread = 0;
+  for (int64_t t = 0; t < nt; ++t) {
+    const GTask& T = P.tasks[t];
+    if (T.oI >= 0) {
+      rd.clear();
+      if (!rows(T.oI, T.sIi, T.sIc, T.m, T.n, (int32_t)t, rd)) return msg("non-unit column stride of I", t, T.sIc);
+      for (const Iv& v : rd) {
+        if (v.lo < 0 || v.hi > WS) return msg("init read outside the workspace", t, v.lo);
+        writers(v.lo, v.hi, ws);
+        for (int32_t w : ws)
+          if (!ordered(w, (int32_t)t)) return msg("init rows written by a task unordered with the reader", t, w);
+        ++nread;
+      }
+    }
+    for (int32_t k = T.t0; k < T.t1; ++k) {
+      const GTerm& g = P.terms[k];
+      if (g.bsel & 1) return msg("segment addresses the scratch base", t, k);
+      const int64_t alo = g.oA, ahi = g.oA + (int64_t)(g.K - 1) * g.sAk + (int64_t)(T.m - 1) * g.sAi + 1;
+      if (g.sAk < 0 || g.sAi < 0 || !op_ok(alo, ahi)) return msg("operator read outside its region", t, k);
+      rd.clear();
+      if (!rows(g.oB, g.sBk, g.sBc, g.K, T.n, (int32_t)t, rd)) return msg("non-unit column stride of B", t, k);
+      for (const Iv& v : rd) {
+        if (v.lo < 0 || v.hi > WS) return msg("segment read outside the workspace", t, k);
+        writers(v.lo, v.hi, ws);
+        for (int32_t w : ws)
+          if (!ordered(w, (int32_t)t)) return msg("segment rows written by a task unordered with the reader", t, w);
+        ++nread;
+      }
+    }
+  }
+  // ticket order
+  const int64_t nw = (int64_t)P.work.size();
+  std::vector<int64_t> last(nt, -1);
+  for (int64_t i = 0; i < nw; ++i) last[P.work[i].task] = std::max(last[P.work[i].task], i);
+  std::vector<int32_t> unit_task(std::max<int32_t>(P.max_units, 1), -1);
+  for (int64_t t = 0; t < nt; ++t)
+    for (int32_t u = 0; u < (P.tasks[t].n + P.NT() - 1) / P.NT(); ++u) unit_task[P.tasks[t].unit0 + u] = (int32_t)t;
+  int64_t max_back = 0;
+  for (int64_t i = 0; i < nw; ++i) {
+    const GWork& w = P.work[i];
+    const GTask& T = P.tasks[w.task];
+    auto need_before = [&](int32_t task) -> bool {
+      if (task < 0) return true;
+      max_back = std::max(max_back, i - last[task]);
+      return last[task] < i;
+    };
+    if (!need_before(T.idep)) return msg("item precedes its init producer", i, T.idep);
+    for (int32_t k = w.ta; k < w.tb; ++k)
+      if (!need_before(P.terms[k].dep)) return msg("item precedes a segment producer", i, P.terms[k].dep);
+    if (w.sw_unit >= 0 && !need_before(unit_task[w.sw_unit])) return msg("item precedes its slots' previous user", i, w.sw_unit);
+  }
+  stats = {nt, (int64_t)P.terms.size(), nw, (int64_t)wr.size(), nread, max_back};
+  return "";
 }
 
 bool use_stages() {
@@ -3048,6 +3215,54 @@ ps_status ps_apply(ps_handle* h, int op, int64_t nrhs, const void* Xin, void* Yo
 }
 
 int ps_analyze(const char* path, double* out, int n) { return ps_analyze_rank(path, 0, 1, out, n); }
+
+int64_t ps_validate(const char* path, int64_t nrhs, int64_t* stats, int nstats) {
+  if (!path || nrhs < 1) return -PS_EINVAL;
+  ps_handle h;
+  try {
+    std::vector<double2> near_arena, far_arena;
+    h.path = path;
+    read_file(&h, path, near_arena, far_arena, /*defer_near=*/true);
+    symbolic(&h);
+    far_layout(&h, far_arena, h.far_host);
+    h.Pbase = 0;
+    h.Dbase = h.Plen;
+    h.Fbase = h.Plen + h.Dlen;
+    h.Tbase = h.Fbase + (int64_t)h.far_host.size();
+    SolvePlan sp;
+    g_host_only = true;
+    build_program(&h, sp, nrhs);
+    g_host_only = false;
+    // PS_VALIDATE_BREAK (tests of the checker itself): 1 drops one segment dependency,
+    // 2 moves the last work item to the front, 3 pushes one operator offset out of its region
+    static const int brk = env_int("PS_VALIDATE_BREAK", 0);
+    Table& Pt = sp.prog;
+    if (brk == 1) {
+      for (GTerm& g : Pt.terms)
+        if (g.dep >= 0) { g.dep = -1; break; }
+    } else if (brk == 2 && Pt.work.size() > 1) {
+      std::rotate(Pt.work.begin(), Pt.work.end() - 1, Pt.work.end());
+    } else if (brk == 3 && !Pt.terms.empty()) {
+      Pt.terms.back().oA = h.Tbase + h.Tlen + 1;
+    }
+    std::vector<int64_t> st;
+    const std::string e = validate_program(&h, sp, st);
+    if (!e.empty()) {
+      g_err = "ps_validate: " + e;
+      return -PS_ESTATE;
+    }
+    for (int i = 0; i < nstats && i < (int)st.size(); ++i) stats[i] = st[i];
+    return (int64_t)sp.prog.work.size();
+  } catch (const PsError& e) {
+    g_host_only = false;
+    g_err = "ps_validate: " + e.msg;
+    return -(int64_t)e.st;
+  } catch (const std::bad_alloc&) {
+    g_host_only = false;
+    g_err = "ps_validate: host allocation failed";
+    return -PS_ENOMEM;
+  }
+}
 
 int ps_analyze_rank(const char* path, int rank, int nranks, double* out, int n) {
   if (!path || !out || n <= 0 || nranks < 1 || rank < 0 || rank >= nranks) return -PS_EINVAL;

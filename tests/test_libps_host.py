@@ -159,3 +159,39 @@ def test_rank_share_of_device_memory(cfgdata, P):
     assert max(r["op_bytes"] for r in ranks) < one["op_bytes"]
     if P >= 4:                                   # the separators are a minority of the setup
         assert max(r["setup_bytes"] for r in ranks) < 0.75 * one["setup_bytes"]
+
+
+@pytest.mark.parametrize("name,nrhs", [("C1", 1), ("C1", 9), ("C1", 70), ("T2", 181), ("C2", 1), ("C2", 181),
+                                       ("C3", 1), ("C4", 360)])
+def test_solve_program_is_race_and_deadlock_free(cfgdata, name, nrhs):
+    """ps_validate (host-only) on the exact tables ps_solve launches: every operand
+    access inside its arena; every pair of tasks writing one workspace element, and
+    every reader / writer pair of a range, ordered by the dependency graph
+    (happens-before) — no data race; every item's producers at smaller tickets —
+    no deadlock of the persistent kernel. (compute-sanitizer is closed on this
+    pool: this is the race / bounds evidence for the dataflow program.)"""
+    from paper_2109_04129_b200.binding import validate
+    r = validate(cfgdata(name)["hm"], nrhs)
+    assert r["items"] > 0 and r["read_ranges"] >= r["segments"]
+
+
+def test_solve_program_edge_cases_validate(synthfile):
+    from paper_2109_04129_b200.binding import validate
+    for kw in (dict(n_points=300, seed=1, clustered=True), dict(n_points=40, seed=2)):
+        path = synthfile(**kw)[0]
+        for nrhs in (1, 8, 64, 65):
+            validate(path, nrhs)
+
+
+@pytest.mark.parametrize("brk,what", [(1, "unordered"), (2, "precedes"), (3, "outside its region")])
+def test_validator_catches_broken_tables(cfgdata, brk, what):
+    """The checker itself: a dropped dependency, an item moved before its producer and
+    an operator offset outside its region are each reported."""
+    import subprocess
+    import sys
+    path = cfgdata("C1")["hm"]
+    code = ("from paper_2109_04129_b200.binding import validate\n"
+            f"validate({path!r}, 1)\n")
+    env = dict(os.environ, PS_VALIDATE_BREAK=str(brk))
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=120)
+    assert r.returncode != 0 and what in r.stderr, r.stderr[-500:]
