@@ -53,25 +53,28 @@ struct PsError {
                     std::string(#x) + ": " + cudaGetErrorString(e_)};                           \
   } while (0)
 
+// Device buffer; alloc() keeps the allocation when it is large enough (tables rebuilt
+// level by level in ps_setup reuse their buffers instead of a cudaMalloc / cudaFree pair each).
 template <class T>
 struct DevBuf {
   T* p = nullptr;
-  int64_t n = 0;
+  int64_t n = 0, cap = 0;
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), cap(o.cap) { o.p = nullptr; o.n = o.cap = 0; }
   DevBuf& operator=(DevBuf&& o) noexcept {
-    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    if (this != &o) { release(); p = o.p; n = o.n; cap = o.cap; o.p = nullptr; o.n = o.cap = 0; }
     return *this;
   }
   ~DevBuf() { release(); }
   void release() {
     if (p) cudaFree(p);
     p = nullptr;
-    n = 0;
+    n = cap = 0;
   }
   void alloc(int64_t count) {
+    if (p && count > 0 && count <= cap) { n = count; return; }
     release();
     if (count <= 0) return;
     const cudaError_t e = cudaMalloc(&p, sizeof(T) * (size_t)count);
@@ -85,7 +88,7 @@ struct DevBuf {
                         " MiB failed (" + cudaGetErrorString(e) + "; " + std::to_string(fr >> 20) + " of " +
                         std::to_string(tot >> 20) + " MiB free)"};
     }
-    n = count;
+    n = cap = count;
   }
   void upload(const std::vector<T>& v, cudaStream_t st) {
     alloc((int64_t)v.size());
@@ -252,6 +255,14 @@ struct Table {
     }
   }
   bool late_keys_used = false;
+  // empty the table for a new level, keeping its device buffers (ps_setup)
+  void reset_keep_device() {
+    Table f;
+    f.d_tasks = std::move(d_tasks); f.d_terms = std::move(d_terms); f.d_work = std::move(d_work);
+    f.d_counters = std::move(d_counters); f.d_partial = std::move(d_partial);
+    f.S = S; f.narrow = narrow; f.chunk_steps = chunk_steps; f.mma = mma;
+    *this = std::move(f);
+  }
   int MT() const { return narrow ? GN_MT : GM_MT; }
   int64_t slot_elems() const { return narrow ? (int64_t)GN_MT * GN_NT : (int64_t)GM_MT * GM_NT; }
   int NT() const { return narrow ? GN_NT : GM_NT; }
@@ -1276,6 +1287,13 @@ struct SetupLevel {
   DevBuf<int64_t> d_src, d_ld, d_dst;
   int64_t nlev = 0;
   int maxn = 0;
+  void reset() {
+    asmb.reset_keep_device();
+    panel.reset_keep_device();
+    asmb.S = panel.S = nullptr;
+    nlev = 0;
+    maxn = 0;
+  }
 };
 
 // mode 0: every descendant's update, near-block init (the whole tree on one rank, or a
@@ -2852,15 +2870,22 @@ ps_status finish_dist(ps_handle* const* hs, int nh, int64_t nrhs, const void* B,
 // the scaled diagonal blocks (Eqs. 23, 30) and form the alpha panels (Eq. 16).
 void setup_levels(ps_handle* h, cudaStream_t s, const std::vector<int32_t>& pos, int mode) {
   if (pos.empty()) return;
+  using clk = std::chrono::steady_clock;
+  static const int verbose = env_int("PS_VERBOSE", 0);
+  double t_build = 0, t_wait = 0;
+  const auto t00 = clk::now();
   std::vector<std::vector<int32_t>> lv(h->max_height + 1);
   for (int32_t p : pos) lv[mode == 1 ? 0 : h->height[p]].push_back(p);   // phase B: one batch
   DevBuf<int32_t> d_status;
   d_status.alloc(std::max<int64_t>((int64_t)pos.size(), 1));
   std::vector<int32_t> status;
+  SetupLevel sp;                                     // device buffers reused level to level
   for (const auto& leaves : lv) {
     if (leaves.empty()) continue;
-    SetupLevel sp;
+    sp.reset();
+    const auto t0 = clk::now();
     build_setup_level(h, leaves, sp, mode);
+    t_build += std::chrono::duration<double>(clk::now() - t0).count();
     // Eq. 21 (left-looking): assemble W_p = [Z~_pp | Z~_p,struct(p)]
     sp.asmb.launch_all(h->d_W.p, h->d_near.p, h->d_P.p, h->d_W.p, s);
     if (mode != 1) {
@@ -2871,7 +2896,9 @@ void setup_levels(ps_handle* h, cudaStream_t s, const std::vector<int32_t>& pos,
                      d_status.p, sp.maxn, s);
       status.assign(nlev, 0);
       CK(cudaMemcpyAsync(status.data(), d_status.p, sizeof(int32_t) * nlev, cudaMemcpyDeviceToHost, s));
+      const auto t1 = clk::now();
       CK(cudaStreamSynchronize(s));
+      t_wait += std::chrono::duration<double>(clk::now() - t1).count();
       for (int64_t i = 0; i < nlev; ++i)
         if (status[i])
           throw PsError{PS_ESINGULAR, "singular scaled diagonal block at elimination position " +
@@ -2880,8 +2907,14 @@ void setup_levels(ps_handle* h, cudaStream_t s, const std::vector<int32_t>& pos,
       // Eq. 16: alpha_p* = -D_p^{-1} Z~_p*
       sp.panel.launch_all(h->d_P.p, nullptr, h->d_D.p, h->d_W.p, s);
     }
+    const auto t1 = clk::now();
     CK(cudaStreamSynchronize(s));                    // the level's tables are freed here
+    t_wait += std::chrono::duration<double>(clk::now() - t1).count();
   }
+  if (verbose)
+    std::fprintf(stderr, "[ps] setup mode %d: %zu positions, %.1f ms (host tables %.1f ms, waiting on the GPU %.1f ms)\n",
+                 mode, pos.size(), 1e3 * std::chrono::duration<double>(clk::now() - t00).count(), 1e3 * t_build,
+                 1e3 * t_wait);
 }
 
 // After the scaling: free the setup-only arenas, upload the far stacks, form T_c.

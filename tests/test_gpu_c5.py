@@ -151,9 +151,10 @@ def test_c5_residual_pins():
     tF = torch.empty_like(Bd)
     h.apply(PS_OP_ZF, y0, tF)
     x, y0h, tFh = _host(Xd), _host(y0), _host(tF)
+    hm = st["meta"]["hm"]
     h.close()
     _state.clear()
-    H = read_hm(st["meta"]["hm"], mmap=True)
+    H = read_hm(hm, mmap=True)
     r0 = rel_l2_cols(_near_apply(H, y0h), B)
     r1 = np.linalg.norm(_near_apply(H, x) - (B - tFh), axis=0) / np.linalg.norm(B, axis=0)
     print(f"C5 N={H.N}: ||Z_N y0 - b||/||b|| = {r0.max():.3e}, ||Z_N x - (b - Z_F y0)||/||b|| = {r1.max():.3e}")
