@@ -53,6 +53,27 @@ struct PsError {
                     std::string(#x) + ": " + cudaGetErrorString(e_)};                           \
   } while (0)
 
+// Pinned host staging of a handle's table uploads: a cudaMemcpyAsync from pageable
+// memory synchronises the stream and stages / pins the pages on every call (measured
+// 16-500 ms of a C2 setup); copying through one pinned ring keeps the uploads cheap and
+// asynchronous. All copies of a ring go to one stream (the handle's), so the event of
+// the latest copy covers every earlier one when the ring wraps.
+struct PinnedRing {
+  char* p = nullptr;
+  size_t cap = 0, off = 0;
+  cudaEvent_t ev = nullptr;
+  bool pending = false;
+  PinnedRing() = default;
+  PinnedRing(const PinnedRing&) = delete;
+  PinnedRing& operator=(const PinnedRing&) = delete;
+  ~PinnedRing() {
+    if (pending) cudaEventSynchronize(ev);
+    if (p) cudaFreeHost(p);
+    if (ev) cudaEventDestroy(ev);
+  }
+  void copy(void* dst, const void* src, size_t bytes, cudaStream_t st);
+};
+
 // Device buffer; alloc() keeps the allocation when it is large enough (tables rebuilt
 // level by level in ps_setup reuse their buffers instead of a cudaMalloc / cudaFree pair each).
 template <class T>
@@ -90,11 +111,35 @@ struct DevBuf {
     }
     n = cap = count;
   }
-  void upload(const std::vector<T>& v, cudaStream_t st) {
+  void upload(const std::vector<T>& v, cudaStream_t st, PinnedRing* ring = nullptr) {
     alloc((int64_t)v.size());
-    if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, st));
+    if (v.empty()) return;
+    if (ring) ring->copy(p, v.data(), sizeof(T) * v.size(), st);
+    else CK(cudaMemcpyAsync(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, st));
   }
 };
+
+void PinnedRing::copy(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return;
+  const size_t need = (bytes + 255) & ~(size_t)255;
+  if (need > cap || off + need > cap) {                 // wrap or grow: the ring's copies must be done
+    if (pending) CK(cudaEventSynchronize(ev));
+    pending = false;
+    off = 0;
+    if (need > cap) {
+      if (p) CK(cudaFreeHost(p));
+      p = nullptr;
+      cap = std::max<size_t>(need, std::max<size_t>(2 * cap, (size_t)64 << 20));
+      CK(cudaMallocHost(&p, cap));
+    }
+  }
+  if (!ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  std::memcpy(p + off, src, bytes);
+  CK(cudaMemcpyAsync(dst, p + off, bytes, cudaMemcpyHostToDevice, st));
+  CK(cudaEventRecord(ev, st));
+  pending = true;
+  off += need;
+}
 
 uint64_t checksum64(const uint8_t* b, size_t nbytes) {
   uint64_t h = 0;
@@ -507,7 +552,7 @@ struct Table {
     }
   }
   double alg_flops = 0, alg_bytes = 0;   // useful flops / operator (A) bytes of one full pass
-  void upload(cudaStream_t st) {
+  void upload(cudaStream_t st, PinnedRing* ring = nullptr) {
     alg_flops = alg_bytes = 0;
     for (const GTask& t : tasks)
       for (int32_t k = t.t0; k < t.t1; ++k) {
@@ -536,9 +581,9 @@ struct Table {
         g.bsel = (g.bsel & 1) | (P.n_mt << 1) | (int32_t)((uint32_t)ntp_of(P) << 16);
         g.dep = P.unit0;
       }
-    d_tasks.upload(dtasks, st);
-    d_terms.upload(dterms, st);
-    d_work.upload(work, st);
+    d_tasks.upload(dtasks, st, ring);
+    d_terms.upload(dterms, st, ring);
+    d_work.upload(work, st, ring);
     d_counters.alloc(1 + (int64_t)max_units + max_tiles);
     d_partial.alloc(std::max<int64_t>(max_slots, 1) * slot_elems());
     static const int verbose = env_int("PS_VERBOSE", 0);
@@ -702,6 +747,7 @@ struct ps_handle {
   int64_t near_file_off = -1;              // byte offset of the near arena in the .hm file (deferred read)
   uint64_t near_file_ck = 0;
   std::string path;
+  PinnedRing ring;                         // pinned staging of the table uploads (h->stream)
   std::vector<int32_t> owner, far_owner;   // per position: interior rank (-1 separator); far-row rank
   std::vector<int64_t> doff;               // first row of position p in the partitioned layout:
                                            // [rank 0 interior | ... | rank P-1 interior | separators],
@@ -1287,6 +1333,7 @@ struct SetupLevel {
   DevBuf<int64_t> d_src, d_ld, d_dst;
   int64_t nlev = 0;
   int maxn = 0;
+  double t_upload = 0;
   void reset() {
     asmb.reset_keep_device();
     panel.reset_keep_device();
@@ -1360,8 +1407,10 @@ void build_setup_level(ps_handle* h, const std::vector<int32_t>& leaves, SetupLe
     }
     sp.panel.close_batch();
   }
-  sp.asmb.upload(h->stream);
-  sp.panel.upload(h->stream);
+  const auto tu0 = std::chrono::steady_clock::now();
+  sp.asmb.upload(h->stream, &h->ring);
+  sp.panel.upload(h->stream, &h->ring);
+  sp.t_upload = std::chrono::duration<double>(std::chrono::steady_clock::now() - tu0).count();
   std::vector<int32_t> sz;
   std::vector<int64_t> src, ld, dst;
   for (int32_t p : leaves) {
@@ -1372,11 +1421,11 @@ void build_setup_level(ps_handle* h, const std::vector<int32_t>& leaves, SetupLe
     sp.maxn = std::max(sp.maxn, h->nsz[p]);
   }
   sp.nlev = (int64_t)leaves.size();
-  sp.d_ids.upload(leaves, h->stream);
-  sp.d_sz.upload(sz, h->stream);
-  sp.d_src.upload(src, h->stream);
-  sp.d_ld.upload(ld, h->stream);
-  sp.d_dst.upload(dst, h->stream);
+  sp.d_ids.upload(leaves, h->stream, &h->ring);
+  sp.d_sz.upload(sz, h->stream, &h->ring);
+  sp.d_src.upload(src, h->stream, &h->ring);
+  sp.d_ld.upload(ld, h->stream, &h->ring);
+  sp.d_dst.upload(dst, h->stream, &h->ring);
 }
 
 // Upload the restacked far factors (once) and point Fbase at them.
@@ -1722,7 +1771,7 @@ void build_solve_plan(ps_handle* h, SolvePlan& sp, int64_t nrhs) {
     sp.far2.tile(t);
   }
   sp.far2.close_batch();
-  for (Table* tb : {&sp.fwd, &sp.bwd, &sp.dinv, &sp.far1, &sp.far2}) tb->upload(h->stream);
+  for (Table* tb : {&sp.fwd, &sp.bwd, &sp.dinv, &sp.far1, &sp.far2}) tb->upload(h->stream, &h->ring);
   const int64_t NR = h->N * R;
   sp.y.alloc(NR); sp.bo.alloc(NR); sp.w.alloc(NR); sp.u.alloc(NR); sp.xt.alloc(NR);
   sp.wm.alloc(NR + std::max<int64_t>(T, 1)); sp.tm.alloc(NR);
@@ -2025,7 +2074,7 @@ void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
   P.sort_close_bounded();
   sp.ws_len = 10 * NR + std::max<int64_t>(Ttot, 1);
   if (g_host_only) return;                           // ps_validate: tables only
-  P.upload(h->stream);
+  P.upload(h->stream, &h->ring);
   sp.ws.alloc(sp.ws_len);
   // the tables were copied from pageable host memory on h->stream (non-blocking):
   // complete them before ps_solve launches the program on the caller's stream
@@ -2657,7 +2706,7 @@ void build_dist_plan(ps_handle* h, DistPlan& dp, int64_t R) {
   dp.far2.close_batch();
   for (Table* tb : {&dp.fwdIA, &dp.fwdSA, &dp.dinvA, &dp.bwdA, &dp.far1, &dp.far2, &dp.fwdIC, &dp.fwdSC,
                     &dp.dinvC, &dp.bwdC})
-    tb->upload(h->stream);
+    tb->upload(h->stream, &h->ring);
   dp.ws.alloc(7 * NP + std::max<int64_t>(Ttot, 1));
   CK(cudaMemsetAsync(dp.ws.p, 0, sizeof(double2) * dp.ws.n, h->stream));   // padding rows stay 0
   dp.nchI = (h->own_rows + dp.rpc - 1) / dp.rpc;
@@ -2872,7 +2921,7 @@ void setup_levels(ps_handle* h, cudaStream_t s, const std::vector<int32_t>& pos,
   if (pos.empty()) return;
   using clk = std::chrono::steady_clock;
   static const int verbose = env_int("PS_VERBOSE", 0);
-  double t_build = 0, t_wait = 0;
+  double t_build = 0, t_wait = 0, t_up = 0;
   const auto t00 = clk::now();
   std::vector<std::vector<int32_t>> lv(h->max_height + 1);
   for (int32_t p : pos) lv[mode == 1 ? 0 : h->height[p]].push_back(p);   // phase B: one batch
@@ -2886,6 +2935,7 @@ void setup_levels(ps_handle* h, cudaStream_t s, const std::vector<int32_t>& pos,
     const auto t0 = clk::now();
     build_setup_level(h, leaves, sp, mode);
     t_build += std::chrono::duration<double>(clk::now() - t0).count();
+    t_up += sp.t_upload;
     // Eq. 21 (left-looking): assemble W_p = [Z~_pp | Z~_p,struct(p)]
     sp.asmb.launch_all(h->d_W.p, h->d_near.p, h->d_P.p, h->d_W.p, s);
     if (mode != 1) {
@@ -2912,9 +2962,9 @@ void setup_levels(ps_handle* h, cudaStream_t s, const std::vector<int32_t>& pos,
     t_wait += std::chrono::duration<double>(clk::now() - t1).count();
   }
   if (verbose)
-    std::fprintf(stderr, "[ps] setup mode %d: %zu positions, %.1f ms (host tables %.1f ms, waiting on the GPU %.1f ms)\n",
-                 mode, pos.size(), 1e3 * std::chrono::duration<double>(clk::now() - t00).count(), 1e3 * t_build,
-                 1e3 * t_wait);
+    std::fprintf(stderr, "[ps] setup mode %d: %zu positions, %.1f ms (host tables %.1f ms of which uploads %.1f ms, "
+                 "waiting on the GPU %.1f ms)\n", mode, pos.size(), 1e3 * std::chrono::duration<double>(clk::now() - t00).count(),
+                 1e3 * t_build, 1e3 * t_up, 1e3 * t_wait);
 }
 
 // After the scaling: free the setup-only arenas, upload the far stacks, form T_c.
