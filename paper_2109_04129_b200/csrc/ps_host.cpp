@@ -300,30 +300,6 @@ struct Table {
     }
   }
   bool late_keys_used = false;
-  // Ticket order by critical path (HLFET list scheduling): an item's key is minus the
-  // longest estimated time from its task to the end of the launch (its own items plus
-  // the longest chain of consumers), so the critical path is handed out first and bulk
-  // work fills the gaps, and a consumer off the critical path sits far behind its
-  // producers in the ticket order (it rarely waits). Producers always have the larger
-  // bottom level, so the order stays topological (deadlock-free, checked by
-  // ps_validate). Cost of an item ~ its operator entries plus a fixed item overhead.
-  void critical_path_keys() {
-    const int64_t nt = (int64_t)tasks.size();
-    std::vector<double> cost(nt, 0.0), bl(nt, 0.0), best(nt, 0.0);
-    static const double over = env_int("PS_PRIO_OVERHEAD", 4096);   // operator entries per item
-    for (const GWork& w : work) {
-      const GTask& T = tasks[w.task];
-      cost[w.task] += (double)std::min(MT(), T.m - w.mt * MT()) * (w.kb - w.ka) + over;
-    }
-    for (int64_t t = nt - 1; t >= 0; --t) {           // consumers have larger task ids
-      bl[t] = cost[t] + best[t];
-      const GTask& T = tasks[t];
-      if (T.idep >= 0) best[T.idep] = std::max(best[T.idep], bl[t]);
-      for (int32_t k = T.t0; k < T.t1; ++k)
-        if (terms[k].dep >= 0) best[terms[k].dep] = std::max(best[terms[k].dep], bl[t]);
-    }
-    for (size_t i = 0; i < work.size(); ++i) keys[i] = keys_late[i] = -bl[work[i].task];
-  }
   // empty the table for a new level, keeping its device buffers (ps_setup)
   void reset_keep_device() {
     Table f;
@@ -2095,8 +2071,6 @@ void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
   dinv_stage(sp.oZ, sp.oXT, sp.oBO, -1, s7, zfin, &s2);                  // S7: xt = bo - D^-1 z
   SC = sp.oSC + 3 * NR;
   bwd_stage(sp.oXT, sp.oX, s8, s7);                                      // S8
-  static const int prio = env_int("PS_PRIO", 1);
-  if (prio) P.critical_path_keys();
   P.sort_close_bounded();
   sp.ws_len = 10 * NR + std::max<int64_t>(Ttot, 1);
   if (g_host_only) return;                           // ps_validate: tables only
