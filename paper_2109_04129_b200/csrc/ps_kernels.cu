@@ -107,9 +107,13 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// swz: the tensor-core consumer's stages are XOR-swizzled — element (k, i) of a stage at
+// k LD + (i ^ 2 (k mod 4)) — so its fragment loads (lane (g, q) reads row g of k-row q) hit
+// 8 distinct 16-byte bank groups per quarter warp instead of 2 (a 4-way conflict on every
+// LDS.128 of an A or B fragment with the plain k-major layout).
 template <int MT, int NT, class KT>
 __device__ __forceinline__ void issue_a(const KT& kt, int k0, int klen, int i0, int mm, bool a_km,
-                                        const double2* __restrict__ Ab, int tid, double2* As) {
+                                        const double2* __restrict__ Ab, int tid, double2* As, bool swz = false) {
 #pragma unroll
   for (int q = 0; q < MT * KC / 256; ++q) {
     const int e = tid + q * 256;
@@ -118,12 +122,12 @@ __device__ __forceinline__ void issue_a(const KT& kt, int k0, int klen, int i0, 
     const int kk = k0 + k;
     const bool v = (i < mm && kk < klen);
     const double2* src = v ? Ab + kt.kA[kk] + (int64_t)(i0 + i) * kt.kSi[kk] : Ab;
-    cp_async16(As + k * MT + i, src, v);
+    cp_async16(As + k * MT + (swz ? (i ^ (2 * (k & 3))) : i), src, v);
   }
 }
 template <int MT, int NT, class KT>
 __device__ __forceinline__ void issue_b(const KT& kt, int k0, int klen, int c0, int nn, bool b_km,
-                                        const double2* __restrict__ Bb, int tid, double2* Bs) {
+                                        const double2* __restrict__ Bb, int tid, double2* Bs, bool swz = false) {
   constexpr int NB = NT * KC;
 #pragma unroll
   for (int q = 0; q < (NB + 255) / 256; ++q) {
@@ -134,7 +138,7 @@ __device__ __forceinline__ void issue_b(const KT& kt, int k0, int klen, int c0, 
     const int kk = k0 + k;
     const bool v = (c < nn && kk < klen);
     const double2* src = v ? kt.kB[kk] + (int64_t)(c0 + c) * kt.kSc[kk] : Bb;
-    cp_async16(Bs + k * NT + c, src, v);
+    cp_async16(Bs + k * NT + (swz ? (c ^ (2 * (k & 3))) : c), src, v);
   }
 }
 
@@ -593,7 +597,7 @@ __device__ __forceinline__ void item_body_dmma(const FlowArgs& a, const GWork& w
   const int nsteps = (klen + KC - 1) / KC;
 #pragma unroll
   for (int s = 0; s < NSTAGE - 1; ++s)
-    if (s < nsteps) issue_a<GM_MT, GM_NT>(kt, s * KC, klen, i0, mm, a_km, a.A, tid, As0 + s * STAGE_A);
+    if (s < nsteps) issue_a<GM_MT, GM_NT>(kt, s * KC, klen, i0, mm, a_km, a.A, tid, As0 + s * STAGE_A, true);
   cp_commit();
   const double sgn = (double)T.sign;
   const bool crit_fin = (w.nchunks > 1 && w.crit >= 0 && w.chunk == w.crit);
@@ -644,15 +648,16 @@ __device__ __forceinline__ void item_body_dmma(const FlowArgs& a, const GWork& w
   if (tr) tr[3] = gtimer();
 #pragma unroll
   for (int s = 0; s < NSTAGE - 1; ++s) {
-    if (s < nsteps) issue_b<GM_MT, GM_NT>(kt, s * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + s * STAGE_B);
+    if (s < nsteps) issue_b<GM_MT, GM_NT>(kt, s * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + s * STAGE_B, true);
     cp_commit();
   }
   for (int s = 0; s < nsteps; ++s) {
     cp_wait<NSTAGE - 2>();
     __syncthreads();
     const int st = s % NSTAGE;
-    const double2* As = As0 + st * STAGE_A + (8 * kh + q) * GM_MT + g;
-    const double2* Bs = Bs0 + st * STAGE_B + (8 * kh + q) * GM_NT + 16 * wc + g;
+    const int gs = g ^ (2 * q);                       // swizzled row / column of this lane's fragments
+    const double2* As = As0 + st * STAGE_A + (8 * kh + q) * GM_MT + gs;
+    const double2* Bs = Bs0 + st * STAGE_B + (8 * kh + q) * GM_NT + 16 * wc + gs;
 #pragma unroll
     for (int kk = 0; kk < 2; ++kk) {
       double2 av[MT], bv[NT];
@@ -678,8 +683,8 @@ __device__ __forceinline__ void item_body_dmma(const FlowArgs& a, const GWork& w
     const int sn = s + NSTAGE - 1;
     if (sn < nsteps) {
       const int stn = sn % NSTAGE;
-      issue_a<GM_MT, GM_NT>(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * STAGE_A);
-      issue_b<GM_MT, GM_NT>(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * STAGE_B);
+      issue_a<GM_MT, GM_NT>(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * STAGE_A, true);
+      issue_b<GM_MT, GM_NT>(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * STAGE_B, true);
     }
     cp_commit();
   }
