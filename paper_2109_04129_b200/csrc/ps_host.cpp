@@ -396,9 +396,11 @@ struct Table {
     // many operator bytes as a 64-row one (C4-1 -5 %; in small stages it would cost parallelism)
     static const int short_x2 = env_int("PS_NARROW_SHORT_X2", 1);
     if (narrow && short_x2 && t.m <= 32 && steps >= NARROW_STEPS()) steps *= 2;   // only where the stage is capped
-    // consumer per task: tall tasks (>= 32 rows: full 32-row tiles, little 8-row
-    // padding) on the FP64 tensor cores, short ones (single 16-19 row leaves) on DFMA
-    static const int auto_mma = env_int("PS_AUTO_MMA", 1), mma_rows = env_int("PS_MMA_MINROWS", 32);
+    // consumer per task: every wide task on the FP64 tensor cores (with the swizzled,
+    // conflict-free fragment loads the DMMA consumer beats DFMA even on 4-20-row leaves
+    // padded to 8-row blocks: C4-360 100.6 -> 91.7 ms); PS_MMA_MINROWS=n keeps tasks
+    // shorter than n rows on the DFMA consumer (PS_MMA=dfma: all of them)
+    static const int auto_mma = env_int("PS_AUTO_MMA", 1), mma_rows = env_int("PS_MMA_MINROWS", 1);
     if (auto_mma && !narrow && t.m >= mma_rows) t.osel |= 4;
     static const int iso_env = env_int("PS_ISOLATE", 0);
     if (!iso_env) isolate = 0;
