@@ -624,6 +624,8 @@ struct Table {
     fa.mma = mma_env >= 0 ? mma_env : mma;
     static const int ksplit = env_int("PS_KSPLIT", 1);
     fa.ksplit = ksplit;
+    static const int gauss = env_int("PS_GAUSS", 1);
+    fa.gauss = gauss;
     if (pf && pf->trace_on && cls == pf->trace_cls) {
       pf->trace_buf.alloc(8 * bt.nw);
       CK(cudaMemsetAsync(pf->trace_buf.p, 0, 8 * sizeof(int64_t) * bt.nw, st));

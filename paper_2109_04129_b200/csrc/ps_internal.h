@@ -90,6 +90,7 @@ struct FlowArgs {
   int32_t narrow;          // 1: narrow 64 x 8 tiles (small nrhs), 0: 32 x 64 tiles
   int32_t mma;             // wide tiles: 0 = DFMA consumer, 1 = FP64 tensor-core (DMMA) consumer
   int32_t ksplit;          // wide DFMA tiles: 1 = k-split two-column layout (item_body_ks), 0 = one column per lane
+  int32_t gauss;           // wide DMMA tiles: 1 = three-multiplication complex product (item_body_dmma3)
 };
 
 // Tile geometry of the gather-GEMM kernel (ps_kernels.cu).

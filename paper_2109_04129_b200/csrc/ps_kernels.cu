@@ -745,6 +745,138 @@ __device__ __forceinline__ void item_body_dmma(const FlowArgs& a, const GWork& w
   }
 }
 
+// Wide tile on the FP64 tensor cores with Gauss's three-multiplication complex product:
+// (Ar + i Ai)(Br + i Bi) = (P1 - P2) + i (P3 - P1 - P2), P1 = Ar Br, P2 = Ai Bi,
+// P3 = (Ar + Ai)(Br + Bi): 3 DMMAs per 8 x 8 complex block and k4 step instead of 4 (the
+// consumer is tensor-pipe bound once its fragment loads are conflict-free). 8 warps = 8
+// column groups of 8 columns, each warp all MT row blocks over the full KC of a stage
+// (no k-half split, so no end-of-item reduction): three accumulator pairs per block
+// (6 MT doubles per lane). The stages use the same swizzled layout as item_body_dmma.
+template <int MT>
+__device__ __forceinline__ void item_body_dmma3(const FlowArgs& a, const GWork& w, const GTask& T,
+                                                const KTab& kt, double2* As0, double2* Bs0, int tid,
+                                                int lane, int warp, int* s_last, int64_t* tr) {
+  const int i0 = w.mt * GM_MT, c0 = w.nt * GM_NT;
+  const int mm = min(GM_MT, T.m - i0), nn = min(GM_NT, T.n - c0);
+  const int klen = w.kb - w.ka;
+  const int g = lane >> 2, q = lane & 3;
+  const int wc = warp;
+  int32_t* done = a.counters + 1;
+  const bool a_km = T.a_kmajor != 0, b_km = T.b_kmajor != 0;
+  const int nsteps = (klen + KC - 1) / KC;
+#pragma unroll
+  for (int s = 0; s < NSTAGE - 1; ++s)
+    if (s < nsteps) issue_a<GM_MT, GM_NT>(kt, s * KC, klen, i0, mm, a_km, a.A, tid, As0 + s * STAGE_A, true);
+  cp_commit();
+  const double sgn = (double)T.sign;
+  const bool crit_fin = (w.nchunks > 1 && w.crit >= 0 && w.chunk == w.crit);
+  const bool owns_init = (w.nchunks == 1) || (w.crit >= 0 ? w.chunk == w.crit : w.chunk == 0);
+  double p1[MT][2], p2[MT][2], p3[MT][2];
+#pragma unroll
+  for (int m = 0; m < MT; ++m) p1[m][0] = p1[m][1] = p2[m][0] = p2[m][1] = p3[m][0] = p3[m][1] = 0.0;
+  auto tile_off = [&](int m, int e) { return (m * 8 + g) * GM_NT + 8 * wc + 2 * q + e; };
+  // start values (init rows, critical chunk's group sum) enter as P1 += re, P3 += re + im, so
+  // that re = P1 - P2 and im = P3 - P1 - P2 carry them exactly once
+  auto add_start = [&](int m, int e, double re, double im) {
+    p1[m][e] += re;
+    p3[m][e] += re + im;
+  };
+  if (crit_fin) {
+    wait_group_sum(a, w, tid);
+    const double2* Gs = a.partial + (w.slot + w.crit) * slot_elems(a);
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double2 v = __ldcg(Gs + tile_off(m, e));
+        add_start(m, e, v.x, v.y);
+      }
+  }
+  auto load_init = [&]() {
+    if (!(owns_init && T.oI >= 0)) return;
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = m * 8 + g, c = 8 * wc + 2 * q + e;
+        if (i < mm && c < nn) {
+          const double2 z = __ldcg(((T.osel & 2) ? (const double2*)a.S : a.I) + T.oI + (int64_t)(i0 + i) * T.sIi + (int64_t)(c0 + c) * T.sIc);
+          add_start(m, e, sgn * z.x, sgn * z.y);
+        }
+      }
+  };
+  if (T.idep < 0) load_init();
+  if (tid < 32) wait_deps(a, w, T, tid);
+  __syncthreads();
+  if (T.idep >= 0) load_init();
+  if (tr) tr[3] = gtimer();
+#pragma unroll
+  for (int s = 0; s < NSTAGE - 1; ++s) {
+    if (s < nsteps) issue_b<GM_MT, GM_NT>(kt, s * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + s * STAGE_B, true);
+    cp_commit();
+  }
+  const int gs = g ^ (2 * q);                         // swizzled row / column of this lane's fragments
+  for (int s = 0; s < nsteps; ++s) {
+    cp_wait<NSTAGE - 2>();
+    __syncthreads();
+    const int st = s % NSTAGE;
+    const double2* As = As0 + st * STAGE_A + q * GM_MT + gs;
+    const double2* Bs = Bs0 + st * STAGE_B + q * GM_NT + 8 * wc + gs;
+#pragma unroll
+    for (int kk = 0; kk < KC / 4; ++kk) {
+      double2 av[MT];
+#pragma unroll
+      for (int m = 0; m < MT; ++m) av[m] = As[kk * 4 * GM_MT + m * 8];
+      const double2 bv = Bs[kk * 4 * GM_NT];
+      const double bs = bv.x + bv.y;
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        dmma(p1[m][0], p1[m][1], av[m].x, bv.x);
+        dmma(p2[m][0], p2[m][1], av[m].y, bv.y);
+        dmma(p3[m][0], p3[m][1], av[m].x + av[m].y, bs);
+      }
+    }
+    const int sn = s + NSTAGE - 1;
+    if (sn < nsteps) {
+      const int stn = sn % NSTAGE;
+      issue_a<GM_MT, GM_NT>(kt, sn * KC, klen, i0, mm, a_km, a.A, tid, As0 + stn * STAGE_A, true);
+      issue_b<GM_MT, GM_NT>(kt, sn * KC, klen, c0, nn, b_km, a.B, tid, Bs0 + stn * STAGE_B, true);
+    }
+    cp_commit();
+  }
+  cp_wait<0>();
+  __syncthreads();
+  if (tr) tr[4] = gtimer();
+  constexpr int E = MT * 2;
+  double2 acc[E];
+  int off[E];
+  bool own[E];
+#pragma unroll
+  for (int m = 0; m < MT; ++m)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      acc[m * 2 + e] = make_double2(p1[m][e] - p2[m][e], p3[m][e] - p1[m][e] - p2[m][e]);
+      off[m * 2 + e] = tile_off(m, e);
+      own[m * 2 + e] = true;
+    }
+  const bool finalize = crit_fin ? true : splitk_combine<E>(a, w, acc, off, own, tid, s_last);
+  if (finalize) {
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = m * 8 + g, c = 8 * wc + 2 * q + e;
+        if (i < mm && c < nn) {
+          const double2 v = acc[m * 2 + e];
+          __stcg(((T.osel & 1) ? a.S : a.O) + T.oO + (int64_t)(i0 + i) * T.sOi + (int64_t)(c0 + c) * T.sOc,
+                 make_double2(sgn * v.x, sgn * v.y));      // O = I + sign * sum
+        }
+      }
+    __syncthreads();
+    if (tid == 0) red_release(done + T.unit0 + w.nt, 1);
+  }
+}
+
 // Output tile: warp w = (wm, wn) = (w % 4, w / 4) owns rows
 // [wm*RM, min(mm, (wm+1)*RM)) with RM = ceil(mm / 4) <= 8 (so the tile is
 // only as tall as the task) and column wn*32 + lane. A values are broadcast
@@ -796,11 +928,20 @@ flow_kernel(const FlowArgs a) {
     const int mm = min(GM_MT, T.m - w.mt * GM_MT);
     const int RM = (mm + GM_WM - 1) / GM_WM;
     if (a.mma || (T.osel & 4)) {
-      switch ((mm + 7) / 8) {
-        case 1: item_body_dmma<1>(a, w, T, kt, As0, Bs0, tid, lane, warp, &s_last, tr); break;
-        case 2: item_body_dmma<2>(a, w, T, kt, As0, Bs0, tid, lane, warp, &s_last, tr); break;
-        case 3: item_body_dmma<3>(a, w, T, kt, As0, Bs0, tid, lane, warp, &s_last, tr); break;
-        default: item_body_dmma<4>(a, w, T, kt, As0, Bs0, tid, lane, warp, &s_last, tr); break;
+      if (a.gauss) {
+        switch ((mm + 7) / 8) {
+          case 1: item_body_dmma3<1>(a, w, T, kt, As0, Bs0, tid, lane, warp, &s_last, tr); break;
+          case 2: item_body_dmma3<2>(a, w, T, kt, As0, Bs0, tid, lane, warp, &s_last, tr); break;
+          case 3: item_body_dmma3<3>(a, w, T, kt, As0, Bs0, tid, lane, warp, &s_last, tr); break;
+          default: item_body_dmma3<4>(a, w, T, kt, As0, Bs0, tid, lane, warp, &s_last, tr); break;
+        }
+      } else {
+        switch ((mm + 7) / 8) {
+          case 1: item_body_dmma<1>(a, w, T, kt, As0, Bs0, tid, lane, warp, &s_last, tr); break;
+          case 2: item_body_dmma<2>(a, w, T, kt, As0, Bs0, tid, lane, warp, &s_last, tr); break;
+          case 3: item_body_dmma<3>(a, w, T, kt, As0, Bs0, tid, lane, warp, &s_last, tr); break;
+          default: item_body_dmma<4>(a, w, T, kt, As0, Bs0, tid, lane, warp, &s_last, tr); break;
+        }
       }
     } else
     switch (RM) {
