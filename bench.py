@@ -310,7 +310,12 @@ def _roofline(h, Bd, Xd, st, nrhs, args, info, rep):
                 "peak_source": ("FP64 (DFMA and mma.sync f64 share one pipe budget; tcgen05 has no f64 kind): "
                                 "measured 37.02 TF on this pool's B200 (profiles/r1/fp64_peak_b200.json) = "
                                 "148 SM x 64 FP64 FMA/clk x 2 flop x 1.965 GHz (37.2 TF derived); "
-                                "MEASURED_PEAKS.json has no FP64 entry")}
+                                "MEASURED_PEAKS.json has no FP64 entry"),
+                # the tensor-core consumer forms each complex product with Gauss's three real
+                # multiplications, so the algorithmic complex rate (8 flop per
+                # complex multiply-add) can reach 4/3 of the real FP64 peak
+                "complex_3m_peak": FP64_PEAK * 4.0 / 3.0,
+                "frac_of_complex_3m_peak": tf / (FP64_PEAK * 4.0 / 3.0)}
     roof.update({
         "traffic": traffic, "traffic_source": traffic_src,
         "algorithmic_per_launch": {"flop": alg_fl, "bytes": alg_by,
