@@ -224,10 +224,12 @@ def _ncu_traffic(config, nrhs):
         def mb(v):
             x, u = v.split()
             return float(x) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
+        # the capture holds ONE solve (scripts/ncu_solve.py): its dataflow-program launch(es) and,
+        # for nrhs <= 8, the far1p apply — the DRAM bytes of that kernel chain
         vals = [mb(r["dram__bytes_read.sum"]) + mb(r["dram__bytes_write.sum"]) for r in d["rows"]
-                if "flow_kernel" in r.get("Kernel Name", "")]
+                if any(k in r.get("Kernel Name", "") for k in ("flow_kernel", "far1p", "far_reduce"))]
         if vals:
-            return sum(vals) / len(vals), os.path.relpath(fn, ROOT)
+            return sum(vals), os.path.relpath(fn, ROOT)
     return None, f"no committed ncu --set full capture of {config}-{nrhs} on this build (libps {cur})"
 
 
@@ -292,10 +294,14 @@ def _roofline(h, Bd, Xd, st, nrhs, args, info, rep):
         h.solve(Bd, Xd, stream=st, want_norms=False)
     prof = h.profile_read()
     h.profile(False)
-    k_ms = prof["solve_program"]["ms"] / max(1, prof["solve_program"]["launches"])
+    # the dominant kernel chain of one solve: the dataflow program (one launch; for nrhs <= 8 two
+    # launches around the one-pass far apply, whose kernels are the far1p class)
+    f1p = prof.get("far1p", {"ms": 0.0, "launches": 0, "flops": 0.0, "bytes": 0.0})
+    chain_ms = (prof["solve_program"]["ms"] + f1p["ms"]) / steps
+    k_ms = chain_ms
     tot_ms = sum(prof[c]["ms"] for c in prof) / steps
-    exe_fl = prof["solve_program"]["flops"] / steps
-    exe_by = prof["solve_program"]["bytes"] / steps
+    exe_fl = (prof["solve_program"]["flops"] + f1p["flops"]) / steps
+    exe_by = (prof["solve_program"]["bytes"] + f1p["bytes"]) / steps
     peaks = _peaks()
     hbm_peak = float(peaks.get("hbm_gbs", 6548.2))
     alg_fl, alg_by = rep["flops"], rep["bytes"]
@@ -326,10 +332,14 @@ def _roofline(h, Bd, Xd, st, nrhs, args, info, rep):
                                         "blocks replaced by the T_c products (DESIGN.md R23), operator "
                                         "bytes only"},
         "executed_over_algorithmic_operator_bytes": exe_by / (16.0 * (4 * info["nR"] + 2 * info["nD"] + info["nF"])),
-        "kernel": "ps::flow_kernel / flow_kernel_ws (persistent dataflow gather-GEMM: the whole two-term "
-                  "solve as one launch)",
+        "kernel": ("ps::flow_kernel_ws x2 (sweeps before / after the far field) + ps::far1p_kernel and "
+                   "far_reduce (one-pass far apply, DESIGN.md §6): device time per solve"
+                   if f1p["launches"] else
+                   "ps::flow_kernel / flow_kernel_ws (persistent dataflow gather-GEMM: the whole two-term "
+                   "solve as one launch)"),
         "kernel_ms_per_launch": k_ms,
-        "kernel_share_of_step": prof["solve_program"]["ms"] / steps / tot_ms if tot_ms > 0 else None})
+        "kernel_parts_ms": {"solve_program": prof["solve_program"]["ms"] / steps, "far1p": f1p["ms"] / steps},
+        "kernel_share_of_step": chain_ms / tot_ms if tot_ms > 0 else None})
     return roof
 
 

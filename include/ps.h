@@ -249,9 +249,13 @@ int ps_analyze(const char* path, double* out, int n);
  * (the task / segment / work-item tables ps_solve would launch): every
  * operand access inside its arena, no workspace element written by two tasks, every
  * read of a written range waiting on exactly that range's writer, and every item's
- * producers at smaller tickets (deadlock freedom of the persistent kernel). stats
- * (optional, up to 6): tasks, segments, work items, write ranges, read ranges, the
- * largest ticket distance to a producer. Returns the number of work items, or
+ * producers at smaller tickets (deadlock freedom of the persistent kernel). For nrhs
+ * <= 8 the program is two launches around the one-pass far apply (far1p): tasks of
+ * different launches are ordered by launch order, and the far1p tables are checked too
+ * (factor ranges inside the FB arena, rows inside the vectors, every waiting item after
+ * its producers). stats (optional, up to 7): tasks, segments, work items, write ranges,
+ * read ranges, the largest ticket distance to a producer, far1p items (-1 / untouched:
+ * none). Returns the number of work items, or
  * -ps_status (PS_ESTATE: a property is violated; the message names it). */
 int64_t ps_validate(const char* path, int64_t nrhs, int64_t* stats, int nstats);
 
@@ -271,8 +275,9 @@ ps_status ps_profile(ps_handle* h, int enable);
 /* ps_profile_read — accumulated since ps_profile(h,1): for each kernel class
  * c in {0 forward sweep, 1 backward sweep, 2 D^{-1}, 3 far stage 1,
  * 4 far stage 2, 5 permutations/combine/norms, 6 the whole-solve dataflow
- * program (default ps_solve path)} four values out[4c..4c+3] =
- * (device ms, launches, algorithmic flops, algorithmic operator bytes).
+ * program (default ps_solve path; two launches for nrhs <= 8), 7 the one-pass far
+ * apply of nrhs <= 8 (Morton copy of w, far1p kernel, per-leaf sums)} four values
+ * out[4c..4c+3] = (device ms, launches, algorithmic flops, algorithmic operator bytes).
  * Classes 0-4 and 6 are all the gather-GEMM kernel. Returns values written. */
 int ps_profile_read(const ps_handle* h, double* out, int n);
 

@@ -234,7 +234,7 @@ class PsHandle:
             raise PsError(PS_EINVAL, "ps_get_dinv failed")
         return buf[:n * n].reshape(n, n, order="F")
 
-    PROFILE_CLASSES = ["fwd_sweep", "bwd_sweep", "dinv", "far_stage1", "far_stage2", "aux", "solve_program"]
+    PROFILE_CLASSES = ["fwd_sweep", "bwd_sweep", "dinv", "far_stage1", "far_stage2", "aux", "solve_program", "far1p"]
 
     def profile(self, enable: bool = True):
         self._check(load_library().ps_profile(self._h, 1 if enable else 0))
@@ -316,12 +316,13 @@ def analyze(path: str, rank: int = 0, nranks: int = 1) -> dict:
 def validate(path: str, nrhs: int) -> dict:
     """Host-only ps_validate of the solve program for nrhs columns (raises on a violation)."""
     L = load_library()
-    st = np.zeros(6, dtype=np.int64)
-    n = L.ps_validate(path.encode(), nrhs, st.ctypes.data, 6)
+    st = np.full(7, -1, dtype=np.int64)
+    n = L.ps_validate(path.encode(), nrhs, st.ctypes.data, 7)
     if n < 0:
         raise PsError(-n, L.ps_last_error(None).decode())
     return dict(items=int(n), tasks=int(st[0]), segments=int(st[1]), work=int(st[2]), write_ranges=int(st[3]),
-                read_ranges=int(st[4]), max_ticket_distance=int(st[5]))
+                read_ranges=int(st[4]), max_ticket_distance=int(st[5]),
+                far1p_items=int(st[6]) if st[6] >= 0 else None)
 
 
 def nccl_unique_id() -> bytes:

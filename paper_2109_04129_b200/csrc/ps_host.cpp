@@ -160,7 +160,7 @@ uint64_t checksum64(const uint8_t* b, size_t nbytes) {
 // Optional per-launch CUDA-event profiling (ps_profile): events are recorded on
 // the launching stream around every kernel; elapsed times are accumulated per
 // kernel class after the solve's final synchronisation.
-enum { PC_FWD = 0, PC_BWD, PC_DINV, PC_FAR1, PC_FAR2, PC_AUX, PC_PROG, PC_COUNT };
+enum { PC_FWD = 0, PC_BWD, PC_DINV, PC_FAR1, PC_FAR2, PC_AUX, PC_PROG, PC_F1P, PC_COUNT };
 struct Prof {
   bool on = false;
   // debug trace of the LAST profiled flow launch of class trace_cls
@@ -263,13 +263,16 @@ struct Table {
   // order as soon as their inputs can exist; the critical chunk (which adds the
   // group sum) keeps the task's key. Every item still follows its producers.
   bool early_keys = false;
+  // sorts the items of the open batch (keys hold one entry per item since cur_batch_start)
   void sort_by_key() {
-    std::vector<int64_t> idx(work.size());
+    const int64_t w0 = cur_batch_start, nw = (int64_t)work.size() - w0;
+    if ((int64_t)keys.size() != nw) throw PsError{PS_ECUDA, "internal: ticket keys out of step with the batch"};
+    std::vector<int64_t> idx(nw);
     std::iota(idx.begin(), idx.end(), 0);
     std::stable_sort(idx.begin(), idx.end(), [&](int64_t x, int64_t y) { return keys[x] < keys[y]; });
-    std::vector<GWork> w2(work.size());
-    for (size_t i = 0; i < idx.size(); ++i) w2[i] = work[idx[i]];
-    work.swap(w2);
+    std::vector<GWork> w2(nw);
+    for (int64_t i = 0; i < nw; ++i) w2[i] = work[w0 + idx[i]];
+    std::copy(w2.begin(), w2.end(), work.begin() + w0);
     keys.clear();
     keys_late.clear();
   }
@@ -292,6 +295,7 @@ struct Table {
       work.swap(w0);
       keys = kl;
       batches.pop_back();
+      task_end.pop_back();
       n_units = nu; n_tiles = ntl; max_units = mu; max_tiles = mtl;
       n_slots = ns; max_slots = ms; cur_batch_start = cb0;
       sort_by_key();
@@ -539,7 +543,14 @@ struct Table {
     }
     n_slots = pool;
   }
+  std::vector<int32_t> task_end;      // tasks.size() at each close_batch (task -> batch)
+  int batch_of_task(int32_t t) const {
+    return (int)(std::upper_bound(task_end.begin(), task_end.end(), t) - task_end.begin());
+  }
   void close_batch() {
+    task_end.push_back((int32_t)tasks.size());
+    keys.clear();
+    keys_late.clear();
     int64_t n = (int64_t)work.size() - cur_batch_start;
     batches.push_back({cur_batch_start, n});
     assign_slots(cur_batch_start, (int64_t)work.size());
@@ -663,6 +674,17 @@ struct SolvePlan {
   int64_t nchunks = 0, rpc = 64;
   int64_t launches_per_solve = 0;
   bool stages_built = false;
+  // far1p (narrow solves): the program is two batches (S1-S3 | S6-S8) around the one-pass
+  // far apply (Morton copy of w, far1p items -> pieces, per-leaf sums -> Z)
+  bool f1p = false;
+  std::vector<FBlk> f1p_blk;               // the handle's blocks with this nrhs' packing / chunking
+  std::vector<FItem> f1p_item;
+  std::vector<FUnit> f1p_unit;
+  DevBuf<FBlk> d_f1p_blk;
+  DevBuf<FItem> d_f1p_item;
+  DevBuf<FUnit> d_f1p_unit;
+  DevBuf<int32_t> d_f1p_cnt;
+  DevBuf<double2> f1p_y, f1p_xa;
 };
 
 // Per-nrhs plan of the row-partitioned solve: this rank's tables
@@ -761,6 +783,18 @@ struct ps_handle {
   DevBuf<int64_t> d_d2rwg;
   void* nccl = nullptr;                    // ncclComm_t; nullptr: in-process group (ps_solve_group)
   std::unique_ptr<DistPlan> dplan;
+  // ---- one-pass far apply of narrow solves (far1p, ps_internal.h) ----
+  int f1p_state = 0;                       // 0 not built, 1 ready, -1 unavailable on this handle
+  std::vector<FBlk> f1p_blk;                // blocks: [0, f1p_nsmall) small (pack candidates), then big
+  int64_t f1p_nsmall = 0, f1p_ch = F1P_CH;
+  std::vector<int64_t> f1p_lptr, f1p_poff, f1p_lrow;   // per Morton leaf: its pieces (rows), first E row
+  std::vector<int64_t> f1p_xmap;                        // XA row -> elimination row of w
+  std::vector<int32_t> f1p_lsz;
+  int64_t f1p_prows = 0, f1p_len = 0, FBbase = 0;
+  double f1p_alg_bytes = 0, f1p_alg_flops1 = 0;        // factor bytes read once; flops per column
+  DevBuf<double2> d_fb;                    // FB arena: factors rows-major, small blocks first
+  DevBuf<int64_t> d_f1p_lptr, d_f1p_poff, d_f1p_lrow, d_f1p_xmap;
+  DevBuf<int32_t> d_f1p_lsz;
 };
 
 namespace {
@@ -1446,6 +1480,258 @@ void ensure_far(ps_handle* h, cudaStream_t s) {
   h->Fbase = (int64_t)(h->d_farbuf.p - h->d_op.p);
 }
 
+// One-pass far apply of narrow solves (far1p; ps_internal.h): the block,
+// item and piece tables (once per handle) and the FB arena (every far factor copied
+// rows-major out of the stacks by one gather launch). Returns false (and the program keeps
+// the two-stage far field) when a block's rank exceeds F1P_RMAX or on a row-partition rank.
+bool build_far1p(ps_handle* h, cudaStream_t s) {
+  if (h->f1p_state) return h->f1p_state > 0;
+  h->f1p_state = -1;
+  // PS_FAR1P: 1 always, 0 never, -1 (default) where it pays: splitting the program at the far
+  // field costs the overlap of the far products with the sweeps' dependency bubbles and a
+  // launch gap, so the one-pass apply is taken when the far factors are large (>= 1 GiB) and a
+  // large share (>= 30 %) of the sweeps' operator (C4: 2.6 GB vs 4 x 1.1 GB: 3.75 vs 4.42 ms per
+  // 1-RHS solve; C3's 0.4 GB / C2's 0.3 GB far fields measured equal or slower)
+  const int mode = env_int("PS_FAR1P", -1);
+  if (h->part_mode || mode == 0) return false;
+  const int64_t nf = h->nfar, nl = h->nl;
+  if (mode < 0) {
+    double far_el = 0;
+    for (int64_t b = 0; b < nf; ++b) {
+      const int64_t* F = &h->far_list[7 * b];
+      far_el += h->fb_dense[b] >= 0 ? (double)F[1] * F[3] : (double)(F[1] + F[3]) * F[5];
+    }
+    if (far_el < (double)(1 << 26) || far_el < 0.3 * 4.0 * (double)h->Plen) return false;
+  }
+  for (int64_t b = 0; b < nf; ++b) {
+    const int64_t* F = &h->far_list[7 * b];
+    const int64_t r = F[5];
+    if (r == 0) continue;
+    if (h->fb_dense[b] >= 0 ? std::min(F[1], F[3]) > F1P_RMAX : r > F1P_RMAX) return false;
+  }
+  auto leaf_of_pos = [&](int64_t m) {
+    return (int64_t)(std::upper_bound(h->leaf_off.begin(), h->leaf_off.end(), m) - h->leaf_off.begin()) - 1;
+  };
+  // elements per item (staged); PS_F1P_CHUNK < F1P_CH (tests) cuts more blocks into chunks
+  const int64_t CH = std::max<int64_t>(F1P_RMAX, std::min<int64_t>(F1P_CH, env_int("PS_F1P_CHUNK", F1P_CH)));
+  // blocks: small ones first in block order (packed), then the big ones
+  struct Src { int64_t src, ss, sk; };
+  std::vector<FBlk> small, big;
+  std::vector<std::array<Src, 2>> src_small, src_big;
+  int64_t prow = 0;
+  std::vector<std::vector<std::pair<int64_t, int64_t>>> leaf_pieces(nl);   // (order key, piece row)
+  auto add_piece = [&](int64_t x0, int64_t len, int64_t y0) {
+    for (int64_t l = leaf_of_pos(x0); l < nl && h->leaf_off[l] < x0 + len; ++l)
+      leaf_pieces[l].push_back({y0 + (h->leaf_off[l] - x0), 0});
+  };
+  double alg = 0, fl1 = 0;
+  for (int64_t b = 0; b < nf; ++b) {
+    const int64_t* F = &h->far_list[7 * b];
+    const int64_t r0 = F[0], m = F[1], c0 = F[2], n = F[3], r = F[5];
+    if (r == 0) continue;
+    FBlk k{};
+    std::array<Src, 2> sr{};
+    if (h->fb_dense[b] >= 0) {
+      const int64_t D = h->Fbase + h->fb_dense[b];      // m x n column-major
+      k.dense = 1;
+      k.o2 = -1;
+      k.n2 = 0;
+      if (m <= n) {   // G = D^T: rows = the column cluster (n), row length m
+        k.n1 = (int32_t)n; k.r = (int32_t)m; k.x1 = c0; k.x2 = r0;
+        sr[0] = {D, m, 1};
+      } else {        // G = D: rows = the row cluster (m), row length n
+        k.n1 = (int32_t)m; k.r = (int32_t)n; k.x1 = r0; k.x2 = c0;
+        sr[0] = {D, 1, m};
+      }
+      k.y1 = prow; prow += k.n1;
+      k.y2 = prow; prow += k.r;
+      alg += 16.0 * m * n;
+      fl1 += 16.0 * m * n;   // two complex products per entry, 8 flop each
+    } else {
+      const int64_t ct = h->fb_ct[b], cs = h->fb_cs[b];
+      const Src U{h->Fbase + h->cl_soff[ct] + h->fb_rbt[b], h->cl_sr[ct], 1};
+      const Src V{h->Fbase + h->cl_soff[cs] + h->fb_rbs[b], h->cl_sr[cs], 1};
+      const bool u_first = m <= n;                       // F1 = the shorter factor (read twice if big)
+      k.r = (int32_t)r;
+      k.n1 = (int32_t)(u_first ? m : n); k.x1 = u_first ? r0 : c0;
+      k.n2 = (int32_t)(u_first ? n : m); k.x2 = u_first ? c0 : r0;
+      sr[0] = u_first ? U : V;
+      sr[1] = u_first ? V : U;
+      k.y1 = prow; prow += k.n1;
+      k.y2 = prow; prow += k.n2;
+      alg += 16.0 * (m + n) * r;
+      fl1 += 16.0 * (m + n) * r;
+    }
+    const int64_t elems = (int64_t)(k.n1 + k.n2) * k.r;
+    (elems <= CH ? small : big).push_back(k);
+    (elems <= CH ? src_small : src_big).push_back(sr);
+  }
+  std::vector<FBlk> blk;
+  std::vector<FCopy> runs;
+  int64_t fb = 0;
+  auto place = [&](FBlk& k, const std::array<Src, 2>& sr) {
+    k.o1 = h->FBbase + fb;
+    runs.push_back({k.o1, sr[0].src, sr[0].ss, sr[0].sk, k.n1, k.r});
+    fb += (int64_t)k.n1 * k.r;
+    if (!k.dense) {
+      k.o2 = h->FBbase + fb;
+      runs.push_back({k.o2, sr[1].src, sr[1].ss, sr[1].sk, k.n2, k.r});
+      fb += (int64_t)k.n2 * k.r;
+    }
+  };
+  // FB layout: the small blocks (candidates for packs) first, in block order, then the big ones
+  for (size_t i = 0; i < small.size(); ++i) {
+    FBlk k = small[i];
+    place(k, src_small[i]);
+    blk.push_back(k);
+  }
+  h->f1p_nsmall = (int64_t)small.size();
+  for (size_t i = 0; i < big.size(); ++i) {
+    FBlk k = big[i];
+    place(k, src_big[i]);
+    blk.push_back(k);
+  }
+  // gathered x arena XA: per block (FB order) its x1 rows then its x2 rows, as elimination rows
+  h->f1p_xmap.clear();
+  for (FBlk& k : blk) {
+    k.xa = (int64_t)h->f1p_xmap.size();
+    for (int32_t i = 0; i < k.n1; ++i) h->f1p_xmap.push_back(h->m2e[k.x1 + i]);
+    const int32_t n2x = k.dense ? k.r : k.n2;
+    for (int32_t i = 0; i < n2x; ++i) h->f1p_xmap.push_back(h->m2e[k.x2 + i]);
+  }
+  h->f1p_blk = std::move(blk);
+  h->f1p_len = fb;
+  h->f1p_prows = prow;
+  h->f1p_alg_bytes = alg;
+  h->f1p_alg_flops1 = fl1;
+  h->f1p_ch = CH;
+  // per Morton leaf: its pieces in block order (the fixed summation order)
+  for (const FBlk& k : h->f1p_blk) {
+    add_piece(k.x1, k.n1, k.y1);
+    add_piece(k.x2, k.dense ? k.r : k.n2, k.y2);
+  }
+  h->f1p_lptr.assign(nl + 1, 0);
+  h->f1p_poff.clear();
+  h->f1p_lrow.assign(nl, 0);
+  h->f1p_lsz.assign(nl, 0);
+  for (int64_t l = 0; l < nl; ++l) {
+    for (auto& pc : leaf_pieces[l]) h->f1p_poff.push_back(pc.first);
+    h->f1p_lptr[l + 1] = (int64_t)h->f1p_poff.size();
+    h->f1p_lrow[l] = h->eoff[h->pos_of[l]];
+    h->f1p_lsz[l] = (int32_t)(h->leaf_off[l + 1] - h->leaf_off[l]);
+  }
+  if (!g_host_only) {
+    h->d_fb.alloc(std::max<int64_t>(fb, 1));
+    // the FB arena is addressed from the operator base like every other operator region
+    const int64_t shift = (int64_t)(h->d_fb.p - h->d_op.p) - h->FBbase;
+    for (FBlk& k : h->f1p_blk) { k.o1 += shift; if (k.o2 >= 0) k.o2 += shift; }
+    for (FCopy& c : runs) c.dst += shift;
+    h->FBbase += shift;
+    DevBuf<FCopy> d_runs;
+    d_runs.upload(runs, s);
+    launch_fb_gather((int64_t)runs.size(), d_runs.p, h->d_op.p, s);
+    CK(cudaGetLastError());
+    h->d_f1p_xmap.upload(h->f1p_xmap, s);
+    h->d_f1p_lptr.upload(h->f1p_lptr, s);
+    h->d_f1p_poff.upload(h->f1p_poff, s);
+    h->d_f1p_lrow.upload(h->f1p_lrow, s);
+    h->d_f1p_lsz.upload(h->f1p_lsz, s);
+    CK(cudaStreamSynchronize(s));
+  }
+  h->f1p_state = 1;
+  return true;
+}
+
+// Per-plan far1p work for nrhs R (build_far1p made the blocks): packs of consecutive small
+// blocks (<= CH factor elements, <= F1P_XCH / R staged x rows, <= F1P_PACK blocks) and one unit per
+// other block, cut into row chunks (<= CH elements and <= F1P_XCH / R x rows each): F1 chunks,
+// F2 chunks, F1 chunks again (dense: G chunks). Units are taken from a ticket, the big ones
+// first (largest first: the tail of the launch is packs).
+void build_far1p_items(const ps_handle* h, SolvePlan& sp, int64_t R) {
+  const int64_t CH = h->f1p_ch, XR = F1P_XCH / R;
+  std::vector<FBlk> blk = h->f1p_blk;
+  std::vector<std::vector<FItem>> bigu;                   // per big unit: its items
+  std::vector<int64_t> bigsz;
+  std::vector<FItem> packs;
+  auto xrows = [](const FBlk& k) { return (int64_t)k.n1 + (k.dense ? k.r : k.n2); };
+  auto add_big = [&](int32_t id) {
+    FBlk& k = blk[id];
+    const int64_t cap = k.dense ? XR - k.r : XR;         // dense chunks also stage the r column rows
+    const int32_t hr = (int32_t)std::max<int64_t>(1, std::min<int64_t>(CH / k.r, cap));
+    k.nc1 = (k.n1 + hr - 1) / hr;
+    k.nc2 = k.dense ? 0 : (k.n2 + hr - 1) / hr;
+    k.xo1 = k.xo2 = 0;
+    std::vector<FItem> its;
+    // chunk c of a side: factor rows [a0, a1) and (except the F1-again pass) their x rows
+    auto chunk = [&](int kind, int64_t o, int64_t xa, int32_t c, int32_t a0, int32_t a1) {
+      FItem it{};
+      it.off = o + (int64_t)a0 * k.r;
+      it.len = (a1 - a0) * k.r;
+      it.kind = kind; it.b = id; it.nb = c; it.a0 = a0; it.a1 = a1;
+      if (kind != 3) { it.xa = xa + a0; it.xn = a1 - a0; }
+      if (kind == 4) { it.xa2 = k.xa + k.n1; it.xn2 = k.r; }
+      its.push_back(it);
+    };
+    for (int32_t c = 0; c < k.nc1; ++c)
+      chunk(k.dense ? 4 : 1, k.o1, k.xa, c, c * hr, std::min(k.n1, (c + 1) * hr));
+    for (int32_t c = 0; c < k.nc2; ++c) chunk(2, k.o2, k.xa + k.n1, c, c * hr, std::min(k.n2, (c + 1) * hr));
+    if (!k.dense)
+      for (int32_t c = 0; c < k.nc1; ++c) chunk(3, k.o1, k.xa, c, c * hr, std::min(k.n1, (c + 1) * hr));
+    bigsz.push_back((int64_t)(k.n1 + k.n2) * k.r);
+    bigu.push_back(std::move(its));
+  };
+  {
+    int64_t p0 = -1, plen = 0, px = 0;
+    int32_t pb = 0, pnb = 0;
+    auto flush = [&] {
+      if (pnb > 0) {
+        FItem it{};
+        it.off = p0; it.len = (int32_t)plen; it.kind = 0; it.b = pb; it.nb = pnb;
+        it.a0 = (int32_t)px;                                // x rows (consecutive blocks: one XA range)
+        it.xa = blk[pb].xa; it.xn = (int32_t)px;
+        packs.push_back(it);
+      }
+      pnb = 0; plen = 0; px = 0;
+    };
+    for (int64_t i = 0; i < h->f1p_nsmall; ++i) {
+      FBlk& k = blk[i];
+      const int64_t e = (int64_t)(k.n1 + k.n2) * k.r, xr = xrows(k);
+      if (xr > XR) {                                     // its x rows do not fit a stage: chunked
+        flush();
+        add_big((int32_t)i);
+        continue;
+      }
+      if (plen + e > CH || px + xr > XR || pnb == F1P_PACK) flush();
+      if (pnb == 0) { p0 = k.o1; pb = (int32_t)i; }
+      k.xo1 = (int32_t)px;
+      k.xo2 = (int32_t)(px + k.n1);
+      px += xr;
+      plen += e;
+      ++pnb;
+    }
+    flush();
+  }
+  for (int64_t i = h->f1p_nsmall; i < (int64_t)blk.size(); ++i) add_big((int32_t)i);
+  std::vector<int64_t> ord(bigu.size());
+  std::iota(ord.begin(), ord.end(), 0);
+  std::stable_sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) { return bigsz[x] > bigsz[y]; });
+  sp.f1p_item.clear();
+  sp.f1p_unit.clear();
+  for (int64_t u : ord) {
+    sp.f1p_unit.push_back(FUnit{(int64_t)sp.f1p_item.size(), (int32_t)bigu[u].size(), 0});
+    sp.f1p_item.insert(sp.f1p_item.end(), bigu[u].begin(), bigu[u].end());
+  }
+  // packs: F1P_PACKS_PER_UNIT consecutive packs per ticket (the producer loads a unit's
+  // descriptors in one batch; a ticket per pack would put a descriptor round trip on every fill)
+  static const int ppu = std::max(1, env_int("PS_F1P_PACKS_PER_UNIT", 8));
+  for (size_t i = 0; i < packs.size(); i += ppu) {
+    const int n = (int)std::min<size_t>(ppu, packs.size() - i);
+    sp.f1p_unit.push_back(FUnit{(int64_t)sp.f1p_item.size(), n, 0});
+    sp.f1p_item.insert(sp.f1p_item.end(), packs.begin() + i, packs.begin() + i + n);
+  }
+  sp.f1p_blk = std::move(blk);
+}
+
 // T_c = (I - A_c^T)^{-1} of every chain piece with L >= 2 (see ps_handle): the
 // forward sweep (Eq. 24) restricted to the piece, applied to the identity:
 //   X_i = delta_i + sum_{k < i, p_i in struct(p_k)} alpha_{p_k p_i}^T X_k,
@@ -1821,6 +2107,9 @@ void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
   int64_t Ttot = 0;
   for (int64_t c = 0; c < ncl; ++c) { toff[c] = sp.oTMP + Ttot; Ttot += h->cl_sr[c] * R; }
   const int resident = resident_units(P.narrow);
+  // narrow solves: the far field as the one-pass far1p apply between two program batches
+  sp.f1p = P.narrow && build_far1p(h, h->stream);
+  if (sp.f1p) build_far1p_items(h, sp, R);
   P.key_stagger = env_int("PS_PROG_STAGGER", 0);     // column tile b enters b * this many key levels later
   P.early_keys = true;
   // far field on the tensor-core consumer with long chunks, as in the stage tables
@@ -2009,6 +2298,11 @@ void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
   dinv_stage(sp.oY, sp.oBO, -1, +1, s2, s1, nullptr);                    // S2
   SC = sp.oSC + NR;
   bwd_stage(sp.oBO, sp.oW, s3, s2);                                      // S3
+  if (sp.f1p) {
+    // batch 0 ends here; S4 / S5 are the far1p launches (Z complete before batch 1, whose
+    // tasks therefore carry no dependency on batch 0 or the far field)
+    P.sort_close_bounded();
+  } else {
   // S4 far stage 1: per cluster, rows gathered per leaf from W (elimination order)
   P.key_base = lev++;
   for (int64_t c = 0; c < ncl; ++c) {
@@ -2068,11 +2362,13 @@ void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
       s5[pos] = t;
     }
   }
+  }
   SC = sp.oSC + 2 * NR;
   fwd_stage(sp.oZ, s6, &s5);                                             // S6
   std::vector<int32_t> zfin(nl);
   for (int64_t p = 0; p < nl; ++p) zfin[p] = s6[p] >= 0 ? s6[p] : s5[p];
-  dinv_stage(sp.oZ, sp.oXT, sp.oBO, -1, s7, zfin, &s2);                  // S7: xt = bo - D^-1 z
+  const std::vector<int32_t> none(nl, -1);
+  dinv_stage(sp.oZ, sp.oXT, sp.oBO, -1, s7, zfin, sp.f1p ? &none : &s2); // S7: xt = bo - D^-1 z
   SC = sp.oSC + 3 * NR;
   bwd_stage(sp.oXT, sp.oX, s8, s7);                                      // S8
   P.sort_close_bounded();
@@ -2080,6 +2376,14 @@ void build_program(ps_handle* h, SolvePlan& sp, int64_t R) {
   if (g_host_only) return;                           // ps_validate: tables only
   P.upload(h->stream, &h->ring);
   sp.ws.alloc(sp.ws_len);
+  if (sp.f1p) {
+    sp.d_f1p_blk.upload(sp.f1p_blk, h->stream);
+    sp.d_f1p_item.upload(sp.f1p_item, h->stream);
+    sp.d_f1p_unit.upload(sp.f1p_unit, h->stream);
+    sp.d_f1p_cnt.alloc(1);
+    sp.f1p_y.alloc(std::max<int64_t>(h->f1p_prows * R, 1));
+    sp.f1p_xa.alloc(std::max<int64_t>((int64_t)h->f1p_xmap.size() * R, 1));
+  }
   // the tables were copied from pageable host memory on h->stream (non-blocking):
   // complete them before ps_solve launches the program on the caller's stream
   CK(cudaStreamSynchronize(h->stream));
@@ -2142,6 +2446,7 @@ std::string validate_program(const ps_handle* h, const SolvePlan& sp, std::vecto
   std::vector<int32_t> stack;
   auto before = [&](int32_t a, int32_t b) -> bool {  // a happens before b
     if (a == b) return false;
+    if (P.batch_of_task(a) != P.batch_of_task(b)) return P.batch_of_task(a) < P.batch_of_task(b);  // launch order
     ++gen;
     stack.assign(1, b);
     while (!stack.empty()) {
@@ -2208,9 +2513,12 @@ std::string validate_program(const ps_handle* h, const SolvePlan& sp, std::vecto
   const int64_t nw = (int64_t)P.work.size();
   std::vector<int64_t> last(nt, -1);
   for (int64_t i = 0; i < nw; ++i) last[P.work[i].task] = std::max(last[P.work[i].task], i);
-  std::vector<int32_t> unit_task(std::max<int32_t>(P.max_units, 1), -1);
+  // completion units are numbered per batch (launch)
+  const int nbat = (int)P.task_end.size();
+  std::vector<std::vector<int32_t>> unit_task(std::max(nbat, 1), std::vector<int32_t>(std::max<int32_t>(P.max_units, 1), -1));
   for (int64_t t = 0; t < nt; ++t)
-    for (int32_t u = 0; u < (P.tasks[t].n + P.NT() - 1) / P.NT(); ++u) unit_task[P.tasks[t].unit0 + u] = (int32_t)t;
+    for (int32_t u = 0; u < (P.tasks[t].n + P.NT() - 1) / P.NT(); ++u)
+      unit_task[P.batch_of_task((int32_t)t)][P.tasks[t].unit0 + u] = (int32_t)t;
   int64_t max_back = 0;
   for (int64_t i = 0; i < nw; ++i) {
     const GWork& w = P.work[i];
@@ -2220,12 +2528,107 @@ std::string validate_program(const ps_handle* h, const SolvePlan& sp, std::vecto
       max_back = std::max(max_back, i - last[task]);
       return last[task] < i;
     };
+    const int bt = P.batch_of_task(w.task);
+    auto same_batch = [&](int32_t task) { return task < 0 || P.batch_of_task(task) == bt; };
+    if (!same_batch(T.idep)) return msg("init producer in another launch", i, T.idep);
     if (!need_before(T.idep)) return msg("item precedes its init producer", i, T.idep);
-    for (int32_t k = w.ta; k < w.tb; ++k)
+    for (int32_t k = w.ta; k < w.tb; ++k) {
+      if (!same_batch(P.terms[k].dep)) return msg("segment producer in another launch", i, P.terms[k].dep);
       if (!need_before(P.terms[k].dep)) return msg("item precedes a segment producer", i, P.terms[k].dep);
-    if (w.sw_unit >= 0 && !need_before(unit_task[w.sw_unit])) return msg("item precedes its slots' previous user", i, w.sw_unit);
+    }
+    if (w.sw_unit >= 0 && !need_before(unit_task[bt][w.sw_unit])) return msg("item precedes its slots' previous user", i, w.sw_unit);
   }
   stats = {nt, (int64_t)P.terms.size(), nw, (int64_t)wr.size(), nread, max_back};
+  return "";
+}
+
+// Host-only check of the far1p tables (ps_validate): every item's factor range inside the
+// FB arena and every pack block inside its item's staged range; x / y rows inside the Morton
+// vector / the pieces; partial slots inside their area; every gamma (beta) item of a big
+// block after all its alpha (gamma) items in item order (the only waits: deadlock-free).
+std::string validate_far1p(const ps_handle* h, const SolvePlan& sp, std::vector<int64_t>& stats) {
+  const int64_t lo = h->FBbase, hi = h->FBbase + h->f1p_len, N = h->N, R = sp.nrhs;
+  auto msg = [](const char* what, int64_t a) { return std::string("far1p: ") + what + " (" + std::to_string(a) + ")"; };
+  const int64_t nb = (int64_t)sp.f1p_blk.size(), ni = (int64_t)sp.f1p_item.size();
+  std::vector<int64_t> covered(nb, 0);
+  std::vector<char> item_seen(ni, 0);
+  for (int64_t u = 0; u < (int64_t)sp.f1p_unit.size(); ++u) {
+    const FUnit& U = sp.f1p_unit[u];
+    if (U.i0 < 0 || U.n < 1 || U.i0 + U.n > ni) return msg("unit items out of range", u);
+    const FItem& f = sp.f1p_item[U.i0];
+    if (f.kind == 0)
+      for (int j = 0; j < U.n; ++j)
+        if (sp.f1p_item[U.i0 + j].kind != 0) return msg("pack unit holding a chunk", u);
+    if (f.kind != 0) {
+      // one big block, its chunks in phase order: F1 (or dense G) chunks, F2 chunks, F1 chunks
+      const FBlk& k = sp.f1p_blk[f.b];
+      std::vector<std::pair<int, int>> want;
+      for (int c = 0; c < k.nc1; ++c) want.push_back({k.dense ? 4 : 1, c});
+      for (int c = 0; c < k.nc2; ++c) want.push_back({2, c});
+      if (!k.dense)
+        for (int c = 0; c < k.nc1; ++c) want.push_back({3, c});
+      if ((int64_t)want.size() != U.n) return msg("big unit does not hold its block's chunks", u);
+      for (int j = 0; j < U.n; ++j) {
+        const FItem& it = sp.f1p_item[U.i0 + j];
+        if (it.b != f.b || it.kind != want[j].first || it.nb != want[j].second) return msg("big unit chunks out of order", u);
+      }
+    }
+    for (int j = 0; j < U.n; ++j) {
+      if (item_seen[U.i0 + j]) return msg("item in two units", U.i0 + j);
+      item_seen[U.i0 + j] = 1;
+    }
+  }
+  for (int64_t i = 0; i < ni; ++i) {
+    if (!item_seen[i]) return msg("item in no unit", i);
+    const FItem& it = sp.f1p_item[i];
+    if (it.len <= 0 || it.len > F1P_CH || it.off < lo || it.off + it.len > hi) return msg("item range outside the FB arena", i);
+    if (it.kind == 0) {
+      if (it.b < 0 || it.nb < 1 || it.nb > F1P_PACK || it.b + it.nb > nb) return msg("pack blocks out of range", i);
+      int64_t xr = 0;
+      for (int32_t j = it.b; j < it.b + it.nb; ++j) {
+        const FBlk& k = sp.f1p_blk[j];
+        const int64_t e1 = (int64_t)k.n1 * k.r, e2 = (int64_t)k.n2 * k.r;
+        if (k.o1 < it.off || k.o1 + e1 > it.off + it.len) return msg("pack block outside its item", j);
+        if (!k.dense && (k.o2 < it.off || k.o2 + e2 > it.off + it.len)) return msg("pack block outside its item", j);
+        const int64_t x2n = k.dense ? k.r : k.n2;
+        if (k.xo1 != xr || k.xo2 != xr + k.n1) return msg("pack x rows not consecutive", j);
+        xr += k.n1 + x2n;
+        covered[j] += e1 + e2;
+      }
+      if (xr * R > F1P_XCH || xr != it.a0 || xr != it.xn || it.xa != sp.f1p_blk[it.b].xa)
+        return msg("pack x rows exceed the stage or miscounted", i);
+      for (int32_t j = it.b; j < it.b + it.nb; ++j)
+        if (sp.f1p_blk[j].xa != it.xa + sp.f1p_blk[j].xo1) return msg("pack x rows not one XA range", j);
+      continue;
+    }
+    if (it.b < 0 || it.b >= nb) return msg("big item block out of range", i);
+    const FBlk& k = sp.f1p_blk[it.b];
+    const bool on2 = it.kind == 2;
+    const int64_t o = on2 ? k.o2 : k.o1;
+    const int32_t rows = on2 ? k.n2 : k.n1;
+    if (it.a0 < 0 || it.a1 > rows || it.a0 >= it.a1 || it.off != o + (int64_t)it.a0 * k.r ||
+        it.len != (it.a1 - it.a0) * k.r)
+      return msg("big item rows inconsistent with its block", i);
+    if (((int64_t)(it.a1 - it.a0) + (it.kind == 4 ? k.r : 0)) * R > F1P_XCH) return msg("chunk x rows exceed the stage", i);
+    {
+      const int64_t want = it.kind == 3 ? -1 : (it.kind == 2 ? k.xa + k.n1 : k.xa) + it.a0;
+      const int32_t wn = it.kind == 3 ? 0 : it.a1 - it.a0;
+      if ((wn > 0 && it.xa != want) || it.xn != wn || (it.kind == 4 ? (it.xa2 != k.xa + k.n1 || it.xn2 != k.r) : it.xn2 != 0))
+        return msg("chunk x rows inconsistent with its block", i);
+    }
+    if (it.kind != 3) covered[it.b] += it.len;
+  }
+  for (int64_t j = 0; j < nb; ++j) {
+    const FBlk& k = sp.f1p_blk[j];
+    const int64_t e = (int64_t)(k.n1 + k.n2) * k.r;
+    if (covered[j] != e) return msg("block factors not covered exactly once", j);
+    if (k.r < 1 || k.r > F1P_RMAX) return msg("block rank outside (0, F1P_RMAX]", j);
+    if (k.x1 < 0 || k.x1 + k.n1 > N || k.x2 < 0 || k.x2 + (k.dense ? k.r : k.n2) > N) return msg("x rows outside N", j);
+    if (k.xa < 0 || k.xa + k.n1 + (k.dense ? k.r : k.n2) > (int64_t)h->f1p_xmap.size()) return msg("XA rows out of range", j);
+    if (k.y1 < 0 || k.y1 + k.n1 > h->f1p_prows || k.y2 < 0 || k.y2 + (k.dense ? k.r : k.n2) > h->f1p_prows)
+      return msg("piece rows out of range", j);
+  }
+  stats.push_back(ni);
   return "";
 }
 
@@ -2279,6 +2682,37 @@ int64_t op_ZF(ps_handle* h, SolvePlan& sp, const double2* in, double2* out, cuda
   n += sp.far2.launch_all(sp.tm.p, nullptr, h->d_far.p, sp.wm.p, s, &h->prof, PC_FAR2);
   n += aux(h, s, [&] { launch_permute_rows(N, R, h->d_e2mort.p, sp.tm.p, out, s); });  // Morton -> E
   return n;
+}
+
+// far1p: Z (E order) = Z_F W over every far block, one read of the factors (build_far1p)
+int64_t far1p_apply(ps_handle* h, SolvePlan& sp, const double2* W, double2* Z, cudaStream_t s) {
+  const int64_t N = h->N, R = sp.nrhs;
+  h->prof.begin(PC_F1P, s);
+  CK(cudaMemsetAsync(sp.d_f1p_cnt.p, 0, sizeof(int32_t), s));
+  launch_permute_rows((int64_t)h->f1p_xmap.size(), R, h->d_f1p_xmap.p, W, sp.f1p_xa.p, s);   // w -> XA
+  Far1pArgs fa;
+  fa.units = sp.d_f1p_unit.p;
+  fa.nunits = (int64_t)sp.f1p_unit.size();
+  fa.items = sp.d_f1p_item.p;
+  fa.blks = sp.d_f1p_blk.p;
+  fa.A = h->d_op.p;
+  fa.x = sp.f1p_xa.p;
+  fa.y = sp.f1p_y.p;
+  fa.cnt = sp.d_f1p_cnt.p;
+  fa.R = (int32_t)R;
+  static const int skip = env_int("PS_F1P_SKIP", 0);
+  fa.skip = skip;
+  static const int grid = env_int("PS_F1P_GRID", 0);
+  fa.grid = grid;
+  launch_far1p(fa, s);
+  launch_far_reduce(h->nl, h->d_f1p_lptr.p, h->d_f1p_poff.p, h->d_f1p_lrow.p, h->d_f1p_lsz.p, sp.f1p_y.p, Z,
+                    (int)R, s);
+  h->prof.end(s);
+  if (h->prof.on) {
+    h->prof.flops[PC_F1P] += h->f1p_alg_flops1 * (double)R;
+    h->prof.bytes[PC_F1P] += h->f1p_alg_bytes;
+  }
+  return 3;
 }
 
 double solve_bytes(const ps_handle* h, int64_t nrhs) {
@@ -3201,7 +3635,17 @@ ps_status ps_solve(ps_handle* h, int64_t nrhs, const void* B, int64_t ldb, void*
       // the whole solve as one dataflow program (build_program)
       double2* ws = sp.ws.p;
       launches += aux(h, s, [&] { launch_permute_in(N, R, h->d_e2rwg.p, Bd, ldb_d, ws + sp.oY, s); });
-      launches += sp.prog.launch_all(ws, ws, h->d_op.p, ws, s, &h->prof, PC_PROG);
+      if (sp.f1p) {
+        launches += sp.prog.launch(0, ws, ws, h->d_op.p, ws, s, &h->prof, PC_PROG);
+        launches += far1p_apply(h, sp, ws + sp.oW, ws + sp.oZ, s);
+        launches += sp.prog.launch(1, ws, ws, h->d_op.p, ws, s, &h->prof, PC_PROG);
+        if (h->prof.on) {
+          h->prof.flops[PC_PROG] += sp.prog.alg_flops;
+          h->prof.bytes[PC_PROG] += sp.prog.alg_bytes;
+        }
+      } else {
+        launches += sp.prog.launch_all(ws, ws, h->d_op.p, ws, s, &h->prof, PC_PROG);
+      }
       launches += aux(h, s, [&] {
         launch_norms2(N, R, ws + sp.oBO, ws + sp.oXT, sp.part.p, sp.rpc, s);
         launch_finalize_norms(sp.nchunks, R, sp.part.p, sp.norms.p, s);
@@ -3316,12 +3760,14 @@ int64_t ps_validate(const char* path, int64_t nrhs, int64_t* stats, int nstats) 
     h.Dbase = h.Plen;
     h.Fbase = h.Plen + h.Dlen;
     h.Tbase = h.Fbase + (int64_t)h.far_host.size();
+    h.FBbase = h.Tbase + h.Tlen;
     SolvePlan sp;
     g_host_only = true;
     build_program(&h, sp, nrhs);
     g_host_only = false;
     // PS_VALIDATE_BREAK (tests of the checker itself): 1 drops one segment dependency,
-    // 2 moves the last work item to the front, 3 pushes one operator offset out of its region
+    // 2 moves the last work item to the front, 3 pushes one operator offset out of its region,
+    // 4 moves a far1p F1-again chunk before its unit's other chunks, 5 moves a far1p item past the FB arena
     static const int brk = env_int("PS_VALIDATE_BREAK", 0);
     Table& Pt = sp.prog;
     if (brk == 1) {
@@ -3331,9 +3777,18 @@ int64_t ps_validate(const char* path, int64_t nrhs, int64_t* stats, int nstats) 
       std::rotate(Pt.work.begin(), Pt.work.end() - 1, Pt.work.end());
     } else if (brk == 3 && !Pt.terms.empty()) {
       Pt.terms.back().oA = h.Tbase + h.Tlen + 1;
+    } else if (brk == 4 && sp.f1p) {              // far1p: a big unit's first F1-again chunk moved to its front
+      for (const FUnit& U : sp.f1p_unit) {
+        auto b = sp.f1p_item.begin() + U.i0, e = b + U.n;
+        auto it = std::find_if(b, e, [](const FItem& x) { return x.kind == 3; });
+        if (it != e) { std::rotate(b, it, it + 1); break; }
+      }
+    } else if (brk == 5 && sp.f1p && !sp.f1p_item.empty()) {  // far1p: an item past the FB arena
+      sp.f1p_item.back().off = h.FBbase + h.f1p_len;
     }
     std::vector<int64_t> st;
-    const std::string e = validate_program(&h, sp, st);
+    std::string e = validate_program(&h, sp, st);
+    if (e.empty() && sp.f1p) e = validate_far1p(&h, sp, st);
     if (!e.empty()) {
       g_err = "ps_validate: " + e;
       return -PS_ESTATE;

@@ -106,6 +106,74 @@ constexpr int GM_CHUNK_K = 512;   // max virtual k per work item (shared-memory 
 constexpr int GN_CHUNK_K = 512;   // same for narrow tiles (warp-specialised kernel, two tables)
 constexpr int GM_MAXSEG = 96;     // max segments per work item
 
+// ---- one-pass far-field apply of narrow solves (nrhs <= 8; DESIGN.md §6 "far1p") ----
+// Z_F w over every far block from ONE read of its factors (Eqs. 11, 13: the
+// symmetric pair Z_ij = U V^T, Z_ji = V U^T). Per low-rank block, with F1 / F2 the factors
+// (U / V or V / U, F1 the shorter one) copied rows-major (row a = r contiguous complex) into
+// the FB arena and x = w in Morton order:
+//   p1 = F1^T x1,  p2 = F2^T x2,  y2 = F2 p1,  y1 = F1 p2
+// (y1 / y2 = that block's contribution to the rows of F1 / F2). A dense (rank-capped, R18)
+// block D (m x n) is read as G = D or D^T, rows-major with the shorter row r = min(m, n):
+//   y1 = G x2 (rows of G; x2 = the vector of G's columns),  y2 = G^T x1 (r rows).
+// Contributions go to per-block pieces of P, summed per leaf in a fixed order (far_reduce):
+// no float atomics. Work units: a pack of small blocks (each applied whole by one warp), or
+// one big block, cut into row chunks applied in order by ONE CTA (F1 chunks -> p1; F2 chunks
+// -> y2 rows and p2; F1 chunks again -> y1 rows), so no unit waits on another.
+constexpr int F1P_CH = 1216;      // factor elements staged per item (19 KB; 3 stages + scratch: 2 CTAs / SM)
+constexpr int F1P_RMAX = 64;      // max rank (dense: shorter side) of a block on this path
+constexpr int F1P_XCH = 512;      // x rows x nrhs staged per item (complex elements)
+constexpr int F1P_PACK = 32;      // max blocks per pack item
+constexpr int F1P_NS = 3;         // shared-memory ring stages of the far1p kernel
+constexpr int F1P_CWARPS = 8;     // consumer warps of the far1p kernel
+struct FBlk {
+  int64_t o1, o2;          // element offsets (operator base) of F1 (n1 x r) / F2 (n2 x r); dense: G, -1
+  int64_t x1, x2;          // first row of x1 / x2 in the Morton vector (rows, not elements)
+  int64_t xa;              // first row of x1 in the gathered x arena XA (x2 follows: XA = [x1 | x2] per block)
+  int64_t pad0;
+  int64_t y1, y2;          // first row of the pieces y1 (n1 rows) / y2 (n2 rows; dense: r rows)
+  int32_t n1, n2, r;
+  int32_t dense;
+  int32_t nc1, nc2;        // big blocks: row chunks of F1 / F2
+  int32_t xo1, xo2;        // packed blocks: first row of x1 / x2 in the item's staged x rows
+};
+struct FItem {
+  int64_t off;             // first element of the item's contiguous factor range (operator base)
+  int64_t xa, xa2;         // staged x rows: XA rows [xa, xa + xn), then (dense big) [xa2, xa2 + xn2)
+  int32_t xn, xn2;
+  int32_t len;             // elements (<= F1P_CH)
+  int32_t kind;            // 0 pack of whole blocks [b, b + nb); big block b, chunk nb, rows [a0, a1):
+                           // 1 F1 rows (p1), 2 F2 rows (y2, p2), 3 F1 rows (y1), 4 dense G rows (y1, y2);
+                           // -1 (kernel-internal) end of the CTA's work
+  int32_t b, nb;           // pack: first block, count; big: block, chunk index
+  int32_t a0, a1;          // big: row range of the chunk; pack: a0 = its staged x rows
+};
+struct FUnit {             // one ticket of work: items [i0, i0 + n) (a pack, or every chunk of a big block)
+  int64_t i0;
+  int32_t n, pad;
+};
+struct Far1pArgs {
+  const FUnit* units;
+  int64_t nunits;
+  const FItem* items;
+  const FBlk* blks;
+  const double2* A;        // operator base (d_op)
+  const double2* x;        // XA: the x rows of every block gathered from w ([x1 | x2] per block, row-major R)
+  double2* y;              // pieces, rows x R row-major
+  int32_t* cnt;            // [0]: unit ticket (zeroed per launch)
+  int32_t R;
+  int32_t skip;            // timing experiments only (PS_F1P_SKIP): 1 packs, 2 big units not computed
+  int32_t grid;            // > 0: at most this many CTAs (PS_F1P_GRID); else one per resident slot
+};
+void launch_far1p(const Far1pArgs& a, cudaStream_t st);
+int far1p_resident_ctas(int R);
+// Z[lrow[l] R + e] = sum_{q in [lptr[l], lptr[l+1])} y[poff[q] R + e], e < lsz[l] R (rows; list order)
+void launch_far_reduce(int64_t nl, const int64_t* lptr, const int64_t* poff, const int64_t* lrow,
+                       const int32_t* lsz, const double2* y, double2* Z, int R, cudaStream_t st);
+// FB arena from the far stacks: run d copies rows x r elements, element (a, k) from
+// src[so + a ss + k sk] to dst[do + a r + k] (operator base)
+struct FCopy { int64_t dst, src, ss, sk; int32_t rows, r; };
+void launch_fb_gather(int64_t n, const FCopy* runs, double2* base, cudaStream_t st);
+
 // ---- kernel launchers (ps_kernels.cu) ----
 // grid <= 0: one persistent CTA per resident slot (148 SMs x occupancy).
 void launch_flow(const FlowArgs& a, int grid, cudaStream_t st);

@@ -1413,6 +1413,478 @@ void launch_flow(const FlowArgs& a, int grid, cudaStream_t st) {
 }
 
 // ---------------------------------------------------------------------------
+// One-pass far-field apply of narrow solves (far1p; ps_internal.h).
+// Persistent, warp-specialised: a producer warp takes work units from a global ticket (a
+// pack of small blocks, or ONE whole big block: its F1 chunks, F2 chunks, F1 chunks again) and
+// stages every item of the unit into a ring of F1P_NS shared-memory stages with bulk async
+// copies (cp.async.bulk -> UBLKCP; completion counted on the stage's mbarrier): the item's
+// contiguous factor range, its block descriptors and the x rows it reads. Eight consumer
+// warps compute out of shared memory, each walking the ring on its own (one arrival on the
+// stage's empty barrier per warp): per block warp-level colsum (lane = (row group, column k),
+// row groups added in a fixed order) and rowsum (lane per row). A big block never leaves its
+// CTA: its column sums accumulate in per-warp shared-memory partials, summed in warp order at
+// the two phase changes (consumer named barrier), so there are no inter-CTA waits; the second
+// read of F1 follows its first by the block's own factor bytes (L2-resident for all but the
+// largest blocks).
+constexpr int F1P_THREADS = 32 * (F1P_CWARPS + 1);       // + the producer warp
+constexpr int F1P_GK = 33 * 32;                          // colsum lane-map table entries (r = 0..32)
+constexpr int F1P_STAGE_BYTES = 16 * (F1P_CH + F1P_XCH) + (int)sizeof(FBlk) * F1P_PACK + 64;
+static_assert(sizeof(FBlk) % 16 == 0, "FBlk is bulk-copied");
+static_assert(F1P_STAGE_BYTES % 16 == 0, "stages are bulk-copy destinations");
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void f1p_cbar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * F1P_CWARPS) : "memory"); }
+
+// dst[k ds + c] (+)= sum_{a in [a_lo, a_hi)} F[a r + k] x[a R + c], k < r, c < R (one warp; F and
+// x in shared memory; accum: add to dst). r <= 32: lane = (g, k) with G = 32 / r row groups
+// (rows a = a_lo + g mod G), two accumulators per lane (alternate rows), the G group sums added
+// in g order through shuffles; r > 32: lane per k in two passes. Fixed order for a given r.
+// Columns c in [R, NR) are computed on whatever follows in shared memory and never stored.
+template <int NR>
+__device__ __forceinline__ void f1p_colsum_w(const double2* F, int a_lo, int a_hi, int r, const double2* x, int R,
+                                             double2* dst, int ds, bool accum, int lane, const uint16_t* gk) {
+  // gk[r * 32 + lane] = (g << 8) | k for 1 <= r <= 32, gk[F1P_GK + r] = G = 32 / r (built once per CTA)
+  const int G = r <= 32 ? gk[F1P_GK + r] : 1;
+  for (int kk = 0; kk < r; kk += 32) {
+    int g = 0, k = kk + lane;
+    if (r <= 32) { const int e = gk[r * 32 + lane]; g = e >> 8; k = e & 255; }
+    double2 s[NR], t[NR];
+#pragma unroll
+    for (int c = 0; c < NR; ++c) s[c] = t[c] = make_double2(0.0, 0.0);
+    if (g < G && k < r) {
+      const int fs = G * r, xs = G * R;
+      const double2* fp = F + (a_lo + g) * r + k;
+      const double2* xp = x + (a_lo + g) * R;
+      int a = a_lo + g;
+      for (; a + G < a_hi; a += 2 * G) {
+        const double2 f0 = fp[0], f1 = fp[fs];
+#pragma unroll
+        for (int c = 0; c < NR; ++c) {
+          cfma(s[c], f0, xp[c]);
+          cfma(t[c], f1, xp[xs + c]);
+        }
+        fp += 2 * fs;
+        xp += 2 * xs;
+      }
+      if (a < a_hi) {
+        const double2 f0 = fp[0];
+#pragma unroll
+        for (int c = 0; c < NR; ++c) cfma(s[c], f0, xp[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < NR; ++c) { s[c].x += t[c].x; s[c].y += t[c].y; }
+    }
+    if (G > 1) {
+#pragma unroll
+      for (int c = 0; c < NR; ++c) t[c] = s[c];
+      for (int g2 = 1; g2 < G; ++g2) {
+        const int src = min(31, k + g2 * r);
+#pragma unroll
+        for (int c = 0; c < NR; ++c) {
+          t[c].x += __shfl_sync(0xffffffffu, s[c].x, src);
+          t[c].y += __shfl_sync(0xffffffffu, s[c].y, src);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < NR; ++c) s[c] = t[c];
+    }
+    if (g == 0 && k < r) {
+      double2* d = dst + k * ds;
+#pragma unroll
+      for (int c = 0; c < NR; ++c)
+        if (c < R) {
+          double2 v = s[c];
+          if (accum) { const double2 o = d[c]; v.x = o.x + v.x; v.y = o.y + v.y; }
+          d[c] = v;
+        }
+    }
+    if (r <= 32) break;
+  }
+}
+
+// y[a R + c] = sum_k F[a r + k] q[k NR + c] for rows a in [a_lo, a_hi), c < R (one warp). L lanes
+// per row (L = the power of two <= 8 that keeps the warp busy on few rows; k = sub, sub + L, ...,
+// the L partial sums added by a fixed xor butterfly); with L = 1 (>= 32 rows) k is rotated per
+// row for even r so a quarter warp's 16-byte loads hit distinct bank groups. Two accumulators.
+template <int NR, bool MULTI>
+__device__ __forceinline__ void f1p_rowsum(const double2* F, int a_lo, int a_hi, int r, const double2* q, int R,
+                                           double2* __restrict__ y, int lane) {
+  const int nrows = a_hi - a_lo;
+  int L = 1;
+  if (MULTI)
+    while (L < 8 && 2 * L <= r && nrows * 2 * L <= 32) L *= 2;
+  const int sub = lane & (L - 1), rpp = 32 / L;          // rows per pass
+  for (int a = a_lo + lane / L; a - (lane / L) < a_hi; a += rpp) {
+    double2 acc[NR], ac2[NR];
+#pragma unroll
+    for (int c = 0; c < NR; ++c) acc[c] = ac2[c] = make_double2(0.0, 0.0);
+    if (a < a_hi) {
+      const double2* Fa = F + a * r;
+      if (L == 1) {
+        int k = (r & 1) ? 0 : (a & 7);                   // any start < r; a & 7 spreads 8 rows over banks
+        while (k >= r) k -= r;
+        int j = 0;
+        for (; j + 2 <= r; j += 2) {
+          const int k1 = (k + 1 == r) ? 0 : k + 1;
+          const double2 f0 = Fa[k], f1 = Fa[k1];
+          const double2* q0 = q + k * NR;
+          const double2* q1 = q + k1 * NR;
+#pragma unroll
+          for (int c = 0; c < NR; ++c) {
+            cfma(acc[c], f0, q0[c]);
+            cfma(ac2[c], f1, q1[c]);
+          }
+          k = (k1 + 1 == r) ? 0 : k1 + 1;
+        }
+        if (j < r) {
+          const double2 f0 = Fa[k];
+          const double2* q0 = q + k * NR;
+#pragma unroll
+          for (int c = 0; c < NR; ++c) cfma(acc[c], f0, q0[c]);
+        }
+      } else {
+        int k = sub;
+        for (; k + L < r; k += 2 * L) {
+          const double2 f0 = Fa[k], f1 = Fa[k + L];
+          const double2* q0 = q + k * NR;
+          const double2* q1 = q + (k + L) * NR;
+#pragma unroll
+          for (int c = 0; c < NR; ++c) {
+            cfma(acc[c], f0, q0[c]);
+            cfma(ac2[c], f1, q1[c]);
+          }
+        }
+        if (k < r) {
+          const double2 f0 = Fa[k];
+          const double2* q0 = q + k * NR;
+#pragma unroll
+          for (int c = 0; c < NR; ++c) cfma(acc[c], f0, q0[c]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < NR; ++c) { acc[c].x += ac2[c].x; acc[c].y += ac2[c].y; }
+    }
+    for (int o = L / 2; o > 0; o >>= 1)
+#pragma unroll
+      for (int c = 0; c < NR; ++c) {
+        acc[c].x += __shfl_xor_sync(0xffffffffu, acc[c].x, o);
+        acc[c].y += __shfl_xor_sync(0xffffffffu, acc[c].y, o);
+      }
+    if (a < a_hi && sub == 0) {
+      double2* ya = y + (int64_t)a * R;
+#pragma unroll
+      for (int c = 0; c < NR; ++c)
+        if (c < R) ya[c] = acc[c];
+    }
+  }
+}
+
+// rows [0, n) of x (stride R) -> q (stride NR), one warp
+template <int NR>
+__device__ __forceinline__ void f1p_to_q(const double2* x, int n, int R, double2* q, int lane) {
+  for (int e = lane; e < n * NR; e += 32) {
+    const int k = e / NR, c = e - k * NR;
+    q[e] = c < R ? x[k * R + c] : make_double2(0.0, 0.0);
+  }
+  __syncwarp();
+}
+
+// A whole small block out of the staged pack, one warp (q1 / q2: this warp's scratch).
+template <int NR>
+__device__ void f1p_small(const Far1pArgs& a, const FBlk& b, const double2* F, int64_t off0, const double2* X,
+                          double2* q1, double2* q2, int lane, const uint16_t* gk) {
+  const int R = a.R;
+  const double2* F1 = F + (b.o1 - off0);
+  const double2* x1 = X + b.xo1 * R;
+  const double2* x2 = X + b.xo2 * R;
+  if (b.dense) {
+    // G (n1 x r): y1 = G x2 (rows of G), y2 = G^T x1 (one per column of G)
+    f1p_to_q<NR>(x2, b.r, R, q2, lane);
+    f1p_rowsum<NR, false>(F1, 0, b.n1, b.r, q2, R, a.y + b.y1 * R, lane);
+    f1p_colsum_w<NR>(F1, 0, b.n1, b.r, x1, R, a.y + b.y2 * R, R, false, lane, gk);
+    __syncwarp();
+    return;
+  }
+  const double2* F2 = F + (b.o2 - off0);
+  f1p_colsum_w<NR>(F1, 0, b.n1, b.r, x1, R, q1, NR, false, lane, gk);
+  f1p_colsum_w<NR>(F2, 0, b.n2, b.r, x2, R, q2, NR, false, lane, gk);
+  __syncwarp();
+  f1p_rowsum<NR, false>(F2, 0, b.n2, b.r, q1, R, a.y + b.y2 * R, lane);
+  f1p_rowsum<NR, false>(F1, 0, b.n1, b.r, q2, R, a.y + b.y1 * R, lane);
+  __syncwarp();
+}
+
+// q[e] = sum over the consumer warps w (in order) of part_w[e], e < n (all consumer threads)
+__device__ __forceinline__ void f1p_warp_sum(const double2* part, int wstride, int n, double2* q) {
+  for (int e = threadIdx.x; e < n; e += 32 * F1P_CWARPS) {
+    double2 s = part[e];
+    for (int v = 1; v < F1P_CWARPS; ++v) {
+      const double2 t = part[v * wstride + e];
+      s.x += t.x; s.y += t.y;
+    }
+    q[e] = s;
+  }
+}
+
+template <int NR>
+__global__ void __launch_bounds__(F1P_THREADS, NR <= 2 ? 2 : 1) far1p_kernel(Far1pArgs a) {
+  // ring stages: F1P_NS, two at 8 columns (the scratch grows with the columns)
+  constexpr int NS = NR >= 8 ? 2 : F1P_NS;
+  extern __shared__ __align__(128) unsigned char f1p_sm[];
+  __shared__ __align__(8) uint64_t full[NS], empty[NS];
+  // per consumer warp 2 x F1P_RMAX x NR (a pack's q1 / q2; a big block's column-sum partial is
+  // the first half), then the big block's final column sums (F1P_RMAX x NR)
+  double2* scr = (double2*)(f1p_sm + NS * F1P_STAGE_BYTES);
+  double2* qf = scr + F1P_CWARPS * 2 * F1P_RMAX * NR;
+  auto stF = [&](int s) { return (double2*)(f1p_sm + s * F1P_STAGE_BYTES); };
+  auto stX = [&](int s) { return stF(s) + F1P_CH; };
+  auto stB = [&](int s) { return (FBlk*)(stX(s) + F1P_XCH); };
+  auto stI = [&](int s) { return (FItem*)(stB(s) + F1P_PACK); };
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int R = a.R;
+  // colsum lane map for r <= 32: gk[r * 32 + lane] = (g << 8) | k, g = lane / r, k = lane % r;
+  // gk[F1P_GK + r] = 32 / r (division-free lookups in the per-block loops)
+  __shared__ uint16_t gk[F1P_GK + 33];
+  for (int e = tid; e < F1P_GK + 33; e += blockDim.x) {
+    if (e < F1P_GK) {
+      const int rr = e >> 5, l = e & 31;
+      gk[e] = rr ? (uint16_t)(((l / rr) << 8) | (l % rr)) : 0;
+    } else {
+      const int rr = e - F1P_GK;
+      gk[e] = rr ? (uint16_t)(32 / rr) : 1;
+    }
+  }
+  if (tid == 0)
+    for (int s = 0; s < NS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], F1P_CWARPS); }
+  __syncthreads();
+  if (w == F1P_CWARPS) {
+    // ---- producer warp: descriptors come in batches (the unit's FItems, lane j holding item
+    // j of a 32-item window, handed out by shuffles; the next unit's ticket is taken when a unit
+    // starts); every item is 3-4 bulk copies (factor range, block descriptors, its x rows, which
+    // are contiguous in the gathered arena XA), so no descriptor load sits between two fills ----
+    int t = 0;
+    int64_t u = 0, unext = 0;
+    if (lane == 0) u = atomicAdd(a.cnt, 1);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    auto shfl_item = [&](const FItem& L, int j) {
+      FItem r;
+      r.off = __shfl_sync(0xffffffffu, L.off, j);
+      r.xa = __shfl_sync(0xffffffffu, L.xa, j);
+      r.xa2 = __shfl_sync(0xffffffffu, L.xa2, j);
+      r.xn = __shfl_sync(0xffffffffu, L.xn, j);
+      r.xn2 = __shfl_sync(0xffffffffu, L.xn2, j);
+      r.len = __shfl_sync(0xffffffffu, L.len, j);
+      r.kind = __shfl_sync(0xffffffffu, L.kind, j);
+      r.b = __shfl_sync(0xffffffffu, L.b, j);
+      r.nb = __shfl_sync(0xffffffffu, L.nb, j);
+      r.a0 = __shfl_sync(0xffffffffu, L.a0, j);
+      r.a1 = __shfl_sync(0xffffffffu, L.a1, j);
+      return r;
+    };
+    while (u < a.nunits) {
+      if (lane == 0) unext = atomicAdd(a.cnt, 1);       // consumed when this unit ends
+      const FUnit U = a.units[u];
+      for (int base = 0; base < U.n; base += 32) {
+        const int nw = min(32, U.n - base);
+        FItem L{};
+        if (lane < nw) L = a.items[U.i0 + base + lane];
+        for (int j = 0; j < nw; ++j, ++t) {
+          const FItem it = shfl_item(L, j);
+          const int s = t % NS;
+          const int nbl = it.kind == 0 ? it.nb : 1;
+          const uint32_t bytes = 16u * it.len + (uint32_t)sizeof(FBlk) * nbl + 16u * R * (uint32_t)(it.xn + it.xn2);
+          if (t >= NS) mbar_wait(&empty[s], ((t / NS) - 1) & 1);
+          if (lane == 0) {
+            *stI(s) = it;
+            mbar_arrive_tx(&full[s], bytes);
+            bulk_g2s(stF(s), a.A + it.off, 16u * it.len, &full[s]);
+            bulk_g2s(stB(s), a.blks + it.b, (uint32_t)sizeof(FBlk) * nbl, &full[s]);
+            if (it.xn > 0) bulk_g2s(stX(s), a.x + it.xa * R, 16u * R * it.xn, &full[s]);
+            if (it.xn2 > 0) bulk_g2s(stX(s) + it.xn * R, a.x + it.xa2 * R, 16u * R * it.xn2, &full[s]);
+          }
+          __syncwarp();
+        }
+      }
+      u = __shfl_sync(0xffffffffu, unext, 0);
+    }
+    // end marker for the consumers
+    const int s = t % NS;
+    if (t >= NS) mbar_wait(&empty[s], ((t / NS) - 1) & 1);
+    if (lane == 0) {
+      FItem end{};
+      end.kind = -1;
+      *stI(s) = end;
+      mbar_arrive(&full[s]);
+    }
+    return;
+  }
+  // ---- consumer warps ----
+  double2* q1 = scr + (w * 2) * F1P_RMAX * NR;           // pack q1 / big-block partial of this warp
+  double2* q2 = q1 + F1P_RMAX * NR;
+  for (int t = 0;; ++t) {
+    const int s = t % NS;
+    mbar_wait(&full[s], (t / NS) & 1);
+    const FItem it = *stI(s);
+    if (it.kind < 0) break;
+    const double2* F = stF(s);
+    const double2* X = stX(s);
+    const FBlk* B = stB(s);
+    if (a.skip & (it.kind == 0 ? 1 : 2)) {
+      // timing experiment (PS_F1P_SKIP): the item is staged but not computed
+    } else if (it.kind == 0) {
+      for (int j = w; j < it.nb; j += F1P_CWARPS) f1p_small<NR>(a, B[j], F, it.off, X, q1, q2, lane, gk);
+    } else {
+      const FBlk b = B[0];
+      const int h = it.a1 - it.a0, ch = it.nb;
+      const int per = (h + F1P_CWARPS - 1) / F1P_CWARPS;
+      const int lo = min(h, w * per), hi = min(h, lo + per);
+      const int rR = b.r * NR;                           // partials / final sums: r x NR
+      if (it.kind == 4) {                                // dense big: G rows [a0, a1)
+        f1p_to_q<NR>(X + h * R, b.r, R, q2, lane);
+        f1p_rowsum<NR, true>(F, lo, hi, b.r, q2, R, a.y + (b.y1 + it.a0) * R, lane);
+        f1p_colsum_w<NR>(F, lo, hi, b.r, X, R, q1, NR, ch > 0, lane, gk);
+        if (ch == b.nc1 - 1) {                           // y2 = G^T x1: the warps' partials in order
+          __syncwarp();
+          f1p_cbar();
+          f1p_warp_sum(scr, 2 * F1P_RMAX * NR, rR, qf);
+          f1p_cbar();
+          for (int e = tid; e < b.r * R; e += 32 * F1P_CWARPS) {
+            const int k = e / R, c = e - k * R;
+            a.y[b.y2 * R + e] = qf[k * NR + c];
+          }
+          f1p_cbar();
+        }
+      } else if (it.kind == 1) {                         // F1 rows: p1 partial
+        f1p_colsum_w<NR>(F, lo, hi, b.r, X, R, q1, NR, ch > 0, lane, gk);
+      } else if (it.kind == 2) {                         // F2 rows: y2 = F2 p1, p2 partial
+        if (ch == 0) {
+          __syncwarp();
+          f1p_cbar();
+          f1p_warp_sum(scr, 2 * F1P_RMAX * NR, rR, qf);
+          f1p_cbar();
+        }
+        f1p_rowsum<NR, true>(F, lo, hi, b.r, qf, R, a.y + (b.y2 + it.a0) * R, lane);
+        f1p_colsum_w<NR>(F, lo, hi, b.r, X, R, q1, NR, ch > 0, lane, gk);
+      } else {                                           // F1 rows again: y1 = F1 p2
+        if (ch == 0) {
+          __syncwarp();
+          f1p_cbar();
+          f1p_warp_sum(scr, 2 * F1P_RMAX * NR, rR, qf);
+          f1p_cbar();
+        }
+        f1p_rowsum<NR, true>(F, lo, hi, b.r, qf, R, a.y + (b.y1 + it.a0) * R, lane);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+}
+
+template <int NR>
+static size_t far1p_smem() {
+  return (size_t)(NR >= 8 ? 2 : F1P_NS) * F1P_STAGE_BYTES + sizeof(double2) * ((size_t)F1P_CWARPS * 2 + 1) * F1P_RMAX * NR;
+}
+template <int NR>
+static int far1p_resident_of() {
+  static int n = 0;
+  if (n == 0) {
+    int per_sm = 0, dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(far1p_kernel<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)far1p_smem<NR>());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, far1p_kernel<NR>, F1P_THREADS, far1p_smem<NR>());
+    n = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  return n;
+}
+int far1p_resident_ctas(int R) {
+  return R <= 1 ? far1p_resident_of<1>() : R <= 2 ? far1p_resident_of<2>() : R <= 4 ? far1p_resident_of<4>()
+                                                                                    : far1p_resident_of<8>();
+}
+template <int NR>
+static void far1p_go(const Far1pArgs& a, cudaStream_t st) {
+  int g = far1p_resident_of<NR>();
+  if (a.grid > 0 && a.grid < g) g = a.grid;
+  if (g > a.nunits) g = (int)a.nunits;
+  far1p_kernel<NR><<<g, F1P_THREADS, far1p_smem<NR>(), st>>>(a);
+}
+void launch_far1p(const Far1pArgs& a, cudaStream_t st) {
+  if (a.nunits <= 0) return;
+  if (a.R <= 1) far1p_go<1>(a, st);
+  else if (a.R <= 2) far1p_go<2>(a, st);
+  else if (a.R <= 4) far1p_go<4>(a, st);
+  else far1p_go<8>(a, st);
+}
+
+// Per leaf: Z rows = sum of its pieces in list order (one warp per leaf, lanes over the
+// leaf's rows x R elements).
+__global__ void far_reduce_kernel(int64_t nl, const int64_t* __restrict__ lptr, const int64_t* __restrict__ poff,
+                                  const int64_t* __restrict__ lrow, const int32_t* __restrict__ lsz,
+                                  const double2* __restrict__ y, double2* __restrict__ Z, int R) {
+  const int lane = threadIdx.x & 31;
+  const int64_t l = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (l >= nl) return;
+  const int64_t q0 = lptr[l], q1 = lptr[l + 1];
+  const int n = lsz[l] * R;
+  for (int e = lane; e < n; e += 32) {
+    double2 s = make_double2(0.0, 0.0);
+    int64_t q = q0;
+    for (; q + 4 <= q1; q += 4) {
+      const double2 t0 = y[poff[q] * R + e], t1 = y[poff[q + 1] * R + e];
+      const double2 t2 = y[poff[q + 2] * R + e], t3 = y[poff[q + 3] * R + e];
+      s.x += t0.x; s.y += t0.y; s.x += t1.x; s.y += t1.y;
+      s.x += t2.x; s.y += t2.y; s.x += t3.x; s.y += t3.y;
+    }
+    for (; q < q1; ++q) {
+      const double2 t = y[poff[q] * R + e];
+      s.x += t.x; s.y += t.y;
+    }
+    Z[lrow[l] * R + e] = s;
+  }
+}
+void launch_far_reduce(int64_t nl, const int64_t* lptr, const int64_t* poff, const int64_t* lrow,
+                       const int32_t* lsz, const double2* y, double2* Z, int R, cudaStream_t st) {
+  if (nl <= 0) return;
+  const int64_t thr = nl * 32;
+  far_reduce_kernel<<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(nl, lptr, poff, lrow, lsz, y, Z, R);
+}
+
+__global__ void fb_gather_kernel(int64_t n, const FCopy* __restrict__ runs, double2* __restrict__ base) {
+  for (int64_t d = blockIdx.x; d < n; d += gridDim.x) {
+    const FCopy c = runs[d];
+    const int64_t tot = (int64_t)c.rows * c.r;
+    for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) {
+      const int64_t row = e / c.r, k = e - row * c.r;
+      base[c.dst + e] = base[c.src + row * c.ss + k * c.sk];
+    }
+  }
+}
+void launch_fb_gather(int64_t n, const FCopy* runs, double2* base, cudaStream_t st) {
+  if (n <= 0) return;
+  fb_gather_kernel<<<(unsigned)(n < 148 * 64 ? n : 148 * 64), 128, 0, st>>>(n, runs, base);
+}
+
+// ---------------------------------------------------------------------------
 // Batched explicit inverse of the scaled diagonal blocks (Eqs. 23, 30):
 // in-place Gauss-Jordan with partial pivoting (max |z|^2, lowest row on ties),
 // one CTA per leaf. Blocks up to SMEM_N fit shared memory; larger ones are

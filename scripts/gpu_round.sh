@@ -33,7 +33,7 @@ timeout 900 ncu --nvtx --nvtx-include "timed/" --metrics gpu__time_duration.sum 
 python scripts/launch_summary.py $O/ncu_launches_C4.csv > $O/ncu_launches_C4_summary.json 2>/dev/null
 for NR in 360 1; do
   python scripts/ncu_solve.py --config C4 --nrhs $NR > $O/plain_solve_$NR.log 2>&1 && \
-  timeout 900 ncu --profile-from-start off --set full --import-source on --clock-control none -k regex:flow_kernel \
+  timeout 900 ncu --profile-from-start off --set full --import-source on --clock-control none -k "regex:flow_kernel|far1p|far_reduce" \
      -o /tmp/full_C4_$NR python scripts/ncu_solve.py --config C4 --nrhs $NR > /dev/null 2>&1; echo "ncu_full_$NR=$?"
   python scripts/ncu_summary.py /tmp/full_C4_$NR.ncu-rep --config C4 --nrhs $NR > $O/ncu_full_C4_${NR}.json 2>/dev/null
   ncu -i /tmp/full_C4_$NR.ncu-rep --page source --csv --print-source sass 2>/dev/null | gzip > $O/ncu_source_C4_${NR}.csv.gz

@@ -67,3 +67,28 @@ def test_variant_matches_oracle(cfgdata, tmp_path, env, nrhs):
     assert rel_l2_cols(x, ref.x).max() <= 1e-11
     assert np.allclose(it[0], ref.it0, rtol=1e-11)
     assert np.allclose(it[1], ref.it1, rtol=1e-10)
+
+
+# The one-pass far apply of narrow solves (far1p): taken by default for nrhs <= 8
+# where the far field is large (C4, C5); PS_FAR1P=1 forces it, 0 keeps the two-stage far field
+# inside one program launch; PS_F1P_CHUNK cuts
+# the items smaller than the 2048-element default, so most blocks of the small configs take
+# the big-block path (alpha / gamma / beta chunks, dense chunks with a last-arriver sum) with
+# many chunks per block and many waits.
+@pytest.mark.parametrize("env", [{"PS_FAR1P": "1"}, {"PS_FAR1P": "0"}, {"PS_FAR1P": "1", "PS_F1P_CHUNK": "64"},
+                                 {"PS_FAR1P": "1", "PS_F1P_CHUNK": "300"}, {"PS_FAR1P": "1", "PS_F1P_CHUNK": "128"},
+                                 {}],
+                         ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default")
+@pytest.mark.parametrize("nrhs", [1, 3, 8])
+@pytest.mark.parametrize("cfg", ["C1", "T2"])
+def test_far1p_matches_oracle(cfgdata, tmp_path, env, nrhs, cfg):
+    from hmgen.synth import random_rhs
+    from oracle import compute_scaling, read_hm, solve
+    from tests.conftest import rel_l2_cols
+    path = cfgdata(cfg)["hm"]
+    x, it = _run(path, nrhs, env, str(tmp_path / "x.npy"))
+    H = read_hm(path)
+    ref = solve(H, compute_scaling(H), random_rhs(H.N, nrhs, 4))
+    assert rel_l2_cols(x, ref.x).max() <= 1e-11
+    assert np.allclose(it[0], ref.it0, rtol=1e-11)
+    assert np.allclose(it[1], ref.it1, rtol=1e-10)

@@ -183,15 +183,34 @@ def test_solve_program_edge_cases_validate(synthfile):
             validate(path, nrhs)
 
 
-@pytest.mark.parametrize("brk,what", [(1, "unordered"), (2, "precedes"), (3, "outside its region")])
+def test_far1p_tables_validate(cfgdata):
+    """nrhs <= 8: the program is two launches around the far1p apply; both the program and
+    the far1p tables pass the checker, also with small items (many big-block chunks)."""
+    import subprocess
+    import sys
+    path = cfgdata("C1")["hm"]
+    for env in ({"PS_FAR1P": "1"}, {"PS_FAR1P": "1", "PS_F1P_CHUNK": "64"}):
+        code = ("from paper_2109_04129_b200.binding import validate\n"
+                f"v = validate({path!r}, 1)\n"
+                "assert v['far1p_items'] and v['far1p_items'] > 0, v\n"
+                f"assert validate({path!r}, 64)['far1p_items'] is None\n"
+                "print(v['far1p_items'])\n")
+        r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=dict(os.environ, **env),
+                           capture_output=True, text=True, timeout=120)
+        assert r.returncode == 0, r.stderr[-800:]
+
+
+@pytest.mark.parametrize("brk,what", [(1, "unordered"), (2, "precedes"), (3, "outside its region"),
+                                      (4, "out of order"), (5, "outside the FB arena")])
 def test_validator_catches_broken_tables(cfgdata, brk, what):
-    """The checker itself: a dropped dependency, an item moved before its producer and
-    an operator offset outside its region are each reported."""
+    """The checker itself: a dropped dependency, an item moved before its producer,
+    an operator offset outside its region, a far1p consumer moved before its producers
+    and a far1p item outside the FB arena are each reported."""
     import subprocess
     import sys
     path = cfgdata("C1")["hm"]
     code = ("from paper_2109_04129_b200.binding import validate\n"
             f"validate({path!r}, 1)\n")
-    env = dict(os.environ, PS_VALIDATE_BREAK=str(brk))
+    env = dict(os.environ, PS_VALIDATE_BREAK=str(brk), PS_FAR1P="1", PS_F1P_CHUNK="64")   # 64: big far1p blocks
     r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=120)
     assert r.returncode != 0 and what in r.stderr, r.stderr[-500:]
