@@ -32,6 +32,10 @@
 #include <unordered_map>
 #include <vector>
 #include <queue>
+#include <condition_variable>
+#include <exception>
+#include <mutex>
+#include <thread>
 #include <tuple>
 
 using namespace ps;
@@ -703,6 +707,7 @@ struct DistPlan {
 struct ps_handle {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t ustream = nullptr;          // ps_setup: table uploads (overlapping the level kernels)
   std::string err;
   // ---- file ----
   int64_t N = 0, nl = 0, nnear = 0, nfar = 0;
@@ -1369,6 +1374,8 @@ struct SetupLevel {
   Table asmb, panel;
   DevBuf<int32_t> d_ids, d_sz;
   DevBuf<int64_t> d_src, d_ld, d_dst;
+  std::vector<int32_t> ids, sz;                       // host side of the inverse launch
+  std::vector<int64_t> src, ld, dst;
   int64_t nlev = 0;
   int maxn = 0;
   double t_upload = 0;
@@ -1378,6 +1385,19 @@ struct SetupLevel {
     asmb.S = panel.S = nullptr;
     nlev = 0;
     maxn = 0;
+  }
+  // take the host tables built (by a worker thread) into `o`, keeping this level's device buffers
+  void adopt(SetupLevel& o) {
+    auto keep = [](Table& dst, Table& src) {
+      src.d_tasks = std::move(dst.d_tasks); src.d_terms = std::move(dst.d_terms); src.d_work = std::move(dst.d_work);
+      src.d_counters = std::move(dst.d_counters); src.d_partial = std::move(dst.d_partial);
+      dst = std::move(src);
+    };
+    keep(asmb, o.asmb);
+    keep(panel, o.panel);
+    ids.swap(o.ids); sz.swap(o.sz); src.swap(o.src); ld.swap(o.ld); dst.swap(o.dst);
+    nlev = o.nlev;
+    maxn = o.maxn;
   }
 };
 
@@ -1445,25 +1465,30 @@ void build_setup_level(ps_handle* h, const std::vector<int32_t>& leaves, SetupLe
     }
     sp.panel.close_batch();
   }
-  const auto tu0 = std::chrono::steady_clock::now();
-  sp.asmb.upload(h->stream, &h->ring);
-  sp.panel.upload(h->stream, &h->ring);
-  sp.t_upload = std::chrono::duration<double>(std::chrono::steady_clock::now() - tu0).count();
-  std::vector<int32_t> sz;
-  std::vector<int64_t> src, ld, dst;
+  sp.ids = leaves;
+  sp.sz.clear(); sp.src.clear(); sp.ld.clear(); sp.dst.clear();
   for (int32_t p : leaves) {
-    sz.push_back(h->nsz[p]);
-    src.push_back(h->Woff[p]);
-    ld.push_back(h->nsz[p]);
-    dst.push_back(h->Doff[p]);
+    sp.sz.push_back(h->nsz[p]);
+    sp.src.push_back(h->Woff[p]);
+    sp.ld.push_back(h->nsz[p]);
+    sp.dst.push_back(h->Doff[p]);
     sp.maxn = std::max(sp.maxn, h->nsz[p]);
   }
   sp.nlev = (int64_t)leaves.size();
-  sp.d_ids.upload(leaves, h->stream, &h->ring);
-  sp.d_sz.upload(sz, h->stream, &h->ring);
-  sp.d_src.upload(src, h->stream, &h->ring);
-  sp.d_ld.upload(ld, h->stream, &h->ring);
-  sp.d_dst.upload(dst, h->stream, &h->ring);
+}
+
+// Device side of a level: its tables and inverse lists, through the pinned ring on the upload
+// stream u (the caller orders u after the kernels that last used these buffers)
+void upload_setup_level(ps_handle* h, SetupLevel& sp, cudaStream_t u) {
+  const auto tu0 = std::chrono::steady_clock::now();
+  sp.asmb.upload(u, &h->ring);
+  sp.panel.upload(u, &h->ring);
+  sp.d_ids.upload(sp.ids, u, &h->ring);
+  sp.d_sz.upload(sp.sz, u, &h->ring);
+  sp.d_src.upload(sp.src, u, &h->ring);
+  sp.d_ld.upload(sp.ld, u, &h->ring);
+  sp.d_dst.upload(sp.dst, u, &h->ring);
+  sp.t_upload = std::chrono::duration<double>(std::chrono::steady_clock::now() - tu0).count();
 }
 
 // Upload the restacked far factors (once) and point Fbase at them.
@@ -3355,67 +3380,163 @@ ps_status finish_dist(ps_handle* const* hs, int nh, int64_t nrhs, const void* B,
 // The positions, elimination level by elimination level (setup tables are built,
 // launched and freed per level): mode as build_setup_level; modes 0 and 2 also invert
 // the scaled diagonal blocks (Eqs. 23, 30) and form the alpha panels (Eq. 16).
+// The elimination levels of ps_setup, bottom-up. Each level's host tables (assembly, panel,
+// inverse lists) depend only on the structure, so worker threads build them ahead of the GPU
+// (at most PS_SETUP_AHEAD levels ahead); the main thread uploads and launches level after level
+// without waiting for the device (stream order protects the reused device buffers), and the
+// singular-block flags of every level are checked once at the end.
 void setup_levels(ps_handle* h, cudaStream_t s, const std::vector<int32_t>& pos, int mode) {
   if (pos.empty()) return;
   using clk = std::chrono::steady_clock;
   static const int verbose = env_int("PS_VERBOSE", 0);
-  double t_build = 0, t_wait = 0, t_up = 0;
+  double t_wait_host = 0, t_up = 0;
   const auto t00 = clk::now();
   std::vector<std::vector<int32_t>> lv(h->max_height + 1);
   for (int32_t p : pos) lv[mode == 1 ? 0 : h->height[p]].push_back(p);   // phase B: one batch
+  std::vector<const std::vector<int32_t>*> order;
+  for (const auto& l : lv)
+    if (!l.empty()) order.push_back(&l);
+  const int L = (int)order.size();
   DevBuf<int32_t> d_status;
   d_status.alloc(std::max<int64_t>((int64_t)pos.size(), 1));
-  std::vector<int32_t> status;
-  SetupLevel sp;                                     // device buffers reused level to level
-  for (const auto& leaves : lv) {
-    if (leaves.empty()) continue;
-    sp.reset();
-    const auto t0 = clk::now();
-    build_setup_level(h, leaves, sp, mode);
-    t_build += std::chrono::duration<double>(clk::now() - t0).count();
-    t_up += sp.t_upload;
-    // Eq. 21 (left-looking): assemble W_p = [Z~_pp | Z~_p,struct(p)]
-    sp.asmb.launch_all(h->d_W.p, h->d_near.p, h->d_P.p, h->d_W.p, s);
-    if (mode != 1) {
-      const int64_t nlev = sp.nlev;
-      CK(cudaMemsetAsync(d_status.p, 0, sizeof(int32_t) * nlev, s));
-      // Eqs. 23/30: D_p^{-1}
-      launch_inverse(nlev, sp.d_ids.p, sp.d_sz.p, sp.d_src.p, sp.d_ld.p, sp.d_dst.p, h->d_W.p, h->d_D.p,
-                     d_status.p, sp.maxn, s);
-      status.assign(nlev, 0);
-      CK(cudaMemcpyAsync(status.data(), d_status.p, sizeof(int32_t) * nlev, cudaMemcpyDeviceToHost, s));
-      const auto t1 = clk::now();
-      CK(cudaStreamSynchronize(s));
-      t_wait += std::chrono::duration<double>(clk::now() - t1).count();
-      for (int64_t i = 0; i < nlev; ++i)
-        if (status[i])
-          throw PsError{PS_ESINGULAR, "singular scaled diagonal block at elimination position " +
-                                          std::to_string(leaves[i]) + " (leaf " + std::to_string(h->leaf_at[leaves[i]]) +
-                                          ")"};
-      // Eq. 16: alpha_p* = -D_p^{-1} Z~_p*
-      sp.panel.launch_all(h->d_P.p, nullptr, h->d_D.p, h->d_W.p, s);
+  CK(cudaMemsetAsync(d_status.p, 0, sizeof(int32_t) * d_status.n, s));
+  static const int nthreads = std::max(1, std::min(env_int("PS_SETUP_THREADS", 8),
+                                                   (int)std::thread::hardware_concurrency()));
+  static const int ahead = std::max(1, env_int("PS_SETUP_AHEAD", 32));
+  std::vector<std::unique_ptr<SetupLevel>> built(L);
+  std::vector<char> ready(L, 0);
+  std::mutex mu;
+  std::condition_variable cv;
+  int next = 0, consumed = 0;
+  bool stop = false;
+  std::exception_ptr err;
+  auto worker = [&] {
+    for (;;) {
+      int i;
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return stop || (next < L && next < consumed + ahead); });
+        if (stop || next >= L) return;
+        i = next++;
+      }
+      auto lvl = std::make_unique<SetupLevel>();
+      try {
+        build_setup_level(h, *order[i], *lvl, mode);
+      } catch (...) {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!err) err = std::current_exception();
+      }
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        built[i] = std::move(lvl);
+        ready[i] = 1;
+      }
+      cv.notify_all();
     }
-    const auto t1 = clk::now();
-    CK(cudaStreamSynchronize(s));                    // the level's tables are freed here
-    t_wait += std::chrono::duration<double>(clk::now() - t1).count();
+  };
+  std::vector<std::thread> pool;
+  for (int t = 0; t < std::min(nthreads, L); ++t) pool.emplace_back(worker);
+  auto finish = [&] {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      stop = true;
+    }
+    cv.notify_all();
+    for (auto& th : pool) th.join();
+    pool.clear();
+  };
+  // two device table sets used by alternate levels: level i's uploads (upload stream) wait for
+  // the kernels of level i - 2 (the previous user of the set); its kernels wait for its uploads
+  SetupLevel dev[2];
+  if (!h->ustream) CK(cudaStreamCreateWithFlags(&h->ustream, cudaStreamNonBlocking));
+  cudaEvent_t kdone[2], udone;
+  for (auto& e : kdone) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&udone, cudaEventDisableTiming));
+  struct EvGuard {
+    cudaEvent_t* k; cudaEvent_t u;
+    ~EvGuard() { cudaEventDestroy(k[0]); cudaEventDestroy(k[1]); cudaEventDestroy(u); }
+  } evg{kdone, udone};
+  int64_t off = 0;
+  try {
+    for (int i = 0; i < L; ++i) {
+      SetupLevel& sp = dev[i & 1];
+      const auto t0 = clk::now();
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return ready[i] || err; });
+        if (err) std::rethrow_exception(err);
+        sp.adopt(*built[i]);
+        built[i].reset();
+        consumed = i + 1;
+      }
+      cv.notify_all();
+      t_wait_host += std::chrono::duration<double>(clk::now() - t0).count();
+      if (mode == 2) sp.asmb.S = h->d_W.p;
+      if (i >= 2) CK(cudaStreamWaitEvent(h->ustream, kdone[i & 1], 0));
+      upload_setup_level(h, sp, h->ustream);
+      CK(cudaEventRecord(udone, h->ustream));
+      CK(cudaStreamWaitEvent(s, udone, 0));
+      t_up += sp.t_upload;
+      // Eq. 21 (left-looking): assemble W_p = [Z~_pp | Z~_p,struct(p)]
+      sp.asmb.launch_all(h->d_W.p, h->d_near.p, h->d_P.p, h->d_W.p, s);
+      if (mode != 1) {
+        // Eqs. 23/30: D_p^{-1}
+        launch_inverse(sp.nlev, sp.d_ids.p, sp.d_sz.p, sp.d_src.p, sp.d_ld.p, sp.d_dst.p, h->d_W.p, h->d_D.p,
+                       d_status.p + off, sp.maxn, s);
+        // Eq. 16: alpha_p* = -D_p^{-1} Z~_p*
+        sp.panel.launch_all(h->d_P.p, nullptr, h->d_D.p, h->d_W.p, s);
+      }
+      CK(cudaEventRecord(kdone[i & 1], s));
+      off += sp.nlev;
+    }
+  } catch (...) {
+    finish();
+    throw;
+  }
+  finish();
+  std::vector<int32_t> status(pos.size(), 0);
+  CK(cudaMemcpyAsync(status.data(), d_status.p, sizeof(int32_t) * status.size(), cudaMemcpyDeviceToHost, s));
+  const auto t1 = clk::now();
+  CK(cudaStreamSynchronize(s));
+  const double t_wait = std::chrono::duration<double>(clk::now() - t1).count();
+  if (mode != 1) {
+    int64_t o = 0;
+    for (int i = 0; i < L; ++i)
+      for (size_t j = 0; j < order[i]->size(); ++j, ++o)
+        if (status[o]) {
+          const int32_t p = (*order[i])[j];
+          throw PsError{PS_ESINGULAR, "singular scaled diagonal block at elimination position " + std::to_string(p) +
+                                          " (leaf " + std::to_string(h->leaf_at[p]) + ")"};
+        }
   }
   if (verbose)
-    std::fprintf(stderr, "[ps] setup mode %d: %zu positions, %.1f ms (host tables %.1f ms of which uploads %.1f ms, "
-                 "waiting on the GPU %.1f ms)\n", mode, pos.size(), 1e3 * std::chrono::duration<double>(clk::now() - t00).count(),
-                 1e3 * t_build, 1e3 * t_up, 1e3 * t_wait);
+    std::fprintf(stderr, "[ps] setup mode %d: %zu positions, %d levels, %.1f ms (waiting on host tables %.1f ms, "
+                 "uploads %.1f ms, final wait on the GPU %.1f ms, %d builder threads)\n", mode, pos.size(), L,
+                 1e3 * std::chrono::duration<double>(clk::now() - t00).count(), 1e3 * t_wait_host, 1e3 * t_up,
+                 1e3 * t_wait, nthreads);
 }
 
 // After the scaling: free the setup-only arenas, upload the far stacks, form T_c.
 void setup_finish(ps_handle* h, cudaStream_t s) {
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(s));
   h->d_W.release();
   h->d_near.release();
+  const auto t1 = clk::now();
   ensure_far(h, s);
+  const auto t2 = clk::now();
   h->d_T.alloc(std::max<int64_t>(h->Tlen, 1));
   h->Tbase = (int64_t)(h->d_T.p - h->d_op.p);
   chain_setup(h, s);
   CK(cudaStreamSynchronize(s));
+  static const int verbose = env_int("PS_VERBOSE", 0);
+  if (verbose)
+    std::fprintf(stderr, "[ps] setup finish: %.1f ms (free W / near %.1f, far upload %.1f, chain matrices %.1f)\n",
+                 1e3 * std::chrono::duration<double>(clk::now() - t0).count(),
+                 1e3 * std::chrono::duration<double>(t1 - t0).count(), 1e3 * std::chrono::duration<double>(t2 - t1).count(),
+                 1e3 * std::chrono::duration<double>(clk::now() - t2).count());
   h->plan.reset();                                  // plans made before setup (ps_apply Z_F) are stale
   h->dplan.reset();
   h->setup_done = true;
@@ -3543,12 +3664,22 @@ ps_status ps_setup(ps_handle* h, const ps_setup_opts* opts) {
                                  (ncclComm_t)h->nccl, s));
       setup_sharded(h, s, 1);
     } else {
+      using clk = std::chrono::steady_clock;
+      const auto t0 = clk::now();
       if (opts && opts->ordering == 2) reorder_rcm(h, s);
       h->d_W.alloc(std::max<int64_t>(h->Wlen, 1));
+      const auto t1 = clk::now();
       std::vector<int32_t> all(h->nl);
       std::iota(all.begin(), all.end(), 0);
       setup_levels(h, s, all, 0);
+      const auto t2 = clk::now();
       setup_finish(h, s);
+      static const int verbose = env_int("PS_VERBOSE", 0);
+      if (verbose)
+        std::fprintf(stderr, "[ps] ps_setup: %.1f ms (arenas %.1f, levels %.1f, finish %.1f)\n",
+                     1e3 * std::chrono::duration<double>(clk::now() - t0).count(),
+                     1e3 * std::chrono::duration<double>(t1 - t0).count(), 1e3 * std::chrono::duration<double>(t2 - t1).count(),
+                     1e3 * std::chrono::duration<double>(clk::now() - t2).count());
     }
   } catch (const PsError& e) {
     h->d_W.release();
@@ -3959,9 +4090,11 @@ void ps_free(ps_handle* h) {
   }
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
-  cudaStream_t s = h->stream;
+  cudaStream_t s = h->stream, u = h->ustream;
+  if (u) cudaStreamSynchronize(u);
   delete h;
   if (s) cudaStreamDestroy(s);
+  if (u) cudaStreamDestroy(u);
 }
 
 int ps_info(const ps_handle* h, double* out, int n) {

@@ -1889,7 +1889,7 @@ void launch_fb_gather(int64_t n, const FCopy* runs, double2* base, cudaStream_t 
 // in-place Gauss-Jordan with partial pivoting (max |z|^2, lowest row on ties),
 // one CTA per leaf. Blocks up to SMEM_N fit shared memory; larger ones are
 // eliminated in place in the destination buffer (L2-resident).
-constexpr int SMEM_N = 80;
+constexpr int SMEM_N = 117;     // n^2 + n complex + n int + the static reductions <= 227 KB
 
 __global__ void __launch_bounds__(512)
 inverse_kernel(const int32_t* __restrict__ leaf_ids, const int32_t* __restrict__ sizes,
@@ -2010,13 +2010,22 @@ void launch_inverse(int64_t nl, const int32_t* leaf_ids, const int32_t* sizes, c
                     const int64_t* src_ld, const int64_t* dst_off, const double2* Wbase,
                     double2* Dbase, int32_t* status, int max_n, cudaStream_t st) {
   if (nl <= 0) return;
-  const int nn = max_n <= SMEM_N ? max_n : 0;
+  int nn = max_n <= SMEM_N ? max_n : 0;
   size_t smem = (size_t)nn * nn * sizeof(double2) + (size_t)max_n * sizeof(double2) +
                 (size_t)max_n * sizeof(int) + 16;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
+  static int max_dyn = -1;
+  if (max_dyn < 0) {                                   // opt-in limit minus the kernel's static reductions
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, inverse_kernel);
+    max_dyn = optin - (int)fa.sharedSizeBytes;
+    cudaFuncSetAttribute(inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
+  }
+  if ((int64_t)smem > max_dyn) {                       // the n x n block stays in global memory
+    nn = 0;
+    smem = (size_t)max_n * sizeof(double2) + (size_t)max_n * sizeof(int) + 16;
   }
   inverse_kernel<<<(unsigned)nl, 512, smem, st>>>(leaf_ids, sizes, src_off, src_ld, dst_off, Wbase,
                                                   Dbase, status, nn > 0 ? 1 : 0);
