@@ -2648,6 +2648,9 @@ std::string validate_far1p(const ps_handle* h, const SolvePlan& sp, std::vector<
     const int64_t e = (int64_t)(k.n1 + k.n2) * k.r;
     if (covered[j] != e) return msg("block factors not covered exactly once", j);
     if (k.r < 1 || k.r > F1P_RMAX) return msg("block rank outside (0, F1P_RMAX]", j);
+    // the kernel applies a small low-rank block as the stacked [F1; F2]: F2, x2 and y2 follow F1, x1, y1
+    if (!k.dense && (k.o2 != k.o1 + (int64_t)k.n1 * k.r || k.y2 != k.y1 + k.n1 || k.xa + k.n1 < 0))
+      return msg("low-rank block sides not stacked", j);
     if (k.x1 < 0 || k.x1 + k.n1 > N || k.x2 < 0 || k.x2 + (k.dense ? k.r : k.n2) > N) return msg("x rows outside N", j);
     if (k.xa < 0 || k.xa + k.n1 + (k.dense ? k.r : k.n2) > (int64_t)h->f1p_xmap.size()) return msg("XA rows out of range", j);
     if (k.y1 < 0 || k.y1 + k.n1 > h->f1p_prows || k.y2 < 0 || k.y2 + (k.dense ? k.r : k.n2) > h->f1p_prows)

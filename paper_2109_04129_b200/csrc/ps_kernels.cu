@@ -1527,8 +1527,9 @@ __device__ __forceinline__ void f1p_colsum_w(const double2* F, int a_lo, int a_h
 // the L partial sums added by a fixed xor butterfly); with L = 1 (>= 32 rows) k is rotated per
 // row for even r so a quarter warp's 16-byte loads hit distinct bank groups. Two accumulators.
 template <int NR, bool MULTI>
-__device__ __forceinline__ void f1p_rowsum(const double2* F, int a_lo, int a_hi, int r, const double2* q, int R,
-                                           double2* __restrict__ y, int lane) {
+__device__ __forceinline__ void f1p_rowsum(const double2* F, int a_lo, int a_hi, int r, const double2* qa, int R,
+                                           double2* __restrict__ y, int lane, int nsplit = 1 << 30,
+                                           const double2* qb = nullptr) {
   const int nrows = a_hi - a_lo;
   int L = 1;
   if (MULTI)
@@ -1540,6 +1541,7 @@ __device__ __forceinline__ void f1p_rowsum(const double2* F, int a_lo, int a_hi,
     for (int c = 0; c < NR; ++c) acc[c] = ac2[c] = make_double2(0.0, 0.0);
     if (a < a_hi) {
       const double2* Fa = F + a * r;
+      const double2* q = a < nsplit ? qa : qb;           // stacked [F1; F2]: rows >= nsplit use qb
       if (L == 1) {
         int k = (r & 1) ? 0 : (a & 7);                   // any start < r; a & 7 spreads 8 rows over banks
         while (k >= r) k -= r;
@@ -1599,6 +1601,79 @@ __device__ __forceinline__ void f1p_rowsum(const double2* F, int a_lo, int a_hi,
   }
 }
 
+// Stacked colsum of a small block's [F1; F2] (rows [0, n1) and [n1, n1 + n2), x stacked the same
+// way): dst1[k NR + c] = sum over F1 rows, dst2 over F2 rows, in one pass of the warp's lanes
+// (lane = (g, k) as f1p_colsum_w; two accumulators per side; the G group sums added in g order).
+template <int NR>
+__device__ __forceinline__ void f1p_colsum2_w(const double2* F, int n1, int n2, int r, const double2* x, int R,
+                                              double2* dst1, double2* dst2, int lane, const uint16_t* gk) {
+  const int G = r <= 32 ? gk[F1P_GK + r] : 1;
+  for (int kk = 0; kk < r; kk += 32) {
+    int g = 0, k = kk + lane;
+    if (r <= 32) { const int e = gk[r * 32 + lane]; g = e >> 8; k = e & 255; }
+    double2 s1[NR], s2[NR];
+#pragma unroll
+    for (int c = 0; c < NR; ++c) s1[c] = s2[c] = make_double2(0.0, 0.0);
+    if (g < G && k < r) {
+      const int fs = G * r, xs = G * R;
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        const int lo = side ? n1 : 0, hi = side ? n1 + n2 : n1;
+        double2 u[NR], v[NR];
+#pragma unroll
+        for (int c = 0; c < NR; ++c) u[c] = v[c] = make_double2(0.0, 0.0);
+        int a = lo + g;
+        const double2* fp = F + a * r + k;
+        const double2* xp = x + a * R;
+        for (; a + G < hi; a += 2 * G) {
+          const double2 f0 = fp[0], f1 = fp[fs];
+#pragma unroll
+          for (int c = 0; c < NR; ++c) {
+            cfma(u[c], f0, xp[c]);
+            cfma(v[c], f1, xp[xs + c]);
+          }
+          fp += 2 * fs;
+          xp += 2 * xs;
+        }
+        if (a < hi) {
+          const double2 f0 = fp[0];
+#pragma unroll
+          for (int c = 0; c < NR; ++c) cfma(u[c], f0, xp[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < NR; ++c) {
+          const double2 w = make_double2(u[c].x + v[c].x, u[c].y + v[c].y);
+          if (side) s2[c] = w; else s1[c] = w;
+        }
+      }
+    }
+    if (G > 1) {
+      double2 t1[NR], t2[NR];
+#pragma unroll
+      for (int c = 0; c < NR; ++c) { t1[c] = s1[c]; t2[c] = s2[c]; }
+      for (int g2 = 1; g2 < G; ++g2) {
+        const int src = min(31, k + g2 * r);
+#pragma unroll
+        for (int c = 0; c < NR; ++c) {
+          t1[c].x += __shfl_sync(0xffffffffu, s1[c].x, src);
+          t1[c].y += __shfl_sync(0xffffffffu, s1[c].y, src);
+          t2[c].x += __shfl_sync(0xffffffffu, s2[c].x, src);
+          t2[c].y += __shfl_sync(0xffffffffu, s2[c].y, src);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < NR; ++c) { s1[c] = t1[c]; s2[c] = t2[c]; }
+    }
+    if (g == 0 && k < r)
+#pragma unroll
+      for (int c = 0; c < NR; ++c) {
+        dst1[k * NR + c] = s1[c];
+        dst2[k * NR + c] = s2[c];
+      }
+    if (r <= 32) break;
+  }
+}
+
 // rows [0, n) of x (stride R) -> q (stride NR), one warp
 template <int NR>
 __device__ __forceinline__ void f1p_to_q(const double2* x, int n, int R, double2* q, int lane) {
@@ -1625,12 +1700,11 @@ __device__ void f1p_small(const Far1pArgs& a, const FBlk& b, const double2* F, i
     __syncwarp();
     return;
   }
-  const double2* F2 = F + (b.o2 - off0);
-  f1p_colsum_w<NR>(F1, 0, b.n1, b.r, x1, R, q1, NR, false, lane, gk);
-  f1p_colsum_w<NR>(F2, 0, b.n2, b.r, x2, R, q2, NR, false, lane, gk);
+  // F2 follows F1 in the stage, x2 follows x1, and the piece y2 follows y1: one stacked pass each
+  // (p1 = F1^T x1 -> q1, p2 = F2^T x2 -> q2; then rows of F1 take q2, rows of F2 take q1)
+  f1p_colsum2_w<NR>(F1, b.n1, b.n2, b.r, x1, R, q1, q2, lane, gk);
   __syncwarp();
-  f1p_rowsum<NR, false>(F2, 0, b.n2, b.r, q1, R, a.y + b.y2 * R, lane);
-  f1p_rowsum<NR, false>(F1, 0, b.n1, b.r, q2, R, a.y + b.y1 * R, lane);
+  f1p_rowsum<NR, false>(F1, 0, b.n1 + b.n2, b.r, q2, R, a.y + b.y1 * R, lane, b.n1, q1);
   __syncwarp();
 }
 
@@ -1800,6 +1874,9 @@ __global__ void __launch_bounds__(F1P_THREADS, NR <= 2 ? 2 : 1) far1p_kernel(Far
   }
 }
 
+// one column: 2 CTAs per SM (the shared-memory ring of each plus its static tables and barriers)
+static_assert(2 * ((size_t)F1P_NS * F1P_STAGE_BYTES + sizeof(double2) * (F1P_CWARPS * 2 + 1) * F1P_RMAX +
+                   2 * (F1P_GK + 33) + 64 + 1024) <= 228 * 1024, "far1p: two CTAs per SM at one column");
 template <int NR>
 static size_t far1p_smem() {
   return (size_t)(NR >= 8 ? 2 : F1P_NS) * F1P_STAGE_BYTES + sizeof(double2) * ((size_t)F1P_CWARPS * 2 + 1) * F1P_RMAX * NR;
