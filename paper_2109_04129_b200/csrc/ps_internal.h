@@ -161,8 +161,6 @@ struct Far1pArgs {
   double2* y;              // pieces, rows x R row-major
   int32_t* cnt;            // [0]: unit ticket (zeroed per launch)
   int32_t R;
-  int32_t skip;            // timing experiments only (PS_F1P_SKIP): 1 packs, 2 big units not computed
-  int32_t grid;            // > 0: at most this many CTAs (PS_F1P_GRID); else one per resident slot
 };
 void launch_far1p(const Far1pArgs& a, cudaStream_t st);
 int far1p_resident_ctas(int R);

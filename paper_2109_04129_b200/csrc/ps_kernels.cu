@@ -1823,9 +1823,7 @@ __global__ void __launch_bounds__(F1P_THREADS, NR <= 2 ? 2 : 1) far1p_kernel(Far
     const double2* F = stF(s);
     const double2* X = stX(s);
     const FBlk* B = stB(s);
-    if (a.skip & (it.kind == 0 ? 1 : 2)) {
-      // timing experiment (PS_F1P_SKIP): the item is staged but not computed
-    } else if (it.kind == 0) {
+    if (it.kind == 0) {
       for (int j = w; j < it.nb; j += F1P_CWARPS) f1p_small<NR>(a, B[j], F, it.off, X, q1, q2, lane, gk);
     } else {
       const FBlk b = B[0];
@@ -1901,7 +1899,6 @@ int far1p_resident_ctas(int R) {
 template <int NR>
 static void far1p_go(const Far1pArgs& a, cudaStream_t st) {
   int g = far1p_resident_of<NR>();
-  if (a.grid > 0 && a.grid < g) g = a.grid;
   if (g > a.nunits) g = (int)a.nunits;
   far1p_kernel<NR><<<g, F1P_THREADS, far1p_smem<NR>(), st>>>(a);
 }
