@@ -2728,6 +2728,8 @@ int64_t far1p_apply(ps_handle* h, SolvePlan& sp, const double2* W, double2* Z, c
   fa.y = sp.f1p_y.p;
   fa.cnt = sp.d_f1p_cnt.p;
   fa.R = (int32_t)R;
+  static const int minrows = env_int("PS_F1P_MINROWS", 0);
+  fa.minrows = minrows;
   launch_far1p(fa, s);
   launch_far_reduce(h->nl, h->d_f1p_lptr.p, h->d_f1p_poff.p, h->d_f1p_lrow.p, h->d_f1p_lsz.p, sp.f1p_y.p, Z,
                     (int)R, s);

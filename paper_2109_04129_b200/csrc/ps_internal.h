@@ -161,6 +161,7 @@ struct Far1pArgs {
   double2* y;              // pieces, rows x R row-major
   int32_t* cnt;            // [0]: unit ticket (zeroed per launch)
   int32_t R;
+  int32_t minrows;         // big chunks: at least this many rows per consumer warp (PS_F1P_MINROWS)
 };
 void launch_far1p(const Far1pArgs& a, cudaStream_t st);
 int far1p_resident_ctas(int R);

@@ -1828,7 +1828,8 @@ __global__ void __launch_bounds__(F1P_THREADS, NR <= 2 ? 2 : 1) far1p_kernel(Far
     } else {
       const FBlk b = B[0];
       const int h = it.a1 - it.a0, ch = it.nb;
-      const int per = (h + F1P_CWARPS - 1) / F1P_CWARPS;
+      // rows per warp: an even split, but at least minrows (fewer warps on a short chunk)
+      const int per = max((h + F1P_CWARPS - 1) / F1P_CWARPS, a.minrows);
       const int lo = min(h, w * per), hi = min(h, lo + per);
       const int rR = b.r * NR;                           // partials / final sums: r x NR
       if (it.kind == 4) {                                // dense big: G rows [a0, a1)
