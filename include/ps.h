@@ -169,6 +169,46 @@ ps_status ps_setup_group(ps_handle* const* hs, int nranks, const ps_setup_opts* 
 ps_status ps_solve(ps_handle* h, int64_t nrhs, const void* B, int64_t ldb, void* X, int64_t ldx,
                    int on_device, void* cuda_stream, ps_report* rep);
 
+/* ps_solve_series — the n-term power series: Eqs. (35)-(36),
+ * P:195-197, x~ = it_0 - it_1 + it_2 - ... (Eq. 44), it_0 = b_o = Z~_N^{-1} R^T b
+ * (Eqs. 24, 32), it_n = U it_{n-1} (Eq. 31), x = R x~ (Eq. 26), with the per-term norm
+ * ratio of Eq. 45 monitored on the device. Terms are added until
+ *   - n == max_terms, or
+ *   - tol > 0 and, after term n >= 1, every column has ||it_n|| <= tol ||x~_{n+1}||
+ *     (x~_{n+1} = the partial sum through it_n; R25).
+ * max_terms = 2, tol = 0 is the two-term solve of ps_solve (same result up to rounding
+ * order: this path runs one launch set per operator, ps_solve one dataflow program).
+ * A column DIVERGES when its last ratio ||it_n|| / ||it_{n-1}|| >= 1 (the terms do not
+ * shrink, so the partial sums cannot converge: ||U|| <= 1 of P:203 fails).
+ *   opts      : max_terms in [1, 4096]; tol >= 0 (NULL: max_terms = 2, tol = 0).
+ *   B, X, ldb, ldx, on_device, cuda_stream : as ps_solve (single-GPU handles only).
+ *   rep       : optional; rep->it_norm (capacity rep->nrhs columns x rep->max_terms
+ *               terms, term-major it_norm[n * rep->nrhs + c]) receives ||it_n||_2 for
+ *               every term computed; n_terms the terms summed; n_diverged as above.
+ * Errors: PS_EINVAL (bad opts / arguments), PS_ESTATE (no ps_setup, or a row-partition
+ * handle), PS_ENOMEM, PS_ECUDA, PS_EDIVERGED (X fully written). */
+typedef struct {
+  int max_terms;
+  double tol;
+} ps_series_opts;
+
+typedef struct {
+  int64_t nrhs;             /* in: column capacity of it_norm */
+  int64_t max_terms;        /* in: term capacity of it_norm */
+  double* it_norm;          /* out [max_terms x nrhs], term-major, or NULL */
+  int n_terms;              /* out: terms summed (it_0 .. it_{n_terms-1}) */
+  int n_diverged;           /* out: columns whose last ratio ||it_n|| / ||it_{n-1}|| >= 1 */
+  double t_solve_ms;        /* out: device time (CUDA events on the solve stream) */
+  double bytes_moved;       /* out: algorithmic bytes: 16 (2 n_R + n_D) + per extra term
+                               16 (2 n_R + n_D + n_F), + vector passes */
+  double flops;             /* out: algorithmic flops: 8 nrhs (2 n_R + n_D) + per extra term
+                               8 nrhs (2 n_R + n_D + 2 n_F) */
+  int64_t kernel_launches;  /* out: libps kernels launched by this call */
+} ps_series_report;
+
+ps_status ps_solve_series(ps_handle* h, const ps_series_opts* opts, int64_t nrhs, const void* B, int64_t ldb,
+                          void* X, int64_t ldx, int on_device, void* cuda_stream, ps_series_report* rep);
+
 /* ps_solve_group — one two-term solve of a row-partitioned problem whose ranks
  * are handles of THIS process (hm_load with partition = 1, nccl_unique_id =
  * NULL, ranks 0..nranks-1 in hs[0..nranks-1], all on one device). The phases

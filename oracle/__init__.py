@@ -13,7 +13,8 @@ Modules
   hmfile  — independent reader of the versioned H-matrix file.
   scaling — Eqs. (14)-(23): sequential right scaling alpha_k with fill-in,
             D_k^{-1} = inverse of the scaled diagonal blocks.
-  series  — Eqs. (24), (26), (30)-(36), (44)-(45): the two-term solve.
+  series  — Eqs. (24), (26), (30)-(36), (44)-(45): the two-term solve, and the
+            n-term / adaptive series (R25).
   dense   — dense materialisation of Z_N, Z_F for the closed-form pin
             x2 = Z_N^{-1} b - Z_N^{-1} Z_F Z_N^{-1} b (Appendix B of
             SURVEY.md) and dense-LU reference solutions.
@@ -24,4 +25,5 @@ paper's textbook cases, closed forms and invariants.
 from .hmfile import HMatrix, read_hm  # noqa: F401
 from .scaling import Scaling, compute_scaling  # noqa: F401
 from .series import (apply_Rt, apply_R, apply_Dinv, apply_ZF, apply_U, series_solve,  # noqa: F401
-                     solve, SolveResult, check_convergence)
+                     solve, SolveResult, check_convergence, series_solve_adaptive,
+                     series_diverged)

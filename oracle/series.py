@@ -97,6 +97,36 @@ def series_solve(apply_op, b_o: np.ndarray, n_terms: int = 2):
     return xt, norms
 
 
+def series_solve_adaptive(apply_op, b_o: np.ndarray, max_terms: int, tol: float):
+    """Eq. (36) with the term count chosen as DESIGN.md R25 reads Eqs. (44)-(45): add
+    it_n = U it_{n-1} (n = 1, 2, ...) to x~ until n + 1 == max_terms or (tol > 0 and
+    n >= 1 and every column has ||it_n|| <= tol ||x~_{n+1}||, x~_{n+1} = the partial sum
+    through it_n). Returns x~, the per-term norms ||it_n||, the partial-sum norms
+    ||x~_{n+1}|| and the number of terms summed."""
+    it = np.array(b_o, dtype=np.complex128, copy=True)
+    xt = it.copy()
+    norms = [np.linalg.norm(it, axis=0)]
+    psum = [np.linalg.norm(xt, axis=0)]
+    n = 0
+    for n in range(1, max_terms):
+        it = apply_op(it)
+        xt = xt + (-1) ** n * it
+        norms.append(np.linalg.norm(it, axis=0))
+        psum.append(np.linalg.norm(xt, axis=0))
+        if tol > 0 and np.all(norms[-1] <= tol * psum[-1]):
+            break
+    return xt, norms, psum, len(norms)
+
+
+def series_diverged(norms) -> np.ndarray:
+    """Per column: the last ratio ||it_n|| / ||it_{n-1}|| (Eq. 45) is >= 1, i.e. the
+    terms do not shrink and ||U|| <= 1 fails (R25)."""
+    if len(norms) < 2:
+        return np.zeros(np.shape(norms[0]), dtype=bool)
+    a, b = norms[-2], norms[-1]
+    return (a > 0) & ~(b < a)
+
+
 @dataclass
 class SolveResult:
     x: np.ndarray          # N x nrhs, RWG order

@@ -48,6 +48,17 @@ class _Report(ctypes.Structure):
                 ("kernel_launches", ctypes.c_int64), ("ratio", ctypes.c_void_p)]
 
 
+class _SeriesOpts(ctypes.Structure):
+    _fields_ = [("max_terms", ctypes.c_int), ("tol", ctypes.c_double)]
+
+
+class _SeriesReport(ctypes.Structure):
+    _fields_ = [("nrhs", ctypes.c_int64), ("max_terms", ctypes.c_int64), ("it_norm", ctypes.c_void_p),
+                ("n_terms", ctypes.c_int), ("n_diverged", ctypes.c_int), ("t_solve_ms", ctypes.c_double),
+                ("bytes_moved", ctypes.c_double), ("flops", ctypes.c_double),
+                ("kernel_launches", ctypes.c_int64)]
+
+
 _lib = None
 
 
@@ -74,6 +85,9 @@ def load_library():
     L.ps_setup.argtypes = [P, ctypes.POINTER(_Opts)]
     L.ps_solve.restype = I
     L.ps_solve.argtypes = [P, I64, P, I64, P, I64, I, P, ctypes.POINTER(_Report)]
+    L.ps_solve_series.restype = I
+    L.ps_solve_series.argtypes = [P, ctypes.POINTER(_SeriesOpts), I64, P, I64, P, I64, I, P,
+                                  ctypes.POINTER(_SeriesReport)]
     L.ps_apply.restype = I
     L.ps_apply.argtypes = [P, I, I64, P, P]
     L.ps_n.restype = I64
@@ -208,6 +222,29 @@ class PsHandle:
         if st == PS_EDIVERGED:
             warnings.warn(load_library().ps_last_error(self._h).decode(), RuntimeWarning, stacklevel=2)
         self.last_report = r
+        return st, r
+
+    def solve_series(self, B, X, max_terms: int = 2, tol: float = 0.0, stream=None):
+        """X <- n-term series solution (ps_solve_series): at most max_terms terms, stopping
+        early once every column's newest term is <= tol x the partial sum (tol > 0).
+        Returns (status, report dict with it_norm[n_terms, nrhs]). PS_EDIVERGED -> warning."""
+        bp, ldb, nrhs, bdev = _ptr_ld(B, self.N)
+        xp, ldx, nrhs2, xdev = _ptr_ld(X, self.N)
+        if nrhs != nrhs2 or bdev != xdev:
+            raise ValueError("B and X must have the same shape and location")
+        itn = np.zeros((max(int(max_terms), 1), nrhs))
+        rep = _SeriesReport(nrhs, itn.shape[0], itn.ctypes.data, 0, 0, 0.0, 0.0, 0.0, 0)
+        o = _SeriesOpts(int(max_terms), float(tol))
+        s = None
+        if stream is not None:
+            s = ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+        st = self._check(load_library().ps_solve_series(self._h, ctypes.byref(o), nrhs, bp, ldb, xp, ldx,
+                                                        bdev, s, ctypes.byref(rep)))
+        r = dict(n_terms=rep.n_terms, it_norm=itn[:rep.n_terms], n_diverged=rep.n_diverged,
+                 t_solve_ms=rep.t_solve_ms, bytes=rep.bytes_moved, flops=rep.flops,
+                 launches=rep.kernel_launches, status=STATUS_NAMES[st])
+        if st == PS_EDIVERGED:
+            warnings.warn(load_library().ps_last_error(self._h).decode(), RuntimeWarning, stacklevel=2)
         return st, r
 
     def apply(self, op: int, X, Y):

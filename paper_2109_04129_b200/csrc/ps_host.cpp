@@ -765,6 +765,7 @@ struct ps_handle {
   bool setup_done = false;
   double ratio_threshold = 0.1;
   std::unique_ptr<SolvePlan> plan;
+  DevBuf<double2> series_norms;            // ps_solve_series: per term (||it_n||, ||x~||) per column
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   Prof prof;
   // ---- row partition (ps_dist.partition = 1) ----
@@ -3874,6 +3875,121 @@ ps_status ps_apply(ps_handle* h, int op, int64_t nrhs, const void* Xin, void* Yo
   } catch (const PsError& e) {
     return fail(h, e.st, "ps_apply: " + e.msg);
   }
+  return PS_OK;
+}
+
+// n-term series (include/ps.h ps_solve_series; Eqs. 35-36, 44-45): it_0 = D^-1 R^T b, then
+// it_n = U it_{n-1} = D^-1 R^T Z_F R it_{n-1} through the per-operator tables, each term
+// folded into the partial sum with its norms in one pass; with tol > 0 the per-column norms
+// of the term just added are read back (one small D2H per term) to decide whether to stop.
+ps_status ps_solve_series(ps_handle* h, const ps_series_opts* opts, int64_t nrhs, const void* B, int64_t ldb,
+                          void* X, int64_t ldx, int on_device, void* cuda_stream, ps_series_report* rep) {
+  if (!h) return fail(nullptr, PS_EINVAL, "ps_solve_series: handle is NULL");
+  const int max_terms = opts ? opts->max_terms : 2;
+  const double tol = opts ? opts->tol : 0.0;
+  if (max_terms < 1 || max_terms > 4096 || !(tol >= 0.0))
+    return fail(h, PS_EINVAL, "ps_solve_series: max_terms must be in [1, 4096] and tol >= 0");
+  if (!h->setup_done) return fail(h, PS_ESTATE, "ps_solve_series: ps_setup has not run");
+  if (h->part_mode || h->sharded)
+    return fail(h, PS_ESTATE, "ps_solve_series: single-GPU handles only (row partition: ps_solve)");
+  if (nrhs < 1 || !B || !X || ldb < h->N || ldx < h->N)
+    return fail(h, PS_EINVAL, "ps_solve_series: bad arguments (nrhs >= 1, B/X non-NULL, ldb/ldx >= N)");
+  {
+    const char* b0 = (const char*)B;
+    const char* b1 = b0 + 16 * (ldb * (nrhs - 1) + h->N);
+    const char* x0 = (const char*)X;
+    const char* x1 = x0 + 16 * (ldx * (nrhs - 1) + h->N);
+    if (b0 < x1 && x0 < b1) return fail(h, PS_EINVAL, "ps_solve_series: X overlaps B");
+  }
+  int ndiv = 0, nterms = 0;
+  try {
+    CK(cudaSetDevice(h->device));
+    cudaStream_t s = cuda_stream ? (cudaStream_t)cuda_stream : h->stream;
+    ensure_far(h, s);
+    SolvePlan& sp = get_plan(h, nrhs, true);
+    const int64_t N = h->N, R = nrhs;
+    int64_t launches = 0;
+    h->series_norms.alloc((int64_t)max_terms * R);
+    const double2* Bd = (const double2*)B;
+    int64_t ldb_d = ldb;
+    if (!on_device) {
+      CK(cudaMemcpy2DAsync(sp.stage.p, 16 * N, B, 16 * ldb, 16 * N, nrhs, cudaMemcpyHostToDevice, s));
+      Bd = sp.stage.p;
+      ldb_d = N;
+    }
+    CK(cudaEventRecord(h->ev0, s));
+    // it (sp.bo) = current term, acc (sp.xt) = partial sum x~, y / w scratch
+    launches += aux(h, s, [&] { launch_permute_in(N, R, h->d_e2rwg.p, Bd, ldb_d, sp.y.p, s); });
+    launches += op_Rt(h, sp, sp.y.p, s);                                 // b~ = R^T b  (Eq. 24)
+    launches += op_Dinv(h, sp, sp.y.p, sp.bo.p, s);                      // it_0 = b_o  (Eq. 32)
+    std::vector<double2> nrm(R);
+    for (int n = 0; n < max_terms; ++n) {
+      if (n > 0) {                                                       // it_n = U it_{n-1} (Eq. 31)
+        launches += op_R(h, sp, sp.bo.p, sp.w.p, s);
+        // Z_F: the one-pass far apply where the solve program uses it (narrow, large far field)
+        launches += sp.f1p ? far1p_apply(h, sp, sp.w.p, sp.y.p, s) : op_ZF(h, sp, sp.w.p, sp.y.p, s);
+        launches += op_Rt(h, sp, sp.y.p, s);
+        launches += op_Dinv(h, sp, sp.y.p, sp.bo.p, s);
+      }
+      double2* nd = h->series_norms.p + (int64_t)n * R;
+      launches += aux(h, s, [&] {                                        // x~ += (-1)^n it_n (Eq. 44)
+        launch_series_accum(N, R, sp.bo.p, sp.xt.p, (n & 1) ? -1.0 : 1.0, n == 0, sp.part.p, sp.rpc, s);
+        launch_finalize_norms(sp.nchunks, R, sp.part.p, nd, s);
+      }) + 1;
+      nterms = n + 1;
+      if (tol > 0.0 && n >= 1 && n + 1 < max_terms) {
+        CK(cudaMemcpyAsync(nrm.data(), nd, 16 * R, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        bool done = true;
+        for (int64_t c = 0; c < R && done; ++c) done = nrm[c].x <= tol * nrm[c].y;
+        if (done) break;
+      }
+    }
+    launches += op_R(h, sp, sp.xt.p, sp.xt.p, s);                        // x = R x~ (Eq. 26)
+    double2* Xd = on_device ? (double2*)X : sp.stage.p;
+    launches += aux(h, s, [&] { launch_permute_out(N, R, h->d_e2rwg.p, sp.xt.p, Xd, on_device ? ldx : N, s); });
+    CK(cudaEventRecord(h->ev1, s));
+    CK(cudaGetLastError());
+    if (!on_device)
+      CK(cudaMemcpy2DAsync(X, 16 * ldx, sp.stage.p, 16 * N, 16 * N, nrhs, cudaMemcpyDeviceToHost, s));
+    std::vector<double2> all((size_t)nterms * R);
+    CK(cudaMemcpyAsync(all.data(), h->series_norms.p, 16 * all.size(), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (h->prof.on) h->prof.collect();
+    if (nterms >= 2)
+      for (int64_t c = 0; c < R; ++c) {
+        const double a = all[(size_t)(nterms - 2) * R + c].x, b = all[(size_t)(nterms - 1) * R + c].x;
+        if (a > 0 && !(b < a)) ++ndiv;
+      }
+    if (rep) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+      rep->t_solve_ms = ms;
+      rep->n_terms = nterms;
+      rep->n_diverged = ndiv;
+      rep->kernel_launches = launches;
+      double nR = 0, nD = 0, nF = 0;
+      for (int64_t p = 0; p < h->nl; ++p) {
+        nR += (double)h->nsz[p] * h->S[p];
+        nD += (double)h->nsz[p] * h->nsz[p];
+      }
+      for (int64_t b = 0; b < h->nfar; ++b)
+        nF += (double)h->far_list[7 * b + 5] * (h->far_list[7 * b + 1] + h->far_list[7 * b + 3]);
+      const double ex = nterms - 1;
+      rep->bytes_moved = 16.0 * ((2 * nR + nD) + ex * (2 * nR + nD + nF)) + 16.0 * 6.0 * (double)N * R * nterms;
+      rep->flops = 8.0 * R * ((2 * nR + nD) + ex * (2 * nR + nD + 2 * nF));
+      if (rep->it_norm)
+        for (int n = 0; n < nterms && n < rep->max_terms; ++n)
+          for (int64_t c = 0; c < R && c < rep->nrhs; ++c) rep->it_norm[(int64_t)n * rep->nrhs + c] = all[(size_t)n * R + c].x;
+    }
+  } catch (const PsError& e) {
+    return fail(h, e.st, "ps_solve_series: " + e.msg);
+  } catch (const std::bad_alloc&) {
+    return fail(h, PS_ENOMEM, "ps_solve_series: host allocation failed");
+  }
+  if (ndiv > 0)
+    return fail(h, PS_EDIVERGED, "ps_solve_series: " + std::to_string(ndiv) + " of " + std::to_string(nrhs) +
+                                     " columns have ||it_n|| / ||it_{n-1}|| >= 1 at the last term");
   return PS_OK;
 }
 

@@ -201,6 +201,9 @@ void launch_combine_norms(int64_t N, int64_t nrhs, const double2* bo, const doub
 // part[chunk*nrhs + c] = (sum |bo|^2, sum |bo - xt|^2) over the chunk's rows
 void launch_norms2(int64_t N, int64_t nrhs, const double2* bo, const double2* xt, double2* part,
                    int64_t rows_per_chunk, cudaStream_t st);
+// acc = (first ? 0 : acc) + sign it; part[chunk*nrhs + c] = (sum |it|^2, sum |acc|^2) (n-term series)
+void launch_series_accum(int64_t N, int64_t nrhs, const double2* it, double2* acc, double sign, int first,
+                         double2* part, int64_t rows_per_chunk, cudaStream_t st);
 // norms[c] = (sqrt sum_chunks part.x, sqrt sum part.y); do_sqrt = 0: the sums themselves
 void launch_finalize_norms(int64_t nchunks, int64_t nrhs, const double2* part, double2* norms,
                            cudaStream_t st, int do_sqrt = 1);

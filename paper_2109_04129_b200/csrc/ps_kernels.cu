@@ -2221,6 +2221,33 @@ void launch_finalize_norms(int64_t nch, int64_t nrhs, const double2* part, doubl
   finalize_norms_kernel<<<(unsigned)((nrhs + 127) / 128), 128, 0, st>>>(nch, nrhs, part, norms, do_sqrt);
 }
 
+// One term of the n-term series (Eq. 44): acc += sign it_n, fused with the per-column squared
+// norms of it_n and of the new partial sum (Eqs. 44-45); fixed chunking as combine_norms.
+__global__ void series_accum_kernel(int64_t N, int64_t nrhs, const double2* __restrict__ it,
+                                    double2* __restrict__ acc, double sign, int first,
+                                    double2* __restrict__ part, int64_t rpc) {
+  const int64_t c = blockIdx.y * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= nrhs) return;
+  const int64_t r0 = blockIdx.x * rpc, r1 = min(N, r0 + rpc);
+  double s0 = 0.0, s1 = 0.0;
+  for (int64_t r = r0; r < r1; ++r) {
+    const int64_t e = r * nrhs + c;
+    const double2 t = it[e];
+    double2 a = first ? make_double2(0.0, 0.0) : acc[e];
+    a.x += sign * t.x;
+    a.y += sign * t.y;
+    s0 += t.x * t.x + t.y * t.y;
+    s1 += a.x * a.x + a.y * a.y;
+    acc[e] = a;
+  }
+  part[blockIdx.x * nrhs + c] = make_double2(s0, s1);
+}
+void launch_series_accum(int64_t N, int64_t nrhs, const double2* it, double2* acc, double sign, int first,
+                         double2* part, int64_t rpc, cudaStream_t st) {
+  dim3 g((unsigned)((N + rpc - 1) / rpc), (unsigned)((nrhs + 127) / 128));
+  series_accum_kernel<<<g, 128, 0, st>>>(N, nrhs, it, acc, sign, first, part, rpc);
+}
+
 __global__ void set_ones_kernel(double2* __restrict__ base, const int64_t* __restrict__ offs, int64_t n) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
     base[offs[e]] = make_double2(1.0, 0.0);

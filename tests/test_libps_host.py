@@ -71,6 +71,7 @@ def test_null_arguments():
     assert L.ps_n(None) == -1
     assert L.ps_setup(None, None) == binding.PS_EINVAL
     assert L.ps_solve(None, 1, None, 1, None, 1, 1, None, None) == binding.PS_EINVAL
+    assert L.ps_solve_series(None, None, 1, None, 1, None, 1, 1, None, None) == binding.PS_EINVAL
     L.ps_free(None)                     # NULL-safe
 
 

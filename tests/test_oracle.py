@@ -323,3 +323,76 @@ def test_truncation_size_report_c1(cfgdata):
     assert abs(now["rel_err_two_term_vs_dense_LU"]["max"] - e0) <= 1e-10 * e0
     assert abs(now["ratio_it1_it0"]["max"] - stored["ratio_it1_it0"]["max"]) <= 1e-12
     assert 0.1 <= e0 <= 1.0 and now["ratio_it1_it0"]["max"] >= 0.1
+
+
+# ---- n-term / adaptive series (R25) ----
+
+def test_n_term_series_matches_dense_closed_form():
+    """x_n = R sum_{k<n} (-U)^k b_o equals sum_{k<n} (-Z_N^{-1} Z_F)^k Z_N^{-1} b, because
+    R U R^{-1} = R D^{-1} R^T Z_F = Z_N^{-1} Z_F (Eqs. 26, 28, 31, 35): dense LU of the
+    file's near field, no scaling code on this side."""
+    from oracle import series_solve
+    hd = synthetic(n_points=260, seed=11, far_scale=0.2)
+    H = _hdata_to_hm(hd)
+    S = compute_scaling(H)
+    B = random_rhs(H.N, 2, seed=4)
+    ZN, ZF = dense_ZN(H), dense_ZF(H)
+    y = direct_solve(ZN, B)
+    ref = np.zeros_like(y)
+    term = y.copy()
+    b_o = apply_Dinv(S, apply_Rt(S, B[S.e2rwg]))
+    for n in range(1, 6):
+        ref = ref + term                             # sum_{k<n} (-ZN^-1 ZF)^k ZN^-1 b
+        xt, _ = series_solve(lambda v: apply_U(H, S, v), b_o, n_terms=n)
+        x = np.empty_like(xt)
+        x[S.e2rwg] = apply_R(S, xt)
+        assert rel_l2_cols(x, ref).max() < 1e-11, n
+        term = -direct_solve(ZN, ZF @ term)
+
+
+def test_adaptive_series_scalar_surrogate():
+    """U = cI: term n has norm |c|^n ||b_o||, the partial sum through it_n is
+    (1 - (-c)^{n+1}) / (1 + c) b_o; the rule stops at the first n >= 1 with
+    |c|^n <= tol |1 - (-c)^{n+1}| / |1 + c| (R25), else at max_terms."""
+    from oracle import series_diverged, series_solve_adaptive
+    rng = np.random.default_rng(5)
+    bo = _cn(rng, 40, 3)
+    for c in (0.05, 0.3, -0.45 + 0.2j, 0.8):
+        for tol in (1e-3, 1e-8, 1e-12):
+            n_exp = 60
+            for n in range(1, 60):
+                if abs(c) ** n <= tol * abs(1 - (-c) ** (n + 1)) / abs(1 + c):
+                    n_exp = n + 1
+                    break
+            xt, norms, psum, nt = series_solve_adaptive(lambda v: c * v, bo, 60, tol)
+            assert nt == n_exp, (c, tol)
+            assert np.allclose(xt, (1 - (-c) ** nt) / (1 + c) * bo, rtol=1e-12, atol=1e-14)
+            assert np.allclose(norms[-1], abs(c) ** (nt - 1) * np.linalg.norm(bo, axis=0), rtol=1e-10)
+            assert not series_diverged(norms).any()
+    # tol = 0: exactly max_terms terms, the same sum as the fixed-n series
+    from oracle import series_solve
+    xt, norms, _, nt = series_solve_adaptive(lambda v: 0.3 * v, bo, 5, 0.0)
+    x5, _ = series_solve(lambda v: 0.3 * v, bo, n_terms=5)
+    assert nt == 5 and np.array_equal(xt, x5)
+    # |c| >= 1: the terms do not shrink -> diverged
+    _, norms, _, nt = series_solve_adaptive(lambda v: -1.2 * v, bo, 4, 1e-6)
+    assert nt == 4 and series_diverged(norms).all()
+
+
+def test_adaptive_series_reaches_dense_solve():
+    """On a convergent synthetic system the adaptive series at tol 1e-13 ends within
+    1e-10 of the dense-LU solution of Z = Z_N + Z_F (PAPER.md:313 metric), and the
+    Eq. 45 ratios settle below 1."""
+    from oracle import series_diverged, series_solve_adaptive
+    hd = synthetic(n_points=300, seed=8, far_scale=0.05)
+    H = _hdata_to_hm(hd)
+    S = compute_scaling(H)
+    B = random_rhs(H.N, 2, seed=6)
+    b_o = apply_Dinv(S, apply_Rt(S, B[S.e2rwg]))
+    xt, norms, psum, nt = series_solve_adaptive(lambda v: apply_U(H, S, v), b_o, 80, 1e-13)
+    assert 2 < nt < 80
+    x = np.empty_like(xt)
+    x[S.e2rwg] = apply_R(S, xt)
+    xd = direct_solve(dense_ZN(H) + dense_ZF(H), B)
+    assert rel_l2_cols(x, xd).max() < 1e-10
+    assert not series_diverged(norms).any()
