@@ -209,6 +209,32 @@ typedef struct {
 ps_status ps_solve_series(ps_handle* h, const ps_series_opts* opts, int64_t nrhs, const void* B, int64_t ldb,
                           void* X, int64_t ldx, int on_device, void* cuda_stream, ps_series_report* rep);
 
+/* ps_farfield — far field and radar cross section of RWG surface currents (SURVEY §8(f)
+ * NEXT-4: the RCS curves of PAPER.md:333-341 computed from the solve's X on the GPU).
+ *   F(r^, c) = sum_n I[n, c] int f_n(r') e^{+j k r^.r'} dS'  (7-point degree-5 rule per
+ *   triangle), f_n the RWG function of P:71: +l_n/(2A+) (r' - v+) on T+, -l_n/(2A-) (r' - v-)
+ *   on T-, l_n = the length of the edge T+ and T- share;
+ *   sigma_theta / sigma_phi = (k eta)^2 / (4 pi) |F . theta^|^2, |F . phi^|^2 in m^2 for a
+ *   unit-amplitude incident plane wave (theta^, phi^ of r^; phi = 0 on the z axis).
+ * ALL arrays are DEVICE pointers on the current device (no handle is needed):
+ *   nodes [nnodes x 3] f64 (m), tris [ntris x 3] i64 node ids;
+ *   tp, tm, vp, vm [N] i64: triangles T+ / T- of basis n and their free vertices
+ *                (node ids; the generator's RWG order = the order of I's rows);
+ *   k (rad/m) >= 0, eta (ohm); I [N x nrhs] complex128 column-major, ldi >= N;
+ *   rhat [ndir x 3] f64 unit observation directions;
+ *   mono = 0: bistatic, F [ndir x nrhs x 3] complex128 (F[(d nrhs + c) 3 + xyz]) and
+ *             sigma [ndir x nrhs x 2] f64 (theta, phi), every direction for every column;
+ *   mono = 1: monostatic, ndir == nrhs, direction d paired with column d only:
+ *             F [ndir x 3], sigma [ndir x 2];
+ *   sigma may be NULL (F only). cuda_stream: cudaStream_t or NULL (legacy default stream);
+ *   returns after the work completed. Index arrays are trusted (not range-checked).
+ * Errors: PS_EINVAL (sizes, NULL pointers, mono with ndir != nrhs), PS_ENOMEM, PS_ECUDA;
+ * message in ps_last_error(NULL). Deterministic (fixed split order). */
+ps_status ps_farfield(int64_t nnodes, const double* nodes, int64_t ntris, const int64_t* tris, int64_t N,
+                      const int64_t* tp, const int64_t* tm, const int64_t* vp, const int64_t* vm, double k,
+                      double eta, const void* I, int64_t ldi, int64_t nrhs, int64_t ndir, const double* rhat,
+                      int mono, void* F, double* sigma, void* cuda_stream);
+
 /* ps_solve_group — one two-term solve of a row-partitioned problem whose ranks
  * are handles of THIS process (hm_load with partition = 1, nccl_unique_id =
  * NULL, ranks 0..nranks-1 in hs[0..nranks-1], all on one device). The phases

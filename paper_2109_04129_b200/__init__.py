@@ -7,4 +7,4 @@ the calls raise.
 """
 from .binding import (PsError, PsHandle, PS_OP_DINV, PS_OP_R, PS_OP_RT, PS_OP_U,  # noqa: F401
                       PS_OP_ZF, load_library, lib_path, INFO_KEYS, solve_group, nccl_unique_id,
-                      partition)
+                      partition, farfield)

@@ -88,6 +88,8 @@ def load_library():
     L.ps_solve_series.restype = I
     L.ps_solve_series.argtypes = [P, ctypes.POINTER(_SeriesOpts), I64, P, I64, P, I64, I, P,
                                   ctypes.POINTER(_SeriesReport)]
+    L.ps_farfield.restype = I
+    L.ps_farfield.argtypes = [I64, P, I64, P, I64, P, P, P, P, D, D, P, I64, I64, I64, P, I, P, P, P]
     L.ps_apply.restype = I
     L.ps_apply.argtypes = [P, I, I64, P, P]
     L.ps_n.restype = I64
@@ -293,6 +295,53 @@ class PsHandle:
 
     def elim_leaf(self, pos: int) -> int:
         return int(load_library().ps_elim_leaf(self._h, pos))
+
+
+def farfield(nodes, tris, tp, tm, vp, vm, k: float, eta: float, I, rhat, mono: bool = False,
+             with_sigma: bool = True, stream=None):
+    """ps_farfield: far-field vectors F and RCS sigma (m^2; theta, phi polarisation) of the RWG
+    currents I (N x nrhs column-major complex128) in the directions rhat (ndir x 3). Host
+    arrays are copied to the current CUDA device (marshalling); returns torch CUDA tensors
+    F (ndir x nrhs x 3, or ndir x 3 with mono) and sigma (ndir x nrhs x 2, or ndir x 2)."""
+    import torch
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    def d(a, dt):
+        t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
+        return t.to(device=dev, dtype=dt).contiguous()
+    nodes_d, tris_d = d(nodes, torch.float64), d(tris, torch.int64)
+    tp_d, tm_d, vp_d, vm_d = (d(a, torch.int64) for a in (tp, tm, vp, vm))
+    rh = d(rhat, torch.float64).reshape(-1, 3)
+    N = int(tp_d.numel())
+    if isinstance(I, torch.Tensor):
+        Id = I.to(device=dev, dtype=torch.complex128)
+    else:
+        Id = torch.from_numpy(np.ascontiguousarray(np.asfortranarray(I, dtype=np.complex128).T)).to(dev).T \
+            if np.ndim(I) == 2 else torch.from_numpy(np.asarray(I, np.complex128)).to(dev)
+    if Id.dim() == 1:
+        Id = Id.unsqueeze(1)
+    if Id.shape[0] != N or Id.stride(0) != 1:
+        Id = Id.T.contiguous().T
+    nrhs, ndir = Id.shape[1], rh.shape[0]
+    ldi = Id.stride(1) if nrhs > 1 else N
+    ncol = 1 if mono else nrhs
+    F = torch.empty((ndir, ncol, 3), dtype=torch.complex128, device=dev)
+    sig = torch.empty((ndir, ncol, 2), dtype=torch.float64, device=dev) if with_sigma else None
+    s = None
+    if stream is not None:
+        s = ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+    L = load_library()
+    st = L.ps_farfield(nodes_d.shape[0] if nodes_d.dim() == 2 else nodes_d.numel() // 3, nodes_d.data_ptr(),
+                       tris_d.numel() // 3, tris_d.data_ptr(), N, tp_d.data_ptr(), tm_d.data_ptr(),
+                       vp_d.data_ptr(), vm_d.data_ptr(), float(k), float(eta), Id.data_ptr(), ldi, nrhs, ndir,
+                       rh.data_ptr(), 1 if mono else 0, F.data_ptr(),
+                       sig.data_ptr() if sig is not None else None, s)
+    if st != PS_OK:
+        raise PsError(st, L.ps_last_error(None).decode())
+    if mono:
+        F = F[:, 0]
+        sig = sig[:, 0] if sig is not None else None
+    return F, sig
 
 
 def _report(nrhs, want_norms):

@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libps.so")
-SOURCES = ["ps_kernels.cu", "ps_host.cpp"]
+SOURCES = ["ps_kernels.cu", "ps_rcs.cu", "ps_host.cpp"]
 HEADERS = ["ps_internal.h", os.path.join("..", "..", "include", "ps.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",

@@ -3993,6 +3993,32 @@ ps_status ps_solve_series(ps_handle* h, const ps_series_opts* opts, int64_t nrhs
   return PS_OK;
 }
 
+// far field / RCS of RWG currents (include/ps.h ps_farfield; ps_rcs.cu)
+ps_status ps_farfield(int64_t nnodes, const double* nodes, int64_t ntris, const int64_t* tris, int64_t N,
+                      const int64_t* tp, const int64_t* tm, const int64_t* vp, const int64_t* vm, double k,
+                      double eta, const void* I, int64_t ldi, int64_t nrhs, int64_t ndir, const double* rhat,
+                      int mono, void* F, double* sigma, void* cuda_stream) {
+  if (nnodes < 3 || ntris < 1 || N < 1 || nrhs < 1 || ndir < 0 || ldi < N || !(k >= 0.0) || !nodes || !tris ||
+      !tp || !tm || !vp || !vm || !I || (ndir > 0 && (!rhat || !F)) || (mono && ndir != nrhs))
+    return fail(nullptr, PS_EINVAL, "ps_farfield: bad arguments");
+  if (ndir == 0) return PS_OK;
+  try {
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    const int64_t need = -launch_farfield(nodes, tris, N, tp, tm, vp, vm, k, eta, (const double2*)I, ldi, nrhs,
+                                          ndir, rhat, mono, (double2*)F, sigma, nullptr, 0, s);
+    void* part = nullptr;
+    CK(cudaMallocAsync(&part, sizeof(double2) * (size_t)need, s));
+    launch_farfield(nodes, tris, N, tp, tm, vp, vm, k, eta, (const double2*)I, ldi, nrhs, ndir, rhat, mono,
+                    (double2*)F, sigma, (double2*)part, need, s);
+    CK(cudaGetLastError());
+    CK(cudaFreeAsync(part, s));
+    CK(cudaStreamSynchronize(s));
+  } catch (const PsError& e) {
+    return fail(nullptr, e.st, "ps_farfield: " + e.msg);
+  }
+  return PS_OK;
+}
+
 int ps_analyze(const char* path, double* out, int n) { return ps_analyze_rank(path, 0, 1, out, n); }
 
 int64_t ps_validate(const char* path, int64_t nrhs, int64_t* stats, int nstats) {

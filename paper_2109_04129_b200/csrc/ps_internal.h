@@ -210,6 +210,13 @@ void launch_finalize_norms(int64_t nchunks, int64_t nrhs, const double2* part, d
 // dst[i] += src[i] (i < n), the in-process stand-in of a sum all-reduce (rank order fixed)
 void launch_add(double* dst, const double* src, int64_t n, cudaStream_t st);
 void launch_zero(double2* p, int64_t n, cudaStream_t st);
+// far field / RCS of RWG currents (ps_rcs.cu, include/ps.h ps_farfield); returns the kernels
+// launched, or -(partial entries needed) when part is NULL or smaller than that
+int64_t launch_farfield(const double* nodes, const int64_t* tris, int64_t N, const int64_t* tp, const int64_t* tm,
+                        const int64_t* vp, const int64_t* vm, double k, double eta, const double2* I, int64_t ldi,
+                        int64_t nrhs, int64_t ndir, const double* rhat, int mono, double2* F, double* sigma,
+                        double2* part, int64_t part_cap, cudaStream_t st);
+
 // base[offs[e]] = 1 (e < n): identity diagonals of the chain matrices T_c
 void launch_set_ones(double2* base, const int64_t* offs, int64_t n, cudaStream_t st);
 
