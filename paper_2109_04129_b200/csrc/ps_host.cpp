@@ -4006,12 +4006,17 @@ ps_status ps_farfield(int64_t nnodes, const double* nodes, int64_t ntris, const 
     cudaStream_t s = (cudaStream_t)cuda_stream;
     const int64_t need = -launch_farfield(nodes, tris, N, tp, tm, vp, vm, k, eta, (const double2*)I, ldi, nrhs,
                                           ndir, rhat, mono, (double2*)F, sigma, nullptr, 0, s);
-    void* part = nullptr;
-    CK(cudaMallocAsync(&part, sizeof(double2) * (size_t)need, s));
+    // split partials: a grow-only workspace per device, kept across calls (calls serialise on it)
+    static std::mutex mu;
+    static std::map<int, DevBuf<double2>> ws;
+    std::lock_guard<std::mutex> lock(mu);
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    DevBuf<double2>& part = ws[dev];
+    if (part.cap < need) part.alloc(need);
     launch_farfield(nodes, tris, N, tp, tm, vp, vm, k, eta, (const double2*)I, ldi, nrhs, ndir, rhat, mono,
-                    (double2*)F, sigma, (double2*)part, need, s);
+                    (double2*)F, sigma, part.p, part.cap, s);
     CK(cudaGetLastError());
-    CK(cudaFreeAsync(part, s));
     CK(cudaStreamSynchronize(s));
   } catch (const PsError& e) {
     return fail(nullptr, e.st, "ps_farfield: " + e.msg);

@@ -1970,7 +1970,7 @@ __global__ void __launch_bounds__(512)
 inverse_kernel(const int32_t* __restrict__ leaf_ids, const int32_t* __restrict__ sizes,
                const int64_t* __restrict__ src_off, const int64_t* __restrict__ src_ld,
                const int64_t* __restrict__ dst_off, const double2* __restrict__ Wb,
-               double2* __restrict__ Db, int32_t* __restrict__ status, int use_smem) {
+               double2* __restrict__ Db, int32_t* __restrict__ status, int use_smem, int n_lo, int n_hi) {
   extern __shared__ double2 sm[];
   __shared__ double red_v[512];
   __shared__ int red_i[512];
@@ -1979,6 +1979,7 @@ inverse_kernel(const int32_t* __restrict__ leaf_ids, const int32_t* __restrict__
   __shared__ int s_sing;
   const int l = blockIdx.x;
   const int n = sizes[l];
+  if (n < n_lo || n > n_hi) return;                   // another launch of this level takes it
   const int64_t ld_src = src_ld[l];
   const double2* src = Wb + src_off[l];
   double2* dst = Db + dst_off[l];
@@ -2003,8 +2004,11 @@ inverse_kernel(const int32_t* __restrict__ leaf_ids, const int32_t* __restrict__
   if (tid == 0) { s_fro = sqrt(red_v[0]); s_sing = 0; }
   __syncthreads();
   const double tol2 = (1e-14 * s_fro) * (1e-14 * s_fro);
+  const int lane = tid & 31, w = tid >> 5, nw = nt >> 5;
+  // per pivot: 3 CTA barriers (pivot reduction, swap + column k copy, elimination); the pivot
+  // search is a warp-shuffle argmax (max |z|^2, lowest row on ties), every column j is owned by
+  // one warp (rows over lanes: coalesced, no index division), which scales row k itself
   for (int k = 0; k < n; ++k) {
-    // pivot search in column k, rows k..n-1
     double best = -1.0;
     int bi = n;
     for (int i = k + tid; i < n; i += nt) {
@@ -2012,52 +2016,58 @@ inverse_kernel(const int32_t* __restrict__ leaf_ids, const int32_t* __restrict__
       const double m2 = v.x * v.x + v.y * v.y;
       if (m2 > best) { best = m2; bi = i; }
     }
-    red_v[tid] = best;
-    red_i[tid] = bi;
-    __syncthreads();
-    for (int s = nt / 2; s > 0; s >>= 1) {
-      if (tid < s) {
-        const double vo = red_v[tid + s];
-        const int io = red_i[tid + s];
-        if (vo > red_v[tid] || (vo == red_v[tid] && io < red_i[tid])) { red_v[tid] = vo; red_i[tid] = io; }
-      }
-      __syncthreads();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double vo = __shfl_xor_sync(0xffffffffu, best, o);
+      const int io = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (vo > best || (vo == best && io < bi)) { best = vo; bi = io; }
     }
-    if (tid == 0) {
-      s_piv = red_i[0];
-      piv[k] = red_i[0];
-      if (!(red_v[0] > tol2)) s_sing = 1;
+    if (lane == 0) { red_v[w] = best; red_i[w] = bi; }
+    __syncthreads();
+    if (w == 0) {
+      best = lane < nw ? red_v[lane] : -1.0;
+      bi = lane < nw ? red_i[lane] : n;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double vo = __shfl_xor_sync(0xffffffffu, best, o);
+        const int io = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (vo > best || (vo == best && io < bi)) { best = vo; bi = io; }
+      }
+      if (lane == 0) {
+        s_piv = bi;
+        piv[k] = bi;
+        if (!(best > tol2)) s_sing = 1;
+      }
     }
     __syncthreads();
     if (s_sing) break;
     const int r = s_piv;
-    if (r != k)
-      for (int j = tid; j < n; j += nt) {
+    // rows k <-> r (column k is rewritten whole by the elimination: not swapped), and column
+    // k as it reads after the swap saved as the elimination factors
+    for (int j = tid; j < n; j += nt) {
+      if (r != k && j != k) {
         const double2 t = a[k + j * n];
         a[k + j * n] = a[r + j * n];
         a[r + j * n] = t;
       }
+    }
+    for (int i = tid; i < n; i += nt) colk[i] = a[(i == k ? r : i == r ? k : i) + k * n];
     __syncthreads();
-    const double2 p = a[k + k * n];
+    const double2 p = colk[k];
     const double pm = p.x * p.x + p.y * p.y;
     const double2 inv = make_double2(p.x / pm, -p.y / pm);
-    // column k factors (before the update), then scale row k
-    for (int i = tid; i < n; i += nt) colk[i] = a[i + k * n];
-    __syncthreads();
-    for (int j = tid; j < n; j += nt) {
-      double2 v = (j == k) ? make_double2(1.0, 0.0) : a[k + j * n];
-      a[k + j * n] = make_double2(v.x * inv.x - v.y * inv.y, v.x * inv.y + v.y * inv.x);
-    }
-    __syncthreads();
-    for (int e = tid; e < n * n; e += nt) {
-      const int i = e % n, j = e / n;
-      if (i == k) continue;
-      const double2 f = colk[i];
-      double2 base = (j == k) ? make_double2(0.0, 0.0) : a[e];
-      const double2 rk = a[k + j * n];
-      base.x -= f.x * rk.x - f.y * rk.y;
-      base.y -= f.x * rk.y + f.y * rk.x;
-      a[e] = base;
+    for (int j = w; j < n; j += nw) {
+      const double2 v = (j == k) ? make_double2(1.0, 0.0) : a[k + j * n];
+      const double2 rk = make_double2(v.x * inv.x - v.y * inv.y, v.x * inv.y + v.y * inv.x);
+      __syncwarp();                                     // every lane has read row k of column j
+      for (int i = lane; i < n; i += 32) {
+        if (i == k) { a[k + j * n] = rk; continue; }
+        const double2 f = colk[i];
+        double2 base = (j == k) ? make_double2(0.0, 0.0) : a[i + j * n];
+        base.x -= f.x * rk.x - f.y * rk.y;
+        base.y -= f.x * rk.y + f.y * rk.x;
+        a[i + j * n] = base;
+      }
     }
     __syncthreads();
   }
@@ -2085,9 +2095,6 @@ void launch_inverse(int64_t nl, const int32_t* leaf_ids, const int32_t* sizes, c
                     const int64_t* src_ld, const int64_t* dst_off, const double2* Wbase,
                     double2* Dbase, int32_t* status, int max_n, cudaStream_t st) {
   if (nl <= 0) return;
-  int nn = max_n <= SMEM_N ? max_n : 0;
-  size_t smem = (size_t)nn * nn * sizeof(double2) + (size_t)max_n * sizeof(double2) +
-                (size_t)max_n * sizeof(int) + 16;
   static int max_dyn = -1;
   if (max_dyn < 0) {                                   // opt-in limit minus the kernel's static reductions
     int dev = 0, optin = 0;
@@ -2098,12 +2105,23 @@ void launch_inverse(int64_t nl, const int32_t* leaf_ids, const int32_t* sizes, c
     max_dyn = optin - (int)fa.sharedSizeBytes;
     cudaFuncSetAttribute(inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
   }
-  if ((int64_t)smem > max_dyn) {                       // the n x n block stays in global memory
-    nn = 0;
-    smem = (size_t)max_n * sizeof(double2) + (size_t)max_n * sizeof(int) + 16;
+  auto smem_of = [](int nn, int mn) {
+    return (size_t)nn * nn * sizeof(double2) + (size_t)mn * sizeof(double2) + (size_t)mn * sizeof(int) + 16;
+  };
+  // blocks up to SMEM_N in shared memory; the larger ones of the level (if any) in a second
+  // launch working in the destination buffer (every CTA of a launch outside its size range
+  // returns at once)
+  const int ns = max_n < SMEM_N ? max_n : SMEM_N;
+  if ((int64_t)smem_of(ns, ns) <= max_dyn) {
+    inverse_kernel<<<(unsigned)nl, 512, smem_of(ns, ns), st>>>(leaf_ids, sizes, src_off, src_ld, dst_off, Wbase,
+                                                               Dbase, status, 1, 0, ns);
+    if (max_n > ns)
+      inverse_kernel<<<(unsigned)nl, 512, smem_of(0, max_n), st>>>(leaf_ids, sizes, src_off, src_ld, dst_off,
+                                                                   Wbase, Dbase, status, 0, ns + 1, max_n);
+  } else {
+    inverse_kernel<<<(unsigned)nl, 512, smem_of(0, max_n), st>>>(leaf_ids, sizes, src_off, src_ld, dst_off, Wbase,
+                                                                 Dbase, status, 0, 0, max_n);
   }
-  inverse_kernel<<<(unsigned)nl, 512, smem, st>>>(leaf_ids, sizes, src_off, src_ld, dst_off, Wbase,
-                                                  Dbase, status, nn > 0 ? 1 : 0);
 }
 
 // ---------------------------------------------------------------------------
