@@ -343,6 +343,69 @@ def _roofline(h, Bd, Xd, st, nrhs, args, info, rep):
     return roof
 
 
+def _next_rows(h, Bd, Xd, st, args, info, N, terms=4, steps=3):
+    """SURVEY 8(f) NEXT-3 / NEXT-4 on the bench's handle and RHS block (CUDA events on the
+    solve stream, after one warm-up call each): ps_solve_series at 2 and `terms` terms
+    (per extra term = one U application: 16 (2 n_R + n_D + n_F) bytes, 8 nrhs (2 n_R + n_D +
+    2 n_F) flop), and the monostatic RCS sweep (ps_farfield, direction c = the backscatter of
+    incidence c) of the solve's currents."""
+    import torch
+    from hmgen.build import CONFIGS, make_mesh, plane_wave_dirs, rwg_basis
+    from paper_2109_04129_b200 import farfield
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(steps):
+            fn()
+        e1.record(st)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / steps
+
+    R = Bd.shape[1]
+    out = {}
+    t2 = timed(lambda: h.solve_series(Bd, Xd, max_terms=2, stream=st))
+    tn = timed(lambda: h.solve_series(Bd, Xd, max_terms=terms, stream=st))
+    _, rep = h.solve_series(Bd, Xd, max_terms=terms, stream=st)
+    tt = (tn - t2) / (terms - 2)
+    nR, nD, nF = info["nR"], info["nD"], info["nF"]
+    by = 16.0 * (2 * nR + nD + nF) + 16.0 * 6 * N * R
+    fl = 8.0 * R * (2 * nR + nD + 2 * nF)
+    peaks = _peaks()
+    hbm = float(peaks.get("hbm_gbs", 6548.2))
+    out["series"] = {"row": "NEXT-3 n-term series (ps_solve_series)", "terms": terms,
+                     "ms_terms_2": t2, f"ms_terms_{terms}": tn, "ms_per_extra_term": tt,
+                     "value": N * R * terms / (tn * 1e-3), "unit": "N*nrhs*terms/s",
+                     "per_term_roofline": ({"bound": "hbm", "achieved": by / (tt * 1e-3) / 1e9, "peak": hbm,
+                                            "unit": "GB/s", "frac": by / (tt * 1e-3) / 1e9 / hbm}
+                                           if R <= 8 else
+                                           {"bound": "alu", "achieved": fl / (tt * 1e-3) / 1e12, "peak": FP64_PEAK,
+                                            "unit": "TFLOP/s", "frac": fl / (tt * 1e-3) / 1e12 / FP64_PEAK}),
+                     "last_ratio_max": float((rep["it_norm"][-1] / rep["it_norm"][-2]).max()),
+                     "launches": int(rep["launches"])}
+    name = args.config
+    if name in CONFIGS and R == len(plane_wave_dirs(CONFIGS[name])[1]):
+        cfg = CONFIGS[name]
+        m = make_mesh(cfg)
+        bs = rwg_basis(m)
+        _, khat, _ = plane_wave_dirs(cfg)
+        g = [torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in (m.nodes, m.tris, bs.tp, bs.tm, bs.vp, bs.vm)]
+        rh = torch.from_numpy(-np.asarray(khat)).cuda()
+        h.solve(Bd, Xd, stream=st, want_norms=False)
+        eta = 120 * np.pi
+        tr = timed(lambda: farfield(*g, cfg.k, eta, Xd, rh, mono=True, stream=st))
+        pairs = R * 14 * bs.N
+        out["rcs"] = {"row": "NEXT-4 monostatic RCS sweep (ps_farfield)", "directions": R, "ms": tr,
+                      "value": pairs / (tr * 1e-3), "unit": "direction-sample pairs/s",
+                      "roofline": {"bound": "alu", "achieved": 26.0 * pairs / (tr * 1e-3) / 1e12, "peak": FP64_PEAK,
+                                   "unit": "TFLOP/s", "frac": 26.0 * pairs / (tr * 1e-3) / 1e12 / FP64_PEAK,
+                                   "note": "13 FMA per pair counted (phase 3, current x phase 4, 3 complex "
+                                           "accumulations 6); the FP64 sincos per pair is not counted"}}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -354,6 +417,8 @@ def main():
     ap.add_argument("--nrhs", type=int, default=0, help="RHS columns (default: the config's full table)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nrhs1", action="store_true", help="skip the embedded nrhs = 1 (HBM-bound) measurement")
+    ap.add_argument("--no-next", action="store_true",
+                    help="skip the NEXT-3 (n-term series) / NEXT-4 (RCS) timings on the bench handle")
     ap.add_argument("--profile-steps", type=int, default=2)
     ap.add_argument("--ref-seconds", type=float, default=0.0,
                     help="--impl reference: seconds of oracle work per step (default: 60 s / steps, 2..20 s)")
@@ -486,6 +551,9 @@ def main():
         line["nrhs1"] = {"workload": f"{args.config}-1 (first column of the same block)",
                          "value": N * world / (ms1 * 1e-3), "unit": UNIT, "ms_per_step": ms1,
                          "roofline": roof1, "clocks": clk1.summary()}
+    # ---- SURVEY 8(f) rows after the two-term solve, on the same handle and block ----
+    if not args.no_next and mode == "cols" and world == 1:
+        line["next_rows"] = _next_rows(h, Bd, Xd, st, args, info, N)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, det = cpu_oracle_arm(meta, B)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": det["cores"], "kind": "oracle",

@@ -17,6 +17,9 @@
 // (4 DFMA per complex multiply-add). DESIGN.md §Roofline derives the peak.
 #include "ps_internal.h"
 
+#include <cooperative_groups.h>
+
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -2091,12 +2094,169 @@ inverse_kernel(const int32_t* __restrict__ leaf_ids, const int32_t* __restrict__
   if (tid == 0) status[l] = 0;
 }
 
+// Blocks too large for one CTA's shared memory (C3's and C5's separator leaves, up to 375
+// unknowns): one thread-block CLUSTER of CL CTAs per block, CTA r holding columns
+// [r w, min(n, (r + 1) w)) of the working matrix in its own shared memory (w = ceil(n / CL)).
+// Per pivot k the CTA owning column k picks the pivot (the same rule: max |z|^2, lowest row on
+// ties) and writes column k as it reads after the row swap, and the pivot row, into every CTA's
+// shared memory (distributed shared memory, double-buffered by the parity of k); one cluster
+// barrier; every CTA then swaps, scales and eliminates its own columns (a warp per column).
+// The final column interchanges become one permuted store per column.
+constexpr int INVC_T = 256;
+
+__global__ void __launch_bounds__(INVC_T)
+inverse_cluster_kernel(const int32_t* __restrict__ sizes, const int64_t* __restrict__ src_off,
+                       const int64_t* __restrict__ src_ld, const int64_t* __restrict__ dst_off,
+                       const double2* __restrict__ Wb, double2* __restrict__ Db, int32_t* __restrict__ status,
+                       int n_lo, int n_hi) {
+  namespace cg = cooperative_groups;
+  extern __shared__ __align__(16) double2 smc[];
+  __shared__ double red_v[32];
+  __shared__ int red_i[32];
+  __shared__ double s_part[16];                        // Frobenius partials of the CTAs (rank 0's copy used)
+  __shared__ double s_tol2;
+  __shared__ int s_r, s_sing;
+  cg::cluster_group cl = cg::this_cluster();
+  const int CL = (int)cl.num_blocks(), rk = (int)cl.block_rank();
+  const int l = blockIdx.x / CL;
+  const int n = sizes[l];
+  if (n < n_lo || n > n_hi) return;                    // the whole cluster returns
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  const int w = (n + CL - 1) / CL;
+  const int j0 = min(n, rk * w), j1 = min(n, j0 + w), nj = j1 - j0;
+  double2* a = smc;                                    // n x w, column-major, ld n
+  double2* cbuf = smc + (size_t)n * w;                 // 2 x n: column k after the swap, by parity of k
+  int* meta = (int*)(cbuf + 2 * n);                    // [par]: pivot row, [2 + par]: singular
+  int* piv = meta + 4;                                 // n pivot rows
+  int* loc = piv + n;                                  // n: final column c <- working column loc[c]
+  const int64_t ld_src = src_ld[l];
+  const double2* src = Wb + src_off[l];
+  double2* dst = Db + dst_off[l];
+  double fro = 0.0;
+  for (int jj = wid; jj < nj; jj += nw)
+    for (int i = lane; i < n; i += 32) {
+      const double2 v = src[i + (int64_t)(j0 + jj) * ld_src];
+      a[i + jj * n] = v;
+      fro += v.x * v.x + v.y * v.y;
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) fro += __shfl_xor_sync(0xffffffffu, fro, o);
+  if (lane == 0) red_v[wid] = fro;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int v = 0; v < nw; ++v) t += red_v[v];
+    *cl.map_shared_rank(&s_part[rk], 0) = t;
+  }
+  cl.sync();
+  if (tid == 0) {
+    const double* p0 = cl.map_shared_rank(s_part, 0);
+    double t = 0.0;
+    for (int v = 0; v < CL; ++v) t += p0[v];          // fixed rank order: the same tolerance everywhere
+    const double f = sqrt(t);
+    s_tol2 = (1e-14 * f) * (1e-14 * f);
+  }
+  __syncthreads();
+  const double tol2 = s_tol2;
+  bool sing = false;
+  for (int k = 0; k < n; ++k) {
+    const int par = k & 1;
+    if (k / w == rk) {                                 // this CTA owns column k
+      __syncthreads();                                 // its columns are up to date
+      const double2* ck = a + (k - j0) * n;
+      double best = -1.0;
+      int bi = n;
+      for (int i = k + tid; i < n; i += nt) {
+        const double m2 = ck[i].x * ck[i].x + ck[i].y * ck[i].y;
+        if (m2 > best) { best = m2; bi = i; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double vo = __shfl_xor_sync(0xffffffffu, best, o);
+        const int io = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (vo > best || (vo == best && io < bi)) { best = vo; bi = io; }
+      }
+      if (lane == 0) { red_v[wid] = best; red_i[wid] = bi; }
+      __syncthreads();
+      if (wid == 0) {
+        best = lane < nw ? red_v[lane] : -1.0;
+        bi = lane < nw ? red_i[lane] : n;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double vo = __shfl_xor_sync(0xffffffffu, best, o);
+          const int io = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (vo > best || (vo == best && io < bi)) { best = vo; bi = io; }
+        }
+        if (lane == 0) { s_r = bi; s_sing = !(best > tol2); }
+      }
+      __syncthreads();
+      const int r = s_r;
+      for (int e = tid; e < n * CL; e += nt) {
+        const int q = e / n, i = e - q * n;
+        *cl.map_shared_rank(cbuf + par * n + i, q) = ck[i == k ? r : i == r ? k : i];
+      }
+      if (tid < CL) {
+        *cl.map_shared_rank(meta + par, tid) = r;
+        *cl.map_shared_rank(meta + 2 + par, tid) = s_sing;
+        *cl.map_shared_rank(piv + k, tid) = r;
+      }
+    }
+    cl.sync();
+    if (meta[2 + par]) { sing = true; break; }
+    const int r = meta[par];
+    const double2* colk = cbuf + par * n;
+    const double2 p = colk[k];
+    const double pm = p.x * p.x + p.y * p.y;
+    const double2 inv = make_double2(p.x / pm, -p.y / pm);
+    for (int jj = wid; jj < nj; jj += nw) {
+      const int j = j0 + jj;
+      double2* c = a + jj * n;
+      const double2 old_k = c[k];                      // row k before the swap (becomes row r)
+      const double2 v = (j == k) ? make_double2(1.0, 0.0) : c[r];
+      const double2 rkv = make_double2(v.x * inv.x - v.y * inv.y, v.x * inv.y + v.y * inv.x);
+      __syncwarp();
+      for (int i = lane; i < n; i += 32) {
+        if (i == k) { c[k] = rkv; continue; }
+        const double2 f = colk[i];
+        double2 base = (j == k) ? make_double2(0.0, 0.0) : (i == r ? old_k : c[i]);
+        base.x -= f.x * rkv.x - f.y * rkv.y;
+        base.y -= f.x * rkv.y + f.y * rkv.x;
+        c[i] = base;
+      }
+    }
+  }
+  if (!sing) {
+    if (tid == 0) {                                    // the column interchanges, composed
+      for (int c = 0; c < n; ++c) loc[c] = c;
+      for (int k = n - 1; k >= 0; --k) {
+        const int t = loc[k];
+        loc[k] = loc[piv[k]];
+        loc[piv[k]] = t;
+      }
+    }
+    __syncthreads();
+    for (int c = wid; c < n; c += nw) {
+      const int jw = loc[c];
+      if (jw < j0 || jw >= j1) continue;
+      const double2* col = a + (jw - j0) * n;
+      for (int i = lane; i < n; i += 32) dst[i + (int64_t)c * n] = col[i];
+    }
+  }
+  if (rk == 0 && tid == 0) status[l] = sing ? 1 : 0;
+  cl.sync();                                           // no CTA leaves while its shared memory may be written
+}
+
+static size_t inv_cluster_smem(int n, int CL) {
+  const int w = (n + CL - 1) / CL;
+  return (size_t)n * w * sizeof(double2) + 2 * (size_t)n * sizeof(double2) + (4 + 2 * (size_t)n) * sizeof(int) + 16;
+}
+
 void launch_inverse(int64_t nl, const int32_t* leaf_ids, const int32_t* sizes, const int64_t* src_off,
                     const int64_t* src_ld, const int64_t* dst_off, const double2* Wbase,
                     double2* Dbase, int32_t* status, int max_n, cudaStream_t st) {
   if (nl <= 0) return;
-  static int max_dyn = -1;
-  if (max_dyn < 0) {                                   // opt-in limit minus the kernel's static reductions
+  static int max_dyn = -1, max_dyn_c = -1;
+  if (max_dyn < 0) {                                   // opt-in limit minus the kernels' static shared memory
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -2104,23 +2264,46 @@ void launch_inverse(int64_t nl, const int32_t* leaf_ids, const int32_t* sizes, c
     cudaFuncGetAttributes(&fa, inverse_kernel);
     max_dyn = optin - (int)fa.sharedSizeBytes;
     cudaFuncSetAttribute(inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
+    cudaFuncAttributes fc{};
+    cudaFuncGetAttributes(&fc, inverse_cluster_kernel);
+    max_dyn_c = optin - (int)fc.sharedSizeBytes;
+    cudaFuncSetAttribute(inverse_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn_c);
+    cudaFuncSetAttribute(inverse_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   }
   auto smem_of = [](int nn, int mn) {
     return (size_t)nn * nn * sizeof(double2) + (size_t)mn * sizeof(double2) + (size_t)mn * sizeof(int) + 16;
   };
-  // blocks up to SMEM_N in shared memory; the larger ones of the level (if any) in a second
-  // launch working in the destination buffer (every CTA of a launch outside its size range
-  // returns at once)
-  const int ns = max_n < SMEM_N ? max_n : SMEM_N;
-  if ((int64_t)smem_of(ns, ns) <= max_dyn) {
+  // sizes >= cmin go to the cluster kernel (default: the ones shared memory of one CTA cannot hold)
+  static const int cmin = [] {
+    const char* e = std::getenv("PS_INV_CLUSTER_MIN");
+    return e ? std::max(1, std::atoi(e)) : SMEM_N + 1;
+  }();
+  const int ns = std::min(max_n, std::min(SMEM_N, cmin - 1));
+  if (ns >= 1)
     inverse_kernel<<<(unsigned)nl, 512, smem_of(ns, ns), st>>>(leaf_ids, sizes, src_off, src_ld, dst_off, Wbase,
                                                                Dbase, status, 1, 0, ns);
-    if (max_n > ns)
-      inverse_kernel<<<(unsigned)nl, 512, smem_of(0, max_n), st>>>(leaf_ids, sizes, src_off, src_ld, dst_off,
-                                                                   Wbase, Dbase, status, 0, ns + 1, max_n);
-  } else {
-    inverse_kernel<<<(unsigned)nl, 512, smem_of(0, max_n), st>>>(leaf_ids, sizes, src_off, src_ld, dst_off, Wbase,
-                                                                 Dbase, status, 0, 0, max_n);
+  if (max_n <= ns) return;
+  int CL = 0;
+  for (int c : {8, 16})
+    if ((int64_t)inv_cluster_smem(max_n, c) <= max_dyn_c) { CL = c; break; }
+  if (CL) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(nl * CL));
+    cfg.blockDim = dim3(INVC_T);
+    cfg.dynamicSmemBytes = inv_cluster_smem(max_n, CL);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, inverse_cluster_kernel, sizes, src_off, src_ld, dst_off, Wbase, Dbase, status,
+                       ns + 1, max_n);
+  } else {                                             // larger still: in place in the destination (L2)
+    inverse_kernel<<<(unsigned)nl, 512, smem_of(0, max_n), st>>>(leaf_ids, sizes, src_off, src_ld, dst_off,
+                                                                 Wbase, Dbase, status, 0, ns + 1, max_n);
   }
 }
 

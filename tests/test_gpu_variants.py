@@ -53,7 +53,7 @@ def _run(path, nrhs, env, out):
 @pytest.mark.parametrize("env", [{"PS_CHAINS": "0"}, {"PS_MMA": "dmma"},
                                  {"PS_MMA": "dfma"}, {"PS_SOLVE": "stages"},
                                  {"PS_SLOT_BUDGET_MB": "-1"}, {"PS_KSPLIT": "0"}, {"PS_DEFER_FIN": "0"},
-                                 {"PS_SLOT_REUSE": "0"}, {}],
+                                 {"PS_SLOT_REUSE": "0"}, {"PS_INV_CLUSTER_MIN": "1"}, {}],
                          ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default")
 @pytest.mark.parametrize("nrhs", [1, 70])
 def test_variant_matches_oracle(cfgdata, tmp_path, env, nrhs):
