@@ -21,6 +21,9 @@ tail -n 3 $O/pytest_gpu.log
 timeout 300 python __graft_entry__.py > $O/smoke.log 2>&1; echo "smoke=$?"; tail -n 1 $O/smoke.log
 fi
 timeout 900 python bench.py > $O/bench_C4.json 2> $O/bench_C4.err; echo "bench=$?"
+if [ -f data/C5.hm ] || ls data/C5* > /dev/null 2>&1; then
+  PS_VERBOSE=1 timeout 900 python bench.py --config C5 --steps 3 --no-cpu-baseline --no-next > $O/bench_C5.json 2> $O/bench_C5.err; echo "bench_C5=$?"
+fi
 for c in C2 C3; do
   timeout 300 python bench.py --config $c --no-cpu-baseline > $O/bench_$c.json 2> $O/bench_$c.err; echo "bench_$c=$?"
 done
