@@ -14,6 +14,25 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: minutes of CPU (large configs)")
 
 
+@pytest.hookimpl(trylast=True)
+def pytest_collection_modifyitems(config, items):
+    """GPU session: test_gpu_c5.py last, its 7-minute input generation started now in a child
+    process (tests/_prefetch.py) so that it overlaps the other configs' GPU tests."""
+    c5 = [it for it in items if os.path.basename(str(it.fspath)) == "test_gpu_c5.py" and it.get_closest_marker("gpu")]
+    if not c5:
+        return
+    rest = [it for it in items if it not in c5]
+    items[:] = rest + c5
+    if rest and os.path.exists("/dev/nvidia0"):
+        from tests import _prefetch
+        _prefetch.start("C5")
+
+
+def pytest_sessionfinish(session, exitstatus):
+    from tests import _prefetch
+    _prefetch.stop()
+
+
 @pytest.fixture(scope="session")
 def cfgdata():
     """Generated physical configs (cached under data/ or $PS_DATA_DIR)."""

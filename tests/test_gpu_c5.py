@@ -70,6 +70,8 @@ def _c5():
     if "h" not in _state:
         from hmgen.build import load_or_generate, read_rhs
         from paper_2109_04129_b200 import PsHandle
+        from tests import _prefetch
+        _prefetch.wait()                  # the generator child started at collection, if any
         meta = load_or_generate("C5")
         B, _ = read_rhs(meta["rhs"])
         h = PsHandle(meta["hm"])
