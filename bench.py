@@ -238,6 +238,10 @@ def _config(args, meta, nrhs, world):
     return {"workload": f"{args.config}-{nrhs}: {meta['desc']}", "N": meta["N"],
             "nrhs_per_gpu": nrhs, "global_nrhs": getattr(args, "nrhs_global", nrhs),
             "n_leaves": meta["n_leaves"],
+            "queueing": ("value / nrhs1: the K timed solves queued back to back with ps_solve_async (all "
+                         "kernels of every step incl. the Eq. 44-45 norms; no host synchronisation between "
+                         "steps), the last solve's report read with ps_solve_report before the closing "
+                         "synchronisation; e2e: synchronous ps_solve per step (host buffers, full report)"),
             "parallelism": (f"row partition x{world} (elimination-tree subtrees per rank, replicated "
                             f"separators; NCCL all-reduce of separator rows, all-gather of w and x)"
                             if rows else f"rhs-columns x{world} (replicated operator, distinct columns per "
@@ -254,8 +258,19 @@ FP64_PEAK = 37.02   # TF/s: measured on this pool's B200 (scripts/fp64_peak.cu, 
 
 
 def _time_solves(h, Bd, Xd, st, steps, flush_buf, dist, world):
-    """Device ms per solve over `steps` timed solves (CUDA events on the solve stream)."""
+    """Device ms per solve over `steps` timed solves (CUDA events on the solve stream). The
+    solves are queued with ps_solve_async (every kernel of the step, the Eq. 44-45 norms
+    included, no host synchronisation between steps); the report of the last one is read
+    back (ps_solve_report) before the closing synchronisation. Row-partition handles
+    (NCCL) keep the synchronous ps_solve."""
     import torch
+    sync_only = not Bd.is_cuda or (world > 1 and getattr(h, "partitioned", False))
+
+    def step():
+        if sync_only:
+            h.solve(Bd, Xd, stream=st, want_norms=False)
+        else:
+            h.solve_async(Bd, Xd, stream=st)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -265,16 +280,20 @@ def _time_solves(h, Bd, Xd, st, steps, flush_buf, dist, world):
         for a_, b_ in evs:
             flush_buf.fill_(1)
             a_.record(st)
-            h.solve(Bd, Xd, stream=st, want_norms=False)
+            step()
             b_.record(st)
+        if not sync_only:
+            h.solve_report()
         torch.cuda.synchronize()
         ms = sum(a_.elapsed_time(b_) for a_, b_ in evs) / steps
     else:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
         for _ in range(steps):
-            h.solve(Bd, Xd, stream=st, want_norms=False)
+            step()
         e1.record(st)
+        if not sync_only:
+            h.solve_report()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / steps
     torch.cuda.nvtx.range_pop()
@@ -476,6 +495,7 @@ def main():
         obj = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         h = PsHandle(meta["hm"], device=local, rank=rank, nranks=world, partition=True, nccl_id=obj[0])
+        h.partitioned = True
     else:
         h = PsHandle(meta["hm"], device=local, rank=rank, nranks=world)
     st = torch.cuda.current_stream()

@@ -169,6 +169,24 @@ ps_status ps_setup_group(ps_handle* const* hs, int nranks, const ps_setup_opts* 
 ps_status ps_solve(ps_handle* h, int64_t nrhs, const void* B, int64_t ldb, void* X, int64_t ldx,
                    int on_device, void* cuda_stream, ps_report* rep);
 
+/* ps_solve_async — ps_solve for DEVICE buffers without its host synchronisation: the same
+ * kernels (Eqs. 24, 26, 30-36, and the per-column norms of Eqs. 44-45) are queued on
+ * cuda_stream (NULL = the handle's own stream) and the call returns; X, the norms and the
+ * ratios are complete when the stream reaches that point. Successive calls on ONE stream
+ * pipeline (the host queues solve i + 1 while solve i runs); a handle must not be used
+ * from two streams at once (its workspace is shared). The report of the LAST queued solve
+ * is fetched with ps_solve_report. Single-GPU handles only (PS_ESTATE on a row-partition rank).
+ * Arguments as ps_solve with on_device = 1. Errors: PS_EINVAL, PS_ESTATE, PS_ENOMEM, PS_ECUDA
+ * (launch errors only; PS_EDIVERGED is reported by ps_solve_report). */
+ps_status ps_solve_async(ps_handle* h, int64_t nrhs, const void* B, int64_t ldb, void* X, int64_t ldx,
+                         void* cuda_stream);
+
+/* ps_solve_report — synchronise the stream of the last ps_solve_async and fill its report
+ * (rep may be NULL: status only): ||it_0||, ||it_1||, the Eq. 45 ratio per column,
+ * n_diverged; t_solve_ms = device time of that last solve. Returns PS_EDIVERGED like ps_solve.
+ * Errors: PS_EINVAL, PS_ESTATE (nothing pending), PS_ECUDA. */
+ps_status ps_solve_report(ps_handle* h, ps_report* rep);
+
 /* ps_solve_series — the n-term power series: Eqs. (35)-(36),
  * P:195-197, x~ = it_0 - it_1 + it_2 - ... (Eq. 44), it_0 = b_o = Z~_N^{-1} R^T b
  * (Eqs. 24, 32), it_n = U it_{n-1} (Eq. 31), x = R x~ (Eq. 26), with the per-term norm

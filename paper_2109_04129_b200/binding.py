@@ -85,6 +85,10 @@ def load_library():
     L.ps_setup.argtypes = [P, ctypes.POINTER(_Opts)]
     L.ps_solve.restype = I
     L.ps_solve.argtypes = [P, I64, P, I64, P, I64, I, P, ctypes.POINTER(_Report)]
+    L.ps_solve_async.restype = I
+    L.ps_solve_async.argtypes = [P, I64, P, I64, P, I64, P]
+    L.ps_solve_report.restype = I
+    L.ps_solve_report.argtypes = [P, ctypes.POINTER(_Report)]
     L.ps_solve_series.restype = I
     L.ps_solve_series.argtypes = [P, ctypes.POINTER(_SeriesOpts), I64, P, I64, P, I64, I, P,
                                   ctypes.POINTER(_SeriesReport)]
@@ -221,6 +225,32 @@ class PsHandle:
                  status=STATUS_NAMES[st])
         if want_norms:
             r["ratio"] = ratio
+        if st == PS_EDIVERGED:
+            warnings.warn(load_library().ps_last_error(self._h).decode(), RuntimeWarning, stacklevel=2)
+        self.last_report = r
+        return st, r
+
+    def solve_async(self, B, X, stream=None):
+        """Queue the two-term solve of DEVICE tensors on `stream` without synchronising
+        (ps_solve_async); solve_report() later returns the last queued solve's report."""
+        bp, ldb, nrhs, bdev = _ptr_ld(B, self.N)
+        xp, ldx, nrhs2, xdev = _ptr_ld(X, self.N)
+        if nrhs != nrhs2 or not (bdev and xdev):
+            raise ValueError("solve_async takes device tensors of the same shape")
+        s = None
+        if stream is not None:
+            s = ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+        self._pend_nrhs = nrhs
+        self._check(load_library().ps_solve_async(self._h, nrhs, bp, ldb, xp, ldx, s))
+
+    def solve_report(self):
+        """(status, report dict) of the last solve_async (ps_solve_report: synchronises its stream)."""
+        nrhs = getattr(self, "_pend_nrhs", 0) or 1
+        rep, it0, it1, ratio = _report(nrhs, True)
+        st = self._check(load_library().ps_solve_report(self._h, ctypes.byref(rep)))
+        r = dict(it0=it0, it1=it1, ratio=ratio, n_diverged=rep.n_diverged, t_solve_ms=rep.t_solve_ms,
+                 bytes=rep.bytes_moved, flops=rep.flops, launches=rep.kernel_launches,
+                 status=STATUS_NAMES[st])
         if st == PS_EDIVERGED:
             warnings.warn(load_library().ps_last_error(self._h).decode(), RuntimeWarning, stacklevel=2)
         self.last_report = r

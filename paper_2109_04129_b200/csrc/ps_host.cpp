@@ -767,6 +767,8 @@ struct ps_handle {
   std::unique_ptr<SolvePlan> plan;
   DevBuf<double2> series_norms;            // ps_solve_series: per term (||it_n||, ||x~||) per column
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int64_t pend_nrhs = 0;               // ps_solve_async: columns of the solve whose report is pending
+  cudaStream_t pend_stream = nullptr;  //                 and the stream it was queued on
   Prof prof;
   // ---- row partition (ps_dist.partition = 1) ----
   int rank = 0, nranks = 1, part_mode = 0;
@@ -3726,8 +3728,12 @@ ps_status ps_setup_group(ps_handle* const* hs, int nranks, const ps_setup_opts* 
   return PS_OK;
 }
 
-ps_status ps_solve(ps_handle* h, int64_t nrhs, const void* B, int64_t ldb, void* X, int64_t ldx,
-                   int on_device, void* cuda_stream, ps_report* rep) {
+static ps_status finish_report(ps_handle* h, SolvePlan& sp, cudaStream_t s, ps_report* rep);
+
+// ps_solve (defer = false) and ps_solve_async (defer = true: device buffers, no host
+// synchronisation; the report is fetched later by ps_solve_report)
+static ps_status solve_impl(ps_handle* h, int64_t nrhs, const void* B, int64_t ldb, void* X, int64_t ldx,
+                            int on_device, void* cuda_stream, ps_report* rep, bool defer) {
   if (!h) return fail(nullptr, PS_EINVAL, "ps_solve: handle is NULL");
   if (!h->setup_done) return fail(h, PS_ESTATE, "ps_solve: ps_setup has not run");
   if (nrhs < 1 || !B || !X || ldb < h->N || ldx < h->N)
@@ -3802,25 +3808,44 @@ ps_status ps_solve(ps_handle* h, int64_t nrhs, const void* B, int64_t ldb, void*
     launches += aux(h, s, [&] { launch_permute_out(N, R, h->d_e2rwg.p, xres, Xd, on_device ? ldx : N, s); });
     CK(cudaEventRecord(h->ev1, s));
     CK(cudaGetLastError());
+    sp.launches_per_solve = launches;
+    h->pend_nrhs = R;
+    h->pend_stream = s;
+    if (defer) return PS_OK;
     if (!on_device)
       CK(cudaMemcpy2DAsync(X, 16 * ldx, sp.stage.p, 16 * N, 16 * N, nrhs, cudaMemcpyDeviceToHost, s));
+    return finish_report(h, sp, s, rep);
+  } catch (const PsError& e) {
+    return fail(h, e.st, "ps_solve: " + e.msg);
+  } catch (const std::bad_alloc&) {
+    return fail(h, PS_ENOMEM, "ps_solve: host allocation failed");
+  }
+  return PS_OK;
+}
+
+// the host half of a solve: norms of the plan's last solve read back (synchronises s), Eq. 45
+// ratios, divergence status, report
+static ps_status finish_report(ps_handle* h, SolvePlan& sp, cudaStream_t s, ps_report* rep) {
+  const int64_t R = sp.nrhs;
+  const int64_t launches = sp.launches_per_solve;
+  {
     std::vector<double2> norms(R);
     CK(cudaMemcpyAsync(norms.data(), sp.norms.p, 16 * R, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    h->pend_nrhs = 0;
     if (h->prof.on) h->prof.collect();
     int ndiv = 0;
     for (int64_t c = 0; c < R; ++c) {
       const double r = norms[c].x > 0 ? norms[c].y / norms[c].x : 0.0;
       if (!(r < h->ratio_threshold)) ++ndiv;
     }
-    sp.launches_per_solve = launches;
     if (rep) {
       float ms = 0;
       CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
       rep->t_solve_ms = ms;
       rep->n_diverged = ndiv;
-      rep->bytes_moved = solve_bytes(h, nrhs);
-      rep->flops = solve_flops(h, nrhs);
+      rep->bytes_moved = solve_bytes(h, R);
+      rep->flops = solve_flops(h, R);
       rep->kernel_launches = launches;
       const int64_t cap = std::min<int64_t>(rep->nrhs, R);
       for (int64_t c = 0; c < cap; ++c) {
@@ -3832,12 +3857,32 @@ ps_status ps_solve(ps_handle* h, int64_t nrhs, const void* B, int64_t ldb, void*
     if (ndiv > 0)
       return fail(h, PS_EDIVERGED, "ps_solve: " + std::to_string(ndiv) + " of " + std::to_string(R) +
                                        " columns have ||it_1||/||it_0|| >= " + std::to_string(h->ratio_threshold));
-  } catch (const PsError& e) {
-    return fail(h, e.st, "ps_solve: " + e.msg);
-  } catch (const std::bad_alloc&) {
-    return fail(h, PS_ENOMEM, "ps_solve: host allocation failed");
   }
   return PS_OK;
+}
+
+ps_status ps_solve(ps_handle* h, int64_t nrhs, const void* B, int64_t ldb, void* X, int64_t ldx,
+                   int on_device, void* cuda_stream, ps_report* rep) {
+  return solve_impl(h, nrhs, B, ldb, X, ldx, on_device, cuda_stream, rep, false);
+}
+
+ps_status ps_solve_async(ps_handle* h, int64_t nrhs, const void* B, int64_t ldb, void* X, int64_t ldx,
+                         void* cuda_stream) {
+  if (h && h->part_mode) return fail(h, PS_ESTATE, "ps_solve_async: row-partition handles solve with ps_solve");
+  return solve_impl(h, nrhs, B, ldb, X, ldx, 1, cuda_stream, nullptr, true);
+}
+
+ps_status ps_solve_report(ps_handle* h, ps_report* rep) {
+  if (!h) return fail(nullptr, PS_EINVAL, "ps_solve_report: handle is NULL");
+  if (h->pend_nrhs < 1) return fail(h, PS_ESTATE, "ps_solve_report: no ps_solve_async is pending");
+  try {
+    CK(cudaSetDevice(h->device));
+    return finish_report(h, get_plan(h, h->pend_nrhs), h->pend_stream, rep);
+  } catch (const PsError& e) {
+    return fail(h, e.st, "ps_solve_report: " + e.msg);
+  } catch (const std::bad_alloc&) {
+    return fail(h, PS_ENOMEM, "ps_solve_report: host allocation failed");
+  }
 }
 
 ps_status ps_apply(ps_handle* h, int op, int64_t nrhs, const void* Xin, void* Yout) {

@@ -123,6 +123,37 @@ def test_solve_c1(cfgdata, nrhs):
     _solve_check(meta["hm"], B)
 
 
+@pytest.mark.parametrize("nrhs", [1, 40])
+def test_solve_async_matches_solve(cfgdata, nrhs):
+    """ps_solve_async queues the same kernels without a host sync: three solves pipelined on
+    one stream (different inputs, one workspace) equal the synchronous solves bitwise, and
+    ps_solve_report returns the last one's norms / status; the result also meets the oracle bar."""
+    meta = cfgdata("C1")
+    H, S, h = _load(meta["hm"])
+    st = torch.cuda.Stream()
+    Bs = [_dev(random_rhs(H.N, nrhs, 20 + i)) for i in range(3)]
+    Xs = [torch.empty_like(b) for b in Bs]
+    Xa = [torch.empty_like(b) for b in Bs]
+    reps = [h.solve(b, x)[1] for b, x in zip(Bs, Xs)]
+    st.wait_stream(torch.cuda.current_stream())
+    with pytest.raises(PsError) as ei:          # nothing pending yet
+        h.solve_report()
+    assert ei.value.status == PS_ESTATE
+    for b, x in zip(Bs, Xa):
+        h.solve_async(b, x, stream=st)
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        status, rep = h.solve_report()
+    for x, y in zip(Xs, Xa):
+        assert torch.equal(x, y)
+    assert np.array_equal(rep["it0"], reps[-1]["it0"]) and np.array_equal(rep["it1"], reps[-1]["it1"])
+    assert rep["n_diverged"] == reps[-1]["n_diverged"] and (status == PS_EDIVERGED) == (rep["n_diverged"] > 0)
+    ref = solve(H, S, _host(Bs[-1]))
+    assert rel_l2_cols(_host(Xa[-1]), ref.x).max() <= TOL
+    assert np.allclose(rep["ratio"], ref.ratio, rtol=1e-10)
+
+
 def test_solve_t2_plane_waves(cfgdata):
     meta = cfgdata("T2")
     B, _ = read_rhs(meta["rhs"])

@@ -72,6 +72,8 @@ def test_null_arguments():
     assert L.ps_setup(None, None) == binding.PS_EINVAL
     assert L.ps_solve(None, 1, None, 1, None, 1, 1, None, None) == binding.PS_EINVAL
     assert L.ps_solve_series(None, None, 1, None, 1, None, 1, 1, None, None) == binding.PS_EINVAL
+    assert L.ps_solve_async(None, 1, None, 1, None, 1, None) == binding.PS_EINVAL
+    assert L.ps_solve_report(None, None) == binding.PS_EINVAL
     L.ps_free(None)                     # NULL-safe
 
 
