@@ -119,11 +119,17 @@ constexpr int GM_MAXSEG = 96;     // max segments per work item
 // no float atomics. Work units: a pack of small blocks (each applied whole by one warp), or
 // one big block, cut into row chunks applied in order by ONE CTA (F1 chunks -> p1; F2 chunks
 // -> y2 rows and p2; F1 chunks again -> y1 rows), so no unit waits on another.
-constexpr int F1P_CH = 1216;      // factor elements staged per item (19 KB; 3 stages + scratch: 2 CTAs / SM)
+#ifndef PS_F1P_CH                 // -DPS_F1P_CH / -DPS_F1P_NS: tiling A/B builds (scripts/f1p_variants.sh)
+#define PS_F1P_CH 1216
+#endif
+#ifndef PS_F1P_NS
+#define PS_F1P_NS 3
+#endif
+constexpr int F1P_CH = PS_F1P_CH; // factor elements staged per item (19 KB; 3 stages + scratch: 2 CTAs / SM)
 constexpr int F1P_RMAX = 64;      // max rank (dense: shorter side) of a block on this path
 constexpr int F1P_XCH = 512;      // x rows x nrhs staged per item (complex elements)
 constexpr int F1P_PACK = 32;      // max blocks per pack item
-constexpr int F1P_NS = 3;         // shared-memory ring stages of the far1p kernel
+constexpr int F1P_NS = PS_F1P_NS;       // shared-memory ring stages of the far1p kernel
 constexpr int F1P_CWARPS = 8;     // consumer warps of the far1p kernel
 struct FBlk {
   int64_t o1, o2;          // element offsets (operator base) of F1 (n1 x r) / F2 (n2 x r); dense: G, -1

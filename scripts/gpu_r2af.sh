@@ -19,6 +19,10 @@ timeout 300 python bench.py --config C1 --nrhs 1 --no-cpu-baseline > $O/bench_C1
 if [ -f data/C5.hm ]; then
   PS_VERBOSE=1 timeout 900 python bench.py --config C5 --steps 3 --no-cpu-baseline --no-next > $O/bench_C5.json 2> $O/bench_C5.err; echo "bench_C5=$?"
 fi
+for v in base 1824_2 2240_2 768_4; do   # far1p tiling A/B (scripts/f1p_variants.sh), C4 at 1 RHS
+  L=ab_libs/libps_$v.so; [ $v = base ] && L=paper_2109_04129_b200/libps.so
+  [ -f $L ] && PS_LIB=$L timeout 300 python bench.py --config C4 --nrhs 1 --no-cpu-baseline --no-next > $O/ab_f1p_$v.json 2> $O/ab_f1p_$v.err
+done
 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $O/plain_launch.log 2>&1 && \
 timeout 900 ncu --nvtx --nvtx-include "timed/" --metrics gpu__time_duration.sum --clock-control none --csv \
    --log-file $O/ncu_launches_C4.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1; echo "ncu_list=$?"
