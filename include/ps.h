@@ -159,7 +159,11 @@ ps_status ps_setup_group(ps_handle* const* hs, int nranks, const ps_setup_opts* 
  *   B, ldb    : N x nrhs input, column-major, ldb >= N; read only.
  *   X, ldx    : N x nrhs output, column-major, ldx >= N; must not overlap B.
  *   on_device : 0 = B and X are host pointers (any host memory; pinned is
- *               faster); 1 = device pointers on this handle's GPU.
+ *               faster); 1 = device pointers on this handle's GPU. Host blocks of
+ *               >= 256 columns are solved as two column halves whose host<->device
+ *               copies run on the handle's copy streams under the other half's
+ *               kernels (columns are independent problems; same result as two
+ *               ps_solve calls on the halves).
  *   cuda_stream : cudaStream_t to order the work on, or NULL for the handle's
  *               own stream. With on_device=1 the call returns once the work is
  *               queued AND complete (it synchronises the stream).

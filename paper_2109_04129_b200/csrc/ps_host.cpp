@@ -767,6 +767,9 @@ struct ps_handle {
   std::unique_ptr<SolvePlan> plan;
   DevBuf<double2> series_norms;            // ps_solve_series: per term (||it_n||, ||x~||) per column
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaStream_t cs_in = nullptr, cs_out = nullptr;   // ps_solve on host buffers, pipelined halves:
+  cudaEvent_t hp_ev[6] = {};                        // copy streams, ordering events, staging
+  DevBuf<double2> hp_in[2], hp_out[2], hp_norms;
   int64_t pend_nrhs = 0;               // ps_solve_async: columns of the solve whose report is pending
   cudaStream_t pend_stream = nullptr;  //                 and the stream it was queued on
   Prof prof;
@@ -3728,43 +3731,16 @@ ps_status ps_setup_group(ps_handle* const* hs, int nranks, const ps_setup_opts* 
   return PS_OK;
 }
 
-static ps_status finish_report(ps_handle* h, SolvePlan& sp, cudaStream_t s, ps_report* rep);
+static ps_status finish_report(ps_handle* h, const double2* d_norms, int64_t R, int64_t launches, cudaStream_t s,
+                                ps_report* rep);
 
-// ps_solve (defer = false) and ps_solve_async (defer = true: device buffers, no host
-// synchronisation; the report is fetched later by ps_solve_report)
-static ps_status solve_impl(ps_handle* h, int64_t nrhs, const void* B, int64_t ldb, void* X, int64_t ldx,
-                            int on_device, void* cuda_stream, ps_report* rep, bool defer) {
-  if (!h) return fail(nullptr, PS_EINVAL, "ps_solve: handle is NULL");
-  if (!h->setup_done) return fail(h, PS_ESTATE, "ps_solve: ps_setup has not run");
-  if (nrhs < 1 || !B || !X || ldb < h->N || ldx < h->N)
-    return fail(h, PS_EINVAL, "ps_solve: bad arguments (nrhs >= 1, B/X non-NULL, ldb/ldx >= N)");
+// Every kernel of one two-term solve of sp.nrhs columns, queued on s: Bd / Xd are DEVICE
+// column-major blocks (ld ldb_d / ldx_d). Returns the number of launches.
+static int64_t queue_solve(ps_handle* h, SolvePlan& sp, const double2* Bd, int64_t ldb_d, double2* Xd,
+                           int64_t ldx_d, cudaStream_t s) {
+  const int64_t N = h->N, R = sp.nrhs;
+  int64_t launches = 0;
   {
-    const char* b0 = (const char*)B;
-    const char* b1 = b0 + 16 * (ldb * (nrhs - 1) + h->N);
-    const char* x0 = (const char*)X;
-    const char* x1 = x0 + 16 * (ldx * (nrhs - 1) + h->N);
-    if (b0 < x1 && x0 < b1) return fail(h, PS_EINVAL, "ps_solve: X overlaps B");
-  }
-  if (h->part_mode) {
-    if (!h->nccl)
-      return fail(h, PS_ESTATE, "ps_solve: in-process row-partition handle (no NCCL id): use ps_solve_group");
-    ps_handle* hs[1] = {h};
-    return finish_dist(hs, 1, nrhs, B, ldb, X, ldx, on_device, cuda_stream, rep, "ps_solve");
-  }
-  try {
-    CK(cudaSetDevice(h->device));
-    cudaStream_t s = cuda_stream ? (cudaStream_t)cuda_stream : h->stream;
-    SolvePlan& sp = get_plan(h, nrhs);
-    const int64_t N = h->N, R = nrhs;
-    int64_t launches = 0;
-    const double2* Bd = (const double2*)B;
-    int64_t ldb_d = ldb;
-    if (!on_device) {
-      CK(cudaMemcpy2DAsync(sp.stage.p, 16 * N, B, 16 * ldb, 16 * N, nrhs, cudaMemcpyHostToDevice, s));
-      Bd = sp.stage.p;
-      ldb_d = N;
-    }
-    CK(cudaEventRecord(h->ev0, s));
     // default: the whole solve as one dataflow launch (build_program: chain-collapsed
     // sweeps, E-order far field, producer-keyed tickets); PS_SOLVE=stages runs one
     // launch per operator (the tables ps_apply uses)
@@ -3804,8 +3780,104 @@ static ps_status solve_impl(ps_handle* h, int64_t nrhs, const void* B, int64_t l
     }) + 1;
     launches += op_R(h, sp, sp.xt.p, sp.xt.p, s);                       // x = R x~       (Eq. 26)
     }
-    double2* Xd = on_device ? (double2*)X : sp.stage.p;
-    launches += aux(h, s, [&] { launch_permute_out(N, R, h->d_e2rwg.p, xres, Xd, on_device ? ldx : N, s); });
+    launches += aux(h, s, [&] { launch_permute_out(N, R, h->d_e2rwg.p, xres, Xd, ldx_d, s); });
+  }
+  return launches;
+}
+
+
+// ps_solve with HOST buffers and many columns: the block is solved as two column halves of equal
+// width c = ceil(nrhs / 2) (one plan; an odd block's second half carries one padding column
+// that is never copied out), so that the copies overlap the kernels: H2D of both halves on
+// one copy stream, the halves' kernels on s in turn (each waits for its own H2D), D2H of a half
+// on a second copy stream as soon as its permute_out is done (half 0's D2H and half 1's H2D run
+// under the other half's kernels). Columns are independent problems (Eqs. 24-36 act column by
+// column), so the result is the narrower launch's; s waits for the last D2H before the report.
+static ps_status solve_host_pipelined(ps_handle* h, int64_t nrhs, const void* B, int64_t ldb, void* X, int64_t ldx,
+                                      cudaStream_t s, ps_report* rep) {
+  const int64_t N = h->N, c = (nrhs + 1) / 2;
+  if (!h->cs_in) {
+    CK(cudaStreamCreateWithFlags(&h->cs_in, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&h->cs_out, cudaStreamNonBlocking));
+    for (auto& e : h->hp_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  SolvePlan& sp = get_plan(h, c);
+  for (int i = 0; i < 2; ++i) {
+    if (h->hp_in[i].cap < N * c) {
+      h->hp_in[i].alloc(N * c);
+      CK(cudaMemsetAsync(h->hp_in[i].p, 0, 16 * N * c, s));        // the padding column stays finite
+    }
+    h->hp_out[i].alloc(N * c);
+  }
+  h->hp_norms.alloc(2 * c);
+  const double2* Bh = (const double2*)B;
+  double2* Xh = (double2*)X;
+  const int64_t w[2] = {c, nrhs - c};
+  CK(cudaEventRecord(h->ev0, s));
+  CK(cudaEventRecord(h->hp_ev[0], s));                 // the copy streams start after s's earlier work
+  CK(cudaStreamWaitEvent(h->cs_in, h->hp_ev[0], 0));
+  CK(cudaStreamWaitEvent(h->cs_out, h->hp_ev[0], 0));
+  for (int i = 0; i < 2; ++i) {
+    CK(cudaMemcpy2DAsync(h->hp_in[i].p, 16 * N, Bh + (int64_t)i * c * ldb, 16 * ldb, 16 * N, w[i],
+                         cudaMemcpyHostToDevice, h->cs_in));
+    CK(cudaEventRecord(h->hp_ev[1 + i], h->cs_in));
+  }
+  int64_t launches = 0;
+  for (int i = 0; i < 2; ++i) {
+    CK(cudaStreamWaitEvent(s, h->hp_ev[1 + i], 0));
+    launches += queue_solve(h, sp, h->hp_in[i].p, N, h->hp_out[i].p, N, s);
+    CK(cudaMemcpyAsync(h->hp_norms.p + (int64_t)i * c, sp.norms.p, 16 * c, cudaMemcpyDeviceToDevice, s));
+    CK(cudaEventRecord(h->hp_ev[3 + i], s));
+    CK(cudaStreamWaitEvent(h->cs_out, h->hp_ev[3 + i], 0));
+    CK(cudaMemcpy2DAsync(Xh + (int64_t)i * c * ldx, 16 * ldx, h->hp_out[i].p, 16 * N, 16 * N, w[i],
+                         cudaMemcpyDeviceToHost, h->cs_out));
+  }
+  CK(cudaEventRecord(h->hp_ev[5], h->cs_out));
+  CK(cudaStreamWaitEvent(s, h->hp_ev[5], 0));
+  CK(cudaEventRecord(h->ev1, s));
+  CK(cudaGetLastError());
+  sp.launches_per_solve = launches / 2;
+  return finish_report(h, h->hp_norms.p, nrhs, launches, s, rep);
+}
+
+// ps_solve (defer = false) and ps_solve_async (defer = true: device buffers, no host
+// synchronisation; the report is fetched later by ps_solve_report)
+static ps_status solve_impl(ps_handle* h, int64_t nrhs, const void* B, int64_t ldb, void* X, int64_t ldx,
+                            int on_device, void* cuda_stream, ps_report* rep, bool defer) {
+  if (!h) return fail(nullptr, PS_EINVAL, "ps_solve: handle is NULL");
+  if (!h->setup_done) return fail(h, PS_ESTATE, "ps_solve: ps_setup has not run");
+  if (nrhs < 1 || !B || !X || ldb < h->N || ldx < h->N)
+    return fail(h, PS_EINVAL, "ps_solve: bad arguments (nrhs >= 1, B/X non-NULL, ldb/ldx >= N)");
+  {
+    const char* b0 = (const char*)B;
+    const char* b1 = b0 + 16 * (ldb * (nrhs - 1) + h->N);
+    const char* x0 = (const char*)X;
+    const char* x1 = x0 + 16 * (ldx * (nrhs - 1) + h->N);
+    if (b0 < x1 && x0 < b1) return fail(h, PS_EINVAL, "ps_solve: X overlaps B");
+  }
+  if (h->part_mode) {
+    if (!h->nccl)
+      return fail(h, PS_ESTATE, "ps_solve: in-process row-partition handle (no NCCL id): use ps_solve_group");
+    ps_handle* hs[1] = {h};
+    return finish_dist(hs, 1, nrhs, B, ldb, X, ldx, on_device, cuda_stream, rep, "ps_solve");
+  }
+  try {
+    CK(cudaSetDevice(h->device));
+    cudaStream_t s = cuda_stream ? (cudaStream_t)cuda_stream : h->stream;
+    static const int64_t pipe_min = env_int("PS_HOST_PIPE_MIN", 256);
+    if (!on_device && !defer && nrhs >= pipe_min && nrhs >= 2) return solve_host_pipelined(h, nrhs, B, ldb, X, ldx, s, rep);
+    SolvePlan& sp = get_plan(h, nrhs);
+    const int64_t N = h->N, R = nrhs;
+    int64_t launches = 0;
+    const double2* Bd = (const double2*)B;
+    int64_t ldb_d = ldb;
+    if (!on_device) {
+      CK(cudaMemcpy2DAsync(sp.stage.p, 16 * N, B, 16 * ldb, 16 * N, nrhs, cudaMemcpyHostToDevice, s));
+      Bd = sp.stage.p;
+      ldb_d = N;
+    }
+    CK(cudaEventRecord(h->ev0, s));
+    launches += queue_solve(h, sp, Bd, ldb_d, on_device ? (double2*)X : sp.stage.p, on_device ? ldx : N, s);
     CK(cudaEventRecord(h->ev1, s));
     CK(cudaGetLastError());
     sp.launches_per_solve = launches;
@@ -3814,7 +3886,7 @@ static ps_status solve_impl(ps_handle* h, int64_t nrhs, const void* B, int64_t l
     if (defer) return PS_OK;
     if (!on_device)
       CK(cudaMemcpy2DAsync(X, 16 * ldx, sp.stage.p, 16 * N, 16 * N, nrhs, cudaMemcpyDeviceToHost, s));
-    return finish_report(h, sp, s, rep);
+    return finish_report(h, sp.norms.p, R, launches, s, rep);
   } catch (const PsError& e) {
     return fail(h, e.st, "ps_solve: " + e.msg);
   } catch (const std::bad_alloc&) {
@@ -3825,12 +3897,11 @@ static ps_status solve_impl(ps_handle* h, int64_t nrhs, const void* B, int64_t l
 
 // the host half of a solve: norms of the plan's last solve read back (synchronises s), Eq. 45
 // ratios, divergence status, report
-static ps_status finish_report(ps_handle* h, SolvePlan& sp, cudaStream_t s, ps_report* rep) {
-  const int64_t R = sp.nrhs;
-  const int64_t launches = sp.launches_per_solve;
+static ps_status finish_report(ps_handle* h, const double2* d_norms, int64_t R, int64_t launches, cudaStream_t s,
+                                ps_report* rep) {
   {
     std::vector<double2> norms(R);
-    CK(cudaMemcpyAsync(norms.data(), sp.norms.p, 16 * R, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(norms.data(), d_norms, 16 * R, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     h->pend_nrhs = 0;
     if (h->prof.on) h->prof.collect();
@@ -3877,7 +3948,8 @@ ps_status ps_solve_report(ps_handle* h, ps_report* rep) {
   if (h->pend_nrhs < 1) return fail(h, PS_ESTATE, "ps_solve_report: no ps_solve_async is pending");
   try {
     CK(cudaSetDevice(h->device));
-    return finish_report(h, get_plan(h, h->pend_nrhs), h->pend_stream, rep);
+    SolvePlan& sp = get_plan(h, h->pend_nrhs);
+    return finish_report(h, sp.norms.p, sp.nrhs, sp.launches_per_solve, h->pend_stream, rep);
   } catch (const PsError& e) {
     return fail(h, e.st, "ps_solve_report: " + e.msg);
   } catch (const std::bad_alloc&) {
@@ -4283,6 +4355,13 @@ void ps_free(ps_handle* h) {
   }
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
+  if (h->cs_in) {
+    cudaStreamSynchronize(h->cs_in);
+    cudaStreamSynchronize(h->cs_out);
+    cudaStreamDestroy(h->cs_in);
+    cudaStreamDestroy(h->cs_out);
+    for (auto e : h->hp_ev) cudaEventDestroy(e);
+  }
   cudaStream_t s = h->stream, u = h->ustream;
   if (u) cudaStreamSynchronize(u);
   delete h;

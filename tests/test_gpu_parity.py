@@ -271,6 +271,12 @@ def test_solve_c4_bench_config_sampled(cfgdata):
     assert err.max() <= TOL, err.max()
     assert np.allclose(rep["it0"][cols], ref.it0, rtol=1e-11)
     assert np.allclose(rep["it1"][cols], ref.it1, rtol=1e-10)
+    # the e2e path of the bench: host buffers, two pipelined 180-column halves
+    Xh = np.zeros_like(np.asfortranarray(B))
+    _, reph = h.solve(np.asfortranarray(B), Xh)
+    assert rel_l2_cols(Xh[:, cols], ref.x).max() <= TOL
+    assert np.allclose(reph["it0"], rep["it0"], rtol=1e-12) and np.allclose(reph["it1"], rep["it1"], rtol=1e-12)
+    assert reph["n_diverged"] == rep["n_diverged"]
 
 
 @pytest.mark.parametrize("nrhs", [8, 9, 63, 64, 65, 128, 129, 200])

@@ -92,3 +92,46 @@ def test_far1p_matches_oracle(cfgdata, tmp_path, env, nrhs, cfg):
     assert rel_l2_cols(x, ref.x).max() <= 1e-11
     assert np.allclose(it[0], ref.it0, rtol=1e-11)
     assert np.allclose(it[1], ref.it1, rtol=1e-10)
+
+
+# ps_solve on HOST buffers with many columns runs as two pipelined column halves on copy streams
+# (default from 256 columns). PS_HOST_PIPE_MIN=2 takes that path on C1: an odd
+# block (second half padded by one column), an even one, and pageable as well as pinned buffers.
+_HOST_SCRIPT = r"""
+import sys, warnings
+import numpy as np, torch
+sys.path.insert(0, {root!r})
+from paper_2109_04129_b200 import PsHandle
+from hmgen.synth import random_rhs
+warnings.simplefilter("ignore")
+h = PsHandle({path!r}); h.setup()
+B = np.asfortranarray(random_rhs(h.N, {nrhs}, 4))
+X = np.zeros_like(B)
+st, rep = h.solve(B, X)
+Bp = torch.from_numpy(np.ascontiguousarray(B.T)).pin_memory().T
+Xp = torch.empty_like(Bp.T).pin_memory().T
+for _ in range(2):
+    h.solve(Bp, Xp)
+assert np.array_equal(Xp.numpy(), X), "pinned and pageable host buffers differ"
+np.save({out!r}, X)
+np.save({out!r} + ".it.npy", np.stack([rep["it0"], rep["it1"]]))
+"""
+
+
+@pytest.mark.parametrize("nrhs", [2, 7, 70])
+def test_host_pipelined_halves_match_oracle(cfgdata, tmp_path, nrhs):
+    from hmgen.synth import random_rhs
+    from oracle import compute_scaling, read_hm, solve
+    from tests.conftest import rel_l2_cols
+    path = cfgdata("C1")["hm"]
+    out = str(tmp_path / "xh.npy")
+    e = dict(os.environ, PS_HOST_PIPE_MIN="2")
+    r = subprocess.run([sys.executable, "-c", _HOST_SCRIPT.format(root=ROOT, path=path, nrhs=nrhs, out=out)],
+                       env=e, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    x, it = np.load(out), np.load(out + ".it.npy")
+    H = read_hm(path)
+    ref = solve(H, compute_scaling(H), random_rhs(H.N, nrhs, 4))
+    assert x.shape == ref.x.shape and rel_l2_cols(x, ref.x).max() <= 1e-11
+    assert np.allclose(it[0], ref.it0, rtol=1e-11)
+    assert np.allclose(it[1], ref.it1, rtol=1e-10)
