@@ -498,7 +498,10 @@ def main():
         h.partitioned = True
     else:
         h = PsHandle(meta["hm"], device=local, rank=rank, nranks=world)
-    st = torch.cuda.current_stream()
+    # one non-default stream for everything timed: torch's ops, libps's launches (ps_solve /
+    # ps_solve_async take its handle) and the CUDA events that bracket them
+    st = torch.cuda.Stream()
+    torch.cuda.set_stream(st)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     h.setup()
