@@ -120,12 +120,12 @@ constexpr int GM_MAXSEG = 96;     // max segments per work item
 // one big block, cut into row chunks applied in order by ONE CTA (F1 chunks -> p1; F2 chunks
 // -> y2 rows and p2; F1 chunks again -> y1 rows), so no unit waits on another.
 #ifndef PS_F1P_CH                 // -DPS_F1P_CH / -DPS_F1P_NS: tiling A/B builds (scripts/f1p_variants.sh)
-#define PS_F1P_CH 1216
+#define PS_F1P_CH 2048
 #endif
 #ifndef PS_F1P_NS
-#define PS_F1P_NS 3
+#define PS_F1P_NS 2
 #endif
-constexpr int F1P_CH = PS_F1P_CH; // factor elements staged per item (19 KB; 3 stages + scratch: 2 CTAs / SM)
+constexpr int F1P_CH = PS_F1P_CH; // factor elements staged per item (32 KB; 2 stages + scratch: 2 CTAs / SM at 1 column, fits 227 KB at 8)
 constexpr int F1P_RMAX = 64;      // max rank (dense: shorter side) of a block on this path
 constexpr int F1P_XCH = 512;      // x rows x nrhs staged per item (complex elements)
 constexpr int F1P_PACK = 32;      // max blocks per pack item

@@ -1879,6 +1879,9 @@ __global__ void __launch_bounds__(F1P_THREADS, NR <= 2 ? 2 : 1) far1p_kernel(Far
 // one column: 2 CTAs per SM (the shared-memory ring of each plus its static tables and barriers)
 static_assert(2 * ((size_t)F1P_NS * F1P_STAGE_BYTES + sizeof(double2) * (F1P_CWARPS * 2 + 1) * F1P_RMAX +
                    2 * (F1P_GK + 33) + 64 + 1024) <= 228 * 1024, "far1p: two CTAs per SM at one column");
+// eight columns: one CTA per SM, two stages plus the 8-column scratch inside the 227 KB opt-in limit
+static_assert(2 * (size_t)F1P_STAGE_BYTES + sizeof(double2) * (F1P_CWARPS * 2 + 1) * F1P_RMAX * 8 +
+                  2 * (F1P_GK + 33) + 64 + 1024 <= 227 * 1024, "far1p: one CTA per SM at eight columns");
 template <int NR>
 static size_t far1p_smem() {
   return (size_t)(NR >= 8 ? 2 : F1P_NS) * F1P_STAGE_BYTES + sizeof(double2) * ((size_t)F1P_CWARPS * 2 + 1) * F1P_RMAX * NR;

@@ -19,7 +19,7 @@ timeout 300 python bench.py --config C1 --nrhs 1 --no-cpu-baseline > $O/bench_C1
 if [ -f data/C5.hm ]; then
   PS_VERBOSE=1 timeout 900 python bench.py --config C5 --steps 3 --no-cpu-baseline --no-next > $O/bench_C5.json 2> $O/bench_C5.err; echo "bench_C5=$?"
 fi
-for v in base 1824_2 2240_2 768_4; do   # far1p tiling A/B (scripts/f1p_variants.sh), C4 at 1 RHS
+for v in ${AB_VARIANTS:-base 1824_2 2240_2 768_4}; do   # far1p tiling A/B (scripts/f1p_variants.sh), C4 at 1 RHS
   L=ab_libs/libps_$v.so; [ $v = base ] && L=paper_2109_04129_b200/libps.so
   [ -f $L ] && PS_LIB=$L timeout 300 python bench.py --config C4 --nrhs 1 --no-cpu-baseline --no-next > $O/ab_f1p_$v.json 2> $O/ab_f1p_$v.err
 done
@@ -34,5 +34,5 @@ for NR in 360 1; do
   python scripts/ncu_summary.py /tmp/full_C4_$NR.ncu-rep --config C4 --nrhs $NR > $O/ncu_full_C4_${NR}.json 2>/dev/null
   ncu -i /tmp/full_C4_$NR.ncu-rep --page source --csv --print-source sass 2>/dev/null | gzip > $O/ncu_source_C4_${NR}.csv.gz
 done
-timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref_C4.json 2> $O/bench_ref_C4.err; echo "ref=$?"
+[ "${SKIP_REF:-0}" = 1 ] || { timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref_C4.json 2> $O/bench_ref_C4.err; echo "ref=$?"; }
 ls -la $O
